@@ -1,0 +1,296 @@
+// Seeded problem definitions shared by the B200 host and the CPU oracle.
+//
+// This header is input generation only: it evaluates the coefficient field b,
+// the volume source s and the impedance data t of a problem at given points.
+// It restates the reference's ProblemSpec callables
+// (proj/include/hps/problems.hpp:22-40, proj/src/problems.cpp:15-52) and adds
+// the seeded synthetic configurations of BASELINE.json (configs 0..4) with the
+// conventions pinned in SURVEY.md §8(d):
+//   * RNG = std::mt19937_64(seed) raw outputs, u = (x >> 11) * 2^-53;
+//     normals by explicit Box-Muller (never std::*_distribution, whose
+//     sequence is implementation-defined);
+//   * draw order: b-field parameters, then source parameters, then the
+//     plane-wave angle(s);
+//   * Gaussian bump g(x; a, c, w) = a * exp(-|x - c|^2 / w) (divisor form);
+//     per bump the draws are centre x, centre y, width, amplitude (only the
+//     ones that are random for that config);
+//   * Fourier field: per mode k = (kx, ky) uniform on {-8..8}^2 by rejection
+//     (k = 0 and |k| > 8 rejected), then amplitude ~ N(0, 0.1^2), then phase
+//     ~ U[0, 2pi); b = clip(sum_j a_j cos(2 pi k_j.x + phi_j), -0.6, 0.6);
+//   * plane-wave data t = i kappa (n.d + 1) e^{i kappa d.x}, d = (cos th, sin th)
+//     (problems.cpp:43-50), eta = kappa.
+#pragma once
+
+#include <cmath>
+#include <complex>
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+namespace hpsb {
+namespace problem {
+
+using cplx = std::complex<double>;
+
+struct Bump {
+  double cx = 0.5, cy = 0.5, w = 1.0, a = 0.0;
+  double operator()(double x, double y) const {
+    const double dx = x - cx, dy = y - cy;
+    return a * std::exp(-(dx * dx + dy * dy) / w);
+  }
+};
+
+struct FourierMode {
+  int kx = 0, ky = 0;
+  double a = 0.0, phi = 0.0;
+};
+
+enum class Kind : int {
+  kRefBump = 0,       // ProblemSpec::bump (problems.cpp:15-32)
+  kRefPlanewave = 1,  // ProblemSpec::planewave (problems.cpp:34-52)
+  kSeeded = 2,        // BASELINE.json configs 0..4
+};
+
+// Uniform double in [0, 1) from one raw mt19937_64 output.
+inline double uniform01(std::mt19937_64& rng) {
+  return static_cast<double>(rng() >> 11) * 0x1.0p-53;
+}
+
+// Standard normal by Box-Muller (cosine branch only, two uniforms per draw).
+inline double normal01(std::mt19937_64& rng) {
+  const double u1 = 1.0 - uniform01(rng);  // (0, 1]
+  const double u2 = uniform01(rng);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+}
+
+struct Spec {
+  Kind kind = Kind::kSeeded;
+  int config = 0;
+  std::uint64_t seed = 0;
+  int n = 4;       // elements per side
+  int order = 8;   // GLL degree N
+  double kappa = 10.0;
+  double eta = 10.0;
+  // b-field
+  std::vector<Bump> b_bumps;
+  std::vector<FourierMode> b_modes;
+  bool b_fourier = false;
+  // source
+  std::vector<Bump> s_bumps;
+  // plane-wave data (one per right-hand side)
+  std::vector<double> angles;
+  // Iterative-solver settings the config is quoted with.
+  int restart = 50;
+  double tol = 1e-10;
+  int nrhs = 1;
+
+  double b(double x, double y) const {
+    if (kind == Kind::kRefBump) {
+      const double dx = x - 0.5, dy = y - 0.5;
+      return 1.5 * std::exp(-160.0 * (dx * dx + dy * dy));
+    }
+    if (kind == Kind::kRefPlanewave) return 0.0;
+    if (b_fourier) {
+      double v = 0.0;
+      for (const auto& m : b_modes)
+        v += m.a * std::cos(2.0 * M_PI * (m.kx * x + m.ky * y) + m.phi);
+      return v < -0.6 ? -0.6 : (v > 0.6 ? 0.6 : v);
+    }
+    double v = 0.0;
+    for (const auto& g : b_bumps) v += g(x, y);
+    return v;
+  }
+
+  cplx source(double x, double y) const {
+    if (kind == Kind::kRefBump)
+      return -kappa * kappa * b(x, y) * std::exp(cplx(0.0, kappa * x));
+    if (kind == Kind::kRefPlanewave) return cplx(0.0, 0.0);
+    double v = 0.0;
+    for (const auto& g : s_bumps) v += g(x, y);
+    return cplx(v, 0.0);
+  }
+
+  // Incoming impedance data for outward normal (nx, ny), right-hand side r.
+  cplx boundary(double x, double y, double nx, double ny, int r = 0) const {
+    if (kind == Kind::kRefBump) return cplx(0.0, 0.0);
+    const double th = angles.at(r);
+    const double dx = std::cos(th), dy = std::sin(th);
+    const cplx u = std::exp(cplx(0.0, kappa * (x * dx + y * dy)));
+    return cplx(0.0, kappa) * (nx * dx + ny * dy + 1.0) * u;
+  }
+
+  // Manufactured solution (plane-wave problem only).
+  cplx exact(double x, double y) const {
+    const double th = angles.at(0);
+    return std::exp(cplx(0.0, kappa * (x * std::cos(th) + y * std::sin(th))));
+  }
+  bool has_exact() const { return kind == Kind::kRefPlanewave; }
+};
+
+inline Spec reference_bump(int n, int order, double kappa) {
+  Spec s;
+  s.kind = Kind::kRefBump;
+  s.n = n, s.order = order, s.kappa = kappa, s.eta = kappa;
+  s.angles = {0.0};
+  return s;
+}
+
+inline Spec reference_planewave(int n, int order, double kappa, double angle = 0.0) {
+  Spec s;
+  s.kind = Kind::kRefPlanewave;
+  s.n = n, s.order = order, s.kappa = kappa, s.eta = kappa;
+  s.angles = {angle};
+  return s;
+}
+
+namespace detail {
+inline Bump random_bump(std::mt19937_64& rng, double lo, double hi, double wlo,
+                        double whi, double alo, double ahi) {
+  Bump g;
+  g.cx = lo + (hi - lo) * uniform01(rng);
+  g.cy = lo + (hi - lo) * uniform01(rng);
+  g.w = (wlo == whi) ? wlo : wlo + (whi - wlo) * uniform01(rng);
+  g.a = (alo == ahi) ? alo : alo + (ahi - alo) * uniform01(rng);
+  return g;
+}
+
+inline std::vector<FourierMode> fourier_modes(std::mt19937_64& rng, int count) {
+  std::vector<FourierMode> modes;
+  while (static_cast<int>(modes.size()) < count) {
+    const int kx = static_cast<int>(uniform01(rng) * 17.0) - 8;
+    const int ky = static_cast<int>(uniform01(rng) * 17.0) - 8;
+    if ((kx == 0 && ky == 0) || kx * kx + ky * ky > 64) continue;
+    FourierMode m;
+    m.kx = kx, m.ky = ky;
+    m.a = 0.1 * normal01(rng);
+    m.phi = 2.0 * M_PI * uniform01(rng);
+    modes.push_back(m);
+  }
+  return modes;
+}
+}  // namespace detail
+
+// BASELINE.json configs[0..4] with the seed (default: the config index).
+// `n_override` / `order_override` > 0 shrink the mesh for parity tests while
+// keeping the config's fields.
+inline Spec baseline_config(int config, std::uint64_t seed, int n_override = 0,
+                            int order_override = 0) {
+  static const int kN[5] = {4, 16, 64, 128, 256};
+  static const int kOrder[5] = {8, 16, 16, 20, 12};
+  static const double kKappa[5] = {10.0, 40.0, 160.0, 400.0, 600.0};
+  static const int kRestart[5] = {50, 50, 100, 100, 60};
+  static const double kTol[5] = {1e-10, 1e-10, 1e-10, 1e-10, 1e-8};
+  if (config < 0 || config > 4)
+    throw std::invalid_argument("baseline_config: config must be 0..4");
+  Spec s;
+  s.kind = Kind::kSeeded;
+  s.config = config;
+  s.seed = seed;
+  s.n = n_override > 0 ? n_override : kN[config];
+  s.order = order_override > 0 ? order_override : kOrder[config];
+  s.kappa = s.eta = kKappa[config];
+  s.restart = kRestart[config];
+  s.tol = kTol[config];
+  std::mt19937_64 rng(seed);
+  using detail::random_bump;
+  // 1. b-field
+  switch (config) {
+    case 0: {
+      Bump g;
+      g.cx = 0.5, g.cy = 0.5, g.w = 0.02, g.a = 0.5;
+      s.b_bumps = {g};
+      break;
+    }
+    case 1:
+    case 2: {
+      const int count = config == 1 ? 4 : 16;
+      for (int j = 0; j < count; ++j)
+        s.b_bumps.push_back(random_bump(rng, 0.1, 0.9, 0.02, 0.08, -0.5, 0.5));
+      break;
+    }
+    default:
+      s.b_fourier = true;
+      s.b_modes = detail::fourier_modes(rng, 64);
+  }
+  // 2. source
+  if (config <= 1) {
+    s.s_bumps = {random_bump(rng, 0.2, 0.8, 0.05, 0.05, 1.0, 1.0)};
+  } else if (config <= 3) {
+    for (int j = 0; j < 4; ++j)
+      s.s_bumps.push_back(random_bump(rng, 0.2, 0.8, 0.02, 0.02, 1.0, 1.0));
+  }
+  // 3. plane-wave angle(s)
+  s.nrhs = config == 4 ? 32 : 1;
+  for (int r = 0; r < s.nrhs; ++r) s.angles.push_back(2.0 * M_PI * uniform01(rng));
+  return s;
+}
+
+// Samples of one problem on the element grid, in the layouts the
+// element/skeleton entry points consume (mesh.cpp:53-103, mesh.cpp:111-139):
+//   coeff[e][(N+1)^2]   c = kappa^2 (1 - b) at every tensor node (real)
+//   source[e][(N-1)^2]  s at the interior nodes, i-major (complex, unweighted)
+//   tside[r][e][4][N-1] t on each side of e (left/right/bottom/top, ascending
+//                       along the side); zero on interior sides.
+struct Samples {
+  int n = 0, order = 0, nrhs = 1;
+  std::vector<double> coeff;
+  std::vector<cplx> source;
+  std::vector<cplx> tside;
+  bool source_is_zero = true;
+};
+
+inline Samples sample(const Spec& spec, const double* nodes) {
+  Samples out;
+  const int n = spec.n, N = spec.order, np = N + 1, m = N - 1;
+  out.n = n, out.order = N, out.nrhs = static_cast<int>(spec.angles.size());
+  const double h = 1.0 / n;
+  const double k2 = spec.kappa * spec.kappa;
+  const std::size_t ne = static_cast<std::size_t>(n) * n;
+  out.coeff.resize(ne * np * np);
+  out.source.resize(ne * m * m);
+  out.tside.assign(static_cast<std::size_t>(out.nrhs) * ne * 4 * m, cplx(0.0, 0.0));
+  for (std::size_t e = 0; e < ne; ++e) {
+    const double ox = h * static_cast<double>(e % n);
+    const double oy = h * static_cast<double>(e / n);
+    for (int i = 0; i < np; ++i) {
+      const double x = ox + 0.5 * (nodes[i] + 1.0) * h;
+      for (int j = 0; j < np; ++j) {
+        const double y = oy + 0.5 * (nodes[j] + 1.0) * h;
+        out.coeff[e * np * np + i * np + j] = k2 * (1.0 - spec.b(x, y));
+      }
+    }
+    for (int i = 1; i < N; ++i) {
+      const double x = ox + 0.5 * (nodes[i] + 1.0) * h;
+      for (int j = 1; j < N; ++j) {
+        const double y = oy + 0.5 * (nodes[j] + 1.0) * h;
+        const cplx sv = spec.source(x, y);
+        if (sv != cplx(0.0, 0.0)) out.source_is_zero = false;
+        out.source[e * m * m + (i - 1) * m + (j - 1)] = sv;
+      }
+    }
+    const int ex = static_cast<int>(e % n), ey = static_cast<int>(e / n);
+    for (int side = 0; side < 4; ++side) {
+      const bool physical = (side == 0 && ex == 0) || (side == 1 && ex == n - 1) ||
+                            (side == 2 && ey == 0) || (side == 3 && ey == n - 1);
+      if (!physical) continue;
+      for (int r = 0; r < out.nrhs; ++r)
+        for (int k = 0; k < m; ++k) {
+          const double along = 0.5 * (nodes[k + 1] + 1.0) * h;
+          double x = 0, y = 0, nx = 0, ny = 0;
+          switch (side) {
+            case 0: x = ox, y = oy + along, nx = -1.0; break;
+            case 1: x = ox + h, y = oy + along, nx = 1.0; break;
+            case 2: x = ox + along, y = oy, ny = -1.0; break;
+            default: x = ox + along, y = oy + h, ny = 1.0; break;
+          }
+          out.tside[((static_cast<std::size_t>(r) * ne + e) * 4 + side) * m + k] =
+              spec.boundary(x, y, nx, ny, r);
+        }
+    }
+  }
+  return out;
+}
+
+}  // namespace problem
+}  // namespace hpsb
