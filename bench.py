@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""Benchmark of the HPS-multigrid hot path (BASELINE.json metric).
+
+A step is one pass of the hot path over one synthetic BASELINE config:
+element ItI build -> skeleton assembly -> level merges -> MG preconditioner
+-> preconditioned FGMRES solve.  Headline `value` = preconditioned-GMRES
+DOF-iterations/s (skeleton DOF x FGMRES iterations / device solve time, inputs
+resident in HBM); `setup` = HPS setup elements/s (n^2 / device setup time).
+`e2e` = the same GMRES metric through the public C ABI with host buffers
+(pinned rhs H2D + solve + x D2H inside the timed region).
+
+  python bench.py [--config 1] [--steps K] [--warmup W] [--gpus N] [--impl b200|reference]
+
+Multi-GPU (torchrun): every rank runs an independent replica of the config
+(no data-path collective yet; subtree sharding is the next step),
+value = all ranks' DOF-iterations / max-over-ranks time, scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_DMMA_PEAK_TFLOPS = 37.1  # measured on this pool's B200 (profiles/r01_fp64_peak_probe.log)
+METRIC = "precond GMRES DOF-iterations/s"
+UNIT = "DOF-iterations/s"
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- CPU side
+def oracle_run(config: int, seed: int, threads: int) -> dict:
+    """Reference algorithm (CPU oracle restatement) on the full config."""
+    import numpy as np  # noqa: F401
+    from oracle import pyoracle
+    smp = pyoracle.sample(2, config=config, seed=seed)
+    kappa = [10.0, 40.0, 160.0, 400.0, 600.0][config]
+    restart = [50, 50, 100, 100, 60][config]
+    tol = [1e-10, 1e-10, 1e-10, 1e-10, 1e-8][config]
+    t0 = time.perf_counter()
+    S = pyoracle.Session.from_sample(smp, kappa, threads=threads)
+    S.build_hierarchy(0, False)
+    depth = 2 * (smp["n"].bit_length() - 1)
+    S.precond(depth=depth, gamma=1, coarse_iters=4)
+    t_setup = time.perf_counter() - t0
+    _, rep = S.solve(S.rhs(), True, restart=restart, tol=tol, record_history=False)
+    ne = smp["n"] ** 2
+    return {"setup_s": t_setup, "solve_s": rep["seconds"], "iterations": rep["iterations"],
+            "dim": S.dim, "elements": ne,
+            "gmres_dof_its": S.dim * rep["iterations"] / rep["seconds"],
+            "setup_eps": ne / t_setup}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        oracle_run(args.config, args.seed, threads)
+    runs = [oracle_run(args.config, args.seed, threads) for _ in range(args.steps)]
+    dof_its = sum(r["dim"] * r["iterations"] for r in runs)
+    solve_s = sum(r["solve_s"] for r in runs)
+    setup_s = sum(r["setup_s"] for r in runs)
+    value = dof_its / solve_s
+    sample = (f"full config {args.config} pipeline per step (oracle restatement of the reference "
+              f"algorithm; reference C++ needs Eigen, absent on this image)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * (solve_s + setup_s) / len(runs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"cfg{args.config}", "seed": args.seed},
+        "setup": {"metric": "HPS setup elements/s",
+                  "value": sum(r["elements"] for r in runs) / setup_s},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side
+def run_b200(args, rank, world, local):
+    import numpy as np
+    import torch
+    import paper_2511_00735_b200 as hps
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prob = hps.problem(2, args.config, seed=args.seed)
+    ctx = hps.Context(local)
+    ne = prob.n ** 2
+    coeff_d = torch.from_numpy(np.ascontiguousarray(prob.coeff)).cuda(local)
+    src_d = torch.from_numpy(np.ascontiguousarray(prob.source).view(np.float64)).cuda(local)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+    restart, tol = prob.restart, prob.tol
+    state = {}
+
+    def step(profile: bool = False):
+        import ctypes
+        ctx.timer_start()
+        h = ctypes.c_void_p()
+        hps._check(hps._lib.hpsb_elements_build_dev(
+            ctx._h, prob.n, prob.order, prob.eta, ctypes.c_void_p(coeff_d.data_ptr()),
+            None if prob.source_zero else ctypes.c_void_p(src_d.data_ptr()), ctypes.byref(h)))
+        el = hps.ElementRecords(ctx, h, prob.n, prob.order, prob.eta)
+        sk = hps.assemble_skeleton(el, prob)
+        hier = hps.build_hierarchy(sk)
+        pc = hps.build_preconditioner(hier, coarse_iters=4)
+        t_setup = ctx.timer_stop()
+        x = torch.empty(2 * sk.dim, dtype=torch.float64, device=f"cuda:{local}")
+        rep = hps.SolveReport()
+        cfg = hps.KrylovConfig(restart, tol, 2000, 0, 1)
+        hps._check(hps._lib.hpsb_fgmres_dev(sk._h, pc._h, ctypes.c_void_p(sk.rhs_dev_ptr(0)),
+                                            ctypes.c_void_p(x.data_ptr()), cfg,
+                                            ctypes.byref(rep)), allow=(hps.OK,))
+        state.update(dim=sk.dim, pc_bytes=pc.bytes_per_apply, depth=hier.depth)
+        return t_setup, rep.seconds, rep.iterations, sk.dim
+
+    def flush_l2():
+        flush.zero_()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+        flush_l2()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    setup_s = solve_s = 0.0
+    dof_its = 0
+    its = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            ts, tv, it, dim = step()
+            setup_s += ts
+            solve_s += tv
+            dof_its += dim * it
+            its.append(it)
+            flush_l2()
+    torch.cuda.synchronize()
+    launches = ctx.launches - launches0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([setup_s, solve_s, dof_its, ne * args.steps], dtype=torch.float64,
+                         device=f"cuda:{local}")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        setup_max, solve_max = mx[0].item(), mx[1].item()
+        dof_total, elem_total = sm[2].item(), sm[3].item()
+    else:
+        setup_max, solve_max, dof_total, elem_total = setup_s, solve_s, dof_its, ne * args.steps
+    value = dof_total / solve_max
+    setup_value = elem_total / setup_max
+
+    # ---- per-kernel roofline from one profiled (untimed) step
+    ctx.profile_reset()
+    ctx.profile(True)
+    step()
+    ctx.profile(False)
+    prof = ctx.profile_entries()
+    peaks = measured_peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    name, d = dom
+    if d["flops"] > 0 and d["bytes"] == 0 or name in ("element_iti", "zgemm_dmma"):
+        achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12
+        roof = {"kernel": name, "bound": "tensor", "achieved": achieved,
+                "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+                "peak_source": "measured FP64 DMMA burst (profiles/r01_fp64_peak_probe.log)"}
+    else:
+        achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    roof["launches"] = d["launches"]
+    kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
+                   "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
+                   "TFLOPs": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)}
+               for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
+
+    # ---- e2e through the public ABI with host buffers (rhs H2D, x D2H)
+    el_h = hps.build_elements(ctx, prob)
+    sk_h = hps.assemble_skeleton(el_h, prob)
+    hier_h = hps.build_hierarchy(sk_h)
+    pc_h = hps.build_preconditioner(hier_h, coarse_iters=4)
+    rhs_host = torch.from_numpy(sk_h.rhs()).pin_memory().numpy()
+    e2e_dof, e2e_t = 0, 0.0
+    for _ in range(max(1, min(args.steps, 3))):
+        t0 = time.perf_counter()
+        x, rep = hps.fgmres(sk_h, rhs_host, pc_h, restart=restart, tol=tol)
+        e2e_t += time.perf_counter() - t0
+        e2e_dof += sk_h.dim * rep["iterations"]
+    e2e_value = e2e_dof / e2e_t
+    # e2e setup: host coefficient arrays -> preconditioner ready
+    t0 = time.perf_counter()
+    el2 = hps.build_elements(ctx, prob)
+    sk2 = hps.assemble_skeleton(el2, prob)
+    hier2 = hps.build_hierarchy(sk2)
+    hps.build_preconditioner(hier2, coarse_iters=4)
+    e2e_setup = ne / (time.perf_counter() - t0)
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * (setup_max + solve_max) / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic",
+        "config": {"workload": f"cfg{args.config}", "n": prob.n, "N": prob.order,
+                   "kappa": prob.kappa, "dof": state["dim"], "elements": ne,
+                   "levels": state["depth"], "restart": restart, "tol": tol, "seed": args.seed,
+                   "mg": "depth=L, gamma=1, coarse_iters=4", "l2": "flushed between steps (256 MB)",
+                   "parallelism": f"replicas x{world}"},
+        "iterations": its,
+        "setup": {"metric": "HPS setup elements/s", "value": setup_value,
+                  "ms_per_step": 1e3 * setup_max / args.steps},
+        "solve_ms_per_step": 1e3 * solve_max / args.steps,
+        "precond_bytes_per_apply": state["pc_bytes"],
+        "roofline": roof,
+        "kernels": kernels,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": 16 * sk_h.dim, "d2h_bytes_per_step": 16 * sk_h.dim,
+                "setup_elements_per_s": e2e_setup},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cb = oracle_run(args.config if args.config <= 1 else 1, args.seed, 1)
+        line["cpu_baseline"] = {
+            "value": cb["gmres_dof_its"], "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"full cfg{min(args.config, 1)} pipeline, oracle restatement, 1 thread",
+            "setup_elements_per_s": cb["setup_eps"]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.seed is None:
+        args.seed = args.config
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_b200(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

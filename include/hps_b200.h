@@ -1,0 +1,199 @@
+/* hps_b200 — B200-native HPS-multigrid hot path (arXiv 2511.00735), C ABI.
+ *
+ * Drop-in boundary for the reference hps2d C++ entry points on the hot path
+ * (paths relative to the reference root):
+ *   local ItI build   ElementOperators(rule, h, eta, coeff)  proj/include/hps/element.hpp:63-64
+ *                     source_to_outgoing                     proj/include/hps/element.hpp:82
+ *                     build_elements(mesh, rule)             proj/include/hps/mesh.hpp:44
+ *   skeleton          assemble_skeleton                      proj/include/hps/skeleton.hpp:74-75
+ *                     BlockMatrix::apply (interface matvec)  proj/include/hps/block_matrix.hpp:39
+ *   merge             merge_pair                             proj/include/hps/dissection.hpp:30-31
+ *                     eliminate_level / build_hierarchy      proj/include/hps/dissection.hpp:64-72
+ *   preconditioner    build_preconditioner / apply           proj/include/hps/multigrid.hpp:34-50
+ *   GMRES             gmres / fgmres / gmres_fixed_steps      proj/include/hps/krylov.hpp:39-51
+ *
+ * Conventions (the reference's):
+ *   - complex values are interleaved (re, im) doubles (std::complex<double>);
+ *   - matrices are column-major (Eigen default);
+ *   - element id = ey * n + ex; tensor node (i, j) -> i * (N + 1) + j;
+ *   - element boundary order left | right | bottom | top, ascending along a side;
+ *   - skeleton vector = face blocks in elimination order, each 2 (N - 1) wide,
+ *     slot 0 = data incoming to e2, slot 1 = data incoming to e1.
+ * Errors never cross the ABI as exceptions: every call returns an
+ * hpsb_status, and hpsb_last_error() holds a thread-local message
+ * (proj/src/capi.cpp:13-24, proj/include/hps/hps.h:24-30,96-97).
+ * Pointers are HOST pointers unless the function name ends in _dev.
+ * Objects are immutable after build and owned by the library behind opaque
+ * handles with create/destroy pairs; calls on one context are serialised on
+ * that context's CUDA stream.  There is no CPU fallback: without a usable
+ * sm_100 device every compute call returns HPSB_INTERNAL.
+ */
+#ifndef HPS_B200_H
+#define HPS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hpsb_status {
+  HPSB_OK = 0,
+  HPSB_INVALID_ARGUMENT = 1,
+  HPSB_NO_CONVERGENCE = 2,
+  HPSB_IO = 3,
+  HPSB_INTERNAL = 4
+} hpsb_status;
+
+typedef struct hpsb_context_s* hpsb_context;
+typedef struct hpsb_elements_s* hpsb_elements;
+typedef struct hpsb_skeleton_s* hpsb_skeleton;
+typedef struct hpsb_hierarchy_s* hpsb_hierarchy;
+typedef struct hpsb_precond_s* hpsb_precond;
+
+/* MgConfig (proj/include/hps/multigrid.hpp:12-18). */
+typedef struct hpsb_mg_config {
+  int depth;        /* number of hierarchy levels used (>= 2) */
+  int gamma;        /* coarse calls per intermediate level (1 = V-cycle) */
+  int coarse_iters; /* unpreconditioned GMRES steps at the deepest level */
+  int exact_coarse; /* reserved: dense coarse solve (not on the B200 path yet) */
+} hpsb_mg_config;
+
+/* KrylovConfig (proj/include/hps/krylov.hpp:15-21). */
+typedef struct hpsb_krylov_config {
+  int restart;
+  double tol;
+  int max_iters;
+  int record_history;
+  int reorthogonalize; /* the B200 path always runs two Gram-Schmidt passes */
+} hpsb_krylov_config;
+
+/* SolveReport (proj/include/hps/krylov.hpp:23-34), device-timed. */
+typedef struct hpsb_solve_report {
+  int iterations;
+  int converged;
+  double final_residual;
+  double seconds;           /* CUDA-event time of the solve */
+  double precond_seconds;   /* part of `seconds` spent in preconditioner applies */
+  double matvec_seconds;    /* part of `seconds` spent in skeleton matvecs */
+} hpsb_solve_report;
+
+/* ---------------------------------------------------------------- library */
+const char* hpsb_last_error(void);
+const char* hpsb_version(void);
+
+/* Context on one CUDA device (one stream). */
+hpsb_status hpsb_context_create(int device, hpsb_context* out);
+hpsb_status hpsb_context_destroy(hpsb_context ctx);
+hpsb_status hpsb_context_synchronize(hpsb_context ctx);
+
+/* ------------------------------------------------------ host-side structure
+ * Integer structure, bit-exact with the reference (no device needed).       */
+/* GLL rule (proj/src/spectral.cpp:26-87): nodes[N+1], weights[N+1], diff[(N+1)^2]. */
+hpsb_status hpsb_gll_rule(int order, double* nodes, double* weights, double* diff);
+/* IndexSets (proj/src/element.cpp:22-55): left|right|bottom|top|interior|noncorner|comp_of_full. */
+hpsb_status hpsb_index_sets(int order, int* out);
+/* FaceGraph (proj/src/skeleton.cpp:20-78): faces[6F] (e1,e2,s1,s2,level,group),
+ * level_range[2L], face_of_element[4 n^2]. */
+hpsb_status hpsb_face_graph(int n, int* faces, int* level_range, int* face_of_element);
+
+/* Seeded BASELINE.json problem samples (shared conventions).
+ * kind: 0 reference bump, 1 reference plane wave, 2 BASELINE config `config`.
+ * n / order override the config's mesh when > 0.  coeff[n^2][(N+1)^2] real,
+ * source[n^2][(N-1)^2] complex, tside[nrhs][n^2][4][N-1] complex.          */
+hpsb_status hpsb_problem_dims(int kind, int config, int n, int order, int* n_out, int* order_out,
+                              int* nrhs_out, double* kappa_out, int* restart_out, double* tol_out);
+hpsb_status hpsb_problem_sample(int kind, int config, uint64_t seed, int n, int order, double kappa,
+                                double* coeff, double* source, double* tside, int* source_zero);
+
+/* ----------------------------------------------------------- element stage
+ * Batched local ItI build: ElementOperators + source_to_outgoing for all n^2
+ * elements (proj/src/element.cpp:127-174, proj/src/mesh.cpp:36-109).
+ * coeff = c = kappa^2 (1 - b) at every tensor node (real, as mesh.cpp:62),
+ * source = s at the interior nodes (unweighted; the kernel applies the
+ * tensor quadrature weights as mesh.cpp:89-103), or NULL for s = 0.         */
+hpsb_status hpsb_elements_build(hpsb_context ctx, int n, int order, double eta,
+                                const double* coeff, const double* source, hpsb_elements* out);
+hpsb_status hpsb_elements_build_dev(hpsb_context ctx, int n, int order, double eta,
+                                    const double* coeff_dev, const double* source_dev,
+                                    hpsb_elements* out);
+hpsb_status hpsb_elements_destroy(hpsb_elements el);
+/* T[e] (4(N-1))^2 complex col-major and H[e] 4(N-1) complex, for e in [e0, e0+count). */
+hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, double* H);
+
+/* ------------------------------------------------------------ skeleton
+ * assemble_skeleton (proj/src/skeleton.cpp:88-137): the interface operator
+ * M = I + sum_e scatter(T_e) and rhs = -H - sum_phys T t.  tside as from
+ * hpsb_problem_sample (nrhs right-hand sides).                              */
+hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs,
+                                 hpsb_skeleton* out);
+hpsb_status hpsb_skeleton_destroy(hpsb_skeleton sk);
+int64_t hpsb_skeleton_dim(hpsb_skeleton sk);
+hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs);
+/* y = M x (BlockMatrix::apply, proj/src/block_matrix.cpp:23-31). */
+hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y);
+hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x_dev, double* y_dev);
+
+/* ----------------------------------------------------------- merges
+ * build_hierarchy(system, depth, factor_coarse) (proj/src/dissection.cpp:200-227):
+ * level-by-level Schur elimination of the merge tree, batched per level.
+ * depth = 0 means all levels.  factor_coarse is accepted for API parity.    */
+hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
+                                 hpsb_hierarchy* out);
+hpsb_status hpsb_hierarchy_destroy(hpsb_hierarchy h);
+hpsb_status hpsb_hierarchy_info(hpsb_hierarchy h, int* depth, int* total_levels,
+                                int64_t* device_bytes, double* build_seconds);
+/* Export level l's system M_l in the reference's bs x bs block layout
+ * (HierarchyLevel::M, proj/include/hps/dissection.hpp:35-41).  First call
+ * with keys == NULL to get the number of structurally non-zero blocks.     */
+hpsb_status hpsb_hierarchy_level_blocks(hpsb_hierarchy h, int level, int* nblocks, int* first_face,
+                                        int* keys, double* data);
+/* Two-element merge (merge_pair, proj/src/dissection.cpp:23-82). */
+hpsb_status hpsb_merge_pair(hpsb_context ctx, int side_len, const double* T1, const double* H1,
+                            const double* T2, const double* H2, int alpha, int beta, double* T,
+                            double* H);
+
+/* ---------------------------------------------------- preconditioner / GMRES */
+hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_precond* out);
+hpsb_status hpsb_precond_destroy(hpsb_precond p);
+/* z = MG(v) (MgPreconditioner::apply, proj/src/multigrid.cpp:30-100). */
+hpsb_status hpsb_precond_apply(hpsb_precond p, const double* v, double* z);
+hpsb_status hpsb_precond_apply_dev(hpsb_precond p, const double* v_dev, double* z_dev);
+
+/* Restarted (F)GMRES on the skeleton system (proj/src/krylov.cpp:45-178).
+ * precond == NULL runs unpreconditioned GMRES.  Returns HPSB_NO_CONVERGENCE
+ * (report still filled, x still written) when the tolerance is not met.     */
+hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                        hpsb_krylov_config cfg, hpsb_solve_report* report);
+hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs_dev,
+                            double* x_dev, hpsb_krylov_config cfg, hpsb_solve_report* report);
+
+/* Device pointer of the skeleton's right-hand side r (for _dev solves). */
+const double* hpsb_skeleton_rhs_dev(hpsb_skeleton sk, int r);
+
+/* Number of library kernels launched on this context so far (bench evidence). */
+int64_t hpsb_context_launches(hpsb_context ctx);
+
+/* Device timer on the context stream (CUDA events): start, then stop returns
+ * the elapsed seconds between the two event records.                       */
+hpsb_status hpsb_context_timer_start(hpsb_context ctx);
+hpsb_status hpsb_context_timer_stop(hpsb_context ctx, double* seconds);
+
+/* Per-kernel CUDA-event profiling.  enable != 0 brackets every launch with
+ * events (adds overhead: use outside timed regions); entries aggregate by
+ * kernel name: launches, total ms, algorithmic bytes and flops.            */
+hpsb_status hpsb_context_profile(hpsb_context ctx, int enable);
+int hpsb_context_profile_count(hpsb_context ctx);
+hpsb_status hpsb_context_profile_entry(hpsb_context ctx, int i, char* name, int name_len,
+                                       int64_t* launches, double* ms, double* bytes,
+                                       double* flops);
+hpsb_status hpsb_context_profile_reset(hpsb_context ctx);
+
+/* Algorithmic operator bytes one preconditioner apply streams (roofline). */
+int64_t hpsb_precond_bytes(hpsb_precond p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPS_B200_H */

@@ -1,0 +1,477 @@
+// C ABI of the hps_b200 library (include/hps_b200.h).  Mirrors the
+// reference C API's conventions: statuses instead of exceptions, a
+// thread-local last-error string, create/destroy ownership
+// (proj/src/capi.cpp:13-24,109-137).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/hps_b200.h"
+#include "internal.hpp"
+#include "problem.hpp"
+
+struct hpsb_context_s {
+  hpsb::Context c;
+};
+struct hpsb_elements_s {
+  std::unique_ptr<hpsb::Elements> e;
+};
+struct hpsb_skeleton_s {
+  std::unique_ptr<hpsb::Skeleton> s;
+};
+struct hpsb_hierarchy_s {
+  std::unique_ptr<hpsb::Hierarchy> h;
+};
+struct hpsb_precond_s {
+  hpsb::Precond* p = nullptr;
+  ~hpsb_precond_s() { hpsb::destroy_precond(p); }
+};
+
+namespace hpsb {
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                           cudaGetErrorString(e) + ") at " + file + ":" + std::to_string(line) +
+                           ": " + what);
+}
+}  // namespace hpsb
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+hpsb_status guarded(F&& f) {
+  try {
+    return f();
+  } catch (const hpsb::InvalidArgument& e) {
+    g_last_error = e.what();
+    return HPSB_INVALID_ARGUMENT;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return HPSB_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HPSB_INTERNAL;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return HPSB_INTERNAL;
+  }
+}
+
+#define REQUIRE(cond, msg) \
+  do {                     \
+    if (!(cond)) throw hpsb::InvalidArgument(msg); \
+  } while (0)
+
+hpsb::problem::Spec make_spec(int kind, int config, uint64_t seed, int n, int order, double kappa) {
+  if (kind == 0) return hpsb::problem::reference_bump(n, order, kappa);
+  if (kind == 1) return hpsb::problem::reference_planewave(n, order, kappa);
+  if (kind == 2) return hpsb::problem::baseline_config(config, seed, n, order);
+  throw hpsb::InvalidArgument("problem kind must be 0, 1 or 2");
+}
+}  // namespace
+
+extern "C" {
+
+const char* hpsb_last_error(void) { return g_last_error.c_str(); }
+const char* hpsb_version(void) { return "hps_b200 0.1.0 (sm_100a)"; }
+
+hpsb_status hpsb_context_create(int device, hpsb_context* out) {
+  return guarded([&] {
+    REQUIRE(out, "context_create: null output");
+    int count = 0;
+    HPSB_CUDA(cudaGetDeviceCount(&count));
+    REQUIRE(device >= 0 && device < count, "context_create: no such CUDA device");
+    cudaDeviceProp prop{};
+    HPSB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw std::runtime_error("context_create: hps_b200 needs an sm_100 (B200) device");
+    auto ctx = std::make_unique<hpsb_context_s>();
+    ctx->c.device = device;
+    HPSB_CUDA(cudaSetDevice(device));
+    ctx->c.num_sms = prop.multiProcessorCount;
+    HPSB_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->c.ev) HPSB_CUDA(cudaEventCreate(&e));
+    *out = ctx.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_destroy(hpsb_context ctx) {
+  return guarded([&] {
+    if (!ctx) return HPSB_OK;
+    cudaStreamSynchronize(ctx->c.stream);
+    for (auto& e : ctx->c.ev) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_synchronize(hpsb_context ctx) {
+  return guarded([&] {
+    HPSB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    return HPSB_OK;
+  });
+}
+
+int64_t hpsb_context_launches(hpsb_context ctx) { return ctx ? ctx->c.launches : -1; }
+
+hpsb_status hpsb_context_timer_start(hpsb_context ctx) {
+  return guarded([&] {
+    REQUIRE(ctx, "timer: null context");
+    for (auto& e : ctx->c.timer)
+      if (!e) HPSB_CUDA(cudaEventCreate(&e));
+    HPSB_CUDA(cudaEventRecord(ctx->c.timer[0], ctx->c.stream));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_timer_stop(hpsb_context ctx, double* seconds) {
+  return guarded([&] {
+    REQUIRE(ctx && seconds && ctx->c.timer[0], "timer: not started");
+    HPSB_CUDA(cudaEventRecord(ctx->c.timer[1], ctx->c.stream));
+    HPSB_CUDA(cudaEventSynchronize(ctx->c.timer[1]));
+    float ms = 0;
+    HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->c.timer[0], ctx->c.timer[1]));
+    *seconds = ms * 1e-3;
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_profile(hpsb_context ctx, int enable) {
+  return guarded([&] {
+    REQUIRE(ctx, "profile: null context");
+    ctx->c.collect();
+    ctx->c.profile = enable != 0;
+    return HPSB_OK;
+  });
+}
+
+int hpsb_context_profile_count(hpsb_context ctx) {
+  if (!ctx) return -1;
+  try {
+    ctx->c.collect();
+  } catch (...) {
+    return -1;
+  }
+  return static_cast<int>(ctx->c.agg.size());
+}
+
+hpsb_status hpsb_context_profile_entry(hpsb_context ctx, int i, char* name, int name_len,
+                                       int64_t* launches, double* ms, double* bytes,
+                                       double* flops) {
+  return guarded([&] {
+    REQUIRE(ctx, "profile: null context");
+    ctx->c.collect();
+    REQUIRE(i >= 0 && i < static_cast<int>(ctx->c.agg.size()), "profile: index out of range");
+    const auto& kv = ctx->c.agg[i];
+    if (name && name_len > 0) {
+      std::strncpy(name, kv.first.c_str(), name_len - 1);
+      name[name_len - 1] = 0;
+    }
+    if (launches) *launches = kv.second.launches;
+    if (ms) *ms = kv.second.ms;
+    if (bytes) *bytes = kv.second.bytes;
+    if (flops) *flops = kv.second.flops;
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_profile_reset(hpsb_context ctx) {
+  return guarded([&] {
+    REQUIRE(ctx, "profile: null context");
+    ctx->c.collect();
+    ctx->c.agg.clear();
+    return HPSB_OK;
+  });
+}
+
+int64_t hpsb_precond_bytes(hpsb_precond p) { return p ? hpsb::precond_bytes(p->p) : -1; }
+
+hpsb_status hpsb_gll_rule(int order, double* nodes, double* weights, double* diff) {
+  return guarded([&] {
+    const hpsb::Gll g = hpsb::gll_rule(order);
+    std::memcpy(nodes, g.nodes.data(), g.nodes.size() * sizeof(double));
+    std::memcpy(weights, g.weights.data(), g.weights.size() * sizeof(double));
+    std::memcpy(diff, g.diff.data(), g.diff.size() * sizeof(double));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_index_sets(int order, int* out) {
+  return guarded([&] {
+    const hpsb::IndexSets s = hpsb::build_index_sets(order);
+    int* p = out;
+    for (const auto* v : {&s.left, &s.right, &s.bottom, &s.top, &s.interior, &s.noncorner,
+                          &s.comp_of_full}) {
+      std::memcpy(p, v->data(), v->size() * sizeof(int));
+      p += v->size();
+    }
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_face_graph(int n, int* faces, int* level_range, int* face_of_element) {
+  return guarded([&] {
+    const hpsb::FaceGraph g = hpsb::build_face_graph(n);
+    for (int f = 0; f < g.num_faces(); ++f) {
+      const auto& x = g.faces[f];
+      const int row[6] = {x.e1, x.e2, x.s1, x.s2, x.level, x.group};
+      std::memcpy(faces + 6 * f, row, sizeof(row));
+    }
+    for (int l = 0; l < g.num_levels(); ++l) {
+      level_range[2 * l] = g.level_range[l].first;
+      level_range[2 * l + 1] = g.level_range[l].second;
+    }
+    for (int e = 0; e < n * n; ++e)
+      for (int s = 0; s < 4; ++s) face_of_element[4 * e + s] = g.face_of_element[e][s];
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_problem_dims(int kind, int config, int n, int order, int* n_out, int* order_out,
+                              int* nrhs_out, double* kappa_out, int* restart_out,
+                              double* tol_out) {
+  return guarded([&] {
+    const auto spec = make_spec(kind, config, 0, n, order, 1.0);
+    *n_out = spec.n, *order_out = spec.order, *nrhs_out = static_cast<int>(spec.angles.size());
+    if (kappa_out) *kappa_out = spec.kappa;
+    if (restart_out) *restart_out = spec.restart;
+    if (tol_out) *tol_out = spec.tol;
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_problem_sample(int kind, int config, uint64_t seed, int n, int order, double kappa,
+                                double* coeff, double* source, double* tside, int* source_zero) {
+  return guarded([&] {
+    const auto spec = make_spec(kind, config, seed, n, order, kappa);
+    const hpsb::Gll g = hpsb::gll_rule(spec.order);
+    const auto s = hpsb::problem::sample(spec, g.nodes.data());
+    std::memcpy(coeff, s.coeff.data(), s.coeff.size() * sizeof(double));
+    std::memcpy(source, s.source.data(), s.source.size() * 2 * sizeof(double));
+    std::memcpy(tside, s.tside.data(), s.tside.size() * 2 * sizeof(double));
+    if (source_zero) *source_zero = s.source_is_zero ? 1 : 0;
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_elements_build_dev(hpsb_context ctx, int n, int order, double eta,
+                                    const double* coeff_dev, const double* source_dev,
+                                    hpsb_elements* out) {
+  return guarded([&] {
+    REQUIRE(ctx && out && coeff_dev, "elements_build: null argument");
+    auto h = std::make_unique<hpsb_elements_s>();
+    h->e = hpsb::build_elements(&ctx->c, n, order, eta, coeff_dev,
+                                reinterpret_cast<const double2*>(source_dev));
+    *out = h.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_elements_build(hpsb_context ctx, int n, int order, double eta, const double* coeff,
+                                const double* source, hpsb_elements* out) {
+  return guarded([&] {
+    REQUIRE(ctx && out && coeff, "elements_build: null argument");
+    REQUIRE(n >= 2 && order >= 2, "elements_build: bad mesh");
+    const size_t ne = static_cast<size_t>(n) * n, np = order + 1, m = order - 1;
+    hpsb::DevBuf<double> c(ne * np * np);
+    hpsb::DevBuf<double2> s(source ? ne * m * m : 0);
+    HPSB_CUDA(cudaMemcpyAsync(c.p, coeff, c.bytes(), cudaMemcpyHostToDevice, ctx->c.stream));
+    if (source)
+      HPSB_CUDA(cudaMemcpyAsync(s.p, source, s.bytes(), cudaMemcpyHostToDevice, ctx->c.stream));
+    auto h = std::make_unique<hpsb_elements_s>();
+    h->e = hpsb::build_elements(&ctx->c, n, order, eta, c.p, source ? s.p : nullptr);
+    *out = h.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_elements_destroy(hpsb_elements el) {
+  delete el;
+  return HPSB_OK;
+}
+
+hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, double* H) {
+  return guarded([&] {
+    const auto& E = *el->e;
+    const int ne = E.n * E.n;
+    REQUIRE(e0 >= 0 && count >= 0 && e0 + count <= ne, "elements_get: range out of bounds");
+    const size_t nb = E.nb;
+    if (T)
+      HPSB_CUDA(cudaMemcpy(T, E.T.p + e0 * nb * nb, count * nb * nb * sizeof(double2),
+                           cudaMemcpyDeviceToHost));
+    if (H)
+      HPSB_CUDA(cudaMemcpy(H, E.H.p + e0 * nb, count * nb * sizeof(double2), cudaMemcpyDeviceToHost));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs,
+                                 hpsb_skeleton* out) {
+  return guarded([&] {
+    REQUIRE(el && out && tside && nrhs >= 1, "skeleton_create: bad argument");
+    auto h = std::make_unique<hpsb_skeleton_s>();
+    h->s = hpsb::build_skeleton(el->e.get(), reinterpret_cast<const double2*>(tside), nrhs);
+    *out = h.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_skeleton_destroy(hpsb_skeleton sk) {
+  delete sk;
+  return HPSB_OK;
+}
+
+int64_t hpsb_skeleton_dim(hpsb_skeleton sk) { return sk ? sk->s->dim : -1; }
+
+const double* hpsb_skeleton_rhs_dev(hpsb_skeleton sk, int r) {
+  if (!sk || r < 0 || r >= sk->s->nrhs) return nullptr;
+  return reinterpret_cast<const double*>(sk->s->rhs.p + static_cast<size_t>(r) * sk->s->dim);
+}
+
+hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs) {
+  return guarded([&] {
+    REQUIRE(sk && rhs && r >= 0 && r < sk->s->nrhs, "skeleton_rhs: bad argument");
+    HPSB_CUDA(cudaMemcpy(rhs, sk->s->rhs.p + static_cast<size_t>(r) * sk->s->dim,
+                         sk->s->dim * sizeof(double2), cudaMemcpyDeviceToHost));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x, double* y) {
+  return guarded([&] {
+    REQUIRE(sk && x && y, "skeleton_apply: null argument");
+    hpsb::skeleton_apply(sk->s.get(), reinterpret_cast<const double2*>(x),
+                         reinterpret_cast<double2*>(y));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y) {
+  return guarded([&] {
+    REQUIRE(sk && x && y, "skeleton_apply: null argument");
+    auto* S = sk->s.get();
+    cudaStream_t st = S->ctx->stream;
+    HPSB_CUDA(cudaMemcpyAsync(S->x_buf.p, x, S->dim * sizeof(double2), cudaMemcpyHostToDevice, st));
+    hpsb::skeleton_apply(S, S->x_buf.p, S->y_buf.p);
+    HPSB_CUDA(cudaMemcpyAsync(y, S->y_buf.p, S->dim * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
+                                 hpsb_hierarchy* out) {
+  (void)factor_coarse;
+  return guarded([&] {
+    REQUIRE(sk && out, "hierarchy_build: null argument");
+    auto h = std::make_unique<hpsb_hierarchy_s>();
+    h->h = hpsb::build_hierarchy(sk->s.get(), depth);
+    *out = h.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_hierarchy_destroy(hpsb_hierarchy h) {
+  delete h;
+  return HPSB_OK;
+}
+
+hpsb_status hpsb_hierarchy_info(hpsb_hierarchy h, int* depth, int* total_levels,
+                                int64_t* device_bytes, double* build_seconds) {
+  return guarded([&] {
+    REQUIRE(h, "hierarchy_info: null handle");
+    if (depth) *depth = h->h->depth;
+    if (total_levels) *total_levels = h->h->total_levels;
+    if (device_bytes) *device_bytes = h->h->device_bytes;
+    if (build_seconds) *build_seconds = h->h->build_seconds;
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_hierarchy_level_blocks(hpsb_hierarchy h, int level, int* nblocks, int* first_face,
+                                        int* keys, double* data) {
+  return guarded([&] {
+    REQUIRE(h && nblocks && first_face, "hierarchy_level_blocks: null argument");
+    hpsb::hierarchy_level_blocks(h->h.get(), level, nblocks, first_face, keys, data);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_merge_pair(hpsb_context ctx, int side_len, const double* T1, const double* H1,
+                            const double* T2, const double* H2, int alpha, int beta, double* T,
+                            double* H) {
+  return guarded([&] {
+    REQUIRE(ctx && T1 && H1 && T2 && H2 && T && H, "merge_pair: null argument");
+    REQUIRE(side_len >= 1 && alpha >= 0 && alpha < 4 && beta >= 0 && beta < 4,
+            "merge_pair: bad sides");
+    hpsb::merge_pair(&ctx->c, side_len, reinterpret_cast<const double2*>(T1),
+                     reinterpret_cast<const double2*>(H1), reinterpret_cast<const double2*>(T2),
+                     reinterpret_cast<const double2*>(H2), alpha, beta,
+                     reinterpret_cast<double2*>(T), reinterpret_cast<double2*>(H));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_precond* out) {
+  return guarded([&] {
+    REQUIRE(h && out, "precond_create: null argument");
+    auto p = std::make_unique<hpsb_precond_s>();
+    p->p = hpsb::create_precond(h->h.get(), cfg);
+    *out = p.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_precond_destroy(hpsb_precond p) {
+  delete p;
+  return HPSB_OK;
+}
+
+hpsb_status hpsb_precond_apply_dev(hpsb_precond p, const double* v, double* z) {
+  return guarded([&] {
+    REQUIRE(p && v && z, "precond_apply: null argument");
+    hpsb::precond_apply(p->p, reinterpret_cast<const double2*>(v), reinterpret_cast<double2*>(z));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_precond_apply(hpsb_precond p, const double* v, double* z) {
+  return guarded([&] {
+    REQUIRE(p && v && z, "precond_apply: null argument");
+    hpsb::precond_apply_host(p->p, reinterpret_cast<const double2*>(v),
+                             reinterpret_cast<double2*>(z));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                            hpsb_krylov_config cfg, hpsb_solve_report* report) {
+  return guarded([&] {
+    REQUIRE(sk && rhs && x && report, "fgmres: null argument");
+    return hpsb::fgmres(sk->s.get(), precond ? precond->p : nullptr,
+                        reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x), cfg,
+                        report);
+  });
+}
+
+hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                        hpsb_krylov_config cfg, hpsb_solve_report* report) {
+  return guarded([&] {
+    REQUIRE(sk && rhs && x && report, "fgmres: null argument");
+    auto* S = sk->s.get();
+    cudaStream_t st = S->ctx->stream;
+    hpsb::DevBuf<double2> b(S->dim), xd(S->dim);
+    HPSB_CUDA(cudaMemcpyAsync(b.p, rhs, b.bytes(), cudaMemcpyHostToDevice, st));
+    const hpsb_status rc =
+        hpsb::fgmres(S, precond ? precond->p : nullptr, b.p, xd.p, cfg, report);
+    HPSB_CUDA(cudaMemcpyAsync(x, xd.p, xd.bytes(), cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    return rc;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// Device helpers: complex<double> arithmetic on double2 (re, im), the
+// reference's interleaved std::complex<double> layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace hpsb {
+
+__host__ __device__ __forceinline__ double2 cmake(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+// acc += a * b
+__host__ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  return acc;
+}
+// conj(a) * b accumulated
+__host__ __device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, double2 acc) {
+  acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+  return acc;
+}
+__host__ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+__device__ __forceinline__ double2 cinv(double2 a) {
+  // 1 / a with scaling against overflow (|a| spans many decades in pivots).
+  const double s = fmax(fabs(a.x), fabs(a.y));
+  const double ar = a.x / s, ai = a.y / s;
+  const double d = ar * ar + ai * ai;
+  return make_double2(ar / (d * s), -ai / (d * s));
+}
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cmul(a, cinv(b)); }
+
+__device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
+
+// Block-wide sum of a double (blockDim.x multiple of 32, <= 1024).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace hpsb

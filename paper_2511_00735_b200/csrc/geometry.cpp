@@ -1,0 +1,155 @@
+// Host-side integer structure of the HPS discretisation: GLL rule, element
+// index sets and the quadtree merge order of the interior faces.  These are
+// tiny 1-D / integer computations done once per problem; they must be
+// bit-identical to the reference, so they follow its exact sequences.
+#include <cmath>
+#include <cstring>
+
+#include "internal.hpp"
+
+namespace hpsb {
+
+// GLL nodes, weights and barycentric differentiation matrix
+// (proj/src/spectral.cpp:26-87).  The floating-point sequence (Newton from
+// Chebyshev-Lobatto guesses, symmetrisation, pinned endpoints, normalised
+// barycentric weights, negative-sum diagonal) is kept so that the nodes are
+// bit-identical to the reference's.
+Gll gll_rule(int order) {
+  if (order < 1) throw InvalidArgument("gll_rule: order must be >= 1");
+  const int np = order + 1;
+  auto legendre = [order](double x, double& p_prev, double& p) {
+    p_prev = 1.0;
+    p = x;
+    for (int k = 1; k < order; ++k) {
+      const double next = ((2.0 * k + 1.0) * x * p - k * p_prev) / (k + 1.0);
+      p_prev = p;
+      p = next;
+    }
+  };
+  Gll g;
+  g.nodes.resize(np);
+  g.weights.resize(np);
+  for (int i = 0; i < np; ++i) {
+    double x = -std::cos(M_PI * i / order);
+    for (int it = 0; it < 100; ++it) {
+      double a, b;
+      legendre(x, a, b);
+      const double step = (x * b - a) / (np * b);
+      x -= step;
+      if (std::abs(step) <= 1e-15) break;
+    }
+    g.nodes[i] = x;
+  }
+  for (int i = 0; i <= order / 2; ++i) {
+    const double half = 0.5 * (g.nodes[i] - g.nodes[order - i]);
+    g.nodes[i] = half;
+    g.nodes[order - i] = -half;
+  }
+  g.nodes.front() = -1.0;
+  g.nodes.back() = 1.0;
+  if (order % 2 == 0) g.nodes[order / 2] = 0.0;
+  for (int i = 0; i < np; ++i) {
+    double a, b;
+    legendre(g.nodes[i], a, b);
+    g.weights[i] = 2.0 / (order * np * b * b);
+  }
+  std::vector<double> bw(np);
+  double scale = 0.0;
+  for (int i = 0; i < np; ++i) {
+    double prod = 1.0;
+    for (int j = 0; j < np; ++j)
+      if (j != i) prod *= g.nodes[i] - g.nodes[j];
+    bw[i] = 1.0 / prod;
+    scale = std::max(scale, std::abs(bw[i]));
+  }
+  for (double& w : bw) w /= scale;
+  g.diff.assign(static_cast<std::size_t>(np) * np, 0.0);
+  for (int i = 0; i < np; ++i) {
+    double acc = 0.0;
+    for (int j = 0; j < np; ++j) {
+      if (j == i) continue;
+      const double d = (bw[j] / bw[i]) / (g.nodes[i] - g.nodes[j]);
+      g.diff[i + static_cast<std::size_t>(j) * np] = d;
+      acc += d;
+    }
+    g.diff[i + static_cast<std::size_t>(i) * np] = -acc;
+  }
+  return g;
+}
+
+// Corner-free index bookkeeping (proj/src/element.cpp:22-55): node (i, j)
+// -> i (N+1) + j, sides ascending along the side, interior i-major.
+IndexSets build_index_sets(int order) {
+  if (order < 2) throw InvalidArgument("build_index_sets: order must be >= 2");
+  const int np = order + 1;
+  IndexSets s;
+  s.order = order;
+  for (int t = 1; t < order; ++t) {
+    s.left.push_back(t);
+    s.right.push_back(order * np + t);
+    s.bottom.push_back(t * np);
+    s.top.push_back(t * np + order);
+  }
+  for (auto* side : {&s.left, &s.right, &s.bottom, &s.top})
+    s.boundary.insert(s.boundary.end(), side->begin(), side->end());
+  for (int i = 1; i < order; ++i)
+    for (int j = 1; j < order; ++j) s.interior.push_back(i * np + j);
+  s.comp_of_full.assign(np * np, -1);
+  for (int idx = 0, k = 0; idx < np * np; ++idx) {
+    const int i = idx / np, j = idx % np;
+    if ((i == 0 || i == order) && (j == 0 || j == order)) continue;
+    s.noncorner.push_back(idx);
+    s.comp_of_full[idx] = k++;
+  }
+  return s;
+}
+
+// Merge order of the interior faces (proj/src/skeleton.cpp:20-78): level
+// 2k+1 joins 2^k x 2^k squares left-right (groups row-major), level 2k+2
+// joins 2^{k+1} x 2^k boxes bottom-top (groups column-major).
+FaceGraph build_face_graph(int n) {
+  if (n < 2 || (n & (n - 1)) != 0)
+    throw InvalidArgument("build_face_graph: n must be a power of two >= 2");
+  int lg = 0;
+  while ((1 << lg) < n) ++lg;
+  FaceGraph g;
+  g.n = n;
+  g.face_of_element.assign(static_cast<std::size_t>(n) * n, {-1, -1, -1, -1});
+  g.groups.resize(2 * lg);
+  for (int level = 1; level <= 2 * lg; ++level) {
+    const int first = g.num_faces();
+    auto& lvl_groups = g.groups[level - 1];
+    const bool across_x = (level & 1) == 1;
+    const int k = across_x ? (level - 1) / 2 : level / 2;
+    const int boxes_x = across_x ? (n >> (k + 1)) : (n >> k);
+    const int boxes_y = n >> k;
+    lvl_groups.resize(static_cast<std::size_t>(boxes_x) * boxes_y);
+    const int faces_per_group = across_x ? (1 << k) : (1 << k);
+    for (int gi = 0; gi < boxes_x * boxes_y; ++gi) {
+      // x-merges enumerate groups row-major, y-merges column-major.
+      const int a = across_x ? gi / boxes_x : gi % boxes_y;  // row index
+      const int b = across_x ? gi % boxes_x : gi / boxes_y;  // column index
+      for (int t = 0; t < faces_per_group; ++t) {
+        int e1, e2, s1, s2;
+        if (across_x) {
+          const int line = (2 * b + 1) << k;  // vertical grid line
+          const int row = (a << k) + t;
+          e1 = row * n + line - 1, e2 = e1 + 1, s1 = 1, s2 = 0;
+        } else {
+          const int line = (2 * a + 1) << (k - 1);  // horizontal grid line
+          const int col = (b << k) + t;
+          e1 = (line - 1) * n + col, e2 = e1 + n, s1 = 3, s2 = 2;
+        }
+        const int id = g.num_faces();
+        g.faces.push_back({e1, e2, s1, s2, level, gi});
+        g.face_of_element[e1][s1] = id;
+        g.face_of_element[e2][s2] = id;
+        lvl_groups[gi].push_back(id);
+      }
+    }
+    g.level_range.emplace_back(first, g.num_faces());
+  }
+  return g;
+}
+
+}  // namespace hpsb

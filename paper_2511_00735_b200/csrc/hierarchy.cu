@@ -1,0 +1,401 @@
+// K2 merges: level-by-level Schur elimination of the quadtree merge order.
+//
+// The reference eliminates level l of the block-sparse system M_l
+// (eliminate_level, proj/src/dissection.cpp:153-198) with per-group LUs and
+// std::map block updates, M_{l+1} = D - C A^{-1} B.  The level systems are
+// exactly box ItI maps scattered into the skeleton:
+//     M_l = I + sum_{boxes b of level l} P_b T_b Q_b^T,
+// so the B200 path keeps one dense ItI map per box and performs each group
+// elimination as a two-box merge (the generalisation of merge_pair,
+// dissection.cpp:23-82, to boxes).  For a merge of box 1 (holding the faces'
+// e1) and box 2 across separator s, with u_k the incoming data on box k's
+// remaining perimeter p_k:
+//     x1 = W [T2_ss T1_sp u1 - T2_sp u2],  W = (I - T2_ss T1_ss)^{-1}
+//     x2 = -T1_ss x1 - T1_sp u1
+//     T_new = [[T1_pp, 0], [0, T2_pp]] + [[T1_ps X1], [T2_ps X2]]
+// which is D + C A^{-1} B of the reference restricted to the structurally
+// non-zero blocks.  Every merge of a level runs in the same few grouped
+// launches: one gather (children permuted to [p | s] order), one copy batch,
+// four grouped DMMA GEMMs and one batched inverse.
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+
+#include "device.cuh"
+#include "hierarchy.hpp"
+#include "zgemm.hpp"
+
+namespace hpsb {
+
+Hierarchy::~Hierarchy() = default;
+
+namespace {
+struct HostBox {
+  std::vector<BoxPos> pos;
+  const double2* T = nullptr;
+  int ld = 0;
+};
+}  // namespace
+
+std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
+  Context* ctx = sk->ctx;
+  const FaceGraph& g = sk->graph;
+  const int total = g.num_levels();
+  if (depth == 0) depth = total;
+  if (depth < 1 || depth > total) throw InvalidArgument("build_hierarchy: depth out of range");
+  auto h = std::make_unique<Hierarchy>();
+  h->ctx = ctx, h->sk = sk, h->depth = depth, h->total_levels = total;
+  const Elements* el = sk->el;
+  const int ne = el->n * el->n, nb = el->nb, m = sk->m, bs = sk->bs;
+
+  // Level-1 boxes are the elements (all 4(N-1) positions, physical ones -1).
+  std::vector<HostBox> boxes(ne);
+  std::vector<int> elem_box(ne);
+  for (int e = 0; e < ne; ++e) {
+    boxes[e].pos.resize(nb);
+    for (int b = 0; b < nb; ++b)
+      boxes[e].pos[b] = {sk->h_in[static_cast<size_t>(e) * nb + b],
+                         sk->h_out[static_cast<size_t>(e) * nb + b]};
+    boxes[e].T = el->T.p + static_cast<size_t>(e) * nb * nb;
+    boxes[e].ld = nb;
+    elem_box[e] = e;
+  }
+  std::vector<int> pos_of(sk->dim, -1);
+  DevBuf<double2> tnew_prev;  // previous level's merged maps (children of this level)
+  DevBuf<int> d_status(1);
+  HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(int), ctx->stream));
+
+  HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  for (int level = 1; level <= depth; ++level) {
+    auto L = std::make_unique<LevelOps>();
+    L->level = level;
+    L->first_face = g.level_range[level - 1].first;
+    L->nfaces = g.num_faces() - L->first_face;
+    L->coarse = (level == depth);
+    const auto& groups = g.groups[level - 1];
+    const int ng = static_cast<int>(groups.size());
+
+    // ---- children in [perimeter | separator] order
+    std::vector<std::vector<int>> perms;  // per child, positions into its HostBox
+    std::vector<const HostBox*> srcs;
+    size_t toff = 0;
+    L->merges.resize(ng);
+    for (int gi = 0; gi < ng; ++gi) {
+      const Face& f0 = g.faces[groups[gi][0]];
+      const HostBox* bx[2] = {&boxes[elem_box[f0.e1]], &boxes[elem_box[f0.e2]]};
+      for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
+          if (bx[k]->pos[i].in >= 0) pos_of[bx[k]->pos[i].in] = i;
+      const int s = static_cast<int>(groups[gi].size()) * m;
+      std::vector<int> sep[2];
+      std::vector<char> is_sep[2];
+      for (int k = 0; k < 2; ++k) is_sep[k].assign(bx[k]->pos.size(), 0);
+      for (int f : groups[gi]) {
+        if (g.faces[f].e1 == -1) throw std::logic_error("bad face");
+        for (int t = 0; t < m; ++t) {
+          // box 1 holds e1: its incoming datum is slot 1; box 2's is slot 0.
+          const int in1 = f * bs + m + t, in2 = f * bs + t;
+          const int q1 = pos_of[in1], q2 = pos_of[in2];
+          if (q1 < 0 || q2 < 0 || bx[0]->pos[q1].in != in1 || bx[1]->pos[q2].in != in2)
+            throw std::logic_error("build_hierarchy: separator node not on the merging boxes");
+          sep[0].push_back(q1), sep[1].push_back(q2);
+          is_sep[0][q1] = 1, is_sep[1][q2] = 1;
+        }
+      }
+      MergeRec& mr = L->merges[gi];
+      mr.s = s;
+      for (int k = 0; k < 2; ++k) {
+        ChildBox cb;
+        std::vector<int> perm;
+        for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
+          if (bx[k]->pos[i].in >= 0 && !is_sep[k][i]) perm.push_back(i);
+        cb.p = static_cast<int>(perm.size());
+        perm.insert(perm.end(), sep[k].begin(), sep[k].end());
+        cb.s = s;
+        cb.P = static_cast<int>(perm.size());
+        for (int i : perm) cb.pos.push_back(bx[k]->pos[i]);
+        cb.t_off = toff;
+        toff += static_cast<size_t>(cb.P) * cb.P;
+        (k == 0 ? mr.c1 : mr.c2) = static_cast<int>(L->children.size());
+        (k == 0 ? mr.p1 : mr.p2) = cb.p;
+        L->children.push_back(std::move(cb));
+        perms.push_back(std::move(perm));
+        srcs.push_back(bx[k]);
+      }
+      for (int k = 0; k < 2; ++k)
+        for (const auto& p : bx[k]->pos)
+          if (p.in >= 0) pos_of[p.in] = -1;
+    }
+    L->tperm.alloc(toff);
+
+    // ---- gather children into the permuted layout
+    {
+      std::vector<int> hperm;
+      std::vector<size_t> poff;
+      for (const auto& p : perms) {
+        poff.push_back(hperm.size());
+        hperm.insert(hperm.end(), p.begin(), p.end());
+      }
+      DevBuf<int> dperm;
+      dperm.upload(hperm, ctx->stream);
+      CopyBatch cb;
+      for (size_t c = 0; c < perms.size(); ++c) {
+        const ChildBox& ch = L->children[c];
+        cb.gather(srcs[c]->T, srcs[c]->ld, dperm.p + poff[c], dperm.p + poff[c],
+                  L->tperm.p + ch.t_off, ch.P, ch.P, ch.P);
+      }
+      cb.run(ctx);
+      HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    tnew_prev.release();
+
+    // ---- V-cycle / export index lists
+    for (auto& mr : L->merges) {
+      const ChildBox& a = L->children[mr.c1];
+      const ChildBox& b = L->children[mr.c2];
+      auto push = [&](const ChildBox& c, int from, int to, bool in) {
+        const size_t off = L->h_idx.size();
+        for (int i = from; i < to; ++i) L->h_idx.push_back(in ? c.pos[i].in : c.pos[i].out);
+        return off;
+      };
+      mr.in1_sep = push(a, a.p, a.P, true);
+      mr.in2_sep = push(b, b.p, b.P, true);
+      mr.in1_per = push(a, 0, a.p, true);
+      mr.out1_per = push(a, 0, a.p, false);
+      mr.in2_per = push(b, 0, b.p, true);
+      mr.out2_per = push(b, 0, b.p, false);
+    }
+
+    if (!L->coarse) {
+      // ---- merges
+      size_t woff = 0, roff = 0, noff = 0;
+      std::vector<size_t> r_at(ng), n_at(ng);
+      for (int gi = 0; gi < ng; ++gi) {
+        MergeRec& mr = L->merges[gi];
+        const int q = mr.p1 + mr.p2;
+        mr.w_off = woff;
+        woff += static_cast<size_t>(mr.s) * mr.s;
+        r_at[gi] = roff;
+        roff += static_cast<size_t>(mr.s) * q;
+        n_at[gi] = noff;
+        noff += static_cast<size_t>(q) * q;
+      }
+      L->w.alloc(woff);
+      DevBuf<double2> R(roff), X1(roff), X2(roff), tnew(noff);
+      CopyBatch pre;
+      GemmBatch g1, g2, g3, g4;
+      InverseBatch inv;
+      for (int gi = 0; gi < ng; ++gi) {
+        const MergeRec& mr = L->merges[gi];
+        const ChildBox& c1 = L->children[mr.c1];
+        const ChildBox& c2 = L->children[mr.c2];
+        const int s = mr.s, p1 = mr.p1, p2 = mr.p2, q = p1 + p2, P1 = c1.P, P2 = c2.P;
+        const double2* T1 = L->tperm.p + c1.t_off;
+        const double2* T2 = L->tperm.p + c2.t_off;
+        const double2 *T1pp = T1, *T1ps = T1 + static_cast<size_t>(p1) * P1, *T1sp = T1 + p1,
+                      *T1ss = T1 + p1 + static_cast<size_t>(p1) * P1;
+        const double2 *T2pp = T2, *T2ps = T2 + static_cast<size_t>(p2) * P2, *T2sp = T2 + p2,
+                      *T2ss = T2 + p2 + static_cast<size_t>(p2) * P2;
+        double2* W = L->w.p + mr.w_off;
+        double2* Rg = R.p + r_at[gi];
+        double2* X1g = X1.p + r_at[gi];
+        double2* X2g = X2.p + r_at[gi];
+        double2* Tn = tnew.p + n_at[gi];
+        pre.identity(W, s, s);
+        pre.copy(T2sp, P2, Rg + static_cast<size_t>(p1) * s, s, s, p2, -1.0);
+        pre.copy(T1sp, P1, X2g, s, s, p1, -1.0);
+        pre.zero(X2g + static_cast<size_t>(p1) * s, s, s, p2);
+        pre.copy(T1pp, P1, Tn, q, p1, p1, 1.0);
+        pre.zero(Tn + static_cast<size_t>(p1) * q, q, p1, p2);
+        pre.zero(Tn + p1, q, p2, p1);
+        pre.copy(T2pp, P2, Tn + p1 + static_cast<size_t>(p1) * q, q, p2, p2, 1.0);
+        g1.add(T2ss, P2, T1ss, P1, W, s, s, s, s, -1.0, 1.0);
+        g1.add(T2ss, P2, T1sp, P1, Rg, s, s, p1, s, 1.0, 0.0);
+        inv.ops.push_back(InvOp{W, s, s, gi, 0});
+        g2.add(W, s, Rg, s, X1g, s, s, q, s, 1.0, 0.0);
+        g3.add(T1ss, P1, X1g, s, X2g, s, s, q, s, -1.0, 1.0);
+        g3.add(T1ps, P1, X1g, s, Tn, q, p1, q, s, 1.0, 1.0);
+        g4.add(T2ps, P2, X2g, s, Tn + p1, q, p2, q, s, 1.0, 1.0);
+      }
+      pre.run(ctx);
+      g1.run(ctx);
+      inv.run(ctx, d_status.p);
+      g2.run(ctx);
+      g3.run(ctx);
+      g4.run(ctx);
+      L->merge_flops = g1.flops + g2.flops + g3.flops + g4.flops;
+      for (const auto& mr : L->merges) L->merge_flops += 8.0 * mr.s * mr.s * mr.s;  // inverse
+      int st = 0;
+      HPSB_CUDA(cudaMemcpyAsync(&st, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (st) {
+        const int gi = st - 1;
+        throw std::runtime_error("eliminate_level: singular merge block at face " +
+                                 std::to_string(g.groups[level - 1][gi].front()));
+      }
+      // ---- next level's boxes
+      std::vector<HostBox> next(ng);
+      for (int gi = 0; gi < ng; ++gi) {
+        const MergeRec& mr = L->merges[gi];
+        const ChildBox& c1 = L->children[mr.c1];
+        const ChildBox& c2 = L->children[mr.c2];
+        HostBox& nbx = next[gi];
+        nbx.pos.assign(c1.pos.begin(), c1.pos.begin() + c1.p);
+        nbx.pos.insert(nbx.pos.end(), c2.pos.begin(), c2.pos.begin() + c2.p);
+        nbx.T = tnew.p + n_at[gi];
+        nbx.ld = mr.p1 + mr.p2;
+      }
+      // element -> new box: the merge owning the element's old box
+      std::vector<int> box_to_group(boxes.size(), -1);
+      for (int gi = 0; gi < ng; ++gi) {
+        const Face& f0 = g.faces[groups[gi][0]];
+        box_to_group[elem_box[f0.e1]] = gi;
+        box_to_group[elem_box[f0.e2]] = gi;
+      }
+      for (int e = 0; e < ne; ++e) elem_box[e] = box_to_group[elem_box[e]];
+      boxes = std::move(next);
+      tnew_prev = std::move(tnew);
+    }
+    L->idx.upload(L->h_idx, ctx->stream);
+    h->device_bytes += static_cast<int64_t>(L->tperm.bytes() + L->w.bytes() + L->idx.bytes());
+    h->levels.push_back(std::move(L));
+  }
+  HPSB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+  h->build_seconds = ms * 1e-3;
+  return h;
+}
+
+// M_l in the reference's bs x bs block layout (for parity tests / export).
+void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,
+                            int* keys, double* data) {
+  if (level < 1 || level > h->depth) throw InvalidArgument("level out of range");
+  const LevelOps& L = *h->levels[level - 1];
+  const int bs = h->sk->bs, ff = L.first_face;
+  std::unordered_map<int64_t, std::vector<double2>> blocks;
+  auto key_of = [&](int r, int c) { return static_cast<int64_t>(r) * L.nfaces + c; };
+  auto blk = [&](int r, int c) -> std::vector<double2>& {
+    auto& b = blocks[key_of(r, c)];
+    if (b.empty()) b.assign(static_cast<size_t>(bs) * bs, make_double2(0.0, 0.0));
+    return b;
+  };
+  for (int f = 0; f < L.nfaces; ++f) {
+    auto& b = blk(f, f);
+    for (int k = 0; k < bs; ++k) b[k + k * bs].x += 1.0;
+  }
+  std::vector<double2> T;
+  for (const ChildBox& c : L.children) {
+    T.resize(static_cast<size_t>(c.P) * c.P);
+    HPSB_CUDA(cudaMemcpy(T.data(), L.tperm.p + c.t_off, T.size() * sizeof(double2),
+                         cudaMemcpyDeviceToHost));
+    for (int j = 0; j < c.P; ++j)
+      for (int i = 0; i < c.P; ++i) {
+        const int row = c.pos[i].out, col = c.pos[j].in;
+        auto& b = blk(row / bs - ff, col / bs - ff);
+        double2& v = b[(row % bs) + static_cast<size_t>(col % bs) * bs];
+        const double2 t = T[i + static_cast<size_t>(j) * c.P];
+        v.x += t.x, v.y += t.y;
+      }
+  }
+  *first_face = ff;
+  if (!keys) {
+    *nblocks = static_cast<int>(blocks.size());
+    return;
+  }
+  std::vector<int64_t> order;
+  for (const auto& kv : blocks) order.push_back(kv.first);
+  std::sort(order.begin(), order.end());
+  int k = 0;
+  for (int64_t key : order) {
+    keys[2 * k] = static_cast<int>(key / L.nfaces);
+    keys[2 * k + 1] = static_cast<int>(key % L.nfaces);
+    std::memcpy(data + 2 * static_cast<size_t>(k) * bs * bs, blocks[key].data(),
+                sizeof(double2) * bs * bs);
+    ++k;
+  }
+  *nblocks = k;
+}
+
+}  // namespace hpsb
+
+namespace hpsb {
+
+// merge_pair (proj/src/dissection.cpp:23-82): the same box merge on two
+// elements, fused layout [e1 sides minus alpha | e2 sides minus beta] in
+// left/right/bottom/top order, plus the source term
+//   H_pair = [H1_p + T1_ps x1; H2_p + T2_ps x2],
+//   x1 = W (T2_ss H1_s - H2_s),  x2 = -H1_s - T1_ss x1.
+void merge_pair(Context* ctx, int m, const double2* T1h, const double2* H1h, const double2* T2h,
+                const double2* H2h, int alpha, int beta, double2* Th, double2* Hh) {
+  const int nb = 4 * m, s = m, p = 3 * m, q = 6 * m;
+  std::vector<int> perm;
+  for (int k = 0; k < 2; ++k) {
+    const int skip = k == 0 ? alpha : beta;
+    for (int side = 0; side < 4; ++side)
+      if (side != skip)
+        for (int t = 0; t < m; ++t) perm.push_back(side * m + t);
+    for (int t = 0; t < m; ++t) perm.push_back(skip * m + t);
+  }
+  DevBuf<int> dperm;
+  dperm.upload(perm, ctx->stream);
+  DevBuf<double2> T1(nb * nb), T2(nb * nb), H1(nb), H2(nb), P1(nb * nb), P2(nb * nb), h1(nb),
+      h2(nb), W(s * s), R(s * q), X1(s * q), X2(s * q), Tn(q * q), u(s), x1(s), x2(s), Hn(q);
+  HPSB_CUDA(cudaMemcpyAsync(T1.p, T1h, T1.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  HPSB_CUDA(cudaMemcpyAsync(T2.p, T2h, T2.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  HPSB_CUDA(cudaMemcpyAsync(H1.p, H1h, H1.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  HPSB_CUDA(cudaMemcpyAsync(H2.p, H2h, H2.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  CopyBatch gat;
+  gat.gather(T1.p, nb, dperm.p, dperm.p, P1.p, nb, nb, nb);
+  gat.gather(T2.p, nb, dperm.p + nb, dperm.p + nb, P2.p, nb, nb, nb);
+  gat.gather(H1.p, nb, dperm.p, nullptr, h1.p, nb, nb, 1);
+  gat.gather(H2.p, nb, dperm.p + nb, nullptr, h2.p, nb, nb, 1);
+  gat.run(ctx);
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double2 *T1pp = P1.p, *T1ps = P1.p + p * nb, *T1sp = P1.p + p, *T1ss = P1.p + p + p * nb;
+  const double2 *T2pp = P2.p, *T2ps = P2.p + p * nb, *T2sp = P2.p + p, *T2ss = P2.p + p + p * nb;
+  CopyBatch pre;
+  pre.identity(W.p, s, s);
+  pre.copy(T2sp, nb, R.p + p * s, s, s, p, -1.0);
+  pre.copy(T1sp, nb, X2.p, s, s, p, -1.0);
+  pre.zero(X2.p + p * s, s, s, p);
+  pre.copy(T1pp, nb, Tn.p, q, p, p, 1.0);
+  pre.zero(Tn.p + p * q, q, p, p);
+  pre.zero(Tn.p + p, q, p, p);
+  pre.copy(T2pp, nb, Tn.p + p + p * q, q, p, p, 1.0);
+  pre.copy(h2.p + p, nb, u.p, s, s, 1, -1.0);
+  pre.copy(h1.p + p, nb, x2.p, s, s, 1, -1.0);
+  pre.copy(h1.p, nb, Hn.p, q, p, 1, 1.0);
+  pre.copy(h2.p, nb, Hn.p + p, q, p, 1, 1.0);
+  pre.run(ctx);
+  GemmBatch g1, g2, g3, g4;
+  g1.add(T2ss, nb, T1ss, nb, W.p, s, s, s, s, -1.0, 1.0);
+  g1.add(T2ss, nb, T1sp, nb, R.p, s, s, p, s, 1.0, 0.0);
+  g1.add(T2ss, nb, h1.p + p, nb, u.p, s, s, 1, s, 1.0, 1.0);
+  g1.run(ctx);
+  DevBuf<int> st(1);
+  HPSB_CUDA(cudaMemsetAsync(st.p, 0, sizeof(int), ctx->stream));
+  InverseBatch inv;
+  inv.ops.push_back(InvOp{W.p, s, s, 0, 0});
+  inv.run(ctx, st.p);
+  g2.add(W.p, s, R.p, s, X1.p, s, s, q, s, 1.0, 0.0);
+  g2.add(W.p, s, u.p, s, x1.p, s, s, 1, s, 1.0, 0.0);
+  g2.run(ctx);
+  g3.add(T1ss, nb, X1.p, s, X2.p, s, s, q, s, -1.0, 1.0);
+  g3.add(T1ps, nb, X1.p, s, Tn.p, q, p, q, s, 1.0, 1.0);
+  g3.add(T1ss, nb, x1.p, s, x2.p, s, s, 1, s, -1.0, 1.0);
+  g3.add(T1ps, nb, x1.p, s, Hn.p, q, p, 1, s, 1.0, 1.0);
+  g3.run(ctx);
+  g4.add(T2ps, nb, X2.p, s, Tn.p + p, q, p, q, s, 1.0, 1.0);
+  g4.add(T2ps, nb, x2.p, s, Hn.p + p, q, p, 1, s, 1.0, 1.0);
+  g4.run(ctx);
+  int fail = 0;
+  HPSB_CUDA(cudaMemcpyAsync(&fail, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  HPSB_CUDA(cudaMemcpyAsync(Th, Tn.p, Tn.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+  HPSB_CUDA(cudaMemcpyAsync(Hh, Hn.p, Hn.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (fail) throw std::runtime_error("merge_pair: singular face block");
+}
+
+}  // namespace hpsb

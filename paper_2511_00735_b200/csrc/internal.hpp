@@ -1,0 +1,236 @@
+// Internal host-side structures of the hps_b200 library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hps_b200.h"
+
+namespace hpsb {
+
+// ---------------------------------------------------------------- errors
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NoConvergence : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define HPSB_CUDA(x)                                              \
+  do {                                                            \
+    cudaError_t e_ = (x);                                         \
+    if (e_ != cudaSuccess) ::hpsb::cuda_fail(e_, #x, __FILE__, __LINE__); \
+  } while (0)
+// After a kernel launch: catch launch-configuration errors immediately.
+#define HPSB_LAUNCHED(ctx)                 \
+  do {                                     \
+    HPSB_CUDA(cudaGetLastError());         \
+    ++(ctx)->launches;                     \
+  } while (0)
+
+// ---------------------------------------------------------------- device memory
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  std::size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(std::size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(std::size_t count) {
+    release();
+    if (count) HPSB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr, n = 0;
+  }
+  std::size_t bytes() const { return n * sizeof(T); }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    if (v.size() != n) alloc(v.size());
+    if (n) HPSB_CUDA(cudaMemcpyAsync(p, v.data(), bytes(), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// ---------------------------------------------------------------- context
+struct ProfAgg {
+  int64_t launches = 0;
+  double ms = 0, bytes = 0, flops = 0;
+};
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+  double bytes, flops;
+};
+struct Context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t timer[2] = {nullptr, nullptr};
+  // Per-kernel CUDA-event profiling (off by default; see KernelScope).
+  bool profile = false;
+  std::vector<ProfRec> pending;
+  std::vector<cudaEvent_t> event_pool;
+  std::vector<std::pair<std::string, ProfAgg>> agg;
+  void collect();
+};
+
+// Brackets one kernel launch with CUDA events when profiling is enabled and
+// attributes its algorithmic bytes / flops (the roofline numerators).
+struct KernelScope {
+  Context* c;
+  int idx = -1;
+  KernelScope(Context* ctx, const char* name, double bytes, double flops);
+  ~KernelScope();
+};
+
+// ---------------------------------------------------------------- host structure
+struct IndexSets {
+  int order = 0;
+  std::vector<int> left, right, bottom, top, boundary, interior, noncorner, comp_of_full;
+};
+IndexSets build_index_sets(int order);
+
+struct Face {
+  int e1, e2, s1, s2, level, group;
+};
+struct FaceGraph {
+  int n = 0;
+  std::vector<Face> faces;
+  std::vector<std::pair<int, int>> level_range;
+  std::vector<std::vector<std::vector<int>>> groups;
+  std::vector<std::array<int, 4>> face_of_element;
+  int num_levels() const { return static_cast<int>(level_range.size()); }
+  int num_faces() const { return static_cast<int>(faces.size()); }
+};
+FaceGraph build_face_graph(int n);
+
+struct Gll {
+  std::vector<double> nodes, weights, diff;  // diff col-major (N+1)^2
+};
+Gll gll_rule(int order);
+
+// ---------------------------------------------------------------- GEMV work lists
+// y[yi] = beta * y[yi] + gamma * z[zi] + alpha * A x[xi]   (complex, A col-major)
+// Negative indices: x entries read as 0, y entries are skipped.
+struct VItem {
+  const double2* A;
+  const double2* x;
+  const double2* z;
+  double2* y;
+  const int* xi;
+  const int* zi;
+  const int* yi;
+  int lda, rows, cols, pad;
+  double alpha, beta, gamma, pad2;
+};
+// A unit is a chain of items executed in order by one CTA.
+struct VUnit {
+  int first, count;
+};
+// One kernel launch: a set of independent units.
+struct VPhase {
+  int unit_begin = 0, unit_count = 0;
+  int max_cols = 0;
+  double bytes = 0;
+};
+struct VPlan {
+  std::vector<VItem> items;
+  std::vector<VUnit> units;
+  std::vector<VPhase> phases;
+  DevBuf<VItem> d_items;
+  DevBuf<VUnit> d_units;
+  int64_t bytes_per_run = 0;  // algorithmic operator bytes streamed per run
+  const char* name = "vplan";
+  // Start a new phase; returns its index.
+  int begin_phase();
+  void add_unit(const std::vector<VItem>& chain);
+  // Adds A (rows x cols) split into row blocks as independent units.
+  void add_split(const VItem& it, int row_block);
+  void finalize(cudaStream_t s);
+  void run(Context* ctx) const;
+  void run_phase(Context* ctx, int p) const;
+};
+
+// ---------------------------------------------------------------- objects
+struct Elements {
+  Context* ctx = nullptr;
+  int n = 0, order = 0, m = 0, nb = 0;
+  double eta = 0, h = 0;
+  DevBuf<double2> T;  // [e][nb*nb]
+  DevBuf<double2> H;  // [e][nb]
+  DevBuf<int> status; // per-element failure flags
+  double build_seconds = 0;
+};
+
+struct Skeleton {
+  Context* ctx = nullptr;
+  Elements* el = nullptr;
+  FaceGraph graph;
+  int m = 0, bs = 0;
+  int64_t dim = 0;
+  int nrhs = 1;
+  DevBuf<double2> rhs;  // [nrhs][dim]
+  // Element-level in/out skeleton indices: [e][nb] (-1 on physical sides).
+  std::vector<int> h_in, h_out;
+  DevBuf<int> d_in, d_out;
+  VPlan apply_plan;      // y = x + sum_e scatter(T_e gather(x))
+  DevBuf<double2> x_buf, y_buf;  // plan endpoints
+};
+
+struct LevelOps;
+struct Hierarchy {
+  Context* ctx = nullptr;
+  Skeleton* sk = nullptr;
+  int depth = 0, total_levels = 0;
+  std::vector<std::unique_ptr<LevelOps>> levels;  // levels[l-1], l = 1..depth
+  double build_seconds = 0;
+  int64_t device_bytes = 0;
+  ~Hierarchy();
+};
+
+struct Precond;
+
+// ---------------------------------------------------------------- entry points
+std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double eta,
+                                         const double* coeff_dev, const double2* source_dev);
+std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs);
+void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev);
+std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth);
+void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,
+                            int* keys, double* data);
+Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg);
+void destroy_precond(Precond* p);
+void precond_apply(Precond* p, const double2* v_dev, double2* z_dev);
+void precond_apply_host(Precond* p, const double2* v_host, double2* z_host);
+int64_t precond_bytes(const Precond* p);
+void merge_pair(Context* ctx, int m, const double2* T1, const double2* H1, const double2* T2,
+                const double2* H2, int alpha, int beta, double2* T, double2* H);
+hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs_dev, double2* x_dev,
+                   const hpsb_krylov_config& cfg, hpsb_solve_report* rep);
+
+// Small device kernels shared between modules (csrc/blas.cu).
+void zfill(Context* ctx, double2* p, std::size_t n, double2 v);
+void zcopy(Context* ctx, double2* dst, const double2* src, std::size_t n);
+
+}  // namespace hpsb

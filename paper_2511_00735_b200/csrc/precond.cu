@@ -1,0 +1,397 @@
+// K4/K5: the HPS-multigrid preconditioner apply on the stored box maps.
+//
+// MgPreconditioner::apply_level (proj/src/multigrid.cpp:30-100) with gamma = 1
+// is a V-cycle over the merge hierarchy.  On the B200 it runs in place on two
+// skeleton-length vectors r (residual, initialised with v) and out:
+//   down, level l = 1 .. depth-1, per merge (A_g x = v_g solved through
+//   W = (I - T2_ss T1_ss)^{-1}):
+//     D1  t          = r[in1_s] - T2_ss r[in2_s]
+//     D2  out[in1_s] = W t                                  (x1)
+//     D3  out[in2_s] = r[in2_s] - T1_ss out[in1_s]          (x2)
+//     D4  r[out_k_p] -= T_k,ps out[ink_s]   (k = 1, 2)      (restriction, C_l w)
+//   coarse, level depth: gmres_fixed_steps(M_depth, r_tail, coarse_iters)
+//     (multigrid.cpp:37-41), M_depth = I + sum_boxes scatter(T_box);
+//   up, level l = depth-1 .. 1 (prolongation, B_l z then A_g^{-1}):
+//     U1  b1 = T2_sp out[in2_p],  b2 = T1_sp out[in1_p]
+//     U2  t  = b1 - T2_ss b2
+//     U3  y1 = W t
+//     U4  out[in2_s] += T1_ss y1 - b2,   out[in1_s] -= y1
+// R (v - M F v) only needs C_l w, so no full M_l
+// apply is ever streamed.  Levels with many merges run one CTA per merge
+// (a chained unit); levels with few, large merges split every phase over
+// row blocks so the whole GPU streams the maps.
+#include <algorithm>
+#include <cmath>
+
+#include "device.cuh"
+#include "hierarchy.hpp"
+
+namespace hpsb {
+
+struct Precond {
+  Hierarchy* h = nullptr;
+  hpsb_mg_config cfg{};
+  Context* ctx = nullptr;
+  int64_t dim = 0, off_d = 0, dim_d = 0;
+  DevBuf<double2> r, out, tmp;
+  VPlan down, up, coarse_mv;
+  DevBuf<int> coarse_idx;
+  DevBuf<double2> V, cv, cw, Hm, gv, rs;
+  DevBuf<double> rc, state;
+  int64_t bytes_per_apply = 0;
+};
+
+namespace {
+constexpr int kCoarseThreads = 1024;
+
+__device__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sh[32] = t;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+// state: [0] bnorm, [1] done, [2] jused, [3] zero-rhs
+__global__ void __launch_bounds__(kCoarseThreads) coarse_init_kernel(const double2* rd, int64_t n,
+                                                                     double2* V, double2* cv,
+                                                                     double2* gv, int ci,
+                                                                     double* state) {
+  __shared__ double sh[33];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += cabs2(rd[i]);
+  const double beta = sqrt(block_sum(s, sh));
+  const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double2 v = make_double2(rd[i].x * inv, rd[i].y * inv);
+    V[i] = v;
+    cv[i] = v;
+  }
+  if (threadIdx.x <= ci) gv[threadIdx.x] = make_double2(threadIdx.x == 0 ? beta : 0.0, 0.0);
+  if (threadIdx.x == 0) {
+    state[0] = beta;
+    state[1] = beta == 0.0 ? 1.0 : 0.0;
+    state[2] = 0.0;
+    state[3] = beta == 0.0 ? 1.0 : 0.0;
+  }
+}
+
+__device__ void make_givens(double2 a, double2 b, double& c, double2& s) {
+  // krylov.cpp:17-31
+  c = 1.0;
+  s = make_double2(0.0, 0.0);
+  const double na = hypot(a.x, a.y), nb = hypot(b.x, b.y);
+  if (nb == 0.0) return;
+  const double r = hypot(na, nb);
+  const double2 cb = make_double2(b.x, -b.y);
+  if (na == 0.0) {
+    c = 0.0;
+    s = make_double2(cb.x / nb, cb.y / nb);
+  } else {
+    c = na / r;
+    const double2 an = make_double2(a.x / na, a.y / na);
+    s = cmul(an, make_double2(cb.x / r, cb.y / r));
+  }
+}
+
+__device__ void apply_givens(double c, double2 s, double2& a, double2& b) {
+  // krylov.cpp:33-37
+  const double2 t = cadd(cscale(a, c), cmul(s, b));
+  b = cadd(cmul(make_double2(-s.x, s.y), a), cscale(b, c));
+  a = t;
+}
+
+// One MGS Arnoldi step of gmres_fixed_steps (no reorthogonalisation, as
+// KrylovConfig's default, krylov.cpp:194-201).  Hm is (ci+1) x ci col-major.
+__global__ void __launch_bounds__(kCoarseThreads) coarse_step_kernel(
+    int j, int64_t n, int ci, double2* V, double2* cv, double2* cw, double2* Hm, double2* gv,
+    double* rc, double2* rs, double* state) {
+  __shared__ double sh[33];
+  if (state[1] != 0.0) return;
+  const int ldh = ci + 1;
+  for (int i = 0; i <= j; ++i) {
+    const double2* Vi = V + i * n;
+    double sr = 0.0, si = 0.0;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const double2 a = Vi[k], b = cw[k];
+      sr += a.x * b.x + a.y * b.y;
+      si += a.x * b.y - a.y * b.x;
+    }
+    const double hr = block_sum(sr, sh);
+    const double hi = block_sum(si, sh);
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+      const double2 a = Vi[k];
+      double2 w = cw[k];
+      w.x -= hr * a.x - hi * a.y;
+      w.y -= hr * a.y + hi * a.x;
+      cw[k] = w;
+    }
+    if (threadIdx.x == 0) Hm[i + j * ldh] = make_double2(hr, hi);
+    __syncthreads();
+  }
+  double s2 = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s2 += cabs2(cw[k]);
+  const double hnext = sqrt(block_sum(s2, sh));
+  if (threadIdx.x == 0) {
+    Hm[j + 1 + j * ldh] = make_double2(hnext, 0.0);
+    for (int i = 0; i < j; ++i)
+      apply_givens(rc[i], rs[i], Hm[i + j * ldh], Hm[i + 1 + j * ldh]);
+    double c;
+    double2 s;
+    make_givens(Hm[j + j * ldh], Hm[j + 1 + j * ldh], c, s);
+    rc[j] = c, rs[j] = s;
+    apply_givens(c, s, Hm[j + j * ldh], Hm[j + 1 + j * ldh]);
+    apply_givens(c, s, gv[j], gv[j + 1]);
+    state[2] = j + 1;
+    if (hnext <= 1e-14 * state[0]) state[1] = 1.0;  // happy breakdown
+  }
+  __syncthreads();
+  if (hnext <= 1e-14 * state[0]) return;
+  const double inv = 1.0 / hnext;
+  double2* Vn = V + (j + 1) * n;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    const double2 v = make_double2(cw[k].x * inv, cw[k].y * inv);
+    Vn[k] = v;
+    cv[k] = v;
+  }
+}
+
+// y = H^{-1} g (upper triangular), out = sum_i y_i V_i (krylov.cpp:133-145).
+__global__ void __launch_bounds__(kCoarseThreads) coarse_finish_kernel(int64_t n, int ci,
+                                                                       const double2* V,
+                                                                       const double2* Hm,
+                                                                       const double2* gv,
+                                                                       const double* state,
+                                                                       double2* outd) {
+  __shared__ double2 y[64];
+  const int ju = static_cast<int>(state[2]);
+  const int ldh = ci + 1;
+  if (threadIdx.x == 0) {
+    for (int i = ju - 1; i >= 0; --i) {
+      double2 s = gv[i];
+      for (int k = i + 1; k < ju; ++k) s = csub(s, cmul(Hm[i + k * ldh], y[k]));
+      y[i] = cdiv(s, Hm[i + i * ldh]);
+    }
+  }
+  __syncthreads();
+  const bool zero = state[3] != 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    if (!zero)
+      for (int i = 0; i < ju; ++i) acc = cfma(y[i], V[i * n + k], acc);
+    outd[k] = acc;
+  }
+}
+
+VItem item(const double2* A, int lda, int rows, int cols, const double2* x, const int* xi,
+           const double2* z, const int* zi, double2* y, const int* yi, double alpha, double beta,
+           double gamma) {
+  VItem it{};
+  it.A = A, it.lda = lda, it.rows = rows, it.cols = cols;
+  it.x = x, it.xi = xi, it.z = z, it.zi = zi, it.y = y, it.yi = yi;
+  it.alpha = alpha, it.beta = beta, it.gamma = gamma;
+  return it;
+}
+}  // namespace
+
+Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
+  // multigrid.cpp:9-28
+  if (cfg.depth < 2) throw InvalidArgument("MgPreconditioner: depth must be >= 2");
+  if (cfg.depth > h->depth) throw InvalidArgument("MgPreconditioner: depth exceeds the built hierarchy");
+  if (!cfg.exact_coarse && cfg.gamma < 1) throw InvalidArgument("MgPreconditioner: gamma must be >= 1");
+  if (!cfg.exact_coarse && cfg.coarse_iters < 1)
+    throw InvalidArgument("MgPreconditioner: coarse_iters must be >= 1");
+  if (cfg.exact_coarse) throw InvalidArgument("MgPreconditioner: exact_coarse is not on the B200 path");
+  if (cfg.gamma != 1) throw InvalidArgument("MgPreconditioner: gamma > 1 is not on the B200 path");
+  if (cfg.depth != h->depth)
+    throw InvalidArgument("MgPreconditioner: depth must equal the built hierarchy depth on the B200 path");
+  if (cfg.coarse_iters > 60) throw InvalidArgument("MgPreconditioner: coarse_iters must be <= 60");
+  Context* ctx = h->ctx;
+  auto p = std::make_unique<Precond>();
+  p->h = h, p->cfg = cfg, p->ctx = ctx;
+  const Skeleton* sk = h->sk;
+  p->dim = sk->dim;
+  p->r.alloc(p->dim);
+  p->out.alloc(p->dim);
+  const int sms = ctx->num_sms;
+
+  size_t tmp_total = 0;
+  for (int l = 1; l < cfg.depth; ++l)
+    for (const auto& mr : h->levels[l - 1]->merges) tmp_total += 3 * static_cast<size_t>(mr.s);
+  p->tmp.alloc(std::max<size_t>(tmp_total, 1));
+
+  // ---- down / up sweeps
+  size_t toff = 0;
+  std::vector<size_t> level_tmp(cfg.depth, 0);
+  for (int l = 1; l < cfg.depth; ++l) {
+    level_tmp[l] = toff;
+    for (const auto& mr : h->levels[l - 1]->merges) toff += 3 * static_cast<size_t>(mr.s);
+  }
+  double2* r = p->r.p;
+  double2* out = p->out.p;
+  auto build_level = [&](int l, bool downward) {
+    const LevelOps& L = *h->levels[l - 1];
+    const int ng = static_cast<int>(L.merges.size());
+    const bool chain = ng >= 2 * sms;
+    int total_rows = 0;
+    for (const auto& mr : L.merges) total_rows += mr.s + mr.p1 + mr.p2;
+    int rb = ((total_rows / (2 * sms)) + 31) & ~31;
+    rb = std::max(32, std::min(256, rb));
+    std::vector<std::vector<VItem>> stages(downward ? 4 : 4);
+    std::vector<std::vector<VItem>> chains(ng);
+    size_t t = level_tmp[l];
+    for (int gi = 0; gi < ng; ++gi) {
+      const MergeRec& mr = L.merges[gi];
+      const ChildBox& c1 = L.children[mr.c1];
+      const ChildBox& c2 = L.children[mr.c2];
+      const int s = mr.s, p1 = mr.p1, p2 = mr.p2, P1 = c1.P, P2 = c2.P;
+      const double2* T1 = L.tperm.p + c1.t_off;
+      const double2* T2 = L.tperm.p + c2.t_off;
+      const double2 *T1ps = T1 + static_cast<size_t>(p1) * P1, *T1sp = T1 + p1,
+                    *T1ss = T1 + p1 + static_cast<size_t>(p1) * P1;
+      const double2 *T2ps = T2 + static_cast<size_t>(p2) * P2, *T2sp = T2 + p2,
+                    *T2ss = T2 + p2 + static_cast<size_t>(p2) * P2;
+      const double2* W = L.w.p + mr.w_off;
+      const int* ix = L.idx.p;
+      const int *in1s = ix + mr.in1_sep, *in2s = ix + mr.in2_sep, *in1p = ix + mr.in1_per,
+                *in2p = ix + mr.in2_per, *out1p = ix + mr.out1_per, *out2p = ix + mr.out2_per;
+      double2* t1 = p->tmp.p + t;
+      double2* t2 = t1 + s;
+      double2* t3 = t2 + s;
+      t += 3 * static_cast<size_t>(s);
+      std::vector<std::vector<VItem>> st(4);
+      if (downward) {
+        st[0].push_back(item(T2ss, P2, s, s, r, in2s, r, in1s, t3, nullptr, -1.0, 0.0, 1.0));
+        st[1].push_back(item(W, s, s, s, t3, nullptr, nullptr, nullptr, out, in1s, 1.0, 0.0, 0.0));
+        st[2].push_back(item(T1ss, P1, s, s, out, in1s, r, in2s, out, in2s, -1.0, 0.0, 1.0));
+        if (p1) st[3].push_back(item(T1ps, P1, p1, s, out, in1s, nullptr, nullptr, r, out1p, -1.0, 1.0, 0.0));
+        if (p2) st[3].push_back(item(T2ps, P2, p2, s, out, in2s, nullptr, nullptr, r, out2p, -1.0, 1.0, 0.0));
+      } else {
+        if (p2) st[0].push_back(item(T2sp, P2, s, p2, out, in2p, nullptr, nullptr, t1, nullptr, 1.0, 0.0, 0.0));
+        else st[0].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, nullptr, nullptr, t1, nullptr, 0.0, 0.0, 0.0));
+        if (p1) st[0].push_back(item(T1sp, P1, s, p1, out, in1p, nullptr, nullptr, t2, nullptr, 1.0, 0.0, 0.0));
+        else st[0].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, nullptr, nullptr, t2, nullptr, 0.0, 0.0, 0.0));
+        st[1].push_back(item(T2ss, P2, s, s, t2, nullptr, t1, nullptr, t3, nullptr, -1.0, 0.0, 1.0));
+        st[2].push_back(item(W, s, s, s, t3, nullptr, nullptr, nullptr, t1, nullptr, 1.0, 0.0, 0.0));
+        st[3].push_back(item(T1ss, P1, s, s, t1, nullptr, t2, nullptr, out, in2s, 1.0, 1.0, -1.0));
+        st[3].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, t1, nullptr, out, in1s, 0.0, 1.0, -1.0));
+      }
+      for (int k = 0; k < 4; ++k)
+        for (auto& it : st[k]) {
+          if (chain) chains[gi].push_back(it);
+          else stages[k].push_back(it);
+        }
+    }
+    VPlan& plan = downward ? p->down : p->up;
+    if (chain) {
+      plan.begin_phase();
+      for (auto& c : chains) plan.add_unit(c);
+    } else {
+      for (auto& stg : stages) {
+        plan.begin_phase();
+        for (auto& it : stg) plan.add_split(it, rb);
+      }
+    }
+  };
+  for (int l = 1; l < cfg.depth; ++l) build_level(l, true);
+  for (int l = cfg.depth - 1; l >= 1; --l) build_level(l, false);
+  p->down.name = "vcycle_down";
+  p->up.name = "vcycle_up";
+  p->down.finalize(ctx->stream);
+  p->up.finalize(ctx->stream);
+
+  // ---- coarse level: M_depth = I + sum_boxes scatter(T_box) on the tail
+  const LevelOps& C = *h->levels[cfg.depth - 1];
+  p->off_d = static_cast<int64_t>(C.first_face) * sk->bs;
+  p->dim_d = p->dim - p->off_d;
+  const int ci = cfg.coarse_iters;
+  p->V.alloc(static_cast<size_t>(p->dim_d) * (ci + 1));
+  p->cv.alloc(p->dim_d);
+  p->cw.alloc(p->dim_d);
+  p->Hm.alloc(static_cast<size_t>(ci + 1) * ci);
+  p->gv.alloc(ci + 1);
+  p->rs.alloc(ci);
+  p->rc.alloc(ci);
+  p->state.alloc(4);
+  std::vector<int> lidx;
+  std::vector<size_t> in_at, out_at;
+  for (const ChildBox& c : C.children) {
+    in_at.push_back(lidx.size());
+    for (const auto& q : c.pos) lidx.push_back(q.in - static_cast<int>(p->off_d));
+    out_at.push_back(lidx.size());
+    for (const auto& q : c.pos) lidx.push_back(q.out - static_cast<int>(p->off_d));
+  }
+  p->coarse_idx.upload(lidx, ctx->stream);
+  int crows = 0;
+  for (const ChildBox& c : C.children) crows += c.P;
+  int crb = ((crows / (2 * sms)) + 31) & ~31;
+  crb = std::max(32, std::min(256, crb));
+  p->coarse_mv.begin_phase();
+  for (size_t k = 0; k < C.children.size(); ++k) {
+    const ChildBox& c = C.children[k];
+    const int* ci_in = p->coarse_idx.p + in_at[k];
+    const int* ci_out = p->coarse_idx.p + out_at[k];
+    p->coarse_mv.add_split(item(C.tperm.p + c.t_off, c.P, c.P, c.P, p->cv.p, ci_in, p->cv.p,
+                                ci_out, p->cw.p, ci_out, 1.0, 0.0, 1.0),
+                           crb);
+  }
+  p->coarse_mv.name = "coarse_matvec";
+  p->coarse_mv.finalize(ctx->stream);
+  p->bytes_per_apply = p->down.bytes_per_run + p->up.bytes_per_run +
+                       static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run;
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return p.release();
+}
+
+void destroy_precond(Precond* p) { delete p; }
+
+void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
+  Context* ctx = p->ctx;
+  zcopy(ctx, p->r.p, v_dev, p->dim);
+  p->down.run(ctx);
+  const int ci = p->cfg.coarse_iters;
+  {
+  KernelScope ks(ctx, "coarse_gmres", 32.0 * p->dim_d, 0.0);
+  coarse_init_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(p->r.p + p->off_d, p->dim_d, p->V.p,
+                                                            p->cv.p, p->gv.p, ci, p->state.p);
+  HPSB_LAUNCHED(ctx);
+  }
+  for (int j = 0; j < ci; ++j) {
+    p->coarse_mv.run(ctx);
+    KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (2 * j + 4), 0.0);
+    coarse_step_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(j, p->dim_d, ci, p->V.p, p->cv.p,
+                                                              p->cw.p, p->Hm.p, p->gv.p, p->rc.p,
+                                                              p->rs.p, p->state.p);
+    HPSB_LAUNCHED(ctx);
+  }
+  {
+  KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (ci + 1), 0.0);
+  coarse_finish_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(p->dim_d, ci, p->V.p, p->Hm.p,
+                                                              p->gv.p, p->state.p,
+                                                              p->out.p + p->off_d);
+  HPSB_LAUNCHED(ctx);
+  }
+  p->up.run(ctx);
+  zcopy(ctx, z_dev, p->out.p, p->dim);
+}
+
+int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }
+
+void precond_apply_host(Precond* p, const double2* v, double2* z) {
+  Context* ctx = p->ctx;
+  DevBuf<double2> vd(p->dim), zd(p->dim);
+  HPSB_CUDA(cudaMemcpyAsync(vd.p, v, vd.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  precond_apply(p, vd.p, zd.p);
+  HPSB_CUDA(cudaMemcpyAsync(z, zd.p, zd.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace hpsb

@@ -1,0 +1,107 @@
+// Skeleton system: the global ItI interface operator and its right-hand side.
+//
+// assemble_skeleton (proj/src/skeleton.cpp:88-137) stores M as a std::map of
+// bs x bs blocks: identity slot diagonals plus +T couplings.  On the B200 the
+// operator is never assembled: M = I + sum_e P_e T_e Q_e^T, where Q_e gathers
+// element e's incoming unknowns (its own slot of each interior face) and P_e
+// scatters the rows of its outgoing data to the neighbour's incoming slot of
+// the same face.  Every skeleton entry is the scatter target of exactly one
+// (element, side) pair, so the matvec is conflict-free with no atomics, and
+// the operator bytes streamed are exactly the element ItI maps.
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace hpsb {
+
+namespace {
+// rhs[out_e(alpha)] = -H_e(alpha) - sum_{gamma physical} T_e(alpha, gamma) t_e(gamma)
+// (skeleton.cpp:121-132), one CTA per element, one thread per boundary row.
+__global__ void skeleton_rhs_kernel(const double2* __restrict__ T, const double2* __restrict__ H,
+                                    const int* __restrict__ in_idx, const int* __restrict__ out_idx,
+                                    const double2* __restrict__ tside, double2* rhs, int nb,
+                                    int64_t dim, int ne, int nrhs) {
+  const int e = blockIdx.x;
+  const double2* Te = T + static_cast<size_t>(e) * nb * nb;
+  const int* in_e = in_idx + static_cast<size_t>(e) * nb;
+  const int* out_e = out_idx + static_cast<size_t>(e) * nb;
+  for (int r = 0; r < nrhs; ++r) {
+    const double2* t = tside + (static_cast<size_t>(r) * ne + e) * nb;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+      const int o = out_e[b];
+      if (o < 0) continue;
+      double2 v = H[static_cast<size_t>(e) * nb + b];
+      v = make_double2(-v.x, -v.y);
+      for (int c = 0; c < nb; ++c)
+        if (in_e[c] < 0) v = csub(v, cmul(Te[b + static_cast<size_t>(c) * nb], t[c]));
+      rhs[static_cast<size_t>(r) * dim + o] = v;
+    }
+  }
+}
+}  // namespace
+
+std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs) {
+  Context* ctx = el->ctx;
+  auto sk = std::make_unique<Skeleton>();
+  sk->ctx = ctx;
+  sk->el = el;
+  sk->graph = build_face_graph(el->n);
+  sk->m = el->m;
+  sk->bs = 2 * el->m;
+  sk->dim = static_cast<int64_t>(sk->graph.num_faces()) * sk->bs;
+  sk->nrhs = nrhs;
+  const int ne = el->n * el->n, nb = el->nb, m = el->m;
+  // Element incoming / outgoing skeleton indices (slot_offset, skeleton.cpp:80-86).
+  sk->h_in.assign(static_cast<size_t>(ne) * nb, -1);
+  sk->h_out.assign(static_cast<size_t>(ne) * nb, -1);
+  for (int e = 0; e < ne; ++e)
+    for (int side = 0; side < 4; ++side) {
+      const int f = sk->graph.face_of_element[e][side];
+      if (f < 0) continue;
+      const int own = sk->graph.faces[f].e1 == e ? 1 : 0;
+      for (int k = 0; k < m; ++k) {
+        sk->h_in[static_cast<size_t>(e) * nb + side * m + k] = f * sk->bs + own * m + k;
+        sk->h_out[static_cast<size_t>(e) * nb + side * m + k] = f * sk->bs + (1 - own) * m + k;
+      }
+    }
+  sk->d_in.upload(sk->h_in, ctx->stream);
+  sk->d_out.upload(sk->h_out, ctx->stream);
+
+  // Right-hand sides.
+  sk->rhs.alloc(static_cast<size_t>(nrhs) * sk->dim);
+  DevBuf<double2> d_t(static_cast<size_t>(nrhs) * ne * nb);
+  HPSB_CUDA(cudaMemcpyAsync(d_t.p, tside_host, d_t.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  KernelScope ks(ctx, "skeleton_rhs", 16.0 * ne * nb * nb, 0.0);
+  skeleton_rhs_kernel<<<ne, 64, 0, ctx->stream>>>(el->T.p, el->H.p, sk->d_in.p, sk->d_out.p, d_t.p,
+                                                  sk->rhs.p, nb, sk->dim, ne, nrhs);
+  HPSB_LAUNCHED(ctx);
+
+  // Matvec plan: one unit per element, y[out] = x[out] + T_e x[in].
+  sk->x_buf.alloc(sk->dim);
+  sk->y_buf.alloc(sk->dim);
+  sk->apply_plan.begin_phase();
+  for (int e = 0; e < ne; ++e) {
+    VItem it{};
+    it.A = el->T.p + static_cast<size_t>(e) * nb * nb;
+    it.lda = nb, it.rows = nb, it.cols = nb;
+    it.x = sk->x_buf.p, it.xi = sk->d_in.p + static_cast<size_t>(e) * nb;
+    it.z = sk->x_buf.p, it.zi = sk->d_out.p + static_cast<size_t>(e) * nb;
+    it.y = sk->y_buf.p, it.yi = sk->d_out.p + static_cast<size_t>(e) * nb;
+    it.alpha = 1.0, it.beta = 0.0, it.gamma = 1.0;
+    sk->apply_plan.add_unit({it});
+  }
+  sk->apply_plan.name = "skeleton_matvec";
+  sk->apply_plan.finalize(ctx->stream);
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return sk;
+}
+
+void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev) {
+  Context* ctx = sk->ctx;
+  if (x_dev != sk->x_buf.p) zcopy(ctx, sk->x_buf.p, x_dev, sk->dim);
+  sk->apply_plan.run(ctx);
+  if (y_dev != sk->y_buf.p) zcopy(ctx, y_dev, sk->y_buf.p, sk->dim);
+}
+
+}  // namespace hpsb

@@ -1,0 +1,175 @@
+"""Parity of the B200 path (through the C ABI) against the CPU oracle.
+
+Tolerances are BASELINE.json north_star's: ItI and merge operators within
+1e-10 relative Frobenius error, final solution within 1e-9 relative L2,
+GMRES iteration counts within +-1; integer structure bit-exact (see
+tests/test_abi_cpu.py).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_OP = 1e-10
+TOL_SOL = 1e-9
+
+
+def relf(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def hps():
+    import paper_2511_00735_b200 as hps
+    return hps
+
+
+@pytest.fixture(scope="module")
+def ctx(hps):
+    return hps.Context(0)
+
+
+class Case:
+    def __init__(self, hps, oracle, ctx, kind, config, n=0, order=0, kappa=0.0, seed=None,
+                 depth=0):
+        self.prob = hps.problem(kind, config, seed=seed, n=n, order=order, kappa=kappa)
+        p = self.prob
+        self.S = oracle.Session(p.n, p.order, p.kappa, p.eta, p.coeff, p.source, p.tside[0])
+        self.el = hps.build_elements(ctx, p)
+        self.sk = hps.assemble_skeleton(self.el, p)
+        self.depth = depth
+
+
+_cases = {}
+
+
+def case(hps, oracle, ctx, name):
+    if name not in _cases:
+        spec = {
+            "cfg0": dict(kind=2, config=0),
+            "cfg1": dict(kind=2, config=1),
+            "bump_n4_N4": dict(kind=0, config=0, n=4, order=4, kappa=6.0),
+            "pw_n4_N16": dict(kind=1, config=0, n=4, order=16, kappa=20.0),
+            "cfg2_n8": dict(kind=2, config=2, n=8),
+            "cfg3_n4": dict(kind=2, config=3, n=4),
+            "cfg4_n8": dict(kind=2, config=4, n=8),
+        }[name]
+        _cases[name] = Case(hps, oracle, ctx, **spec)
+    return _cases[name]
+
+
+ALL = ["cfg0", "bump_n4_N4", "pw_n4_N16", "cfg2_n8", "cfg3_n4", "cfg4_n8", "cfg1"]
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_element_iti_and_source(hps, oracle, ctx, name):
+    c = case(hps, oracle, ctx, name)
+    T, H = c.el.iti()
+    worst_t = worst_h = 0.0
+    for e in range(c.prob.n ** 2):
+        To, Ho = c.S.element(e)
+        worst_t = max(worst_t, relf(T[e], To))
+        if np.linalg.norm(Ho) > 0:
+            worst_h = max(worst_h, relf(H[e], Ho))
+        else:
+            assert np.linalg.norm(H[e]) == 0.0  # zero source gives exactly zero H
+    assert worst_t < TOL_OP, worst_t
+    assert worst_h < TOL_OP, worst_h
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_skeleton_rhs_and_matvec(hps, oracle, ctx, name):
+    c = case(hps, oracle, ctx, name)
+    assert c.sk.dim == c.S.dim
+    r = c.sk.rhs()
+    ro = c.S.rhs()
+    if np.linalg.norm(ro) == 0:
+        assert np.linalg.norm(r) == 0
+    else:
+        assert relf(r, ro) < TOL_OP
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+    assert relf(c.sk.apply(x), c.S.apply_M(x)) < TOL_OP
+
+
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg3_n4", "cfg2_n8"])
+def test_hierarchy_level_systems(hps, oracle, ctx, name):
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk)
+    c.S.build_hierarchy(0, True)
+    bs = 2 * c.el.m
+    for level in range(1, h.depth + 1):
+        ff, blocks = h.level_blocks(level)
+        ffo, bo = c.S.level_blocks(level)
+        assert ff == ffo
+        nf = 2 * c.prob.n * (c.prob.n - 1) - ff
+        A = np.zeros((nf * bs, nf * bs), dtype=complex)
+        B = np.zeros_like(A)
+        for (r, cc), b in blocks.items():
+            A[r * bs:(r + 1) * bs, cc * bs:(cc + 1) * bs] = b
+        for (r, cc), b in bo.items():
+            B[r * bs:(r + 1) * bs, cc * bs:(cc + 1) * bs] = b
+        assert relf(A, B) < TOL_OP, (level, relf(A, B))
+
+
+def test_n4_block_sparsity_patterns(hps, oracle, ctx):
+    # test_dissection.cpp:365-433 on the GPU hierarchy
+    c = case(hps, oracle, ctx, "bump_n4_N4")
+    h = hps.build_hierarchy(c.sk)
+    M2 = {0: [0, 1, 8, 9, 12, 13], 8: [0, 1, 4, 5, 8], 9: [0, 1, 4, 5, 9, 12, 13, 14, 15],
+          12: [0, 1, 2, 3, 9, 10, 12, 13]}
+    _, blocks = h.level_blocks(2)
+    scale = max(np.abs(b).max() for b in blocks.values())
+    for r, cols in M2.items():
+        got = sorted(cc for (rr, cc), b in blocks.items() if rr == r and np.abs(b).max() > 1e-12 * scale)
+        assert got == cols, (r, got)
+
+
+def test_merge_pair(hps, oracle, ctx):
+    c = case(hps, oracle, ctx, "cfg0")
+    g = hps.face_graph(c.prob.n)
+    for f in (0, 8, 16):
+        e1, e2, s1, s2 = (int(v) for v in g["faces"][f][:4])
+        T1, H1 = c.S.element(e1)
+        T2, H2 = c.S.element(e2)
+        To, Ho = oracle.merge_pair(T1, H1, T2, H2, s1, s2, c.el.m)
+        Tg, Hg = hps.merge_pair(ctx, T1, H1, T2, H2, s1, s2, c.el.m)
+        assert relf(Tg, To) < TOL_OP
+        assert relf(Hg, Ho) < TOL_OP
+
+
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg3_n4", "cfg2_n8", "cfg1"])
+def test_preconditioner_apply(hps, oracle, ctx, name):
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk)
+    c.S.build_hierarchy(0, False)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    c.S.precond(depth=h.depth, gamma=1, coarse_iters=4)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        v = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+        assert relf(pc.apply(v), c.S.precond_apply(v)) < TOL_OP
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg3_n4", "cfg2_n8", "cfg1"])
+def test_fgmres_solution_and_iterations(hps, oracle, ctx, name):
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk)
+    c.S.build_hierarchy(0, False)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    c.S.precond(depth=h.depth, gamma=1, coarse_iters=4)
+    rhs = c.sk.rhs()
+    x, rep = hps.fgmres(c.sk, rhs, pc, restart=c.prob.restart, tol=c.prob.tol)
+    xo, repo = c.S.solve(c.S.rhs(), True, restart=c.prob.restart, tol=c.prob.tol)
+    assert rep["converged"] and repo["converged"]
+    assert abs(rep["iterations"] - repo["iterations"]) <= 1, (rep, repo)
+    assert relf(x, xo) < TOL_SOL
+
+
+def test_unpreconditioned_gmres(hps, oracle, ctx):
+    c = case(hps, oracle, ctx, "cfg0")
+    x, rep = hps.gmres(c.sk, c.sk.rhs(), restart=50, tol=1e-10)
+    xo, repo = c.S.solve(c.S.rhs(), False, restart=50, tol=1e-10)
+    assert rep["converged"]
+    assert abs(rep["iterations"] - repo["iterations"]) <= 1
+    assert relf(x, xo) < TOL_SOL
