@@ -93,6 +93,11 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     ctx->c.num_sms = prop.multiProcessorCount;
     HPSB_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
     for (auto& e : ctx->c.ev) HPSB_CUDA(cudaEventCreate(&e));
+    cudaMemPool_t pool;
+    HPSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    HPSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    hpsb::alloc_stream() = ctx->c.stream;
     *out = ctx.release();
     return HPSB_OK;
   });
@@ -102,7 +107,12 @@ hpsb_status hpsb_context_destroy(hpsb_context ctx) {
   return guarded([&] {
     if (!ctx) return HPSB_OK;
     cudaStreamSynchronize(ctx->c.stream);
+    if (hpsb::alloc_stream() == ctx->c.stream) hpsb::alloc_stream() = nullptr;
     for (auto& e : ctx->c.ev) cudaEventDestroy(e);
+    for (auto& e : ctx->c.timer)
+      if (e) cudaEventDestroy(e);
+    ctx->c.pending.clear();
+    for (auto& e : ctx->c.event_pool) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
     return HPSB_OK;

@@ -36,6 +36,15 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
   } while (0)
 
 // ---------------------------------------------------------------- device memory
+// Device buffers come from the stream-ordered pool of the active context's
+// stream (cudaMallocAsync with an unbounded release threshold): the merge
+// stage allocates and frees per level, and pooled allocations keep that off
+// the critical path (no implicit device synchronisation as in cudaFree).
+inline cudaStream_t& alloc_stream() {
+  static cudaStream_t s = nullptr;
+  return s;
+}
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -56,11 +65,19 @@ struct DevBuf {
   ~DevBuf() { release(); }
   void alloc(std::size_t count) {
     release();
-    if (count) HPSB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    if (count) {
+      if (alloc_stream())
+        HPSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
+      else
+        HPSB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
+    }
     n = count;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (alloc_stream()) cudaFreeAsync(p, alloc_stream());
+      else cudaFree(p);
+    }
     p = nullptr, n = 0;
   }
   std::size_t bytes() const { return n * sizeof(T); }

@@ -202,14 +202,105 @@ __global__ void __launch_bounds__(256) inverse_smem_kernel(const InvOp* __restri
   if (threadIdx.x == 0 && !ok) status[0] = op.tag + 1;
 }
 
-// Large matrices: the same algorithm on global memory (ld == n required).
-__global__ void __launch_bounds__(1024) inverse_global_kernel(const InvOp* __restrict__ ops,
-                                                              int* perm_ws, int* status) {
+// ---- blocked Gauss-Jordan (large matrices), one panel of kb columns per step
+// Pivot rows for columns [k0, k0+kb): partial-pivoting LU of a copy of the
+// panel rows k0..n-1 (one CTA per matrix).  ipiv[k0+j] = row swapped with k0+j.
+__global__ void __launch_bounds__(1024) panel_pivot_kernel(const InvOp* __restrict__ ops, int k0,
+                                                           int kb, double2* panel_ws,
+                                                           int* ipiv_ws, int* status) {
   const InvOp op = ops[blockIdx.x];
+  if (k0 >= op.n) return;
+  const int n = op.n, kw = min(kb, n - k0), rows = n - k0;
+  double2* P = panel_ws + op.perm_off * (size_t)kb;  // rows x kw, ld rows
+  int* ipiv = ipiv_ws + op.perm_off;
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  const bool ok = gj_inverse_cta(op.A, op.n, perm_ws + op.perm_off, red_v, red_i);
-  if (threadIdx.x == 0 && !ok) status[0] = op.tag + 1;
+  __shared__ int s_p;
+  for (int idx = threadIdx.x; idx < rows * kw; idx += blockDim.x) {
+    const int r = idx % rows, c = idx / rows;
+    P[idx] = op.A[(size_t)(k0 + r) + (size_t)(k0 + c) * op.lda];
+  }
+  __syncthreads();
+  for (int j = 0; j < kw; ++j) {
+    double best = -1.0;
+    int bi = j;
+    for (int i = j + threadIdx.x; i < rows; i += blockDim.x) {
+      const double v = cabs2(P[i + j * rows]);
+      if (v > best) best = v, bi = i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
+    }
+    if ((threadIdx.x & 31) == 0) red_v[threadIdx.x >> 5] = best, red_i[threadIdx.x >> 5] = bi;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = -1.0;
+      int p = j;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+        if (red_v[w] > b || (red_v[w] == b && red_i[w] < p)) b = red_v[w], p = red_i[w];
+      s_p = p;
+      ipiv[k0 + j] = k0 + p;
+      if (!(b > 0.0)) status[0] = op.tag + 1;
+    }
+    __syncthreads();
+    const int p = s_p;
+    if (p != j)
+      for (int c = threadIdx.x; c < kw; c += blockDim.x) {
+        const double2 t = P[j + c * rows];
+        P[j + c * rows] = P[p + c * rows];
+        P[p + c * rows] = t;
+      }
+    __syncthreads();
+    const double2 inv = cinv(P[j + j * rows]);
+    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x)
+      P[i + j * rows] = cmul(P[i + j * rows], inv);
+    __syncthreads();
+    const int rem = rows - j - 1, cw = kw - j - 1;
+    for (int idx = threadIdx.x; idx < rem * cw; idx += blockDim.x) {
+      const int i = j + 1 + idx % rem, c = j + 1 + idx / rem;
+      P[i + c * rows] = csub(P[i + c * rows], cmul(P[i + j * rows], P[j + c * rows]));
+    }
+    __syncthreads();
+  }
+}
+
+// Apply the panel's row swaps to every column of A (sequential swaps per column).
+__global__ void swap_rows_kernel(const InvOp* __restrict__ ops, int k0, int kb,
+                                 const int* __restrict__ ipiv_ws) {
+  const InvOp op = ops[blockIdx.y];
+  if (k0 >= op.n) return;
+  const int kw = min(kb, op.n - k0);
+  const int* ipiv = ipiv_ws + op.perm_off;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < op.n; c += gridDim.x * blockDim.x) {
+    double2* col = op.A + (size_t)c * op.lda;
+    for (int j = 0; j < kw; ++j) {
+      const int p = ipiv[k0 + j];
+      if (p != k0 + j) {
+        const double2 t = col[k0 + j];
+        col[k0 + j] = col[p];
+        col[p] = t;
+      }
+    }
+  }
+}
+
+// Undo the row interchanges as column interchanges, in reverse order.
+__global__ void unscramble_kernel(const InvOp* __restrict__ ops, const int* __restrict__ ipiv_ws) {
+  const InvOp op = ops[blockIdx.y];
+  const int* ipiv = ipiv_ws + op.perm_off;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < op.n; r += gridDim.x * blockDim.x)
+    for (int j = op.n - 1; j >= 0; --j) {
+      const int p = ipiv[j];
+      if (p != j) {
+        double2* a = op.A + r + (size_t)j * op.lda;
+        double2* b = op.A + r + (size_t)p * op.lda;
+        const double2 t = *a;
+        *a = *b;
+        *b = t;
+      }
+    }
 }
 }  // namespace
 
@@ -288,14 +379,73 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     HPSB_LAUNCHED(ctx);
   }
   if (!large.empty()) {
+    // Blocked Gauss-Jordan with partial pivoting: for each panel K of kb
+    // columns, choose pivot rows by a panel LU, swap them in, invert the
+    // pivot block P = A_KK^{-1} and sweep the rest of the matrix with grouped
+    // DMMA GEMMs:  U = P A_KR,  A_RR -= A_RK U,  A_RK = -A_RK P,  A_KR = U.
+    constexpr int kb = 32;
     d_large.upload(large, ctx->stream);
     perm_ws.alloc(perm_total);
-    double fl = 0;
-    for (const auto& o : large) fl += 8.0 * o.n * double(o.n) * o.n;
-    KernelScope ks(ctx, "zinverse_global", 0.0, fl);
-    inverse_global_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(
-        d_large.p, perm_ws.p, status_dev);
+    int nmax = 0;
+    for (const auto& o : large) nmax = std::max(nmax, o.n);
+    DevBuf<double2> panel(static_cast<size_t>(perm_total) * kb), U(static_cast<size_t>(perm_total) * kb),
+        Q(static_cast<size_t>(perm_total) * kb);
+    std::vector<InvOp> pivops(large.size());
+    for (int k0 = 0; k0 < nmax; k0 += kb) {
+      {
+        KernelScope ks(ctx, "zinverse_panel", 0.0, 0.0);
+        panel_pivot_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(
+            d_large.p, k0, kb, panel.p, perm_ws.p, status_dev);
+        HPSB_LAUNCHED(ctx);
+      }
+      {
+        KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);
+        dim3 grid((nmax + 255) / 256, static_cast<unsigned>(large.size()));
+        swap_rows_kernel<<<grid, 256, 0, ctx->stream>>>(d_large.p, k0, kb, perm_ws.p);
+        HPSB_LAUNCHED(ctx);
+      }
+      InverseBatch piv;
+      GemmBatch gu, gr, gq;
+      CopyBatch back;
+      for (const auto& o : large) {
+        if (k0 >= o.n) continue;
+        const int n = o.n, kw = std::min(kb, n - k0), k1 = k0 + kw, tail = n - k1;
+        double2* A = o.A;
+        const size_t ld = o.lda;
+        double2* AKK = A + k0 + k0 * ld;
+        piv.ops.push_back(InvOp{AKK, kw, o.lda, o.tag, 0});
+        double2* Ub = U.p + static_cast<size_t>(o.perm_off) * kb;  // kw x n, ld kw
+        double2* Qb = Q.p + static_cast<size_t>(o.perm_off) * kb;  // n x kw, ld n
+        // U = P A_KR (left and right column ranges)
+        gu.add(AKK, o.lda, A + k0, o.lda, Ub, kw, kw, k0, kw, 1.0, 0.0);
+        gu.add(AKK, o.lda, A + k0 + k1 * ld, o.lda, Ub + static_cast<size_t>(k1) * kw, kw, kw, tail,
+               kw, 1.0, 0.0);
+        // A_RR -= A_RK U (four blocks)
+        for (int rb = 0; rb < 2; ++rb) {
+          const int r0 = rb == 0 ? 0 : k1, rn = rb == 0 ? k0 : tail;
+          for (int cb = 0; cb < 2; ++cb) {
+            const int c0 = cb == 0 ? 0 : k1, cn = cb == 0 ? k0 : tail;
+            gr.add(A + r0 + k0 * ld, o.lda, Ub + static_cast<size_t>(c0) * kw, kw,
+                   A + r0 + c0 * ld, o.lda, rn, cn, kw, -1.0, 1.0);
+          }
+          // Q = -A_RK P
+          gq.add(A + r0 + k0 * ld, o.lda, AKK, o.lda, Qb + r0, n, rn, kw, kw, -1.0, 0.0);
+          back.copy(Qb + r0, n, A + r0 + k0 * ld, o.lda, rn, kw, 1.0);
+        }
+        back.copy(Ub, kw, A + k0, o.lda, kw, k0, 1.0);
+        back.copy(Ub + static_cast<size_t>(k1) * kw, kw, A + k0 + k1 * ld, o.lda, kw, tail, 1.0);
+      }
+      piv.run(ctx, status_dev);  // in place: A_KK <- P (kw <= 32 uses the smem kernel)
+      gu.run(ctx);
+      gr.run(ctx);
+      gq.run(ctx);
+      back.run(ctx);
+    }
+    KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);
+    dim3 grid((nmax + 255) / 256, static_cast<unsigned>(large.size()));
+    unscramble_kernel<<<grid, 256, 0, ctx->stream>>>(d_large.p, perm_ws.p);
     HPSB_LAUNCHED(ctx);
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   }
 }
 
