@@ -222,7 +222,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
       zcopy(ctx, tmp.p, rhs, n);
       beta = bnorm;
     } else {
-      beta = true_residual();
+      beta = true_residual() * bnorm;  // r0 = rhs - M x (krylov.cpp:72-73)
     }
     if (beta / bnorm <= cfg.tol) {
       converged = true;
