@@ -41,8 +41,82 @@ struct ElemArgs {
   int* status;
   double* ws;        // per-slot workspace
   size_t ws_stride;  // doubles per slot
+  const int* elist;  // optional element list (fallback re-run)
+  int nlist;
+  int npad, nbc;     // v2: padded interior size (multiple of 16), padded rhs count
 };
 
+// Boundary Schur complement and ItI map from the interior solve
+// Y = L_ii^{-1} [L_iG | b~] (ld ldy, interior order q = (i-1) m + (j-1)):
+//   S = L_GG - L_Gi Y,  f = L_Gi y_b,  T = I - 2 i eta S^{-1},  H = 2 i eta S^{-1} f.
+// L_Gi / L_GG are the impedance rows I_in = deriv + i eta trace
+// (element.cpp:92-125, :137-139); L_Gi has N-1 entries per row.
+__device__ bool iti_epilogue(const ElemArgs& a, int e, const double* Y, int ldy, double2* S,
+                             double2* f, int* perm, double* red_v, int* red_i) {
+  const int tid = threadIdx.x, m = a.m, nb = a.nb, np = a.order + 1, N = a.order;
+  auto D = [&](int r, int c) { return __ldg(a.diff + r + c * np); };
+  auto lgi = [&](int b, int k, int& q) {  // entry of row b at interior node k of its line
+    const int side = b / m, t = b % m + 1;
+    switch (side) {
+      case 0: q = (k - 1) * m + (t - 1); return -D(0, k);
+      case 1: q = (k - 1) * m + (t - 1); return D(N, k);
+      case 2: q = (t - 1) * m + (k - 1); return -D(0, k);
+      default: q = (t - 1) * m + (k - 1); return D(N, k);
+    }
+  };
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const int b = idx % nb, c = idx / nb;
+    const int side = b / m, t = b % m + 1;
+    double acc = 0.0;
+    for (int k = 1; k <= m; ++k) {
+      int q;
+      const double d = lgi(b, k, q);
+      acc += d * Y[q + static_cast<size_t>(c) * ldy];
+    }
+    // L_GG: derivative entries on the two boundary nodes of the same line
+    const int cs = c / m, ct = c % m + 1;
+    double lgg = 0.0;
+    if (ct == t) {
+      if (side <= 1 && cs <= 1)
+        lgg = (side == 0 ? -1.0 : 1.0) * D(side == 0 ? 0 : N, cs == 0 ? 0 : N);
+      else if (side >= 2 && cs >= 2)
+        lgg = (side == 2 ? -1.0 : 1.0) * D(side == 2 ? 0 : N, cs == 2 ? 0 : N);
+    }
+    double2 sv = make_double2(lgg - acc, 0.0);
+    if (b == c) sv.y += a.eta;
+    S[idx] = sv;
+  }
+  double2 fv = make_double2(0.0, 0.0);
+  if (tid < nb && a.source)
+    for (int k = 1; k <= m; ++k) {
+      int q;
+      const double d = lgi(tid, k, q);
+      fv.x += d * Y[q + static_cast<size_t>(nb) * ldy];
+      fv.y += d * Y[q + static_cast<size_t>(nb + 1) * ldy];
+    }
+  __syncthreads();
+  const bool ok = gj_inverse_cta(S, nb, perm, red_v, red_i);
+  if (tid < nb) f[tid] = fv;
+  __syncthreads();
+  const double te = 2.0 * a.eta;
+  double2* Te = a.T + static_cast<size_t>(e) * nb * nb;
+  for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
+    const double2 s = S[idx];
+    const int b = idx % nb, c = idx / nb;
+    Te[idx] = make_double2((b == c ? 1.0 : 0.0) + te * s.y, -te * s.x);
+  }
+  if (tid < nb) {
+    double2 acc = make_double2(0.0, 0.0);
+    if (a.source)
+      for (int c = 0; c < nb; ++c) acc = cfma(S[tid + c * nb], f[c], acc);
+    a.H[static_cast<size_t>(e) * nb + tid] = make_double2(-te * acc.y, te * acc.x);
+  }
+  __syncthreads();
+  return ok;
+}
+
+// v1 / fallback: unblocked right-looking Cholesky (pivoted LU when L_ii is
+// indefinite) on the element's workspace.  Processes a.elist when given.
 __global__ void __launch_bounds__(kThreads) element_kernel(ElemArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
@@ -62,9 +136,10 @@ __global__ void __launch_bounds__(kThreads) element_kernel(ElemArgs a) {
 
   for (int i = tid; i < np; i += blockDim.x) mass[i] = a.mass[i];
   auto K = [&](int r, int c) { return __ldg(a.stiff + r + c * np); };
-  auto D = [&](int r, int c) { return __ldg(a.diff + r + c * np); };
+  const int count = a.elist ? a.nlist : a.ne;
 
-  for (int e = blockIdx.x; e < a.ne; e += gridDim.x) {
+  for (int ii = blockIdx.x; ii < count; ii += gridDim.x) {
+    const int e = a.elist ? a.elist[ii] : ii;
     __syncthreads();
     if (tid == 0) s_fail = 0;
     const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
@@ -228,78 +303,253 @@ __global__ void __launch_bounds__(kThreads) element_kernel(ElemArgs a) {
       __syncthreads();
     }
     }
-    // 5. S = L_GG - L_Gi Y (boundary rows, element.cpp:92-125 with the
-    //    Gamma rows replaced by the incoming impedance rows, :137-139)
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const int b = idx % nb, c = idx / nb;
-      const int side = b / m, t = b % m + 1;
-      double acc = 0.0;
-      for (int k = 1; k <= m; ++k) {
-        double d;
-        int q;
-        switch (side) {
-          case 0: d = -D(0, k); q = (k - 1) * m + (t - 1); break;
-          case 1: d = D(N, k); q = (k - 1) * m + (t - 1); break;
-          case 2: d = -D(0, k); q = (t - 1) * m + (k - 1); break;
-          default: d = D(N, k); q = (t - 1) * m + (k - 1); break;
-        }
-        acc += d * Y[q + c * ni];
-      }
-      // L_GG: derivative entries on the two boundary nodes of the same line
-      const int cs = c / m, ct = c % m + 1;
-      double lgg = 0.0;
-      if (ct == t) {
-        if (side <= 1 && cs <= 1) {
-          const int row = side == 0 ? 0 : N, col = cs == 0 ? 0 : N;
-          lgg = (side == 0 ? -1.0 : 1.0) * D(row == 0 ? 0 : N, col);
-        } else if (side >= 2 && cs >= 2) {
-          const int col = cs == 2 ? 0 : N;
-          lgg = (side == 2 ? -1.0 : 1.0) * D(side == 2 ? 0 : N, col);
-        }
-      }
-      double2 sv = make_double2(lgg - acc, 0.0);
-      if (b == c) sv.y += a.eta;
-      S[idx] = sv;
-    }
-    // f = L_Gi y_b (complex), kept in the ncol-th rows of Y's spare space
     __syncthreads();
-    double2 fv = make_double2(0.0, 0.0);
-    if (tid < nb && a.source) {
-      const int b = tid, side = b / m, t = b % m + 1;
-      for (int k = 1; k <= m; ++k) {
-        double d;
-        int q;
-        switch (side) {
-          case 0: d = -D(0, k); q = (k - 1) * m + (t - 1); break;
-          case 1: d = D(N, k); q = (k - 1) * m + (t - 1); break;
-          case 2: d = -D(0, k); q = (t - 1) * m + (k - 1); break;
-          default: d = D(N, k); q = (t - 1) * m + (k - 1); break;
-        }
-        fv.x += d * Y[q + nb * ni];
-        fv.y += d * Y[q + (nb + 1) * ni];
-      }
-    }
-    __syncthreads();
-    // 6. S^{-1}
-    const bool ok = gj_inverse_cta(S, nb, perm, red_v, red_i);
-    if (tid < nb) f[tid] = fv;
-    __syncthreads();
-    // 7. T = I - 2 i eta S^{-1};  H = 2 i eta S^{-1} f
-    const double te = 2.0 * a.eta;
-    double2* Te = a.T + static_cast<size_t>(e) * nb * nb;
-    for (int idx = tid; idx < nb * nb; idx += blockDim.x) {
-      const double2 s = S[idx];
-      const int b = idx % nb, c = idx / nb;
-      Te[idx] = make_double2((b == c ? 1.0 : 0.0) + te * s.y, -te * s.x);
-    }
-    if (tid < nb) {
-      double2 acc = make_double2(0.0, 0.0);
-      if (a.source)
-        for (int c = 0; c < nb; ++c) acc = cfma(S[tid + c * nb], f[c], acc);
-      a.H[static_cast<size_t>(e) * nb + tid] = make_double2(-te * acc.y, te * acc.x);
-    }
-    __syncthreads();
+    const bool ok = iti_epilogue(a, e, Y, ni, S, f, perm, red_v, red_i);
     if (tid == 0) a.status[e] = (s_fail ? 1 : 0) | (ok ? 0 : 2);  // 1: singular L_ii
+  }
+}
+
+// ---------------------------------------------------------------- v2
+constexpr int PW = 16;  // panel width
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ inline int v2_ldp(int P) { return ((P - PW + 15) & ~15) + 4; }
+constexpr int kLdq = PW + 4;
+__host__ __device__ inline size_t v2_region(int P, int nbc, int nb) {
+  const size_t panel = PW * PW + static_cast<size_t>(v2_ldp(P)) * PW + kLdq * nbc;
+  const size_t epi = 2 * (static_cast<size_t>(nb) * nb + nb);
+  return panel > epi ? panel : epi;
+}
+
+// v2: blocked right-looking Cholesky of the interior block, padded to P (a
+// multiple of 16, identity on the padding), with the forward solve of the
+// nb + 2 right-hand sides fused into each panel step; the trailing-matrix
+// (SYRK) and right-hand-side (GEMM) updates run on the FP64 tensor cores
+// (mma.sync m8n8k4, one 8 x 8 tile per warp step, panels staged in smem).
+// The backward solve R^T X = Y is blocked the same way, right-looking from
+// the last panel.  An indefinite L_ii (first failing pivot) marks the
+// element for the pivoted-LU fallback (v1 kernel, status bit 4).
+__global__ void __launch_bounds__(kThreads) element_v2_kernel(ElemArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int m = a.m, ni = a.ni, nb = a.nb, np = a.order + 1, N = a.order;
+  const int P = a.npad, nbc = a.nbc, ldp = v2_ldp(P);
+  double* D11 = reinterpret_cast<double*>(smem_raw);
+  double* L21s = D11 + PW * PW;
+  double* Bp = L21s + static_cast<size_t>(ldp) * PW;
+  double2* S = reinterpret_cast<double2*>(smem_raw);
+  double2* f = S + nb * nb;
+  double* mass = reinterpret_cast<double*>(smem_raw) + v2_region(P, nbc, nb);
+  int* perm = reinterpret_cast<int*>(mass + np);
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_fail;
+
+  double* A = a.ws + blockIdx.x * a.ws_stride;  // P x P, ld P (lower triangle used)
+  double* B = A + static_cast<size_t>(P) * P;    // P x nbc, ld P
+  for (int i = tid; i < np; i += blockDim.x) mass[i] = a.mass[i];
+  auto K = [&](int r, int c) { return __ldg(a.stiff + r + c * np); };
+
+  for (int e = blockIdx.x; e < a.ne; e += gridDim.x) {
+    __syncthreads();
+    if (tid == 0) s_fail = 0;
+    const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
+    // assemble the lower triangle of L_ii (element.cpp:57-90), identity padding
+    for (int idx = tid; idx < P * P; idx += blockDim.x) {
+      const int r = idx % P, c = idx / P;
+      if (c > r) continue;
+      double v;
+      if (r >= ni) {
+        v = (r == c) ? 1.0 : 0.0;
+      } else {
+        const int i = r / m + 1, j = r % m + 1, k = c / m + 1, l = c % m + 1;
+        v = 0.0;
+        if (j == l) v += K(i, k) * mass[j];
+        if (i == k) v += mass[i] * K(j, l);
+        if (r == c) v -= __ldg(ce + i * np + j) * mass[i] * mass[j];
+      }
+      A[idx] = v;
+    }
+    // right-hand sides [L_iG | re b~ | im b~ | 0 ...]
+    for (int idx = tid; idx < P * nbc; idx += blockDim.x) {
+      const int q = idx % P, b = idx / P;
+      double v = 0.0;
+      if (q < ni && b < nb + 2) {
+        const int i = q / m + 1, j = q % m + 1;
+        if (b < nb) {
+          const int side = b / m, t = b % m + 1;
+          switch (side) {
+            case 0: v = (j == t) ? K(i, 0) * mass[j] : 0.0; break;
+            case 1: v = (j == t) ? K(i, N) * mass[j] : 0.0; break;
+            case 2: v = (i == t) ? mass[i] * K(j, 0) : 0.0; break;
+            default: v = (i == t) ? mass[i] * K(j, N) : 0.0; break;
+          }
+        } else if (a.source) {
+          const double2 s = a.source[static_cast<size_t>(e) * ni + q];
+          const double w = mass[i] * mass[j];
+          v = (b == nb) ? s.x * w : s.y * w;
+        }
+      }
+      B[idx] = v;
+    }
+    __syncthreads();
+
+    // ---- factorisation + forward solve, panel by panel
+    for (int k0 = 0; k0 < P; k0 += PW) {
+      const int rem = P - k0 - PW;
+      for (int idx = tid; idx < PW * PW; idx += blockDim.x) {
+        const int r = idx % PW, c = idx / PW;
+        D11[idx] = c <= r ? A[(k0 + r) + static_cast<size_t>(k0 + c) * P] : 0.0;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int j = 0; j < PW; ++j) {
+          if (lane == 0) {
+            const double d = D11[j + j * PW];
+            if (!(d > 0.0)) s_fail = 1;
+            D11[j + j * PW] = sqrt(fmax(d, 1e-300));
+          }
+          __syncwarp();
+          const double inv = 1.0 / D11[j + j * PW];
+          if (lane > j && lane < PW) D11[lane + j * PW] *= inv;
+          __syncwarp();
+          for (int p = lane; p < PW * PW; p += 32) {
+            const int r = p % PW, c = p / PW;
+            if (c > j && r >= c) D11[r + c * PW] -= D11[r + j * PW] * D11[c + j * PW];
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (s_fail) break;
+      for (int idx = tid; idx < PW * PW; idx += blockDim.x) {
+        const int r = idx % PW, c = idx / PW;
+        if (c <= r) A[(k0 + r) + static_cast<size_t>(k0 + c) * P] = D11[idx];
+      }
+      // L21 = A21 L11^{-T} (one row per thread)
+      for (int r = tid; r < rem; r += blockDim.x) {
+        double x[PW];
+        double* row = A + (k0 + PW + r) + static_cast<size_t>(k0) * P;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) x[j] = row[static_cast<size_t>(j) * P];
+#pragma unroll
+        for (int j = 0; j < PW; ++j) {
+          double s = x[j];
+#pragma unroll
+          for (int t = 0; t < j; ++t) s -= x[t] * D11[j + t * PW];
+          x[j] = s / D11[j + j * PW];
+          L21s[r + j * ldp] = x[j];
+          row[static_cast<size_t>(j) * P] = x[j];
+        }
+      }
+      // forward solve of the panel rows of B
+      for (int c = tid; c < nbc; c += blockDim.x) {
+        double y[PW];
+        double* col = B + k0 + static_cast<size_t>(c) * P;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) y[j] = col[j];
+#pragma unroll
+        for (int j = 0; j < PW; ++j) {
+          double s = y[j];
+#pragma unroll
+          for (int t = 0; t < j; ++t) s -= D11[j + t * PW] * y[t];
+          y[j] = s / D11[j + j * PW];
+          Bp[j + c * kLdq] = y[j];
+          col[j] = y[j];
+        }
+      }
+      __syncthreads();
+      // trailing SYRK (lower 8x8 tiles) and B update, DMMA
+      const int nt = rem / 8, ntri = nt * (nt + 1) / 2, nbt = nbc / 8;
+      const int total = ntri + nt * nbt;
+      for (int tile = warp; tile < total; tile += kThreads / 32) {
+        double c0, c1;
+        if (tile < ntri) {
+          int I = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+          while (I * (I + 1) / 2 > tile) --I;
+          while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+          const int J = tile - I * (I + 1) / 2;
+          double* C = A + (k0 + PW + 8 * I + g) + static_cast<size_t>(k0 + PW + 8 * J + 2 * t4) * P;
+          c0 = C[0];
+          c1 = C[P];
+#pragma unroll
+          for (int kk = 0; kk < PW; kk += 4) {
+            const double av = -L21s[(8 * I + g) + (kk + t4) * ldp];
+            const double bv = L21s[(8 * J + g) + (kk + t4) * ldp];
+            dmma(c0, c1, av, bv);
+          }
+          C[0] = c0;
+          C[P] = c1;
+        } else {
+          const int tt = tile - ntri, I = tt % nt, J = tt / nt;
+          double* C = B + (k0 + PW + 8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
+          c0 = C[0];
+          c1 = C[P];
+#pragma unroll
+          for (int kk = 0; kk < PW; kk += 4) {
+            const double av = -L21s[(8 * I + g) + (kk + t4) * ldp];
+            const double bv = Bp[(kk + t4) + (8 * J + g) * kLdq];
+            dmma(c0, c1, av, bv);
+          }
+          C[0] = c0;
+          C[P] = c1;
+        }
+      }
+      __syncthreads();
+    }
+    if (s_fail) {
+      if (tid == 0) a.status[e] = 4;  // indefinite: pivoted-LU fallback
+      continue;
+    }
+    // ---- backward solve R^T X = Y, right-looking from the last panel
+    for (int k0 = P - PW; k0 >= 0; k0 -= PW) {
+      for (int idx = tid; idx < PW * PW; idx += blockDim.x) {
+        const int r = idx % PW, c = idx / PW;
+        D11[idx] = c <= r ? A[(k0 + r) + static_cast<size_t>(k0 + c) * P] : 0.0;
+      }
+      __syncthreads();
+      for (int c = tid; c < nbc; c += blockDim.x) {
+        double y[PW];
+        double* col = B + k0 + static_cast<size_t>(c) * P;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) y[j] = col[j];
+#pragma unroll
+        for (int j = PW - 1; j >= 0; --j) {
+          double s = y[j];
+#pragma unroll
+          for (int t = j + 1; t < PW; ++t) s -= D11[t + j * PW] * y[t];
+          y[j] = s / D11[j + j * PW];
+        }
+#pragma unroll
+        for (int j = 0; j < PW; ++j) {
+          col[j] = y[j];
+          Bp[j + c * kLdq] = y[j];
+        }
+      }
+      __syncthreads();
+      const int nr = k0 / 8, nbt = nbc / 8;
+      for (int tile = warp; tile < nr * nbt; tile += kThreads / 32) {
+        const int I = tile % nr, J = tile / nr;
+        double* C = B + (8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
+        double c0 = C[0], c1 = C[P];
+#pragma unroll
+        for (int kk = 0; kk < PW; kk += 4) {
+          const double av = -A[(k0 + kk + t4) + static_cast<size_t>(8 * I + g) * P];
+          const double bv = Bp[(kk + t4) + (8 * J + g) * kLdq];
+          dmma(c0, c1, av, bv);
+        }
+        C[0] = c0;
+        C[P] = c1;
+      }
+      __syncthreads();
+    }
+    const bool ok = iti_epilogue(a, e, B, P, S, f, perm, red_v, red_i);
+    if (tid == 0) a.status[e] = ok ? 0 : 2;
   }
 }
 
@@ -338,32 +588,59 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   el->H.alloc(static_cast<size_t>(ne) * nb);
   el->status.alloc(ne);
 
-  const int slots = std::min(ne, 2 * ctx->num_sms);
-  const size_t stride = static_cast<size_t>(ni) * ni + static_cast<size_t>(ni) * (nb + 2);
-  DevBuf<double> ws(stride * slots);
-
   ElemArgs a{};
   a.ne = ne, a.order = order, a.m = m, a.ni = ni, a.nb = nb, a.eta = eta;
   a.mass = d_mass.p, a.diff = d_diff.p, a.stiff = d_stiff.p;
   a.coeff = coeff_dev, a.source = source_dev;
   a.T = el->T.p, a.H = el->H.p, a.status = el->status.p;
-  a.ws = ws.p, a.ws_stride = stride;
-  const size_t smem = sizeof(double2) * (nb * nb + nb) + sizeof(double) * (ni + np) +
-                      sizeof(int) * nb + 16;
-  HPSB_CUDA(cudaFuncSetAttribute(element_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+  a.npad = (ni + PW - 1) / PW * PW;
+  a.nbc = (nb + 2 + 7) / 8 * 8;
+
+  // v2 (blocked, DMMA) for every element
+  const size_t smem2 = sizeof(double) * (v2_region(a.npad, a.nbc, nb) + np) + sizeof(int) * nb + 16;
+  HPSB_CUDA(cudaFuncSetAttribute(element_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem2)));
+  int per_sm = 0;
+  HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_v2_kernel, kThreads, smem2));
+  const int slots2 = std::min(ne, std::max(1, std::min(per_sm, 3)) * ctx->num_sms);
+  const size_t stride2 = static_cast<size_t>(a.npad) * (a.npad + a.nbc);
+  DevBuf<double> ws(stride2 * slots2);
+  a.ws = ws.p, a.ws_stride = stride2;
   HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   {
     // pinned algorithmic flops: ni^3/3 + 2 ni^2 nb + 8 nb^3 per element
     const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
     KernelScope ks(ctx, "element_iti", 8.0 * ne * (np * np + 2 * ni + 2 * nb * nb + 2 * nb), fe * ne);
-    element_kernel<<<slots, kThreads, smem, ctx->stream>>>(a);
+    element_v2_kernel<<<slots2, kThreads, smem2, ctx->stream>>>(a);
     HPSB_LAUNCHED(ctx);
   }
-  HPSB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   std::vector<int> st(ne);
   HPSB_CUDA(cudaMemcpyAsync(st.data(), el->status.p, ne * sizeof(int), cudaMemcpyDeviceToHost,
                             ctx->stream));
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  // pivoted-LU fallback (v1) for elements whose interior block is indefinite
+  std::vector<int> redo;
+  for (int e = 0; e < ne; ++e)
+    if (st[e] & 4) redo.push_back(e);
+  if (!redo.empty()) {
+    DevBuf<int> d_redo;
+    d_redo.upload(redo, ctx->stream);
+    const int slots = std::min(static_cast<int>(redo.size()), 2 * ctx->num_sms);
+    const size_t stride = static_cast<size_t>(ni) * ni + static_cast<size_t>(ni) * (nb + 2);
+    ws.alloc(stride * slots);
+    a.ws = ws.p, a.ws_stride = stride;
+    a.elist = d_redo.p, a.nlist = static_cast<int>(redo.size());
+    const size_t smem = sizeof(double2) * (nb * nb + nb) + sizeof(double) * (ni + np) +
+                        sizeof(int) * nb + 16;
+    HPSB_CUDA(cudaFuncSetAttribute(element_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    KernelScope ks(ctx, "element_iti_lu", 0.0, 0.0);
+    element_kernel<<<slots, kThreads, smem, ctx->stream>>>(a);
+    HPSB_LAUNCHED(ctx);
+    HPSB_CUDA(cudaMemcpyAsync(st.data(), el->status.p, ne * sizeof(int), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+  }
+  HPSB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   float ms = 0;
   HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
