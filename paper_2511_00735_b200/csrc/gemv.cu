@@ -8,80 +8,47 @@
 //     proj/src/multigrid.cpp:47-98): group solves, restriction C_l w and
 //     prolongation B_l z, all expressed on the stored box maps;
 //   - the coarse-level matvec inside gmres_fixed_steps.
-// A plan is a list of phases (kernel launches); a phase is a list of units
-// (one CTA each); a unit is a chain of items run in order by its CTA.  Each
-// item streams its matrix once with coalesced 16-byte loads (threads map to
-// rows of the column-major block, column groups split the K loop) and
-// reduces the column groups through shared memory.
+// A plan is a list of phases (kernel launches); a phase is a list of units;
+// a unit is a chain of items run in order by one thread-block cluster of
+// `csize` CTAs (csize = 1: a single CTA).  The CTAs of a cluster split the
+// rows of every item; items flagged kPhaseEnd are followed by a cluster
+// barrier (barrier.cluster release/acquire), so a whole merge's dependent
+// GEMV chain runs in one launch on up to 16 SMs.  Each item streams its
+// matrix once with coalesced 16-byte loads (threads map to rows of the
+// column-major block, column groups split the K loop, shared-memory
+// reduction); vector traffic goes through L2 (ld/st .cg) so the cluster
+// barrier is the only ordering needed.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "device.cuh"
+#include "gemv_device.cuh"
 #include "internal.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace hpsb {
 
 namespace {
-constexpr int kThreads = 256;
+constexpr int kThreads = kGemvThreads;
 
-__device__ __forceinline__ double2 ld_vec(const double2* base, const int* idx, int j) {
-  if (idx) {
-    const int k = idx[j];
-    return k >= 0 ? base[k] : make_double2(0.0, 0.0);
-  }
-  return base[j];
-}
-
+template <bool kCluster>
 __global__ void __launch_bounds__(kThreads) vplan_kernel(const VItem* __restrict__ items,
                                                          const VUnit* __restrict__ units,
-                                                         int unit_begin) {
+                                                         int unit_begin, int csize) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* xs = reinterpret_cast<double2*>(smem_raw);
   __shared__ double2 red[kThreads];
-  const int tid = threadIdx.x;
-  const VUnit u = units[unit_begin + blockIdx.x];
+  const int crank = kCluster ? static_cast<int>(blockIdx.x % csize) : 0;
+  const VUnit u = units[unit_begin + (kCluster ? blockIdx.x / csize : blockIdx.x)];
   for (int it = u.first; it < u.first + u.count; ++it) {
     const VItem I = items[it];
-    for (int j = tid; j < I.cols; j += kThreads) xs[j] = ld_vec(I.x, I.xi, j);
-    __syncthreads();
-    for (int r0 = 0; r0 < I.rows; r0 += kThreads) {
-      const int rows = min(I.rows - r0, kThreads);
-      const int rpad = (rows + 31) & ~31;
-      const int groups = kThreads / rpad;
-      const int r = tid % rpad, g = tid / rpad;
-      double2 acc = make_double2(0.0, 0.0);
-      if (I.A && g < groups && r < rows) {
-        const double2* Ar = I.A + r0 + r;
-        const size_t lda = I.lda;
-        int j = g;
-        double2 a0, a1, a2, a3;
-        for (; j + 3 * groups < I.cols; j += 4 * groups) {
-          a0 = ldg2(Ar + j * lda);
-          a1 = ldg2(Ar + (j + groups) * lda);
-          a2 = ldg2(Ar + (j + 2 * groups) * lda);
-          a3 = ldg2(Ar + (j + 3 * groups) * lda);
-          acc = cfma(a0, xs[j], acc);
-          acc = cfma(a1, xs[j + groups], acc);
-          acc = cfma(a2, xs[j + 2 * groups], acc);
-          acc = cfma(a3, xs[j + 3 * groups], acc);
-        }
-        for (; j < I.cols; j += groups) acc = cfma(ldg2(Ar + j * lda), xs[j], acc);
-      }
-      red[tid] = acc;
-      __syncthreads();
-      if (tid < rows) {
-        double2 s = red[tid];
-        for (int gg = 1; gg < groups; ++gg) s = cadd(s, red[tid + gg * rpad]);
-        const int row = r0 + tid;
-        const int yk = I.yi ? I.yi[row] : row;
-        if (yk >= 0) {
-          double2 v = cscale(s, I.alpha);
-          if (I.gamma != 0.0) v = cadd(v, cscale(ld_vec(I.z, I.zi, row), I.gamma));
-          if (I.beta != 0.0) v = cadd(v, cscale(I.y[yk], I.beta));
-          I.y[yk] = v;
-        }
-      }
-      __syncthreads();
-    }
+    const int chunk = kCluster ? (((I.rows + csize - 1) / csize + 31) & ~31) : I.rows;
+    const int rb = crank * chunk, re = min(I.rows, rb + chunk);
+    if (rb < re) gemv_item_rows(I, rb, re, I.x, I.z, I.y, xs, red);
+    if (kCluster && (I.flags & VItem::kPhaseEnd)) cg::this_cluster().sync();
+    else __syncthreads();
   }
 }
 
@@ -92,9 +59,10 @@ __global__ void fill_kernel(double2* p, size_t n, double2 v) {
 }
 }  // namespace
 
-int VPlan::begin_phase() {
+int VPlan::begin_phase(int csize) {
   VPhase ph;
   ph.unit_begin = static_cast<int>(units.size());
+  ph.csize = csize;
   phases.push_back(ph);
   return static_cast<int>(phases.size()) - 1;
 }
@@ -135,12 +103,40 @@ void VPlan::run_phase(Context* ctx, int p) const {
   const VPhase& ph = phases[p];
   if (ph.unit_count == 0) return;
   const size_t smem = sizeof(double2) * std::max(ph.max_cols, 1);
-  if (smem > 48 * 1024)
-    HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
   KernelScope ks(ctx, name, ph.bytes, 0.0);
-  vplan_kernel<<<ph.unit_count, kThreads, smem, ctx->stream>>>(d_items.p, d_units.p,
-                                                                  ph.unit_begin);
+  if (ph.csize <= 1) {
+    if (smem > 48 * 1024)
+      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    vplan_kernel<false><<<ph.unit_count, kThreads, smem, ctx->stream>>>(d_items.p, d_units.p,
+                                                                         ph.unit_begin, 1);
+  } else {
+    static bool nonportable = false;
+    if (!nonportable) {
+      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      nonportable = true;
+    }
+    if (smem > 48 * 1024)
+      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ph.unit_count * ph.csize);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ph.csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HPSB_CUDA(cudaLaunchKernelEx(&cfg, vplan_kernel<true>, d_items.p, d_units.p, ph.unit_begin,
+                                 ph.csize));
+  }
   HPSB_LAUNCHED(ctx);
 }
 

@@ -1,0 +1,70 @@
+// Device side of the GEMV work items (shared by the plan kernel and the fused
+// coarse-solve kernel).
+#pragma once
+
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace hpsb {
+
+constexpr int kGemvThreads = 256;
+
+__device__ __forceinline__ double2 ld_vec(const double2* base, const int* idx, int j) {
+  if (idx) {
+    const int k = __ldg(idx + j);
+    return k >= 0 ? __ldcg(base + k) : make_double2(0.0, 0.0);
+  }
+  return __ldcg(base + j);
+}
+
+// Rows [rb, re) of item I:  y[yi] = beta y[yi] + gamma z[zi] + alpha A x[xi].
+// x / z / y may be overridden (coarse solve: the Krylov vector of the step).
+// xs: shared staging for x (>= I.cols), red: kGemvThreads shared doubles2.
+__device__ __forceinline__ void gemv_item_rows(const VItem& I, int rb, int re, const double2* x,
+                                               const double2* z, double2* y, double2* xs,
+                                               double2* red) {
+  const int tid = threadIdx.x;
+  if (I.A)
+    for (int j = tid; j < I.cols; j += kGemvThreads) xs[j] = ld_vec(x, I.xi, j);
+  __syncthreads();
+  for (int r0 = rb; r0 < re; r0 += kGemvThreads) {
+    const int rows = min(re - r0, kGemvThreads);
+    const int rpad = (rows + 31) & ~31;
+    const int groups = kGemvThreads / rpad;
+    const int r = tid % rpad, g = tid / rpad;
+    double2 acc = make_double2(0.0, 0.0);
+    if (I.A && g < groups && r < rows) {
+      const double2* Ar = I.A + r0 + r;
+      const size_t lda = I.lda;
+      int j = g;
+      for (; j + 3 * groups < I.cols; j += 4 * groups) {
+        const double2 a0 = ldg2(Ar + j * lda);
+        const double2 a1 = ldg2(Ar + (j + groups) * lda);
+        const double2 a2 = ldg2(Ar + (j + 2 * groups) * lda);
+        const double2 a3 = ldg2(Ar + (j + 3 * groups) * lda);
+        acc = cfma(a0, xs[j], acc);
+        acc = cfma(a1, xs[j + groups], acc);
+        acc = cfma(a2, xs[j + 2 * groups], acc);
+        acc = cfma(a3, xs[j + 3 * groups], acc);
+      }
+      for (; j < I.cols; j += groups) acc = cfma(ldg2(Ar + j * lda), xs[j], acc);
+    }
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < rows) {
+      double2 s = red[tid];
+      for (int gg = 1; gg < groups; ++gg) s = cadd(s, red[tid + gg * rpad]);
+      const int row = r0 + tid;
+      const int yk = I.yi ? __ldg(I.yi + row) : row;
+      if (yk >= 0) {
+        double2 v = cscale(s, I.alpha);
+        if (I.gamma != 0.0) v = cadd(v, cscale(ld_vec(z, I.zi, row), I.gamma));
+        if (I.beta != 0.0) v = cadd(v, cscale(__ldcg(y + yk), I.beta));
+        __stcg(y + yk, v);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace hpsb

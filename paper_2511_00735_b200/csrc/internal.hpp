@@ -158,8 +158,9 @@ struct VItem {
   const int* xi;
   const int* zi;
   const int* yi;
-  int lda, rows, cols, pad;
+  int lda, rows, cols, flags;
   double alpha, beta, gamma, pad2;
+  static constexpr int kPhaseEnd = 1;  // cluster barrier after this item
 };
 // A unit is a chain of items executed in order by one CTA.
 struct VUnit {
@@ -169,6 +170,7 @@ struct VUnit {
 struct VPhase {
   int unit_begin = 0, unit_count = 0;
   int max_cols = 0;
+  int csize = 1;  // CTAs per unit (thread-block cluster)
   double bytes = 0;
 };
 struct VPlan {
@@ -179,8 +181,8 @@ struct VPlan {
   DevBuf<VUnit> d_units;
   int64_t bytes_per_run = 0;  // algorithmic operator bytes streamed per run
   const char* name = "vplan";
-  // Start a new phase; returns its index.
-  int begin_phase();
+  // Start a new phase (one launch, csize CTAs per unit); returns its index.
+  int begin_phase(int csize = 1);
   void add_unit(const std::vector<VItem>& chain);
   // Adds A (rows x cols) split into row blocks as independent units.
   void add_split(const VItem& it, int row_block);

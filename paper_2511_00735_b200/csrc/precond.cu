@@ -23,7 +23,10 @@
 #include <algorithm>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "device.cuh"
+#include "gemv_device.cuh"
 #include "hierarchy.hpp"
 
 namespace hpsb {
@@ -39,10 +42,129 @@ struct Precond {
   DevBuf<double2> V, cv, cw, Hm, gv, rs;
   DevBuf<double> rc, state;
   int64_t bytes_per_apply = 0;
+  // fused coarse solve (one cluster launch)
+  bool coarse_fused = false;
+  DevBuf<VItem> coarse_items;
+  int coarse_nitems = 0, coarse_max_cols = 0;
 };
+
+constexpr int kMaxCoarseIters = 30;
 
 namespace {
 constexpr int kCoarseThreads = 1024;
+namespace cg = cooperative_groups;
+__device__ void make_givens(double2 a, double2 b, double& c, double2& s);
+__device__ void apply_givens(double c, double2 s, double2& a, double2& b);
+
+// gmres_fixed_steps (krylov.cpp:194-201, driver 45-178 with fixed_steps) on
+// the coarse system in ONE launch: a cluster of CTAs owns contiguous slices
+// of the Krylov vectors; the matvec rows are split across the cluster; dot
+// products reduce through distributed shared memory; the tiny Hessenberg /
+// Givens state is kept (identically) by every CTA, so no broadcast is needed.
+__global__ void __launch_bounds__(kGemvThreads) coarse_fused_kernel(
+    const VItem* __restrict__ items, int nitems, int64_t n, int ci, double2* V, double2* w,
+    const double2* rd, double2* outd, int max_cols) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int cs = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* xs = reinterpret_cast<double2*>(smem_raw);
+  __shared__ double2 red[kGemvThreads];
+  __shared__ double2 part[kMaxCoarseIters + 2];
+  __shared__ double2 Hs[(kMaxCoarseIters + 1) * kMaxCoarseIters];
+  __shared__ double2 gs[kMaxCoarseIters + 1], rs[kMaxCoarseIters], ys[kMaxCoarseIters];
+  __shared__ double rcs[kMaxCoarseIters];
+  const int64_t s0 = n * rank / cs, s1 = n * (rank + 1) / cs;
+  const int ldh = ci + 1;
+
+  auto cluster_sum = [&](double2 v, int slot) {
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int q = 0; q < kGemvThreads / 32; ++q) t = cadd(t, red[q]);
+      part[slot] = t;
+    }
+    cl.sync();
+    double2 t = make_double2(0.0, 0.0);
+    for (int q = 0; q < cs; ++q) t = cadd(t, *cl.map_shared_rank(&part[slot], q));
+    return t;
+  };
+
+  double2 loc = make_double2(0.0, 0.0);
+  for (int64_t k = s0 + tid; k < s1; k += kGemvThreads) loc.x += cabs2(__ldcg(rd + k));
+  const double beta = sqrt(cluster_sum(loc, 0).x);
+  if (beta == 0.0) {
+    for (int64_t k = s0 + tid; k < s1; k += kGemvThreads) outd[k] = make_double2(0.0, 0.0);
+    cl.sync();  // no CTA may exit while others still read its shared memory
+    return;
+  }
+  for (int64_t k = s0 + tid; k < s1; k += kGemvThreads) {
+    const double2 v = __ldcg(rd + k);
+    __stcg(V + k, make_double2(v.x / beta, v.y / beta));
+  }
+  if (tid <= ci) gs[tid] = make_double2(tid == 0 ? beta : 0.0, 0.0);
+  cl.sync();
+  int jused = 0;
+  for (int j = 0; j < ci; ++j) {
+    const double2* Vj = V + j * n;
+    for (int it = 0; it < nitems; ++it) {
+      const VItem I = items[it];
+      const int chunk = (((I.rows + cs - 1) / cs + 31) & ~31);
+      const int rb = rank * chunk, re = min(I.rows, rb + chunk);
+      if (rb < re) gemv_item_rows(I, rb, re, Vj, Vj, w, xs, red);
+      __syncthreads();
+    }
+    cl.sync();
+    for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+      const double2* Vi = V + i * n;
+      double2 d = make_double2(0.0, 0.0);
+      for (int64_t k = s0 + tid; k < s1; k += kGemvThreads)
+        d = cfma_conj(__ldcg(Vi + k), __ldcg(w + k), d);
+      const double2 h = cluster_sum(d, 1 + i);
+      for (int64_t k = s0 + tid; k < s1; k += kGemvThreads)
+        __stcg(w + k, csub(__ldcg(w + k), cmul(h, __ldcg(Vi + k))));
+      if (tid == 0) Hs[i + j * ldh] = h;
+    }
+    double2 nn = make_double2(0.0, 0.0);
+    for (int64_t k = s0 + tid; k < s1; k += kGemvThreads) nn.x += cabs2(__ldcg(w + k));
+    const double hnext = sqrt(cluster_sum(nn, j + 2).x);
+    if (tid == 0) {
+      Hs[j + 1 + j * ldh] = make_double2(hnext, 0.0);
+      for (int i = 0; i < j; ++i) apply_givens(rcs[i], rs[i], Hs[i + j * ldh], Hs[i + 1 + j * ldh]);
+      double c;
+      double2 s;
+      make_givens(Hs[j + j * ldh], Hs[j + 1 + j * ldh], c, s);
+      rcs[j] = c, rs[j] = s;
+      apply_givens(c, s, Hs[j + j * ldh], Hs[j + 1 + j * ldh]);
+      apply_givens(c, s, gs[j], gs[j + 1]);
+    }
+    __syncthreads();
+    jused = j + 1;
+    if (hnext <= 1e-14 * beta) break;  // happy breakdown
+    double2* Vn = V + (j + 1) * n;
+    for (int64_t k = s0 + tid; k < s1; k += kGemvThreads) {
+      const double2 v = __ldcg(w + k);
+      __stcg(Vn + k, make_double2(v.x / hnext, v.y / hnext));
+    }
+    cl.sync();
+  }
+  cl.sync();  // all DSMEM reads of this step are done before any CTA can exit
+  if (tid == 0)
+    for (int i = jused - 1; i >= 0; --i) {
+      double2 s = gs[i];
+      for (int k = i + 1; k < jused; ++k) s = csub(s, cmul(Hs[i + k * ldh], ys[k]));
+      ys[i] = cdiv(s, Hs[i + i * ldh]);
+    }
+  __syncthreads();
+  for (int64_t k = s0 + tid; k < s1; k += kGemvThreads) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < jused; ++i) acc = cfma(ys[i], __ldcg(V + i * n + k), acc);
+    outd[k] = acc;
+  }
+}
 
 __device__ double block_sum(double v, double* sh) {
   v = warp_sum(v);
@@ -240,7 +362,23 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   auto build_level = [&](int l, bool downward) {
     const LevelOps& L = *h->levels[l - 1];
     const int ng = static_cast<int>(L.merges.size());
-    const bool chain = ng >= 2 * sms;
+    // Execution mode of the level (one launch unless the maps are huge):
+    //  - one CTA per merge when there are enough merges to fill the GPU;
+    //  - a cluster of up to 16 CTAs per merge otherwise (row-split items,
+    //    cluster barriers between the dependent phases);
+    //  - separate row-split launches per phase when a few merges carry
+    //    tens of MB each (top levels of the large configs), so every SM streams.
+    double bytes = 0;
+    int smin = 1 << 30;
+    for (const auto& mr : L.merges) {
+      bytes += 16.0 * (3.0 * mr.s * mr.s + static_cast<double>(mr.s) * (mr.p1 + mr.p2));
+      smin = std::min(smin, mr.s);
+    }
+    const double per_merge = bytes / std::max(ng, 1);
+    int csize = 1;
+    while (csize < 16 && csize * ng < 2 * sms && 16 * csize * 2 <= smin) csize *= 2;
+    const bool split = per_merge > 8e6 && ng * 16 < sms;
+    const bool chain = !split;
     int total_rows = 0;
     for (const auto& mr : L.merges) total_rows += mr.s + mr.p1 + mr.p2;
     int rb = ((total_rows / (2 * sms)) + 31) & ~31;
@@ -284,15 +422,17 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
         st[3].push_back(item(T1ss, P1, s, s, t1, nullptr, t2, nullptr, out, in2s, 1.0, 1.0, -1.0));
         st[3].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, t1, nullptr, out, in1s, 0.0, 1.0, -1.0));
       }
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 4; ++k) {
+        if (!st[k].empty()) st[k].back().flags |= VItem::kPhaseEnd;
         for (auto& it : st[k]) {
           if (chain) chains[gi].push_back(it);
           else stages[k].push_back(it);
         }
+      }
     }
     VPlan& plan = downward ? p->down : p->up;
     if (chain) {
-      plan.begin_phase();
+      plan.begin_phase(csize);
       for (auto& c : chains) plan.add_unit(c);
     } else {
       for (auto& stg : stages) {
@@ -345,6 +485,22 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   }
   p->coarse_mv.name = "coarse_matvec";
   p->coarse_mv.finalize(ctx->stream);
+  // Fused single-launch coarse solve when the coarse maps are small enough
+  // for one 16-CTA cluster to stream them quickly.
+  {
+    std::vector<VItem> whole;
+    for (size_t k = 0; k < C.children.size(); ++k) {
+      const ChildBox& c = C.children[k];
+      const int* ci_in = p->coarse_idx.p + in_at[k];
+      const int* ci_out = p->coarse_idx.p + out_at[k];
+      whole.push_back(item(C.tperm.p + c.t_off, c.P, c.P, c.P, nullptr, ci_in, nullptr, ci_out,
+                           nullptr, ci_out, 1.0, 0.0, 1.0));
+      p->coarse_max_cols = std::max(p->coarse_max_cols, c.P);
+    }
+    p->coarse_fused = p->coarse_mv.bytes_per_run <= (64ll << 20) && ci <= kMaxCoarseIters;
+    p->coarse_items.upload(whole, ctx->stream);
+    p->coarse_nitems = static_cast<int>(whole.size());
+  }
   p->bytes_per_apply = p->down.bytes_per_run + p->up.bytes_per_run +
                        static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run;
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -358,6 +514,38 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   zcopy(ctx, p->r.p, v_dev, p->dim);
   p->down.run(ctx);
   const int ci = p->cfg.coarse_iters;
+  if (p->coarse_fused) {
+    static bool attr = false;
+    if (!attr) {
+      HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attr = true;
+    }
+    const size_t smem = sizeof(double2) * std::max(p->coarse_max_cols, 1);
+    if (smem > 16 * 1024)
+      HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(16);
+    lc.blockDim = dim3(kGemvThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    KernelScope ks(ctx, "coarse_fused", static_cast<double>(ci) * p->coarse_mv.bytes_per_run, 0.0);
+    HPSB_CUDA(cudaLaunchKernelEx(&lc, coarse_fused_kernel,
+                                 static_cast<const VItem*>(p->coarse_items.p), p->coarse_nitems,
+                                 p->dim_d, ci, p->V.p, p->cw.p,
+                                 static_cast<const double2*>(p->r.p + p->off_d),
+                                 p->out.p + p->off_d, p->coarse_max_cols));
+    HPSB_LAUNCHED(ctx);
+  } else {
   {
   KernelScope ks(ctx, "coarse_gmres", 32.0 * p->dim_d, 0.0);
   coarse_init_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(p->r.p + p->off_d, p->dim_d, p->V.p,
@@ -378,6 +566,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
                                                               p->gv.p, p->state.p,
                                                               p->out.p + p->off_d);
   HPSB_LAUNCHED(ctx);
+  }
   }
   p->up.run(ctx);
   zcopy(ctx, z_dev, p->out.p, p->dim);
