@@ -98,6 +98,13 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     uint64_t threshold = UINT64_MAX;
     HPSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     hpsb::alloc_stream() = ctx->c.stream;
+    auto& st = hpsb::staging();
+    if (!st.base) {
+      st.size = size_t(64) << 20;
+      HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.base), st.size));
+    }
+    st.stream = ctx->c.stream;
+    st.head = 0;
     *out = ctx.release();
     return HPSB_OK;
   });
@@ -108,6 +115,7 @@ hpsb_status hpsb_context_destroy(hpsb_context ctx) {
     if (!ctx) return HPSB_OK;
     cudaStreamSynchronize(ctx->c.stream);
     if (hpsb::alloc_stream() == ctx->c.stream) hpsb::alloc_stream() = nullptr;
+    if (hpsb::staging().stream == ctx->c.stream) hpsb::staging().stream = nullptr;
     for (auto& e : ctx->c.ev) cudaEventDestroy(e);
     for (auto& e : ctx->c.timer)
       if (e) cudaEventDestroy(e);

@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "device.cuh"
 #include "gemv_device.cuh"
@@ -103,7 +104,7 @@ void VPlan::run_phase(Context* ctx, int p) const {
   const VPhase& ph = phases[p];
   if (ph.unit_count == 0) return;
   const size_t smem = sizeof(double2) * std::max(ph.max_cols, 1);
-  KernelScope ks(ctx, name, ph.bytes, 0.0);
+  KernelScope ks(ctx, ph.label.empty() ? name : ph.label.c_str(), ph.bytes, 0.0);
   if (ph.csize <= 1) {
     if (smem > 48 * 1024)
       HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<false>,
@@ -182,6 +183,22 @@ void Context::collect() {
     event_pool.push_back(r.b);
   }
   pending.clear();
+}
+
+void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  Staging& st = staging();
+  if (!st.base || st.stream != s || bytes > st.size / 2) {
+    HPSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    return;
+  }
+  const size_t need = (bytes + 255) & ~size_t(255);
+  if (st.head + need > st.size) {
+    HPSB_CUDA(cudaStreamSynchronize(s));  // all earlier staged copies have completed
+    st.head = 0;
+  }
+  std::memcpy(st.base + st.head, src, bytes);
+  HPSB_CUDA(cudaMemcpyAsync(dst, st.base + st.head, bytes, cudaMemcpyHostToDevice, s));
+  st.head += need;
 }
 
 void zfill(Context* ctx, double2* p, std::size_t n, double2 v) {

@@ -19,24 +19,54 @@ __device__ __forceinline__ double2 ld_vec(const double2* base, const int* idx, i
 
 // Rows [rb, re) of item I:  y[yi] = beta y[yi] + gamma z[zi] + alpha A x[xi].
 // x / z / y may be overridden (coarse solve: the Krylov vector of the step).
-// xs: shared staging for x (>= I.cols), red: kGemvThreads shared doubles2.
+// xs: shared staging for x (>= I.cols), red: kGemvThreads shared double2.
+// Latency matters as much as bandwidth here (a level is a chain of dependent
+// items), so everything that does not depend on x -- the first four A
+// columns of each thread, the output index and the z / y operands of the
+// first row block -- is loaded before the barrier that publishes x.
 __device__ __forceinline__ void gemv_item_rows(const VItem& I, int rb, int re, const double2* x,
                                                const double2* z, double2* y, double2* xs,
                                                double2* red) {
   const int tid = threadIdx.x;
   if (I.A)
     for (int j = tid; j < I.cols; j += kGemvThreads) xs[j] = ld_vec(x, I.xi, j);
-  __syncthreads();
+  bool first = true;
   for (int r0 = rb; r0 < re; r0 += kGemvThreads) {
     const int rows = min(re - r0, kGemvThreads);
-    const int rpad = (rows + 31) & ~31;
+    // 8 / 16-row blocks keep every lane busy (a warp then reads 4 / 2 column
+    // segments of 128 / 256 B per load) for short row blocks.
+    const int rpad = rows <= 8 ? 8 : rows <= 16 ? 16 : (rows + 31) & ~31;
     const int groups = kGemvThreads / rpad;
     const int r = tid % rpad, g = tid / rpad;
+    const bool active = I.A && g < groups && r < rows;
+    const double2* Ar = I.A ? I.A + r0 + r : nullptr;
+    const size_t lda = I.lda;
+    double2 a_pre[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = g + q * groups;
+      a_pre[q] = (active && j < I.cols) ? ldg2(Ar + j * lda) : make_double2(0.0, 0.0);
+    }
+    int yk = -1;
+    double2 zv = make_double2(0.0, 0.0), yv = make_double2(0.0, 0.0);
+    if (tid < rows) {
+      const int row = r0 + tid;
+      yk = I.yi ? __ldg(I.yi + row) : row;
+      if (yk >= 0) {
+        if (I.gamma != 0.0) zv = ld_vec(z, I.zi, row);
+        if (I.beta != 0.0) yv = __ldcg(y + yk);
+      }
+    }
+    if (first) __syncthreads();  // xs published
+    first = false;
     double2 acc = make_double2(0.0, 0.0);
-    if (I.A && g < groups && r < rows) {
-      const double2* Ar = I.A + r0 + r;
-      const size_t lda = I.lda;
-      int j = g;
+    if (active) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = g + q * groups;
+        if (j < I.cols) acc = cfma(a_pre[q], xs[j], acc);
+      }
+      int j = g + 4 * groups;
       for (; j + 3 * groups < I.cols; j += 4 * groups) {
         const double2 a0 = ldg2(Ar + j * lda);
         const double2 a1 = ldg2(Ar + (j + groups) * lda);
@@ -51,20 +81,17 @@ __device__ __forceinline__ void gemv_item_rows(const VItem& I, int rb, int re, c
     }
     red[tid] = acc;
     __syncthreads();
-    if (tid < rows) {
+    if (tid < rows && yk >= 0) {
       double2 s = red[tid];
       for (int gg = 1; gg < groups; ++gg) s = cadd(s, red[tid + gg * rpad]);
-      const int row = r0 + tid;
-      const int yk = I.yi ? __ldg(I.yi + row) : row;
-      if (yk >= 0) {
-        double2 v = cscale(s, I.alpha);
-        if (I.gamma != 0.0) v = cadd(v, cscale(ld_vec(z, I.zi, row), I.gamma));
-        if (I.beta != 0.0) v = cadd(v, cscale(__ldcg(y + yk), I.beta));
-        __stcg(y + yk, v);
-      }
+      double2 v = cscale(s, I.alpha);
+      if (I.gamma != 0.0) v = cadd(v, cscale(zv, I.gamma));
+      if (I.beta != 0.0) v = cadd(v, cscale(yv, I.beta));
+      __stcg(y + yk, v);
     }
     __syncthreads();
   }
+  if (first) __syncthreads();
 }
 
 }  // namespace hpsb

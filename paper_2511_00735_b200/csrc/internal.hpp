@@ -45,6 +45,22 @@ inline cudaStream_t& alloc_stream() {
   return s;
 }
 
+// Pinned staging ring for host->device descriptor uploads: a cudaMemcpyAsync
+// from pageable memory waits for the stream to drain, which would serialise
+// every batched launch of the merge stage with the host.  Uploads are copied
+// into this ring and issued from pinned memory; the ring is recycled after a
+// stream synchronisation when it wraps.
+struct Staging {
+  unsigned char* base = nullptr;
+  size_t size = 0, head = 0;
+  cudaStream_t stream = nullptr;
+};
+inline Staging& staging() {
+  static Staging s;
+  return s;
+}
+void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -83,7 +99,7 @@ struct DevBuf {
   std::size_t bytes() const { return n * sizeof(T); }
   void upload(const std::vector<T>& v, cudaStream_t s) {
     if (v.size() != n) alloc(v.size());
-    if (n) HPSB_CUDA(cudaMemcpyAsync(p, v.data(), bytes(), cudaMemcpyHostToDevice, s));
+    if (n) staged_upload(p, v.data(), bytes(), s);
   }
 };
 
@@ -172,6 +188,7 @@ struct VPhase {
   int max_cols = 0;
   int csize = 1;  // CTAs per unit (thread-block cluster)
   double bytes = 0;
+  std::string label;  // profiling name (defaults to the plan's name)
 };
 struct VPlan {
   std::vector<VItem> items;

@@ -45,7 +45,7 @@ struct Precond {
   // fused coarse solve (one cluster launch)
   bool coarse_fused = false;
   DevBuf<VItem> coarse_items;
-  int coarse_nitems = 0, coarse_max_cols = 0;
+  int coarse_nitems = 0, coarse_max_cols = 0, coarse_csize = 16;
 };
 
 constexpr int kMaxCoarseIters = 30;
@@ -313,6 +313,15 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_finish_kernel(int64_t n
   }
 }
 
+// Row-block size for a split phase: enough units for ~2 CTAs per SM,
+// 8 / 16 / multiple-of-32 rows (the shapes the GEMV item kernel maps well).
+int split_rows(int total_rows, int sms) {
+  const int want = (total_rows + 2 * sms - 1) / (2 * sms);
+  if (want <= 8) return 8;
+  if (want <= 16) return 16;
+  return std::min(256, (want + 31) & ~31);
+}
+
 VItem item(const double2* A, int lda, int rows, int cols, const double2* x, const int* xi,
            const double2* z, const int* zi, double2* y, const int* yi, double alpha, double beta,
            double gamma) {
@@ -431,13 +440,17 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       }
     }
     VPlan& plan = downward ? p->down : p->up;
+    const std::string label = std::string(downward ? "vcycle_down" : "vcycle_up") +
+                              (std::getenv("HPSB_PROFILE_LEVELS") ? "_L" + std::to_string(l) : "");
     if (chain) {
-      plan.begin_phase(csize);
+      plan.phases[plan.begin_phase(csize)].label = label;
       for (auto& c : chains) plan.add_unit(c);
     } else {
       for (auto& stg : stages) {
-        plan.begin_phase();
-        for (auto& it : stg) plan.add_split(it, rb);
+        plan.phases[plan.begin_phase()].label = label;
+        int rows = 0;
+        for (auto& it : stg) rows += it.rows;
+        for (auto& it : stg) plan.add_split(it, split_rows(rows, sms));
       }
     }
   };
@@ -472,8 +485,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   p->coarse_idx.upload(lidx, ctx->stream);
   int crows = 0;
   for (const ChildBox& c : C.children) crows += c.P;
-  int crb = ((crows / (2 * sms)) + 31) & ~31;
-  crb = std::max(32, std::min(256, crb));
+  const int crb = split_rows(crows, sms);
   p->coarse_mv.begin_phase();
   for (size_t k = 0; k < C.children.size(); ++k) {
     const ChildBox& c = C.children[k];
@@ -497,7 +509,13 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
                            nullptr, ci_out, 1.0, 0.0, 1.0));
       p->coarse_max_cols = std::max(p->coarse_max_cols, c.P);
     }
-    p->coarse_fused = p->coarse_mv.bytes_per_run <= (64ll << 20) && ci <= kMaxCoarseIters;
+    // One cluster streams ~0.3 MB per CTA per matvec within a few us; larger
+    // coarse systems need the whole GPU for their matvecs (split launches).
+    p->coarse_fused = p->coarse_mv.bytes_per_run <= (4ll << 20) && ci <= kMaxCoarseIters;
+    p->coarse_csize = 1;
+    while (p->coarse_csize < 16 &&
+           p->coarse_mv.bytes_per_run > p->coarse_csize * static_cast<int64_t>(256 << 10))
+      p->coarse_csize *= 2;
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
   }
@@ -527,13 +545,13 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(16);
+    lc.gridDim = dim3(p->coarse_csize);
     lc.blockDim = dim3(kGemvThreads);
     lc.dynamicSmemBytes = smem;
     lc.stream = ctx->stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.x = p->coarse_csize;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     lc.attrs = at;
