@@ -34,10 +34,21 @@ namespace hpsb {
 namespace {
 constexpr int kThreads = kGemvThreads;
 
+// Pointer rebinding: vectors a plan was built on (bind.from[k]) are replaced
+// at run time by the caller's buffers (bind.to[k]), so no copies are needed
+// around a plan run.
+struct Rebind {
+  const double2* from[2];
+  double2* to[2];
+};
+__device__ __forceinline__ const double2* rebind(const double2* p, const Rebind& b) {
+  return p == b.from[0] ? b.to[0] : p == b.from[1] ? b.to[1] : p;
+}
+
 template <bool kCluster>
 __global__ void __launch_bounds__(kThreads) vplan_kernel(const VItem* __restrict__ items,
                                                          const VUnit* __restrict__ units,
-                                                         int unit_begin, int csize) {
+                                                         int unit_begin, int csize, Rebind bind) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* xs = reinterpret_cast<double2*>(smem_raw);
   __shared__ double2 red[kThreads];
@@ -47,7 +58,9 @@ __global__ void __launch_bounds__(kThreads) vplan_kernel(const VItem* __restrict
     const VItem I = items[it];
     const int chunk = kCluster ? (((I.rows + csize - 1) / csize + 31) & ~31) : I.rows;
     const int rb = crank * chunk, re = min(I.rows, rb + chunk);
-    if (rb < re) gemv_item_rows(I, rb, re, I.x, I.z, I.y, xs, red);
+    if (rb < re)
+      gemv_item_rows(I, rb, re, rebind(I.x, bind), rebind(I.z, bind),
+                     const_cast<double2*>(rebind(I.y, bind)), xs, red);
     if (kCluster && (I.flags & VItem::kPhaseEnd)) cg::this_cluster().sync();
     else __syncthreads();
   }
@@ -100,9 +113,11 @@ void VPlan::finalize(cudaStream_t s) {
   d_units.upload(units, s);
 }
 
-void VPlan::run_phase(Context* ctx, int p) const {
+void VPlan::run_phase(Context* ctx, int p, const double2* from0, double2* to0,
+                      const double2* from1, double2* to1) const {
   const VPhase& ph = phases[p];
   if (ph.unit_count == 0) return;
+  Rebind bind{{from0, from1}, {to0, to1}};
   const size_t smem = sizeof(double2) * std::max(ph.max_cols, 1);
   KernelScope ks(ctx, ph.label.empty() ? name : ph.label.c_str(), ph.bytes, 0.0);
   if (ph.csize <= 1) {
@@ -111,7 +126,7 @@ void VPlan::run_phase(Context* ctx, int p) const {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
     vplan_kernel<false><<<ph.unit_count, kThreads, smem, ctx->stream>>>(d_items.p, d_units.p,
-                                                                         ph.unit_begin, 1);
+                                                                         ph.unit_begin, 1, bind);
   } else {
     static bool nonportable = false;
     if (!nonportable) {
@@ -136,13 +151,15 @@ void VPlan::run_phase(Context* ctx, int p) const {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     HPSB_CUDA(cudaLaunchKernelEx(&cfg, vplan_kernel<true>, d_items.p, d_units.p, ph.unit_begin,
-                                 ph.csize));
+                                 ph.csize, bind));
   }
   HPSB_LAUNCHED(ctx);
 }
 
-void VPlan::run(Context* ctx) const {
-  for (int p = 0; p < static_cast<int>(phases.size()); ++p) run_phase(ctx, p);
+void VPlan::run(Context* ctx, const double2* from0, double2* to0, const double2* from1,
+                double2* to1) const {
+  for (int p = 0; p < static_cast<int>(phases.size()); ++p)
+    run_phase(ctx, p, from0, to0, from1, to1);
 }
 
 KernelScope::KernelScope(Context* ctx, const char* name, double bytes, double flops) : c(ctx) {

@@ -204,8 +204,11 @@ struct VPlan {
   // Adds A (rows x cols) split into row blocks as independent units.
   void add_split(const VItem& it, int row_block);
   void finalize(cudaStream_t s);
-  void run(Context* ctx) const;
-  void run_phase(Context* ctx, int p) const;
+  // Run all phases; vectors `from*` the plan was built on are replaced by `to*`.
+  void run(Context* ctx, const double2* from0 = nullptr, double2* to0 = nullptr,
+           const double2* from1 = nullptr, double2* to1 = nullptr) const;
+  void run_phase(Context* ctx, int p, const double2* from0 = nullptr, double2* to0 = nullptr,
+                 const double2* from1 = nullptr, double2* to1 = nullptr) const;
 };
 
 // ---------------------------------------------------------------- objects

@@ -57,6 +57,45 @@ __global__ void __launch_bounds__(kThreads) dots_kernel(const double2* __restric
   }
 }
 
+// out[0..ncols) = V^H w in one launch: block b reduces rows
+// [b*chunk, (b+1)*chunk) into partial[b*ncols + i]; the last block to finish
+// (atomic ticket) sums the partials in fixed block order (deterministic).
+__global__ void __launch_bounds__(kThreads) dots_fused_kernel(
+    const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ w,
+    int64_t n, int64_t chunk, double2* partial, double2* out, unsigned* ticket) {
+  __shared__ double2 sh[kThreads / 32][104];
+  __shared__ bool last;
+  const int64_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = 0; i < ncols; ++i) {
+    const double2* Vi = V + i * ld;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t k = r0 + threadIdx.x; k < r1; k += kThreads)
+      acc = cfma_conj(ldg2(Vi + k), __ldcg(w + k), acc);
+    acc.x = warp_sum(acc.x);
+    acc.y = warp_sum(acc.y);
+    if (lane == 0) sh[warp][i] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ncols; i += kThreads) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = 0; q < kThreads / 32; ++q) s = cadd(s, sh[q][i]);
+    __stcg(partial + static_cast<int64_t>(blockIdx.x) * ncols + i, s);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < ncols; i += kThreads) {
+    double2 s = make_double2(0.0, 0.0);
+    for (unsigned b = 0; b < gridDim.x; ++b) s = cadd(s, __ldcg(partial + b * ncols + i));
+    out[i] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+}
+
 // out[i] = sum_b partial[b * ncols + i]  (fixed order: deterministic)
 __global__ void reduce_kernel(const double2* __restrict__ partial, int nblocks, int ncols,
                               double2* out) {
@@ -133,22 +172,23 @@ struct Work {
   Context* ctx;
   int64_t n;
   int blocks;
+  int64_t chunk;
   DevBuf<double2> partial, hdev;
+  DevBuf<unsigned> ticket;
   explicit Work(Context* c, int64_t dim, int maxcols) : ctx(c), n(dim) {
-    blocks = static_cast<int>((dim + kRowsPerBlock - 1) / kRowsPerBlock);
+    blocks = static_cast<int>(std::min<int64_t>((dim + kThreads - 1) / kThreads, 2 * c->num_sms));
+    chunk = (dim + blocks - 1) / blocks;
     partial.alloc(static_cast<size_t>(blocks) * maxcols);
     hdev.alloc(3 * static_cast<size_t>(maxcols) + 4);
+    ticket.alloc(1);
+    HPSB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
   }
   int grid() const { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * ctx->num_sms)); }
   // out[0..ncols) = V^H w
   void dots(const double2* V, int ncols, const double2* w, double2* out) {
-    {
-      KernelScope ks(ctx, "gmres_dots", 16.0 * n * (ncols + 1), 8.0 * n * ncols);
-      dots_kernel<<<blocks, kThreads, 0, ctx->stream>>>(V, n, ncols, w, n, partial.p);
-      HPSB_LAUNCHED(ctx);
-    }
-    KernelScope ks(ctx, "gmres_reduce", 16.0 * blocks * ncols, 0.0);
-    reduce_kernel<<<ncols, 256, 0, ctx->stream>>>(partial.p, blocks, ncols, out);
+    KernelScope ks(ctx, "gmres_dots", 16.0 * n * (ncols + 1), 8.0 * n * ncols);
+    dots_fused_kernel<<<blocks, kThreads, 0, ctx->stream>>>(V, n, ncols, w, n, chunk, partial.p,
+                                                            out, ticket.p);
     HPSB_LAUNCHED(ctx);
   }
   void axpy(const double2* V, int ncols, const double2* h, double sign, double2* w) {

@@ -530,7 +530,8 @@ void destroy_precond(Precond* p) { delete p; }
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   Context* ctx = p->ctx;
   zcopy(ctx, p->r.p, v_dev, p->dim);
-  p->down.run(ctx);
+  // `out` of the plans is bound to the caller's z: no copy-out.
+  p->down.run(ctx, p->out.p, z_dev);
   const int ci = p->cfg.coarse_iters;
   if (p->coarse_fused) {
     static bool attr = false;
@@ -561,7 +562,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
                                  static_cast<const VItem*>(p->coarse_items.p), p->coarse_nitems,
                                  p->dim_d, ci, p->V.p, p->cw.p,
                                  static_cast<const double2*>(p->r.p + p->off_d),
-                                 p->out.p + p->off_d, p->coarse_max_cols));
+                                 z_dev + p->off_d, p->coarse_max_cols));
     HPSB_LAUNCHED(ctx);
   } else {
   {
@@ -582,12 +583,11 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (ci + 1), 0.0);
   coarse_finish_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(p->dim_d, ci, p->V.p, p->Hm.p,
                                                               p->gv.p, p->state.p,
-                                                              p->out.p + p->off_d);
+                                                              z_dev + p->off_d);
   HPSB_LAUNCHED(ctx);
   }
   }
-  p->up.run(ctx);
-  zcopy(ctx, z_dev, p->out.p, p->dim);
+  p->up.run(ctx, p->out.p, z_dev);
 }
 
 int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }

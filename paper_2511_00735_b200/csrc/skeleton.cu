@@ -98,10 +98,8 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
 }
 
 void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev) {
-  Context* ctx = sk->ctx;
-  if (x_dev != sk->x_buf.p) zcopy(ctx, sk->x_buf.p, x_dev, sk->dim);
-  sk->apply_plan.run(ctx);
-  if (y_dev != sk->y_buf.p) zcopy(ctx, y_dev, sk->y_buf.p, sk->dim);
+  // The plan was built on x_buf / y_buf; bind the caller's vectors instead.
+  sk->apply_plan.run(sk->ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
 }
 
 }  // namespace hpsb
