@@ -176,20 +176,28 @@ struct Work {
   DevBuf<double2> partial, hdev;
   DevBuf<unsigned> ticket;
   explicit Work(Context* c, int64_t dim, int maxcols) : ctx(c), n(dim) {
-    blocks = static_cast<int>(std::min<int64_t>((dim + kThreads - 1) / kThreads, 2 * c->num_sms));
-    chunk = (dim + blocks - 1) / blocks;
+    blocks = static_cast<int>((dim + kRowsPerBlock - 1) / kRowsPerBlock);
+    chunk = kRowsPerBlock;
     partial.alloc(static_cast<size_t>(blocks) * maxcols);
     hdev.alloc(3 * static_cast<size_t>(maxcols) + 4);
     ticket.alloc(1);
     HPSB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
   }
   int grid() const { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * ctx->num_sms)); }
-  // out[0..ncols) = V^H w
+  // out[0..ncols) = V^H w.  Short vectors: one launch (last-block reduction);
+  // long vectors: many row blocks + a column-parallel reduce launch.
   void dots(const double2* V, int ncols, const double2* w, double2* out) {
     KernelScope ks(ctx, "gmres_dots", 16.0 * n * (ncols + 1), 8.0 * n * ncols);
-    dots_fused_kernel<<<blocks, kThreads, 0, ctx->stream>>>(V, n, ncols, w, n, chunk, partial.p,
-                                                            out, ticket.p);
-    HPSB_LAUNCHED(ctx);
+    if (blocks <= 64) {
+      dots_fused_kernel<<<blocks, kThreads, 0, ctx->stream>>>(V, n, ncols, w, n, chunk, partial.p,
+                                                              out, ticket.p);
+      HPSB_LAUNCHED(ctx);
+    } else {
+      dots_kernel<<<blocks, kThreads, 0, ctx->stream>>>(V, n, ncols, w, n, partial.p);
+      HPSB_LAUNCHED(ctx);
+      reduce_kernel<<<ncols, 256, 0, ctx->stream>>>(partial.p, blocks, ncols, out);
+      HPSB_LAUNCHED(ctx);
+    }
   }
   void axpy(const double2* V, int ncols, const double2* h, double sign, double2* w) {
     KernelScope ks(ctx, "gmres_axpy", 16.0 * n * (ncols + 2), 8.0 * n * ncols);
