@@ -193,6 +193,30 @@ hpsb_status hpsb_context_profile_reset(hpsb_context ctx);
 /* Algorithmic operator bytes one preconditioner apply streams (roofline). */
 int64_t hpsb_precond_bytes(hpsb_precond p);
 
+/* ------------------------------------------------------------ multi-GPU
+ * Quadtree-subtree sharding over G = 2^g ranks, one per GPU.
+ * Attach a communicator to a context BEFORE building objects on it; every
+ * object built on that context is then sharded: each rank builds the
+ * elements and merge levels 1..L-g of its own subtree, the subtree boxes
+ * are broadcast, the top g levels run on every rank, and the matvec /
+ * preconditioner combine their partial results with an allreduce.  Vectors
+ * at the ABI stay full length (replicated) on every rank.                   */
+typedef struct hpsb_local_group_s* hpsb_local_group;
+/* NCCL (one process per GPU): rank 0 makes the id, all ranks attach. */
+hpsb_status hpsb_nccl_unique_id(unsigned char id[128]);
+hpsb_status hpsb_context_attach_nccl(hpsb_context ctx, const unsigned char id[128], int rank,
+                                     int world);
+/* Single-process emulation of `world` ranks (one host thread + context per
+ * rank, host barriers; used to test the sharded path on one GPU).          */
+hpsb_status hpsb_local_group_create(int world, hpsb_local_group* out);
+hpsb_status hpsb_local_group_destroy(hpsb_local_group g);
+hpsb_status hpsb_context_attach_local(hpsb_context ctx, hpsb_local_group g, int rank);
+hpsb_status hpsb_context_comm_info(hpsb_context ctx, int* rank, int* world);
+/* Host-only: the sharding plan (element owner per element, face owner per
+ * face with -1 on the shared top-level faces) and the last local level.    */
+hpsb_status hpsb_partition(int n, int world, int rank, int* elem_owner, int* face_owner,
+                           int* last_local_level);
+
 #ifdef __cplusplus
 }
 #endif

@@ -118,6 +118,13 @@ _sig("hpsb_context_profile_entry", _st, _VP, ctypes.c_int, ctypes.c_char_p, ctyp
      ctypes.POINTER(ctypes.c_int64), _D, _D, _D)
 _sig("hpsb_context_profile_reset", _st, _VP)
 _sig("hpsb_precond_bytes", ctypes.c_int64, _VP)
+_sig("hpsb_nccl_unique_id", _st, ctypes.c_char_p)
+_sig("hpsb_context_attach_nccl", _st, _VP, ctypes.c_char_p, ctypes.c_int, ctypes.c_int)
+_sig("hpsb_local_group_create", _st, ctypes.c_int, ctypes.POINTER(_VP))
+_sig("hpsb_local_group_destroy", _st, _VP)
+_sig("hpsb_context_attach_local", _st, _VP, _VP, ctypes.c_int)
+_sig("hpsb_context_comm_info", _st, _VP, _I, _I)
+_sig("hpsb_partition", _st, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I, _I)
 
 
 def _check(status: int, allow=(OK,)) -> int:
@@ -230,6 +237,21 @@ class Context:
     def launches(self) -> int:
         return int(_lib.hpsb_context_launches(self._h))
 
+    def attach_nccl(self, uid: bytes, rank: int, world: int):
+        """Shard every object built on this context over `world` GPUs (NCCL)."""
+        _check(_lib.hpsb_context_attach_nccl(self._h, uid, rank, world))
+
+    def attach_local(self, group: "LocalGroup", rank: int):
+        """Single-process emulation: this context is `rank` of `group`."""
+        _check(_lib.hpsb_context_attach_local(self._h, group._h, rank))
+        self._group = group
+
+    @property
+    def rank_world(self):
+        r, w = ctypes.c_int(), ctypes.c_int()
+        _check(_lib.hpsb_context_comm_info(self._h, ctypes.byref(r), ctypes.byref(w)))
+        return r.value, w.value
+
     def timer_start(self):
         _check(_lib.hpsb_context_timer_start(self._h))
 
@@ -266,6 +288,23 @@ class Context:
         self.close()
 
 
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.hpsb_nccl_unique_id(buf))
+    return buf.raw
+
+
+def partition(n: int, world: int, rank: int) -> dict:
+    """Host-side sharding plan: element owners, face owners (-1 = shared top level)."""
+    nf = 2 * n * (n - 1)
+    eo = np.zeros(n * n, dtype=np.int32)
+    fo = np.zeros(nf, dtype=np.int32)
+    ll = ctypes.c_int()
+    _check(_lib.hpsb_partition(n, world, rank, eo.ctypes.data_as(_I), fo.ctypes.data_as(_I),
+                               ctypes.byref(ll)))
+    return {"elem_owner": eo, "face_owner": fo, "last_local": ll.value}
+
+
 class _Handle:
     _destroy = None
 
@@ -276,6 +315,16 @@ class _Handle:
 
     def __del__(self):
         self.close()
+
+
+class LocalGroup(_Handle):
+    """Single-process group of emulated ranks (one thread + Context each)."""
+    _destroy = _lib.hpsb_local_group_destroy
+
+    def __init__(self, world: int):
+        h = _VP()
+        _check(_lib.hpsb_local_group_create(world, ctypes.byref(h)))
+        self._h, self.world = h, world
 
 
 class ElementRecords(_Handle):

@@ -28,6 +28,9 @@ struct hpsb_precond_s {
   hpsb::Precond* p = nullptr;
   ~hpsb_precond_s() { hpsb::destroy_precond(p); }
 };
+struct hpsb_local_group_s {
+  std::shared_ptr<hpsb::LocalGroup> g;
+};
 
 namespace hpsb {
 void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
@@ -207,6 +210,64 @@ hpsb_status hpsb_context_profile_reset(hpsb_context ctx) {
 }
 
 int64_t hpsb_precond_bytes(hpsb_precond p) { return p ? hpsb::precond_bytes(p->p) : -1; }
+
+hpsb_status hpsb_nccl_unique_id(unsigned char id[128]) {
+  return guarded([&] {
+    REQUIRE(id, "nccl_unique_id: null output");
+    hpsb::nccl_unique_id(id);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_attach_nccl(hpsb_context ctx, const unsigned char id[128], int rank,
+                                     int world) {
+  return guarded([&] {
+    REQUIRE(ctx && id && world >= 1 && rank >= 0 && rank < world, "attach_nccl: bad argument");
+    ctx->c.comm = hpsb::make_nccl_comm(id, rank, world, ctx->c.device);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_local_group_create(int world, hpsb_local_group* out) {
+  return guarded([&] {
+    REQUIRE(out && world >= 1, "local_group_create: bad argument");
+    *out = new hpsb_local_group_s{hpsb::make_local_group(world)};
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_local_group_destroy(hpsb_local_group g) {
+  delete g;
+  return HPSB_OK;
+}
+
+hpsb_status hpsb_context_attach_local(hpsb_context ctx, hpsb_local_group g, int rank) {
+  return guarded([&] {
+    REQUIRE(ctx && g, "attach_local: null argument");
+    ctx->c.comm = hpsb::make_thread_comm(g->g, rank);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_context_comm_info(hpsb_context ctx, int* rank, int* world) {
+  return guarded([&] {
+    REQUIRE(ctx, "comm_info: null context");
+    if (rank) *rank = ctx->c.rank();
+    if (world) *world = ctx->c.world();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_partition(int n, int world, int rank, int* elem_owner, int* face_owner,
+                           int* last_local_level) {
+  return guarded([&] {
+    const hpsb::Partition p = hpsb::make_partition(hpsb::build_face_graph(n), world, rank);
+    if (elem_owner) std::memcpy(elem_owner, p.elem_owner.data(), p.elem_owner.size() * sizeof(int));
+    if (face_owner) std::memcpy(face_owner, p.face_owner.data(), p.face_owner.size() * sizeof(int));
+    if (last_local_level) *last_local_level = p.last_local;
+    return HPSB_OK;
+  });
+}
 
 hpsb_status hpsb_gll_rule(int order, double* nodes, double* weights, double* diff) {
   return guarded([&] {

@@ -354,8 +354,10 @@ __global__ void __launch_bounds__(kThreads) element_v2_kernel(ElemArgs a) {
   double* B = A + static_cast<size_t>(P) * P;    // P x nbc, ld P
   for (int i = tid; i < np; i += blockDim.x) mass[i] = a.mass[i];
   auto K = [&](int r, int c) { return __ldg(a.stiff + r + c * np); };
+  const int count = a.elist ? a.nlist : a.ne;
 
-  for (int e = blockIdx.x; e < a.ne; e += gridDim.x) {
+  for (int ii = blockIdx.x; ii < count; ii += gridDim.x) {
+    const int e = a.elist ? a.elist[ii] : ii;
     __syncthreads();
     if (tid == 0) s_fail = 0;
     const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
@@ -587,6 +589,17 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   el->T.alloc(static_cast<size_t>(ne) * nb * nb);
   el->H.alloc(static_cast<size_t>(ne) * nb);
   el->status.alloc(ne);
+  HPSB_CUDA(cudaMemsetAsync(el->status.p, 0, ne * sizeof(int), ctx->stream));
+  // Sharded (one rank per GPU): build only this rank's quadtree subtree.
+  el->part = make_partition(build_face_graph(n), ctx->world(), ctx->rank());
+  DevBuf<int> d_own;
+  const bool sharded = ctx->world() > 1;
+  if (sharded) {
+    HPSB_CUDA(cudaMemsetAsync(el->T.p, 0, el->T.bytes(), ctx->stream));
+    HPSB_CUDA(cudaMemsetAsync(el->H.p, 0, el->H.bytes(), ctx->stream));
+    d_own.upload(el->part.own_elems, ctx->stream);
+  }
+  const int nwork = sharded ? static_cast<int>(el->part.own_elems.size()) : ne;
 
   ElemArgs a{};
   a.ne = ne, a.order = order, a.m = m, a.ni = ni, a.nb = nb, a.eta = eta;
@@ -595,6 +608,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   a.T = el->T.p, a.H = el->H.p, a.status = el->status.p;
   a.npad = (ni + PW - 1) / PW * PW;
   a.nbc = (nb + 2 + 7) / 8 * 8;
+  if (sharded) a.elist = d_own.p, a.nlist = nwork;
 
   // v2 (blocked, DMMA) for every element
   const size_t smem2 = sizeof(double) * (v2_region(a.npad, a.nbc, nb) + np) + sizeof(int) * nb + 16;
@@ -602,7 +616,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
                                  static_cast<int>(smem2)));
   int per_sm = 0;
   HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_v2_kernel, kThreads, smem2));
-  const int slots2 = std::min(ne, std::max(1, std::min(per_sm, 3)) * ctx->num_sms);
+  const int slots2 = std::min(nwork, std::max(1, std::min(per_sm, 3)) * ctx->num_sms);
   const size_t stride2 = static_cast<size_t>(a.npad) * (a.npad + a.nbc);
   DevBuf<double> ws(stride2 * slots2);
   a.ws = ws.p, a.ws_stride = stride2;
@@ -610,7 +624,8 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   {
     // pinned algorithmic flops: ni^3/3 + 2 ni^2 nb + 8 nb^3 per element
     const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
-    KernelScope ks(ctx, "element_iti", 8.0 * ne * (np * np + 2 * ni + 2 * nb * nb + 2 * nb), fe * ne);
+    KernelScope ks(ctx, "element_iti", 8.0 * nwork * (np * np + 2 * ni + 2 * nb * nb + 2 * nb),
+                   fe * nwork);
     element_v2_kernel<<<slots2, kThreads, smem2, ctx->stream>>>(a);
     HPSB_LAUNCHED(ctx);
   }

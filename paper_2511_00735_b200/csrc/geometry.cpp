@@ -152,4 +152,41 @@ FaceGraph build_face_graph(int n) {
   return g;
 }
 
+Partition make_partition(const FaceGraph& g, int G, int rank) {
+  if (G < 1 || (G & (G - 1)) != 0) throw InvalidArgument("partition: ranks must be a power of two");
+  if (rank < 0 || rank >= G) throw InvalidArgument("partition: rank out of range");
+  Partition p;
+  p.G = G, p.rank = rank, p.L = g.num_levels();
+  while ((1 << p.g) < G) ++p.g;
+  if (G > 1 && p.g > p.L - 1)
+    throw InvalidArgument("partition: too many ranks for the mesh (need at least one local level)");
+  p.last_local = p.L - p.g;
+  const int ne = g.n * g.n;
+  // Follow the merges of levels 1..last_local: after level l an element's
+  // box is identified by the level-l group that produced it.
+  std::vector<int> box(ne);
+  for (int e = 0; e < ne; ++e) box[e] = e;
+  std::vector<int> elem_first_box(ne);
+  for (int level = 1; level <= p.last_local; ++level) {
+    const auto& groups = g.groups[level - 1];
+    std::vector<int> merged(ne, -1);  // old box id -> group id at this level
+    for (int gi = 0; gi < static_cast<int>(groups.size()); ++gi) {
+      const Face& f = g.faces[groups[gi][0]];
+      merged[box[f.e1]] = gi;
+      merged[box[f.e2]] = gi;
+    }
+    for (int e = 0; e < ne; ++e) box[e] = merged[box[e]];
+  }
+  p.elem_owner.resize(ne);
+  for (int e = 0; e < ne; ++e) {
+    p.elem_owner[e] = G == 1 ? 0 : box[e];
+    if (p.elem_owner[e] == rank) p.own_elems.push_back(e);
+  }
+  p.face_owner.resize(g.num_faces());
+  for (int f = 0; f < g.num_faces(); ++f)
+    p.face_owner[f] = g.faces[f].level <= p.last_local ? p.elem_owner[g.faces[f].e1] : -1;
+  if (G == 1) p.last_local = p.L;
+  return p;
+}
+
 }  // namespace hpsb

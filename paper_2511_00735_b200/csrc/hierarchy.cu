@@ -47,6 +47,13 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
   h->ctx = ctx, h->sk = sk, h->depth = depth, h->total_levels = total;
   const Elements* el = sk->el;
   const int ne = el->n * el->n, nb = el->nb, m = sk->m, bs = sk->bs;
+  // Sharded: levels 1..last_local run on this rank's subtree only; the
+  // subtree boxes are then broadcast and the top levels run on every rank.
+  const Partition& part = el->part;
+  const bool sharded = ctx->world() > 1;
+  if (sharded && depth <= part.last_local)
+    throw InvalidArgument("build_hierarchy: a sharded hierarchy must reach the global levels (depth > " +
+                          std::to_string(part.last_local) + ")");
 
   // Level-1 boxes are the elements (all 4(N-1) positions, physical ones -1).
   std::vector<HostBox> boxes(ne);
@@ -79,9 +86,11 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     std::vector<std::vector<int>> perms;  // per child, positions into its HostBox
     std::vector<const HostBox*> srcs;
     size_t toff = 0;
-    L->merges.resize(ng);
+    std::vector<std::vector<BoxPos>> next_pos(ng);  // merged box perimeter, every group
+    std::vector<int> merge_of(ng, -1);              // group -> this rank's merge index
     for (int gi = 0; gi < ng; ++gi) {
       const Face& f0 = g.faces[groups[gi][0]];
+      const bool own = !sharded || level > part.last_local || part.owns_elem(f0.e1);
       const HostBox* bx[2] = {&boxes[elem_box[f0.e1]], &boxes[elem_box[f0.e2]]};
       for (int k = 0; k < 2; ++k)
         for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
@@ -102,14 +111,17 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
           is_sep[0][q1] = 1, is_sep[1][q2] = 1;
         }
       }
-      MergeRec& mr = L->merges[gi];
+      MergeRec mr;
       mr.s = s;
+      mr.group = gi;
       for (int k = 0; k < 2; ++k) {
         ChildBox cb;
         std::vector<int> perm;
         for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
           if (bx[k]->pos[i].in >= 0 && !is_sep[k][i]) perm.push_back(i);
         cb.p = static_cast<int>(perm.size());
+        for (int i : perm) next_pos[gi].push_back(bx[k]->pos[i]);
+        if (!own) continue;
         perm.insert(perm.end(), sep[k].begin(), sep[k].end());
         cb.s = s;
         cb.P = static_cast<int>(perm.size());
@@ -121,6 +133,10 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
         L->children.push_back(std::move(cb));
         perms.push_back(std::move(perm));
         srcs.push_back(bx[k]);
+      }
+      if (own) {
+        merge_of[gi] = static_cast<int>(L->merges.size());
+        L->merges.push_back(mr);
       }
       for (int k = 0; k < 2; ++k)
         for (const auto& p : bx[k]->pos)
@@ -167,10 +183,11 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     }
 
     if (!L->coarse) {
-      // ---- merges
+      // ---- merges (this rank's)
+      const int nm = static_cast<int>(L->merges.size());
       size_t woff = 0, roff = 0, noff = 0;
-      std::vector<size_t> r_at(ng), n_at(ng);
-      for (int gi = 0; gi < ng; ++gi) {
+      std::vector<size_t> r_at(nm), n_at(nm);
+      for (int gi = 0; gi < nm; ++gi) {
         MergeRec& mr = L->merges[gi];
         const int q = mr.p1 + mr.p2;
         mr.w_off = woff;
@@ -185,7 +202,7 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
       CopyBatch pre;
       GemmBatch g1, g2, g3, g4;
       InverseBatch inv;
-      for (int gi = 0; gi < ng; ++gi) {
+      for (int gi = 0; gi < nm; ++gi) {
         const MergeRec& mr = L->merges[gi];
         const ChildBox& c1 = L->children[mr.c1];
         const ChildBox& c2 = L->children[mr.c2];
@@ -211,7 +228,7 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
         pre.copy(T2pp, P2, Tn + p1 + static_cast<size_t>(p1) * q, q, p2, p2, 1.0);
         g1.add(T2ss, P2, T1ss, P1, W, s, s, s, s, -1.0, 1.0);
         g1.add(T2ss, P2, T1sp, P1, Rg, s, s, p1, s, 1.0, 0.0);
-        inv.ops.push_back(InvOp{W, s, s, gi, 0});
+        inv.ops.push_back(InvOp{W, s, s, mr.group, 0});
         g2.add(W, s, Rg, s, X1g, s, s, q, s, 1.0, 0.0);
         g3.add(T1ss, P1, X1g, s, X2g, s, s, q, s, -1.0, 1.0);
         g3.add(T1ps, P1, X1g, s, Tn, q, p1, q, s, 1.0, 1.0);
@@ -233,17 +250,32 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
         throw std::runtime_error("eliminate_level: singular merge block at face " +
                                  std::to_string(g.groups[level - 1][gi].front()));
       }
-      // ---- next level's boxes
+      // ---- next level's boxes (positions for every group, maps for ours)
       std::vector<HostBox> next(ng);
       for (int gi = 0; gi < ng; ++gi) {
-        const MergeRec& mr = L->merges[gi];
-        const ChildBox& c1 = L->children[mr.c1];
-        const ChildBox& c2 = L->children[mr.c2];
         HostBox& nbx = next[gi];
-        nbx.pos.assign(c1.pos.begin(), c1.pos.begin() + c1.p);
-        nbx.pos.insert(nbx.pos.end(), c2.pos.begin(), c2.pos.begin() + c2.p);
-        nbx.T = tnew.p + n_at[gi];
-        nbx.ld = mr.p1 + mr.p2;
+        nbx.pos = std::move(next_pos[gi]);
+        nbx.ld = static_cast<int>(nbx.pos.size());
+        nbx.T = merge_of[gi] >= 0 ? tnew.p + n_at[merge_of[gi]] : nullptr;
+      }
+      if (sharded && level == part.last_local) {
+        // Subtree boxes -> every rank (NCCL broadcast per owner): the top
+        // merges and the coarse system are then built on all ranks.
+        size_t tot = 0;
+        std::vector<size_t> at(ng);
+        for (int gi = 0; gi < ng; ++gi) {
+          at[gi] = tot;
+          tot += static_cast<size_t>(next[gi].ld) * next[gi].ld;
+        }
+        DevBuf<double2> all(tot);
+        const int me = ctx->rank();
+        if (merge_of[me] < 0) throw std::logic_error("build_hierarchy: rank owns no subtree box");
+        zcopy(ctx, all.p + at[me], next[me].T, static_cast<size_t>(next[me].ld) * next[me].ld);
+        for (int r = 0; r < ng; ++r)
+          ctx->comm->broadcast(all.p + at[r],
+                               sizeof(double2) * static_cast<size_t>(next[r].ld) * next[r].ld, r, ctx);
+        for (int gi = 0; gi < ng; ++gi) next[gi].T = all.p + at[gi];
+        tnew = std::move(all);
       }
       // element -> new box: the merge owning the element's old box
       std::vector<int> box_to_group(boxes.size(), -1);

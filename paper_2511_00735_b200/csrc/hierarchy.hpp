@@ -28,6 +28,7 @@ struct ChildBox {
 struct MergeRec {
   int c1 = 0, c2 = 0;
   int s = 0, p1 = 0, p2 = 0;
+  int group = 0;  // group index within the level (face-graph order)
   size_t w_off = 0;
   // offsets (in ints) into LevelOps::idx of the V-cycle index lists
   size_t in1_sep = 0, in2_sep = 0, in1_per = 0, out1_per = 0, in2_per = 0, out2_per = 0;

@@ -40,8 +40,9 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 // stream (cudaMallocAsync with an unbounded release threshold): the merge
 // stage allocates and frees per level, and pooled allocations keep that off
 // the critical path (no implicit device synchronisation as in cudaFree).
+// Per host thread (one context per thread, e.g. the emulated ranks).
 inline cudaStream_t& alloc_stream() {
-  static cudaStream_t s = nullptr;
+  thread_local cudaStream_t s = nullptr;
   return s;
 }
 
@@ -56,7 +57,7 @@ struct Staging {
   cudaStream_t stream = nullptr;
 };
 inline Staging& staging() {
-  static Staging s;
+  thread_local Staging s;
   return s;
 }
 void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
@@ -103,6 +104,25 @@ struct DevBuf {
   }
 };
 
+// ---------------------------------------------------------------- communication
+struct Context;
+// Collectives used by the sharded path (one rank per GPU).  NcclComm runs
+// them with NCCL over NVLink / NVSwitch; ThreadComm is the single-process
+// emulation used to test the sharded path with several ranks on one GPU
+// (host barriers only -- no kernel ever waits on another rank's kernel).
+struct Comm {
+  int rank = 0, size = 1;
+  virtual ~Comm() = default;
+  // In-place sum over ranks of n complex values on the context stream.
+  virtual void allreduce_sum(double2* buf, size_t n, Context* ctx) = 0;
+  virtual void broadcast(void* buf, size_t bytes, int root, Context* ctx) = 0;
+};
+std::unique_ptr<Comm> make_nccl_comm(const unsigned char id[128], int rank, int size, int device);
+struct LocalGroup;
+std::shared_ptr<LocalGroup> make_local_group(int size);
+std::unique_ptr<Comm> make_thread_comm(std::shared_ptr<LocalGroup> group, int rank);
+void nccl_unique_id(unsigned char id[128]);
+
 // ---------------------------------------------------------------- context
 struct ProfAgg {
   int64_t launches = 0;
@@ -126,6 +146,9 @@ struct Context {
   std::vector<cudaEvent_t> event_pool;
   std::vector<std::pair<std::string, ProfAgg>> agg;
   void collect();
+  std::unique_ptr<Comm> comm;  // null: single GPU
+  int rank() const { return comm ? comm->rank : 0; }
+  int world() const { return comm ? comm->size : 1; }
 };
 
 // Brackets one kernel launch with CUDA events when profiling is enabled and
@@ -162,6 +185,20 @@ struct Gll {
   std::vector<double> nodes, weights, diff;  // diff col-major (N+1)^2
 };
 Gll gll_rule(int order);
+
+// Quadtree-subtree sharding over G = 2^g ranks: levels
+// 1..last_local of the merge tree are eliminated inside each rank's box (the
+// box produced by group `rank` of level last_local = L - g); the top g
+// levels are global.  Faces of local levels belong to one rank; faces of
+// global levels (the cuts between rank boxes) are shared.
+struct Partition {
+  int G = 1, g = 0, rank = 0, L = 0, last_local = 0;
+  std::vector<int> elem_owner;  // [n^2]
+  std::vector<int> face_owner;  // [faces], -1 on global-level faces
+  std::vector<int> own_elems;
+  bool owns_elem(int e) const { return elem_owner[e] == rank; }
+};
+Partition make_partition(const FaceGraph& g, int G, int rank);
 
 // ---------------------------------------------------------------- GEMV work lists
 // y[yi] = beta * y[yi] + gamma * z[zi] + alpha * A x[xi]   (complex, A col-major)
@@ -220,6 +257,7 @@ struct Elements {
   DevBuf<double2> H;  // [e][nb]
   DevBuf<int> status; // per-element failure flags
   double build_seconds = 0;
+  Partition part;     // sharding of the elements over the context's ranks
 };
 
 struct Skeleton {

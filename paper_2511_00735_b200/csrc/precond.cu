@@ -38,6 +38,9 @@ struct Precond {
   int64_t dim = 0, off_d = 0, dim_d = 0;
   DevBuf<double2> r, out, tmp;
   VPlan down, up, coarse_mv;
+  // sharded: levels above the subtree boxes (replicated on every rank)
+  VPlan down_g, up_g;
+  DevBuf<int> keep_face;  // faces whose result this rank contributes to z
   DevBuf<int> coarse_idx;
   DevBuf<double2> V, cv, cw, Hm, gv, rs;
   DevBuf<double> rc, state;
@@ -180,6 +183,20 @@ __device__ double block_sum(double v, double* sh) {
   }
   __syncthreads();
   return sh[32];
+}
+
+// y += s x
+__global__ void axpy_vec_kernel(double2* y, const double2* __restrict__ x, double s, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[k] = make_double2(y[k].x + s * x[k].x, y[k].y + s * x[k].y);
+}
+
+// zero the face blocks this rank does not contribute
+__global__ void mask_faces_kernel(double2* z, const int* __restrict__ keep, int bs) {
+  if (keep[blockIdx.x]) return;
+  for (int k = threadIdx.x; k < bs; k += blockDim.x)
+    z[static_cast<int64_t>(blockIdx.x) * bs + k] = make_double2(0.0, 0.0);
 }
 
 // state: [0] bnorm, [1] done, [2] jused, [3] zero-rhs
@@ -439,7 +456,8 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
         }
       }
     }
-    VPlan& plan = downward ? p->down : p->up;
+    const bool global_level = l > h->sk->el->part.last_local;
+    VPlan& plan = downward ? (global_level ? p->down_g : p->down) : (global_level ? p->up_g : p->up);
     const std::string label = std::string(downward ? "vcycle_down" : "vcycle_up") +
                               (std::getenv("HPSB_PROFILE_LEVELS") ? "_L" + std::to_string(l) : "");
     if (chain) {
@@ -458,8 +476,19 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   for (int l = cfg.depth - 1; l >= 1; --l) build_level(l, false);
   p->down.name = "vcycle_down";
   p->up.name = "vcycle_up";
+  p->down_g.name = "vcycle_down";
+  p->up_g.name = "vcycle_up";
   p->down.finalize(ctx->stream);
   p->up.finalize(ctx->stream);
+  p->down_g.finalize(ctx->stream);
+  p->up_g.finalize(ctx->stream);
+  if (ctx->world() > 1) {
+    const Partition& part = h->sk->el->part;
+    std::vector<int> keep(part.face_owner.size());
+    for (size_t f = 0; f < keep.size(); ++f)
+      keep[f] = part.face_owner[f] == ctx->rank() || (part.face_owner[f] < 0 && ctx->rank() == 0);
+    p->keep_face.upload(keep, ctx->stream);
+  }
 
   // ---- coarse level: M_depth = I + sum_boxes scatter(T_box) on the tail
   const LevelOps& C = *h->levels[cfg.depth - 1];
@@ -519,7 +548,8 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
   }
-  p->bytes_per_apply = p->down.bytes_per_run + p->up.bytes_per_run +
+  p->bytes_per_apply = p->down.bytes_per_run + p->up.bytes_per_run + p->down_g.bytes_per_run +
+                       p->up_g.bytes_per_run +
                        static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run;
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   return p.release();
@@ -532,6 +562,18 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   zcopy(ctx, p->r.p, v_dev, p->dim);
   // `out` of the plans is bound to the caller's z: no copy-out.
   p->down.run(ctx, p->out.p, z_dev);
+  const bool sharded = ctx->world() > 1;
+  if (sharded) {
+    // Each residual entry was updated by at most one rank's subtree:
+    // r = v + sum_ranks (r_rank - v).
+    const int blocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
+    axpy_vec_kernel<<<blocks, 256, 0, ctx->stream>>>(p->r.p, v_dev, -1.0, p->dim);
+    HPSB_LAUNCHED(ctx);
+    ctx->comm->allreduce_sum(p->r.p, p->dim, ctx);
+    axpy_vec_kernel<<<blocks, 256, 0, ctx->stream>>>(p->r.p, v_dev, 1.0, p->dim);
+    HPSB_LAUNCHED(ctx);
+  }
+  p->down_g.run(ctx, p->out.p, z_dev);
   const int ci = p->cfg.coarse_iters;
   if (p->coarse_fused) {
     static bool attr = false;
@@ -587,7 +629,16 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   HPSB_LAUNCHED(ctx);
   }
   }
+  p->up_g.run(ctx, p->out.p, z_dev);
   p->up.run(ctx, p->out.p, z_dev);
+  if (sharded) {
+    // Local faces come from their owner, global faces from rank 0: sum.
+    const int bs = p->h->sk->bs;
+    const int nf = static_cast<int>(p->dim / bs);
+    mask_faces_kernel<<<nf, 64, 0, ctx->stream>>>(z_dev, p->keep_face.p, bs);
+    HPSB_LAUNCHED(ctx);
+    ctx->comm->allreduce_sum(z_dev, p->dim, ctx);
+  }
 }
 
 int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }

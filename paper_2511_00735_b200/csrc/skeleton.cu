@@ -21,8 +21,8 @@ namespace {
 __global__ void skeleton_rhs_kernel(const double2* __restrict__ T, const double2* __restrict__ H,
                                     const int* __restrict__ in_idx, const int* __restrict__ out_idx,
                                     const double2* __restrict__ tside, double2* rhs, int nb,
-                                    int64_t dim, int ne, int nrhs) {
-  const int e = blockIdx.x;
+                                    int64_t dim, int ne, int nrhs, const int* __restrict__ elist) {
+  const int e = elist ? elist[blockIdx.x] : blockIdx.x;
   const double2* Te = T + static_cast<size_t>(e) * nb * nb;
   const int* in_e = in_idx + static_cast<size_t>(e) * nb;
   const int* out_e = out_idx + static_cast<size_t>(e) * nb;
@@ -68,20 +68,31 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
   sk->d_in.upload(sk->h_in, ctx->stream);
   sk->d_out.upload(sk->h_out, ctx->stream);
 
-  // Right-hand sides.
+  // Right-hand sides (sharded: each rank adds its elements' rows, then sum).
+  const bool sharded = ctx->world() > 1;
+  const std::vector<int>& own = el->part.own_elems;
   sk->rhs.alloc(static_cast<size_t>(nrhs) * sk->dim);
+  HPSB_CUDA(cudaMemsetAsync(sk->rhs.p, 0, sk->rhs.bytes(), ctx->stream));
   DevBuf<double2> d_t(static_cast<size_t>(nrhs) * ne * nb);
   HPSB_CUDA(cudaMemcpyAsync(d_t.p, tside_host, d_t.bytes(), cudaMemcpyHostToDevice, ctx->stream));
-  KernelScope ks(ctx, "skeleton_rhs", 16.0 * ne * nb * nb, 0.0);
-  skeleton_rhs_kernel<<<ne, 64, 0, ctx->stream>>>(el->T.p, el->H.p, sk->d_in.p, sk->d_out.p, d_t.p,
-                                                  sk->rhs.p, nb, sk->dim, ne, nrhs);
-  HPSB_LAUNCHED(ctx);
+  DevBuf<int> d_own;
+  if (sharded) d_own.upload(own, ctx->stream);
+  const int nwork = sharded ? static_cast<int>(own.size()) : ne;
+  {
+    KernelScope ks(ctx, "skeleton_rhs", 16.0 * nwork * nb * nb, 0.0);
+    skeleton_rhs_kernel<<<nwork, 64, 0, ctx->stream>>>(el->T.p, el->H.p, sk->d_in.p, sk->d_out.p,
+                                                       d_t.p, sk->rhs.p, nb, sk->dim, ne, nrhs,
+                                                       sharded ? d_own.p : nullptr);
+    HPSB_LAUNCHED(ctx);
+  }
+  if (sharded) ctx->comm->allreduce_sum(sk->rhs.p, sk->rhs.n, ctx);
 
-  // Matvec plan: one unit per element, y[out] = x[out] + T_e x[in].
+  // Matvec plan: one unit per (own) element, y[out] = x[out] + T_e x[in].
   sk->x_buf.alloc(sk->dim);
   sk->y_buf.alloc(sk->dim);
   sk->apply_plan.begin_phase();
   for (int e = 0; e < ne; ++e) {
+    if (sharded && !el->part.owns_elem(e)) continue;
     VItem it{};
     it.A = el->T.p + static_cast<size_t>(e) * nb * nb;
     it.lda = nb, it.rows = nb, it.cols = nb;
@@ -99,7 +110,12 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
 
 void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev) {
   // The plan was built on x_buf / y_buf; bind the caller's vectors instead.
-  sk->apply_plan.run(sk->ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
+  Context* ctx = sk->ctx;
+  const bool sharded = ctx->world() > 1;
+  if (sharded) HPSB_CUDA(cudaMemsetAsync(y_dev, 0, sk->dim * sizeof(double2), ctx->stream));
+  sk->apply_plan.run(ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
+  // Every skeleton row is produced by exactly one rank's element: sum.
+  if (sharded) ctx->comm->allreduce_sum(y_dev, sk->dim, ctx);
 }
 
 }  // namespace hpsb

@@ -1,0 +1,81 @@
+"""The sharded (quadtree-subtree, multi-rank) path on one GPU.
+
+Ranks are emulated in one process (hpsb_local_group: one host thread and one
+context per rank, host barriers for the collectives -- no kernel ever waits
+on another rank's kernel).  Every rank must reproduce the single-GPU results:
+rhs, matvec, preconditioner apply, FGMRES solution and iteration count.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def relf(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def _single(hps, prob, x, v):
+    ctx = hps.Context(0)
+    el = hps.build_elements(ctx, prob)
+    sk = hps.assemble_skeleton(el, prob)
+    h = hps.build_hierarchy(sk)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    sol, rep = hps.fgmres(sk, sk.rhs(), pc, restart=prob.restart, tol=prob.tol)
+    return {"rhs": sk.rhs(), "Mx": sk.apply(x), "Pv": pc.apply(v), "x": sol, "rep": rep}
+
+
+def _sharded(hps, prob, world, x, v):
+    grp = hps.LocalGroup(world)
+    out, errs = [None] * world, [None] * world
+
+    def run(rank):
+        try:
+            ctx = hps.Context(0)
+            ctx.attach_local(grp, rank)
+            el = hps.build_elements(ctx, prob)
+            sk = hps.assemble_skeleton(el, prob)
+            h = hps.build_hierarchy(sk)
+            pc = hps.build_preconditioner(h, coarse_iters=4)
+            res = {"rhs": sk.rhs(), "Mx": sk.apply(x), "Pv": pc.apply(v)}
+            res["x"], res["rep"] = hps.fgmres(sk, sk.rhs(), pc, restart=prob.restart, tol=prob.tol)
+            res["rank_world"] = ctx.rank_world
+            out[rank] = res
+        except Exception as exc:  # noqa: BLE001
+            errs[rank] = exc
+
+    threads = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in threads), "sharded run hung"
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
+@pytest.mark.parametrize("config,world", [(1, 2), (1, 4), (0, 2), (1, 8)])
+def test_sharded_matches_single_gpu(config, world):
+    import paper_2511_00735_b200 as hps
+    prob = hps.problem(2, config)
+    rng = np.random.default_rng(3)
+    dim = 2 * (2 * prob.n * (prob.n - 1)) * (prob.order - 1)
+    x = rng.standard_normal(dim) + 1j * rng.standard_normal(dim)
+    v = rng.standard_normal(dim) + 1j * rng.standard_normal(dim)
+    ref = _single(hps, prob, x, v)
+    shards = _sharded(hps, prob, world, x, v)
+    for rank, s in enumerate(shards):
+        assert s["rank_world"] == (rank, world)
+        assert relf(s["rhs"], ref["rhs"]) < 1e-12
+        assert relf(s["Mx"], ref["Mx"]) < 1e-12
+        assert relf(s["Pv"], ref["Pv"]) < 1e-10
+        assert s["rep"]["converged"]
+        assert abs(s["rep"]["iterations"] - ref["rep"]["iterations"]) <= 1
+        assert relf(s["x"], ref["x"]) < 1e-9
+    # every rank holds the same replicated solution
+    for s in shards[1:]:
+        assert relf(s["x"], shards[0]["x"]) < 1e-12
