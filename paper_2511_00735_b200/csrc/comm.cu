@@ -2,6 +2,7 @@
 // NVSwitch) and a single-process emulation over host threads.
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -50,16 +51,24 @@ struct LocalGroup {
   std::condition_variable cv;
   int arrived = 0, generation = 0;
   std::vector<void*> slots;
+  bool broken = false;
+  // A rank that fails (throws) before a collective would leave the others
+  // waiting: the wait is bounded and a timed-out group stays broken so every
+  // rank reports the failure instead of hanging.
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (broken) throw std::runtime_error("local group: a rank failed");
     const int gen = generation;
     if (++arrived == size) {
       arrived = 0;
       ++generation;
       cv.notify_all();
-    } else {
-      cv.wait(lk, [&] { return generation != gen; });
+    } else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return generation != gen; })) {
+      broken = true;
+      cv.notify_all();
+      throw std::runtime_error("local group: collective timed out (another rank failed?)");
     }
+    if (broken) throw std::runtime_error("local group: a rank failed");
   }
 };
 

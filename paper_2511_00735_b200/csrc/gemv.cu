@@ -121,23 +121,17 @@ void VPlan::run_phase(Context* ctx, int p, const double2* from0, double2* to0,
   const size_t smem = sizeof(double2) * std::max(ph.max_cols, 1);
   KernelScope ks(ctx, ph.label.empty() ? name : ph.label.c_str(), ph.bytes, 0.0);
   if (ph.csize <= 1) {
-    if (smem > 48 * 1024)
-      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+    allow_max_smem<vplan_kernel<false>>();
     vplan_kernel<false><<<ph.unit_count, kThreads, smem, ctx->stream>>>(d_items.p, d_units.p,
                                                                          ph.unit_begin, 1, bind);
   } else {
-    static bool nonportable = false;
-    if (!nonportable) {
+    static const bool nonportable = [] {  // thread-safe one-time init
       HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      nonportable = true;
-    }
-    if (smem > 48 * 1024)
-      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+      return true;
+    }();
+    (void)nonportable;
+    allow_max_smem<vplan_kernel<true>>();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ph.unit_count * ph.csize);
     cfg.blockDim = dim3(kThreads);

@@ -28,6 +28,21 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
     cudaError_t e_ = (x);                                         \
     if (e_ != cudaSuccess) ::hpsb::cuda_fail(e_, #x, __FILE__, __LINE__); \
   } while (0)
+// Raise a kernel's dynamic shared-memory cap once, to the device maximum.
+// The attribute is process-wide, so per-launch values would race between
+// host threads driving different contexts (the emulated ranks).
+constexpr int kMaxDynamicSmem = 227 * 1024;
+template <auto Kernel>
+void allow_max_smem() {
+  static const bool once = [] {
+    const cudaError_t e =
+        cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynamicSmem);
+    if (e != cudaSuccess) cuda_fail(e, "cudaFuncSetAttribute", __FILE__, __LINE__);
+    return true;
+  }();
+  (void)once;
+}
+
 // After a kernel launch: catch launch-configuration errors immediately.
 #define HPSB_LAUNCHED(ctx)                 \
   do {                                     \

@@ -576,17 +576,14 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   p->down_g.run(ctx, p->out.p, z_dev);
   const int ci = p->cfg.coarse_iters;
   if (p->coarse_fused) {
-    static bool attr = false;
-    if (!attr) {
+    static const bool attr = [] {  // thread-safe one-time init
       HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      attr = true;
-    }
+      return true;
+    }();
+    (void)attr;
     const size_t smem = sizeof(double2) * std::max(p->coarse_max_cols, 1);
-    if (smem > 16 * 1024)
-      HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+    allow_max_smem<coarse_fused_kernel>();
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(p->coarse_csize);
     lc.blockDim = dim3(kGemvThreads);

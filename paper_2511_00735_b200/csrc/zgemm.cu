@@ -320,13 +320,13 @@ void GemmBatch::run(Context* ctx) {
   if (descs.empty()) return;
   // K == 0 problems still apply the epilogue (C = beta C): keep them valid.
   d_descs.upload(descs, ctx->stream);
-  static bool attr = false;
-  if (!attr) {
+  static const bool attr = [] {  // thread-safe one-time init
     HPSB_CUDA(cudaFuncSetAttribute(zgemm_grouped_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(GEMM_SMEM)));
-    attr = true;
-  }
+    return true;
+  }();
+  (void)attr;
   KernelScope ks(ctx, "zgemm_dmma", 0.0, flops);
   zgemm_grouped_kernel<<<total_tiles, THREADS, GEMM_SMEM, ctx->stream>>>(
       d_descs.p, static_cast<int>(descs.size()));
@@ -367,9 +367,7 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     int nmax = 0;
     for (const auto& o : small) nmax = std::max(nmax, o.n);
     const size_t smem = sizeof(double2) * nmax * nmax + sizeof(int) * nmax + 16;
-    HPSB_CUDA(cudaFuncSetAttribute(inverse_smem_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
+    allow_max_smem<inverse_smem_kernel>();
     d_small.upload(small, ctx->stream);
     double fl = 0;
     for (const auto& o : small) fl += 8.0 * o.n * double(o.n) * o.n;

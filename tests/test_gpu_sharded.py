@@ -50,11 +50,10 @@ def _sharded(hps, prob, world, x, v):
     for t in threads:
         t.start()
     for t in threads:
-        t.join(timeout=600)
+        t.join(timeout=300)
     assert not any(t.is_alive() for t in threads), "sharded run hung"
-    for e in errs:
-        if e is not None:
-            raise e
+    failed = [(r, repr(e)) for r, e in enumerate(errs) if e is not None]
+    assert not failed, failed
     return out
 
 
