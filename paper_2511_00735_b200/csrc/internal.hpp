@@ -31,12 +31,18 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 // Raise a kernel's dynamic shared-memory cap once, to the device maximum.
 // The attribute is process-wide, so per-launch values would race between
 // host threads driving different contexts (the emulated ranks).
-constexpr int kMaxDynamicSmem = 227 * 1024;
 template <auto Kernel>
 void allow_max_smem() {
   static const bool once = [] {
-    const cudaError_t e =
-        cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynamicSmem);
+    int dev = 0, optin = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess)
+      e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, Kernel);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               optin - static_cast<int>(fa.sharedSizeBytes));
     if (e != cudaSuccess) cuda_fail(e, "cudaFuncSetAttribute", __FILE__, __LINE__);
     return true;
   }();
