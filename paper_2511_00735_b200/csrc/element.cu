@@ -612,7 +612,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
 
   // v2 (blocked, DMMA) for every element
   const size_t smem2 = sizeof(double) * (v2_region(a.npad, a.nbc, nb) + np) + sizeof(int) * nb + 16;
-  allow_max_smem<element_v2_kernel>();
+  allow_smem<element_v2_kernel>(smem2);
   int per_sm = 0;
   HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_v2_kernel, kThreads, smem2));
   const int slots2 = std::min(nwork, std::max(1, std::min(per_sm, 3)) * ctx->num_sms);
@@ -646,7 +646,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
     a.elist = d_redo.p, a.nlist = static_cast<int>(redo.size());
     const size_t smem = sizeof(double2) * (nb * nb + nb) + sizeof(double) * (ni + np) +
                         sizeof(int) * nb + 16;
-    allow_max_smem<element_kernel>();
+    allow_smem<element_kernel>(smem);
     KernelScope ks(ctx, "element_iti_lu", 0.0, 0.0);
     element_kernel<<<slots, kThreads, smem, ctx->stream>>>(a);
     HPSB_LAUNCHED(ctx);

@@ -121,7 +121,7 @@ void VPlan::run_phase(Context* ctx, int p, const double2* from0, double2* to0,
   const size_t smem = sizeof(double2) * std::max(ph.max_cols, 1);
   KernelScope ks(ctx, ph.label.empty() ? name : ph.label.c_str(), ph.bytes, 0.0);
   if (ph.csize <= 1) {
-    allow_max_smem<vplan_kernel<false>>();
+    allow_smem<vplan_kernel<false>>(smem);
     vplan_kernel<false><<<ph.unit_count, kThreads, smem, ctx->stream>>>(d_items.p, d_units.p,
                                                                          ph.unit_begin, 1, bind);
   } else {
@@ -131,7 +131,7 @@ void VPlan::run_phase(Context* ctx, int p, const double2* from0, double2* to0,
       return true;
     }();
     (void)nonportable;
-    allow_max_smem<vplan_kernel<true>>();
+    allow_smem<vplan_kernel<true>>(smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(ph.unit_count * ph.csize);
     cfg.blockDim = dim3(kThreads);

@@ -6,6 +6,7 @@
 #include <array>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -31,22 +32,20 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 // Raise a kernel's dynamic shared-memory cap once, to the device maximum.
 // The attribute is process-wide, so per-launch values would race between
 // host threads driving different contexts (the emulated ranks).
+// The cap only ever grows (under a lock), so a concurrent launch that needs
+// less shared memory is never invalidated by another thread's setting.
 template <auto Kernel>
-void allow_max_smem() {
-  static const bool once = [] {
-    int dev = 0, optin = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess)
-      e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa{};
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, Kernel);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               optin - static_cast<int>(fa.sharedSizeBytes));
+void allow_smem(size_t bytes) {
+  static std::mutex mu;
+  static int cap = 48 * 1024;
+  if (static_cast<int>(bytes) <= cap) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<int>(bytes) > cap) {
+    const cudaError_t e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(bytes));
     if (e != cudaSuccess) cuda_fail(e, "cudaFuncSetAttribute", __FILE__, __LINE__);
-    return true;
-  }();
-  (void)once;
+    cap = static_cast<int>(bytes);
+  }
 }
 
 // After a kernel launch: catch launch-configuration errors immediately.

@@ -583,7 +583,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
     }();
     (void)attr;
     const size_t smem = sizeof(double2) * std::max(p->coarse_max_cols, 1);
-    allow_max_smem<coarse_fused_kernel>();
+    allow_smem<coarse_fused_kernel>(smem);
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(p->coarse_csize);
     lc.blockDim = dim3(kGemvThreads);

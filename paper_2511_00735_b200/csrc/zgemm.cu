@@ -367,7 +367,7 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     int nmax = 0;
     for (const auto& o : small) nmax = std::max(nmax, o.n);
     const size_t smem = sizeof(double2) * nmax * nmax + sizeof(int) * nmax + 16;
-    allow_max_smem<inverse_smem_kernel>();
+    allow_smem<inverse_smem_kernel>(smem);
     d_small.upload(small, ctx->stream);
     double fl = 0;
     for (const auto& o : small) fl += 8.0 * o.n * double(o.n) * o.n;
