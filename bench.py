@@ -11,9 +11,10 @@ resident in HBM); `setup` = HPS setup elements/s (n^2 / device setup time).
 
   python bench.py [--config 1] [--steps K] [--warmup W] [--gpus N] [--impl b200|reference]
 
-Multi-GPU (torchrun): every rank runs an independent replica of the config
-(no data-path collective yet; subtree sharding is the next step),
-value = all ranks' DOF-iterations / max-over-ranks time, scaling "weak".
+Multi-GPU (torchrun): the config is sharded by quadtree subtree over the
+ranks (NCCL: subtree-box broadcast at setup, allreduce in the matvec and the
+V-cycle), value = the problem's DOF-iterations / max-over-ranks time,
+scaling "strong"; --replicas runs independent copies instead ("weak").
 """
 from __future__ import annotations
 
@@ -160,6 +161,11 @@ def run_b200(args, rank, world, local):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prob = hps.problem(2, args.config, seed=args.seed)
     ctx = hps.Context(local)
+    if world > 1 and not args.replicas:
+        # Quadtree-subtree sharding of ONE problem over the ranks (NCCL).
+        uid = [hps.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        ctx.attach_nccl(uid[0], rank, world)
     ne = prob.n ** 2
     coeff_d = torch.from_numpy(np.ascontiguousarray(prob.coeff)).cuda(local)
     src_d = torch.from_numpy(np.ascontiguousarray(prob.source).view(np.float64)).cuda(local)
@@ -212,6 +218,7 @@ def run_b200(args, rank, world, local):
             flush_l2()
     torch.cuda.synchronize()
     launches = ctx.launches - launches0
+    sharded = world > 1 and not args.replicas
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([setup_s, solve_s, dof_its, ne * args.steps], dtype=torch.float64,
@@ -221,7 +228,10 @@ def run_b200(args, rank, world, local):
         sm = t.clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
         setup_max, solve_max = mx[0].item(), mx[1].item()
-        dof_total, elem_total = sm[2].item(), sm[3].item()
+        if sharded:  # one problem solved by all ranks together
+            dof_total, elem_total = dof_its, ne * args.steps
+        else:        # independent replicas
+            dof_total, elem_total = sm[2].item(), sm[3].item()
     else:
         setup_max, solve_max, dof_total, elem_total = setup_s, solve_s, dof_its, ne * args.steps
     value = dof_total / solve_max
@@ -279,13 +289,14 @@ def run_b200(args, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * (setup_max + solve_max) / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": f"cfg{args.config}", "n": prob.n, "N": prob.order,
                    "kappa": prob.kappa, "dof": state["dim"], "elements": ne,
                    "levels": state["depth"], "restart": restart, "tol": tol, "seed": args.seed,
                    "mg": "depth=L, gamma=1, coarse_iters=4", "l2": "flushed between steps (256 MB)",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": (f"quadtree-subtree sharding x{world} (NCCL)" if sharded
+                                   else f"replicas x{world}")},
         "iterations": its,
         "setup": {"metric": "HPS setup elements/s", "value": setup_value,
                   "ms_per_step": 1e3 * setup_max / args.steps},
@@ -317,6 +328,8 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas instead of subtree sharding")
     args = ap.parse_args()
     if args.seed is None:
         args.seed = args.config
