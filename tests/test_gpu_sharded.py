@@ -57,6 +57,21 @@ def _sharded(hps, prob, world, x, v):
     return out
 
 
+def test_nccl_attach_single_rank():
+    # The NCCL communicator itself (init, one-rank world) on the real device;
+    # multi-rank NCCL needs one GPU per rank and runs under bench.py --gpus N.
+    import paper_2511_00735_b200 as hps
+    prob = hps.problem(2, 0)
+    ctx = hps.Context(0)
+    ctx.attach_nccl(hps.nccl_unique_id(), 0, 1)
+    assert ctx.rank_world == (0, 1)
+    el = hps.build_elements(ctx, prob)
+    sk = hps.assemble_skeleton(el, prob)
+    pc = hps.build_preconditioner(hps.build_hierarchy(sk), coarse_iters=4)
+    _, rep = hps.fgmres(sk, sk.rhs(), pc, restart=prob.restart, tol=prob.tol)
+    assert rep["converged"]
+
+
 @pytest.mark.parametrize("config,world", [(1, 2), (1, 4), (0, 2), (1, 8)])
 def test_sharded_matches_single_gpu(config, world):
     import paper_2511_00735_b200 as hps
