@@ -28,6 +28,7 @@
 #include "device.cuh"
 #include "gemv_device.cuh"
 #include "hierarchy.hpp"
+#include "vcycle_small.hpp"
 
 namespace hpsb {
 
@@ -49,9 +50,28 @@ struct Precond {
   bool coarse_fused = false;
   DevBuf<VItem> coarse_items;
   int coarse_nitems = 0, coarse_max_cols = 0, coarse_csize = 16;
+  // per-level execution order of the sweeps
+  struct Step {
+    int level = 0, small = -1;
+    const VPlan* plan = nullptr;
+    int p0 = 0, p1 = 0;
+  };
+  std::vector<Step> down_steps, up_steps;
+  std::vector<std::unique_ptr<SmallLevel>> smalls;
+  double bytes_small = 0;
+  void run_steps(bool down, bool global, double2* z) const {
+    const int last_local = h->sk->el->part.last_local;
+    for (const Step& st : down ? down_steps : up_steps) {
+      if ((st.level > last_local) != global) continue;
+      if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
+      else
+        for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
+    }
+  }
 };
 
 constexpr int kMaxCoarseIters = 30;
+constexpr size_t kSmallMergeSmemMax = 160 * 1024;
 
 namespace {
 constexpr int kCoarseThreads = 1024;
@@ -472,8 +492,58 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       }
     }
   };
-  for (int l = 1; l < cfg.depth; ++l) build_level(l, true);
-  for (int l = cfg.depth - 1; l >= 1; --l) build_level(l, false);
+  // Per level: the fused small-merge kernel when every merge's operators fit
+  // in shared memory, else the work-list plan phases.
+  auto small_level = [&](int l) -> int {
+    const LevelOps& L = *h->levels[l - 1];
+    if (L.merges.empty() || std::getenv("HPSB_NO_SMALL_MERGE")) return -1;
+    auto sl = std::make_unique<SmallLevel>();
+    std::vector<SmallMerge> v;
+    const int* ix = L.idx.p;
+    for (const MergeRec& mr : L.merges) {
+      const ChildBox& c1 = L.children[mr.c1];
+      const ChildBox& c2 = L.children[mr.c2];
+      const size_t need = small_merge_smem(mr.s, mr.p1, mr.p2);
+      if (need > kSmallMergeSmemMax) return -1;
+      sl->smem = std::max(sl->smem, need);
+      SmallMerge m{};
+      m.T1 = L.tperm.p + c1.t_off, m.T2 = L.tperm.p + c2.t_off, m.W = L.w.p + mr.w_off;
+      m.in1s = ix + mr.in1_sep, m.in2s = ix + mr.in2_sep, m.in1p = ix + mr.in1_per;
+      m.in2p = ix + mr.in2_per, m.out1p = ix + mr.out1_per, m.out2p = ix + mr.out2_per;
+      m.s = mr.s, m.p1 = mr.p1, m.p2 = mr.p2, m.P1 = c1.P, m.P2 = c2.P;
+      v.push_back(m);
+      const double ss = 16.0 * mr.s * mr.s, sp = 16.0 * mr.s * (mr.p1 + mr.p2);
+      sl->bytes_down += 3 * ss + sp;
+      sl->bytes_up += 3 * ss + sp;
+    }
+    sl->level = l;
+    sl->count = static_cast<int>(v.size());
+    if (std::getenv("HPSB_PROFILE_LEVELS")) sl->label = "vcycle_small_L" + std::to_string(l);
+    sl->d.upload(v, ctx->stream);
+    p->smalls.push_back(std::move(sl));
+    return static_cast<int>(p->smalls.size()) - 1;
+  };
+  std::vector<int> small_of(cfg.depth, -1);
+  for (int l = 1; l < cfg.depth; ++l) small_of[l] = small_level(l);
+  auto add_step = [&](int l, bool downward) {
+    Precond::Step st;
+    st.level = l;
+    st.small = small_of[l];
+    if (st.small < 0) {
+      const bool global_level = l > h->sk->el->part.last_local;
+      VPlan& plan =
+          downward ? (global_level ? p->down_g : p->down) : (global_level ? p->up_g : p->up);
+      st.plan = &plan;
+      st.p0 = static_cast<int>(plan.phases.size());
+      build_level(l, downward);
+      st.p1 = static_cast<int>(plan.phases.size());
+    } else {
+      p->bytes_small += downward ? p->smalls[st.small]->bytes_down : p->smalls[st.small]->bytes_up;
+    }
+    (downward ? p->down_steps : p->up_steps).push_back(st);
+  };
+  for (int l = 1; l < cfg.depth; ++l) add_step(l, true);
+  for (int l = cfg.depth - 1; l >= 1; --l) add_step(l, false);
   p->down.name = "vcycle_down";
   p->up.name = "vcycle_up";
   p->down_g.name = "vcycle_down";
@@ -548,7 +618,8 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
   }
-  p->bytes_per_apply = p->down.bytes_per_run + p->up.bytes_per_run + p->down_g.bytes_per_run +
+  p->bytes_per_apply = static_cast<int64_t>(p->bytes_small) + p->down.bytes_per_run +
+                       p->up.bytes_per_run + p->down_g.bytes_per_run +
                        p->up_g.bytes_per_run +
                        static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run;
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -561,7 +632,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   Context* ctx = p->ctx;
   zcopy(ctx, p->r.p, v_dev, p->dim);
   // `out` of the plans is bound to the caller's z: no copy-out.
-  p->down.run(ctx, p->out.p, z_dev);
+  p->run_steps(true, false, z_dev);  // local levels, down
   const bool sharded = ctx->world() > 1;
   if (sharded) {
     // Each residual entry was updated by at most one rank's subtree:
@@ -573,7 +644,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
     axpy_vec_kernel<<<blocks, 256, 0, ctx->stream>>>(p->r.p, v_dev, 1.0, p->dim);
     HPSB_LAUNCHED(ctx);
   }
-  p->down_g.run(ctx, p->out.p, z_dev);
+  p->run_steps(true, true, z_dev);  // top (global) levels, down
   const int ci = p->cfg.coarse_iters;
   if (p->coarse_fused) {
     static const bool attr = [] {  // thread-safe one-time init
@@ -626,8 +697,8 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   HPSB_LAUNCHED(ctx);
   }
   }
-  p->up_g.run(ctx, p->out.p, z_dev);
-  p->up.run(ctx, p->out.p, z_dev);
+  p->run_steps(false, true, z_dev);
+  p->run_steps(false, false, z_dev);
   if (sharded) {
     // Local faces come from their owner, global faces from rank 0: sum.
     const int bs = p->h->sk->bs;

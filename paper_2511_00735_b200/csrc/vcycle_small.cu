@@ -1,0 +1,166 @@
+// Fused V-cycle step for small merges: one CTA per merge, operators in smem.
+//
+// For the low levels of the hierarchy a merge's operators are a few tens of
+// KB, and the generic work-list execution is bound by the latency of its
+// dependent GEMV chain (each item waits for the previous item's output in
+// L2).  Here a CTA first issues ONE burst of cp.async copies for everything
+// the step needs -- the [T_ps; T_ss] (down) or [T_sp, T_ss] (up) column /
+// row blocks of both children (contiguous / 2-D slices of the stored
+// [p | s]-permuted maps) and W -- together with the vector gathers, then runs
+// the whole chain of multigrid.cpp:47-98 out of shared memory:
+//   down: t = r1 - T2_ss r2, x1 = W t, x2 = r2 - T1_ss x1,
+//         out[s] = (x1, x2), r[out_k,p] -= T_k,ps x_k
+//   up:   b1 = T2_sp u2, b2 = T1_sp u1, t = b1 - T2_ss b2, y1 = W t,
+//         out[s2] += T1_ss y1 - b2, out[s1] -= y1
+#include <algorithm>
+
+#include "device.cuh"
+#include "hierarchy.hpp"
+#include "vcycle_small.hpp"
+
+namespace hpsb {
+
+namespace {
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+
+// y = A x (A in smem, col-major, rows <= kThreads); returns row tid's value.
+// Column groups split the K loop, reduction through `red`.  Block-wide.
+__device__ double2 smem_gemv(const double2* A, int lda, int rows, int cols, const double2* x,
+                             double2* red) {
+  const int tid = threadIdx.x;
+  const int rpad = rows <= 8 ? 8 : rows <= 16 ? 16 : (rows + 31) & ~31;
+  const int groups = kThreads / rpad;
+  const int r = tid % rpad, g = tid / rpad;
+  double2 acc = make_double2(0.0, 0.0);
+  if (g < groups && r < rows)
+    for (int j = g; j < cols; j += groups) acc = cfma(A[r + j * lda], x[j], acc);
+  red[tid] = acc;
+  __syncthreads();
+  double2 s = make_double2(0.0, 0.0);
+  if (tid < rows) {
+    s = red[tid];
+    for (int q = 1; q < groups; ++q) s = cadd(s, red[tid + q * rpad]);
+  }
+  __syncthreads();
+  return s;
+}
+
+__global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge* __restrict__ ms,
+                                                               int down, double2* r,
+                                                               double2* out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const SmallMerge M = ms[blockIdx.x];
+  const int tid = threadIdx.x, s = M.s, p1 = M.p1, p2 = M.p2, P1 = M.P1, P2 = M.P2;
+  double2* A1 = reinterpret_cast<double2*>(smem_raw);
+  double2* A2 = A1 + static_cast<size_t>(P1) * s;
+  double2* Ws = A2 + static_cast<size_t>(P2) * s;
+  double2* v1 = Ws + static_cast<size_t>(s) * s;
+  double2* v2 = v1 + s;
+  double2* t = v2 + s;
+  double2* w1 = t + s;
+  double2* u1 = w1 + s;
+  double2* u2 = u1 + p1;
+  __shared__ double2 red[kThreads];
+
+  // ---- one burst of asynchronous copies: operators (+ W)
+  if (down) {
+    const double2* g1 = M.T1 + static_cast<size_t>(p1) * P1;  // [T1_ps; T1_ss], P1 x s
+    const double2* g2 = M.T2 + static_cast<size_t>(p2) * P2;
+    for (int k = tid; k < P1 * s; k += kThreads) cp_async16(A1 + k, g1 + k);
+    for (int k = tid; k < P2 * s; k += kThreads) cp_async16(A2 + k, g2 + k);
+  } else {
+    for (int k = tid; k < s * P1; k += kThreads)  // [T1_sp, T1_ss], s x P1 (ld s)
+      cp_async16(A1 + k, M.T1 + p1 + (k % s) + static_cast<size_t>(k / s) * P1);
+    for (int k = tid; k < s * P2; k += kThreads)
+      cp_async16(A2 + k, M.T2 + p2 + (k % s) + static_cast<size_t>(k / s) * P2);
+  }
+  for (int k = tid; k < s * s; k += kThreads) cp_async16(Ws + k, M.W + k);
+  asm volatile("cp.async.commit_group;\n" ::);
+  // vector gathers overlap the copies
+  if (down) {
+    for (int k = tid; k < s; k += kThreads) {
+      v1[k] = __ldcg(r + M.in1s[k]);
+      v2[k] = __ldcg(r + M.in2s[k]);
+    }
+  } else {
+    for (int k = tid; k < p1; k += kThreads) u1[k] = __ldcg(out + M.in1p[k]);
+    for (int k = tid; k < p2; k += kThreads) u2[k] = __ldcg(out + M.in2p[k]);
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+
+  if (down) {
+    const double2 *T1ps = A1, *T1ss = A1 + p1, *T2ps = A2, *T2ss = A2 + p2;
+    double2 y = smem_gemv(T2ss, P2, s, s, v2, red);  // t = v1 - T2_ss v2
+    if (tid < s) t[tid] = csub(v1[tid], y);
+    __syncthreads();
+    y = smem_gemv(Ws, s, s, s, t, red);  // x1 = W t
+    if (tid < s) {
+      w1[tid] = y;
+      __stcg(out + M.in1s[tid], y);
+    }
+    __syncthreads();
+    y = smem_gemv(T1ss, P1, s, s, w1, red);  // x2 = v2 - T1_ss x1
+    if (tid < s) {
+      const double2 x2 = csub(v2[tid], y);
+      t[tid] = x2;
+      __stcg(out + M.in2s[tid], x2);
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < p1; r0 += kThreads) {  // r[out1_p] -= T1_ps x1
+      y = smem_gemv(T1ps + r0, P1, min(p1 - r0, kThreads), s, w1, red);
+      if (tid < p1 - r0) {
+        const int o = M.out1p[r0 + tid];
+        __stcg(r + o, csub(__ldcg(r + o), y));
+      }
+    }
+    for (int r0 = 0; r0 < p2; r0 += kThreads) {  // r[out2_p] -= T2_ps x2
+      y = smem_gemv(T2ps + r0, P2, min(p2 - r0, kThreads), s, t, red);
+      if (tid < p2 - r0) {
+        const int o = M.out2p[r0 + tid];
+        __stcg(r + o, csub(__ldcg(r + o), y));
+      }
+    }
+  } else {
+    const double2 *T1sp = A1, *T1ss = A1 + static_cast<size_t>(p1) * s, *T2sp = A2,
+                  *T2ss = A2 + static_cast<size_t>(p2) * s;
+    double2 b1 = smem_gemv(T2sp, s, s, p2, u2, red);  // b1 = T2_sp u2
+    double2 b2 = smem_gemv(T1sp, s, s, p1, u1, red);  // b2 = T1_sp u1
+    if (tid < s) v1[tid] = b1, v2[tid] = b2;
+    __syncthreads();
+    double2 y = smem_gemv(T2ss, s, s, s, v2, red);  // t = b1 - T2_ss b2
+    if (tid < s) t[tid] = csub(v1[tid], y);
+    __syncthreads();
+    y = smem_gemv(Ws, s, s, s, t, red);  // y1 = W t
+    if (tid < s) w1[tid] = y;
+    __syncthreads();
+    const double2 z = smem_gemv(T1ss, s, s, s, w1, red);  // T1_ss y1
+    if (tid < s) {
+      const int o2 = M.in2s[tid], o1 = M.in1s[tid];
+      __stcg(out + o2, cadd(__ldcg(out + o2), csub(z, v2[tid])));
+      __stcg(out + o1, csub(__ldcg(out + o1), w1[tid]));
+    }
+  }
+}
+}  // namespace
+
+size_t small_merge_smem(int s, int p1, int p2) {
+  const size_t P1 = p1 + s, P2 = p2 + s;
+  return sizeof(double2) * ((P1 + P2 + s) * s + 4 * static_cast<size_t>(s) + p1 + p2);
+}
+
+void SmallLevel::run(Context* ctx, bool down, double2* r, double2* out) const {
+  if (!count) return;
+  allow_smem<merge_small_kernel>(smem);
+  KernelScope ks(ctx, label.empty() ? (down ? "vcycle_down" : "vcycle_up") : label.c_str(),
+                 down ? bytes_down : bytes_up, 0.0);
+  merge_small_kernel<<<count, kThreads, smem, ctx->stream>>>(d.p, down ? 1 : 0, r, out);
+  HPSB_LAUNCHED(ctx);
+}
+
+}  // namespace hpsb

@@ -1,0 +1,28 @@
+// Fused small-merge V-cycle step (csrc/vcycle_small.cu).
+#pragma once
+
+#include <string>
+
+#include "internal.hpp"
+
+namespace hpsb {
+
+struct SmallMerge {
+  const double2 *T1, *T2, *W;  // [p | s]-permuted child maps (ld P1 / P2), W (ld s)
+  const int *in1s, *in2s, *in1p, *in2p, *out1p, *out2p;
+  int s, p1, p2, P1, P2, pad;
+};
+
+// Shared memory one merge needs (operators + vectors).
+size_t small_merge_smem(int s, int p1, int p2);
+
+struct SmallLevel {
+  int level = 0, count = 0;
+  size_t smem = 0;
+  double bytes_down = 0, bytes_up = 0;
+  std::string label;
+  DevBuf<SmallMerge> d;
+  void run(Context* ctx, bool down, double2* r, double2* out) const;
+};
+
+}  // namespace hpsb
