@@ -37,7 +37,7 @@ void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
 template <auto Kernel>
 void allow_smem(size_t bytes) {
   static std::mutex mu;
-  static int cap = 48 * 1024;
+  static int cap = 0;  // the default limit is 48 KB minus the kernel's static smem
   if (static_cast<int>(bytes) <= cap) return;
   std::lock_guard<std::mutex> lk(mu);
   if (static_cast<int>(bytes) > cap) {
