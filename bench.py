@@ -173,18 +173,29 @@ def run_b200(args, rank, world, local):
     restart, tol = prob.restart, prob.tol
     state = {}
 
+    verbose = bool(os.environ.get("HPSB_BENCH_VERBOSE"))
+
     def step(profile: bool = False):
         import ctypes
         ctx.timer_start()
+        w0 = time.perf_counter()
         h = ctypes.c_void_p()
         hps._check(hps._lib.hpsb_elements_build_dev(
             ctx._h, prob.n, prob.order, prob.eta, ctypes.c_void_p(coeff_d.data_ptr()),
             None if prob.source_zero else ctypes.c_void_p(src_d.data_ptr()), ctypes.byref(h)))
         el = hps.ElementRecords(ctx, h, prob.n, prob.order, prob.eta)
+        w1 = time.perf_counter()
         sk = hps.assemble_skeleton(el, prob)
+        w2 = time.perf_counter()
         hier = hps.build_hierarchy(sk)
+        w3 = time.perf_counter()
         pc = hps.build_preconditioner(hier, coarse_iters=4)
         t_setup = ctx.timer_stop()
+        w4 = time.perf_counter()
+        if verbose:
+            print(f"[setup wall ms] elements {1e3 * (w1 - w0):.1f} skeleton {1e3 * (w2 - w1):.1f} "
+                  f"hierarchy {1e3 * (w3 - w2):.1f} (device {1e3 * hier.build_seconds:.1f}) "
+                  f"precond {1e3 * (w4 - w3):.1f}", file=sys.stderr)
         x = torch.empty(2 * sk.dim, dtype=torch.float64, device=f"cuda:{local}")
         rep = hps.SolveReport()
         cfg = hps.KrylovConfig(restart, tol, 2000, 0, 1)
