@@ -18,6 +18,8 @@
 // launches: one gather (children permuted to [p | s] order), one copy batch,
 // four grouped DMMA GEMMs and one batched inverse.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <unordered_map>
 
@@ -34,6 +36,32 @@ struct HostBox {
   std::vector<BoxPos> pos;
   const double2* T = nullptr;
   int ld = 0;
+};
+
+// HPSB_TRACE=1: host wall time per build phase (stderr), to separate host
+// bookkeeping from device time.
+struct Trace {
+  bool on = std::getenv("HPSB_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::vector<std::pair<std::string, double>> acc;
+  void mark(const char* name) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+    for (auto& kv : acc)
+      if (kv.first == name) {
+        kv.second += ms;
+        return;
+      }
+    acc.emplace_back(name, ms);
+  }
+  ~Trace() {
+    if (!on) return;
+    std::fprintf(stderr, "[hpsb trace hierarchy]");
+    for (auto& kv : acc) std::fprintf(stderr, " %s=%.1fms", kv.first.c_str(), kv.second);
+    std::fprintf(stderr, "\n");
+  }
 };
 }  // namespace
 
@@ -73,7 +101,9 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
   HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(int), ctx->stream));
 
   HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+  Trace tr;
   for (int level = 1; level <= depth; ++level) {
+    tr.mark("other");
     auto L = std::make_unique<LevelOps>();
     L->level = level;
     L->first_face = g.level_range[level - 1].first;
@@ -142,7 +172,9 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
         for (const auto& p : bx[k]->pos)
           if (p.in >= 0) pos_of[p.in] = -1;
     }
+    tr.mark("bookkeeping");
     L->tperm.alloc(toff);
+    tr.mark("alloc");
 
     // ---- gather children into the permuted layout
     {
@@ -161,7 +193,9 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
                   L->tperm.p + ch.t_off, ch.P, ch.P, ch.P);
       }
       cb.run(ctx);
+      tr.mark("gather_enqueue");
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+      tr.mark("gather_wait");
     }
     tnew_prev.release();
 
@@ -198,7 +232,9 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
         noff += static_cast<size_t>(q) * q;
       }
       L->w.alloc(woff);
+      tr.mark("idx");
       DevBuf<double2> R(roff), X1(roff), X2(roff), tnew(noff);
+      tr.mark("alloc");
       CopyBatch pre;
       GemmBatch g1, g2, g3, g4;
       InverseBatch inv;
@@ -243,8 +279,10 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
       L->merge_flops = g1.flops + g2.flops + g3.flops + g4.flops;
       for (const auto& mr : L->merges) L->merge_flops += 8.0 * mr.s * mr.s * mr.s;  // inverse
       int st = 0;
+      tr.mark("merge_enqueue");
       HPSB_CUDA(cudaMemcpyAsync(&st, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+      tr.mark("merge_wait");
       if (st) {
         const int gi = st - 1;
         throw std::runtime_error("eliminate_level: singular merge block at face " +
