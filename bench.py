@@ -287,7 +287,12 @@ def run_b200(args, rank, world, local):
         e2e_t += time.perf_counter() - t0
         e2e_dof += sk_h.dim * rep["iterations"]
     e2e_value = e2e_dof / e2e_t
-    # e2e setup: host coefficient arrays -> preconditioner ready
+    # e2e setup: host coefficient arrays -> preconditioner ready (previous
+    # objects released first, as in the timed steps)
+    del pc_h, hier_h, sk_h, el_h
+    import gc
+    gc.collect()
+    ctx.synchronize()
     t0 = time.perf_counter()
     el2 = hps.build_elements(ctx, prob)
     sk2 = hps.assemble_skeleton(el2, prob)

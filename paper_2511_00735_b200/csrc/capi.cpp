@@ -4,6 +4,8 @@
 // (proj/src/capi.cpp:13-24,109-137).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -101,6 +103,27 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     uint64_t threshold = UINT64_MAX;
     HPSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     hpsb::alloc_stream() = ctx->c.stream;
+    // Map pool memory once, here, instead of inside the first setups: growing
+    // a stream-ordered pool maps physical pages (~60 ms/GB measured), which
+    // would otherwise land inside build_hierarchy.  HPSB_POOL_RESERVE_GB
+    // overrides the default (min(48 GB, 40% of free memory)).
+    {
+      size_t free_b = 0, total_b = 0;
+      HPSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      double gb = std::min(48.0, 0.4 * free_b / double(1 << 30));
+      if (const char* env = std::getenv("HPSB_POOL_RESERVE_GB")) gb = std::atof(env);
+      uint64_t used = 0;
+      HPSB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &used));
+      const size_t want = static_cast<size_t>(gb * double(1 << 30));
+      if (want > used) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, want - used, ctx->c.stream) == cudaSuccess)
+          HPSB_CUDA(cudaFreeAsync(p, ctx->c.stream));
+        else
+          cudaGetLastError();  // best effort
+        HPSB_CUDA(cudaStreamSynchronize(ctx->c.stream));
+      }
+    }
     auto& st = hpsb::staging();
     if (!st.base) {
       st.size = size_t(64) << 20;
