@@ -323,7 +323,7 @@ def run_b200(args, rank, world, local):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": 16 * sk_h.dim, "d2h_bytes_per_step": 16 * sk_h.dim,
+                "h2d_bytes_per_step": 16 * state["dim"], "d2h_bytes_per_step": 16 * state["dim"],
                 "setup_elements_per_s": e2e_setup},
     }
     if world == 1 and not args.no_cpu_baseline:
