@@ -334,7 +334,7 @@ __host__ __device__ inline size_t v2_region(int P, int nbc, int nb) {
 // The backward solve R^T X = Y is blocked the same way, right-looking from
 // the last panel.  An indefinite L_ii (first failing pivot) marks the
 // element for the pivoted-LU fallback (v1 kernel, status bit 4).
-__global__ void __launch_bounds__(kThreads) element_v2_kernel(ElemArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) element_v2_kernel(ElemArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
   const int m = a.m, ni = a.ni, nb = a.nb, np = a.order + 1, N = a.order;
@@ -469,38 +469,57 @@ __global__ void __launch_bounds__(kThreads) element_v2_kernel(ElemArgs a) {
       // trailing SYRK (lower 8x8 tiles) and B update, DMMA
       const int nt = rem / 8, ntri = nt * (nt + 1) / 2, nbt = nbc / 8;
       const int total = ntri + nt * nbt;
-      for (int tile = warp; tile < total; tile += kThreads / 32) {
-        double c0, c1;
-        if (tile < ntri) {
-          int I = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
-          while (I * (I + 1) / 2 > tile) --I;
-          while ((I + 1) * (I + 2) / 2 <= tile) ++I;
-          const int J = tile - I * (I + 1) / 2;
-          double* C = A + (k0 + PW + 8 * I + g) + static_cast<size_t>(k0 + PW + 8 * J + 2 * t4) * P;
-          c0 = C[0];
-          c1 = C[P];
+      // Each warp takes kBatch tiles at a time: all C fragments are loaded
+      // first (kBatch x 2 loads in flight), then the DMMAs, then the stores,
+      // so the L2 latency of one tile overlaps the others'.
+      constexpr int kBatch = 4;
+      constexpr int kWarps = kThreads / 32;
+      for (int base = warp; base < total; base += kWarps * kBatch) {
+        double* Cp[kBatch];
+        const double* Ap[kBatch];
+        const double* Bq[kBatch];
+        int bstride[kBatch];
+        double c0[kBatch], c1[kBatch];
 #pragma unroll
-          for (int kk = 0; kk < PW; kk += 4) {
-            const double av = -L21s[(8 * I + g) + (kk + t4) * ldp];
-            const double bv = L21s[(8 * J + g) + (kk + t4) * ldp];
-            dmma(c0, c1, av, bv);
+        for (int q = 0; q < kBatch; ++q) {
+          const int tile = base + q * kWarps;
+          Cp[q] = nullptr;
+          if (tile >= total) continue;
+          if (tile < ntri) {
+            int I = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+            while (I * (I + 1) / 2 > tile) --I;
+            while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+            const int J = tile - I * (I + 1) / 2;
+            Cp[q] = A + (k0 + PW + 8 * I + g) + static_cast<size_t>(k0 + PW + 8 * J + 2 * t4) * P;
+            Ap[q] = L21s + 8 * I + g;
+            Bq[q] = L21s + 8 * J + g;
+            bstride[q] = ldp;
+          } else {
+            const int tt = tile - ntri, I = tt % nt, J = tt / nt;
+            Cp[q] = B + (k0 + PW + 8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
+            Ap[q] = L21s + 8 * I + g;
+            Bq[q] = Bp + (8 * J + g) * kLdq;
+            bstride[q] = -1;  // Bp: k runs along the column (stride 1)
           }
-          C[0] = c0;
-          C[P] = c1;
-        } else {
-          const int tt = tile - ntri, I = tt % nt, J = tt / nt;
-          double* C = B + (k0 + PW + 8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
-          c0 = C[0];
-          c1 = C[P];
-#pragma unroll
-          for (int kk = 0; kk < PW; kk += 4) {
-            const double av = -L21s[(8 * I + g) + (kk + t4) * ldp];
-            const double bv = Bp[(kk + t4) + (8 * J + g) * kLdq];
-            dmma(c0, c1, av, bv);
-          }
-          C[0] = c0;
-          C[P] = c1;
+          c0[q] = Cp[q][0];
+          c1[q] = Cp[q][P];
         }
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+          if (!Cp[q]) continue;
+#pragma unroll
+          for (int kk = 0; kk < PW; kk += 4) {
+            const double av = -Ap[q][(kk + t4) * ldp];
+            const double bv = bstride[q] < 0 ? Bq[q][kk + t4] : Bq[q][(kk + t4) * ldp];
+            dmma(c0[q], c1[q], av, bv);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q)
+          if (Cp[q]) {
+            Cp[q][0] = c0[q];
+            Cp[q][P] = c1[q];
+          }
       }
       __syncthreads();
     }
@@ -535,18 +554,34 @@ __global__ void __launch_bounds__(kThreads) element_v2_kernel(ElemArgs a) {
       }
       __syncthreads();
       const int nr = k0 / 8, nbt = nbc / 8;
-      for (int tile = warp; tile < nr * nbt; tile += kThreads / 32) {
-        const int I = tile % nr, J = tile / nr;
-        double* C = B + (8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
-        double c0 = C[0], c1 = C[P];
+      constexpr int kBatch = 4;
+      constexpr int kWarps = kThreads / 32;
+      for (int base = warp; base < nr * nbt; base += kWarps * kBatch) {
+        double* Cp[kBatch];
+        double c0[kBatch], c1[kBatch], av[kBatch][PW / 4];
 #pragma unroll
-        for (int kk = 0; kk < PW; kk += 4) {
-          const double av = -A[(k0 + kk + t4) + static_cast<size_t>(8 * I + g) * P];
-          const double bv = Bp[(kk + t4) + (8 * J + g) * kLdq];
-          dmma(c0, c1, av, bv);
+        for (int q = 0; q < kBatch; ++q) {
+          const int tile = base + q * kWarps;
+          Cp[q] = nullptr;
+          if (tile >= nr * nbt) continue;
+          const int I = tile % nr, J = tile / nr;
+          Cp[q] = B + (8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
+          c0[q] = Cp[q][0];
+          c1[q] = Cp[q][P];
+#pragma unroll
+          for (int kk = 0; kk < PW / 4; ++kk)
+            av[q][kk] = -A[(k0 + 4 * kk + t4) + static_cast<size_t>(8 * I + g) * P];
         }
-        C[0] = c0;
-        C[P] = c1;
+#pragma unroll
+        for (int q = 0; q < kBatch; ++q) {
+          if (!Cp[q]) continue;
+          const int J = (base + q * kWarps) / nr;
+#pragma unroll
+          for (int kk = 0; kk < PW / 4; ++kk)
+            dmma(c0[q], c1[q], av[q][kk], Bp[(4 * kk + t4) + (8 * J + g) * kLdq]);
+          Cp[q][0] = c0[q];
+          Cp[q][P] = c1[q];
+        }
       }
       __syncthreads();
     }
