@@ -67,6 +67,20 @@ __device__ __forceinline__ void gemv_item_rows(const VItem& I, int rb, int re, c
         if (j < I.cols) acc = cfma(a_pre[q], xs[j], acc);
       }
       int j = g + 4 * groups;
+      // 8 independent 16-byte loads in flight per thread (Little's law:
+      // ~35 KB in flight per SM are needed to cover HBM latency).
+      double2 acc2 = make_double2(0.0, 0.0);
+      for (; j + 7 * groups < I.cols; j += 8 * groups) {
+        double2 a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = ldg2(Ar + (j + q * groups) * lda);
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          acc = cfma(a[q], xs[j + q * groups], acc);
+          acc2 = cfma(a[q + 1], xs[j + (q + 1) * groups], acc2);
+        }
+      }
+      acc = cadd(acc, acc2);
       for (; j + 3 * groups < I.cols; j += 4 * groups) {
         const double2 a0 = ldg2(Ar + j * lda);
         const double2 a1 = ldg2(Ar + (j + groups) * lda);
