@@ -353,7 +353,9 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_finish_kernel(int64_t n
 // Row-block size for a split phase: enough units for ~2 CTAs per SM,
 // 8 / 16 / multiple-of-32 rows (the shapes the GEMV item kernel maps well).
 int split_rows(int total_rows, int sms) {
-  const int want = (total_rows + 2 * sms - 1) / (2 * sms);
+  // ~8 units per SM: small units balance the SMs (no tail wave) at the cost
+  // of re-gathering x per unit (a few % of the matrix bytes at these sizes).
+  const int want = (total_rows + 8 * sms - 1) / (8 * sms);
   if (want <= 8) return 8;
   if (want <= 16) return 16;
   return std::min(256, (want + 31) & ~31);
