@@ -91,6 +91,19 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def gmres_roofline(state, its, restart, solve_s, hbm_gbs) -> dict:
+    """Pinned bytes of all timed iterations: operators + fused
+    CGS2 vector traffic 16 dim (4(j+1)+6) at Arnoldi step j."""
+    total = 0.0
+    for n_it in its:
+        for i in range(n_it):
+            j = i % restart
+            total += state["pinned_bytes"] + 16.0 * state["dim"] * (4 * (j + 1) + 6)
+    achieved = total / solve_s / 1e9
+    return {"pinned_bytes_per_iteration_operators": state["pinned_bytes"],
+            "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s", "frac": achieved / hbm_gbs}
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -202,7 +215,9 @@ def run_b200(args, rank, world, local):
         hps._check(hps._lib.hpsb_fgmres_dev(sk._h, pc._h, ctypes.c_void_p(sk.rhs_dev_ptr(0)),
                                             ctypes.c_void_p(x.data_ptr()), cfg,
                                             ctypes.byref(rep)), allow=(hps.OK,))
-        state.update(dim=sk.dim, pc_bytes=pc.bytes_per_apply, depth=hier.depth)
+        fe, fm = hier.pinned_flops()
+        state.update(dim=sk.dim, pc_bytes=pc.bytes_per_apply, depth=hier.depth,
+                     pinned_flops=fe + fm, pinned_bytes=pc.pinned_bytes_per_iteration)
         return t_setup, rep.seconds, rep.iterations, sk.dim
 
     def flush_l2():
@@ -318,6 +333,15 @@ def run_b200(args, rank, world, local):
                   "ms_per_step": 1e3 * setup_max / args.steps},
         "solve_ms_per_step": 1e3 * solve_max / args.steps,
         "precond_bytes_per_apply": state["pc_bytes"],
+        # Path-level rooflines with SURVEY §8(d)'s pinned numerators (one rank's
+        # share when sharded): setup flops vs the measured FP64 DMMA peak, and
+        # per-iteration operator + CGS2 vector bytes vs the measured HBM copy rate.
+        "roofline_setup": {
+            "pinned_flops": state["pinned_flops"],
+            "achieved": state["pinned_flops"] * args.steps / setup_max / 1e12,
+            "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
+            "frac": state["pinned_flops"] * args.steps / setup_max / 1e12 / FP64_DMMA_PEAK_TFLOPS},
+        "roofline_gmres": gmres_roofline(state, its, restart, solve_max, peaks["hbm_gbs"]),
         "roofline": roof,
         "kernels": kernels,
         "gpu_launches": launches,

@@ -193,6 +193,16 @@ hpsb_status hpsb_context_profile_reset(hpsb_context ctx);
 /* Algorithmic operator bytes one preconditioner apply streams (roofline). */
 int64_t hpsb_precond_bytes(hpsb_precond p);
 
+/* Pinned algorithmic work of SURVEY.md §8(d) (the roofline numerators):
+ * setup flops = sum_e (ni^3/3 + 2 ni^2 nb + 8 nb^3)
+ *             + sum_merges 8 [(8/3) s^3 + 4 s^2 (p1+p2) + s (p1+p2)^2];
+ * operator bytes per outer FGMRES iteration =
+ *   16 [nnz(M_1) + sum_{l<depth} (2 (2s)^2 + 2 s (p1+p2)) + ci nnz(M_depth)]
+ * (sub-block entries without identities; vector traffic excluded).          */
+hpsb_status hpsb_hierarchy_pinned_flops(hpsb_hierarchy h, double* element_flops,
+                                        double* merge_flops);
+double hpsb_precond_pinned_bytes(hpsb_precond p);
+
 /* ------------------------------------------------------------ multi-GPU
  * Quadtree-subtree sharding over G = 2^g ranks, one per GPU.
  * Attach a communicator to a context BEFORE building objects on it; every

@@ -125,6 +125,8 @@ _sig("hpsb_local_group_destroy", _st, _VP)
 _sig("hpsb_context_attach_local", _st, _VP, _VP, ctypes.c_int)
 _sig("hpsb_context_comm_info", _st, _VP, _I, _I)
 _sig("hpsb_partition", _st, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I, _I)
+_sig("hpsb_hierarchy_pinned_flops", _st, _VP, _D, _D)
+_sig("hpsb_precond_pinned_bytes", ctypes.c_double, _VP)
 
 
 def _check(status: int, allow=(OK,)) -> int:
@@ -398,6 +400,12 @@ class MergeHierarchy(_Handle):
         self.depth, self.total_levels = d.value, t.value
         self.device_bytes, self.build_seconds = b.value, s.value
 
+    def pinned_flops(self) -> tuple[float, float]:
+        """SURVEY §8(d) pinned setup flops: (element stage, merges)."""
+        fe, fm = ctypes.c_double(), ctypes.c_double()
+        _check(_lib.hpsb_hierarchy_pinned_flops(self._h, ctypes.byref(fe), ctypes.byref(fm)))
+        return fe.value, fm.value
+
     def level_blocks(self, level: int):
         """(first_face, {(r, c): bs x bs block}) of the level system M_l."""
         nb, ff = ctypes.c_int(), ctypes.c_int()
@@ -432,6 +440,11 @@ class MgPreconditioner(_Handle):
     def bytes_per_apply(self) -> int:
         """Algorithmic operator bytes one apply streams (the HBM roofline numerator)."""
         return int(_lib.hpsb_precond_bytes(self._h))
+
+    @property
+    def pinned_bytes_per_iteration(self) -> float:
+        """SURVEY §8(d) pinned operator bytes per outer FGMRES iteration."""
+        return float(_lib.hpsb_precond_pinned_bytes(self._h))
 
     def apply(self, v) -> np.ndarray:
         v = _cplx(v)

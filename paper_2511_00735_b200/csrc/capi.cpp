@@ -234,6 +234,27 @@ hpsb_status hpsb_context_profile_reset(hpsb_context ctx) {
 
 int64_t hpsb_precond_bytes(hpsb_precond p) { return p ? hpsb::precond_bytes(p->p) : -1; }
 
+hpsb_status hpsb_hierarchy_pinned_flops(hpsb_hierarchy h, double* element_flops,
+                                        double* merge_flops) {
+  return guarded([&] {
+    REQUIRE(h, "hierarchy_pinned_flops: null handle");
+    double fe = 0, fm = 0;
+    hpsb::hierarchy_pinned(h->h.get(), &fe, &fm, nullptr);
+    if (element_flops) *element_flops = fe;
+    if (merge_flops) *merge_flops = fm;
+    return HPSB_OK;
+  });
+}
+
+double hpsb_precond_pinned_bytes(hpsb_precond p) {
+  if (!p) return -1.0;
+  try {
+    return hpsb::precond_pinned_bytes(p->p);
+  } catch (...) {
+    return -1.0;
+  }
+}
+
 hpsb_status hpsb_nccl_unique_id(unsigned char id[128]) {
   return guarded([&] {
     REQUIRE(id, "nccl_unique_id: null output");

@@ -338,6 +338,25 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
   return h;
 }
 
+void hierarchy_pinned(const Hierarchy* h, double* elem_flops, double* merge_flops,
+                      double* level_entries) {
+  const Elements* el = h->sk->el;
+  const double ni = static_cast<double>(el->m) * el->m, nb = el->nb;
+  const double ne = static_cast<double>(el->n) * el->n;
+  if (elem_flops) *elem_flops = ne * (ni * ni * ni / 3.0 + 2.0 * ni * ni * nb + 8.0 * nb * nb * nb);
+  double fm = 0, ent = 0;
+  for (const auto& L : h->levels) {
+    if (L->coarse) continue;
+    for (const MergeRec& mr : L->merges) {
+      const double s = mr.s, p = mr.p1 + mr.p2;
+      fm += 8.0 * ((8.0 / 3.0) * s * s * s + 4.0 * s * s * p + s * p * p);
+      ent += 2.0 * (2.0 * s) * (2.0 * s) + 2.0 * s * p;
+    }
+  }
+  if (merge_flops) *merge_flops = fm;
+  if (level_entries) *level_entries = ent;
+}
+
 // M_l in the reference's bs x bs block layout (for parity tests / export).
 void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,
                             int* keys, double* data) {

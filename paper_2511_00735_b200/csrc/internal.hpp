@@ -321,6 +321,11 @@ void destroy_precond(Precond* p);
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev);
 void precond_apply_host(Precond* p, const double2* v_host, double2* z_host);
 int64_t precond_bytes(const Precond* p);
+// Pinned SURVEY §8(d) work: element flops, merge flops (all merges of the
+// problem), and per-level operator entries used by precond_pinned_bytes.
+void hierarchy_pinned(const Hierarchy* h, double* elem_flops, double* merge_flops,
+                      double* level_entries);
+double precond_pinned_bytes(const Precond* p);
 void merge_pair(Context* ctx, int m, const double2* T1, const double2* H1, const double2* T2,
                 const double2* H2, int alpha, int beta, double2* T, double2* H);
 hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs_dev, double2* x_dev,

@@ -713,6 +713,24 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
 
 int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }
 
+double precond_pinned_bytes(const Precond* p) {
+  // 16 [nnz(M_1) + sum_l (2 LU_l + B_l + C_l) + ci nnz(M_depth)]
+  const Skeleton* sk = p->h->sk;
+  const int nb = sk->el->nb, ne = sk->el->n * sk->el->n;
+  double m1 = 0;
+  for (int e = 0; e < ne; ++e) {
+    double k = 0;
+    for (int b = 0; b < nb; ++b) k += sk->h_in[static_cast<size_t>(e) * nb + b] >= 0;
+    m1 += k * k;
+  }
+  double levels = 0;
+  hierarchy_pinned(p->h, nullptr, nullptr, &levels);
+  double coarse = 0;
+  for (const ChildBox& c : p->h->levels[p->cfg.depth - 1]->children)
+    coarse += static_cast<double>(c.P) * c.P;
+  return 16.0 * (m1 + levels + p->cfg.coarse_iters * coarse);
+}
+
 void precond_apply_host(Precond* p, const double2* v, double2* z) {
   Context* ctx = p->ctx;
   DevBuf<double2> vd(p->dim), zd(p->dim);
