@@ -194,8 +194,8 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
       }
       cb.run(ctx);
       tr.mark("gather_enqueue");
-      HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
-      tr.mark("gather_wait");
+      // No synchronisation: buffers are freed stream-ordered, so the host
+      // moves on to the next level's bookkeeping while the GPU works.
     }
     tnew_prev.release();
 
@@ -264,7 +264,7 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
         pre.copy(T2pp, P2, Tn + p1 + static_cast<size_t>(p1) * q, q, p2, p2, 1.0);
         g1.add(T2ss, P2, T1ss, P1, W, s, s, s, s, -1.0, 1.0);
         g1.add(T2ss, P2, T1sp, P1, Rg, s, s, p1, s, 1.0, 0.0);
-        inv.ops.push_back(InvOp{W, s, s, mr.group, 0});
+        inv.ops.push_back(InvOp{W, s, s, (level << 20) | mr.group, 0});
         g2.add(W, s, Rg, s, X1g, s, s, q, s, 1.0, 0.0);
         g3.add(T1ss, P1, X1g, s, X2g, s, s, q, s, -1.0, 1.0);
         g3.add(T1ps, P1, X1g, s, Tn, q, p1, q, s, 1.0, 1.0);
@@ -278,16 +278,7 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
       g4.run(ctx);
       L->merge_flops = g1.flops + g2.flops + g3.flops + g4.flops;
       for (const auto& mr : L->merges) L->merge_flops += 8.0 * mr.s * mr.s * mr.s;  // inverse
-      int st = 0;
       tr.mark("merge_enqueue");
-      HPSB_CUDA(cudaMemcpyAsync(&st, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
-      tr.mark("merge_wait");
-      if (st) {
-        const int gi = st - 1;
-        throw std::runtime_error("eliminate_level: singular merge block at face " +
-                                 std::to_string(g.groups[level - 1][gi].front()));
-      }
       // ---- next level's boxes (positions for every group, maps for ours)
       std::vector<HostBox> next(ng);
       for (int gi = 0; gi < ng; ++gi) {
@@ -331,7 +322,15 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     h->levels.push_back(std::move(L));
   }
   HPSB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
+  int st = 0;
+  HPSB_CUDA(cudaMemcpyAsync(&st, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  tr.mark("final_wait");
+  if (st) {  // first singular group pivot (inverse status tag = level << 20 | group) + 1
+    const int tag = st - 1, level = tag >> 20, gi = tag & ((1 << 20) - 1);
+    throw std::runtime_error("eliminate_level: singular merge block at face " +
+                             std::to_string(g.groups[level - 1][gi].front()));
+  }
   float ms = 0;
   HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
   h->build_seconds = ms * 1e-3;
