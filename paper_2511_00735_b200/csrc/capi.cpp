@@ -126,7 +126,9 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     }
     auto& st = hpsb::staging();
     if (!st.base) {
-      st.size = size_t(64) << 20;
+      // Large enough that one setup's descriptor uploads never wrap (a wrap
+      // synchronises the stream and stalls host/device overlap).
+      st.size = size_t(512) << 20;
       HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.base), st.size));
     }
     st.stream = ctx->c.stream;
