@@ -200,7 +200,7 @@ def run_b200(args, rank, world, local):
         w1 = time.perf_counter()
         sk = hps.assemble_skeleton(el, prob)
         w2 = time.perf_counter()
-        hier = hps.build_hierarchy(sk)
+        hier = hps.build_hierarchy(sk, factor_coarse=False)
         w3 = time.perf_counter()
         pc = hps.build_preconditioner(hier, coarse_iters=4)
         t_setup = ctx.timer_stop()
@@ -292,7 +292,7 @@ def run_b200(args, rank, world, local):
     # ---- e2e through the public ABI with host buffers (rhs H2D, x D2H)
     el_h = hps.build_elements(ctx, prob)
     sk_h = hps.assemble_skeleton(el_h, prob)
-    hier_h = hps.build_hierarchy(sk_h)
+    hier_h = hps.build_hierarchy(sk_h, factor_coarse=False)
     pc_h = hps.build_preconditioner(hier_h, coarse_iters=4)
     rhs_host = torch.from_numpy(sk_h.rhs()).pin_memory().numpy()
     e2e_dof, e2e_t = 0, 0.0
@@ -311,7 +311,7 @@ def run_b200(args, rank, world, local):
     t0 = time.perf_counter()
     el2 = hps.build_elements(ctx, prob)
     sk2 = hps.assemble_skeleton(el2, prob)
-    hier2 = hps.build_hierarchy(sk2)
+    hier2 = hps.build_hierarchy(sk2, factor_coarse=False)
     hps.build_preconditioner(hier2, coarse_iters=4)
     e2e_setup = ne / (time.perf_counter() - t0)
 

@@ -57,7 +57,7 @@ typedef struct hpsb_mg_config {
   int depth;        /* number of hierarchy levels used (>= 2) */
   int gamma;        /* coarse calls per intermediate level (1 = V-cycle) */
   int coarse_iters; /* unpreconditioned GMRES steps at the deepest level */
-  int exact_coarse; /* reserved: dense coarse solve (not on the B200 path yet) */
+  int exact_coarse; /* dense inverse of M_depth instead of coarse GMRES (gamma = 1) */
 } hpsb_mg_config;
 
 /* KrylovConfig (proj/include/hps/krylov.hpp:15-21). */
@@ -134,11 +134,18 @@ hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs);
 /* y = M x (BlockMatrix::apply, proj/src/block_matrix.cpp:23-31). */
 hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y);
 hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x_dev, double* y_dev);
+/* recover_solution(mesh, elements, graph, g) (proj/src/problems.cpp:60-92):
+ * the field on every element's corner-free nodes from the skeleton solution
+ * x (dim complex) of right-hand side r.  field: n^2 x ((N+1)^2 - 4) complex,
+ * element-major, nodes in the compressed order of element.cpp:47-53.       */
+hpsb_status hpsb_recover(hpsb_skeleton sk, const double* x, int r, double* field);
+hpsb_status hpsb_recover_dev(hpsb_skeleton sk, const double* x_dev, int r, double* field_dev);
 
 /* ----------------------------------------------------------- merges
  * build_hierarchy(system, depth, factor_coarse) (proj/src/dissection.cpp:200-227):
  * level-by-level Schur elimination of the merge tree, batched per level.
- * depth = 0 means all levels.  factor_coarse is accepted for API parity.    */
+ * depth = 0 means all levels.  factor_coarse != 0 also factors M_depth
+ * (dense inverse, dissection.cpp:225) for hpsb_direct_solve.              */
 hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
                                  hpsb_hierarchy* out);
 hpsb_status hpsb_hierarchy_destroy(hpsb_hierarchy h);
@@ -160,6 +167,12 @@ hpsb_status hpsb_precond_destroy(hpsb_precond p);
 /* z = MG(v) (MgPreconditioner::apply, proj/src/multigrid.cpp:30-100). */
 hpsb_status hpsb_precond_apply(hpsb_precond p, const double* v, double* z);
 hpsb_status hpsb_precond_apply_dev(hpsb_precond p, const double* v_dev, double* z_dev);
+/* direct_solve(hierarchy, rhs) (proj/src/dissection.cpp:240-292): forward
+ * elimination through every level, the coarse solve, back substitution.
+ * Needs a full-depth hierarchy built with factor_coarse != 0 (the dense
+ * coarse factor of dissection.cpp:225); else HPSB_INVALID_ARGUMENT.       */
+hpsb_status hpsb_direct_solve(hpsb_hierarchy h, const double* rhs, double* x);
+hpsb_status hpsb_direct_solve_dev(hpsb_hierarchy h, const double* rhs_dev, double* x_dev);
 
 /* Restarted (F)GMRES on the skeleton system (proj/src/krylov.cpp:45-178).
  * precond == NULL runs unpreconditioned GMRES.  Returns HPSB_NO_CONVERGENCE

@@ -99,6 +99,8 @@ _sig("hpsb_skeleton_rhs", _st, _VP, ctypes.c_int, _D)
 _sig("hpsb_skeleton_rhs_dev", _VP, _VP, ctypes.c_int)
 _sig("hpsb_skeleton_apply", _st, _VP, _D, _D)
 _sig("hpsb_skeleton_apply_dev", _st, _VP, _VP, _VP)
+_sig("hpsb_recover", _st, _VP, _D, ctypes.c_int, _D)
+_sig("hpsb_recover_dev", _st, _VP, _VP, ctypes.c_int, _VP)
 _sig("hpsb_hierarchy_build", _st, _VP, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_VP))
 _sig("hpsb_hierarchy_destroy", _st, _VP)
 _sig("hpsb_hierarchy_info", _st, _VP, _I, _I, ctypes.POINTER(ctypes.c_int64), _D)
@@ -107,6 +109,8 @@ _sig("hpsb_merge_pair", _st, _VP, ctypes.c_int, _D, _D, _D, _D, ctypes.c_int, ct
 _sig("hpsb_precond_create", _st, _VP, MgConfig, ctypes.POINTER(_VP))
 _sig("hpsb_precond_destroy", _st, _VP)
 _sig("hpsb_precond_apply", _st, _VP, _D, _D)
+_sig("hpsb_direct_solve", _st, _VP, _D, _D)
+_sig("hpsb_direct_solve_dev", _st, _VP, _VP, _VP)
 _sig("hpsb_precond_apply_dev", _st, _VP, _VP, _VP)
 _sig("hpsb_fgmres", _st, _VP, _VP, _D, _D, KrylovConfig, ctypes.POINTER(SolveReport))
 _sig("hpsb_fgmres_dev", _st, _VP, _VP, _VP, _VP, KrylovConfig, ctypes.POINTER(SolveReport))
@@ -380,6 +384,15 @@ class SkeletonSystem(_Handle):
     def rhs_dev_ptr(self, r: int = 0) -> int:
         return int(_lib.hpsb_skeleton_rhs_dev(self._h, r))
 
+    def recover(self, g, r: int = 0) -> np.ndarray:
+        """recover_solution (proj/src/problems.cpp:60-92): the field on every
+        element's corner-free nodes, shape (n^2, (N+1)^2 - 4)."""
+        g = _cplx(g)
+        el = self.elements
+        field = np.zeros((el.n * el.n, (el.order + 1) ** 2 - 4), dtype=np.complex128)
+        _check(_lib.hpsb_recover(self._h, _dp(g.view(np.float64)), r, _dp(field.view(np.float64))))
+        return field
+
 
 def assemble_skeleton(elements: ElementRecords, prob: Problem) -> SkeletonSystem:
     t = _cplx(prob.tside)
@@ -399,6 +412,14 @@ class MergeHierarchy(_Handle):
                                         ctypes.byref(s)))
         self.depth, self.total_levels = d.value, t.value
         self.device_bytes, self.build_seconds = b.value, s.value
+
+    def direct_solve(self, rhs) -> np.ndarray:
+        """direct_solve (proj/src/dissection.cpp:240-292); needs a full-depth
+        hierarchy built with factor_coarse=True."""
+        rhs = _cplx(rhs)
+        x = np.zeros_like(rhs)
+        _check(_lib.hpsb_direct_solve(self._h, _dp(rhs.view(np.float64)), _dp(x.view(np.float64))))
+        return x
 
     def pinned_flops(self) -> tuple[float, float]:
         """SURVEY §8(d) pinned setup flops: (element stage, merges)."""

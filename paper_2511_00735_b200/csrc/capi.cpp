@@ -25,6 +25,10 @@ struct hpsb_skeleton_s {
 };
 struct hpsb_hierarchy_s {
   std::unique_ptr<hpsb::Hierarchy> h;
+  // factor_coarse: the exact (dense-inverse) coarse solve at the built depth,
+  // used by direct_solve (dissection.cpp:225, :240-292).
+  hpsb::Precond* direct = nullptr;
+  ~hpsb_hierarchy_s() { hpsb::destroy_precond(direct); }
 };
 struct hpsb_precond_s {
   hpsb::Precond* p = nullptr;
@@ -488,13 +492,42 @@ hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y) {
   });
 }
 
+hpsb_status hpsb_recover_dev(hpsb_skeleton sk, const double* x, int r, double* field) {
+  return guarded([&] {
+    REQUIRE(sk && x && field, "recover: null argument");
+    hpsb::recover_field(sk->s.get(), reinterpret_cast<const double2*>(x), r,
+                        reinterpret_cast<double2*>(field));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_recover(hpsb_skeleton sk, const double* x, int r, double* field) {
+  return guarded([&] {
+    REQUIRE(sk && x && field, "recover: null argument");
+    auto* S = sk->s.get();
+    cudaStream_t st = S->ctx->stream;
+    const auto* el = S->el;
+    const size_t nf = static_cast<size_t>(el->n) * el->n * ((el->order + 1) * (el->order + 1) - 4);
+    hpsb::DevBuf<double2> d_f(nf);
+    HPSB_CUDA(cudaMemcpyAsync(S->x_buf.p, x, S->dim * sizeof(double2), cudaMemcpyHostToDevice, st));
+    hpsb::recover_field(S, S->x_buf.p, r, d_f.p);
+    HPSB_CUDA(cudaMemcpyAsync(field, d_f.p, nf * sizeof(double2), cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    return HPSB_OK;
+  });
+}
+
 hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
                                  hpsb_hierarchy* out) {
-  (void)factor_coarse;
   return guarded([&] {
     REQUIRE(sk && out, "hierarchy_build: null argument");
     auto h = std::make_unique<hpsb_hierarchy_s>();
     h->h = hpsb::build_hierarchy(sk->s.get(), depth);
+    if (factor_coarse && h->h->depth >= 2) {
+      hpsb_mg_config c{};
+      c.depth = h->h->depth, c.gamma = 1, c.coarse_iters = 0, c.exact_coarse = 1;
+      h->direct = hpsb::create_precond(h->h.get(), c);
+    }
     *out = h.release();
     return HPSB_OK;
   });
@@ -547,6 +580,27 @@ hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_preco
     auto p = std::make_unique<hpsb_precond_s>();
     p->p = hpsb::create_precond(h->h.get(), cfg);
     *out = p.release();
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_direct_solve_dev(hpsb_hierarchy h, const double* rhs, double* x) {
+  return guarded([&] {
+    REQUIRE(h && rhs && x, "direct_solve: null argument");
+    REQUIRE(h->direct && h->h->depth == h->h->total_levels,
+            "direct_solve: hierarchy not built to full depth");
+    hpsb::precond_apply(h->direct, reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x));
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_direct_solve(hpsb_hierarchy h, const double* rhs, double* x) {
+  return guarded([&] {
+    REQUIRE(h && rhs && x, "direct_solve: null argument");
+    REQUIRE(h->direct && h->h->depth == h->h->total_levels,
+            "direct_solve: hierarchy not built to full depth");
+    hpsb::precond_apply_host(h->direct, reinterpret_cast<const double2*>(rhs),
+                             reinterpret_cast<double2*>(x));
     return HPSB_OK;
   });
 }

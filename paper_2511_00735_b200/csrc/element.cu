@@ -44,7 +44,19 @@ struct ElemArgs {
   const int* elist;  // optional element list (fallback re-run)
   int nlist;
   int npad, nbc;     // v2: padded interior size (multiple of 16), padded rhs count
+  double* Y;         // [e][nb+2][ni]: L_ii^{-1} [L_iG | re b~ | im b~] kept for recovery
 };
+
+// Keep Y = L_ii^{-1} [L_iG | b~] (ld ldy in the workspace) for the solution
+// recovery u_i = Y_b - Y_G u_G (problems.cpp:60-92 / element.cpp:176-188).
+__device__ __forceinline__ void keep_interior(const ElemArgs& a, int e, const double* Y, int ldy) {
+  const int ni = a.ni, cols = a.nb + 2;
+  double* dst = a.Y + static_cast<size_t>(e) * ni * cols;
+  for (int idx = threadIdx.x; idx < ni * cols; idx += blockDim.x) {
+    const int q = idx % ni, c = idx / ni;
+    dst[idx] = Y[q + static_cast<size_t>(c) * ldy];
+  }
+}
 
 // Boundary Schur complement and ItI map from the interior solve
 // Y = L_ii^{-1} [L_iG | b~] (ld ldy, interior order q = (i-1) m + (j-1)):
@@ -304,6 +316,7 @@ __global__ void __launch_bounds__(kThreads) element_kernel(ElemArgs a) {
     }
     }
     __syncthreads();
+    keep_interior(a, e, Y, ni);
     const bool ok = iti_epilogue(a, e, Y, ni, S, f, perm, red_v, red_i);
     if (tid == 0) a.status[e] = (s_fail ? 1 : 0) | (ok ? 0 : 2);  // 1: singular L_ii
   }
@@ -585,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 2) element_v2_kernel(ElemArgs a) {
       }
       __syncthreads();
     }
+    keep_interior(a, e, B, P);
     const bool ok = iti_epilogue(a, e, B, P, S, f, perm, red_v, red_i);
     if (tid == 0) a.status[e] = ok ? 0 : 2;
   }
@@ -624,6 +638,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   el->T.alloc(static_cast<size_t>(ne) * nb * nb);
   el->H.alloc(static_cast<size_t>(ne) * nb);
   el->status.alloc(ne);
+  el->Y.alloc(static_cast<size_t>(ne) * ni * (nb + 2));
   HPSB_CUDA(cudaMemsetAsync(el->status.p, 0, ne * sizeof(int), ctx->stream));
   // Sharded (one rank per GPU): build only this rank's quadtree subtree.
   el->part = make_partition(build_face_graph(n), ctx->world(), ctx->rank());
@@ -640,7 +655,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   a.ne = ne, a.order = order, a.m = m, a.ni = ni, a.nb = nb, a.eta = eta;
   a.mass = d_mass.p, a.diff = d_diff.p, a.stiff = d_stiff.p;
   a.coeff = coeff_dev, a.source = source_dev;
-  a.T = el->T.p, a.H = el->H.p, a.status = el->status.p;
+  a.T = el->T.p, a.H = el->H.p, a.status = el->status.p, a.Y = el->Y.p;
   a.npad = (ni + PW - 1) / PW * PW;
   a.nbc = (nb + 2 + 7) / 8 * 8;
   if (sharded) a.elist = d_own.p, a.nlist = nwork;

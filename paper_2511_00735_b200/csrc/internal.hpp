@@ -276,6 +276,7 @@ struct Elements {
   DevBuf<double2> T;  // [e][nb*nb]
   DevBuf<double2> H;  // [e][nb]
   DevBuf<int> status; // per-element failure flags
+  DevBuf<double> Y;   // [e][nb+2][ni] L_ii^{-1}[L_iG | re b~ | im b~] (solution recovery)
   double build_seconds = 0;
   Partition part;     // sharding of the elements over the context's ranks
 };
@@ -291,6 +292,7 @@ struct Skeleton {
   // Element-level in/out skeleton indices: [e][nb] (-1 on physical sides).
   std::vector<int> h_in, h_out;
   DevBuf<int> d_in, d_out;
+  DevBuf<double2> tside;  // [nrhs][e][nb] physical-side impedance data
   VPlan apply_plan;      // y = x + sum_e scatter(T_e gather(x))
   DevBuf<double2> x_buf, y_buf;  // plan endpoints
 };
@@ -313,6 +315,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
                                          const double* coeff_dev, const double2* source_dev);
 std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs);
 void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev);
+void recover_field(const Skeleton* sk, const double2* x_dev, int rhs_index, double2* field_dev);
 std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth);
 void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,
                             int* keys, double* data);

@@ -29,6 +29,7 @@
 #include "gemv_device.cuh"
 #include "hierarchy.hpp"
 #include "vcycle_small.hpp"
+#include "zgemm.hpp"
 
 namespace hpsb {
 
@@ -50,6 +51,10 @@ struct Precond {
   bool coarse_fused = false;
   DevBuf<VItem> coarse_items;
   int coarse_nitems = 0, coarse_max_cols = 0, coarse_csize = 16;
+  // exact coarse (MgConfig.exact_coarse): dense inverse of M_depth + one GEMV
+  DevBuf<double2> cinv;
+  DevBuf<int> exact_yi;
+  VPlan exact_mv;
   // per-level execution order of the sweeps
   struct Step {
     int level = 0, small = -1;
@@ -71,10 +76,29 @@ struct Precond {
 };
 
 constexpr int kMaxCoarseIters = 30;
+constexpr int64_t kExactCoarseMax = 24576;  // dense coarse inverse: <= 9.7 GB
 constexpr size_t kSmallMergeSmemMax = 160 * 1024;
 
 namespace {
 constexpr int kCoarseThreads = 1024;
+
+// Dense M_depth = I + sum_boxes scatter(T_box): box b writes rows out_b (its
+// outgoing slots, owned by b alone) and columns in_b; the identity was
+// written beforehand and no box touches a diagonal entry (in != out).
+__global__ void coarse_densify_kernel(const double2* __restrict__ tperm, const int64_t* __restrict__ toff,
+                                      const int* __restrict__ P, const int* __restrict__ idx,
+                                      const int64_t* __restrict__ at, double2* M, int64_t ld) {
+  const int b = blockIdx.y;
+  const int n = P[b];
+  const double2* T = tperm + toff[b];
+  const int* in = idx + at[2 * b];
+  const int* out = idx + at[2 * b + 1];
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < int64_t(n) * n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(k % n), j = static_cast<int>(k / n);
+    M[out[i] + in[j] * ld] = T[k];
+  }
+}
 namespace cg = cooperative_groups;
 __device__ void make_givens(double2 a, double2 b, double& c, double2& s);
 __device__ void apply_givens(double c, double2 s, double2& a, double2& b);
@@ -379,11 +403,12 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   if (!cfg.exact_coarse && cfg.gamma < 1) throw InvalidArgument("MgPreconditioner: gamma must be >= 1");
   if (!cfg.exact_coarse && cfg.coarse_iters < 1)
     throw InvalidArgument("MgPreconditioner: coarse_iters must be >= 1");
-  if (cfg.exact_coarse) throw InvalidArgument("MgPreconditioner: exact_coarse is not on the B200 path");
-  if (cfg.gamma != 1) throw InvalidArgument("MgPreconditioner: gamma > 1 is not on the B200 path");
+  // multigrid.cpp:71: the exact coarse mode runs gamma = 1.
+  if (!cfg.exact_coarse && cfg.gamma != 1)
+    throw InvalidArgument("MgPreconditioner: gamma > 1 is not on the B200 path");
   if (cfg.depth != h->depth)
     throw InvalidArgument("MgPreconditioner: depth must equal the built hierarchy depth on the B200 path");
-  if (cfg.coarse_iters > 60) throw InvalidArgument("MgPreconditioner: coarse_iters must be <= 60");
+  if (!cfg.exact_coarse && cfg.coarse_iters > 60) throw InvalidArgument("MgPreconditioner: coarse_iters must be <= 60");
   Context* ctx = h->ctx;
   auto p = std::make_unique<Precond>();
   p->h = h, p->cfg = cfg, p->ctx = ctx;
@@ -566,7 +591,9 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   const LevelOps& C = *h->levels[cfg.depth - 1];
   p->off_d = static_cast<int64_t>(C.first_face) * sk->bs;
   p->dim_d = p->dim - p->off_d;
-  const int ci = cfg.coarse_iters;
+  if (cfg.exact_coarse && p->dim_d > kExactCoarseMax)
+    throw InvalidArgument("MgPreconditioner: exact coarse system too large for a dense inverse");
+  const int ci = cfg.exact_coarse ? 0 : cfg.coarse_iters;
   p->V.alloc(static_cast<size_t>(p->dim_d) * (ci + 1));
   p->cv.alloc(p->dim_d);
   p->cw.alloc(p->dim_d);
@@ -620,10 +647,64 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
   }
+  if (cfg.exact_coarse) {
+    // exact_lu = LU(M_depth.to_dense()) (multigrid.cpp:22-27); here the dense
+    // inverse (blocked Gauss-Jordan on the DMMA GEMMs) and one GEMV per apply.
+    const int64_t nd = p->dim_d;
+    p->cinv.alloc(static_cast<size_t>(nd) * nd);
+    CopyBatch cb;
+    cb.identity(p->cinv.p, static_cast<int>(nd), static_cast<int>(nd));
+    cb.run(ctx);
+    std::vector<int64_t> toff, at;
+    std::vector<int> Ps;
+    for (size_t k = 0; k < C.children.size(); ++k) {
+      toff.push_back(static_cast<int64_t>(C.children[k].t_off));
+      Ps.push_back(C.children[k].P);
+      at.push_back(static_cast<int64_t>(in_at[k]));
+      at.push_back(static_cast<int64_t>(out_at[k]));
+    }
+    DevBuf<int64_t> d_toff, d_at;
+    DevBuf<int> d_P, d_status(1);
+    d_toff.upload(toff, ctx->stream);
+    d_at.upload(at, ctx->stream);
+    d_P.upload(Ps, ctx->stream);
+    HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(int), ctx->stream));
+    if (!C.children.empty()) {
+      KernelScope ks(ctx, "coarse_densify", 0.0, 0.0);
+      coarse_densify_kernel<<<dim3(32, static_cast<unsigned>(C.children.size())), 256, 0, ctx->stream>>>(
+          C.tperm.p, d_toff.p, d_P.p, p->coarse_idx.p, d_at.p, p->cinv.p, nd);
+      HPSB_LAUNCHED(ctx);
+    }
+    InverseBatch inv;
+    inv.ops.push_back(InvOp{p->cinv.p, static_cast<int>(nd), static_cast<int>(nd), 0, 0});
+    inv.run(ctx, d_status.p);
+    int st = 0;
+    HPSB_CUDA(cudaMemcpyAsync(&st, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (st) throw std::runtime_error("MgPreconditioner: singular coarse system");
+    std::vector<int> yi(nd);
+    for (int64_t k = 0; k < nd; ++k) yi[k] = static_cast<int>(p->off_d + k);
+    p->exact_yi.upload(yi, ctx->stream);
+    // z_tail = M_depth^{-1} r_tail, column chunks accumulate (beta = 1)
+    constexpr int kChunk = 4096;
+    const int rows_blk = split_rows(static_cast<int>(nd), sms);
+    for (int64_t c0 = 0; c0 < nd; c0 += kChunk) {
+      const int cc = static_cast<int>(std::min<int64_t>(kChunk, nd - c0));
+      p->exact_mv.begin_phase();
+      p->exact_mv.add_split(item(p->cinv.p + c0 * nd, static_cast<int>(nd), static_cast<int>(nd), cc,
+                                 p->r.p + p->off_d + c0, nullptr, nullptr, nullptr, p->out.p,
+                                 p->exact_yi.p, 1.0, c0 > 0 ? 1.0 : 0.0, 0.0),
+                            rows_blk);
+    }
+    p->exact_mv.name = "coarse_exact";
+    p->exact_mv.finalize(ctx->stream);
+    p->coarse_fused = false;
+  }
   p->bytes_per_apply = static_cast<int64_t>(p->bytes_small) + p->down.bytes_per_run +
                        p->up.bytes_per_run + p->down_g.bytes_per_run +
                        p->up_g.bytes_per_run +
-                       static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run;
+                       static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run +
+                       p->exact_mv.bytes_per_run;
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   return p.release();
 }
@@ -648,7 +729,9 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   }
   p->run_steps(true, true, z_dev);  // top (global) levels, down
   const int ci = p->cfg.coarse_iters;
-  if (p->coarse_fused) {
+  if (p->cfg.exact_coarse) {
+    p->exact_mv.run(ctx, p->out.p, z_dev);
+  } else if (p->coarse_fused) {
     static const bool attr = [] {  // thread-safe one-time init
       HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -728,6 +811,7 @@ double precond_pinned_bytes(const Precond* p) {
   double coarse = 0;
   for (const ChildBox& c : p->h->levels[p->cfg.depth - 1]->children)
     coarse += static_cast<double>(c.P) * c.P;
+  if (p->cfg.exact_coarse) return 16.0 * (m1 + levels + double(p->dim_d) * p->dim_d);
   return 16.0 * (m1 + levels + p->cfg.coarse_iters * coarse);
 }
 

@@ -73,7 +73,8 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
   const std::vector<int>& own = el->part.own_elems;
   sk->rhs.alloc(static_cast<size_t>(nrhs) * sk->dim);
   HPSB_CUDA(cudaMemsetAsync(sk->rhs.p, 0, sk->rhs.bytes(), ctx->stream));
-  DevBuf<double2> d_t(static_cast<size_t>(nrhs) * ne * nb);
+  DevBuf<double2>& d_t = sk->tside;  // kept for the solution recovery
+  d_t.alloc(static_cast<size_t>(nrhs) * ne * nb);
   HPSB_CUDA(cudaMemcpyAsync(d_t.p, tside_host, d_t.bytes(), cudaMemcpyHostToDevice, ctx->stream));
   DevBuf<int> d_own;
   if (sharded) d_own.upload(own, ctx->stream);

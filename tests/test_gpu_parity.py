@@ -192,3 +192,104 @@ def test_unpreconditioned_gmres(hps, oracle, ctx):
     assert rep["converged"]
     assert abs(rep["iterations"] - repo["iterations"]) <= 1
     assert relf(x, xo) < TOL_SOL
+
+
+def _planewave_field_l2(oracle, n, order, kappa, field):
+    """Mass-weighted relative L2 error of a recovered field against exp(i kappa x)
+    (test_problems.cpp:65-71's plane-wave accuracy check)."""
+    x, w, _ = oracle.gll_rule(order)
+    s = oracle.index_sets(order)
+    np1, h = order + 1, 1.0 / n
+    ii, jj = s["noncorner"] // np1, s["noncorner"] % np1
+    err2 = ref2 = 0.0
+    for e in range(n * n):
+        X = h * (e % n) + 0.5 * (x[ii] + 1) * h
+        ref = np.exp(1j * kappa * X)
+        wt = (0.5 * h * w[ii]) * (0.5 * h * w[jj])
+        err2 += np.sum(wt * np.abs(field[e] - ref) ** 2)
+        ref2 += np.sum(wt * np.abs(ref) ** 2)
+    return np.sqrt(err2 / ref2)
+
+
+@pytest.mark.parametrize("name", ALL)
+def test_recover_field(hps, oracle, ctx, name):
+    # recover_solution (problems.cpp:60-92) on the same skeleton data.
+    c = case(hps, oracle, ctx, name)
+    rng = np.random.default_rng(7)
+    g = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+    f = c.sk.recover(g)
+    fo = c.S.recover(g)
+    assert f.shape == fo.shape
+    assert relf(f, fo) < TOL_OP
+
+
+def test_recover_planewave_after_fgmres(hps, oracle, ctx):
+    # End to end on the GPU: rhs -> FGMRES -> field, against the exact plane
+    # wave (test_problems.cpp:65-71, <= 1e-8) and the oracle's field (1e-9).
+    c = case(hps, oracle, ctx, "pw_n4_N16")
+    h = hps.build_hierarchy(c.sk)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    x, rep = hps.fgmres(c.sk, c.sk.rhs(), pc, restart=50, tol=1e-12)
+    assert rep["converged"]
+    f = c.sk.recover(x)
+    assert _planewave_field_l2(oracle, c.prob.n, c.prob.order, c.prob.kappa, f) < 1e-8
+    c.S.build_hierarchy(0, True)
+    fo = c.S.recover(c.S.direct_solve(c.S.rhs()))
+    assert relf(f, fo) < TOL_SOL
+
+
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg2_n8", "cfg1"])
+def test_direct_solve(hps, oracle, ctx, name):
+    # direct_solve (dissection.cpp:240-292) against the oracle's, and the
+    # residual of the dense-coarse block elimination.
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk, factor_coarse=True)
+    c.S.build_hierarchy(0, True)
+    rhs = c.sk.rhs()
+    x = h.direct_solve(rhs)
+    xo = c.S.direct_solve(c.S.rhs())
+    assert relf(x, xo) < TOL_SOL
+    assert np.linalg.norm(rhs - c.S.apply_M(x)) < 1e-9 * np.linalg.norm(rhs)
+
+
+def test_direct_solve_needs_factored_full_depth(hps, oracle, ctx):
+    c = case(hps, oracle, ctx, "cfg0")
+    h = hps.build_hierarchy(c.sk, factor_coarse=False)
+    with pytest.raises(hps.HpsError, match="full depth"):
+        h.direct_solve(c.sk.rhs())
+    h2 = hps.build_hierarchy(c.sk, depth=2, factor_coarse=True)
+    with pytest.raises(hps.HpsError, match="full depth"):
+        h2.direct_solve(c.sk.rhs())
+
+
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg2_n8", "cfg1"])
+def test_exact_coarse_full_depth(hps, oracle, ctx, name):
+    # MgConfig.exact_coarse (multigrid.cpp:22-27, :37-38) at full depth: the
+    # V-cycle is an exact inverse, so FGMRES converges in one iteration.
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk, factor_coarse=False)
+    c.S.build_hierarchy(0, True)
+    pc = hps.build_preconditioner(h, exact_coarse=True)
+    c.S.precond(depth=h.depth, gamma=1, coarse_iters=4, exact=True)
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+    assert relf(pc.apply(v), c.S.precond_apply(v)) < TOL_OP
+    x, rep = hps.fgmres(c.sk, c.sk.rhs(), pc, restart=10, tol=1e-10)
+    assert rep["converged"] and rep["iterations"] <= 2, rep
+    assert relf(x, c.S.direct_solve(c.S.rhs())) < TOL_SOL
+
+
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg2_n8"])
+def test_exact_coarse_partial_depth(hps, oracle, ctx, name):
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk, depth=2, factor_coarse=False)
+    c.S.build_hierarchy(0, False)
+    pc = hps.build_preconditioner(h, exact_coarse=True)
+    c.S.precond(depth=2, gamma=1, coarse_iters=4, exact=True)
+    rng = np.random.default_rng(12)
+    v = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+    assert relf(pc.apply(v), c.S.precond_apply(v)) < TOL_OP
+    x, rep = hps.fgmres(c.sk, c.sk.rhs(), pc, restart=50, tol=1e-10)
+    xo, repo = c.S.solve(c.S.rhs(), True, restart=50, tol=1e-10)
+    assert rep["converged"] and abs(rep["iterations"] - repo["iterations"]) <= 1, (rep, repo)
+    assert relf(x, xo) < TOL_SOL
