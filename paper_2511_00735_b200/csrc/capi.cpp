@@ -100,6 +100,7 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     ctx->c.device = device;
     HPSB_CUDA(cudaSetDevice(device));
     ctx->c.num_sms = prop.multiProcessorCount;
+    ctx->c.pdl = std::getenv("HPSB_NO_PDL") == nullptr;
     HPSB_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
     for (auto& e : ctx->c.ev) HPSB_CUDA(cudaEventCreate(&e));
     cudaMemPool_t pool;

@@ -43,6 +43,17 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cmul(a, c
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 
+// Programmatic dependent launch (internal.hpp launch_k): wait until the
+// preceding grid has completed and its writes are visible / allow the next
+// grid in the stream to be scheduled.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Hint: fetch the 128-byte line holding p into L2.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Block-wide sum of a double (blockDim.x multiple of 32, <= 1024).
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -21,7 +21,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <tuple>
 
 #include "device.cuh"
 #include "gemv_device.cuh"
@@ -45,25 +47,90 @@ __device__ __forceinline__ const double2* rebind(const double2* p, const Rebind&
   return p == b.from[0] ? b.to[0] : p == b.from[1] ? b.to[1] : p;
 }
 
-template <bool kCluster>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// kStage: every item's operator rows for this CTA are copied into shared
+// memory before the PDL wait -- operators never depend on the vectors, so
+// the copies overlap the previous kernel's tail and the chain below then
+// runs on on-chip operands (the small / medium levels are latency bound).
+// Otherwise the first 32 KB of the CTA's operator rows are prefetched into L2.
+template <bool kCluster, bool kStage>
 __global__ void __launch_bounds__(kThreads) vplan_kernel(const VItem* __restrict__ items,
                                                          const VUnit* __restrict__ units,
-                                                         int unit_begin, int csize, Rebind bind) {
+                                                         int unit_begin, int csize, int xs_cols,
+                                                         Rebind bind) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* xs = reinterpret_cast<double2*>(smem_raw);
+  double2* stage = xs + xs_cols;
   __shared__ double2 red[kThreads];
+  pdl_trigger();
   const int crank = kCluster ? static_cast<int>(blockIdx.x % csize) : 0;
   const VUnit u = units[unit_begin + (kCluster ? blockIdx.x / csize : blockIdx.x)];
+  auto rows_of = [&](const VItem& I, int& rb, int& re) {
+    const int chunk = kCluster ? cluster_chunk(I.rows, csize) : I.rows;
+    rb = crank * chunk;
+    re = min(I.rows, rb + chunk);
+  };
+  if (kStage) {
+    size_t off = 0;
+    for (int it = u.first; it < u.first + u.count; ++it) {
+      const VItem I = items[it];
+      int rb, re;
+      rows_of(I, rb, re);
+      if (!I.A || rb >= re) continue;
+      const int nr = re - rb;
+      for (int k = threadIdx.x; k < nr * I.cols; k += kThreads)
+        cp_async16(stage + off + k, I.A + rb + (k % nr) + static_cast<size_t>(k / nr) * I.lda);
+      off += static_cast<size_t>(nr) * I.cols;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  } else {
+    int budget = 256;  // 128-byte lines per CTA
+    for (int it = u.first; it < u.first + u.count && budget > 0; ++it) {
+      const VItem I = items[it];
+      int rb, re;
+      rows_of(I, rb, re);
+      if (!I.A || rb >= re) continue;
+      const int lines = ((re - rb) * 16 + 127) / 128;
+      const int n = min(budget, lines * I.cols);
+      for (int k = threadIdx.x; k < n; k += kThreads)
+        prefetch_l2(I.A + rb + (k % lines) * 8 + static_cast<size_t>(k / lines) * I.lda);
+      budget -= n;
+    }
+  }
+  pdl_wait();
+  if (kStage) {
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();  // every thread's copies visible before any operand read
+  }
+  size_t off = 0;
   for (int it = u.first; it < u.first + u.count; ++it) {
     const VItem I = items[it];
-    const int chunk = kCluster ? (((I.rows + csize - 1) / csize + 31) & ~31) : I.rows;
-    const int rb = crank * chunk, re = min(I.rows, rb + chunk);
-    if (rb < re)
-      gemv_item_rows(I, rb, re, rebind(I.x, bind), rebind(I.z, bind),
-                     const_cast<double2*>(rebind(I.y, bind)), xs, red);
+    int rb, re;
+    rows_of(I, rb, re);
+    if (rb < re) {
+      if (kStage) {
+        gemv_item_rows<true>(I, rb, re, rebind(I.x, bind), rebind(I.z, bind),
+                             const_cast<double2*>(rebind(I.y, bind)), xs, red, stage + off, re - rb);
+        if (I.A) off += static_cast<size_t>(re - rb) * I.cols;
+      } else {
+        gemv_item_rows<false>(I, rb, re, rebind(I.x, bind), rebind(I.z, bind),
+                              const_cast<double2*>(rebind(I.y, bind)), xs, red);
+      }
+    }
     if (kCluster && (I.flags & VItem::kPhaseEnd)) cg::this_cluster().sync();
     else __syncthreads();
   }
+}
+
+template <auto Kernel, typename Tuple>
+void launch_plan(Context* ctx, int grid, size_t smem, int csize, const Tuple& args) {
+  allow_smem<Kernel>(smem);
+  std::apply([&](auto... a) { launch_k(ctx, Kernel, dim3(grid), dim3(kThreads), smem, csize, a...); },
+             args);
 }
 
 __global__ void fill_kernel(double2* p, size_t n, double2 v) {
@@ -109,6 +176,30 @@ void VPlan::add_split(const VItem& it, int row_block) {
 }
 
 void VPlan::finalize(cudaStream_t s) {
+  // Stage a phase's operators in shared memory when every CTA's share fits
+  // (default 96 KB: two CTAs per SM).
+  static const size_t limit = [] {
+    const char* e = std::getenv("HPSB_STAGE_KB");
+    return static_cast<size_t>(e ? std::atoi(e) : 96) * 1024;
+  }();
+  for (VPhase& ph : phases) {
+    size_t worst = 0;
+    for (int ui = ph.unit_begin; ui < ph.unit_begin + ph.unit_count; ++ui) {
+      const VUnit& u = units[ui];
+      for (int rank = 0; rank < ph.csize; ++rank) {
+        size_t b = 0;
+        for (int it = u.first; it < u.first + u.count; ++it) {
+          const VItem& I = items[it];
+          if (!I.A) continue;
+          const int chunk = ph.csize > 1 ? cluster_chunk(I.rows, ph.csize) : I.rows;
+          const int rb = rank * chunk, re = std::min(I.rows, rb + chunk);
+          if (re > rb) b += sizeof(double2) * static_cast<size_t>(re - rb) * I.cols;
+        }
+        worst = std::max(worst, b);
+      }
+    }
+    ph.stage = worst <= limit ? worst : 0;
+  }
   d_items.upload(items, s);
   d_units.upload(units, s);
 }
@@ -118,36 +209,27 @@ void VPlan::run_phase(Context* ctx, int p, const double2* from0, double2* to0,
   const VPhase& ph = phases[p];
   if (ph.unit_count == 0) return;
   Rebind bind{{from0, from1}, {to0, to1}};
-  const size_t smem = sizeof(double2) * std::max(ph.max_cols, 1);
+  const int xs_cols = std::max(ph.max_cols, 1);
+  const size_t smem = sizeof(double2) * xs_cols + ph.stage;
   KernelScope ks(ctx, ph.label.empty() ? name : ph.label.c_str(), ph.bytes, 0.0);
+  const int grid = ph.unit_count * std::max(ph.csize, 1);
+  auto args = std::make_tuple(d_items.p, d_units.p, ph.unit_begin, ph.csize, xs_cols, bind);
   if (ph.csize <= 1) {
-    allow_smem<vplan_kernel<false>>(smem);
-    vplan_kernel<false><<<ph.unit_count, kThreads, smem, ctx->stream>>>(d_items.p, d_units.p,
-                                                                         ph.unit_begin, 1, bind);
+    if (ph.stage) launch_plan<vplan_kernel<false, true>>(ctx, grid, smem, 1, args);
+    else launch_plan<vplan_kernel<false, false>>(ctx, grid, smem, 1, args);
   } else {
     static const bool nonportable = [] {  // thread-safe one-time init
-      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true>,
+      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true, true>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      HPSB_CUDA(cudaFuncSetAttribute(vplan_kernel<true, false>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       return true;
     }();
     (void)nonportable;
-    allow_smem<vplan_kernel<true>>(smem);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(ph.unit_count * ph.csize);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = ctx->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ph.csize;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    HPSB_CUDA(cudaLaunchKernelEx(&cfg, vplan_kernel<true>, d_items.p, d_units.p, ph.unit_begin,
-                                 ph.csize, bind));
+    if (ph.stage) launch_plan<vplan_kernel<true, true>>(ctx, grid, smem, ph.csize, args);
+    else launch_plan<vplan_kernel<true, false>>(ctx, grid, smem, ph.csize, args);
   }
-  HPSB_LAUNCHED(ctx);
+  HPSB_CUDA(cudaGetLastError());
 }
 
 void VPlan::run(Context* ctx, const double2* from0, double2* to0, const double2* from1,

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <utility>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -169,6 +170,10 @@ struct Context {
   std::unique_ptr<Comm> comm;  // null: single GPU
   int rank() const { return comm ? comm->rank : 0; }
   int world() const { return comm ? comm->size : 1; }
+  // Programmatic dependent launch for the per-iteration kernels (off while
+  // profiling, so each kernel's events bracket only its own work).
+  bool pdl = true;
+  bool use_pdl() const { return pdl && !profile; }
 };
 
 // Brackets one kernel launch with CUDA events when profiling is enabled and
@@ -179,6 +184,41 @@ struct KernelScope {
   KernelScope(Context* ctx, const char* name, double bytes, double flops);
   ~KernelScope();
 };
+
+// Launch on the context stream with programmatic dependent launch (PDL) and
+// an optional thread-block cluster.  A PDL kernel may start while its
+// predecessor drains: it must execute pdl_wait() (device.cuh) before it reads
+// or writes anything a predecessor produces or consumes; only prefetches of
+// data written before the previous host synchronisation may precede it.
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+void launch_k(Context* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+              int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute at[2];
+  unsigned na = 0;
+  if (ctx->use_pdl()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (cluster > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = static_cast<unsigned>(cluster);
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  HPSB_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  ++ctx->launches;
+}
+#endif
 
 // ---------------------------------------------------------------- host structure
 struct IndexSets {
@@ -245,6 +285,7 @@ struct VPhase {
   int max_cols = 0;
   int csize = 1;  // CTAs per unit (thread-block cluster)
   double bytes = 0;
+  size_t stage = 0;  // operator bytes per CTA staged in smem (0: streamed)
   std::string label;  // profiling name (defaults to the plan's name)
 };
 struct VPlan {

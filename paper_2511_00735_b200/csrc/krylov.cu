@@ -96,9 +96,114 @@ __global__ void __launch_bounds__(kThreads) dots_fused_kernel(
   if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
 }
 
+// One pass of CGS2 over the rows of a block (kOrthThreads x R rows per block,
+// w's rows kept in registers):
+//   kUpdate: w -= V h_upd (the previous pass's projection), written back;
+//   then partial[b, i] = sum_rows conj(V[k, i]) w[k] for i < ncols, or, with
+//   ncols == 0, partial[b, 0] = sum_rows |w[k]|^2.
+// With `fused`, the last block to finish (atomic ticket) sums the partials in
+// fixed block order into out (deterministic); else reduce_kernel does.
+constexpr int kOrthThreads = 128;
+constexpr int kOrthMaxR = 8;
+template <bool kUpdate>
+__global__ void __launch_bounds__(kOrthThreads) orth_kernel(
+    const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd,
+    int nupd, double2* w, int64_t n, int R, double2* partial, double2* out, unsigned* ticket,
+    int fused) {
+  __shared__ double2 sh[kOrthThreads / 32][104];
+  __shared__ double2 hs[104];
+  __shared__ bool last;
+  pdl_trigger();
+  pdl_wait();
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kOrthThreads * R;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (kUpdate) {
+    for (int i = threadIdx.x; i < nupd; i += kOrthThreads) hs[i] = h_upd[i];
+    __syncthreads();
+  }
+  double2 wv[kOrthMaxR];
+#pragma unroll
+  for (int r = 0; r < kOrthMaxR; ++r) {
+    const int64_t k = base + threadIdx.x + r * kOrthThreads;
+    wv[r] = (r < R && k < n) ? __ldcg(w + k) : make_double2(0.0, 0.0);
+    if (kUpdate && r < R && k < n) {
+      double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+      int i = 0;
+      for (; i + 8 <= nupd; i += 8) {  // 8 independent loads in flight
+        double2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = ldg2(V + (i + q) * ld + k);
+#pragma unroll
+        for (int q = 0; q < 8; q += 2) {
+          acc = cfma(hs[i + q], v[q], acc);
+          acc2 = cfma(hs[i + q + 1], v[q + 1], acc2);
+        }
+      }
+      for (; i < nupd; ++i) acc = cfma(hs[i], ldg2(V + i * ld + k), acc);
+      wv[r] = csub(wv[r], cadd(acc, acc2));
+      __stcg(w + k, wv[r]);
+    }
+  }
+  const int nout = ncols > 0 ? ncols : 1;
+  if (ncols == 0) {
+    double a = 0.0;
+#pragma unroll
+    for (int r = 0; r < kOrthMaxR; ++r)
+      if (r < R) a += cabs2(wv[r]);
+    a = warp_sum(a);
+    if (lane == 0) sh[warp][0] = make_double2(a, 0.0);
+  } else {
+    // 8 columns at a time: all their loads are issued before any reduction.
+    for (int i0 = 0; i0 < ncols; i0 += 8) {
+      double2 acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < kOrthMaxR; ++r) {
+        const int64_t k = base + threadIdx.x + r * kOrthThreads;
+        if (r < R && k < n) {
+          double2 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            v[q] = i0 + q < ncols ? ldg2(V + (i0 + q) * ld + k) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = cfma_conj(v[q], wv[r], acc[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        acc[q].x = warp_sum(acc[q].x);
+        acc[q].y = warp_sum(acc[q].y);
+        if (lane == 0 && i0 + q < ncols) sh[warp][i0 + q] = acc[q];
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nout; i += kOrthThreads) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = 0; q < kOrthThreads / 32; ++q) s = cadd(s, sh[q][i]);
+    __stcg(partial + static_cast<int64_t>(blockIdx.x) * nout + i, s);
+  }
+  if (!fused) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int i = threadIdx.x; i < nout; i += kOrthThreads) {
+    double2 s = make_double2(0.0, 0.0);
+    for (unsigned b = 0; b < gridDim.x; ++b) s = cadd(s, __ldcg(partial + b * nout + i));
+    out[i] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+}
+
 // out[i] = sum_b partial[b * ncols + i]  (fixed order: deterministic)
 __global__ void reduce_kernel(const double2* __restrict__ partial, int nblocks, int ncols,
                               double2* out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double2 sh[256];
   const int i = blockIdx.x;
   double2 s = make_double2(0.0, 0.0);
@@ -117,6 +222,8 @@ __global__ void reduce_kernel(const double2* __restrict__ partial, int nblocks, 
 __global__ void __launch_bounds__(kThreads) axpy_kernel(const double2* __restrict__ V, int64_t ld,
                                                        int ncols, const double2* __restrict__ h,
                                                        double sign, double2* w, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double2 hs[104];
   for (int i = threadIdx.x; i < ncols; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
@@ -129,6 +236,8 @@ __global__ void __launch_bounds__(kThreads) axpy_kernel(const double2* __restric
 }
 
 __global__ void scale_kernel(const double2* __restrict__ src, double s, double2* dst, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x)
     dst[k] = make_double2(src[k].x * s, src[k].y * s);
@@ -137,6 +246,8 @@ __global__ void scale_kernel(const double2* __restrict__ src, double s, double2*
 // r = b - y
 __global__ void sub_kernel(const double2* __restrict__ b, const double2* __restrict__ y, double2* r,
                            int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x)
     r[k] = csub(b[k], y[k]);
@@ -178,12 +289,35 @@ struct Work {
   explicit Work(Context* c, int64_t dim, int maxcols) : ctx(c), n(dim) {
     blocks = static_cast<int>((dim + kRowsPerBlock - 1) / kRowsPerBlock);
     chunk = kRowsPerBlock;
-    partial.alloc(static_cast<size_t>(blocks) * maxcols);
+    partial.alloc(static_cast<size_t>((dim + kOrthThreads - 1) / kOrthThreads + blocks) * maxcols);
     hdev.alloc(3 * static_cast<size_t>(maxcols) + 4);
     ticket.alloc(1);
     HPSB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
   }
   int grid() const { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * ctx->num_sms)); }
+  // One CGS2 pass (orth_kernel): optionally w -= V h_upd, then out = V^H w
+  // (ncols > 0) or out[0] = ||w||^2 (ncols == 0).
+  void orth(const double2* V, int ncols, const double2* h_upd, int nupd, double2* w, double2* out) {
+    // rows per thread: enough blocks for ~2 per SM, at most kOrthMaxR
+    int R = 1;
+    while (R < kOrthMaxR && (n + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
+      R *= 2;
+    const int nb = static_cast<int>((n + kOrthThreads * R - 1) / (kOrthThreads * R));
+    const int nout = ncols > 0 ? ncols : 1;
+    const bool fused = nb <= 4 * ctx->num_sms;
+    if (static_cast<size_t>(nb) * nout > partial.n) partial.alloc(static_cast<size_t>(nb) * nout);
+    KernelScope ks(ctx, "gmres_orth", 16.0 * n * (nout + nupd + (h_upd ? 2 : 1)),
+                   8.0 * n * (ncols + nupd));
+    if (h_upd)
+      launch_k(ctx, orth_kernel<true>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0);
+    else
+      launch_k(ctx, orth_kernel<false>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0);
+    if (!fused)
+      launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1,
+               static_cast<const double2*>(partial.p), nb, nout, out);
+  }
   // out[0..ncols) = V^H w.  Short vectors: one launch (last-block reduction);
   // long vectors: many row blocks + a column-parallel reduce launch.
   void dots(const double2* V, int ncols, const double2* w, double2* out) {
@@ -201,8 +335,7 @@ struct Work {
   }
   void axpy(const double2* V, int ncols, const double2* h, double sign, double2* w) {
     KernelScope ks(ctx, "gmres_axpy", 16.0 * n * (ncols + 2), 8.0 * n * ncols);
-    axpy_kernel<<<grid(), kThreads, 0, ctx->stream>>>(V, n, ncols, h, sign, w, n);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, axpy_kernel, dim3(grid()), dim3(kThreads), 0, 1, V, n, ncols, h, sign, w, n);
   }
   double norm(const double2* w) {
     dots(w, 1, w, hdev.p);
@@ -213,13 +346,11 @@ struct Work {
   }
   void scale(const double2* src, double s, double2* dst) {
     KernelScope ks(ctx, "gmres_scale", 32.0 * n, 0.0);
-    scale_kernel<<<grid(), 256, 0, ctx->stream>>>(src, s, dst, n);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, scale_kernel, dim3(grid()), dim3(256), 0, 1, src, s, dst, n);
   }
   void sub(const double2* b, const double2* y, double2* r) {
     KernelScope ks(ctx, "gmres_sub", 48.0 * n, 0.0);
-    sub_kernel<<<grid(), 256, 0, ctx->stream>>>(b, y, r, n);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, sub_kernel, dim3(grid()), dim3(256), 0, 1, b, y, r, n);
   }
 };
 }  // namespace
@@ -294,11 +425,9 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
       double2* h1 = wk.hdev.p;
       double2* h2 = wk.hdev.p + (j + 1);
       double2* nn = wk.hdev.p + 2 * (j + 1);
-      wk.dots(V.p, j + 1, w.p, h1);
-      wk.axpy(V.p, j + 1, h1, -1.0, w.p);
-      wk.dots(V.p, j + 1, w.p, h2);
-      wk.axpy(V.p, j + 1, h2, -1.0, w.p);
-      wk.dots(w.p, 1, w.p, nn);
+      wk.orth(V.p, j + 1, nullptr, 0, w.p, h1);     // h1 = V^H w
+      wk.orth(V.p, j + 1, h1, j + 1, w.p, h2);      // w -= V h1; h2 = V^H w
+      wk.orth(V.p, 0, h2, j + 1, w.p, nn);          // w -= V h2; nn = ||w||^2
       HPSB_CUDA(cudaMemcpyAsync(hh.data(), wk.hdev.p, sizeof(double2) * (2 * (j + 1) + 1),
                                 cudaMemcpyDeviceToHost, ctx->stream));
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -111,6 +111,8 @@ __device__ void apply_givens(double c, double2 s, double2& a, double2& b);
 __global__ void __launch_bounds__(kGemvThreads) coarse_fused_kernel(
     const VItem* __restrict__ items, int nitems, int64_t n, int ci, double2* V, double2* w,
     const double2* rd, double2* outd, int max_cols) {
+  pdl_trigger();
+  pdl_wait();
   cg::cluster_group cl = cg::this_cluster();
   const int cs = static_cast<int>(cl.num_blocks()), rank = static_cast<int>(cl.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(kGemvThreads) coarse_fused_kernel(
     const double2* Vj = V + j * n;
     for (int it = 0; it < nitems; ++it) {
       const VItem I = items[it];
-      const int chunk = (((I.rows + cs - 1) / cs + 31) & ~31);
+      const int chunk = cluster_chunk(I.rows, cs);
       const int rb = rank * chunk, re = min(I.rows, rb + chunk);
       if (rb < re) gemv_item_rows(I, rb, re, Vj, Vj, w, xs, red);
       __syncthreads();
@@ -231,13 +233,25 @@ __device__ double block_sum(double v, double* sh) {
 
 // y += s x
 __global__ void axpy_vec_kernel(double2* y, const double2* __restrict__ x, double s, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<int64_t>(gridDim.x) * blockDim.x)
     y[k] = make_double2(y[k].x + s * x[k].x, y[k].y + s * x[k].y);
 }
 
+__global__ void copy_vec_kernel(double2* y, const double2* __restrict__ x, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    y[k] = x[k];
+}
+
 // zero the face blocks this rank does not contribute
 __global__ void mask_faces_kernel(double2* z, const int* __restrict__ keep, int bs) {
+  pdl_trigger();
+  pdl_wait();
   if (keep[blockIdx.x]) return;
   for (int k = threadIdx.x; k < bs; k += blockDim.x)
     z[static_cast<int64_t>(blockIdx.x) * bs + k] = make_double2(0.0, 0.0);
@@ -248,6 +262,8 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_init_kernel(const doubl
                                                                      double2* V, double2* cv,
                                                                      double2* gv, int ci,
                                                                      double* state) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sh[33];
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += cabs2(rd[i]);
@@ -297,6 +313,8 @@ __device__ void apply_givens(double c, double2 s, double2& a, double2& b) {
 __global__ void __launch_bounds__(kCoarseThreads) coarse_step_kernel(
     int j, int64_t n, int ci, double2* V, double2* cv, double2* cw, double2* Hm, double2* gv,
     double* rc, double2* rs, double* state) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double sh[33];
   if (state[1] != 0.0) return;
   const int ldh = ci + 1;
@@ -354,6 +372,8 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_finish_kernel(int64_t n
                                                                        const double2* gv,
                                                                        const double* state,
                                                                        double2* outd) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ double2 y[64];
   const int ju = static_cast<int>(state[2]);
   const int ldh = ci + 1;
@@ -449,7 +469,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     }
     const double per_merge = bytes / std::max(ng, 1);
     int csize = 1;
-    while (csize < 16 && csize * ng < 2 * sms && 16 * csize * 2 <= smin) csize *= 2;
+    while (csize < 16 && csize * ng < 2 * sms && 8 * csize < smin + 8) csize *= 2;
     const bool split = per_merge > 8e6 && ng * 16 < sms;
     const bool chain = !split;
     int total_rows = 0;
@@ -642,7 +662,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->coarse_fused = p->coarse_mv.bytes_per_run <= (4ll << 20) && ci <= kMaxCoarseIters;
     p->coarse_csize = 1;
     while (p->coarse_csize < 16 &&
-           p->coarse_mv.bytes_per_run > p->coarse_csize * static_cast<int64_t>(256 << 10))
+           p->coarse_mv.bytes_per_run > p->coarse_csize * static_cast<int64_t>(64 << 10))
       p->coarse_csize *= 2;
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
@@ -713,7 +733,8 @@ void destroy_precond(Precond* p) { delete p; }
 
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   Context* ctx = p->ctx;
-  zcopy(ctx, p->r.p, v_dev, p->dim);
+  const int vblocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
+  launch_k(ctx, copy_vec_kernel, dim3(vblocks), dim3(256), 0, 1, p->r.p, v_dev, p->dim);
   // `out` of the plans is bound to the caller's z: no copy-out.
   p->run_steps(true, false, z_dev);  // local levels, down
   const bool sharded = ctx->world() > 1;
@@ -721,11 +742,9 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
     // Each residual entry was updated by at most one rank's subtree:
     // r = v + sum_ranks (r_rank - v).
     const int blocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
-    axpy_vec_kernel<<<blocks, 256, 0, ctx->stream>>>(p->r.p, v_dev, -1.0, p->dim);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, -1.0, p->dim);
     ctx->comm->allreduce_sum(p->r.p, p->dim, ctx);
-    axpy_vec_kernel<<<blocks, 256, 0, ctx->stream>>>(p->r.p, v_dev, 1.0, p->dim);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, 1.0, p->dim);
   }
   p->run_steps(true, true, z_dev);  // top (global) levels, down
   const int ci = p->cfg.coarse_iters;
@@ -740,46 +759,30 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
     (void)attr;
     const size_t smem = sizeof(double2) * std::max(p->coarse_max_cols, 1);
     allow_smem<coarse_fused_kernel>(smem);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(p->coarse_csize);
-    lc.blockDim = dim3(kGemvThreads);
-    lc.dynamicSmemBytes = smem;
-    lc.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = p->coarse_csize;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
     KernelScope ks(ctx, "coarse_fused", static_cast<double>(ci) * p->coarse_mv.bytes_per_run, 0.0);
-    HPSB_CUDA(cudaLaunchKernelEx(&lc, coarse_fused_kernel,
-                                 static_cast<const VItem*>(p->coarse_items.p), p->coarse_nitems,
-                                 p->dim_d, ci, p->V.p, p->cw.p,
-                                 static_cast<const double2*>(p->r.p + p->off_d),
-                                 z_dev + p->off_d, p->coarse_max_cols));
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, coarse_fused_kernel, dim3(p->coarse_csize), dim3(kGemvThreads), smem,
+             p->coarse_csize, static_cast<const VItem*>(p->coarse_items.p), p->coarse_nitems,
+             p->dim_d, ci, p->V.p, p->cw.p, static_cast<const double2*>(p->r.p + p->off_d),
+             z_dev + p->off_d, p->coarse_max_cols);
   } else {
   {
   KernelScope ks(ctx, "coarse_gmres", 32.0 * p->dim_d, 0.0);
-  coarse_init_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(p->r.p + p->off_d, p->dim_d, p->V.p,
-                                                            p->cv.p, p->gv.p, ci, p->state.p);
-  HPSB_LAUNCHED(ctx);
+  launch_k(ctx, coarse_init_kernel, dim3(1), dim3(kCoarseThreads), 0, 1,
+           static_cast<const double2*>(p->r.p + p->off_d), p->dim_d, p->V.p, p->cv.p, p->gv.p, ci,
+           p->state.p);
   }
   for (int j = 0; j < ci; ++j) {
     p->coarse_mv.run(ctx);
     KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (2 * j + 4), 0.0);
-    coarse_step_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(j, p->dim_d, ci, p->V.p, p->cv.p,
-                                                              p->cw.p, p->Hm.p, p->gv.p, p->rc.p,
-                                                              p->rs.p, p->state.p);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, coarse_step_kernel, dim3(1), dim3(kCoarseThreads), 0, 1, j, p->dim_d, ci, p->V.p,
+             p->cv.p, p->cw.p, p->Hm.p, p->gv.p, p->rc.p, p->rs.p, p->state.p);
   }
   {
   KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (ci + 1), 0.0);
-  coarse_finish_kernel<<<1, kCoarseThreads, 0, ctx->stream>>>(p->dim_d, ci, p->V.p, p->Hm.p,
-                                                              p->gv.p, p->state.p,
-                                                              z_dev + p->off_d);
-  HPSB_LAUNCHED(ctx);
+  launch_k(ctx, coarse_finish_kernel, dim3(1), dim3(kCoarseThreads), 0, 1, p->dim_d, ci,
+           static_cast<const double2*>(p->V.p), static_cast<const double2*>(p->Hm.p),
+           static_cast<const double2*>(p->gv.p), static_cast<const double*>(p->state.p),
+           z_dev + p->off_d);
   }
   }
   p->run_steps(false, true, z_dev);
@@ -788,8 +791,8 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
     // Local faces come from their owner, global faces from rank 0: sum.
     const int bs = p->h->sk->bs;
     const int nf = static_cast<int>(p->dim / bs);
-    mask_faces_kernel<<<nf, 64, 0, ctx->stream>>>(z_dev, p->keep_face.p, bs);
-    HPSB_LAUNCHED(ctx);
+    launch_k(ctx, mask_faces_kernel, dim3(nf), dim3(64), 0, 1, z_dev,
+             static_cast<const int*>(p->keep_face.p), bs);
     ctx->comm->allreduce_sum(z_dev, p->dim, ctx);
   }
 }

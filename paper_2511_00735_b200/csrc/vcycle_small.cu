@@ -66,8 +66,11 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
   double2* u1 = w1 + s;
   double2* u2 = u1 + p1;
   __shared__ double2 red[kThreads];
+  pdl_trigger();
 
-  // ---- one burst of asynchronous copies: operators (+ W)
+  // ---- one burst of asynchronous copies: operators (+ W); they never depend
+  // on the vectors, so they are issued before the PDL wait
+  // (overlapping the previous kernel's tail).
   if (down) {
     const double2* g1 = M.T1 + static_cast<size_t>(p1) * P1;  // [T1_ps; T1_ss], P1 x s
     const double2* g2 = M.T2 + static_cast<size_t>(p2) * P2;
@@ -81,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
   }
   for (int k = tid; k < s * s; k += kThreads) cp_async16(Ws + k, M.W + k);
   asm volatile("cp.async.commit_group;\n" ::);
+  pdl_wait();
   // vector gathers overlap the copies
   if (down) {
     for (int k = tid; k < s; k += kThreads) {
@@ -159,8 +163,8 @@ void SmallLevel::run(Context* ctx, bool down, double2* r, double2* out) const {
   allow_smem<merge_small_kernel>(smem);
   KernelScope ks(ctx, label.empty() ? (down ? "vcycle_down" : "vcycle_up") : label.c_str(),
                  down ? bytes_down : bytes_up, 0.0);
-  merge_small_kernel<<<count, kThreads, smem, ctx->stream>>>(d.p, down ? 1 : 0, r, out);
-  HPSB_LAUNCHED(ctx);
+  launch_k(ctx, merge_small_kernel, dim3(count), dim3(kThreads), smem, 1,
+           static_cast<const SmallMerge*>(d.p), down ? 1 : 0, r, out);
 }
 
 }  // namespace hpsb
