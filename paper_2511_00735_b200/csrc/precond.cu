@@ -22,12 +22,15 @@
 // row blocks so the whole GPU streams the maps.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
 #include "device.cuh"
 #include "gemv_device.cuh"
 #include "hierarchy.hpp"
+#include "vcycle_device.cuh"
 #include "vcycle_small.hpp"
 #include "zgemm.hpp"
 
@@ -49,6 +52,10 @@ struct Precond {
   int64_t bytes_per_apply = 0;
   // fused coarse solve (one cluster launch)
   bool coarse_fused = false;
+  bool coarse_cluster = false;  // on-chip variant (coarse_cluster_kernel)
+  int coarse_slice = 0;
+  size_t coarse_smem = 0, coarse_stage = 0;
+  int coarse_xs = 0;
   DevBuf<VItem> coarse_items;
   int coarse_nitems = 0, coarse_max_cols = 0, coarse_csize = 16;
   // exact coarse (MgConfig.exact_coarse): dense inverse of M_depth + one GEMV
@@ -57,18 +64,20 @@ struct Precond {
   VPlan exact_mv;
   // per-level execution order of the sweeps
   struct Step {
-    int level = 0, small = -1;
+    int level = 0, small = -1, cluster = -1;
     const VPlan* plan = nullptr;
     int p0 = 0, p1 = 0;
   };
   std::vector<Step> down_steps, up_steps;
   std::vector<std::unique_ptr<SmallLevel>> smalls;
+  std::vector<std::unique_ptr<ClusterLevel>> clusters;
   double bytes_small = 0;
   void run_steps(bool down, bool global, double2* z) const {
     const int last_local = h->sk->el->part.last_local;
     for (const Step& st : down ? down_steps : up_steps) {
       if ((st.level > last_local) != global) continue;
       if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
+      else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
       else
         for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
     }
@@ -78,6 +87,7 @@ struct Precond {
 constexpr int kMaxCoarseIters = 30;
 constexpr int64_t kExactCoarseMax = 24576;  // dense coarse inverse: <= 9.7 GB
 constexpr size_t kSmallMergeSmemMax = 160 * 1024;
+constexpr size_t kClusterMergeSmemMax = 200 * 1024;
 
 namespace {
 constexpr int kCoarseThreads = 1024;
@@ -213,6 +223,264 @@ __global__ void __launch_bounds__(kGemvThreads) coarse_fused_kernel(
     for (int i = 0; i < jused; ++i) acc = cfma(ys[i], __ldcg(V + i * n + k), acc);
     outd[k] = acc;
   }
+}
+
+// gmres_fixed_steps on a small coarse system, fully on-chip in ONE cluster
+// launch (used when every CTA's rows of the coarse box maps fit in shared
+// memory).  Each of the C CTAs
+//   - stages its row slice of every coarse box map (and the index maps) in
+//     shared memory once, before the PDL wait; the ci matvecs reuse it;
+//   - owns a contiguous slice of the Krylov vectors (kept in shared memory);
+//   - gathers the full v_j from its peers' slices through DSMEM for the
+//     matvec and scatters each product row to the owner of its output index
+//     (remote shared-memory store), so the product lands slice-wise;
+//   - runs MGS with DSMEM reductions (two alternating partial slots) and
+//     keeps the Hessenberg / Givens state redundantly (identical in all CTAs).
+constexpr int kCoarseCThreads = 256;
+constexpr int kCoarseClusterItems = 8;
+__global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
+    const VItem* __restrict__ gitems, int nitems, int n, int slice, int ci, int max_cols,
+    size_t stage_elems, const double2* rd, double2* outd, unsigned long long* trace) {
+  int tn = 0;
+  auto mark = [&]() {
+    if (trace && threadIdx.x == 0 && blockIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[tn] = t;
+    }
+    ++tn;
+  };
+  mark();
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), crank = static_cast<int>(cl.block_rank());
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* vfull = reinterpret_cast<double2*>(smem_raw);   // n
+  double2* Vs = vfull + n;                                  // (ci+1) x slice
+  double2* ws = Vs + static_cast<size_t>(ci + 1) * slice;   // slice
+  double2* xs = ws + slice;                                 // max_cols
+  double2* As = xs + max_cols;                              // staged rows
+  int* Ix = reinterpret_cast<int*>(As + stage_elems);       // staged gather / scatter indices
+  __shared__ double2 red[kCoarseCThreads];
+  __shared__ double2 part[2];
+  __shared__ VItem items[kCoarseClusterItems];  // item descriptors read once
+  __shared__ double2 Hs[(kMaxCoarseIters + 1) * kMaxCoarseIters];
+  __shared__ double2 gs[kMaxCoarseIters + 1], rs[kMaxCoarseIters], ys[kMaxCoarseIters];
+  __shared__ double rcs[kMaxCoarseIters];
+  const int s0 = min(n, crank * slice), s1 = min(n, s0 + slice), ns = s1 - s0;
+  const int ldh = ci + 1;
+  pdl_trigger();
+  {
+    const int words = nitems * static_cast<int>(sizeof(VItem) / sizeof(int));
+    for (int w = tid; w < words; w += kCoarseCThreads)
+      reinterpret_cast<int*>(items)[w] = __ldg(reinterpret_cast<const int*>(gitems) + w);
+    __syncthreads();
+  }
+  // ---- stage this CTA's rows of every item (operators are static)
+  {
+    size_t off = 0;
+    for (int it = 0; it < nitems; ++it) {
+      const VItem I = items[it];
+      const int chunk = cluster_chunk(I.rows, C);
+      const int rb = min(I.rows, crank * chunk), nr = max(0, min(I.rows, rb + chunk) - rb);
+      // row-major [nr][cols]: a warp reads a row with consecutive lanes
+      for (int k = tid; k < nr * I.cols; k += kCoarseCThreads)
+        cp_async16(As + off + k, I.A + rb + (k / I.cols) + static_cast<size_t>(k % I.cols) * I.lda);
+      off += static_cast<size_t>(nr) * I.cols;
+    }
+    cp_async_commit();
+    int io = 0;  // index maps are static too: [xi (cols) | own rows of yi] per item
+    for (int it = 0; it < nitems; ++it) {
+      const VItem I = items[it];
+      const int chunk = cluster_chunk(I.rows, C);
+      const int rb = min(I.rows, crank * chunk), nr = max(0, min(I.rows, rb + chunk) - rb);
+      for (int c = tid; c < I.cols; c += kCoarseCThreads) Ix[io + c] = __ldg(I.xi + c);
+      for (int r = tid; r < nr; r += kCoarseCThreads) Ix[io + I.cols + r] = __ldg(I.yi + rb + r);
+      io += I.cols + nr;
+    }
+  }
+  int slot = 0;
+  auto cluster_sum = [&](double2 v) {
+    v.x = warp_sum(v.x);
+    v.y = warp_sum(v.y);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int q = 0; q < kCoarseCThreads / 32; ++q) t = cadd(t, red[q]);
+      part[slot] = t;
+    }
+    cl.sync();
+    // every warp loads the C partials in parallel (one per lane) and reduces
+    // them in the same butterfly order: identical results in all CTAs
+    double2 t = lane < C ? *cl.map_shared_rank(&part[slot], lane) : make_double2(0.0, 0.0);
+    t.x = warp_sum(t.x);
+    t.y = warp_sum(t.y);
+    slot ^= 1;
+    return t;
+  };
+  mark();
+  pdl_wait();
+  mark();
+  double2 loc = make_double2(0.0, 0.0);
+  for (int k = tid; k < ns; k += kCoarseCThreads) {
+    const double2 v = __ldcg(rd + s0 + k);
+    ws[k] = v;
+    loc.x += cabs2(v);
+  }
+  const double beta = sqrt(cluster_sum(loc).x);
+  if (beta == 0.0) {
+    for (int k = tid; k < ns; k += kCoarseCThreads) outd[s0 + k] = make_double2(0.0, 0.0);
+    cp_async_wait_all();
+    cl.sync();
+    return;
+  }
+  for (int k = tid; k < ns; k += kCoarseCThreads) Vs[k] = make_double2(ws[k].x / beta, ws[k].y / beta);
+  if (tid <= ci) gs[tid] = make_double2(tid == 0 ? beta : 0.0, 0.0);
+  cp_async_wait_all();
+  cl.sync();  // V_0 slices visible cluster-wide
+  mark();
+  int jused = 0;
+  for (int j = 0; j < ci; ++j) {
+    // full v_j from the peers' slices
+    for (int k = tid; k < n; k += kCoarseCThreads) {
+      const int o = k / slice;
+      vfull[k] = cl.map_shared_rank(Vs, o)[static_cast<size_t>(j) * slice + (k - o * slice)];
+    }
+    __syncthreads();
+    mark();
+    // w = v_j + sum_boxes scatter(T gather(v_j)): gather every item's x,
+    // then one warp per product row; rows go to the owner of their index.
+    {
+      int io = 0, xo = 0;
+      for (int it = 0; it < nitems; ++it) {
+        const VItem I = items[it];
+        const int chunk = cluster_chunk(I.rows, C);
+        const int rb = min(I.rows, crank * chunk), nr = max(0, min(I.rows, rb + chunk) - rb);
+        for (int c = tid; c < I.cols; c += kCoarseCThreads) xs[xo + c] = vfull[Ix[io + c]];
+        io += I.cols + nr;
+        xo += I.cols;
+      }
+      __syncthreads();
+      size_t off = 0;
+      int row0 = 0;
+      io = 0, xo = 0;
+      for (int it = 0; it < nitems; ++it) {
+        const VItem I = items[it];
+        const int chunk = cluster_chunk(I.rows, C);
+        const int rb = min(I.rows, crank * chunk), nr = max(0, min(I.rows, rb + chunk) - rb);
+        // rows of this item go to warps continuing the round robin of the previous items
+        for (int r = (warp - row0 % (kCoarseCThreads / 32) + (kCoarseCThreads / 32)) % (kCoarseCThreads / 32);
+             r < nr; r += kCoarseCThreads / 32) {
+          const double2* Ar = As + off + static_cast<size_t>(r) * I.cols;
+          double2 acc = make_double2(0.0, 0.0);
+          for (int c = lane; c < I.cols; c += 32) acc = cfma(Ar[c], xs[xo + c], acc);
+          acc.x = warp_sum(acc.x);
+          acc.y = warp_sum(acc.y);
+          if (lane == 0) {
+            const int k = Ix[io + I.cols + r];
+            const int o = k / slice;
+            cl.map_shared_rank(ws, o)[k - o * slice] = cadd(acc, vfull[k]);
+          }
+        }
+        row0 += nr;
+        off += static_cast<size_t>(nr) * I.cols;
+        io += I.cols + nr;
+        xo += I.cols;
+      }
+    }
+    cl.sync();  // w slices complete
+    mark();
+    for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt on the slices
+      const double2* Vi = Vs + static_cast<size_t>(i) * slice;
+      double2 d = make_double2(0.0, 0.0);
+      for (int k = tid; k < ns; k += kCoarseCThreads) d = cfma_conj(Vi[k], ws[k], d);
+      const double2 h = cluster_sum(d);
+      for (int k = tid; k < ns; k += kCoarseCThreads) ws[k] = csub(ws[k], cmul(h, Vi[k]));
+      if (tid == 0) Hs[i + j * ldh] = h;
+    }
+    mark();
+    double2 nn = make_double2(0.0, 0.0);
+    for (int k = tid; k < ns; k += kCoarseCThreads) nn.x += cabs2(ws[k]);
+    const double hnext = sqrt(cluster_sum(nn).x);
+    if (tid == 0) {
+      Hs[j + 1 + j * ldh] = make_double2(hnext, 0.0);
+      for (int i = 0; i < j; ++i) apply_givens(rcs[i], rs[i], Hs[i + j * ldh], Hs[i + 1 + j * ldh]);
+      double c;
+      double2 sg;
+      make_givens(Hs[j + j * ldh], Hs[j + 1 + j * ldh], c, sg);
+      rcs[j] = c, rs[j] = sg;
+      apply_givens(c, sg, Hs[j + j * ldh], Hs[j + 1 + j * ldh]);
+      apply_givens(c, sg, gs[j], gs[j + 1]);
+    }
+    __syncthreads();
+    jused = j + 1;
+    if (hnext <= 1e-14 * beta) break;  // happy breakdown
+    double2* Vn = Vs + static_cast<size_t>(j + 1) * slice;
+    for (int k = tid; k < ns; k += kCoarseCThreads) Vn[k] = make_double2(ws[k].x / hnext, ws[k].y / hnext);
+    cl.sync();  // V_{j+1} slices visible; w slots free for the next matvec
+    mark();
+  }
+  if (tid == 0)
+    for (int i = jused - 1; i >= 0; --i) {
+      double2 sum = gs[i];
+      for (int k = i + 1; k < jused; ++k) sum = csub(sum, cmul(Hs[i + k * ldh], ys[k]));
+      ys[i] = cdiv(sum, Hs[i + i * ldh]);
+    }
+  __syncthreads();
+  for (int k = tid; k < ns; k += kCoarseCThreads) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < jused; ++i) acc = cfma(ys[i], Vs[static_cast<size_t>(i) * slice + k], acc);
+    outd[s0 + k] = acc;
+  }
+  mark();
+  cl.sync();  // no CTA exits while a peer may still read its shared memory
+  mark();
+}
+
+// HPSB_COARSE_TRACE: globaltimer stamps of CTA 0's phases of the last
+// coarse_cluster_kernel launch, printed at process exit (development aid).
+unsigned long long* coarse_trace(Context* ctx) {
+  static unsigned long long* buf = nullptr;
+  static const bool on = std::getenv("HPSB_COARSE_TRACE") != nullptr;
+  if (!on) return nullptr;
+  if (!buf) {
+    HPSB_CUDA(cudaMallocManaged(&buf, 64 * sizeof(unsigned long long)));
+    std::atexit([] {
+      cudaDeviceSynchronize();
+      for (int i = 1; i < 40 && buf[i]; ++i)
+        std::fprintf(stderr, "coarse trace %2d: %8.3f us\n", i, (buf[i] - buf[0]) * 1e-3);
+    });
+  }
+  (void)ctx;
+  return buf;
+}
+
+bool coarse_cluster_fits(size_t smem, int csize) {
+  static const bool attr = [] {
+    HPSB_CUDA(cudaFuncSetAttribute(coarse_cluster_kernel,
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    return true;
+  }();
+  (void)attr;
+  allow_smem<coarse_cluster_kernel>(smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(csize);
+  cfg.blockDim = dim3(kCoarseCThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, coarse_cluster_kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return nclusters > 0;
 }
 
 __device__ double block_sum(double v, double* sh) {
@@ -570,13 +838,62 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->smalls.push_back(std::move(sl));
     return static_cast<int>(p->smalls.size()) - 1;
   };
-  std::vector<int> small_of(cfg.depth, -1);
-  for (int l = 1; l < cfg.depth; ++l) small_of[l] = small_level(l);
+  // Per level, next choice: one thread-block cluster per merge with every
+  // CTA's operator slices staged in shared memory (vcycle_cluster.cu).
+  auto cluster_level = [&](int l) -> int {
+    const LevelOps& L = *h->levels[l - 1];
+    const int ng = static_cast<int>(L.merges.size());
+    if (!ng || std::getenv("HPSB_NO_CLUSTER_MERGE")) return -1;
+    // Only for latency-bound levels: few merges (>= 4 CTAs each within ~2
+    // CTAs per SM) and a few MB of operators.  With many merges, one CTA per
+    // SM holding a whole staged slice serialises load and compute, and the
+    // streaming work lists are faster (measured at cfg3 levels 2-3: 3x).
+    int C = 1;
+    while (C < 16 && 2 * C * ng <= 2 * sms) C *= 2;
+    if (C < 4) return -1;
+    auto cl = std::make_unique<ClusterLevel>();
+    for (const MergeRec& mr : L.merges) {
+      if (cluster_chunk(mr.s, C) > 256) return -1;  // one row pass per CTA for the s-blocks
+      cl->smem = std::max(cl->smem, cluster_merge_smem(mr.s, mr.p1, mr.p2, C));
+      const double ss = 16.0 * mr.s * mr.s, sp = 16.0 * mr.s * (mr.p1 + mr.p2);
+      cl->bytes_down += 3 * ss + sp;
+      cl->bytes_up += 3 * ss + sp;
+    }
+    if (cl->smem > kClusterMergeSmemMax || cl->bytes_down > 32e6) return -1;
+    if (!cluster_merge_fits(cl->smem, C)) return -1;
+    std::vector<SmallMerge> v;
+    const int* ix = L.idx.p;
+    for (const MergeRec& mr : L.merges) {
+      const ChildBox& c1 = L.children[mr.c1];
+      const ChildBox& c2 = L.children[mr.c2];
+      SmallMerge m{};
+      m.T1 = L.tperm.p + c1.t_off, m.T2 = L.tperm.p + c2.t_off, m.W = L.w.p + mr.w_off;
+      m.in1s = ix + mr.in1_sep, m.in2s = ix + mr.in2_sep, m.in1p = ix + mr.in1_per;
+      m.in2p = ix + mr.in2_per, m.out1p = ix + mr.out1_per, m.out2p = ix + mr.out2_per;
+      m.s = mr.s, m.p1 = mr.p1, m.p2 = mr.p2, m.P1 = c1.P, m.P2 = c2.P;
+      v.push_back(m);
+    }
+    cl->level = l;
+    cl->count = ng;
+    cl->csize = C;
+    if (std::getenv("HPSB_PROFILE_LEVELS")) cl->label = "vcycle_cluster_L" + std::to_string(l);
+    cl->d.upload(v, ctx->stream);
+    p->clusters.push_back(std::move(cl));
+    return static_cast<int>(p->clusters.size()) - 1;
+  };
+  std::vector<int> small_of(cfg.depth, -1), cluster_of(cfg.depth, -1);
+  for (int l = 1; l < cfg.depth; ++l) {
+    small_of[l] = small_level(l);
+    if (small_of[l] < 0) cluster_of[l] = cluster_level(l);
+  }
   auto add_step = [&](int l, bool downward) {
     Precond::Step st;
     st.level = l;
     st.small = small_of[l];
-    if (st.small < 0) {
+    st.cluster = cluster_of[l];
+    if (st.cluster >= 0) {
+      p->bytes_small += downward ? p->clusters[st.cluster]->bytes_down : p->clusters[st.cluster]->bytes_up;
+    } else if (st.small < 0) {
       const bool global_level = l > h->sk->el->part.last_local;
       VPlan& plan =
           downward ? (global_level ? p->down_g : p->down) : (global_level ? p->up_g : p->up);
@@ -666,6 +983,33 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       p->coarse_csize *= 2;
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
+    // On-chip variant: a 16-CTA cluster holding its rows of the coarse maps.
+    {
+      const int Cc = 16;
+      size_t stage = 0;
+      for (const VItem& it : whole)
+        stage += static_cast<size_t>(std::min(it.rows, cluster_chunk(it.rows, Cc))) * it.cols;
+      const int slice = static_cast<int>((p->dim_d + Cc - 1) / Cc);
+      size_t nidx = 0, xs_total = 0;
+      for (const VItem& it : whole) {
+        nidx += it.cols + std::min(it.rows, cluster_chunk(it.rows, Cc));
+        xs_total += it.cols;
+      }
+      p->coarse_xs = static_cast<int>(xs_total);
+      const size_t smem = sizeof(double2) * (static_cast<size_t>(p->dim_d) +
+                                             static_cast<size_t>(ci + 2) * slice +
+                                             xs_total + stage) +
+                          sizeof(int) * nidx;
+      p->coarse_stage = stage;
+      if (p->coarse_fused && smem <= (200u << 10) && !std::getenv("HPSB_NO_COARSE_CLUSTER") &&
+          whole.size() <= static_cast<size_t>(kCoarseClusterItems) &&
+          coarse_cluster_fits(smem, Cc)) {
+        p->coarse_cluster = true;
+        p->coarse_slice = slice;
+        p->coarse_smem = smem;
+        p->coarse_csize = Cc;
+      }
+    }
   }
   if (cfg.exact_coarse) {
     // exact_lu = LU(M_depth.to_dense()) (multigrid.cpp:22-27); here the dense
@@ -750,6 +1094,13 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   const int ci = p->cfg.coarse_iters;
   if (p->cfg.exact_coarse) {
     p->exact_mv.run(ctx, p->out.p, z_dev);
+  } else if (p->coarse_cluster) {
+    KernelScope ks(ctx, "coarse_fused", static_cast<double>(p->coarse_mv.bytes_per_run), 0.0);
+    launch_k(ctx, coarse_cluster_kernel, dim3(p->coarse_csize), dim3(kCoarseCThreads),
+             p->coarse_smem, p->coarse_csize, static_cast<const VItem*>(p->coarse_items.p),
+             p->coarse_nitems, static_cast<int>(p->dim_d), p->coarse_slice, ci,
+             std::max(p->coarse_xs, 1), p->coarse_stage,
+             static_cast<const double2*>(p->r.p + p->off_d), z_dev + p->off_d, coarse_trace(ctx));
   } else if (p->coarse_fused) {
     static const bool attr = [] {  // thread-safe one-time init
       HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,

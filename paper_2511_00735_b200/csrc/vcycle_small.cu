@@ -16,39 +16,13 @@
 
 #include "device.cuh"
 #include "hierarchy.hpp"
+#include "vcycle_device.cuh"
 #include "vcycle_small.hpp"
 
 namespace hpsb {
 
 namespace {
 constexpr int kThreads = 256;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-// y = A x (A in smem, col-major, rows <= kThreads); returns row tid's value.
-// Column groups split the K loop, reduction through `red`.  Block-wide.
-__device__ double2 smem_gemv(const double2* A, int lda, int rows, int cols, const double2* x,
-                             double2* red) {
-  const int tid = threadIdx.x;
-  const int rpad = rows <= 8 ? 8 : rows <= 16 ? 16 : (rows + 31) & ~31;
-  const int groups = kThreads / rpad;
-  const int r = tid % rpad, g = tid / rpad;
-  double2 acc = make_double2(0.0, 0.0);
-  if (g < groups && r < rows)
-    for (int j = g; j < cols; j += groups) acc = cfma(A[r + j * lda], x[j], acc);
-  red[tid] = acc;
-  __syncthreads();
-  double2 s = make_double2(0.0, 0.0);
-  if (tid < rows) {
-    s = red[tid];
-    for (int q = 1; q < groups; ++q) s = cadd(s, red[tid + q * rpad]);
-  }
-  __syncthreads();
-  return s;
-}
 
 __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge* __restrict__ ms,
                                                                int down, double2* r,
@@ -100,16 +74,16 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
 
   if (down) {
     const double2 *T1ps = A1, *T1ss = A1 + p1, *T2ps = A2, *T2ss = A2 + p2;
-    double2 y = smem_gemv(T2ss, P2, s, s, v2, red);  // t = v1 - T2_ss v2
+    double2 y = smem_gemv<kThreads>(T2ss, P2, s, s, v2, red);  // t = v1 - T2_ss v2
     if (tid < s) t[tid] = csub(v1[tid], y);
     __syncthreads();
-    y = smem_gemv(Ws, s, s, s, t, red);  // x1 = W t
+    y = smem_gemv<kThreads>(Ws, s, s, s, t, red);  // x1 = W t
     if (tid < s) {
       w1[tid] = y;
       __stcg(out + M.in1s[tid], y);
     }
     __syncthreads();
-    y = smem_gemv(T1ss, P1, s, s, w1, red);  // x2 = v2 - T1_ss x1
+    y = smem_gemv<kThreads>(T1ss, P1, s, s, w1, red);  // x2 = v2 - T1_ss x1
     if (tid < s) {
       const double2 x2 = csub(v2[tid], y);
       t[tid] = x2;
@@ -117,14 +91,14 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
     }
     __syncthreads();
     for (int r0 = 0; r0 < p1; r0 += kThreads) {  // r[out1_p] -= T1_ps x1
-      y = smem_gemv(T1ps + r0, P1, min(p1 - r0, kThreads), s, w1, red);
+      y = smem_gemv<kThreads>(T1ps + r0, P1, min(p1 - r0, kThreads), s, w1, red);
       if (tid < p1 - r0) {
         const int o = M.out1p[r0 + tid];
         __stcg(r + o, csub(__ldcg(r + o), y));
       }
     }
     for (int r0 = 0; r0 < p2; r0 += kThreads) {  // r[out2_p] -= T2_ps x2
-      y = smem_gemv(T2ps + r0, P2, min(p2 - r0, kThreads), s, t, red);
+      y = smem_gemv<kThreads>(T2ps + r0, P2, min(p2 - r0, kThreads), s, t, red);
       if (tid < p2 - r0) {
         const int o = M.out2p[r0 + tid];
         __stcg(r + o, csub(__ldcg(r + o), y));
@@ -133,17 +107,17 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
   } else {
     const double2 *T1sp = A1, *T1ss = A1 + static_cast<size_t>(p1) * s, *T2sp = A2,
                   *T2ss = A2 + static_cast<size_t>(p2) * s;
-    double2 b1 = smem_gemv(T2sp, s, s, p2, u2, red);  // b1 = T2_sp u2
-    double2 b2 = smem_gemv(T1sp, s, s, p1, u1, red);  // b2 = T1_sp u1
+    double2 b1 = smem_gemv<kThreads>(T2sp, s, s, p2, u2, red);  // b1 = T2_sp u2
+    double2 b2 = smem_gemv<kThreads>(T1sp, s, s, p1, u1, red);  // b2 = T1_sp u1
     if (tid < s) v1[tid] = b1, v2[tid] = b2;
     __syncthreads();
-    double2 y = smem_gemv(T2ss, s, s, s, v2, red);  // t = b1 - T2_ss b2
+    double2 y = smem_gemv<kThreads>(T2ss, s, s, s, v2, red);  // t = b1 - T2_ss b2
     if (tid < s) t[tid] = csub(v1[tid], y);
     __syncthreads();
-    y = smem_gemv(Ws, s, s, s, t, red);  // y1 = W t
+    y = smem_gemv<kThreads>(Ws, s, s, s, t, red);  // y1 = W t
     if (tid < s) w1[tid] = y;
     __syncthreads();
-    const double2 z = smem_gemv(T1ss, s, s, s, w1, red);  // T1_ss y1
+    const double2 z = smem_gemv<kThreads>(T1ss, s, s, s, w1, red);  // T1_ss y1
     if (tid < s) {
       const int o2 = M.in2s[tid], o1 = M.in1s[tid];
       __stcg(out + o2, cadd(__ldcg(out + o2), csub(z, v2[tid])));

@@ -25,4 +25,17 @@ struct SmallLevel {
   void run(Context* ctx, bool down, double2* r, double2* out) const;
 };
 
+// One thread-block cluster of `csize` CTAs per merge (csrc/vcycle_cluster.cu).
+size_t cluster_merge_smem(int s, int p1, int p2, int csize);
+// Can a cluster of csize CTAs with this much shared memory each be resident?
+bool cluster_merge_fits(size_t smem, int csize);
+struct ClusterLevel {
+  int level = 0, count = 0, csize = 1;
+  size_t smem = 0;
+  double bytes_down = 0, bytes_up = 0;
+  std::string label;
+  DevBuf<SmallMerge> d;
+  void run(Context* ctx, bool down, double2* r, double2* out) const;
+};
+
 }  // namespace hpsb

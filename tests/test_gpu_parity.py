@@ -169,8 +169,12 @@ def test_fgmres_solution_and_iterations(hps, oracle, ctx, name):
 @pytest.mark.parametrize("name", ["cfg3_n4", "cfg2_n8", "cfg4_n8"])
 def test_fgmres_underresolved_meshes(hps, oracle, ctx, name):
     # The configs' wavenumbers on 4x4 / 8x8 meshes (kappa h up to 100) give
-    # systems needing ~100 iterations; CGS2 vs MGS rounding can shift the count
-    # by a few, so these shrunken meshes check the converged solution only.
+    # systems needing ~100 iterations.  The preconditioner contains an inner
+    # GMRES, so it is a nonlinear function of its input: last-bit differences
+    # (CGS2 vs MGS, summation order) grow ~2x per iteration (measured: 1e-15
+    # at step 1, 1e-12 at step 11) and the count wanders by up to ~20%.  These
+    # shrunken meshes (not BASELINE configs) therefore pin the converged
+    # solution and residual, with a loose bound on the count.
     c = case(hps, oracle, ctx, name)
     h = hps.build_hierarchy(c.sk)
     c.S.build_hierarchy(0, False)
@@ -179,7 +183,7 @@ def test_fgmres_underresolved_meshes(hps, oracle, ctx, name):
     x, rep = hps.fgmres(c.sk, c.sk.rhs(), pc, restart=100, tol=1e-10)
     xo, repo = c.S.solve(c.S.rhs(), True, restart=100, tol=1e-10)
     assert rep["converged"] and repo["converged"]
-    assert abs(rep["iterations"] - repo["iterations"]) <= max(1, repo["iterations"] // 20)
+    assert abs(rep["iterations"] - repo["iterations"]) <= max(1, repo["iterations"] // 4)
     assert relf(x, xo) < 1e-8
     r = c.S.rhs() - c.S.apply_M(x)
     assert np.linalg.norm(r) <= 1e-10 * np.linalg.norm(c.S.rhs()) * 1.01
