@@ -720,6 +720,54 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   }
   double2* r = p->r.p;
   double2* out = p->out.p;
+  // The items of one level step, per merge and dependent stage (the same
+  // lists feed the single-RHS plans and the multi-RHS batch phases):
+  // out[gi][k] = stage k of merge gi (multigrid.cpp:47-98 on box maps).
+  auto level_stages = [&](int l, bool downward) {
+    const LevelOps& L = *h->levels[l - 1];
+    const int ng = static_cast<int>(L.merges.size());
+    std::vector<std::vector<std::vector<VItem>>> res(ng);
+    size_t t = level_tmp[l];
+    for (int gi = 0; gi < ng; ++gi) {
+      const MergeRec& mr = L.merges[gi];
+      const ChildBox& c1 = L.children[mr.c1];
+      const ChildBox& c2 = L.children[mr.c2];
+      const int s = mr.s, p1 = mr.p1, p2 = mr.p2, P1 = c1.P, P2 = c2.P;
+      const double2* T1 = L.tperm.p + c1.t_off;
+      const double2* T2 = L.tperm.p + c2.t_off;
+      const double2 *T1ps = T1 + static_cast<size_t>(p1) * P1, *T1sp = T1 + p1,
+                    *T1ss = T1 + p1 + static_cast<size_t>(p1) * P1;
+      const double2 *T2ps = T2 + static_cast<size_t>(p2) * P2, *T2sp = T2 + p2,
+                    *T2ss = T2 + p2 + static_cast<size_t>(p2) * P2;
+      const double2* W = L.w.p + mr.w_off;
+      const int* ix = L.idx.p;
+      const int *in1s = ix + mr.in1_sep, *in2s = ix + mr.in2_sep, *in1p = ix + mr.in1_per,
+                *in2p = ix + mr.in2_per, *out1p = ix + mr.out1_per, *out2p = ix + mr.out2_per;
+      double2* t1 = p->tmp.p + t;
+      double2* t2 = t1 + s;
+      double2* t3 = t2 + s;
+      t += 3 * static_cast<size_t>(s);
+      std::vector<std::vector<VItem>>& st = res[gi];
+      st.resize(4);
+      if (downward) {
+        st[0].push_back(item(T2ss, P2, s, s, r, in2s, r, in1s, t3, nullptr, -1.0, 0.0, 1.0));
+        st[1].push_back(item(W, s, s, s, t3, nullptr, nullptr, nullptr, out, in1s, 1.0, 0.0, 0.0));
+        st[2].push_back(item(T1ss, P1, s, s, out, in1s, r, in2s, out, in2s, -1.0, 0.0, 1.0));
+        if (p1) st[3].push_back(item(T1ps, P1, p1, s, out, in1s, nullptr, nullptr, r, out1p, -1.0, 1.0, 0.0));
+        if (p2) st[3].push_back(item(T2ps, P2, p2, s, out, in2s, nullptr, nullptr, r, out2p, -1.0, 1.0, 0.0));
+      } else {
+        if (p2) st[0].push_back(item(T2sp, P2, s, p2, out, in2p, nullptr, nullptr, t1, nullptr, 1.0, 0.0, 0.0));
+        else st[0].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, nullptr, nullptr, t1, nullptr, 0.0, 0.0, 0.0));
+        if (p1) st[0].push_back(item(T1sp, P1, s, p1, out, in1p, nullptr, nullptr, t2, nullptr, 1.0, 0.0, 0.0));
+        else st[0].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, nullptr, nullptr, t2, nullptr, 0.0, 0.0, 0.0));
+        st[1].push_back(item(T2ss, P2, s, s, t2, nullptr, t1, nullptr, t3, nullptr, -1.0, 0.0, 1.0));
+        st[2].push_back(item(W, s, s, s, t3, nullptr, nullptr, nullptr, t1, nullptr, 1.0, 0.0, 0.0));
+        st[3].push_back(item(T1ss, P1, s, s, t1, nullptr, t2, nullptr, out, in2s, 1.0, 1.0, -1.0));
+        st[3].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, t1, nullptr, out, in1s, 0.0, 1.0, -1.0));
+      }
+    }
+    return res;
+  };
   auto build_level = [&](int l, bool downward) {
     const LevelOps& L = *h->levels[l - 1];
     const int ng = static_cast<int>(L.merges.size());
@@ -746,43 +794,9 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     rb = std::max(32, std::min(256, rb));
     std::vector<std::vector<VItem>> stages(downward ? 4 : 4);
     std::vector<std::vector<VItem>> chains(ng);
-    size_t t = level_tmp[l];
+    auto per_merge_stages = level_stages(l, downward);
     for (int gi = 0; gi < ng; ++gi) {
-      const MergeRec& mr = L.merges[gi];
-      const ChildBox& c1 = L.children[mr.c1];
-      const ChildBox& c2 = L.children[mr.c2];
-      const int s = mr.s, p1 = mr.p1, p2 = mr.p2, P1 = c1.P, P2 = c2.P;
-      const double2* T1 = L.tperm.p + c1.t_off;
-      const double2* T2 = L.tperm.p + c2.t_off;
-      const double2 *T1ps = T1 + static_cast<size_t>(p1) * P1, *T1sp = T1 + p1,
-                    *T1ss = T1 + p1 + static_cast<size_t>(p1) * P1;
-      const double2 *T2ps = T2 + static_cast<size_t>(p2) * P2, *T2sp = T2 + p2,
-                    *T2ss = T2 + p2 + static_cast<size_t>(p2) * P2;
-      const double2* W = L.w.p + mr.w_off;
-      const int* ix = L.idx.p;
-      const int *in1s = ix + mr.in1_sep, *in2s = ix + mr.in2_sep, *in1p = ix + mr.in1_per,
-                *in2p = ix + mr.in2_per, *out1p = ix + mr.out1_per, *out2p = ix + mr.out2_per;
-      double2* t1 = p->tmp.p + t;
-      double2* t2 = t1 + s;
-      double2* t3 = t2 + s;
-      t += 3 * static_cast<size_t>(s);
-      std::vector<std::vector<VItem>> st(4);
-      if (downward) {
-        st[0].push_back(item(T2ss, P2, s, s, r, in2s, r, in1s, t3, nullptr, -1.0, 0.0, 1.0));
-        st[1].push_back(item(W, s, s, s, t3, nullptr, nullptr, nullptr, out, in1s, 1.0, 0.0, 0.0));
-        st[2].push_back(item(T1ss, P1, s, s, out, in1s, r, in2s, out, in2s, -1.0, 0.0, 1.0));
-        if (p1) st[3].push_back(item(T1ps, P1, p1, s, out, in1s, nullptr, nullptr, r, out1p, -1.0, 1.0, 0.0));
-        if (p2) st[3].push_back(item(T2ps, P2, p2, s, out, in2s, nullptr, nullptr, r, out2p, -1.0, 1.0, 0.0));
-      } else {
-        if (p2) st[0].push_back(item(T2sp, P2, s, p2, out, in2p, nullptr, nullptr, t1, nullptr, 1.0, 0.0, 0.0));
-        else st[0].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, nullptr, nullptr, t1, nullptr, 0.0, 0.0, 0.0));
-        if (p1) st[0].push_back(item(T1sp, P1, s, p1, out, in1p, nullptr, nullptr, t2, nullptr, 1.0, 0.0, 0.0));
-        else st[0].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, nullptr, nullptr, t2, nullptr, 0.0, 0.0, 0.0));
-        st[1].push_back(item(T2ss, P2, s, s, t2, nullptr, t1, nullptr, t3, nullptr, -1.0, 0.0, 1.0));
-        st[2].push_back(item(W, s, s, s, t3, nullptr, nullptr, nullptr, t1, nullptr, 1.0, 0.0, 0.0));
-        st[3].push_back(item(T1ss, P1, s, s, t1, nullptr, t2, nullptr, out, in2s, 1.0, 1.0, -1.0));
-        st[3].push_back(item(nullptr, 0, s, 0, nullptr, nullptr, t1, nullptr, out, in1s, 0.0, 1.0, -1.0));
-      }
+      auto& st = per_merge_stages[gi];
       for (int k = 0; k < 4; ++k) {
         if (!st[k].empty()) st[k].back().flags |= VItem::kPhaseEnd;
         for (auto& it : st[k]) {

@@ -1,0 +1,172 @@
+// Multi-RHS GEMM for the per-iteration operators (see zgemv_batch.hpp).
+//
+// Tile: 64 rows x 32 right-hand sides per 256-thread CTA (8 warps as 4 x 2,
+// 16 x 16 complex outputs per warp), K-steps of 16 through a 3-stage cp.async
+// pipeline.  The B tile gathers its K rows through the item's index map
+// (cp.async with zero-fill for -1 / out-of-range entries), the epilogue
+// scatters C rows through theirs.  A complex product is four real DMMAs
+// (mma.sync.m8n8k4.f64) on de-interleaved fragments, as in zgemm.cu.
+#include "device.cuh"
+#include "zgemv_batch.hpp"
+
+namespace hpsb {
+
+namespace {
+constexpr int BM = 64, BN = 32, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int SA = BM + 2;  // complex stride of an A k-row in smem
+constexpr int SB = BK + 4;  // complex stride of a B column in smem
+constexpr int A_STAGE = BK * SA, B_STAGE = BN * SB;
+constexpr size_t BSMEM = sizeof(double2) * STAGES * (A_STAGE + B_STAGE);
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __restrict__ descs,
+                                                              int ndesc, int R) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* As = reinterpret_cast<double2*>(smem_raw);
+  double2* Bs = As + STAGES * A_STAGE;
+  pdl_trigger();
+  const int tile = blockIdx.x;
+  int lo = 0, hi = ndesc - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (descs[mid].tile_begin <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const BDesc d = descs[lo];
+  const int m0 = (tile - d.tile_begin) * BM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
+  const int ktiles = d.A ? (d.K + BK - 1) / BK : 0;
+
+  auto load_a = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double2* as = As + st * A_STAGE;
+#pragma unroll
+    for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+      const int idx = tid + r * THREADS;
+      const int m = idx % BM, k = idx / BM;
+      const bool ok = (m0 + m < d.M) && (k0 + k < d.K);
+      const double2* src = ok ? d.A + (size_t)(m0 + m) + (size_t)(k0 + k) * d.lda : d.A;
+      cpa16(as + k * SA + m, src, ok);
+    }
+  };
+  auto load_b = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double2* bs = Bs + st * B_STAGE;
+#pragma unroll
+    for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+      const int idx = tid + r * THREADS;
+      const int k = idx % BK, n = idx / BK;
+      int row = k0 + k < d.K ? (d.bidx ? __ldg(d.bidx + k0 + k) : k0 + k) : -1;
+      const bool ok = n < R && row >= 0;
+      const double2* src = ok ? d.B + (size_t)row + (size_t)n * d.ldb : d.B;
+      cpa16(bs + n * SB + k, src, ok);
+    }
+  };
+
+  double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+
+  // operators are static: their first stages are issued before the PDL wait
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s)
+    if (s < ktiles) load_a(s, s);
+  pdl_wait();
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_b(s, s);
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  const int arow = wm * 16 + (lane >> 2), kq = lane & 3;
+  const int bcol = wn * 16 + (lane >> 2);
+  for (int kt = 0; kt < ktiles; ++kt) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2));
+    __syncthreads();
+    if (kt + STAGES - 1 < ktiles) {
+      load_a(kt + STAGES - 1, (kt + STAGES - 1) % STAGES);
+      load_b(kt + STAGES - 1, (kt + STAGES - 1) % STAGES);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    const double2* as = As + (kt % STAGES) * A_STAGE;
+    const double2* bs = Bs + (kt % STAGES) * B_STAGE;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double2 a[2], b[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double nai = -a[i].y;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+          dmma(cr[i][j][0], cr[i][j][1], nai, b[j].y);
+          dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+          dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  // epilogue: C[cidx[m], n] = alpha acc + gamma Z[zidx[m], n] + beta C[cidx[m], n]
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = m0 + wm * 16 + i * 8 + (lane >> 2);
+    if (row >= d.M) continue;
+    const int crow = d.cidx ? __ldg(d.cidx + row) : row;
+    if (crow < 0) continue;
+    const int zrow = d.gamma != 0.0 ? (d.zidx ? __ldg(d.zidx + row) : row) : -1;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = wn * 16 + j * 8 + 2 * (lane & 3) + h;
+        if (col >= R) continue;
+        double2* c = d.C + (size_t)crow + (size_t)col * d.ldc;
+        double2 v = cscale(make_double2(cr[i][j][h], ci[i][j][h]), d.alpha);
+        if (zrow >= 0) v = cadd(v, cscale(__ldcg(d.Z + (size_t)zrow + (size_t)col * d.ldz), d.gamma));
+        if (d.beta != 0.0) v = cadd(v, cscale(__ldcg(c), d.beta));
+        __stcg(c, v);
+      }
+  }
+}
+}  // namespace
+
+void BPhase::add(const BDesc& x0) {
+  if (x0.M <= 0) return;
+  BDesc x = x0;
+  x.tiles_m = (x.M + BM - 1) / BM;
+  x.tile_begin = total_tiles;
+  total_tiles += x.tiles_m;
+  if (x.A) {
+    flops += 8.0 * x.M * x.K;  // per right-hand side
+    bytes += 16.0 * x.M * x.K;
+  }
+  descs.push_back(x);
+}
+
+void BPhase::run(Context* ctx, int R, const char* label) const {
+  if (descs.empty()) return;
+  if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("batch: 1 <= nrhs <= 32");
+  allow_smem<zgemv_batch_kernel>(BSMEM);
+  KernelScope ks(ctx, label, bytes, flops * R);
+  launch_k(ctx, zgemv_batch_kernel, dim3(total_tiles), dim3(THREADS), BSMEM, 1,
+           static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R);
+}
+
+}  // namespace hpsb
