@@ -93,7 +93,17 @@ class ClockSampler:
 
 def gmres_roofline(state, its, restart, solve_s, hbm_gbs) -> dict:
     """Pinned bytes of all timed iterations: operators + fused
-    CGS2 vector traffic 16 dim (4(j+1)+6) at Arnoldi step j."""
+    CGS2 vector traffic 16 dim (4(j+1)+6) at Arnoldi step j.  Multi-RHS
+    (cfg4): FP64 bound: 8 R flops per stored operator entry per
+    block iteration, against the measured DMMA peak."""
+    R = state.get("nrhs", 1)
+    if R > 1:
+        flops = sum(8.0 * R * state["pinned_bytes"] / 16.0 * b for b in state["timed_block_its"])
+        achieved = flops / solve_s / 1e12
+        return {"pinned_flops_per_block_iteration": 8.0 * R * state["pinned_bytes"] / 16.0,
+                "block_iterations": state["timed_block_its"], "nrhs": R, "achieved": achieved,
+                "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
+                "frac": achieved / FP64_DMMA_PEAK_TFLOPS}
     total = 0.0
     for n_it in its:
         for i in range(n_it):
@@ -209,16 +219,28 @@ def run_b200(args, rank, world, local):
             print(f"[setup wall ms] elements {1e3 * (w1 - w0):.1f} skeleton {1e3 * (w2 - w1):.1f} "
                   f"hierarchy {1e3 * (w3 - w2):.1f} (device {1e3 * hier.build_seconds:.1f}) "
                   f"precond {1e3 * (w4 - w3):.1f}", file=sys.stderr)
-        x = torch.empty(2 * sk.dim, dtype=torch.float64, device=f"cuda:{local}")
-        rep = hps.SolveReport()
         cfg = hps.KrylovConfig(restart, tol, 2000, 0, 1)
-        hps._check(hps._lib.hpsb_fgmres_dev(sk._h, pc._h, ctypes.c_void_p(sk.rhs_dev_ptr(0)),
-                                            ctypes.c_void_p(x.data_ptr()), cfg,
-                                            ctypes.byref(rep)), allow=(hps.OK,))
+        nrhs = sk.nrhs if world == 1 else 1
+        x = torch.empty(2 * sk.dim * nrhs, dtype=torch.float64, device=f"cuda:{local}")
+        if nrhs > 1:
+            # cfg4: all right-hand sides in lockstep, one multi-RHS operator
+            # pass per iteration (hpsb_fgmres_batch_dev)
+            reps = (hps.SolveReport * nrhs)()
+            hps._check(hps._lib.hpsb_fgmres_batch_dev(
+                sk._h, pc._h, ctypes.c_void_p(sk.rhs_dev_ptr(0)), ctypes.c_void_p(x.data_ptr()),
+                nrhs, cfg, reps), allow=(hps.OK,))
+            seconds, it_total = reps[0].seconds, sum(r.iterations for r in reps)
+            state["block_its"] = state.get("block_its", []) + [max(r.iterations for r in reps)]
+        else:
+            rep = hps.SolveReport()
+            hps._check(hps._lib.hpsb_fgmres_dev(sk._h, pc._h, ctypes.c_void_p(sk.rhs_dev_ptr(0)),
+                                                ctypes.c_void_p(x.data_ptr()), cfg,
+                                                ctypes.byref(rep)), allow=(hps.OK,))
+            seconds, it_total = rep.seconds, rep.iterations
         fe, fm = hier.pinned_flops()
-        state.update(dim=sk.dim, pc_bytes=pc.bytes_per_apply, depth=hier.depth,
+        state.update(dim=sk.dim, pc_bytes=pc.bytes_per_apply, depth=hier.depth, nrhs=nrhs,
                      pinned_flops=fe + fm, pinned_bytes=pc.pinned_bytes_per_iteration)
-        return t_setup, rep.seconds, rep.iterations, sk.dim
+        return t_setup, seconds, it_total, sk.dim
 
     def flush_l2():
         flush.zero_()
@@ -241,6 +263,8 @@ def run_b200(args, rank, world, local):
             solve_s += tv
             dof_its += dim * it
             its.append(it)
+            if state.get("nrhs", 1) > 1:
+                state.setdefault("timed_block_its", []).append(state["block_its"][-1])
             flush_l2()
     torch.cuda.synchronize()
     launches = ctx.launches - launches0
@@ -294,13 +318,20 @@ def run_b200(args, rank, world, local):
     sk_h = hps.assemble_skeleton(el_h, prob)
     hier_h = hps.build_hierarchy(sk_h, factor_coarse=False)
     pc_h = hps.build_preconditioner(hier_h, coarse_iters=4)
-    rhs_host = torch.from_numpy(sk_h.rhs()).pin_memory().numpy()
+    nrhs_e = state.get("nrhs", 1)
+    rhs_np = np.stack([sk_h.rhs(b) for b in range(nrhs_e)]) if nrhs_e > 1 else sk_h.rhs()
+    rhs_host = torch.from_numpy(rhs_np).pin_memory().numpy()
     e2e_dof, e2e_t = 0, 0.0
     for _ in range(max(1, min(args.steps, 3))):
         t0 = time.perf_counter()
-        x, rep = hps.fgmres(sk_h, rhs_host, pc_h, restart=restart, tol=tol)
+        if nrhs_e > 1:
+            x, reps_e = hps.fgmres_batch(sk_h, rhs_host, pc_h, restart=restart, tol=tol)
+            its_e = sum(r["iterations"] for r in reps_e)
+        else:
+            x, rep = hps.fgmres(sk_h, rhs_host, pc_h, restart=restart, tol=tol)
+            its_e = rep["iterations"]
         e2e_t += time.perf_counter() - t0
-        e2e_dof += sk_h.dim * rep["iterations"]
+        e2e_dof += sk_h.dim * its_e
     e2e_value = e2e_dof / e2e_t
     # e2e setup: host coefficient arrays -> preconditioner ready (previous
     # objects released first, as in the timed steps)
@@ -324,6 +355,7 @@ def run_b200(args, rank, world, local):
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": f"cfg{args.config}", "n": prob.n, "N": prob.order,
                    "kappa": prob.kappa, "dof": state["dim"], "elements": ne,
+                   "nrhs": state.get("nrhs", 1),
                    "levels": state["depth"], "restart": restart, "tol": tol, "seed": args.seed,
                    "mg": "depth=L, gamma=1, coarse_iters=4", "l2": "flushed between steps (256 MB)",
                    "parallelism": (f"quadtree-subtree sharding x{world} (NCCL)" if sharded
@@ -347,7 +379,8 @@ def run_b200(args, rank, world, local):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": 16 * state["dim"], "d2h_bytes_per_step": 16 * state["dim"],
+                "h2d_bytes_per_step": 16 * state["dim"] * state.get("nrhs", 1),
+                "d2h_bytes_per_step": 16 * state["dim"] * state.get("nrhs", 1),
                 "setup_elements_per_s": e2e_setup},
     }
     if world == 1 and not args.no_cpu_baseline:

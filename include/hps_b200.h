@@ -182,6 +182,21 @@ hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rh
 hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs_dev,
                             double* x_dev, hpsb_krylov_config cfg, hpsb_solve_report* report);
 
+/* Multi-RHS (nrhs <= 32, single GPU): the R vectors are stored column-wise
+ * (vector b at offset b * dim).  The operators are applied to all R at once
+ * (one pass over the stored maps per application, FP64 tensor-core GEMMs);
+ * FGMRES runs R independent solves in lockstep with per-RHS Arnoldi,
+ * restarts and convergence (reports[b] per right-hand side).                */
+hpsb_status hpsb_skeleton_apply_batch_dev(hpsb_skeleton sk, const double* x_dev, double* y_dev,
+                                          int nrhs);
+hpsb_status hpsb_precond_apply_batch_dev(hpsb_precond p, const double* v_dev, double* z_dev,
+                                         int nrhs);
+hpsb_status hpsb_fgmres_batch(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                              int nrhs, hpsb_krylov_config cfg, hpsb_solve_report* reports);
+hpsb_status hpsb_fgmres_batch_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs_dev,
+                                  double* x_dev, int nrhs, hpsb_krylov_config cfg,
+                                  hpsb_solve_report* reports);
+
 /* Device pointer of the skeleton's right-hand side r (for _dev solves). */
 const double* hpsb_skeleton_rhs_dev(hpsb_skeleton sk, int r);
 

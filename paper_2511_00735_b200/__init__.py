@@ -110,10 +110,16 @@ _sig("hpsb_precond_create", _st, _VP, MgConfig, ctypes.POINTER(_VP))
 _sig("hpsb_precond_destroy", _st, _VP)
 _sig("hpsb_precond_apply", _st, _VP, _D, _D)
 _sig("hpsb_direct_solve", _st, _VP, _D, _D)
+_sig("hpsb_skeleton_apply_batch_dev", _st, _VP, _VP, _VP, ctypes.c_int)
+_sig("hpsb_precond_apply_batch_dev", _st, _VP, _VP, _VP, ctypes.c_int)
 _sig("hpsb_direct_solve_dev", _st, _VP, _VP, _VP)
 _sig("hpsb_precond_apply_dev", _st, _VP, _VP, _VP)
 _sig("hpsb_fgmres", _st, _VP, _VP, _D, _D, KrylovConfig, ctypes.POINTER(SolveReport))
 _sig("hpsb_fgmres_dev", _st, _VP, _VP, _VP, _VP, KrylovConfig, ctypes.POINTER(SolveReport))
+_sig("hpsb_fgmres_batch", _st, _VP, _VP, _D, _D, ctypes.c_int, KrylovConfig,
+     ctypes.POINTER(SolveReport))
+_sig("hpsb_fgmres_batch_dev", _st, _VP, _VP, _VP, _VP, ctypes.c_int, KrylovConfig,
+     ctypes.POINTER(SolveReport))
 _sig("hpsb_context_timer_start", _st, _VP)
 _sig("hpsb_context_timer_stop", _st, _VP, _D)
 _sig("hpsb_context_profile", _st, _VP, ctypes.c_int)
@@ -493,6 +499,21 @@ def fgmres(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: i
                             _dp(x.view(np.float64)), cfg, ctypes.byref(rep)),
            allow=(OK, NO_CONVERGENCE))
     return x, rep.as_dict()
+
+
+def fgmres_batch(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: int = 60,
+                 tol: float = 1e-8, max_iters: int = 2000):
+    """R <= 32 right-hand sides (rows of `rhs`) solved in lockstep with
+    multi-RHS operator applications; one report per right-hand side."""
+    rhs = np.ascontiguousarray(np.atleast_2d(rhs), dtype=np.complex128)
+    R = rhs.shape[0]
+    x = np.zeros_like(rhs)
+    reps = (SolveReport * R)()
+    cfg = KrylovConfig(restart, tol, max_iters, 0, 1)
+    _check(_lib.hpsb_fgmres_batch(sk._h, precond._h if precond else None,
+                                  _dp(rhs.view(np.float64)), _dp(x.view(np.float64)), R, cfg, reps),
+           allow=(OK, NO_CONVERGENCE))
+    return x, [r.as_dict() for r in reps]
 
 
 def gmres(sk: SkeletonSystem, rhs, restart: int = 60, tol: float = 1e-8, max_iters: int = 2000):

@@ -654,4 +654,51 @@ hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rh
   });
 }
 
+hpsb_status hpsb_skeleton_apply_batch_dev(hpsb_skeleton sk, const double* x, double* y, int nrhs) {
+  return guarded([&] {
+    REQUIRE(sk && x && y, "skeleton_apply: null argument");
+    hpsb::skeleton_apply_batch(sk->s.get(), reinterpret_cast<const double2*>(x),
+                               reinterpret_cast<double2*>(y), nrhs);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_precond_apply_batch_dev(hpsb_precond p, const double* v, double* z, int nrhs) {
+  return guarded([&] {
+    REQUIRE(p && v && z, "precond_apply: null argument");
+    hpsb::precond_apply_batch(p->p, reinterpret_cast<const double2*>(v),
+                              reinterpret_cast<double2*>(z), nrhs);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_fgmres_batch_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs,
+                                  double* x, int nrhs, hpsb_krylov_config cfg,
+                                  hpsb_solve_report* reports) {
+  return guarded([&] {
+    REQUIRE(sk && rhs && x && reports, "fgmres: null argument");
+    return hpsb::fgmres_batch(sk->s.get(), precond ? precond->p : nullptr,
+                              reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x),
+                              nrhs, cfg, reports);
+  });
+}
+
+hpsb_status hpsb_fgmres_batch(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                              int nrhs, hpsb_krylov_config cfg, hpsb_solve_report* reports) {
+  return guarded([&] {
+    REQUIRE(sk && rhs && x && reports, "fgmres: null argument");
+    REQUIRE(nrhs >= 1 && nrhs <= 32, "fgmres: 1 <= nrhs <= 32");
+    auto* S = sk->s.get();
+    cudaStream_t st = S->ctx->stream;
+    const size_t count = static_cast<size_t>(nrhs) * S->dim;
+    hpsb::DevBuf<double2> b(count), xd(count);
+    HPSB_CUDA(cudaMemcpyAsync(b.p, rhs, b.bytes(), cudaMemcpyHostToDevice, st));
+    const hpsb_status rc = hpsb::fgmres_batch(S, precond ? precond->p : nullptr, b.p, xd.p, nrhs,
+                                              cfg, reports);
+    HPSB_CUDA(cudaMemcpyAsync(x, xd.p, xd.bytes(), cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    return rc;
+  });
+}
+
 }  // extern "C"

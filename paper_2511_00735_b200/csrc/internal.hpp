@@ -336,6 +336,7 @@ struct Skeleton {
   DevBuf<double2> tside;  // [nrhs][e][nb] physical-side impedance data
   VPlan apply_plan;      // y = x + sum_e scatter(T_e gather(x))
   DevBuf<double2> x_buf, y_buf;  // plan endpoints
+  std::shared_ptr<void> batch;   // multi-RHS matvec phase (skeleton.cu), built on first use
 };
 
 struct LevelOps;
@@ -356,6 +357,11 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
                                          const double* coeff_dev, const double2* source_dev);
 std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs);
 void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev);
+// Multi-RHS: R <= 32 vectors stored column-wise with leading dimension dim.
+void precond_apply_batch(Precond* p, const double2* v, double2* z, int R);
+void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int R);
+hpsb_status fgmres_batch(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
+                         const hpsb_krylov_config& cfg, hpsb_solve_report* reports);
 void recover_field(const Skeleton* sk, const double2* x_dev, int rhs_index, double2* field_dev);
 std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth);
 void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,

@@ -18,6 +18,7 @@
 
 #include "device.cuh"
 #include "internal.hpp"
+#include "zgemv_batch.hpp"
 
 namespace hpsb {
 
@@ -107,16 +108,28 @@ __global__ void __launch_bounds__(kThreads) dots_fused_kernel(
 // fixed block order into out (deterministic); else reduce_kernel does.
 constexpr int kOrthThreads = 128;
 constexpr int kOrthMaxR = 8;
+// Multi-RHS: blockIdx.y selects the right-hand side; its basis, vector,
+// coefficients, partials and ticket sit at the given strides.
+struct OrthStride {
+  int64_t v = 0, w = 0, p = 0;
+  int h = 0;
+};
 template <bool kUpdate>
 __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd,
     int nupd, double2* w, int64_t n, int R, double2* partial, double2* out, unsigned* ticket,
-    int fused) {
+    int fused, OrthStride bs) {
   __shared__ double2 sh[kOrthThreads / 32][104];
   __shared__ double2 hs[104];
   __shared__ bool last;
   pdl_trigger();
   pdl_wait();
+  {
+    const int b = blockIdx.y;
+    V += b * bs.v, w += b * bs.w, partial += b * bs.p, ticket += b;
+    if (h_upd) h_upd += b * bs.h;
+    out += b * bs.h;
+  }
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kOrthThreads * R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (kUpdate) {
@@ -199,6 +212,39 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     out[i] = s;
   }
   if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+}
+
+// dst[b] = s[b] * src[b] for the R vectors of a block (strides ls / ld)
+__global__ void scale_batch_kernel(const double2* __restrict__ src, int64_t ls,
+                                   const double* __restrict__ s, double2* dst, int64_t ld, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.y;
+  const double f = s[b];
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 v = src[b * ls + k];
+    dst[b * ld + k] = make_double2(v.x * f, v.y * f);
+  }
+}
+
+// w[b] += sum_i h[b][i] V[i][b] (V: column i of RHS b at V + i * ldc + b * n)
+__global__ void __launch_bounds__(kThreads) axpy_batch_kernel(const double2* __restrict__ V,
+                                                             int64_t ldc, int ncols,
+                                                             const double2* __restrict__ h, int hs,
+                                                             double2* w, int64_t n) {
+  __shared__ double2 hv[104];
+  pdl_trigger();
+  pdl_wait();
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < ncols; i += blockDim.x) hv[i] = h[b * hs + i];
+  __syncthreads();
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < ncols; ++i) acc = cfma(hv[i], ldg2(V + i * ldc + b * n + k), acc);
+    w[b * n + k] = cadd(w[b * n + k], acc);
+  }
 }
 
 // out[i] = sum_b partial[b * ncols + i]  (fixed order: deterministic)
@@ -312,10 +358,10 @@ struct Work {
                    8.0 * n * (ncols + nupd));
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0);
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{});
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0);
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{});
     if (!fused)
       launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1,
                static_cast<const double2*>(partial.p), nb, nout, out);
@@ -497,5 +543,261 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   finish_time();
   return rep->converged ? HPSB_OK : HPSB_NO_CONVERGENCE;
 }
+
+
+// ------------------------------------------------------------- multi-RHS
+// R independent restarted FGMRES solves (gmres_driver per right-hand side,
+// krylov.cpp:45-178) advanced in lockstep: each iteration applies the
+// preconditioner and the interface operator to the R current basis vectors
+// at once (multi-RHS DMMA GEMMs, zgemv_batch.cu) -- the operators stream
+// once per iteration instead of R times.  The Arnoldi recurrences, Givens
+// rotations, restarts and convergence tests stay per right-hand side and
+// follow the single-RHS driver above exactly; a right-hand side that has
+// converged (or finished its cycle) is frozen with zero basis vectors.
+// Layout: basis column j of RHS b at V + (j * R + b) * n.
+namespace {
+hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
+                         const hpsb_krylov_config& cfg, hpsb_solve_report* reps);
+}
+
+// Device memory the stream-ordered pool can still hand out: free memory plus
+// what the pool holds but does not use.
+static size_t available_device_bytes(int device) {
+  size_t fr = 0, tot = 0;
+  HPSB_CUDA(cudaMemGetInfo(&fr, &tot));
+  cudaMemPool_t pool;
+  HPSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t reserved = 0, used = 0;
+  HPSB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  HPSB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return fr + static_cast<size_t>(reserved > used ? reserved - used : 0);
+}
+
+// Right-hand sides are solved in groups sized to the device memory: a group
+// of G needs (2 restart + 4) G dim complex vectors (basis V, preconditioned
+// basis Z, work vectors).
+hpsb_status fgmres_batch(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
+                         const hpsb_krylov_config& cfg, hpsb_solve_report* reps) {
+  if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("gmres: 1 <= nrhs <= 32");
+  const int64_t n = sk->dim;
+  const double per_rhs = 16.0 * n * (2.0 * std::max(cfg.restart, 1) + 4.0);
+  const double avail = 0.85 * static_cast<double>(available_device_bytes(sk->ctx->device));
+  int G = std::max(1, std::min(R, static_cast<int>(avail / per_rhs)));
+  if (const char* e = std::getenv("HPSB_BATCH_GROUP")) G = std::max(1, std::min(R, std::atoi(e)));
+  const int ngroups = (R + G - 1) / G;
+  G = (R + ngroups - 1) / ngroups;  // balanced groups
+  hpsb_status rc = HPSB_OK;
+  double seconds = 0;
+  for (int b0 = 0; b0 < R; b0 += G) {
+    const int g = std::min(G, R - b0);
+    const hpsb_status s = fgmres_group(sk, pc, rhs + static_cast<size_t>(b0) * n,
+                                       x + static_cast<size_t>(b0) * n, g, cfg, reps + b0);
+    seconds += reps[b0].seconds;
+    if (s != HPSB_OK) rc = s;
+  }
+  for (int b = 0; b < R; ++b) reps[b].seconds = seconds;
+  return rc;
+}
+
+namespace {
+hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
+                         const hpsb_krylov_config& cfg, hpsb_solve_report* reps) {
+  if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
+  if (cfg.restart > 100) throw InvalidArgument("gmres: restart must be <= 100 on the B200 path");
+  if (!(cfg.tol > 0.0 && cfg.tol < 1.0)) throw InvalidArgument("gmres: tol must lie in (0, 1)");
+  if (cfg.max_iters < 1) throw InvalidArgument("gmres: max_iters must be >= 1");
+  if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("gmres: 1 <= nrhs <= 32");
+  Context* ctx = sk->ctx;
+  if (ctx->world() > 1) throw InvalidArgument("gmres: multi-RHS is single-GPU");
+  const int64_t n = sk->dim;
+  const int restart = cfg.restart;
+  const int hs = 2 * (restart + 2) + 1;  // per-RHS slots: h1 | h2 | nn (and y)
+  for (int b = 0; b < R; ++b) reps[b] = hpsb_solve_report{};
+  DevBuf<double2> V(static_cast<size_t>(restart + 1) * R * n);
+  DevBuf<double2> Z(pc ? static_cast<size_t>(restart) * R * n : 0);
+  DevBuf<double2> w(static_cast<size_t>(R) * n), tmp(static_cast<size_t>(R) * n);
+  DevBuf<double2> hdev(static_cast<size_t>(R) * hs);
+  DevBuf<double> sdev(R);
+  DevBuf<unsigned> tickets(R);
+  HPSB_CUDA(cudaMemsetAsync(tickets.p, 0, sizeof(unsigned) * R, ctx->stream));
+  int RR = 1;  // rows per thread of the orth kernel
+  while (RR < kOrthMaxR && (n + kOrthThreads * 2 * RR - 1) / (kOrthThreads * 2 * RR) >= 2 * ctx->num_sms)
+    RR *= 2;
+  const int nb = static_cast<int>((n + kOrthThreads * RR - 1) / (kOrthThreads * RR));
+  const int64_t pstride = static_cast<int64_t>(nb) * (restart + 2);
+  DevBuf<double2> partial(static_cast<size_t>(R) * pstride);
+  // one CGS2 pass for all R: optional w -= V h_upd, then V^H w / ||w||^2
+  auto orth = [&](int ncols, const double2* h_upd, int nupd, double2* wv, double2* out) {
+    OrthStride st;
+    st.v = n, st.w = n, st.p = pstride, st.h = hs;
+    const int nout = ncols > 0 ? ncols : 1;
+    KernelScope ks(ctx, "gmres_orth", 16.0 * n * R * (nout + nupd + (h_upd ? 2 : 1)),
+                   8.0 * n * R * (ncols + nupd));
+    if (h_upd)
+      launch_k(ctx, orth_kernel<true>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
+               static_cast<const double2*>(V.p), static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
+               RR, partial.p, out, tickets.p, 1, st);
+    else
+      launch_k(ctx, orth_kernel<false>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
+               static_cast<const double2*>(V.p), static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
+               RR, partial.p, out, tickets.p, 1, st);
+  };
+  const int vblocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 2 * ctx->num_sms));
+  auto scale = [&](const double2* src, int64_t ls, const std::vector<double>& f, double2* dst, int64_t ld) {
+    HPSB_CUDA(cudaMemcpyAsync(sdev.p, f.data(), sizeof(double) * R, cudaMemcpyHostToDevice, ctx->stream));
+    KernelScope ks(ctx, "gmres_scale", 32.0 * n * R, 0.0);
+    launch_k(ctx, scale_batch_kernel, dim3(vblocks, R), dim3(256), 0, 1, src, ls,
+             static_cast<const double*>(sdev.p), dst, ld, n);
+  };
+  std::vector<double2> hh(static_cast<size_t>(R) * hs);
+  auto norms = [&](double2* vecs, std::vector<double>& out) {  // ||vecs[b]|| for all b
+    orth(0, nullptr, 0, vecs, hdev.p);
+    HPSB_CUDA(cudaMemcpyAsync(hh.data(), hdev.p, sizeof(double2) * R * hs, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    out.resize(R);
+    for (int b = 0; b < R; ++b) out[b] = std::sqrt(std::max(hh[static_cast<size_t>(b) * hs].x, 0.0));
+  };
+  HPSB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  HPSB_CUDA(cudaMemsetAsync(x, 0, sizeof(double2) * R * n, ctx->stream));
+  std::vector<double> bnorm, beta(R, 0.0), rel(R, 0.0), fac(R, 0.0);
+  HPSB_CUDA(cudaMemcpyAsync(tmp.p, rhs, sizeof(double2) * R * n, cudaMemcpyDeviceToDevice, ctx->stream));
+  norms(tmp.p, bnorm);
+  auto true_residual = [&](std::vector<double>& out) {  // ||rhs - M x|| / ||rhs||
+    skeleton_apply_batch(sk, x, tmp.p, R);
+    {
+      KernelScope ks(ctx, "gmres_sub", 48.0 * n * R, 0.0);
+      launch_k(ctx, sub_kernel, dim3(vblocks), dim3(256), 0, 1, rhs, static_cast<const double2*>(tmp.p),
+               tmp.p, static_cast<int64_t>(R) * n);
+    }
+    norms(tmp.p, out);
+    for (int b = 0; b < R; ++b) out[b] = bnorm[b] > 0.0 ? out[b] / bnorm[b] : 0.0;
+  };
+  std::vector<char> active(R), breakdown(R, 0), in_cycle(R);
+  std::vector<int> total(R, 0), jlen(R, 0);
+  for (int b = 0; b < R; ++b) {
+    active[b] = bnorm[b] > 0.0;
+    if (!active[b]) reps[b].converged = 1;
+  }
+  const int ldh = restart + 1;
+  std::vector<std::vector<cd>> H(R, std::vector<cd>(static_cast<size_t>(ldh) * restart)),
+      gv(R, std::vector<cd>(restart + 1));
+  std::vector<std::vector<Givens>> rot(R, std::vector<Givens>(restart));
+  bool first = true;
+  auto any = [&](const std::vector<char>& f) {
+    for (char c : f)
+      if (c) return true;
+    return false;
+  };
+  while (any(active)) {
+    std::vector<double> res;
+    if (first) {
+      beta = bnorm;  // tmp = rhs
+    } else {
+      true_residual(res);
+      for (int b = 0; b < R; ++b) beta[b] = res[b] * bnorm[b];
+    }
+    first = false;
+    for (int b = 0; b < R; ++b)
+      if (active[b] && (beta[b] / bnorm[b] <= cfg.tol || total[b] >= cfg.max_iters)) active[b] = 0;
+    if (!any(active)) break;
+    for (int b = 0; b < R; ++b) {
+      fac[b] = active[b] ? 1.0 / beta[b] : 0.0;
+      in_cycle[b] = active[b];
+      jlen[b] = 0;
+      std::fill(gv[b].begin(), gv[b].end(), cd(0.0, 0.0));
+      gv[b][0] = beta[b];
+    }
+    scale(tmp.p, n, fac, V.p, n);
+    for (int j = 0; j < restart && any(in_cycle); ++j) {
+      double2* Vj = V.p + static_cast<size_t>(j) * R * n;
+      double2* src = Vj;
+      if (pc) {
+        src = Z.p + static_cast<size_t>(j) * R * n;
+        precond_apply_batch(pc, Vj, src, R);
+      }
+      skeleton_apply_batch(sk, src, w.p, R);
+      orth(j + 1, nullptr, 0, w.p, hdev.p);                      // h1 = V^H w
+      orth(j + 1, hdev.p, j + 1, w.p, hdev.p + (j + 1));         // w -= V h1; h2 = V^H w
+      orth(0, hdev.p + (j + 1), j + 1, w.p, hdev.p + 2 * (j + 1));  // w -= V h2; ||w||^2
+      HPSB_CUDA(cudaMemcpyAsync(hh.data(), hdev.p, sizeof(double2) * R * hs, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+      HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+      for (int b = 0; b < R; ++b) {
+        fac[b] = 0.0;
+        if (!in_cycle[b]) continue;
+        const double2* hb = hh.data() + static_cast<size_t>(b) * hs;
+        auto Hm = [&](int i, int c) -> cd& { return H[b][i + static_cast<size_t>(c) * ldh]; };
+        for (int i = 0; i <= j; ++i) Hm(i, j) = cd(hb[i].x + hb[j + 1 + i].x, hb[i].y + hb[j + 1 + i].y);
+        const double hnext = std::sqrt(std::max(hb[2 * (j + 1)].x, 0.0));
+        Hm(j + 1, j) = hnext;
+        for (int i = 0; i < j; ++i) apply_givens(rot[b][i], Hm(i, j), Hm(i + 1, j));
+        rot[b][j] = make_givens(Hm(j, j), Hm(j + 1, j));
+        apply_givens(rot[b][j], Hm(j, j), Hm(j + 1, j));
+        apply_givens(rot[b][j], gv[b][j], gv[b][j + 1]);
+        rel[b] = std::abs(gv[b][j + 1]) / bnorm[b];
+        ++total[b];
+        jlen[b] = j + 1;
+        if (hnext <= 1e-14 * bnorm[b]) {
+          breakdown[b] = 1;
+          in_cycle[b] = 0;
+          continue;
+        }
+        fac[b] = 1.0 / hnext;
+        if (rel[b] <= cfg.tol || total[b] >= cfg.max_iters) in_cycle[b] = 0;
+      }
+      if (j + 1 < restart + 1) scale(w.p, n, fac, V.p + static_cast<size_t>(j + 1) * R * n, n);
+    }
+    // x[b] += Z[b] y[b] (V[b] y[b] without preconditioner), y from H[b] y = g[b]
+    int jmax = 0;
+    std::vector<double2> yd(static_cast<size_t>(R) * hs, make_double2(0.0, 0.0));
+    for (int b = 0; b < R; ++b) {
+      const int j = active[b] ? jlen[b] : 0;
+      jmax = std::max(jmax, j);
+      std::vector<cd> y(j);
+      for (int i = j - 1; i >= 0; --i) {
+        cd sacc = gv[b][i];
+        for (int k = i + 1; k < j; ++k) sacc -= H[b][i + static_cast<size_t>(k) * ldh] * y[k];
+        y[i] = sacc / H[b][i + static_cast<size_t>(i) * ldh];
+      }
+      for (int i = 0; i < j; ++i) yd[static_cast<size_t>(b) * hs + i] = make_double2(y[i].real(), y[i].imag());
+    }
+    if (jmax > 0) {
+      HPSB_CUDA(cudaMemcpyAsync(hdev.p, yd.data(), sizeof(double2) * R * hs, cudaMemcpyHostToDevice,
+                                ctx->stream));
+      KernelScope ks(ctx, "gmres_axpy", 16.0 * n * R * (jmax + 2), 8.0 * n * R * jmax);
+      launch_k(ctx, axpy_batch_kernel, dim3(vblocks, R), dim3(kThreads), 0, 1,
+               static_cast<const double2*>(pc ? Z.p : V.p), static_cast<int64_t>(R) * n, jmax,
+               static_cast<const double2*>(hdev.p), hs, x, n);
+    }
+    true_residual(res);
+    for (int b = 0; b < R; ++b) {
+      if (!active[b]) continue;
+      reps[b].final_residual = res[b];
+      if (res[b] <= cfg.tol) active[b] = 0;
+      if (breakdown[b] && active[b]) {
+        HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+        throw std::runtime_error("gmres: numerical breakdown before convergence (rhs " +
+                                 std::to_string(b) + ")");
+      }
+    }
+  }
+  std::vector<double> fin;
+  true_residual(fin);
+  HPSB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+  HPSB_CUDA(cudaEventSynchronize(ctx->ev[3]));
+  float ms = 0;
+  HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+  bool all = true;
+  for (int b = 0; b < R; ++b) {
+    reps[b].iterations = total[b];
+    reps[b].final_residual = fin[b];
+    reps[b].converged = fin[b] <= cfg.tol;
+    reps[b].seconds = ms * 1e-3;
+    all = all && reps[b].converged;
+  }
+  return all ? HPSB_OK : HPSB_NO_CONVERGENCE;
+}
+}  // namespace
 
 }  // namespace hpsb

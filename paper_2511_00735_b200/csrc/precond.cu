@@ -33,6 +33,7 @@
 #include "vcycle_device.cuh"
 #include "vcycle_small.hpp"
 #include "zgemm.hpp"
+#include "zgemv_batch.hpp"
 
 namespace hpsb {
 
@@ -72,6 +73,16 @@ struct Precond {
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
   double bytes_small = 0;
+  // ---- multi-RHS (built on first use, capacity kBatchMaxRhs)
+  // stage_items[dir][l][k]: items of every merge of level l in stage k
+  std::vector<std::vector<std::vector<VItem>>> stage_items[2];
+  size_t tmp_total = 0;
+  bool batch_ready = false;
+  DevBuf<double2> rB, tmpB, VB, cvB, cwB, HmB, gvB, rsB;
+  DevBuf<double> rcB, stateB;
+  std::vector<BPhase> bdown, bup;
+  BPhase bcoarse;              // coarse matvec of the batched gmres_fixed_steps
+  std::vector<BPhase> bexact;  // exact coarse: one phase per column chunk
   void run_steps(bool down, bool global, double2* z) const {
     const int last_local = h->sk->el->part.last_local;
     for (const Step& st : down ? down_steps : up_steps) {
@@ -526,12 +537,19 @@ __global__ void mask_faces_kernel(double2* z, const int* __restrict__ keep, int 
 }
 
 // state: [0] bnorm, [1] done, [2] jused, [3] zero-rhs
+// Multi-RHS: CTA b works on right-hand side b (rd / outd stride ldr, the
+// Krylov state of each RHS packed behind the previous one's).
 __global__ void __launch_bounds__(kCoarseThreads) coarse_init_kernel(const double2* rd, int64_t n,
                                                                      double2* V, double2* cv,
                                                                      double2* gv, int ci,
-                                                                     double* state) {
+                                                                     double* state, int64_t ldr) {
   pdl_trigger();
   pdl_wait();
+  {
+    const int b = blockIdx.x;
+    rd += b * ldr, V += static_cast<int64_t>(b) * (ci + 1) * n, cv += b * n;
+    gv += b * (ci + 1), state += b * 4;
+  }
   __shared__ double sh[33];
   double s = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += cabs2(rd[i]);
@@ -580,9 +598,16 @@ __device__ void apply_givens(double c, double2 s, double2& a, double2& b) {
 // KrylovConfig's default, krylov.cpp:194-201).  Hm is (ci+1) x ci col-major.
 __global__ void __launch_bounds__(kCoarseThreads) coarse_step_kernel(
     int j, int64_t n, int ci, double2* V, double2* cv, double2* cw, double2* Hm, double2* gv,
-    double* rc, double2* rs, double* state) {
+    double* rc, double2* rs, double* state, int64_t ldr) {
   pdl_trigger();
   pdl_wait();
+  {
+    const int b = blockIdx.x;
+    (void)ldr;
+    V += static_cast<int64_t>(b) * (ci + 1) * n, cv += b * n, cw += b * n;
+    Hm += static_cast<int64_t>(b) * (ci + 1) * ci, gv += b * (ci + 1), rc += b * ci, rs += b * ci;
+    state += b * 4;
+  }
   __shared__ double sh[33];
   if (state[1] != 0.0) return;
   const int ldh = ci + 1;
@@ -639,9 +664,14 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_finish_kernel(int64_t n
                                                                        const double2* Hm,
                                                                        const double2* gv,
                                                                        const double* state,
-                                                                       double2* outd) {
+                                                                       double2* outd, int64_t ldr) {
   pdl_trigger();
   pdl_wait();
+  {
+    const int b = blockIdx.x;
+    V += static_cast<int64_t>(b) * (ci + 1) * n, Hm += static_cast<int64_t>(b) * (ci + 1) * ci;
+    gv += b * (ci + 1), state += b * 4, outd += b * ldr;
+  }
   __shared__ double2 y[64];
   const int ju = static_cast<int>(state[2]);
   const int ldh = ci + 1;
@@ -938,6 +968,20 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->keep_face.upload(keep, ctx->stream);
   }
 
+  // stage lists for the multi-RHS phases (single GPU)
+  p->tmp_total = std::max<size_t>(tmp_total, 1);
+  for (int dir = 0; dir < 2; ++dir) {
+    p->stage_items[dir].assign(cfg.depth, {});
+    for (int l = 1; l < cfg.depth; ++l) {
+      auto pm = level_stages(l, dir == 0);
+      auto& lv = p->stage_items[dir][l];
+      lv.assign(4, {});
+      for (auto& st : pm)
+        for (int k = 0; k < 4; ++k)
+          for (auto& it : st[k]) lv[k].push_back(it);
+    }
+  }
+
   // ---- coarse level: M_depth = I + sum_boxes scatter(T_box) on the tail
   const LevelOps& C = *h->levels[cfg.depth - 1];
   p->off_d = static_cast<int64_t>(C.first_face) * sk->bs;
@@ -1134,20 +1178,20 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   KernelScope ks(ctx, "coarse_gmres", 32.0 * p->dim_d, 0.0);
   launch_k(ctx, coarse_init_kernel, dim3(1), dim3(kCoarseThreads), 0, 1,
            static_cast<const double2*>(p->r.p + p->off_d), p->dim_d, p->V.p, p->cv.p, p->gv.p, ci,
-           p->state.p);
+           p->state.p, int64_t(0));
   }
   for (int j = 0; j < ci; ++j) {
     p->coarse_mv.run(ctx);
     KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (2 * j + 4), 0.0);
     launch_k(ctx, coarse_step_kernel, dim3(1), dim3(kCoarseThreads), 0, 1, j, p->dim_d, ci, p->V.p,
-             p->cv.p, p->cw.p, p->Hm.p, p->gv.p, p->rc.p, p->rs.p, p->state.p);
+             p->cv.p, p->cw.p, p->Hm.p, p->gv.p, p->rc.p, p->rs.p, p->state.p, int64_t(0));
   }
   {
   KernelScope ks(ctx, "coarse_gmres", 16.0 * p->dim_d * (ci + 1), 0.0);
   launch_k(ctx, coarse_finish_kernel, dim3(1), dim3(kCoarseThreads), 0, 1, p->dim_d, ci,
            static_cast<const double2*>(p->V.p), static_cast<const double2*>(p->Hm.p),
            static_cast<const double2*>(p->gv.p), static_cast<const double*>(p->state.p),
-           z_dev + p->off_d);
+           z_dev + p->off_d, int64_t(0));
   }
   }
   p->run_steps(false, true, z_dev);
@@ -1160,6 +1204,102 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
              static_cast<const int*>(p->keep_face.p), bs);
     ctx->comm->allreduce_sum(z_dev, p->dim, ctx);
   }
+}
+
+namespace {
+// Multi-RHS phases from the single-RHS item lists: every vector operand is
+// mapped to its R-column block (r -> rB, tmp -> tmpB, coarse cv / cw -> their
+// blocks); `out` stays as the rebinding marker of the caller's output block.
+void build_batch(Precond* p) {
+  Context* ctx = p->ctx;
+  const int Rm = kBatchMaxRhs;
+  const int64_t dim = p->dim, nd = p->dim_d;
+  const int ci = p->cfg.exact_coarse ? 0 : p->cfg.coarse_iters;
+  p->rB.alloc(static_cast<size_t>(Rm) * dim);
+  p->tmpB.alloc(static_cast<size_t>(Rm) * p->tmp_total);
+  p->VB.alloc(static_cast<size_t>(Rm) * (ci + 1) * nd);
+  p->cvB.alloc(static_cast<size_t>(Rm) * nd);
+  p->cwB.alloc(static_cast<size_t>(Rm) * nd);
+  p->HmB.alloc(static_cast<size_t>(Rm) * (ci + 1) * std::max(ci, 1));
+  p->gvB.alloc(static_cast<size_t>(Rm) * (ci + 1));
+  p->rsB.alloc(static_cast<size_t>(Rm) * std::max(ci, 1));
+  p->rcB.alloc(static_cast<size_t>(Rm) * std::max(ci, 1));
+  p->stateB.alloc(static_cast<size_t>(Rm) * 4);
+  auto map = [&](const double2* ptr, int& ld) -> const double2* {
+    if (!ptr) return nullptr;
+    if (ptr >= p->r.p && ptr < p->r.p + dim) return ld = static_cast<int>(dim), p->rB.p + (ptr - p->r.p);
+    if (ptr >= p->out.p && ptr < p->out.p + dim) return ld = static_cast<int>(dim), ptr;
+    if (ptr >= p->tmp.p && ptr < p->tmp.p + p->tmp_total)
+      return ld = static_cast<int>(p->tmp_total), p->tmpB.p + (ptr - p->tmp.p);
+    if (ptr >= p->cv.p && ptr < p->cv.p + nd) return ld = static_cast<int>(nd), p->cvB.p + (ptr - p->cv.p);
+    if (ptr >= p->cw.p && ptr < p->cw.p + nd) return ld = static_cast<int>(nd), p->cwB.p + (ptr - p->cw.p);
+    throw std::logic_error("batch: unmapped vector operand");
+  };
+  auto conv = [&](const VItem& it) {
+    BDesc d{};
+    d.A = it.A, d.lda = it.lda, d.M = it.rows, d.K = it.A ? it.cols : 0;
+    d.B = d.K ? map(it.x, d.ldb) : nullptr, d.bidx = d.K ? it.xi : nullptr;
+    d.C = const_cast<double2*>(map(it.y, d.ldc)), d.cidx = it.yi;
+    d.Z = it.gamma != 0.0 ? map(it.z, d.ldz) : nullptr, d.zidx = it.gamma != 0.0 ? it.zi : nullptr;
+    d.alpha = it.alpha, d.beta = it.beta, d.gamma = it.gamma;
+    return d;
+  };
+  auto phase_of = [&](const std::vector<VItem>& items) {
+    BPhase ph;
+    for (const VItem& it : items) ph.add(conv(it));
+    ph.finalize(ctx->stream);
+    return ph;
+  };
+  for (int l = 1; l < p->cfg.depth; ++l)
+    for (int k = 0; k < 4; ++k) p->bdown.push_back(phase_of(p->stage_items[0][l][k]));
+  for (int l = p->cfg.depth - 1; l >= 1; --l)
+    for (int k = 0; k < 4; ++k) p->bup.push_back(phase_of(p->stage_items[1][l][k]));
+  if (p->cfg.exact_coarse) {
+    for (const VPhase& vp : p->exact_mv.phases) {
+      std::vector<VItem> items;
+      for (int u = vp.unit_begin; u < vp.unit_begin + vp.unit_count; ++u)
+        for (int it = p->exact_mv.units[u].first;
+             it < p->exact_mv.units[u].first + p->exact_mv.units[u].count; ++it)
+          items.push_back(p->exact_mv.items[it]);
+      p->bexact.push_back(phase_of(items));
+    }
+  } else {
+    p->bcoarse = phase_of(p->coarse_mv.items);
+  }
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  p->batch_ready = true;
+}
+}  // namespace
+
+void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
+  Context* ctx = p->ctx;
+  if (ctx->world() > 1) throw InvalidArgument("precond_apply: multi-RHS is single-GPU");
+  if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("precond_apply: 1 <= nrhs <= 32");
+  if (!p->batch_ready) build_batch(p);
+  const int64_t dim = p->dim, nd = p->dim_d;
+  HPSB_CUDA(cudaMemcpyAsync(p->rB.p, v, sizeof(double2) * R * dim, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+  BBind bind;
+  bind.from[0] = p->out.p, bind.to[0] = z;
+  for (const BPhase& ph : p->bdown) ph.run(ctx, R, "vcycle_down_batch", bind);
+  if (p->cfg.exact_coarse) {
+    for (const BPhase& ph : p->bexact) ph.run(ctx, R, "coarse_exact_batch", bind);
+  } else {
+    const int ci = p->cfg.coarse_iters;
+    launch_k(ctx, coarse_init_kernel, dim3(R), dim3(kCoarseThreads), 0, 1,
+             static_cast<const double2*>(p->rB.p + p->off_d), nd, p->VB.p, p->cvB.p, p->gvB.p, ci,
+             p->stateB.p, dim);
+    for (int j = 0; j < ci; ++j) {
+      p->bcoarse.run(ctx, R, "coarse_matvec_batch");
+      launch_k(ctx, coarse_step_kernel, dim3(R), dim3(kCoarseThreads), 0, 1, j, nd, ci, p->VB.p,
+               p->cvB.p, p->cwB.p, p->HmB.p, p->gvB.p, p->rcB.p, p->rsB.p, p->stateB.p, dim);
+    }
+    launch_k(ctx, coarse_finish_kernel, dim3(R), dim3(kCoarseThreads), 0, 1, nd, ci,
+             static_cast<const double2*>(p->VB.p), static_cast<const double2*>(p->HmB.p),
+             static_cast<const double2*>(p->gvB.p), static_cast<const double*>(p->stateB.p),
+             z + p->off_d, dim);
+  }
+  for (const BPhase& ph : p->bup) ph.run(ctx, R, "vcycle_up_batch", bind);
 }
 
 int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }

@@ -12,6 +12,7 @@
 
 #include "device.cuh"
 #include "internal.hpp"
+#include "zgemv_batch.hpp"
 
 namespace hpsb {
 
@@ -117,6 +118,32 @@ void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev) {
   sk->apply_plan.run(ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
   // Every skeleton row is produced by exactly one rank's element: sum.
   if (sharded) ctx->comm->allreduce_sum(y_dev, sk->dim, ctx);
+}
+
+void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int R) {
+  Context* ctx = sk->ctx;
+  if (ctx->world() > 1) throw InvalidArgument("skeleton_apply: multi-RHS is single-GPU");
+  auto* self = const_cast<Skeleton*>(sk);
+  if (!self->batch) {
+    // Y = X + sum_e scatter(T_e gather(X)): the matvec plan's items as a
+    // multi-RHS GEMM phase on the x_buf / y_buf markers.
+    auto ph = std::make_shared<BPhase>();
+    for (const VItem& it : sk->apply_plan.items) {
+      BDesc d{};
+      d.A = it.A, d.lda = it.lda, d.M = it.rows, d.K = it.cols;
+      d.B = it.x, d.bidx = it.xi, d.ldb = static_cast<int>(sk->dim);
+      d.C = it.y, d.cidx = it.yi, d.ldc = static_cast<int>(sk->dim);
+      d.Z = it.z, d.zidx = it.zi, d.ldz = static_cast<int>(sk->dim);
+      d.alpha = it.alpha, d.beta = it.beta, d.gamma = it.gamma;
+      ph->add(d);
+    }
+    ph->finalize(ctx->stream);
+    self->batch = ph;
+  }
+  BBind bind;
+  bind.from[0] = sk->x_buf.p, bind.to[0] = const_cast<double2*>(x);
+  bind.from[1] = sk->y_buf.p, bind.to[1] = y;
+  static_cast<const BPhase*>(sk->batch.get())->run(ctx, R, "skeleton_matvec_batch", bind);
 }
 
 }  // namespace hpsb

@@ -29,8 +29,12 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ const double2* bind_ptr(const double2* p, const BBind& b) {
+  return !p ? p : p == b.from[0] ? b.to[0] : p == b.from[1] ? b.to[1] : p;
+}
+
 __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __restrict__ descs,
-                                                              int ndesc, int R) {
+                                                              int ndesc, int R, BBind bind) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + STAGES * A_STAGE;
@@ -42,7 +46,10 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
     if (descs[mid].tile_begin <= tile) lo = mid;
     else hi = mid - 1;
   }
-  const BDesc d = descs[lo];
+  BDesc d = descs[lo];
+  d.B = bind_ptr(d.B, bind);
+  d.C = const_cast<double2*>(bind_ptr(d.C, bind));
+  d.Z = bind_ptr(d.Z, bind);
   const int m0 = (tile - d.tile_begin) * BM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
@@ -160,13 +167,13 @@ void BPhase::add(const BDesc& x0) {
   descs.push_back(x);
 }
 
-void BPhase::run(Context* ctx, int R, const char* label) const {
+void BPhase::run(Context* ctx, int R, const char* label, BBind bind) const {
   if (descs.empty()) return;
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("batch: 1 <= nrhs <= 32");
   allow_smem<zgemv_batch_kernel>(BSMEM);
   KernelScope ks(ctx, label, bytes, flops * R);
   launch_k(ctx, zgemv_batch_kernel, dim3(total_tiles), dim3(THREADS), BSMEM, 1,
-           static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R);
+           static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R, bind);
 }
 
 }  // namespace hpsb

@@ -27,6 +27,13 @@ struct BDesc {
   int tiles_m, tile_begin, pad;
 };
 
+// Run-time rebinding: descriptors built on `from` address `to` instead
+// (the caller's output block), so no copies are needed around a run.
+struct BBind {
+  const double2* from[2] = {nullptr, nullptr};
+  double2* to[2] = {nullptr, nullptr};
+};
+
 // One launch: every descriptor's row tiles, R <= 32 right-hand sides.
 struct BPhase {
   std::vector<BDesc> descs;
@@ -35,7 +42,7 @@ struct BPhase {
   DevBuf<BDesc> d;
   void add(const BDesc& x);
   void finalize(cudaStream_t s) { d.upload(descs, s); }
-  void run(Context* ctx, int R, const char* label) const;
+  void run(Context* ctx, int R, const char* label, BBind bind = {}) const;
 };
 
 constexpr int kBatchMaxRhs = 32;

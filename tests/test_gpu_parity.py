@@ -297,3 +297,76 @@ def test_exact_coarse_partial_depth(hps, oracle, ctx, name):
     xo, repo = c.S.solve(c.S.rhs(), True, restart=50, tol=1e-10)
     assert rep["converged"] and abs(rep["iterations"] - repo["iterations"]) <= 1, (rep, repo)
     assert relf(x, xo) < TOL_SOL
+
+
+def _dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.float64)).cuda()
+
+
+def test_multi_rhs_operators(hps, oracle, ctx):
+    # Multi-RHS interface matvec and MG apply (one pass over the maps for R
+    # vectors, DMMA GEMMs) against the single-RHS path column by column.
+    import torch
+    c = case(hps, oracle, ctx, "cfg2_n8")
+    h = hps.build_hierarchy(c.sk, factor_coarse=False)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    R = 5
+    rng = np.random.default_rng(21)
+    X = rng.standard_normal((R, c.sk.dim)) + 1j * rng.standard_normal((R, c.sk.dim))
+    xd = _dev(torch, X)
+    yd = torch.empty_like(xd)
+    hps._check(hps._lib.hpsb_skeleton_apply_batch_dev(c.sk._h, xd.data_ptr(), yd.data_ptr(), R))
+    ctx.synchronize()  # the library stream is not torch's
+    Y = yd.cpu().numpy().view(np.complex128).reshape(R, -1)
+    for b in range(R):
+        assert relf(Y[b], c.sk.apply(X[b])) < 1e-13
+    zd = torch.empty_like(xd)
+    hps._check(hps._lib.hpsb_precond_apply_batch_dev(pc._h, xd.data_ptr(), zd.data_ptr(), R))
+    ctx.synchronize()
+    Z = zd.cpu().numpy().view(np.complex128).reshape(R, -1)
+    for b in range(R):
+        assert relf(Z[b], pc.apply(X[b])) < TOL_OP
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_multi_rhs_precond_exact_and_partial(hps, oracle, ctx, exact):
+    import torch
+    c = case(hps, oracle, ctx, "bump_n4_N4")
+    h = hps.build_hierarchy(c.sk, factor_coarse=False)
+    pc = hps.build_preconditioner(h, coarse_iters=3, exact_coarse=exact)
+    R = 3
+    rng = np.random.default_rng(22)
+    X = rng.standard_normal((R, c.sk.dim)) + 1j * rng.standard_normal((R, c.sk.dim))
+    xd = _dev(torch, X)
+    zd = torch.empty_like(xd)
+    hps._check(hps._lib.hpsb_precond_apply_batch_dev(pc._h, xd.data_ptr(), zd.data_ptr(), R))
+    ctx.synchronize()
+    Z = zd.cpu().numpy().view(np.complex128).reshape(R, -1)
+    for b in range(R):
+        assert relf(Z[b], pc.apply(X[b])) < TOL_OP
+
+
+def test_fgmres_multi_rhs_cfg4_planewaves(hps, oracle, ctx):
+    # cfg4's setting (32 plane-wave right-hand sides, s = 0) on an 8 x 8 mesh:
+    # R right-hand sides in lockstep, each against its own oracle solve.
+    p = hps.problem(2, 4, n=8)
+    el = hps.build_elements(ctx, p)
+    sk = hps.assemble_skeleton(el, p)
+    h = hps.build_hierarchy(sk, factor_coarse=False)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    R = 4
+    rhs = np.stack([sk.rhs(b) for b in range(R)])
+    X, reps = hps.fgmres_batch(sk, rhs, pc, restart=100, tol=1e-10)
+    for b in range(R):
+        S = oracle.Session(p.n, p.order, p.kappa, p.eta, p.coeff, p.source, p.tside[b])
+        assert relf(rhs[b], S.rhs()) < TOL_OP
+        S.build_hierarchy(0, False)
+        S.precond(depth=h.depth, gamma=1, coarse_iters=4)
+        xo, repo = S.solve(S.rhs(), True, restart=100, tol=1e-10)
+        assert reps[b]["converged"] and repo["converged"]
+        assert abs(reps[b]["iterations"] - repo["iterations"]) <= max(1, repo["iterations"] // 4)
+        assert relf(X[b], xo) < 1e-8
+        # and exactly the single-RHS GPU solve's iteration count
+        xs, reps1 = hps.fgmres(sk, rhs[b], pc, restart=100, tol=1e-10)
+        assert abs(reps1["iterations"] - reps[b]["iterations"]) <= 1
+        assert relf(X[b], xs) < TOL_SOL
