@@ -72,6 +72,7 @@ struct Precond {
   std::vector<Step> down_steps, up_steps;
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
+  std::vector<int> small_level_of;  // level -> smalls index (-1: none)
   double bytes_small = 0;
   // ---- multi-RHS (built on first use, capacity kBatchMaxRhs)
   // stage_items[dir][l][k]: items of every merge of level l in stage k
@@ -865,6 +866,9 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       const size_t need = small_merge_smem(mr.s, mr.p1, mr.p2);
       if (need > kSmallMergeSmemMax) return -1;
       sl->smem = std::max(sl->smem, need);
+      sl->batch_ops = std::max(sl->batch_ops, small_merge_batch_smem(mr.s, mr.p1, mr.p2, 0));
+      sl->batch_vec = std::max(sl->batch_vec, small_merge_batch_smem(mr.s, mr.p1, mr.p2, 1) -
+                                                  small_merge_batch_smem(mr.s, mr.p1, mr.p2, 0));
       SmallMerge m{};
       m.T1 = L.tperm.p + c1.t_off, m.T2 = L.tperm.p + c2.t_off, m.W = L.w.p + mr.w_off;
       m.in1s = ix + mr.in1_sep, m.in2s = ix + mr.in2_sep, m.in1p = ix + mr.in1_per;
@@ -930,6 +934,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     small_of[l] = small_level(l);
     if (small_of[l] < 0) cluster_of[l] = cluster_level(l);
   }
+  p->small_level_of = small_of;
   auto add_step = [&](int l, bool downward) {
     Precond::Step st;
     st.level = l;
@@ -1250,10 +1255,17 @@ void build_batch(Precond* p) {
     ph.finalize(ctx->stream);
     return ph;
   };
+  const bool lv = std::getenv("HPSB_PROFILE_LEVELS") != nullptr;
   for (int l = 1; l < p->cfg.depth; ++l)
-    for (int k = 0; k < 4; ++k) p->bdown.push_back(phase_of(p->stage_items[0][l][k]));
+    for (int k = 0; k < 4; ++k) {
+      p->bdown.push_back(phase_of(p->stage_items[0][l][k]));
+      if (lv) p->bdown.back().label = "vcycle_down_batch_L" + std::to_string(l);
+    }
   for (int l = p->cfg.depth - 1; l >= 1; --l)
-    for (int k = 0; k < 4; ++k) p->bup.push_back(phase_of(p->stage_items[1][l][k]));
+    for (int k = 0; k < 4; ++k) {
+      p->bup.push_back(phase_of(p->stage_items[1][l][k]));
+      if (lv) p->bup.back().label = "vcycle_up_batch_L" + std::to_string(l);
+    }
   if (p->cfg.exact_coarse) {
     for (const VPhase& vp : p->exact_mv.phases) {
       std::vector<VItem> items;
@@ -1281,7 +1293,21 @@ void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
                             ctx->stream));
   BBind bind;
   bind.from[0] = p->out.p, bind.to[0] = z;
-  for (const BPhase& ph : p->bdown) ph.run(ctx, R, "vcycle_down_batch", bind);
+  // levels of small merges: the fused per-merge chain when its R-wide
+  // vectors fit in shared memory, else the level's four GEMM phases
+  auto small_fits = [&](int l) {
+    const int si = p->small_level_of[l];
+    return si >= 0 && p->smalls[si]->batch_smem(R) <= (200u << 10) &&
+           !std::getenv("HPSB_NO_SMALL_BATCH");
+  };
+  const int depth = p->cfg.depth;
+  for (int l = 1; l < depth; ++l) {
+    if (small_fits(l)) {
+      p->smalls[p->small_level_of[l]]->run_batch(ctx, true, p->rB.p, z, R, dim);
+      continue;
+    }
+    for (int k = 0; k < 4; ++k) p->bdown[(l - 1) * 4 + k].run(ctx, R, "vcycle_down_batch", bind);
+  }
   if (p->cfg.exact_coarse) {
     for (const BPhase& ph : p->bexact) ph.run(ctx, R, "coarse_exact_batch", bind);
   } else {
@@ -1299,7 +1325,13 @@ void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
              static_cast<const double2*>(p->gvB.p), static_cast<const double*>(p->stateB.p),
              z + p->off_d, dim);
   }
-  for (const BPhase& ph : p->bup) ph.run(ctx, R, "vcycle_up_batch", bind);
+  for (int l = depth - 1; l >= 1; --l) {
+    if (small_fits(l)) {
+      p->smalls[p->small_level_of[l]]->run_batch(ctx, false, p->rB.p, z, R, dim);
+      continue;
+    }
+    for (int k = 0; k < 4; ++k) p->bup[(depth - 1 - l) * 4 + k].run(ctx, R, "vcycle_up_batch", bind);
+  }
 }
 
 int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }

@@ -125,7 +125,132 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
     }
   }
 }
+// Multi-RHS variant: the same fused chain for R right-hand sides (vectors
+// with RHS stride ld); every GEMV becomes a small GEMM on shared memory,
+// one (row, rhs) output per thread pass.  Block-wide.
+template <class F>
+__device__ __forceinline__ void smem_gemm_r(const double2* A, int lda, int rows, int K,
+                                            const double2* X, int ldx, int R, F&& emit) {
+  for (int idx = threadIdx.x; idx < rows * R; idx += kThreads) {
+    const int r = idx % rows, b = idx / rows;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < K; ++k) acc = cfma(A[r + k * lda], X[k + b * ldx], acc);
+    emit(r, b, acc);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
+    const SmallMerge* __restrict__ ms, int down, double2* r, double2* out, int R, int64_t ld) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const SmallMerge M = ms[blockIdx.x];
+  const int tid = threadIdx.x, s = M.s, p1 = M.p1, p2 = M.p2, P1 = M.P1, P2 = M.P2;
+  double2* A1 = reinterpret_cast<double2*>(smem_raw);
+  double2* A2 = A1 + static_cast<size_t>(P1) * s;
+  double2* Ws = A2 + static_cast<size_t>(P2) * s;
+  double2* v1 = Ws + static_cast<size_t>(s) * s;  // s x R each
+  double2* v2 = v1 + static_cast<size_t>(s) * R;
+  double2* t = v2 + static_cast<size_t>(s) * R;
+  double2* w1 = t + static_cast<size_t>(s) * R;
+  double2* u1 = w1 + static_cast<size_t>(s) * R;  // p1 x R
+  double2* u2 = u1 + static_cast<size_t>(p1) * R;  // p2 x R
+  pdl_trigger();
+  if (down) {
+    const double2* g1 = M.T1 + static_cast<size_t>(p1) * P1;
+    const double2* g2 = M.T2 + static_cast<size_t>(p2) * P2;
+    for (int k = tid; k < P1 * s; k += kThreads) cp_async16(A1 + k, g1 + k);
+    for (int k = tid; k < P2 * s; k += kThreads) cp_async16(A2 + k, g2 + k);
+  } else {
+    for (int k = tid; k < s * P1; k += kThreads)
+      cp_async16(A1 + k, M.T1 + p1 + (k % s) + static_cast<size_t>(k / s) * P1);
+    for (int k = tid; k < s * P2; k += kThreads)
+      cp_async16(A2 + k, M.T2 + p2 + (k % s) + static_cast<size_t>(k / s) * P2);
+  }
+  for (int k = tid; k < s * s; k += kThreads) cp_async16(Ws + k, M.W + k);
+  cp_async_commit();
+  pdl_wait();
+  if (down) {
+    for (int k = tid; k < s * R; k += kThreads) {
+      const int i = k % s, b = k / s;
+      v1[k] = __ldcg(r + b * ld + M.in1s[i]);
+      v2[k] = __ldcg(r + b * ld + M.in2s[i]);
+    }
+  } else {
+    for (int k = tid; k < p1 * R; k += kThreads)
+      u1[k] = __ldcg(out + (k / p1) * ld + M.in1p[k % p1]);
+    for (int k = tid; k < p2 * R; k += kThreads)
+      u2[k] = __ldcg(out + (k / p2) * ld + M.in2p[k % p2]);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (down) {
+    const double2 *T1ps = A1, *T1ss = A1 + p1, *T2ps = A2, *T2ss = A2 + p2;
+    // t = v1 - T2_ss v2
+    smem_gemm_r(T2ss, P2, s, s, v2, s, R, [&](int i, int b, double2 y) {
+      t[i + b * s] = csub(v1[i + b * s], y);
+    });
+    __syncthreads();
+    // x1 = W t
+    smem_gemm_r(Ws, s, s, s, t, s, R, [&](int i, int b, double2 y) {
+      w1[i + b * s] = y;
+      __stcg(out + b * ld + M.in1s[i], y);
+    });
+    __syncthreads();
+    // x2 = v2 - T1_ss x1  (into t)
+    smem_gemm_r(T1ss, P1, s, s, w1, s, R, [&](int i, int b, double2 y) {
+      const double2 x2 = csub(v2[i + b * s], y);
+      t[i + b * s] = x2;
+      __stcg(out + b * ld + M.in2s[i], x2);
+    });
+    // r[out1_p] -= T1_ps x1 (independent of the x2 rows above)
+    smem_gemm_r(T1ps, P1, p1, s, w1, s, R, [&](int i, int b, double2 y) {
+      double2* q = r + b * ld + M.out1p[i];
+      __stcg(q, csub(__ldcg(q), y));
+    });
+    __syncthreads();
+    smem_gemm_r(T2ps, P2, p2, s, t, s, R, [&](int i, int b, double2 y) {
+      double2* q = r + b * ld + M.out2p[i];
+      __stcg(q, csub(__ldcg(q), y));
+    });
+  } else {
+    const double2 *T1sp = A1, *T1ss = A1 + static_cast<size_t>(p1) * s, *T2sp = A2,
+                  *T2ss = A2 + static_cast<size_t>(p2) * s;
+    // b1 = T2_sp u2 (v1), b2 = T1_sp u1 (v2)
+    smem_gemm_r(T2sp, s, s, p2, u2, p2, R, [&](int i, int b, double2 y) { v1[i + b * s] = y; });
+    smem_gemm_r(T1sp, s, s, p1, u1, p1, R, [&](int i, int b, double2 y) { v2[i + b * s] = y; });
+    __syncthreads();
+    // t = b1 - T2_ss b2
+    smem_gemm_r(T2ss, s, s, s, v2, s, R, [&](int i, int b, double2 y) {
+      t[i + b * s] = csub(v1[i + b * s], y);
+    });
+    __syncthreads();
+    // y1 = W t
+    smem_gemm_r(Ws, s, s, s, t, s, R, [&](int i, int b, double2 y) { w1[i + b * s] = y; });
+    __syncthreads();
+    // out[s2] += T1_ss y1 - b2,  out[s1] -= y1
+    smem_gemm_r(T1ss, s, s, s, w1, s, R, [&](int i, int b, double2 y) {
+      double2* q2 = out + b * ld + M.in2s[i];
+      __stcg(q2, cadd(__ldcg(q2), csub(y, v2[i + b * s])));
+      double2* q1 = out + b * ld + M.in1s[i];
+      __stcg(q1, csub(__ldcg(q1), w1[i + b * s]));
+    });
+  }
+}
 }  // namespace
+
+size_t small_merge_batch_smem(int s, int p1, int p2, int R) {
+  const size_t P1 = p1 + s, P2 = p2 + s;
+  return sizeof(double2) * ((P1 + P2 + s) * s + static_cast<size_t>(R) * (4 * s + p1 + p2));
+}
+
+void SmallLevel::run_batch(Context* ctx, bool down, double2* r, double2* out, int R, int64_t ld) const {
+  if (!count) return;
+  const size_t smem = batch_smem(R);
+  allow_smem<merge_small_batch_kernel>(smem);
+  KernelScope ks(ctx, label.empty() ? (down ? "vcycle_down_batch" : "vcycle_up_batch") : label.c_str(),
+                 down ? bytes_down : bytes_up, 0.0);
+  launch_k(ctx, merge_small_batch_kernel, dim3(count), dim3(kThreads), smem, 1,
+           static_cast<const SmallMerge*>(d.p), down ? 1 : 0, r, out, R, ld);
+}
 
 size_t small_merge_smem(int s, int p1, int p2) {
   const size_t P1 = p1 + s, P2 = p2 + s;

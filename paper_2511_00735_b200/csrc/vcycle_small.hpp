@@ -16,13 +16,18 @@ struct SmallMerge {
 // Shared memory one merge needs (operators + vectors).
 size_t small_merge_smem(int s, int p1, int p2);
 
+size_t small_merge_batch_smem(int s, int p1, int p2, int R);
 struct SmallLevel {
   int level = 0, count = 0;
   size_t smem = 0;
+  size_t batch_ops = 0, batch_vec = 0;  // multi-RHS smem: operators + per-RHS vectors
+  size_t batch_smem(int R) const { return batch_ops + static_cast<size_t>(R) * batch_vec; }
   double bytes_down = 0, bytes_up = 0;
   std::string label;
   DevBuf<SmallMerge> d;
   void run(Context* ctx, bool down, double2* r, double2* out) const;
+  // R right-hand sides, vectors with RHS stride ld
+  void run_batch(Context* ctx, bool down, double2* r, double2* out, int R, int64_t ld) const;
 };
 
 // One thread-block cluster of `csize` CTAs per merge (csrc/vcycle_cluster.cu).

@@ -12,11 +12,14 @@
 namespace hpsb {
 
 namespace {
-constexpr int BM = 64, BN = 32, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int BM = 64, BK = 16, STAGES = 3, THREADS = 256;
 constexpr int SA = BM + 2;  // complex stride of an A k-row in smem
 constexpr int SB = BK + 4;  // complex stride of a B column in smem
-constexpr int A_STAGE = BK * SA, B_STAGE = BN * SB;
-constexpr size_t BSMEM = sizeof(double2) * STAGES * (A_STAGE + B_STAGE);
+constexpr int A_STAGE = BK * SA;
+template <int BN>
+constexpr size_t bsmem() {
+  return sizeof(double2) * STAGES * (A_STAGE + BN * SB);
+}
 
 __device__ __forceinline__ void cpa16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -33,8 +36,12 @@ __device__ __forceinline__ const double2* bind_ptr(const double2* p, const BBind
   return !p ? p : p == b.from[0] ? b.to[0] : p == b.from[1] ? b.to[1] : p;
 }
 
+// BN = 32 (R > 16): 4 x 2 warps of 16 x 16 outputs; BN = 16: 8 x 1 warps of 8 x 16.
+template <int BN>
 __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __restrict__ descs,
                                                               int ndesc, int R, BBind bind) {
+  constexpr int WN = BN / 16, WM = 8 / WN, I = BM / (8 * WM);
+  constexpr int B_STAGE = BN * SB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + STAGES * A_STAGE;
@@ -52,7 +59,7 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
   d.Z = bind_ptr(d.Z, bind);
   const int m0 = (tile - d.tile_begin) * BM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 3, wn = warp >> 2;  // 4 x 2 warps
+  const int wm = warp % WM, wn = warp / WM;
   const int ktiles = d.A ? (d.K + BK - 1) / BK : 0;
 
   auto load_a = [&](int kt, int st) {
@@ -81,9 +88,9 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
     }
   };
 
-  double cr[2][2][2], ci[2][2][2];
+  double cr[I][2][2], ci[I][2][2];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < I; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
     if (s < ktiles) load_b(s, s);
     asm volatile("cp.async.commit_group;\n" ::);
   }
-  const int arow = wm * 16 + (lane >> 2), kq = lane & 3;
+  const int arow = wm * (8 * I) + (lane >> 2), kq = lane & 3;
   const int bcol = wn * 16 + (lane >> 2);
   for (int kt = 0; kt < ktiles; ++kt) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(STAGES - 2));
@@ -111,13 +118,13 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
     const double2* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double2 a[2], b[2];
+      double2 a[I], b[2];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
+      for (int i = 0; i < I; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
 #pragma unroll
       for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < I; ++i) {
         const double nai = -a[i].y;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -132,8 +139,8 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
   asm volatile("cp.async.wait_group 0;\n" ::);
   // epilogue: C[cidx[m], n] = alpha acc + gamma Z[zidx[m], n] + beta C[cidx[m], n]
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int row = m0 + wm * 16 + i * 8 + (lane >> 2);
+  for (int i = 0; i < I; ++i) {
+    const int row = m0 + wm * (8 * I) + i * 8 + (lane >> 2);
     if (row >= d.M) continue;
     const int crow = d.cidx ? __ldg(d.cidx + row) : row;
     if (crow < 0) continue;
@@ -170,10 +177,16 @@ void BPhase::add(const BDesc& x0) {
 void BPhase::run(Context* ctx, int R, const char* label, BBind bind) const {
   if (descs.empty()) return;
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("batch: 1 <= nrhs <= 32");
-  allow_smem<zgemv_batch_kernel>(BSMEM);
-  KernelScope ks(ctx, label, bytes, flops * R);
-  launch_k(ctx, zgemv_batch_kernel, dim3(total_tiles), dim3(THREADS), BSMEM, 1,
-           static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R, bind);
+  KernelScope ks(ctx, this->label.empty() ? label : this->label.c_str(), bytes, flops * R);
+  if (R <= 16) {
+    allow_smem<zgemv_batch_kernel<16>>(bsmem<16>());
+    launch_k(ctx, zgemv_batch_kernel<16>, dim3(total_tiles), dim3(THREADS), bsmem<16>(), 1,
+             static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R, bind);
+  } else {
+    allow_smem<zgemv_batch_kernel<32>>(bsmem<32>());
+    launch_k(ctx, zgemv_batch_kernel<32>, dim3(total_tiles), dim3(THREADS), bsmem<32>(), 1,
+             static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R, bind);
+  }
 }
 
 }  // namespace hpsb

@@ -8,6 +8,7 @@
 // bytes): the apply is FP64 compute bound and runs on the DMMA tensor cores.
 #pragma once
 
+#include <string>
 #include <vector>
 
 #include "internal.hpp"
@@ -39,6 +40,7 @@ struct BPhase {
   std::vector<BDesc> descs;
   int total_tiles = 0;
   double flops = 0, bytes = 0;
+  std::string label;  // profiling name (overrides run()'s)
   DevBuf<BDesc> d;
   void add(const BDesc& x);
   void finalize(cudaStream_t s) { d.upload(descs, s); }
