@@ -18,6 +18,10 @@
 // launches: one gather (children permuted to [p | s] order), one copy batch,
 // four grouped DMMA GEMMs and one batched inverse.
 #include <algorithm>
+#include <cstdlib>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -63,6 +67,49 @@ struct Trace {
     std::fprintf(stderr, "\n");
   }
 };
+
+// Host threads for the per-group bookkeeping of a level (independent groups;
+// results land in per-group slots, so the outcome does not depend on T).
+int host_threads() {
+  static const int t = [] {
+    const char* e = std::getenv("HPSB_HOST_THREADS");
+    const int hw = static_cast<int>(std::thread::hardware_concurrency());
+    return std::max(1, e ? std::atoi(e) : std::min(16, hw > 0 ? hw : 1));
+  }();
+  return t;
+}
+template <class F>
+void parallel_chunks(int count, int threads, F&& fn) {  // fn(begin, end, thread)
+  threads = std::max(1, std::min(threads, count / 256 + 1));
+  if (threads == 1) {
+    fn(0, count, 0);
+    return;
+  }
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex mu;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        fn(static_cast<int>(static_cast<int64_t>(count) * t / threads),
+           static_cast<int>(static_cast<int64_t>(count) * (t + 1) / threads), t);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
+// Per-group result of the bookkeeping pass.
+struct GroupPlan {
+  bool own = false;
+  int p[2] = {0, 0};
+  std::vector<int> perm[2];           // [perimeter | separator] positions (own groups)
+  std::vector<BoxPos> cpos[2];        // the child's positions in that order
+  std::vector<BoxPos> next_pos;       // merged box perimeter
+};
 }  // namespace
 
 std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
@@ -95,6 +142,9 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     boxes[e].ld = nb;
     elem_box[e] = e;
   }
+  // skeleton index -> position in its box (-1 elsewhere).  The boxes merging
+  // at a level own disjoint slots, so the threads of the parallel pass below
+  // write disjoint entries of one shared table.
   std::vector<int> pos_of(sk->dim, -1);
   DevBuf<double2> tnew_prev;  // previous level's merged maps (children of this level)
   DevBuf<int> d_status(1);
@@ -112,65 +162,82 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     const auto& groups = g.groups[level - 1];
     const int ng = static_cast<int>(groups.size());
 
-    // ---- children in [perimeter | separator] order
+    // ---- children in [perimeter | separator] order (parallel over groups)
     std::vector<std::vector<int>> perms;  // per child, positions into its HostBox
     std::vector<const HostBox*> srcs;
     size_t toff = 0;
     std::vector<std::vector<BoxPos>> next_pos(ng);  // merged box perimeter, every group
     std::vector<int> merge_of(ng, -1);              // group -> this rank's merge index
-    for (int gi = 0; gi < ng; ++gi) {
-      const Face& f0 = g.faces[groups[gi][0]];
-      const bool own = !sharded || level > part.last_local || part.owns_elem(f0.e1);
-      const HostBox* bx[2] = {&boxes[elem_box[f0.e1]], &boxes[elem_box[f0.e2]]};
-      for (int k = 0; k < 2; ++k)
-        for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
-          if (bx[k]->pos[i].in >= 0) pos_of[bx[k]->pos[i].in] = i;
-      const int s = static_cast<int>(groups[gi].size()) * m;
-      std::vector<int> sep[2];
+    std::vector<GroupPlan> plan(ng);
+    parallel_chunks(ng, host_threads(), [&](int g0, int g1, int) {
       std::vector<char> is_sep[2];
-      for (int k = 0; k < 2; ++k) is_sep[k].assign(bx[k]->pos.size(), 0);
-      for (int f : groups[gi]) {
-        if (g.faces[f].e1 == -1) throw std::logic_error("bad face");
-        for (int t = 0; t < m; ++t) {
-          // box 1 holds e1: its incoming datum is slot 1; box 2's is slot 0.
-          const int in1 = f * bs + m + t, in2 = f * bs + t;
-          const int q1 = pos_of[in1], q2 = pos_of[in2];
-          if (q1 < 0 || q2 < 0 || bx[0]->pos[q1].in != in1 || bx[1]->pos[q2].in != in2)
-            throw std::logic_error("build_hierarchy: separator node not on the merging boxes");
-          sep[0].push_back(q1), sep[1].push_back(q2);
-          is_sep[0][q1] = 1, is_sep[1][q2] = 1;
+      std::vector<int> sep[2];
+      for (int gi = g0; gi < g1; ++gi) {
+        GroupPlan& gp = plan[gi];
+        const Face& f0 = g.faces[groups[gi][0]];
+        gp.own = !sharded || level > part.last_local || part.owns_elem(f0.e1);
+        const HostBox* bx[2] = {&boxes[elem_box[f0.e1]], &boxes[elem_box[f0.e2]]};
+        for (int k = 0; k < 2; ++k)
+          for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
+            if (bx[k]->pos[i].in >= 0) pos_of[bx[k]->pos[i].in] = i;
+        for (int k = 0; k < 2; ++k) {
+          is_sep[k].assign(bx[k]->pos.size(), 0);
+          sep[k].clear();
         }
+        for (int f : groups[gi]) {
+          if (g.faces[f].e1 == -1) throw std::logic_error("bad face");
+          for (int t = 0; t < m; ++t) {
+            // box 1 holds e1: its incoming datum is slot 1; box 2's is slot 0.
+            const int in1 = f * bs + m + t, in2 = f * bs + t;
+            const int q1 = pos_of[in1], q2 = pos_of[in2];
+            if (q1 < 0 || q2 < 0 || bx[0]->pos[q1].in != in1 || bx[1]->pos[q2].in != in2)
+              throw std::logic_error("build_hierarchy: separator node not on the merging boxes");
+            sep[0].push_back(q1), sep[1].push_back(q2);
+            is_sep[0][q1] = 1, is_sep[1][q2] = 1;
+          }
+        }
+        for (int k = 0; k < 2; ++k) {
+          std::vector<int>& perm = gp.perm[k];
+          for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
+            if (bx[k]->pos[i].in >= 0 && !is_sep[k][i]) perm.push_back(i);
+          gp.p[k] = static_cast<int>(perm.size());
+          for (int i : perm) gp.next_pos.push_back(bx[k]->pos[i]);
+          if (!gp.own) continue;
+          perm.insert(perm.end(), sep[k].begin(), sep[k].end());
+          gp.cpos[k].reserve(perm.size());
+          for (int i : perm) gp.cpos[k].push_back(bx[k]->pos[i]);
+        }
+        for (int k = 0; k < 2; ++k)
+          for (const auto& q : bx[k]->pos)
+            if (q.in >= 0) pos_of[q.in] = -1;
       }
+    });
+    // serial pass: indices and offsets in group order
+    for (int gi = 0; gi < ng; ++gi) {
+      GroupPlan& gp = plan[gi];
+      next_pos[gi] = std::move(gp.next_pos);
+      if (!gp.own) continue;
+      const Face& f0 = g.faces[groups[gi][0]];
+      const HostBox* bx[2] = {&boxes[elem_box[f0.e1]], &boxes[elem_box[f0.e2]]};
       MergeRec mr;
-      mr.s = s;
+      mr.s = static_cast<int>(groups[gi].size()) * m;
       mr.group = gi;
       for (int k = 0; k < 2; ++k) {
         ChildBox cb;
-        std::vector<int> perm;
-        for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
-          if (bx[k]->pos[i].in >= 0 && !is_sep[k][i]) perm.push_back(i);
-        cb.p = static_cast<int>(perm.size());
-        for (int i : perm) next_pos[gi].push_back(bx[k]->pos[i]);
-        if (!own) continue;
-        perm.insert(perm.end(), sep[k].begin(), sep[k].end());
-        cb.s = s;
-        cb.P = static_cast<int>(perm.size());
-        for (int i : perm) cb.pos.push_back(bx[k]->pos[i]);
+        cb.p = gp.p[k];
+        cb.s = mr.s;
+        cb.P = static_cast<int>(gp.perm[k].size());
+        cb.pos = std::move(gp.cpos[k]);
         cb.t_off = toff;
         toff += static_cast<size_t>(cb.P) * cb.P;
         (k == 0 ? mr.c1 : mr.c2) = static_cast<int>(L->children.size());
         (k == 0 ? mr.p1 : mr.p2) = cb.p;
         L->children.push_back(std::move(cb));
-        perms.push_back(std::move(perm));
+        perms.push_back(std::move(gp.perm[k]));
         srcs.push_back(bx[k]);
       }
-      if (own) {
-        merge_of[gi] = static_cast<int>(L->merges.size());
-        L->merges.push_back(mr);
-      }
-      for (int k = 0; k < 2; ++k)
-        for (const auto& p : bx[k]->pos)
-          if (p.in >= 0) pos_of[p.in] = -1;
+      merge_of[gi] = static_cast<int>(L->merges.size());
+      L->merges.push_back(mr);
     }
     tr.mark("bookkeeping");
     L->tperm.alloc(toff);
@@ -199,21 +266,36 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     }
     tnew_prev.release();
 
-    // ---- V-cycle / export index lists
-    for (auto& mr : L->merges) {
-      const ChildBox& a = L->children[mr.c1];
-      const ChildBox& b = L->children[mr.c2];
-      auto push = [&](const ChildBox& c, int from, int to, bool in) {
-        const size_t off = L->h_idx.size();
-        for (int i = from; i < to; ++i) L->h_idx.push_back(in ? c.pos[i].in : c.pos[i].out);
-        return off;
-      };
-      mr.in1_sep = push(a, a.p, a.P, true);
-      mr.in2_sep = push(b, b.p, b.P, true);
-      mr.in1_per = push(a, 0, a.p, true);
-      mr.out1_per = push(a, 0, a.p, false);
-      mr.in2_per = push(b, 0, b.p, true);
-      mr.out2_per = push(b, 0, b.p, false);
+    // ---- V-cycle / export index lists (offsets serially, fill in parallel)
+    {
+      size_t total_idx = 0;
+      for (auto& mr : L->merges) {
+        const ChildBox& a = L->children[mr.c1];
+        const ChildBox& b = L->children[mr.c2];
+        mr.in1_sep = total_idx, total_idx += a.P - a.p;
+        mr.in2_sep = total_idx, total_idx += b.P - b.p;
+        mr.in1_per = total_idx, total_idx += a.p;
+        mr.out1_per = total_idx, total_idx += a.p;
+        mr.in2_per = total_idx, total_idx += b.p;
+        mr.out2_per = total_idx, total_idx += b.p;
+      }
+      L->h_idx.resize(total_idx);
+      parallel_chunks(static_cast<int>(L->merges.size()), host_threads(), [&](int m0, int m1, int) {
+        for (int gi = m0; gi < m1; ++gi) {
+          const MergeRec& mr = L->merges[gi];
+          const ChildBox& a = L->children[mr.c1];
+          const ChildBox& b = L->children[mr.c2];
+          auto put = [&](const ChildBox& c, int from, int to, bool in, size_t at) {
+            for (int i = from; i < to; ++i) L->h_idx[at++] = in ? c.pos[i].in : c.pos[i].out;
+          };
+          put(a, a.p, a.P, true, mr.in1_sep);
+          put(b, b.p, b.P, true, mr.in2_sep);
+          put(a, 0, a.p, true, mr.in1_per);
+          put(a, 0, a.p, false, mr.out1_per);
+          put(b, 0, b.p, true, mr.in2_per);
+          put(b, 0, b.p, false, mr.out2_per);
+        }
+      });
     }
 
     if (!L->coarse) {
