@@ -308,6 +308,19 @@ def run_b200(args, rank, world, local):
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof["launches"] = d["launches"]
+    # DRAM traffic per launch of the same kernel label from a committed ncu
+    # capture of this config (profiles/r01_traffic.json), when there is one
+    try:
+        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                         "profiles", "r01_traffic.json")))
+        ent = tr.get(f"cfg{args.config}", {})
+        if name in ent:
+            roof["traffic"] = ent[name]
+            roof["traffic_unit"] = "bytes per launch (DRAM read + write, ncu)"
+            roof["traffic_source"] = ent.get("source", "")
+            roof["algorithmic_bytes_per_launch"] = d["bytes"] / max(d["launches"], 1)
+    except (OSError, ValueError):
+        pass
     kernels = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                    "GBps": round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1),
                    "TFLOPs": round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3)}

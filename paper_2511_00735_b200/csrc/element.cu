@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(kThreads) element_kernel(ElemArgs a) {
 
 // ---------------------------------------------------------------- v2
 constexpr int PW = 16;  // panel width
+#ifndef HPSB_TRAIL_BATCH
+#define HPSB_TRAIL_BATCH 4
+#endif
+constexpr int kTrailBatch = HPSB_TRAIL_BATCH;  // trailing-update tiles per warp in flight
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -485,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 2) element_v2_kernel(ElemArgs a) {
       // Each warp takes kBatch tiles at a time: all C fragments are loaded
       // first (kBatch x 2 loads in flight), then the DMMAs, then the stores,
       // so the L2 latency of one tile overlaps the others'.
-      constexpr int kBatch = 4;
+      constexpr int kBatch = kTrailBatch;
       constexpr int kWarps = kThreads / 32;
       for (int base = warp; base < total; base += kWarps * kBatch) {
         double* Cp[kBatch];
