@@ -17,6 +17,9 @@
 // complex samples of s; T[e] nb x nb complex column-major in the boundary
 // order left|right|bottom|top; H[e] nb complex.
 #include <cmath>
+#include <cstring>
+#include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "linalg.cuh"
@@ -64,9 +67,10 @@ __device__ __forceinline__ void keep_interior(const ElemArgs& a, int e, const do
 // L_Gi / L_GG are the impedance rows I_in = deriv + i eta trace
 // (element.cpp:92-125, :137-139); L_Gi has N-1 entries per row.
 __device__ bool iti_epilogue(const ElemArgs& a, int e, const double* Y, int ldy, double2* S,
-                             double2* f, int* perm, double* red_v, int* red_i) {
+                             double2* f, int* perm, double* red_v, int* red_i,
+                             const double* diff_s = nullptr) {
   const int tid = threadIdx.x, m = a.m, nb = a.nb, np = a.order + 1, N = a.order;
-  auto D = [&](int r, int c) { return __ldg(a.diff + r + c * np); };
+  auto D = [&](int r, int c) { return diff_s ? diff_s[r + c * np] : __ldg(a.diff + r + c * np); };
   auto lgi = [&](int b, int k, int& q) {  // entry of row b at interior node k of its line
     const int side = b / m, t = b % m + 1;
     switch (side) {
@@ -608,6 +612,238 @@ __global__ void __launch_bounds__(kThreads, 2) element_v2_kernel(ElemArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- v3
+// Shared-memory-resident variant for small interiors (P <= ~128, i.e. N <= 12):
+// the whole interior block L_ii (column-major, ld P+4 so 8x8 DMMA fragments
+// are bank-conflict free) and the right-hand sides [L_iG | b~] live in shared
+// memory; one 512-thread CTA per SM loops over elements.  Blocked right-
+// looking Cholesky with 16-wide panels (warp 0 factors the diagonal block,
+// rows / columns of the panel solves on all threads), trailing SYRK and
+// right-hand-side updates on DMMA tiles with every operand on-chip, blocked
+// backward solve likewise.  No global-memory round trips inside the
+// factorisation (the v2 kernel's trailing updates go through L2).
+constexpr int kV3Threads = 512;
+__host__ __device__ inline size_t v3_smem_doubles(int P, int nbc, int nb) {
+  const size_t lda = P + 4;
+  const size_t fact = lda * P + lda * nbc;              // A | B
+  const size_t epi = 2 * (static_cast<size_t>(nb) * nb + nb) + lda * nbc;  // S, f over A; B kept
+  return (fact > epi ? fact : epi);
+}
+
+__device__ unsigned long long* g_v3_trace = nullptr;  // development aid (HPSB_V3_TRACE)
+__device__ __forceinline__ void v3_mark(int slot) {
+  if (g_v3_trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicAdd(g_v3_trace + slot, t);
+  }
+}
+__global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  constexpr int kWarps = kV3Threads / 32;
+  const int m = a.m, ni = a.ni, nb = a.nb, np = a.order + 1, N = a.order;
+  const int P = a.npad, nbc = a.nbc, lda = P + 4;
+  double* A = reinterpret_cast<double*>(smem_raw);    // P x P (lower used), ld lda
+  double* B = A + static_cast<size_t>(lda) * P;       // P x nbc, ld lda
+  double2* S = reinterpret_cast<double2*>(smem_raw);  // epilogue overlay on A
+  double2* f = S + nb * nb;
+  __shared__ double mass[64];
+  // the 1-D operators on chip: the large shared-memory carve-out leaves
+  // little L1, and the assembly / epilogue index them in every inner loop
+  __shared__ double stiff_s[64 * 64 / 2], diff_s[64 * 64 / 2];
+  __shared__ int perm[128];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_fail;
+  for (int i = tid; i < np; i += kV3Threads) mass[i] = a.mass[i];
+  for (int i = tid; i < np * np; i += kV3Threads) stiff_s[i] = a.stiff[i], diff_s[i] = a.diff[i];
+  auto K = [&](int r, int c) { return stiff_s[r + c * np]; };
+  const int count = a.elist ? a.nlist : a.ne;
+
+  for (int ii = blockIdx.x; ii < count; ii += gridDim.x) {
+    const int e = a.elist ? a.elist[ii] : ii;
+    __syncthreads();
+    if (tid == 0) s_fail = 0;
+    if (ii == blockIdx.x + gridDim.x) v3_mark(0);
+    const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
+    for (int idx = tid; idx < P * P; idx += kV3Threads) {
+      const int r = idx % P, c = idx / P;
+      if (c > r) continue;
+      double v;
+      if (r >= ni) {
+        v = (r == c) ? 1.0 : 0.0;
+      } else {
+        const int i = r / m + 1, j = r % m + 1, k = c / m + 1, l = c % m + 1;
+        v = 0.0;
+        if (j == l) v += K(i, k) * mass[j];
+        if (i == k) v += mass[i] * K(j, l);
+        if (r == c) v -= __ldg(ce + i * np + j) * mass[i] * mass[j];
+      }
+      A[r + c * lda] = v;
+    }
+    for (int idx = tid; idx < P * nbc; idx += kV3Threads) {
+      const int q = idx % P, b = idx / P;
+      double v = 0.0;
+      if (q < ni && b < nb + 2) {
+        const int i = q / m + 1, j = q % m + 1;
+        if (b < nb) {
+          const int side = b / m, t = b % m + 1;
+          switch (side) {
+            case 0: v = (j == t) ? K(i, 0) * mass[j] : 0.0; break;
+            case 1: v = (j == t) ? K(i, N) * mass[j] : 0.0; break;
+            case 2: v = (i == t) ? mass[i] * K(j, 0) : 0.0; break;
+            default: v = (i == t) ? mass[i] * K(j, N) : 0.0; break;
+          }
+        } else if (a.source) {
+          const double2 sv = a.source[static_cast<size_t>(e) * ni + q];
+          const double w = mass[i] * mass[j];
+          v = (b == nb) ? sv.x * w : sv.y * w;
+        }
+      }
+      B[q + b * lda] = v;
+    }
+    __syncthreads();
+    if (ii == blockIdx.x + gridDim.x) v3_mark(1);
+
+    // ---- factorisation + forward solve
+    for (int k0 = 0; k0 < P; k0 += PW) {
+      if (warp == 0) {  // Cholesky of the 16 x 16 diagonal block
+        for (int j = 0; j < PW; ++j) {
+          double* cj = A + (k0 + j) * lda + k0;
+          if (lane == 0) {
+            const double d = cj[j];
+            if (!(d > 0.0)) s_fail = 1;
+            cj[j] = sqrt(fmax(d, 1e-300));
+          }
+          __syncwarp();
+          const double inv = 1.0 / cj[j];
+          if (lane > j && lane < PW) cj[lane] *= inv;
+          __syncwarp();
+          for (int q = lane; q < PW * PW; q += 32) {
+            const int r = q % PW, c = q / PW;
+            if (c > j && r >= c) A[(k0 + r) + (k0 + c) * lda] -= cj[r] * cj[c];
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (s_fail) break;
+      const int rem = P - k0 - PW;
+      // L21 = A21 L11^{-T} (a row per thread) and the panel rows of B (a column per thread)
+      for (int r = tid; r < rem + nbc; r += kV3Threads) {
+        double x[PW];
+        if (r < rem) {
+          double* row = A + (k0 + PW + r) + k0 * lda;
+#pragma unroll
+          for (int j = 0; j < PW; ++j) x[j] = row[j * lda];
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
+            double sacc = x[j];
+#pragma unroll
+            for (int t = 0; t < j; ++t) sacc -= x[t] * A[(k0 + j) + (k0 + t) * lda];
+            x[j] = sacc / A[(k0 + j) + (k0 + j) * lda];
+            row[j * lda] = x[j];
+          }
+        } else {
+          double* col = B + k0 + (r - rem) * lda;
+#pragma unroll
+          for (int j = 0; j < PW; ++j) x[j] = col[j];
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
+            double sacc = x[j];
+#pragma unroll
+            for (int t = 0; t < j; ++t) sacc -= A[(k0 + j) + (k0 + t) * lda] * x[t];
+            x[j] = sacc / A[(k0 + j) + (k0 + j) * lda];
+            col[j] = x[j];
+          }
+        }
+      }
+      __syncthreads();
+      // trailing: A22 -= L21 L21^T (lower 8x8 tiles), B2 -= L21 B1 (DMMA, all in smem)
+      const int nt = rem / 8, ntri = nt * (nt + 1) / 2, nbt = nbc / 8;
+      const int total = ntri + nt * nbt;
+      for (int tile = warp; tile < total; tile += kWarps) {
+        double* Cp;
+        int arow, brow;  // A-fragment row, B-fragment (col of result) row of L21 / column of B
+        bool isB;
+        if (tile < ntri) {
+          int I = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+          while (I * (I + 1) / 2 > tile) --I;
+          while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+          const int J = tile - I * (I + 1) / 2;
+          Cp = A + (k0 + PW + 8 * I + g) + (k0 + PW + 8 * J + 2 * t4) * lda;
+          arow = k0 + PW + 8 * I + g;
+          brow = k0 + PW + 8 * J + g;
+          isB = false;
+        } else {
+          const int tt = tile - ntri, I = tt % nt, J = tt / nt;
+          Cp = B + (k0 + PW + 8 * I + g) + (8 * J + 2 * t4) * lda;
+          arow = k0 + PW + 8 * I + g;
+          brow = 8 * J + g;  // column of B
+          isB = true;
+        }
+        double c0 = Cp[0], c1 = Cp[lda];
+#pragma unroll
+        for (int kk = 0; kk < PW; kk += 4) {
+          const double av = -A[arow + (k0 + kk + t4) * lda];
+          const double bv = isB ? B[(k0 + kk + t4) + brow * lda] : A[brow + (k0 + kk + t4) * lda];
+          dmma(c0, c1, av, bv);
+        }
+        Cp[0] = c0;
+        Cp[lda] = c1;
+      }
+      __syncthreads();
+    }
+    if (s_fail) {
+      if (tid == 0) a.status[e] = 4;  // indefinite: pivoted-LU fallback
+      continue;
+    }
+    if (ii == blockIdx.x + gridDim.x) v3_mark(2);
+    // ---- backward solve R^T X = Y, from the last panel
+    for (int k0 = P - PW; k0 >= 0; k0 -= PW) {
+      for (int c = tid; c < nbc; c += kV3Threads) {
+        double y[PW];
+        double* col = B + k0 + c * lda;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) y[j] = col[j];
+#pragma unroll
+        for (int j = PW - 1; j >= 0; --j) {
+          double sacc = y[j];
+#pragma unroll
+          for (int t = j + 1; t < PW; ++t) sacc -= A[(k0 + t) + (k0 + j) * lda] * y[t];
+          y[j] = sacc / A[(k0 + j) + (k0 + j) * lda];
+        }
+#pragma unroll
+        for (int j = 0; j < PW; ++j) col[j] = y[j];
+      }
+      __syncthreads();
+      const int nr = k0 / 8, nbt = nbc / 8;
+      for (int tile = warp; tile < nr * nbt; tile += kWarps) {
+        const int I = tile % nr, J = tile / nr;
+        double* Cp = B + (8 * I + g) + (8 * J + 2 * t4) * lda;
+        double c0 = Cp[0], c1 = Cp[lda];
+#pragma unroll
+        for (int kk = 0; kk < PW; kk += 4) {
+          const double av = -A[(k0 + kk + t4) + (8 * I + g) * lda];
+          const double bv = B[(k0 + kk + t4) + (8 * J + g) * lda];
+          dmma(c0, c1, av, bv);
+        }
+        Cp[0] = c0;
+        Cp[lda] = c1;
+      }
+      __syncthreads();
+    }
+    if (ii == blockIdx.x + gridDim.x) v3_mark(3);
+    keep_interior(a, e, B, lda);
+    __syncthreads();
+    if (ii == blockIdx.x + gridDim.x) v3_mark(4);
+    const bool ok = iti_epilogue(a, e, B, lda, S, f, perm, red_v, red_i, diff_s);
+    if (ii == blockIdx.x + gridDim.x) v3_mark(5);
+    if (tid == 0) a.status[e] = ok ? 0 : 2;
+  }
+}
+
 }  // namespace
 
 std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double eta,
@@ -664,6 +900,44 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   a.nbc = (nb + 2 + 7) / 8 * 8;
   if (sharded) a.elist = d_own.p, a.nlist = nwork;
 
+  // v3 (shared-memory resident) when the interior block fits, else v2
+  DevBuf<double> ws;
+  bool done = false;
+  {
+    const size_t smem3 = sizeof(double) * v3_smem_doubles(a.npad, a.nbc, nb);
+    // Opt-in (HPSB_ELEMENT_V3=1): measured slower than v2 at cfg4 (132 vs 113 ms):
+    // with one 512-thread CTA per SM the serial panel / pivot steps leave 15
+    // warps waiting (ncu: 20% of stall samples at the panel barrier).
+    if (smem3 <= 200u * 1024 && np * np <= 2048 && nb <= 128 && std::getenv("HPSB_ELEMENT_V3")) {
+      allow_smem<element_v3_kernel>(smem3);
+      const int slots3 = std::min(nwork, ctx->num_sms);
+      HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+      {
+        const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
+        KernelScope ks(ctx, "element_iti", 8.0 * nwork * (np * np + 2 * ni + 2 * nb * nb + 2 * nb),
+                       fe * nwork);
+        unsigned long long* tr = nullptr;
+        if (std::getenv("HPSB_V3_TRACE")) {
+          HPSB_CUDA(cudaMallocManaged(&tr, 8 * sizeof(unsigned long long)));
+          std::memset(tr, 0, 8 * sizeof(unsigned long long));
+          HPSB_CUDA(cudaMemcpyToSymbol(g_v3_trace, &tr, sizeof(tr)));
+        }
+        element_v3_kernel<<<slots3, kV3Threads, smem3, ctx->stream>>>(a);
+        HPSB_LAUNCHED(ctx);
+        if (tr) {
+          HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+          std::fprintf(stderr, "[v3 trace us] assemble %.1f factor %.1f backward %.1f keep %.1f epilogue %.1f\n",
+                       (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3,
+                       (tr[4] - tr[3]) * 1e-3, (tr[5] - tr[4]) * 1e-3);
+          unsigned long long* z = nullptr;
+          HPSB_CUDA(cudaMemcpyToSymbol(g_v3_trace, &z, sizeof(z)));
+          cudaFree(tr);
+        }
+      }
+      done = true;
+    }
+  }
+  if (!done) {
   // v2 (blocked, DMMA) for every element
   const size_t smem2 = sizeof(double) * (v2_region(a.npad, a.nbc, nb) + np) + sizeof(int) * nb + 16;
   allow_smem<element_v2_kernel>(smem2);
@@ -671,7 +945,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_v2_kernel, kThreads, smem2));
   const int slots2 = std::min(nwork, std::max(1, std::min(per_sm, 3)) * ctx->num_sms);
   const size_t stride2 = static_cast<size_t>(a.npad) * (a.npad + a.nbc);
-  DevBuf<double> ws(stride2 * slots2);
+  ws.alloc(stride2 * slots2);
   a.ws = ws.p, a.ws_stride = stride2;
   HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   {
@@ -681,6 +955,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
                    fe * nwork);
     element_v2_kernel<<<slots2, kThreads, smem2, ctx->stream>>>(a);
     HPSB_LAUNCHED(ctx);
+  }
   }
   std::vector<int> st(ne);
   HPSB_CUDA(cudaMemcpyAsync(st.data(), el->status.p, ne * sizeof(int), cudaMemcpyDeviceToHost,
