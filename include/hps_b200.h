@@ -203,6 +203,11 @@ const double* hpsb_skeleton_rhs_dev(hpsb_skeleton sk, int r);
 /* Number of library kernels launched on this context so far (bench evidence). */
 int64_t hpsb_context_launches(hpsb_context ctx);
 
+/* Residual history (|g_{j+1}| / ||b|| per iteration, krylov.cpp:118) of the
+ * last single-RHS hpsb_fgmres[_dev] run with record_history != 0.  Copies up
+ * to cap values into out (may be NULL); returns the history length.       */
+int64_t hpsb_context_residual_history(hpsb_context ctx, double* out, int64_t cap);
+
 /* Device timer on the context stream (CUDA events): start, then stop returns
  * the elapsed seconds between the two event records.                       */
 hpsb_status hpsb_context_timer_start(hpsb_context ctx);

@@ -79,6 +79,7 @@ _sig("hpsb_context_create", _st, ctypes.c_int, ctypes.POINTER(_VP))
 _sig("hpsb_context_destroy", _st, _VP)
 _sig("hpsb_context_synchronize", _st, _VP)
 _sig("hpsb_context_launches", ctypes.c_int64, _VP)
+_sig("hpsb_context_residual_history", ctypes.c_int64, _VP, _D, ctypes.c_int64)
 _sig("hpsb_gll_rule", _st, ctypes.c_int, _D, _D, _D)
 _sig("hpsb_index_sets", _st, ctypes.c_int, _I)
 _sig("hpsb_face_graph", _st, ctypes.c_int, _I, _I, _I)
@@ -489,16 +490,25 @@ def build_preconditioner(hier: MergeHierarchy, depth: int = 0, gamma: int = 1,
 
 
 def fgmres(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: int = 60,
-           tol: float = 1e-8, max_iters: int = 2000):
-    """Flexible GMRES (fgmres, proj/src/krylov.cpp:188-192); precond None = gmres."""
+           tol: float = 1e-8, max_iters: int = 2000, record_history: bool = False):
+    """Flexible GMRES (fgmres, proj/src/krylov.cpp:188-192); precond None = gmres.
+    record_history adds the per-iteration |g_{j+1}| / ||b|| (krylov.cpp:118)."""
     rhs = _cplx(rhs)
     x = np.zeros_like(rhs)
     rep = SolveReport()
-    cfg = KrylovConfig(restart, tol, max_iters, 0, 1)
+    cfg = KrylovConfig(restart, tol, max_iters, int(record_history), 1)
     _check(_lib.hpsb_fgmres(sk._h, precond._h if precond else None, _dp(rhs.view(np.float64)),
                             _dp(x.view(np.float64)), cfg, ctypes.byref(rep)),
            allow=(OK, NO_CONVERGENCE))
-    return x, rep.as_dict()
+    out = rep.as_dict()
+    if record_history:
+        ctx = sk.elements.ctx._h
+        count = int(_lib.hpsb_context_residual_history(ctx, None, 0))
+        hist = np.zeros(max(count, 0))
+        if count > 0:
+            _lib.hpsb_context_residual_history(ctx, _dp(hist), count)
+        out["residual_history"] = hist.tolist()
+    return x, out
 
 
 def fgmres_batch(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: int = 60,

@@ -169,6 +169,15 @@ hpsb_status hpsb_context_synchronize(hpsb_context ctx) {
 
 int64_t hpsb_context_launches(hpsb_context ctx) { return ctx ? ctx->c.launches : -1; }
 
+int64_t hpsb_context_residual_history(hpsb_context ctx, double* out, int64_t cap) {
+  if (!ctx) return -1;
+  const auto& hst = ctx->c.history;
+  const int64_t n = static_cast<int64_t>(hst.size());
+  if (out)
+    for (int64_t i = 0; i < std::min(n, cap); ++i) out[i] = hst[i];
+  return n;
+}
+
 hpsb_status hpsb_context_timer_start(hpsb_context ctx) {
   return guarded([&] {
     REQUIRE(ctx, "timer: null context");

@@ -174,6 +174,9 @@ struct Context {
   // profiling, so each kernel's events bracket only its own work).
   bool pdl = true;
   bool use_pdl() const { return pdl && !profile; }
+  // residual history of the last single-RHS (F)GMRES with record_history
+  // (gmres_driver's report.residual_history, krylov.cpp:118)
+  std::vector<double> history;
 };
 
 // Brackets one kernel launch with CUDA events when profiling is enabled and

@@ -414,6 +414,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   const int restart = cfg.restart;
   *rep = hpsb_solve_report{};
   Work wk(ctx, n, restart + 2);
+  ctx->history.clear();
   DevBuf<double2> V(static_cast<size_t>(n) * (restart + 1));
   DevBuf<double2> Z(pc ? static_cast<size_t>(n) * restart : 0);
   DevBuf<double2> w(n), tmp(n);
@@ -497,6 +498,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
       apply_givens(rot[j], Hm(j, j), Hm(j + 1, j));
       apply_givens(rot[j], gv[j], gv[j + 1]);
       const double rel = std::abs(gv[j + 1]) / bnorm;
+      if (cfg.record_history) ctx->history.push_back(rel);
       static const bool dbg = std::getenv("HPSB_DEBUG_ORTH") != nullptr;
       if (dbg)
         std::fprintf(stderr, "it %d h00 %.17g %.17g hnext %.17g rel %.6e\n", total, hh[0].x, hh[0].y,
