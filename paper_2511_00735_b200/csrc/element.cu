@@ -630,14 +630,6 @@ __host__ __device__ inline size_t v3_smem_doubles(int P, int nbc, int nb) {
   return (fact > epi ? fact : epi);
 }
 
-__device__ unsigned long long* g_v3_trace = nullptr;  // development aid (HPSB_V3_TRACE)
-__device__ __forceinline__ void v3_mark(int slot) {
-  if (g_v3_trace && blockIdx.x == 0 && threadIdx.x == 0) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    atomicAdd(g_v3_trace + slot, t);
-  }
-}
 __global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
@@ -665,7 +657,6 @@ __global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
     const int e = a.elist ? a.elist[ii] : ii;
     __syncthreads();
     if (tid == 0) s_fail = 0;
-    if (ii == blockIdx.x + gridDim.x) v3_mark(0);
     const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
     for (int idx = tid; idx < P * P; idx += kV3Threads) {
       const int r = idx % P, c = idx / P;
@@ -704,7 +695,6 @@ __global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
       B[q + b * lda] = v;
     }
     __syncthreads();
-    if (ii == blockIdx.x + gridDim.x) v3_mark(1);
 
     // ---- factorisation + forward solve
     for (int k0 = 0; k0 < P; k0 += PW) {
@@ -799,7 +789,6 @@ __global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
       if (tid == 0) a.status[e] = 4;  // indefinite: pivoted-LU fallback
       continue;
     }
-    if (ii == blockIdx.x + gridDim.x) v3_mark(2);
     // ---- backward solve R^T X = Y, from the last panel
     for (int k0 = P - PW; k0 >= 0; k0 -= PW) {
       for (int c = tid; c < nbc; c += kV3Threads) {
@@ -834,12 +823,9 @@ __global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
       }
       __syncthreads();
     }
-    if (ii == blockIdx.x + gridDim.x) v3_mark(3);
     keep_interior(a, e, B, lda);
     __syncthreads();
-    if (ii == blockIdx.x + gridDim.x) v3_mark(4);
     const bool ok = iti_epilogue(a, e, B, lda, S, f, perm, red_v, red_i, diff_s);
-    if (ii == blockIdx.x + gridDim.x) v3_mark(5);
     if (tid == 0) a.status[e] = ok ? 0 : 2;
   }
 }
@@ -916,23 +902,8 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
         const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
         KernelScope ks(ctx, "element_iti", 8.0 * nwork * (np * np + 2 * ni + 2 * nb * nb + 2 * nb),
                        fe * nwork);
-        unsigned long long* tr = nullptr;
-        if (std::getenv("HPSB_V3_TRACE")) {
-          HPSB_CUDA(cudaMallocManaged(&tr, 8 * sizeof(unsigned long long)));
-          std::memset(tr, 0, 8 * sizeof(unsigned long long));
-          HPSB_CUDA(cudaMemcpyToSymbol(g_v3_trace, &tr, sizeof(tr)));
-        }
         element_v3_kernel<<<slots3, kV3Threads, smem3, ctx->stream>>>(a);
         HPSB_LAUNCHED(ctx);
-        if (tr) {
-          HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
-          std::fprintf(stderr, "[v3 trace us] assemble %.1f factor %.1f backward %.1f keep %.1f epilogue %.1f\n",
-                       (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3,
-                       (tr[4] - tr[3]) * 1e-3, (tr[5] - tr[4]) * 1e-3);
-          unsigned long long* z = nullptr;
-          HPSB_CUDA(cudaMemcpyToSymbol(g_v3_trace, &z, sizeof(z)));
-          cudaFree(tr);
-        }
       }
       done = true;
     }

@@ -474,18 +474,9 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
       double2* h1 = wk.hdev.p;
       double2* h2 = wk.hdev.p + (j + 1);
       double2* nn = wk.hdev.p + 2 * (j + 1);
-      static const bool old_orth = std::getenv("HPSB_OLD_ORTH") != nullptr;
-      if (old_orth) {
-        wk.dots(V.p, j + 1, w.p, h1);
-        wk.axpy(V.p, j + 1, h1, -1.0, w.p);
-        wk.dots(V.p, j + 1, w.p, h2);
-        wk.axpy(V.p, j + 1, h2, -1.0, w.p);
-        wk.dots(w.p, 1, w.p, nn);
-      } else {
-      wk.orth(V.p, j + 1, nullptr, 0, w.p, h1);     // h1 = V^H w
-      wk.orth(V.p, j + 1, h1, j + 1, w.p, h2);      // w -= V h1; h2 = V^H w
-      wk.orth(V.p, 0, h2, j + 1, w.p, nn);          // w -= V h2; nn = ||w||^2
-      }
+      wk.orth(V.p, j + 1, nullptr, 0, w.p, h1);  // h1 = V^H w
+      wk.orth(V.p, j + 1, h1, j + 1, w.p, h2);   // w -= V h1; h2 = V^H w
+      wk.orth(V.p, 0, h2, j + 1, w.p, nn);       // w -= V h2; nn = ||w||^2
       HPSB_CUDA(cudaMemcpyAsync(hh.data(), wk.hdev.p, sizeof(double2) * (2 * (j + 1) + 1),
                                 cudaMemcpyDeviceToHost, ctx->stream));
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -499,10 +490,6 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
       apply_givens(rot[j], gv[j], gv[j + 1]);
       const double rel = std::abs(gv[j + 1]) / bnorm;
       if (cfg.record_history) ctx->history.push_back(rel);
-      static const bool dbg = std::getenv("HPSB_DEBUG_ORTH") != nullptr;
-      if (dbg)
-        std::fprintf(stderr, "it %d h00 %.17g %.17g hnext %.17g rel %.6e\n", total, hh[0].x, hh[0].y,
-                     hnext, rel);
       if (hnext <= 1e-14 * bnorm) {
         breakdown = true;
         ++j;

@@ -252,17 +252,7 @@ constexpr int kCoarseCThreads = 256;
 constexpr int kCoarseClusterItems = 8;
 __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
     const VItem* __restrict__ gitems, int nitems, int n, int slice, int ci, int max_cols,
-    size_t stage_elems, const double2* rd, double2* outd, unsigned long long* trace) {
-  int tn = 0;
-  auto mark = [&]() {
-    if (trace && threadIdx.x == 0 && blockIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      trace[tn] = t;
-    }
-    ++tn;
-  };
-  mark();
+    size_t stage_elems, const double2* rd, double2* outd) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), crank = static_cast<int>(cl.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -331,9 +321,7 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
     slot ^= 1;
     return t;
   };
-  mark();
   pdl_wait();
-  mark();
   double2 loc = make_double2(0.0, 0.0);
   for (int k = tid; k < ns; k += kCoarseCThreads) {
     const double2 v = __ldcg(rd + s0 + k);
@@ -351,7 +339,6 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
   if (tid <= ci) gs[tid] = make_double2(tid == 0 ? beta : 0.0, 0.0);
   cp_async_wait_all();
   cl.sync();  // V_0 slices visible cluster-wide
-  mark();
   int jused = 0;
   for (int j = 0; j < ci; ++j) {
     // full v_j from the peers' slices
@@ -360,7 +347,6 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       vfull[k] = cl.map_shared_rank(Vs, o)[static_cast<size_t>(j) * slice + (k - o * slice)];
     }
     __syncthreads();
-    mark();
     // w = v_j + sum_boxes scatter(T gather(v_j)): gather every item's x,
     // then one warp per product row; rows go to the owner of their index.
     {
@@ -402,7 +388,6 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       }
     }
     cl.sync();  // w slices complete
-    mark();
     for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt on the slices
       const double2* Vi = Vs + static_cast<size_t>(i) * slice;
       double2 d = make_double2(0.0, 0.0);
@@ -411,7 +396,6 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       for (int k = tid; k < ns; k += kCoarseCThreads) ws[k] = csub(ws[k], cmul(h, Vi[k]));
       if (tid == 0) Hs[i + j * ldh] = h;
     }
-    mark();
     double2 nn = make_double2(0.0, 0.0);
     for (int k = tid; k < ns; k += kCoarseCThreads) nn.x += cabs2(ws[k]);
     const double hnext = sqrt(cluster_sum(nn).x);
@@ -431,7 +415,6 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
     double2* Vn = Vs + static_cast<size_t>(j + 1) * slice;
     for (int k = tid; k < ns; k += kCoarseCThreads) Vn[k] = make_double2(ws[k].x / hnext, ws[k].y / hnext);
     cl.sync();  // V_{j+1} slices visible; w slots free for the next matvec
-    mark();
   }
   if (tid == 0)
     for (int i = jused - 1; i >= 0; --i) {
@@ -445,27 +428,7 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
     for (int i = 0; i < jused; ++i) acc = cfma(ys[i], Vs[static_cast<size_t>(i) * slice + k], acc);
     outd[s0 + k] = acc;
   }
-  mark();
   cl.sync();  // no CTA exits while a peer may still read its shared memory
-  mark();
-}
-
-// HPSB_COARSE_TRACE: globaltimer stamps of CTA 0's phases of the last
-// coarse_cluster_kernel launch, printed at process exit (development aid).
-unsigned long long* coarse_trace(Context* ctx) {
-  static unsigned long long* buf = nullptr;
-  static const bool on = std::getenv("HPSB_COARSE_TRACE") != nullptr;
-  if (!on) return nullptr;
-  if (!buf) {
-    HPSB_CUDA(cudaMallocManaged(&buf, 64 * sizeof(unsigned long long)));
-    std::atexit([] {
-      cudaDeviceSynchronize();
-      for (int i = 1; i < 40 && buf[i]; ++i)
-        std::fprintf(stderr, "coarse trace %2d: %8.3f us\n", i, (buf[i] - buf[0]) * 1e-3);
-    });
-  }
-  (void)ctx;
-  return buf;
 }
 
 bool coarse_cluster_fits(size_t smem, int csize) {
@@ -1163,7 +1126,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
              p->coarse_smem, p->coarse_csize, static_cast<const VItem*>(p->coarse_items.p),
              p->coarse_nitems, static_cast<int>(p->dim_d), p->coarse_slice, ci,
              std::max(p->coarse_xs, 1), p->coarse_stage,
-             static_cast<const double2*>(p->r.p + p->off_d), z_dev + p->off_d, coarse_trace(ctx));
+             static_cast<const double2*>(p->r.p + p->off_d), z_dev + p->off_d);
   } else if (p->coarse_fused) {
     static const bool attr = [] {  // thread-safe one-time init
       HPSB_CUDA(cudaFuncSetAttribute(coarse_fused_kernel,
