@@ -71,8 +71,11 @@ __host__ __device__ inline size_t cluster_layout(int s, int p1, int p2, int C, b
 
 __device__ __forceinline__ void stage_rows(double2* dst, const double2* A, int lda, int r0, int nr,
                                            int ncols) {
-  for (int k = threadIdx.x; k < nr * ncols; k += kThreads)
-    cp_async16(dst + k, A + r0 + (k % nr) + static_cast<size_t>(k / nr) * lda);
+  // column segments of nr rows; warps over columns, lanes over rows (no division)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < ncols; c += kThreads / 32)
+    for (int r = lane; r < nr; r += 32)
+      cp_async16(dst + r + static_cast<size_t>(c) * nr, A + r0 + r + static_cast<size_t>(c) * lda);
 }
 
 // full[j] = slice_owner(j)[j - owner * cs] for j < n (DSMEM gather)

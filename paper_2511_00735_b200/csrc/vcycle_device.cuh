@@ -27,12 +27,28 @@ __device__ double2 smem_gemv(const double2* A, int lda, int rows, int cols, cons
   double2 acc = make_double2(0.0, 0.0);
   if (g < groups && r < rows)
     for (int j = g; j < cols; j += groups) acc = cfma(A[r + j * lda], x[j], acc);
-  red[tid] = acc;
-  __syncthreads();
   double2 s = make_double2(0.0, 0.0);
-  if (tid < rows) {
-    s = red[tid];
-    for (int q = 1; q < groups; ++q) s = cadd(s, red[tid + q * rpad]);
+  if (rpad <= 32) {
+    // a warp holds 32 / rpad groups of the same rows: fold them with
+    // shuffles, then one partial per warp and row goes through `red`
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int o = rpad; o < 32; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane < rpad) red[warp * rpad + lane] = acc;
+    __syncthreads();
+    if (tid < rows) {
+      s = red[tid];
+      for (int w = 1; w < kThreads / 32; ++w) s = cadd(s, red[w * rpad + tid]);
+    }
+  } else {
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < rows) {
+      s = red[tid];
+      for (int q = 1; q < groups; ++q) s = cadd(s, red[tid + q * rpad]);
+    }
   }
   __syncthreads();
   return s;
