@@ -55,7 +55,7 @@ typedef struct hpsb_precond_s* hpsb_precond;
 /* MgConfig (proj/include/hps/multigrid.hpp:12-18). */
 typedef struct hpsb_mg_config {
   int depth;        /* number of hierarchy levels used (>= 2) */
-  int gamma;        /* coarse calls per intermediate level (1 = V-cycle) */
+  int gamma;        /* coarse calls per intermediate level (1 = V-cycle, <= 16; > 1 single GPU) */
   int coarse_iters; /* unpreconditioned GMRES steps at the deepest level */
   int exact_coarse; /* dense inverse of M_depth instead of coarse GMRES (gamma = 1) */
 } hpsb_mg_config;

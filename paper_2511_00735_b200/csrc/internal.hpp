@@ -299,6 +299,7 @@ struct VPlan {
   DevBuf<VUnit> d_units;
   int64_t bytes_per_run = 0;  // algorithmic operator bytes streamed per run
   const char* name = "vplan";
+  DevBuf<int> idx_store;  // index lists owned by the plan (optional)
   // Start a new phase (one launch, csize CTAs per unit); returns its index.
   int begin_phase(int csize = 1);
   void add_unit(const std::vector<VItem>& chain);

@@ -73,6 +73,10 @@ struct Precond {
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
   std::vector<int> small_level_of;  // level -> smalls index (-1: none)
+  // gamma > 1: level systems M_l on faces >= first_face(l) (global indices),
+  // and per-level saved residual / accumulated correction
+  std::vector<VPlan> level_mv;  // [l], l = 2..depth
+  DevBuf<double2> gam_rc, gam_z, gam_t;
   double bytes_small = 0;
   // ---- multi-RHS (built on first use, capacity kBatchMaxRhs)
   // stage_items[dir][l][k]: items of every merge of level l in stage k
@@ -685,9 +689,12 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   if (!cfg.exact_coarse && cfg.gamma < 1) throw InvalidArgument("MgPreconditioner: gamma must be >= 1");
   if (!cfg.exact_coarse && cfg.coarse_iters < 1)
     throw InvalidArgument("MgPreconditioner: coarse_iters must be >= 1");
-  // multigrid.cpp:71: the exact coarse mode runs gamma = 1.
-  if (!cfg.exact_coarse && cfg.gamma != 1)
-    throw InvalidArgument("MgPreconditioner: gamma > 1 is not on the B200 path");
+  // multigrid.cpp:71: the exact coarse mode runs gamma = 1.  gamma > 1
+  // (W- / gamma-cycles) runs host-recursively on one GPU.
+  if (!cfg.exact_coarse && cfg.gamma > 1 && h->ctx->world() > 1)
+    throw InvalidArgument("MgPreconditioner: gamma > 1 is single-GPU");
+  if (!cfg.exact_coarse && cfg.gamma > 16)
+    throw InvalidArgument("MgPreconditioner: gamma must be <= 16");
   if (cfg.depth != h->depth)
     throw InvalidArgument("MgPreconditioner: depth must equal the built hierarchy depth on the B200 path");
   if (!cfg.exact_coarse && cfg.coarse_iters > 60) throw InvalidArgument("MgPreconditioner: coarse_iters must be <= 60");
@@ -1037,6 +1044,41 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       }
     }
   }
+  if (!cfg.exact_coarse && cfg.gamma > 1) {
+    // next.M.apply(z) of apply_level's gamma loop (multigrid.cpp:71-80):
+    // M_l = I + sum_boxes scatter_out(T gather_in(.)) over the boxes entering level l
+    p->level_mv.resize(cfg.depth + 1);
+    p->gam_rc.alloc(static_cast<size_t>(cfg.depth) * p->dim);
+    p->gam_z.alloc(static_cast<size_t>(cfg.depth) * p->dim);
+    p->gam_t.alloc(p->dim);
+    for (int l = 2; l <= cfg.depth; ++l) {
+      const LevelOps& Lv = *h->levels[l - 1];
+      std::vector<int> gidx;
+      std::vector<size_t> in_at2, out_at2;
+      for (const ChildBox& c : Lv.children) {
+        in_at2.push_back(gidx.size());
+        for (const auto& q : c.pos) gidx.push_back(q.in);
+        out_at2.push_back(gidx.size());
+        for (const auto& q : c.pos) gidx.push_back(q.out);
+      }
+      VPlan& mv = p->level_mv[l];
+      mv.idx_store.upload(gidx, ctx->stream);
+      int rows = 0;
+      for (const ChildBox& c : Lv.children) rows += c.P;
+      const int rb2 = split_rows(std::max(rows, 1), sms);
+      mv.begin_phase();
+      for (size_t k = 0; k < Lv.children.size(); ++k) {
+        const ChildBox& c = Lv.children[k];
+        const int* gi = mv.idx_store.p + in_at2[k];
+        const int* go = mv.idx_store.p + out_at2[k];
+        mv.add_split(item(Lv.tperm.p + c.t_off, c.P, c.P, c.P, p->gam_t.p, gi, p->gam_t.p, go, p->r.p,
+                          go, 1.0, 0.0, 1.0),
+                     rb2);
+      }
+      mv.name = "level_matvec";
+      mv.finalize(ctx->stream);
+    }
+  }
   if (cfg.exact_coarse) {
     // exact_lu = LU(M_depth.to_dense()) (multigrid.cpp:22-27); here the dense
     // inverse (blocked Gauss-Jordan on the DMMA GEMMs) and one GEMV per apply.
@@ -1101,22 +1143,11 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
 
 void destroy_precond(Precond* p) { delete p; }
 
-void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
+namespace {
+// The deepest level's solve: gmres_fixed_steps on M_depth (or the exact
+// dense inverse), r[off_d:] -> z[off_d:].
+void run_coarse(Precond* p, double2* z_dev) {
   Context* ctx = p->ctx;
-  const int vblocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
-  launch_k(ctx, copy_vec_kernel, dim3(vblocks), dim3(256), 0, 1, p->r.p, v_dev, p->dim);
-  // `out` of the plans is bound to the caller's z: no copy-out.
-  p->run_steps(true, false, z_dev);  // local levels, down
-  const bool sharded = ctx->world() > 1;
-  if (sharded) {
-    // Each residual entry was updated by at most one rank's subtree:
-    // r = v + sum_ranks (r_rank - v).
-    const int blocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
-    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, -1.0, p->dim);
-    ctx->comm->allreduce_sum(p->r.p, p->dim, ctx);
-    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, 1.0, p->dim);
-  }
-  p->run_steps(true, true, z_dev);  // top (global) levels, down
   const int ci = p->cfg.coarse_iters;
   if (p->cfg.exact_coarse) {
     p->exact_mv.run(ctx, p->out.p, z_dev);
@@ -1162,6 +1193,76 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
            z_dev + p->off_d, int64_t(0));
   }
   }
+}
+
+void run_level(Precond* p, int l, bool down, double2* z) {
+  for (const Precond::Step& st : down ? p->down_steps : p->up_steps) {
+    if (st.level != l) continue;
+    if (st.small >= 0) p->smalls[st.small]->run(p->ctx, down, p->r.p, z);
+    else if (st.cluster >= 0) p->clusters[st.cluster]->run(p->ctx, down, p->r.p, z);
+    else
+      for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(p->ctx, q, p->out.p, z);
+  }
+}
+
+// apply_level (multigrid.cpp:30-100) with gamma > 1: F and restriction at
+// level l (down step), gamma recursive coarse corrections with the level
+// system residual rc - M_{l+1} z in between, prolongation (up step).
+void apply_level_gamma(Precond* p, int l, double2* z) {
+  Context* ctx = p->ctx;
+  if (l == p->cfg.depth) {
+    run_coarse(p, z);
+    return;
+  }
+  run_level(p, l, true, z);
+  const Hierarchy* h = p->h;
+  const int64_t off = static_cast<int64_t>(h->levels[l]->first_face) * h->sk->bs;  // level l+1 tail
+  const int64_t len = p->dim - off;
+  double2* rc = p->gam_rc.p + static_cast<size_t>(l) * p->dim;
+  double2* zacc = p->gam_z.p + static_cast<size_t>(l) * p->dim;
+  const int blocks = static_cast<int>(std::min<int64_t>((len + 255) / 256, 8 * ctx->num_sms));
+  launch_k(ctx, copy_vec_kernel, dim3(blocks), dim3(256), 0, 1, rc + off, p->r.p + off, len);
+  HPSB_CUDA(cudaMemsetAsync(zacc + off, 0, sizeof(double2) * len, ctx->stream));
+  for (int step = 0; step < p->cfg.gamma; ++step) {
+    if (step > 0) {
+      // r = rc - M_{l+1} z on the tail
+      p->level_mv[l + 1].run(ctx, p->gam_t.p, zacc, p->r.p, p->gam_t.p);
+      launch_k(ctx, copy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p + off,
+               static_cast<const double2*>(rc + off), len);
+      launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p + off,
+               static_cast<const double2*>(p->gam_t.p + off), -1.0, len);
+    }
+    apply_level_gamma(p, l + 1, z);
+    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, zacc + off,
+             static_cast<const double2*>(z + off), 1.0, len);
+  }
+  launch_k(ctx, copy_vec_kernel, dim3(blocks), dim3(256), 0, 1, z + off,
+           static_cast<const double2*>(zacc + off), len);
+  run_level(p, l, false, z);
+}
+}  // namespace
+
+void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
+  Context* ctx = p->ctx;
+  const int vblocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
+  launch_k(ctx, copy_vec_kernel, dim3(vblocks), dim3(256), 0, 1, p->r.p, v_dev, p->dim);
+  if (!p->cfg.exact_coarse && p->cfg.gamma > 1) {
+    apply_level_gamma(p, 1, z_dev);
+    return;
+  }
+  // `out` of the plans is bound to the caller's z: no copy-out.
+  p->run_steps(true, false, z_dev);  // local levels, down
+  const bool sharded = ctx->world() > 1;
+  if (sharded) {
+    // Each residual entry was updated by at most one rank's subtree:
+    // r = v + sum_ranks (r_rank - v).
+    const int blocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
+    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, -1.0, p->dim);
+    ctx->comm->allreduce_sum(p->r.p, p->dim, ctx);
+    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, 1.0, p->dim);
+  }
+  p->run_steps(true, true, z_dev);  // top (global) levels, down
+  run_coarse(p, z_dev);
   p->run_steps(false, true, z_dev);
   p->run_steps(false, false, z_dev);
   if (sharded) {
@@ -1250,6 +1351,8 @@ void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
   Context* ctx = p->ctx;
   if (ctx->world() > 1) throw InvalidArgument("precond_apply: multi-RHS is single-GPU");
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("precond_apply: 1 <= nrhs <= 32");
+  if (!p->cfg.exact_coarse && p->cfg.gamma > 1)
+    throw InvalidArgument("precond_apply: multi-RHS runs gamma = 1");
   if (!p->batch_ready) build_batch(p);
   const int64_t dim = p->dim, nd = p->dim_d;
   HPSB_CUDA(cudaMemcpyAsync(p->rB.p, v, sizeof(double2) * R * dim, cudaMemcpyDeviceToDevice,

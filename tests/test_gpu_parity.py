@@ -370,3 +370,23 @@ def test_fgmres_multi_rhs_cfg4_planewaves(hps, oracle, ctx):
         xs, reps1 = hps.fgmres(sk, rhs[b], pc, restart=100, tol=1e-10)
         assert abs(reps1["iterations"] - reps[b]["iterations"]) <= 1
         assert relf(X[b], xs) < TOL_SOL
+
+
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg2_n8"])
+@pytest.mark.parametrize("gamma", [2, 3])
+def test_gamma_cycle(hps, oracle, ctx, name, gamma):
+    # apply_level's gamma recursion (multigrid.cpp:71-80): gamma coarse
+    # corrections per level with the level-system residual in between.
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk, factor_coarse=False)
+    c.S.build_hierarchy(0, False)
+    pc = hps.build_preconditioner(h, gamma=gamma, coarse_iters=4)
+    c.S.precond(depth=h.depth, gamma=gamma, coarse_iters=4)
+    rng = np.random.default_rng(30 + gamma)
+    v = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+    assert relf(pc.apply(v), c.S.precond_apply(v)) < TOL_OP
+    if name != "cfg2_n8":
+        x, rep = hps.fgmres(c.sk, c.sk.rhs(), pc, restart=50, tol=1e-10)
+        xo, repo = c.S.solve(c.S.rhs(), True, restart=50, tol=1e-10)
+        assert rep["converged"] and abs(rep["iterations"] - repo["iterations"]) <= 1
+        assert relf(x, xo) < TOL_SOL
