@@ -24,7 +24,9 @@ def _single(hps, prob, x, v):
     h = hps.build_hierarchy(sk)
     pc = hps.build_preconditioner(h, coarse_iters=4)
     sol, rep = hps.fgmres(sk, sk.rhs(), pc, restart=prob.restart, tol=prob.tol)
-    return {"rhs": sk.rhs(), "Mx": sk.apply(x), "Pv": pc.apply(v), "x": sol, "rep": rep}
+    pe = hps.build_preconditioner(h, exact_coarse=True)
+    return {"rhs": sk.rhs(), "Mx": sk.apply(x), "Pv": pc.apply(v), "x": sol, "rep": rep,
+            "Pe": pe.apply(v), "direct": h.direct_solve(sk.rhs()), "field": sk.recover(sol)}
 
 
 def _sharded(hps, prob, world, x, v):
@@ -41,6 +43,10 @@ def _sharded(hps, prob, world, x, v):
             pc = hps.build_preconditioner(h, coarse_iters=4)
             res = {"rhs": sk.rhs(), "Mx": sk.apply(x), "Pv": pc.apply(v)}
             res["x"], res["rep"] = hps.fgmres(sk, sk.rhs(), pc, restart=prob.restart, tol=prob.tol)
+            pe = hps.build_preconditioner(h, exact_coarse=True)
+            res["Pe"] = pe.apply(v)
+            res["direct"] = h.direct_solve(sk.rhs())
+            res["field"] = sk.recover(res["x"])
             res["rank_world"] = ctx.rank_world
             out[rank] = res
         except Exception as exc:  # noqa: BLE001
@@ -90,6 +96,9 @@ def test_sharded_matches_single_gpu(config, world):
         assert s["rep"]["converged"]
         assert abs(s["rep"]["iterations"] - ref["rep"]["iterations"]) <= 1
         assert relf(s["x"], ref["x"]) < 1e-9
+        assert relf(s["Pe"], ref["Pe"]) < 1e-10          # exact coarse (dense inverse)
+        assert relf(s["direct"], ref["direct"]) < 1e-9   # direct_solve
+        assert relf(s["field"], ref["field"]) < 1e-9     # recover_solution
     # every rank holds the same replicated solution
     for s in shards[1:]:
         assert relf(s["x"], shards[0]["x"]) < 1e-12
