@@ -146,6 +146,7 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
   // at a level own disjoint slots, so the threads of the parallel pass below
   // write disjoint entries of one shared table.
   std::vector<int> pos_of(sk->dim, -1);
+  std::vector<int> prev_merge_of;  // previous level: group (= box of this level) -> merge index
   DevBuf<double2> tnew_prev;  // previous level's merged maps (children of this level)
   DevBuf<int> d_status(1);
   HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(int), ctx->stream));
@@ -222,6 +223,10 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
       MergeRec mr;
       mr.s = static_cast<int>(groups[gi].size()) * m;
       mr.group = gi;
+      if (level > 1) {
+        mr.src1 = prev_merge_of[elem_box[f0.e1]];
+        mr.src2 = prev_merge_of[elem_box[f0.e2]];
+      }
       for (int k = 0; k < 2; ++k) {
         ChildBox cb;
         cb.p = gp.p[k];
@@ -240,6 +245,7 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
       L->merges.push_back(mr);
     }
     tr.mark("bookkeeping");
+    prev_merge_of = merge_of;
     L->tperm.alloc(toff);
     tr.mark("alloc");
 

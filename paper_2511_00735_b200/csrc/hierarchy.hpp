@@ -29,6 +29,9 @@ struct MergeRec {
   int c1 = 0, c2 = 0;
   int s = 0, p1 = 0, p2 = 0;
   int group = 0;  // group index within the level (face-graph order)
+  // merges of the previous level that produced child 1 / child 2 (-1: an
+  // element at level 1, or another rank's box)
+  int src1 = -1, src2 = -1;
   size_t w_off = 0;
   // offsets (in ints) into LevelOps::idx of the V-cycle index lists
   size_t in1_sep = 0, in2_sep = 0, in1_per = 0, out1_per = 0, in2_per = 0, out2_per = 0;

@@ -65,13 +65,14 @@ struct Precond {
   VPlan exact_mv;
   // per-level execution order of the sweeps
   struct Step {
-    int level = 0, small = -1, cluster = -1;
+    int level = 0, small = -1, cluster = -1, subtree = -1;
     const VPlan* plan = nullptr;
     int p0 = 0, p1 = 0;
   };
   std::vector<Step> down_steps, up_steps;
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
+  std::vector<std::unique_ptr<SubtreeLevels>> subtrees;
   std::vector<int> small_level_of;  // level -> smalls index (-1: none)
   // gamma > 1: level systems M_l on faces >= first_face(l) (global indices),
   // and per-level saved residual / accumulated correction
@@ -92,7 +93,8 @@ struct Precond {
     const int last_local = h->sk->el->part.last_local;
     for (const Step& st : down ? down_steps : up_steps) {
       if ((st.level > last_local) != global) continue;
-      if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
+      if (st.subtree >= 0) subtrees[st.subtree]->run(ctx, down, r.p, z);
+      else if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
       else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
       else
         for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
@@ -851,6 +853,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     }
     sl->level = l;
     sl->count = static_cast<int>(v.size());
+    sl->host = v;
     if (std::getenv("HPSB_PROFILE_LEVELS")) sl->label = "vcycle_small_L" + std::to_string(l);
     sl->d.upload(v, ctx->stream);
     p->smalls.push_back(std::move(sl));
@@ -927,6 +930,65 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   };
   for (int l = 1; l < cfg.depth; ++l) add_step(l, true);
   for (int l = cfg.depth - 1; l >= 1; --l) add_step(l, false);
+  // Fuse the leading run of small-merge levels 1..k into one launch per
+  // direction (one CTA per level-k subtree), single GPU / V-cycle only.
+  {
+    int k = 0;
+    while (k + 1 < cfg.depth && small_of[k + 1] >= 0) ++k;
+    if (const char* e = std::getenv("HPSB_SUBTREE_LEVELS")) k = std::min(k, std::atoi(e));
+    else k = 0;  // opt-in: measured slower (sequential merges per CTA, see DESIGN)
+    if (k >= 2 && ctx->world() == 1 && cfg.gamma == 1) {
+      auto st = std::make_unique<SubtreeLevels>();
+      std::vector<SmallMerge> all;
+      std::vector<size_t> base(k + 1, 0);
+      for (int l = 1; l <= k; ++l) {
+        base[l] = all.size();
+        const SmallLevel& sl = *p->smalls[small_of[l]];
+        all.insert(all.end(), sl.host.begin(), sl.host.end());
+        st->smem = std::max(st->smem, sl.smem);
+        st->bytes_down += sl.bytes_down;
+        st->bytes_up += sl.bytes_up;
+      }
+      std::vector<int> order, seg{0};
+      const auto& topm = h->levels[k - 1]->merges;
+      for (size_t b = 0; b < topm.size(); ++b) {
+        std::vector<std::vector<int>> per(k + 1);
+        per[k].push_back(static_cast<int>(b));
+        for (int l = k; l >= 2; --l)
+          for (int mi : per[l]) {
+            const MergeRec& mr = h->levels[l - 1]->merges[mi];
+            if (mr.src1 < 0 || mr.src2 < 0) throw std::logic_error("subtree: missing child merge");
+            per[l - 1].push_back(mr.src1);
+            per[l - 1].push_back(mr.src2);
+          }
+        for (int l = 1; l <= k; ++l)
+          for (int mi : per[l]) order.push_back(static_cast<int>(base[l]) + mi);
+        seg.push_back(static_cast<int>(order.size()));
+      }
+      if (order.size() != all.size()) throw std::logic_error("subtree: merges not covered exactly once");
+      st->levels = k;
+      st->count = static_cast<int>(topm.size());
+      if (std::getenv("HPSB_PROFILE_LEVELS")) st->label = "vcycle_subtree_L1-" + std::to_string(k);
+      st->d.upload(all, ctx->stream);
+      st->order.upload(order, ctx->stream);
+      st->seg.upload(seg, ctx->stream);
+      p->subtrees.push_back(std::move(st));
+      const int si = static_cast<int>(p->subtrees.size()) - 1;
+      auto fuse = [&](std::vector<Precond::Step>& steps, bool front) {
+        std::vector<Precond::Step> kept;
+        for (const auto& s2 : steps)
+          if (s2.level > k) kept.push_back(s2);
+        Precond::Step f;
+        f.level = 1;
+        f.subtree = si;
+        if (front) kept.insert(kept.begin(), f);
+        else kept.push_back(f);
+        steps = std::move(kept);
+      };
+      fuse(p->down_steps, true);
+      fuse(p->up_steps, false);
+    }
+  }
   p->down.name = "vcycle_down";
   p->up.name = "vcycle_up";
   p->down_g.name = "vcycle_down";
