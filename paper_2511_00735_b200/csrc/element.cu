@@ -612,6 +612,268 @@ __global__ void __launch_bounds__(kThreads, 2) element_v2_kernel(ElemArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- v4
+// Left-looking blocked Cholesky (16-wide panels) with the interior block and
+// right-hand sides in the per-CTA global workspace (L2).  Per panel k:
+//   1. the panel's rows of L (16 x k0) are staged once in shared memory;
+//   2. the panel column block is brought up to date with one GEMM
+//      A[k0:, k0:k0+16] -= L[k0:, :k0] L[k0:k0+16, :k0]^T: every warp owns
+//      8-row strips whose 8 x 16 accumulators stay in registers over the whole
+//      K loop (the A operand streams from L2, each element read once per
+//      panel; no read-modify-write of the trailing matrix as in v2);
+//   3. likewise the panel rows of the right-hand sides,
+//      B[k0:k0+16, :] -= L[k0:k0+16, :k0] Y[:k0, :];
+//   4. the 16 x 16 diagonal block is factored (warp 0), the rows below solved
+//      against it (TRSM) and the panel rows of B solved (forward).
+// The backward solve is left-looking the same way:
+//   X_k = L_kk^{-T} (Y_k - L[k0+16:, k]^T X[k0+16:]).
+constexpr int kV4Ld = 8;  // smem padding of the staged panel rows
+#ifndef HPSB_V4_UNROLL
+#define HPSB_V4_UNROLL 16
+#endif
+constexpr int kV4Unroll = HPSB_V4_UNROLL;
+__host__ __device__ inline size_t v4_region(int P, int nbc, int nb) {
+  const size_t panel = static_cast<size_t>(PW) * (P + kV4Ld) + PW * PW + static_cast<size_t>(PW) * (nbc + 4);
+  const size_t epi = 2 * (static_cast<size_t>(nb) * nb + nb);
+  return panel > epi ? panel : epi;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) element_v4_kernel(ElemArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  constexpr int kWarps = kThreads / 32;
+  const int m = a.m, ni = a.ni, nb = a.nb, np = a.order + 1, N = a.order;
+  const int P = a.npad, nbc = a.nbc, ldk = P + kV4Ld;
+  double* Ls = reinterpret_cast<double*>(smem_raw);        // [16][ldk]: L[k0 + n][k]
+  double* D11 = Ls + static_cast<size_t>(PW) * ldk;         // 16 x 16
+  double* Xp = D11 + PW * PW;                               // [16][nbc + 4]: panel rows of X
+  const int ldx = nbc + 4;
+  double2* S = reinterpret_cast<double2*>(smem_raw);        // epilogue overlay
+  double2* f = S + nb * nb;
+  double* mass = reinterpret_cast<double*>(smem_raw) + v4_region(P, nbc, nb);
+  int* perm = reinterpret_cast<int*>(mass + np);
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_fail;
+
+  double* A = a.ws + blockIdx.x * a.ws_stride;  // P x P, ld P (lower used)
+  double* B = A + static_cast<size_t>(P) * P;    // P x nbc, ld P
+  for (int i = tid; i < np; i += blockDim.x) mass[i] = a.mass[i];
+  auto K = [&](int r, int c) { return __ldg(a.stiff + r + c * np); };
+  const int count = a.elist ? a.nlist : a.ne;
+
+  for (int ii = blockIdx.x; ii < count; ii += gridDim.x) {
+    const int e = a.elist ? a.elist[ii] : ii;
+    __syncthreads();
+    if (tid == 0) s_fail = 0;
+    const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
+    for (int idx = tid; idx < P * P; idx += blockDim.x) {
+      const int r = idx % P, c = idx / P;
+      if (c > r) continue;
+      double v;
+      if (r >= ni) {
+        v = (r == c) ? 1.0 : 0.0;
+      } else {
+        const int i = r / m + 1, j = r % m + 1, k = c / m + 1, l = c % m + 1;
+        v = 0.0;
+        if (j == l) v += K(i, k) * mass[j];
+        if (i == k) v += mass[i] * K(j, l);
+        if (r == c) v -= __ldg(ce + i * np + j) * mass[i] * mass[j];
+      }
+      A[idx] = v;
+    }
+    for (int idx = tid; idx < P * nbc; idx += blockDim.x) {
+      const int q = idx % P, b = idx / P;
+      double v = 0.0;
+      if (q < ni && b < nb + 2) {
+        const int i = q / m + 1, j = q % m + 1;
+        if (b < nb) {
+          const int side = b / m, t = b % m + 1;
+          switch (side) {
+            case 0: v = (j == t) ? K(i, 0) * mass[j] : 0.0; break;
+            case 1: v = (j == t) ? K(i, N) * mass[j] : 0.0; break;
+            case 2: v = (i == t) ? mass[i] * K(j, 0) : 0.0; break;
+            default: v = (i == t) ? mass[i] * K(j, N) : 0.0; break;
+          }
+        } else if (a.source) {
+          const double2 sv = a.source[static_cast<size_t>(e) * ni + q];
+          const double w = mass[i] * mass[j];
+          v = (b == nb) ? sv.x * w : sv.y * w;
+        }
+      }
+      B[idx] = v;
+    }
+    __syncthreads();
+
+    // ---- factorisation + forward solve, left-looking
+    for (int k0 = 0; k0 < P; k0 += PW) {
+      // 1. panel rows of L (final) -> smem
+      for (int idx = tid; idx < PW * k0; idx += blockDim.x) {
+        const int n = idx % PW, k = idx / PW;
+        Ls[n * ldk + k] = A[(k0 + n) + static_cast<size_t>(k) * P];
+      }
+      __syncthreads();
+      const int nstrip = (P - k0) / 8, nbt = nbc / 8;
+      // 2. + 3. GEMM updates: strips of the panel column block, then the
+      //    panel rows of B (2 row tiles x nbt column tiles)
+      for (int w = warp; w < nstrip + 2 * nbt; w += kWarps) {
+        if (w < nstrip) {
+          const int r0 = k0 + 8 * w;
+          double* C0 = A + (r0 + g) + static_cast<size_t>(k0 + 2 * t4) * P;
+          double* C1 = C0 + static_cast<size_t>(8) * P;
+          double c00 = C0[0], c01 = C0[P], c10 = C1[0], c11 = C1[P];
+          const double* Ar = A + (r0 + g) + static_cast<size_t>(t4) * P;
+          int kk = 0;
+          for (; kk + 4 * kV4Unroll <= k0; kk += 4 * kV4Unroll) {
+            double av[kV4Unroll];  // kV4Unroll independent L2 loads in flight per lane
+#pragma unroll
+            for (int q = 0; q < kV4Unroll; ++q) av[q] = -Ar[static_cast<size_t>(kk + 4 * q) * P];
+#pragma unroll
+            for (int q = 0; q < kV4Unroll; ++q) {
+              dmma(c00, c01, av[q], Ls[g * ldk + kk + 4 * q + t4]);
+              dmma(c10, c11, av[q], Ls[(8 + g) * ldk + kk + 4 * q + t4]);
+            }
+          }
+          for (; kk < k0; kk += 4) {
+            const double av = -Ar[static_cast<size_t>(kk) * P];
+            dmma(c00, c01, av, Ls[g * ldk + kk + t4]);
+            dmma(c10, c11, av, Ls[(8 + g) * ldk + kk + t4]);
+          }
+          C0[0] = c00, C0[P] = c01, C1[0] = c10, C1[P] = c11;
+        } else {
+          const int tt = w - nstrip, I = tt % 2, J = tt / 2;
+          double* Cp = B + (k0 + 8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
+          double c0 = Cp[0], c1 = Cp[P];
+          const double* Yc = B + t4 + static_cast<size_t>(8 * J + g) * P;  // Y[k][8J + g]
+          int kk = 0;
+          for (; kk + 32 <= k0; kk += 32) {
+            double ya[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ya[q] = Yc[kk + 4 * q];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dmma(c0, c1, -Ls[(8 * I + g) * ldk + kk + 4 * q + t4], ya[q]);
+          }
+          for (; kk < k0; kk += 4)
+            dmma(c0, c1, -Ls[(8 * I + g) * ldk + kk + t4], Yc[kk]);
+          Cp[0] = c0, Cp[P] = c1;
+        }
+      }
+      __syncthreads();
+      // 4. diagonal block, TRSM below, forward solve of the panel rows of B
+      for (int idx = tid; idx < PW * PW; idx += blockDim.x) {
+        const int r = idx % PW, c = idx / PW;
+        D11[idx] = c <= r ? A[(k0 + r) + static_cast<size_t>(k0 + c) * P] : 0.0;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        for (int j = 0; j < PW; ++j) {
+          if (lane == 0) {
+            const double d = D11[j + j * PW];
+            if (!(d > 0.0)) s_fail = 1;
+            D11[j + j * PW] = sqrt(fmax(d, 1e-300));
+          }
+          __syncwarp();
+          const double inv = 1.0 / D11[j + j * PW];
+          if (lane > j && lane < PW) D11[lane + j * PW] *= inv;
+          __syncwarp();
+          for (int q = lane; q < PW * PW; q += 32) {
+            const int r = q % PW, c = q / PW;
+            if (c > j && r >= c) D11[r + c * PW] -= D11[r + j * PW] * D11[c + j * PW];
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+      if (s_fail) break;
+      const int rem = P - k0 - PW;
+      for (int idx = tid; idx < PW * PW; idx += blockDim.x) {
+        const int r = idx % PW, c = idx / PW;
+        if (c <= r) A[(k0 + r) + static_cast<size_t>(k0 + c) * P] = D11[idx];
+      }
+      for (int r = tid; r < rem + nbc; r += blockDim.x) {
+        double x[PW];
+        if (r < rem) {
+          double* row = A + (k0 + PW + r) + static_cast<size_t>(k0) * P;
+#pragma unroll
+          for (int j = 0; j < PW; ++j) x[j] = row[static_cast<size_t>(j) * P];
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
+            double sacc = x[j];
+#pragma unroll
+            for (int t = 0; t < j; ++t) sacc -= x[t] * D11[j + t * PW];
+            x[j] = sacc / D11[j + j * PW];
+            row[static_cast<size_t>(j) * P] = x[j];
+          }
+        } else {
+          double* col = B + k0 + static_cast<size_t>(r - rem) * P;
+#pragma unroll
+          for (int j = 0; j < PW; ++j) x[j] = col[j];
+#pragma unroll
+          for (int j = 0; j < PW; ++j) {
+            double sacc = x[j];
+#pragma unroll
+            for (int t = 0; t < j; ++t) sacc -= D11[j + t * PW] * x[t];
+            x[j] = sacc / D11[j + j * PW];
+            col[j] = x[j];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (s_fail) {
+      if (tid == 0) a.status[e] = 4;  // indefinite: pivoted-LU fallback
+      continue;
+    }
+    // ---- backward solve, left-looking: X_k = L_kk^{-T}(Y_k - L[k0+16:, k]^T X[k0+16:])
+    for (int k0 = P - PW; k0 >= 0; k0 -= PW) {
+      const int nbt = nbc / 8, kb = k0 + PW, klen = P - kb;
+      for (int idx = tid; idx < PW * PW; idx += blockDim.x) {
+        const int r = idx % PW, c = idx / PW;
+        D11[idx] = c <= r ? A[(k0 + r) + static_cast<size_t>(k0 + c) * P] : 0.0;
+      }
+      for (int w = warp; w < 2 * nbt; w += kWarps) {
+        const int I = w % 2, J = w / 2;
+        double* Cp = B + (k0 + 8 * I + g) + static_cast<size_t>(8 * J + 2 * t4) * P;
+        double c0 = Cp[0], c1 = Cp[P];
+        // A-fragment (row 8I+g, k) = L[kb + k][k0 + 8I + g]; B-fragment (k, col 8J+g) = X[kb + k][8J + g]
+        const double* Lc = A + kb + t4 + static_cast<size_t>(k0 + 8 * I + g) * P;
+        const double* Xc = B + kb + t4 + static_cast<size_t>(8 * J + g) * P;
+        int kk = 0;
+        for (; kk + 32 <= klen; kk += 32) {
+          double la[8], xa[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) la[q] = -Lc[kk + 4 * q], xa[q] = Xc[kk + 4 * q];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) dmma(c0, c1, la[q], xa[q]);
+        }
+        for (; kk < klen; kk += 4) dmma(c0, c1, -Lc[kk], Xc[kk]);
+        Cp[0] = c0, Cp[P] = c1;
+      }
+      __syncthreads();
+      for (int c = tid; c < nbc; c += blockDim.x) {
+        double y[PW];
+        double* col = B + k0 + static_cast<size_t>(c) * P;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) y[j] = col[j];
+#pragma unroll
+        for (int j = PW - 1; j >= 0; --j) {
+          double sacc = y[j];
+#pragma unroll
+          for (int t = j + 1; t < PW; ++t) sacc -= D11[t + j * PW] * y[t];
+          y[j] = sacc / D11[j + j * PW];
+        }
+#pragma unroll
+        for (int j = 0; j < PW; ++j) col[j] = y[j];
+      }
+      __syncthreads();
+    }
+    (void)Xp, (void)ldx;
+    keep_interior(a, e, B, P);
+    const bool ok = iti_epilogue(a, e, B, P, S, f, perm, red_v, red_i);
+    if (tid == 0) a.status[e] = ok ? 0 : 2;
+  }
+}
+
 // ---------------------------------------------------------------- v3
 // Shared-memory-resident variant for small interiors (P <= ~128, i.e. N <= 12):
 // the whole interior block L_ii (column-major, ld P+4 so 8x8 DMMA fragments
@@ -907,6 +1169,26 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
       }
       done = true;
     }
+  }
+  if (!done && !std::getenv("HPSB_ELEMENT_V2")) {
+    // v4 (left-looking, DMMA GEMM panels)
+    const size_t smem4 = sizeof(double) * (v4_region(a.npad, a.nbc, nb) + np) + sizeof(int) * nb + 16;
+    allow_smem<element_v4_kernel>(smem4);
+    int per_sm = 0;
+    HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, element_v4_kernel, kThreads, smem4));
+    const int slots4 = std::min(nwork, std::max(1, std::min(per_sm, 3)) * ctx->num_sms);
+    const size_t stride4 = static_cast<size_t>(a.npad) * (a.npad + a.nbc);
+    ws.alloc(stride4 * slots4);
+    a.ws = ws.p, a.ws_stride = stride4;
+    HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
+    {
+      const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
+      KernelScope ks(ctx, "element_iti", 8.0 * nwork * (np * np + 2 * ni + 2 * nb * nb + 2 * nb),
+                     fe * nwork);
+      element_v4_kernel<<<slots4, kThreads, smem4, ctx->stream>>>(a);
+      HPSB_LAUNCHED(ctx);
+    }
+    done = true;
   }
   if (!done) {
   // v2 (blocked, DMMA) for every element
