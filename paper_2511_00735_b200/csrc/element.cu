@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 2) element_v2_kernel(ElemArgs a) {
 //   X_k = L_kk^{-T} (Y_k - L[k0+16:, k]^T X[k0+16:]).
 constexpr int kV4Ld = 8;  // smem padding of the staged panel rows
 #ifndef HPSB_V4_UNROLL
-#define HPSB_V4_UNROLL 16
+#define HPSB_V4_UNROLL 8
 #endif
 constexpr int kV4Unroll = HPSB_V4_UNROLL;
 __host__ __device__ inline size_t v4_region(int P, int nbc, int nb) {
