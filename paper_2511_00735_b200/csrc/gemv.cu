@@ -198,7 +198,11 @@ void VPlan::finalize(cudaStream_t s) {
         worst = std::max(worst, b);
       }
     }
-    ph.stage = worst <= limit ? worst : 0;
+    // Staging serialises each CTA's load and compute and (at up to 96 KB a
+    // CTA) caps residency at ~2 CTAs/SM: it pays for latency-bound phases of
+    // a few MB, not for streaming phases (ncu, cfg3: staged 47 MB phases ran
+    // at 1.7-2.1 TB/s, streamed ones at 2.3-4.7).
+    ph.stage = (worst <= limit && ph.bytes <= 16e6) ? worst : 0;
   }
   d_items.upload(items, s);
   d_units.upload(units, s);
