@@ -74,6 +74,14 @@ struct Precond {
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
   std::vector<std::unique_ptr<SubtreeLevels>> subtrees;
   std::vector<int> small_level_of;  // level -> smalls index (-1: none)
+  // fused-operator levels: per level, the folded down / up operators of every
+  // merge, their index lists and the plan items that apply them
+  struct FusedOps {
+    DevBuf<double2> K;
+    DevBuf<int> idx;
+    std::vector<VItem> down, up;
+  };
+  std::vector<std::unique_ptr<FusedOps>> fused;
   // gamma > 1: level systems M_l on faces >= first_face(l) (global indices),
   // and per-level saved residual / accumulated correction
   std::vector<VPlan> level_mv;  // [l], l = 2..depth
@@ -246,36 +254,48 @@ __global__ void __launch_bounds__(kGemvThreads) coarse_fused_kernel(
 // gmres_fixed_steps on a small coarse system, fully on-chip in ONE cluster
 // launch (used when every CTA's rows of the coarse box maps fit in shared
 // memory).  Each of the C CTAs
-//   - stages its row slice of every coarse box map (and the index maps) in
-//     shared memory once, before the PDL wait; the ci matvecs reuse it;
-//   - owns a contiguous slice of the Krylov vectors (kept in shared memory);
-//   - gathers the full v_j from its peers' slices through DSMEM for the
-//     matvec and scatters each product row to the owner of its output index
-//     (remote shared-memory store), so the product lands slice-wise;
-//   - runs MGS with DSMEM reductions (two alternating partial slots) and
-//     keeps the Hessenberg / Givens state redundantly (identical in all CTAs).
+//   - stages its row slice of every coarse box map (column-major) and the
+//     index maps in shared memory once, before the PDL wait; the ci matvecs
+//     reuse them;
+//   - owns a contiguous slice (<= one row per thread) of the Krylov vectors
+//     and keeps a full copy of the current basis vector, which every CTA
+//     fills by pushing its new slice into all peers (DSMEM stores);
+//   - scatters each product row to the owner of its output index (remote
+//     store), so w lands slice-wise.
+// Orthogonalisation is classical Gram-Schmidt: the j+1 projections of a step
+// reduce together, so a step costs four cluster barriers instead of one per
+// basis vector (MGS, krylov.cpp:98-101, equal in exact arithmetic; the
+// parity tests bound the difference).  Partial sums are pushed to every peer
+// and summed in rank order, so all CTAs hold identical Hessenberg / Givens
+// state without a broadcast.
 constexpr int kCoarseCThreads = 256;
 constexpr int kCoarseClusterItems = 8;
+constexpr int kCoarseMaxCluster = 16;
 __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
     const VItem* __restrict__ gitems, int nitems, int n, int slice, int ci, int max_cols,
     size_t stage_elems, const double2* rd, double2* outd) {
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), crank = static_cast<int>(cl.block_rank());
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kWarps = kCoarseCThreads / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2* vfull = reinterpret_cast<double2*>(smem_raw);   // n
+  double2* vfull = reinterpret_cast<double2*>(smem_raw);   // n: current basis vector (full)
   double2* Vs = vfull + n;                                  // (ci+1) x slice
   double2* ws = Vs + static_cast<size_t>(ci + 1) * slice;   // slice
   double2* xs = ws + slice;                                 // max_cols
-  double2* As = xs + max_cols;                              // staged rows
+  double2* As = xs + max_cols;                              // staged rows, column-major
   int* Ix = reinterpret_cast<int*>(As + stage_elems);       // staged gather / scatter indices
   __shared__ double2 red[kCoarseCThreads];
-  __shared__ double2 part[2];
+  __shared__ double2 wred[kWarps][kMaxCoarseIters + 1];
+  __shared__ double2 part[kCoarseMaxCluster][kMaxCoarseIters + 1];  // pushed by rank
+  __shared__ double pnorm[kCoarseMaxCluster];
+  __shared__ double2 hsum[kMaxCoarseIters + 1];
   __shared__ VItem items[kCoarseClusterItems];  // item descriptors read once
   __shared__ double2 Hs[(kMaxCoarseIters + 1) * kMaxCoarseIters];
   __shared__ double2 gs[kMaxCoarseIters + 1], rs[kMaxCoarseIters], ys[kMaxCoarseIters];
   __shared__ double rcs[kMaxCoarseIters];
   const int s0 = min(n, crank * slice), s1 = min(n, s0 + slice), ns = s1 - s0;
+  const bool own = tid < ns;  // this thread's row of the slice
   const int ldh = ci + 1;
   pdl_trigger();
   {
@@ -291,9 +311,8 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       const VItem I = items[it];
       const int chunk = cluster_chunk(I.rows, C);
       const int rb = min(I.rows, crank * chunk), nr = max(0, min(I.rows, rb + chunk) - rb);
-      // row-major [nr][cols]: a warp reads a row with consecutive lanes
       for (int k = tid; k < nr * I.cols; k += kCoarseCThreads)
-        cp_async16(As + off + k, I.A + rb + (k / I.cols) + static_cast<size_t>(k % I.cols) * I.lda);
+        cp_async16(As + off + k, I.A + rb + (k % nr) + static_cast<size_t>(k / nr) * I.lda);
       off += static_cast<size_t>(nr) * I.cols;
     }
     cp_async_commit();
@@ -307,54 +326,49 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       io += I.cols + nr;
     }
   }
-  int slot = 0;
-  auto cluster_sum = [&](double2 v) {
-    v.x = warp_sum(v.x);
-    v.y = warp_sum(v.y);
-    if (lane == 0) red[warp] = v;
+  // block-reduce one value per thread, push the CTA's sum to every peer's
+  // pnorm[crank]; after the next cluster barrier all CTAs sum in rank order
+  auto push_norm = [&](double v) {
+    v = warp_sum(v);
+    if (lane == 0) red[warp].x = v;
     __syncthreads();
-    if (tid == 0) {
-      double2 t = make_double2(0.0, 0.0);
-      for (int q = 0; q < kCoarseCThreads / 32; ++q) t = cadd(t, red[q]);
-      part[slot] = t;
+    if (tid < C) {
+      double t = 0.0;
+      for (int q = 0; q < kWarps; ++q) t += red[q].x;
+      *cl.map_shared_rank(&pnorm[crank], tid) = t;
     }
-    cl.sync();
-    // every warp loads the C partials in parallel (one per lane) and reduces
-    // them in the same butterfly order: identical results in all CTAs
-    double2 t = lane < C ? *cl.map_shared_rank(&part[slot], lane) : make_double2(0.0, 0.0);
-    t.x = warp_sum(t.x);
-    t.y = warp_sum(t.y);
-    slot ^= 1;
+  };
+  auto sum_norm = [&]() {
+    double t = 0.0;
+    for (int q = 0; q < C; ++q) t += pnorm[q];
     return t;
   };
+  // V_j slice -> every peer's vfull
+  auto push_basis = [&](double2 v) {
+    if (own)
+      for (int q = 0; q < C; ++q) cl.map_shared_rank(vfull, q)[s0 + tid] = v;
+  };
   pdl_wait();
-  double2 loc = make_double2(0.0, 0.0);
-  for (int k = tid; k < ns; k += kCoarseCThreads) {
-    const double2 v = __ldcg(rd + s0 + k);
-    ws[k] = v;
-    loc.x += cabs2(v);
-  }
-  const double beta = sqrt(cluster_sum(loc).x);
+  double2 wv = own ? __ldcg(rd + s0 + tid) : make_double2(0.0, 0.0);
+  push_norm(cabs2(wv));
+  cp_async_wait_all();
+  cl.sync();
+  const double beta = sqrt(sum_norm());
   if (beta == 0.0) {
-    for (int k = tid; k < ns; k += kCoarseCThreads) outd[s0 + k] = make_double2(0.0, 0.0);
-    cp_async_wait_all();
+    if (own) outd[s0 + tid] = make_double2(0.0, 0.0);
     cl.sync();
     return;
   }
-  for (int k = tid; k < ns; k += kCoarseCThreads) Vs[k] = make_double2(ws[k].x / beta, ws[k].y / beta);
+  {
+    const double2 v0 = make_double2(wv.x / beta, wv.y / beta);
+    if (own) Vs[tid] = v0;
+    push_basis(v0);
+  }
   if (tid <= ci) gs[tid] = make_double2(tid == 0 ? beta : 0.0, 0.0);
-  cp_async_wait_all();
-  cl.sync();  // V_0 slices visible cluster-wide
+  cl.sync();  // vfull = V_0 in every CTA
   int jused = 0;
   for (int j = 0; j < ci; ++j) {
-    // full v_j from the peers' slices
-    for (int k = tid; k < n; k += kCoarseCThreads) {
-      const int o = k / slice;
-      vfull[k] = cl.map_shared_rank(Vs, o)[static_cast<size_t>(j) * slice + (k - o * slice)];
-    }
-    __syncthreads();
-    // w = v_j + sum_boxes scatter(T gather(v_j)): gather every item's x,
-    // then one warp per product row; rows go to the owner of their index.
+    // (A) w = v_j + sum_boxes scatter(T gather(v_j)); rows go to their owner
     {
       int io = 0, xo = 0;
       for (int it = 0; it < nitems; ++it) {
@@ -367,45 +381,56 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       }
       __syncthreads();
       size_t off = 0;
-      int row0 = 0;
       io = 0, xo = 0;
       for (int it = 0; it < nitems; ++it) {
         const VItem I = items[it];
         const int chunk = cluster_chunk(I.rows, C);
         const int rb = min(I.rows, crank * chunk), nr = max(0, min(I.rows, rb + chunk) - rb);
-        // rows of this item go to warps continuing the round robin of the previous items
-        for (int r = (warp - row0 % (kCoarseCThreads / 32) + (kCoarseCThreads / 32)) % (kCoarseCThreads / 32);
-             r < nr; r += kCoarseCThreads / 32) {
-          const double2* Ar = As + off + static_cast<size_t>(r) * I.cols;
-          double2 acc = make_double2(0.0, 0.0);
-          for (int c = lane; c < I.cols; c += 32) acc = cfma(Ar[c], xs[xo + c], acc);
-          acc.x = warp_sum(acc.x);
-          acc.y = warp_sum(acc.y);
-          if (lane == 0) {
-            const int k = Ix[io + I.cols + r];
+        for (int r0 = 0; r0 < nr; r0 += kCoarseCThreads) {
+          const int rows = min(nr - r0, kCoarseCThreads);
+          const double2 y = smem_gemv<kCoarseCThreads>(As + off + r0, nr, rows, I.cols, xs + xo, red);
+          if (tid < rows) {
+            const int k = Ix[io + I.cols + r0 + tid];
             const int o = k / slice;
-            cl.map_shared_rank(ws, o)[k - o * slice] = cadd(acc, vfull[k]);
+            cl.map_shared_rank(ws, o)[k - o * slice] = cadd(y, vfull[k]);
           }
         }
-        row0 += nr;
         off += static_cast<size_t>(nr) * I.cols;
         io += I.cols + nr;
         xo += I.cols;
       }
     }
-    cl.sync();  // w slices complete
-    for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt on the slices
-      const double2* Vi = Vs + static_cast<size_t>(i) * slice;
-      double2 d = make_double2(0.0, 0.0);
-      for (int k = tid; k < ns; k += kCoarseCThreads) d = cfma_conj(Vi[k], ws[k], d);
-      const double2 h = cluster_sum(d);
-      for (int k = tid; k < ns; k += kCoarseCThreads) ws[k] = csub(ws[k], cmul(h, Vi[k]));
-      if (tid == 0) Hs[i + j * ldh] = h;
+    cl.sync();  // (1) w slices complete
+    // (B) the j+1 projections V_i^H w, reduced together
+    wv = own ? ws[tid] : make_double2(0.0, 0.0);
+    for (int i = 0; i <= j; ++i) {
+      double2 d = own ? cmul(make_double2(Vs[i * slice + tid].x, -Vs[i * slice + tid].y), wv)
+                      : make_double2(0.0, 0.0);
+      d.x = warp_sum(d.x);
+      d.y = warp_sum(d.y);
+      if (lane == 0) wred[warp][i] = d;
     }
-    double2 nn = make_double2(0.0, 0.0);
-    for (int k = tid; k < ns; k += kCoarseCThreads) nn.x += cabs2(ws[k]);
-    const double hnext = sqrt(cluster_sum(nn).x);
+    __syncthreads();
+    if (tid <= j) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int q = 0; q < kWarps; ++q) t = cadd(t, wred[q][tid]);
+      for (int q = 0; q < C; ++q) *cl.map_shared_rank(&part[crank][tid], q) = t;
+    }
+    cl.sync();  // (2) partial projections of every CTA delivered
+    if (tid <= j) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int q = 0; q < C; ++q) t = cadd(t, part[q][tid]);
+      hsum[tid] = t;
+    }
+    __syncthreads();
+    // (C) w -= V h, ||w||^2
+    if (own)
+      for (int i = 0; i <= j; ++i) wv = csub(wv, cmul(hsum[i], Vs[i * slice + tid]));
+    push_norm(cabs2(wv));
+    cl.sync();  // (3) norm partials delivered
+    const double hnext = sqrt(sum_norm());
     if (tid == 0) {
+      for (int i = 0; i <= j; ++i) Hs[i + j * ldh] = hsum[i];
       Hs[j + 1 + j * ldh] = make_double2(hnext, 0.0);
       for (int i = 0; i < j; ++i) apply_givens(rcs[i], rs[i], Hs[i + j * ldh], Hs[i + 1 + j * ldh]);
       double c;
@@ -415,13 +440,15 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       apply_givens(c, sg, Hs[j + j * ldh], Hs[j + 1 + j * ldh]);
       apply_givens(c, sg, gs[j], gs[j + 1]);
     }
-    __syncthreads();
     jused = j + 1;
-    if (hnext <= 1e-14 * beta) break;  // happy breakdown
-    double2* Vn = Vs + static_cast<size_t>(j + 1) * slice;
-    for (int k = tid; k < ns; k += kCoarseCThreads) Vn[k] = make_double2(ws[k].x / hnext, ws[k].y / hnext);
-    cl.sync();  // V_{j+1} slices visible; w slots free for the next matvec
+    if (hnext <= 1e-14 * beta) break;  // happy breakdown (identical in all CTAs)
+    // (D) V_{j+1} = w / hnext, pushed to every peer's vfull
+    const double2 vn = make_double2(wv.x / hnext, wv.y / hnext);
+    if (own) Vs[(j + 1) * slice + tid] = vn;
+    push_basis(vn);
+    cl.sync();  // (4) vfull = V_{j+1}; w and partial slots free again
   }
+  __syncthreads();
   if (tid == 0)
     for (int i = jused - 1; i >= 0; --i) {
       double2 sum = gs[i];
@@ -429,12 +456,12 @@ __global__ void __launch_bounds__(kCoarseCThreads) coarse_cluster_kernel(
       ys[i] = cdiv(sum, Hs[i + i * ldh]);
     }
   __syncthreads();
-  for (int k = tid; k < ns; k += kCoarseCThreads) {
+  if (own) {
     double2 acc = make_double2(0.0, 0.0);
-    for (int i = 0; i < jused; ++i) acc = cfma(ys[i], Vs[static_cast<size_t>(i) * slice + k], acc);
-    outd[s0 + k] = acc;
+    for (int i = 0; i < jused; ++i) acc = cfma(ys[i], Vs[static_cast<size_t>(i) * slice + tid], acc);
+    outd[s0 + tid] = acc;
   }
-  cl.sync();  // no CTA exits while a peer may still read its shared memory
+  cl.sync();  // no CTA exits while a peer may still write its shared memory
 }
 
 bool coarse_cluster_fits(size_t smem, int csize) {
@@ -902,8 +929,102 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->clusters.push_back(std::move(cl));
     return static_cast<int>(p->clusters.size()) - 1;
   };
-  std::vector<int> small_of(cfg.depth, -1), cluster_of(cfg.depth, -1);
+  // Fused-operator levels.  The down and up chains of multigrid.cpp:47-98
+  // are linear in the level's inputs, so for latency-bound levels they are
+  // folded at setup (DMMA GEMMs) into one operator per merge and direction:
+  //   down: [x1; x2; dr_p1; dr_p2] = Kd [r1; r2],  X = [W, -W T2ss],
+  //         Y = [0, I] - T1ss X,  Kd = [X; Y; -T1ps X; -T2ps Y]
+  //         (x -> out[s], dr -> r[p] +=);
+  //   up:   [ds1; ds2] = Ku [u1; u2],  Ku_1 = [W T2ss T1sp, -W T2sp],
+  //         Ku_2 = -T1ss Ku_1 - [T1sp, 0]  (ds -> out[s] +=).
+  // A level step is then ONE launch of independent row blocks -- no chain of
+  // dependent GEMVs, no barriers -- for up to ~1.7x the chain's operator
+  // bytes.  Used where the level's folded operators are small (latency
+  // bound); HPSB_FUSED_MB sets the threshold (0 disables).
+  static const double fused_max = [] {
+    const char* e = std::getenv("HPSB_FUSED_MB");
+    return (e ? std::atof(e) : 24.0) * 1e6;
+  }();
+  auto fused_level = [&](int l) -> int {
+    const LevelOps& L = *h->levels[l - 1];
+    if (L.merges.empty() || fused_max <= 0.0) return -1;
+    size_t kn = 0, nidx = 0;
+    for (const MergeRec& mr : L.merges) {
+      const size_t s2 = 2 * static_cast<size_t>(mr.s), pp = mr.p1 + mr.p2;
+      kn += (s2 + pp) * s2 + s2 * pp;
+      nidx += s2 + 2 * pp;
+    }
+    if (16.0 * static_cast<double>(kn) > fused_max) return -1;
+    auto f = std::make_unique<Precond::FusedOps>();
+    f->K.alloc(kn);
+    f->idx.alloc(nidx);
+    std::vector<int> hidx(nidx);
+    CopyBatch c0;
+    GemmBatch g1, g2, g3;
+    size_t ko = 0, io = 0;
+    const int* hx = L.h_idx.data();
+    for (const MergeRec& mr : L.merges) {
+      const ChildBox& c1 = L.children[mr.c1];
+      const ChildBox& c2 = L.children[mr.c2];
+      const int s = mr.s, p1 = mr.p1, p2 = mr.p2, P1 = c1.P, P2 = c2.P, pp = p1 + p2;
+      const int Rd = 2 * s + pp, s2 = 2 * s;
+      const double2* T1 = L.tperm.p + c1.t_off;
+      const double2* T2 = L.tperm.p + c2.t_off;
+      const double2 *T1ps = T1 + static_cast<size_t>(p1) * P1, *T1sp = T1 + p1,
+                    *T1ss = T1 + p1 + static_cast<size_t>(p1) * P1;
+      const double2 *T2ps = T2 + static_cast<size_t>(p2) * P2, *T2sp = T2 + p2,
+                    *T2ss = T2 + p2 + static_cast<size_t>(p2) * P2;
+      const double2* W = L.w.p + mr.w_off;
+      double2* Kd = f->K.p + ko;
+      double2* Ku = Kd + static_cast<size_t>(Rd) * s2;
+      ko += static_cast<size_t>(Rd) * s2 + static_cast<size_t>(s2) * pp;
+      // index lists: [in1s; in2s], [out1p; out2p], [in1p; in2p]
+      int* hs = hidx.data() + io;
+      int* hpo = hs + s2;
+      int* hpi = hpo + pp;
+      for (int i = 0; i < s; ++i) hs[i] = hx[mr.in1_sep + i], hs[s + i] = hx[mr.in2_sep + i];
+      for (int i = 0; i < p1; ++i) hpo[i] = hx[mr.out1_per + i], hpi[i] = hx[mr.in1_per + i];
+      for (int i = 0; i < p2; ++i) hpo[p1 + i] = hx[mr.out2_per + i], hpi[p1 + i] = hx[mr.in2_per + i];
+      const int* ds = f->idx.p + io;
+      const int* dpo = ds + s2;
+      const int* dpi = dpo + pp;
+      io += s2 + 2 * static_cast<size_t>(pp);
+      // round 0: X_1 = W, Y = [0, I], Ku_2 = [-T1sp, 0]
+      c0.copy(W, s, Kd, Rd, s, s, 1.0);
+      c0.zero(Kd + s, Rd, s, s);
+      c0.identity(Kd + s + static_cast<size_t>(s) * Rd, Rd, s);
+      if (p1) c0.copy(T1sp, P1, Ku + s, s2, s, p1, -1.0);
+      if (p2) c0.zero(Ku + s + static_cast<size_t>(p1) * s2, s2, s, p2);
+      // round 1: X_2 = -W T2ss
+      g1.add(W, s, T2ss, P2, Kd + static_cast<size_t>(s) * Rd, Rd, s, s, s, -1.0, 0.0);
+      // round 2: Y -= T1ss X, -T1ps X, Ku_1
+      g2.add(T1ss, P1, Kd, Rd, Kd + s, Rd, s, s2, s, -1.0, 1.0);
+      if (p1) {
+        g2.add(T1ps, P1, Kd, Rd, Kd + s2, Rd, p1, s2, s, -1.0, 0.0);
+        g2.add(Kd + static_cast<size_t>(s) * Rd, Rd, T1sp, P1, Ku, s2, s, p1, s, -1.0, 0.0);
+      }
+      if (p2) g2.add(W, s, T2sp, P2, Ku + static_cast<size_t>(p1) * s2, s2, s, p2, s, -1.0, 0.0);
+      // round 3: -T2ps Y, Ku_2 -= T1ss Ku_1
+      if (p2) g3.add(T2ps, P2, Kd + s, Rd, Kd + s2 + p1, Rd, p2, s2, s, -1.0, 0.0);
+      if (pp) g3.add(T1ss, P1, Ku, s2, Ku + s, s2, s, pp, s, -1.0, 1.0);
+      f->down.push_back(item(Kd, Rd, s2, s2, r, ds, nullptr, nullptr, out, ds, 1.0, 0.0, 0.0));
+      if (pp) {
+        f->down.push_back(item(Kd + s2, Rd, pp, s2, r, ds, nullptr, nullptr, r, dpo, 1.0, 1.0, 0.0));
+        f->up.push_back(item(Ku, s2, s2, pp, out, dpi, nullptr, nullptr, out, ds, 1.0, 1.0, 0.0));
+      }
+    }
+    f->idx.upload(hidx, ctx->stream);
+    c0.run(ctx);
+    g1.run(ctx);
+    g2.run(ctx);
+    g3.run(ctx);
+    p->fused.push_back(std::move(f));
+    return static_cast<int>(p->fused.size()) - 1;
+  };
+  std::vector<int> small_of(cfg.depth, -1), cluster_of(cfg.depth, -1), fused_of(cfg.depth, -1);
   for (int l = 1; l < cfg.depth; ++l) {
+    fused_of[l] = fused_level(l);
+    if (fused_of[l] >= 0) continue;
     small_of[l] = small_level(l);
     if (small_of[l] < 0) cluster_of[l] = cluster_level(l);
   }
@@ -913,7 +1034,23 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     st.level = l;
     st.small = small_of[l];
     st.cluster = cluster_of[l];
-    if (st.cluster >= 0) {
+    if (fused_of[l] >= 0) {
+      const bool global_level = l > h->sk->el->part.last_local;
+      VPlan& plan =
+          downward ? (global_level ? p->down_g : p->down) : (global_level ? p->up_g : p->up);
+      st.plan = &plan;
+      st.p0 = static_cast<int>(plan.phases.size());
+      const std::vector<VItem>& its = downward ? p->fused[fused_of[l]]->down : p->fused[fused_of[l]]->up;
+      if (!its.empty()) {
+        plan.phases[plan.begin_phase()].label =
+            std::string(downward ? "vcycle_down" : "vcycle_up") +
+            (std::getenv("HPSB_PROFILE_LEVELS") ? "_fused_L" + std::to_string(l) : "");
+        int rows = 0;
+        for (const VItem& it : its) rows += it.rows;
+        for (const VItem& it : its) plan.add_split(it, split_rows(rows, sms));
+      }
+      st.p1 = static_cast<int>(plan.phases.size());
+    } else if (st.cluster >= 0) {
       p->bytes_small += downward ? p->clusters[st.cluster]->bytes_down : p->clusters[st.cluster]->bytes_up;
     } else if (st.small < 0) {
       const bool global_level = l > h->sk->el->part.last_local;
@@ -1078,31 +1215,39 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       p->coarse_csize *= 2;
     p->coarse_items.upload(whole, ctx->stream);
     p->coarse_nitems = static_cast<int>(whole.size());
-    // On-chip variant: a 16-CTA cluster holding its rows of the coarse maps.
+    // On-chip variant: a cluster of 16 CTAs (else 8, 4, 2) whose CTAs hold
+    // their rows of the coarse maps in shared memory.  The largest cluster
+    // wins: each CTA's staging burst is on the critical path when the
+    // previous kernel's CTAs still occupy the SMs (cfg1: 16 CTAs 116 us per
+    // apply, 4 CTAs 149 us).  HPSB_COARSE_CSIZE forces a size.
     {
-      const int Cc = 16;
-      size_t stage = 0;
-      for (const VItem& it : whole)
-        stage += static_cast<size_t>(std::min(it.rows, cluster_chunk(it.rows, Cc))) * it.cols;
-      const int slice = static_cast<int>((p->dim_d + Cc - 1) / Cc);
-      size_t nidx = 0, xs_total = 0;
-      for (const VItem& it : whole) {
-        nidx += it.cols + std::min(it.rows, cluster_chunk(it.rows, Cc));
-        xs_total += it.cols;
-      }
-      p->coarse_xs = static_cast<int>(xs_total);
-      const size_t smem = sizeof(double2) * (static_cast<size_t>(p->dim_d) +
-                                             static_cast<size_t>(ci + 2) * slice +
-                                             xs_total + stage) +
-                          sizeof(int) * nidx;
-      p->coarse_stage = stage;
-      if (p->coarse_fused && smem <= (200u << 10) && !std::getenv("HPSB_NO_COARSE_CLUSTER") &&
-          whole.size() <= static_cast<size_t>(kCoarseClusterItems) &&
-          coarse_cluster_fits(smem, Cc)) {
-        p->coarse_cluster = true;
-        p->coarse_slice = slice;
-        p->coarse_smem = smem;
-        p->coarse_csize = Cc;
+      const char* force = std::getenv("HPSB_COARSE_CSIZE");
+      for (int Cc = kCoarseMaxCluster; Cc >= 2 && !p->coarse_cluster; Cc /= 2) {
+        if (force && std::atoi(force) != Cc) continue;
+        size_t stage = 0;
+        for (const VItem& it : whole)
+          stage += static_cast<size_t>(std::min(it.rows, cluster_chunk(it.rows, Cc))) * it.cols;
+        const int slice = static_cast<int>((p->dim_d + Cc - 1) / Cc);
+        size_t nidx = 0, xs_total = 0;
+        for (const VItem& it : whole) {
+          nidx += it.cols + std::min(it.rows, cluster_chunk(it.rows, Cc));
+          xs_total += it.cols;
+        }
+        const size_t smem = sizeof(double2) * (static_cast<size_t>(p->dim_d) +
+                                               static_cast<size_t>(ci + 2) * slice +
+                                               xs_total + stage) +
+                            sizeof(int) * nidx;
+        if (p->coarse_fused && smem <= (200u << 10) && slice <= kCoarseCThreads &&
+            !std::getenv("HPSB_NO_COARSE_CLUSTER") &&
+            whole.size() <= static_cast<size_t>(kCoarseClusterItems) &&
+            coarse_cluster_fits(smem, Cc)) {
+          p->coarse_cluster = true;
+          p->coarse_xs = static_cast<int>(xs_total);
+          p->coarse_stage = stage;
+          p->coarse_slice = slice;
+          p->coarse_smem = smem;
+          p->coarse_csize = Cc;
+        }
       }
     }
   }
