@@ -34,10 +34,12 @@ __host__ __device__ __forceinline__ double2 cfma_conj(double2 a, double2 b, doub
 __host__ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
 __device__ __forceinline__ double2 cinv(double2 a) {
   // 1 / a with scaling against overflow (|a| spans many decades in pivots).
+  // (two divisions: 1/s and (1/s)/|a/s|^2)
   const double s = fmax(fabs(a.x), fabs(a.y));
-  const double ar = a.x / s, ai = a.y / s;
-  const double d = ar * ar + ai * ai;
-  return make_double2(ar / (d * s), -ai / (d * s));
+  const double rs = 1.0 / s;
+  const double ar = a.x * rs, ai = a.y * rs;
+  const double t = rs / (ar * ar + ai * ai);
+  return make_double2(ar * t, -ai * t);
 }
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) { return cmul(a, cinv(b)); }
 

@@ -1,0 +1,613 @@
+// K1 element_iti, v5: the element stage as a batched blocked Cholesky.
+//
+// Same mathematics as the other element kernels (element.cu header; SURVEY.md
+// Appendix B.1): per element the real SPD interior block L_ii (ni x ni, padded
+// with identity to P, a multiple of 16) is factored, L_ii = L L^T, the nb + 2
+// right-hand sides [L_iG | re b~ | im b~] are solved, and the boundary Schur
+// complement / ItI epilogue follows (iti_epilogue, element_common.cuh).
+//
+// Instead of one CTA walking one element through a long chain of dependent
+// steps (v4: 16-wide panels, operands streamed from L2 with ~2 M issued
+// instructions per element), the factorisation is split into 64-wide block
+// columns and every step runs as ONE launch over a whole chunk of elements:
+//   assemble   L_ii and the right-hand sides B into the chunk workspace;
+//   for k = 0 .. nblk-1 (left-looking, Crout order):
+//     update   A[i,k] -= sum_{j<k} L[i,j] L[k,j]^T  for i >= k, and
+//              B[k,:] -= sum_{j<k} L[k,j] Y[j,:]      (tiles of 64 x 64, K = 64k)
+//     panel    one CTA per element: L[k,k] = chol(A[k,k]), Linv_k = L[k,k]^{-1},
+//              L[i,k] = A[i,k] Linv_k^T (i > k), Y[k,:] = Linv_k B[k,:]
+//   for k = nblk-1 .. 0 (backward solve L^T X = Y):
+//     back     X[k,:] = Linv_k^T (Y[k,:] - sum_{j>k} L[j,k]^T X[j,:])
+//   epilogue   one CTA per element: S = L_GG - L_Gi X, T, H (complex GJ inverse)
+// All O(ni^3) and O(ni^2 nb) work is 64 x 64 DMMA tiles (mma.sync m8n8k4 f64)
+// fed from shared memory by a 3-stage cp.async pipeline; a launch holds
+// (elements x tiles) CTAs, so the SMs stay full with no serial step inside a
+// CTA except the 64 x 64 diagonal factorisations.  The chunk workspace
+// (A: P x P, B: P x nbc, Linv: nblk 64 x 64 blocks per element) is bounded
+// by a memory budget; elements run in chunks.
+#include <algorithm>
+#include <cstdlib>
+
+#include "element_common.cuh"
+#include "vcycle_device.cuh"
+#include "gj_reg.cuh"
+
+namespace hpsb {
+
+namespace {
+
+constexpr int V5B = 64;                 // block size of the factorisation
+constexpr int V5T = 128;                // threads of the tile / panel kernels (4 warps, 2 x 2)
+constexpr int V5K = 16;                 // k depth of one pipeline stage
+constexpr int V5S = 3;                  // pipeline stages
+constexpr int LDM = V5B + 4;            // [k][m] staging stride (m contiguous)
+constexpr int LDK = V5K + 4;            // [m][k] staging stride (k contiguous)
+constexpr int V5STAGE = V5B * LDK;      // doubles per operand per stage (>= V5K * LDM)
+constexpr int V5_TILE_SMEM = 2 * V5S * V5STAGE;  // doubles
+constexpr int LDD = V5B + 1;            // diagonal block stride in the panel kernel
+static_assert(V5STAGE >= V5K * LDM, "stage size");
+
+struct V5Args {
+  ElemArgs a;
+  int base;        // chunk start in the work list
+  int count;       // elements in the chunk
+  double* A;       // [c][P x P]
+  double* B;       // [c][P x nbc]
+  double* Linv;    // [c][nblk][64 x 64]
+  size_t sA, sB, sL;
+  int P, nbc, nblk, k;
+};
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ int v5_elem(const V5Args& v, int c) {
+  return v.a.elist ? v.a.elist[v.base + c] : v.base + c;
+}
+
+__device__ __forceinline__ void dmma5(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// acc = op1 (M x K) * op2 (K x N) for one tile of at most 64 x 64, K a
+// multiple of 16.  Operand layouts (template):
+//   A_KC = false: op1(m, k) = op1[m + k * ld1]   (column-major slice)
+//   A_KC = true : op1(m, k) = op1[k + m * ld1]   (transposed access)
+//   B_KC = false: op2(k, n) = op2[n + k * ld2]   (transposed access)
+//   B_KC = true : op2(k, n) = op2[k + n * ld2]   (column-major slice)
+// Warp w owns rows 32 (w & 1) .. +32 and columns 32 (w >> 1) .. +32 as 4 x 4
+// DMMA fragments; acc[i][j][h] = C[32 wm + 8 i + g][32 wn + 8 j + 2 t4 + h].
+// Every pointer and leading dimension must keep 16-byte alignment of
+// 2-element runs.  Ends with a CTA barrier (the staging buffers are free).
+template <bool A_KC, bool B_KC>
+__device__ __forceinline__ void tile_mma(const double* __restrict__ op1, int ld1,
+                                         const double* __restrict__ op2, int ld2, int M, int N,
+                                         int K, double (&acc)[4][4][2], double* smem) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double* As = smem;
+  double* Bs = smem + V5S * V5STAGE;
+  const int ksteps = K / V5K;
+  auto load = [&](int ks, int st) {
+    const int k0 = ks * V5K;
+    double* as = As + st * V5STAGE;
+    double* bs = Bs + st * V5STAGE;
+#pragma unroll
+    for (int r = 0; r < (V5B * V5K / 2) / V5T; ++r) {
+      const int idx = tid + r * V5T;
+      if (!A_KC) {
+        const int m2 = idx % (V5B / 2), kk = idx / (V5B / 2);
+        const bool ok = 2 * m2 < M;
+        cp_async16_zfill(as + kk * LDM + 2 * m2, ok ? op1 + 2 * m2 + static_cast<size_t>(k0 + kk) * ld1 : op1, ok);
+      } else {
+        const int c2 = idx % (V5K / 2), m = idx / (V5K / 2);
+        const bool ok = m < M;
+        cp_async16_zfill(as + m * LDK + 2 * c2, ok ? op1 + k0 + 2 * c2 + static_cast<size_t>(m) * ld1 : op1, ok);
+      }
+      if (!B_KC) {
+        const int n2 = idx % (V5B / 2), kk = idx / (V5B / 2);
+        const bool ok = 2 * n2 < N;
+        cp_async16_zfill(bs + kk * LDM + 2 * n2, ok ? op2 + 2 * n2 + static_cast<size_t>(k0 + kk) * ld2 : op2, ok);
+      } else {
+        const int c2 = idx % (V5K / 2), n = idx / (V5K / 2);
+        const bool ok = n < N;
+        cp_async16_zfill(bs + n * LDK + 2 * c2, ok ? op2 + k0 + 2 * c2 + static_cast<size_t>(n) * ld2 : op2, ok);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < V5S - 1; ++s) {
+    if (s < ksteps) load(s, s);
+    cp_async_commit();
+  }
+  for (int ks = 0; ks < ksteps; ++ks) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(V5S - 2));
+    __syncthreads();
+    if (ks + V5S - 1 < ksteps) load(ks + V5S - 1, (ks + V5S - 1) % V5S);
+    cp_async_commit();
+    const double* as = As + (ks % V5S) * V5STAGE;
+    const double* bs = Bs + (ks % V5S) * V5STAGE;
+#pragma unroll
+    for (int kk = 0; kk < V5K; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int row = 32 * wm + 8 * i + g;
+        af[i] = A_KC ? as[row * LDK + kk + t4] : as[(kk + t4) * LDM + row];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int col = 32 * wn + 8 * j + g;
+        bf[j] = B_KC ? bs[col * LDK + kk + t4] : bs[(kk + t4) * LDM + col];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma5(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+// C (column-major, ldc) = beta * C + alpha * acc over the tile's M x N part.
+__device__ __forceinline__ void tile_store(double* C, int ldc, int M, int N, const double (&acc)[4][4][2],
+                                           double alpha, bool accumulate) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 1, wn = warp >> 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = 32 * wm + 8 * i + g;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 32 * wn + 8 * j + 2 * t4 + h;
+        if (col >= N) continue;
+        double* c = C + row + static_cast<size_t>(col) * ldc;
+        *c = accumulate ? *c + alpha * acc[i][j][h] : alpha * acc[i][j][h];
+      }
+  }
+}
+
+// ---- assemble: A = L_ii (lower triangle incl. diagonal blocks; identity
+// padding), B = [L_iG | b~].  Only the lower triangle is ever read.
+__global__ void __launch_bounds__(256) v5_assemble_kernel(V5Args v) {
+  const ElemArgs& a = v.a;
+  const int c = blockIdx.x, e = v5_elem(v, c);
+  const int m = a.m, ni = a.ni, nb = a.nb, np = a.order + 1, N = a.order, P = v.P, nbc = v.nbc;
+  extern __shared__ __align__(16) double smem5[];
+  double* mass = smem5;       // np
+  double* Ks = mass + np;     // np x np
+  double* cm = Ks + np * np;  // ni: c * mass_i * mass_j at the interior nodes
+  for (int i = threadIdx.x; i < np; i += blockDim.x) mass[i] = a.mass[i];
+  for (int i = threadIdx.x; i < np * np; i += blockDim.x) Ks[i] = a.stiff[i];
+  __syncthreads();
+  const double* ce = a.coeff + static_cast<size_t>(e) * np * np;
+  for (int q = threadIdx.x; q < ni; q += blockDim.x) {
+    const int i = q / m + 1, j = q % m + 1;
+    cm[q] = __ldg(ce + i * np + j) * mass[i] * mass[j];
+  }
+  __syncthreads();
+  double* A = v.A + c * v.sA;
+  double* B = v.B + c * v.sB;
+  // column col: rows from the top of its diagonal block (the diagonal tile is read whole)
+  for (int col = threadIdx.x >> 5; col < P; col += blockDim.x >> 5) {
+    const int r0 = col / V5B * V5B;
+    const int k = col / m + 1, l = col % m + 1;
+    double* Ac = A + static_cast<size_t>(col) * P;
+    for (int r = r0 + (threadIdx.x & 31); r < P; r += 32) {
+      double val;
+      if (r >= ni || col >= ni) {
+        val = (r == col) ? 1.0 : 0.0;
+      } else {
+        const int i = r / m + 1, j = r - (i - 1) * m + 1;
+        val = 0.0;
+        if (j == l) val += Ks[i + k * np] * mass[j];
+        if (i == k) val += mass[i] * Ks[j + l * np];
+        if (r == col) val -= cm[r];
+      }
+      Ac[r] = val;
+    }
+  }
+  for (int idx = threadIdx.x; idx < P * nbc; idx += blockDim.x) {
+    const int q = idx % P, b = idx / P;
+    double val = 0.0;
+    if (q < ni && b < nb + 2) {
+      const int i = q / m + 1, j = q % m + 1;
+      if (b < nb) {
+        const int side = b / m, t = b % m + 1;
+        switch (side) {
+          case 0: val = (j == t) ? Ks[i + 0 * np] * mass[j] : 0.0; break;
+          case 1: val = (j == t) ? Ks[i + N * np] * mass[j] : 0.0; break;
+          case 2: val = (i == t) ? mass[i] * Ks[j + 0 * np] : 0.0; break;
+          default: val = (i == t) ? mass[i] * Ks[j + N * np] : 0.0; break;
+        }
+      } else if (a.source) {
+        const double2 sv = a.source[static_cast<size_t>(e) * ni + q];
+        const double w = mass[i] * mass[j];
+        val = (b == nb) ? sv.x * w : sv.y * w;
+      }
+    }
+    B[idx] = val;
+  }
+}
+
+// ---- update (left-looking): tiles of block column k and of block row k of B
+__global__ void __launch_bounds__(V5T, 3) v5_update_kernel(V5Args v) {
+  extern __shared__ __align__(16) double smem5[];
+  const int P = v.P, k = v.k, nA = v.nblk - k, nBt = (v.nbc + V5B - 1) / V5B;
+  const int c = blockIdx.x / (nA + nBt), t = blockIdx.x % (nA + nBt);
+  const int e = v5_elem(v, c);
+  if (v.a.status[e] & 4) return;
+  double* A = v.A + c * v.sA;
+  double* B = v.B + c * v.sB;
+  const int bk = min(V5B, P - V5B * k), K = V5B * k;
+  double acc[4][4][2];
+  if (t < nA) {
+    const int r0 = V5B * (k + t), M = min(V5B, P - r0);
+    tile_mma<false, false>(A + r0, P, A + V5B * k, P, M, bk, K, acc, smem5);
+    tile_store(A + r0 + static_cast<size_t>(V5B * k) * P, P, M, bk, acc, -1.0, true);
+  } else {
+    const int c0 = V5B * (t - nA), N = min(V5B, v.nbc - c0);
+    tile_mma<false, true>(A + V5B * k, P, B + static_cast<size_t>(c0) * P, P, bk, N, K, acc, smem5);
+    tile_store(B + V5B * k + static_cast<size_t>(c0) * P, P, bk, N, acc, -1.0, true);
+  }
+}
+
+// ---- diag: L[k,k] = chol(A[k,k]) and Linv_k = L[k,k]^{-1}, one warp per
+// element (the 64-step chains are latency bound: no CTA barriers, six
+// elements resident per SM)
+__global__ void __launch_bounds__(32) v5_diag_kernel(V5Args v) {
+  extern __shared__ __align__(16) double smem5[];
+  const int P = v.P, k = v.k, c = blockIdx.x, e = v5_elem(v, c), lane = threadIdx.x;
+  if (v.a.status[e] & 4) return;
+  const double* A = v.A + c * v.sA;
+  double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;  // ld 64
+  const int k0 = V5B * k, bk = min(V5B, P - k0);
+  double* D = smem5;  // [bk][LDD] column-major, factored and inverted in place
+  double* rdiag = smem5 + V5B * LDD;
+  // load the lower triangle: 8 independent global loads in flight per lane
+  // (__ldg: the global-space loads may pass the shared stores)
+  for (int col0 = 0; col0 < bk; col0 += 4) {
+    double t[4][2];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = col0 + u, r = lane + 32 * h;
+        t[u][h] = (col < bk && r < bk && r >= col) ? __ldg(A + k0 + r + static_cast<size_t>(k0 + col) * P) : 0.0;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = col0 + u, r = lane + 32 * h;
+        if (col < bk && r < bk && r >= col) D[r + col * LDD] = t[u][h];
+      }
+  }
+  __syncwarp();
+  // left-looking Cholesky: column j = A[:, j] - L[:, :j] L[j, :j]^T, lanes
+  // over rows (no read-modify-write chains in shared memory: the dot
+  // products' loads are independent and pipeline)
+  for (int j = 0; j < bk; ++j) {
+    const int r0 = j + lane, r1 = r0 + 32;
+    double s0 = r0 < bk ? D[r0 + j * LDD] : 0.0, s1 = r1 < bk ? D[r1 + j * LDD] : 0.0;
+    double u0 = 0.0, u1 = 0.0;
+    int q = 0;
+    for (; q + 1 < j; q += 2) {
+      const double a0 = D[j + q * LDD], a1 = D[j + (q + 1) * LDD];
+      if (r0 < bk) s0 -= D[r0 + q * LDD] * a0, u0 -= D[r0 + (q + 1) * LDD] * a1;
+      if (r1 < bk) s1 -= D[r1 + q * LDD] * a0, u1 -= D[r1 + (q + 1) * LDD] * a1;
+    }
+    if (q < j) {
+      const double a0 = D[j + q * LDD];
+      if (r0 < bk) s0 -= D[r0 + q * LDD] * a0;
+      if (r1 < bk) s1 -= D[r1 + q * LDD] * a0;
+    }
+    s0 += u0, s1 += u1;
+    const double d = __shfl_sync(0xffffffffu, s0, 0);  // row j is lane 0's r0
+    if (!(d > 0.0)) {
+      if (lane == 0) atomicOr(v.a.status + e, 4);  // indefinite: pivoted-LU fallback (v1)
+      return;
+    }
+    const double sq = sqrt(d), rs = 1.0 / sq;
+    __syncwarp();
+    if (r0 < bk) D[r0 + j * LDD] = (lane == 0) ? sq : s0 * rs;
+    if (r1 < bk) D[r1 + j * LDD] = s1 * rs;
+    if (lane == 0) rdiag[j] = rs;
+    __syncwarp();
+  }
+  // in-place inverse, row by row: X[i][j] = -X[i][i] sum_{q=j}^{i-1} L[i][q] X[q][j]
+  // (the diagonal becomes X's first; rows of L below i are still intact)
+  for (int r = lane; r < bk; r += 32) D[r + r * LDD] = rdiag[r];
+  __syncwarp();
+  for (int i = 1; i < bk; ++i) {
+    const int j0 = lane, j1 = lane + 32;
+    double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
+    if (j0 < i) {
+      int q = j0;
+      for (; q + 1 < i; q += 2) {
+        s0 += D[i + q * LDD] * D[q + j0 * LDD];
+        t0 += D[i + (q + 1) * LDD] * D[q + 1 + j0 * LDD];
+      }
+      if (q < i) s0 += D[i + q * LDD] * D[q + j0 * LDD];
+    }
+    if (j1 < i) {
+      int q = j1;
+      for (; q + 1 < i; q += 2) {
+        s1 += D[i + q * LDD] * D[q + j1 * LDD];
+        t1 += D[i + (q + 1) * LDD] * D[q + 1 + j1 * LDD];
+      }
+      if (q < i) s1 += D[i + q * LDD] * D[q + j1 * LDD];
+    }
+    __syncwarp();
+    const double ri = rdiag[i];
+    if (j0 < i) D[i + j0 * LDD] = -ri * (s0 + t0);
+    if (j1 < i) D[i + j1 * LDD] = -ri * (s1 + t1);
+    __syncwarp();
+  }
+  // diagonal of the inverse and write-out (full 64 x 64 block, zero upper part)
+  for (int col = 0; col < bk; ++col)
+    for (int r = lane; r < bk; r += 32)
+      Lg[r + col * V5B] = r >= col ? D[r + col * LDD] : 0.0;
+}
+
+// ---- trsm: L[i,k] = A[i,k] Linv_k^T (i > k) and Y[k,:] = Linv_k B[k,:], one tile per CTA
+__global__ void __launch_bounds__(V5T, 3) v5_trsm_kernel(V5Args v) {
+  extern __shared__ __align__(16) double smem5[];
+  const int P = v.P, k = v.k, k0 = V5B * k, bk = min(V5B, P - k0);
+  const int nA = v.nblk - k - 1, nBt = (v.nbc + V5B - 1) / V5B;
+  const int c = blockIdx.x / (nA + nBt), t = blockIdx.x % (nA + nBt);
+  const int e = v5_elem(v, c);
+  if (v.a.status[e] & 4) return;
+  double* A = v.A + c * v.sA;
+  double* B = v.B + c * v.sB;
+  const double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;
+  double acc[4][4][2];
+  if (t < nA) {
+    const int r0 = k0 + bk + V5B * t, M = min(V5B, P - r0);
+    double* Ci = A + r0 + static_cast<size_t>(k0) * P;
+    tile_mma<false, false>(Ci, P, Lg, V5B, M, bk, bk, acc, smem5);
+    tile_store(Ci, P, M, bk, acc, 1.0, false);
+  } else {
+    const int c0 = V5B * (t - nA), N = min(V5B, v.nbc - c0);
+    double* Ck = B + k0 + static_cast<size_t>(c0) * P;
+    tile_mma<false, true>(Lg, V5B, Ck, P, bk, N, bk, acc, smem5);
+    tile_store(Ck, P, bk, N, acc, 1.0, false);
+  }
+}
+
+// ---- backward: X[k,:] = Linv_k^T (Y[k,:] - sum_{j>k} L[j,k]^T X[j,:]), one column tile per CTA
+__global__ void __launch_bounds__(V5T, 3) v5_back_kernel(V5Args v) {
+  extern __shared__ __align__(16) double smem5[];
+  const int P = v.P, k = v.k, nBt = (v.nbc + V5B - 1) / V5B;
+  const int c = blockIdx.x / nBt, c0 = V5B * (blockIdx.x % nBt), e = v5_elem(v, c);
+  if (v.a.status[e] & 4) return;
+  double* A = v.A + c * v.sA;
+  double* B = v.B + c * v.sB;
+  const double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;
+  const int k0 = V5B * k, bk = min(V5B, P - k0), N = min(V5B, v.nbc - c0), kb = k0 + bk;
+  double* Ck = B + k0 + static_cast<size_t>(c0) * P;
+  double acc[4][4][2];
+  if (kb < P) {
+    tile_mma<true, true>(A + kb + static_cast<size_t>(k0) * P, P, B + kb + static_cast<size_t>(c0) * P, P,
+                         bk, N, P - kb, acc, smem5);
+    tile_store(Ck, P, bk, N, acc, -1.0, true);
+    __threadfence_block();
+    __syncthreads();
+  }
+  tile_mma<true, true>(Lg, V5B, Ck, P, bk, N, bk, acc, smem5);
+  tile_store(Ck, P, bk, N, acc, 1.0, false);
+}
+
+// ---- schur: S = L_GG - L_Gi X (+ i eta I), f = L_Gi x_b, and the recovery
+// copy Y[e] = X[:ni, :nb+2].  L_Gi has N-1 entries per row (the normal
+// derivative along the row's grid line), so this is a gather-contraction of
+// each solution column staged in shared memory (one warp per column).
+constexpr int V5ST = 256;
+__global__ void __launch_bounds__(V5ST) v5_schur_kernel(V5Args v, double2* Sw, double* fw) {
+  extern __shared__ __align__(16) double smem5[];
+  const ElemArgs& a = v.a;
+  const int c = blockIdx.x, e = v5_elem(v, c);
+  if (a.status[e] & 4) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = V5ST / 32;
+  const int m = a.m, ni = a.ni, nb = a.nb, np = a.order + 1, N = a.order, P = v.P;
+  __shared__ double d0[64], dN[64];  // D(0, k), D(N, k)
+  for (int i = tid; i < np; i += V5ST) d0[i] = a.diff[0 + i * np], dN[i] = a.diff[N + i * np];
+  __syncthreads();
+  const double* X = v.B + c * v.sB;
+  double* xs = smem5 + warp * P;
+  double* Ye = a.Y + static_cast<size_t>(e) * ni * (nb + 2);
+  double2* S = Sw + static_cast<size_t>(c) * nb * nb;
+  for (int col = warp; col < nb + 2; col += kW) {
+    for (int q0 = 0; q0 < ni; q0 += 128) {
+      double t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + 32 * u + lane;
+        t[u] = q < ni ? __ldg(X + q + static_cast<size_t>(col) * P) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + 32 * u + lane;
+        if (q < ni) xs[q] = t[u], Ye[q + static_cast<size_t>(col) * ni] = t[u];
+      }
+    }
+    __syncwarp();
+    if (col < nb || a.source) {
+      for (int b = lane; b < nb; b += 32) {
+        const int side = b / m, t = b % m + 1;
+        double acc = 0.0;
+        for (int kk = 1; kk <= m; ++kk) {
+          const int q = side < 2 ? (kk - 1) * m + (t - 1) : (t - 1) * m + (kk - 1);
+          const double dcoef = (side & 1) ? dN[kk] : -d0[kk];
+          acc += dcoef * xs[q];
+        }
+        if (col < nb) {
+          // L_GG: derivative entries on the two boundary nodes of the same line
+          const int cs = col / m, ct = col % m + 1;
+          double lgg = 0.0;
+          if (ct == t) {
+            if (side <= 1 && cs <= 1)
+              lgg = (side == 0 ? -1.0 : 1.0) * (cs == 0 ? (side == 0 ? d0[0] : dN[0]) : (side == 0 ? d0[N] : dN[N]));
+            else if (side >= 2 && cs >= 2)
+              lgg = (side == 2 ? -1.0 : 1.0) * (cs == 2 ? (side == 2 ? d0[0] : dN[0]) : (side == 2 ? d0[N] : dN[N]));
+          }
+          S[b + static_cast<size_t>(col) * nb] = make_double2(lgg - acc, b == col ? a.eta : 0.0);
+        } else {
+          fw[(static_cast<size_t>(c) * nb + b) * 2 + (col - nb)] = acc;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- iti: T = I - 2 i eta S^{-1}, H = 2 i eta S^{-1} f: register-resident
+// Gauss-Jordan (gj_reg.cuh), one 512-thread CTA per element
+template <int TR>
+__global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const double2* Sw, const double2* fw) {
+  constexpr int TC = (TR + 1) / 2;
+  __shared__ GjShared sh;
+  __shared__ double2 fs[kGjMax];
+  __shared__ double2 hpart[kGjThreads / 32][kGjMax];
+  const ElemArgs& a = v.a;
+  const int c = blockIdx.x, e = v5_elem(v, c), nb = a.nb, tid = threadIdx.x;
+  if (a.status[e] & 4) return;
+  const double2* Sg = Sw + static_cast<size_t>(c) * nb * nb;
+  if (tid < nb) fs[tid] = a.source ? fw[static_cast<size_t>(c) * nb + tid] : make_double2(0.0, 0.0);
+  GjReg<TR, TC> g;
+  const bool ok = gj_reg_inverse<TR, TC>(nb, [&](int i, int j) { return Sg[i + static_cast<size_t>(j) * nb]; }, g, sh);
+  const int ty = tid % kGjY, tx = tid / kGjY, lane = tid & 31, warp = tid >> 5;
+  const double te = 2.0 * a.eta;
+  double2* Te = a.T + static_cast<size_t>(e) * nb * nb;
+#pragma unroll
+  for (int aa = 0; aa < TR; ++aa) {
+    const int i = ty + kGjY * aa;
+    double2 h = make_double2(0.0, 0.0);
+    if (i < nb) {
+      const int r = sh.step[i];
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        const int j = tx + kGjX * b;
+        if (j >= nb) continue;
+        const int col = sh.piv[j];
+        const double2 sv = g.x[aa][b];
+        Te[r + static_cast<size_t>(col) * nb] = make_double2((r == col ? 1.0 : 0.0) + te * sv.y, -te * sv.x);
+        h = cfma(sv, fs[col], h);
+      }
+    }
+    // the two column owners tx = 2w, 2w + 1 of a warp, then the warps in order
+    h.x += __shfl_xor_sync(0xffffffffu, h.x, 16);
+    h.y += __shfl_xor_sync(0xffffffffu, h.y, 16);
+    if (lane < kGjY && i < nb) hpart[warp][i] = h;
+  }
+  __syncthreads();
+  if (tid < nb) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int w = 0; w < kGjThreads / 32; ++w) acc = cadd(acc, hpart[w][tid]);
+    a.H[static_cast<size_t>(e) * nb + sh.step[tid]] =
+        a.source ? make_double2(-te * acc.y, te * acc.x) : make_double2(0.0, 0.0);
+  }
+  if (tid == 0) a.status[e] = ok ? 0 : 2;
+}
+
+}  // namespace
+
+bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
+  if (std::getenv("HPSB_ELEMENT_V4")) return false;
+  const int P = a0.npad, nbc = a0.nbc, nb = a0.nb;
+  if (a0.order + 1 > 64 || nb > kGjMax || nwork <= 0) return false;
+  const int nblk = (P + V5B - 1) / V5B;
+  const size_t sA = static_cast<size_t>(P) * P, sB = static_cast<size_t>(P) * nbc,
+               sL = static_cast<size_t>(nblk) * V5B * V5B, sS = static_cast<size_t>(nb) * nb;
+  const size_t per = sizeof(double) * (sA + sB + sL) + sizeof(double2) * (sS + nb);
+  size_t free_b = 0, total_b = 0;
+  HPSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t budget = std::min<size_t>(size_t(6) << 30, free_b / 4);
+  const int cap = static_cast<int>(std::max<size_t>(1, std::min<size_t>(nwork, budget / per)));
+  const int nchunks = (nwork + cap - 1) / cap;
+  const int chunk = (nwork + nchunks - 1) / nchunks;  // even chunks
+  DevBuf<double> wA(sA * chunk), wB(sB * chunk), wL(sL * chunk);
+  DevBuf<double2> wS(sS * chunk), wf(static_cast<size_t>(nb) * chunk);
+
+  const size_t tile_smem = sizeof(double) * V5_TILE_SMEM;
+  const size_t diag_smem = sizeof(double) * (V5B * LDD + V5B);
+  const size_t schur_smem = sizeof(double) * (V5ST / 32) * P;
+  const size_t asm_smem = sizeof(double) * ((a0.order + 1) * (a0.order + 2) + a0.ni);
+  allow_smem<v5_assemble_kernel>(asm_smem);
+  allow_smem<v5_update_kernel>(tile_smem);
+  allow_smem<v5_trsm_kernel>(tile_smem);
+  allow_smem<v5_back_kernel>(tile_smem);
+  allow_smem<v5_diag_kernel>(diag_smem);
+  allow_smem<v5_schur_kernel>(schur_smem);
+
+  const int ni = a0.ni;
+  const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
+  const double bytes_e = 8.0 * ((a0.order + 1) * (a0.order + 1) + 2 * ni + 2 * nb * nb + 2 * nb);
+  const int nBt = (nbc + V5B - 1) / V5B;
+  for (int base = 0; base < nwork; base += chunk) {
+    V5Args v{};
+    v.a = a0;
+    v.base = base, v.count = std::min(chunk, nwork - base);
+    v.A = wA.p, v.B = wB.p, v.Linv = wL.p, v.sA = sA, v.sB = sB, v.sL = sL;
+    v.P = P, v.nbc = nbc, v.nblk = nblk;
+    const int cn = v.count;
+    {
+      // pinned algorithmic work of the chunk on the first launch of the label
+      KernelScope ks(ctx, "element_iti", bytes_e * cn, fe * cn);
+      v5_assemble_kernel<<<cn, 256, asm_smem, ctx->stream>>>(v);
+      HPSB_LAUNCHED(ctx);
+    }
+    for (int k = 0; k < nblk; ++k) {
+      v.k = k;
+      if (k > 0) {
+        KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+        v5_update_kernel<<<cn * (nblk - k + nBt), V5T, tile_smem, ctx->stream>>>(v);
+        HPSB_LAUNCHED(ctx);
+      }
+      {
+        KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+        v5_diag_kernel<<<cn, 32, diag_smem, ctx->stream>>>(v);
+        HPSB_LAUNCHED(ctx);
+      }
+      KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+      v5_trsm_kernel<<<cn * (nblk - k - 1 + nBt), V5T, tile_smem, ctx->stream>>>(v);
+      HPSB_LAUNCHED(ctx);
+    }
+    for (int k = nblk - 1; k >= 0; --k) {
+      v.k = k;
+      KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+      v5_back_kernel<<<cn * nBt, V5T, tile_smem, ctx->stream>>>(v);
+      HPSB_LAUNCHED(ctx);
+    }
+    {
+      KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+      v5_schur_kernel<<<cn, V5ST, schur_smem, ctx->stream>>>(v, wS.p, reinterpret_cast<double*>(wf.p));
+      HPSB_LAUNCHED(ctx);
+    }
+    KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+    switch ((nb + kGjY - 1) / kGjY) {
+      case 1: case 2: v5_iti_kernel<2><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
+      case 3: v5_iti_kernel<3><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
+      case 4: v5_iti_kernel<4><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
+      case 5: v5_iti_kernel<5><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
+      default: v5_iti_kernel<6><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
+    }
+    HPSB_LAUNCHED(ctx);
+  }
+  return true;
+}
+
+}  // namespace hpsb

@@ -18,6 +18,7 @@
 #include "internal.hpp"
 #include "linalg.cuh"
 #include "zgemm.hpp"
+#include "gj_reg.cuh"
 
 namespace hpsb {
 
@@ -180,24 +181,29 @@ __global__ void copy_ops_kernel(const CopyOp* __restrict__ ops, int nops) {
   }
 }
 
-// One CTA per matrix: complex Gauss-Jordan inverse (n <= kSmemInvMax in smem).
-__global__ void __launch_bounds__(256) inverse_smem_kernel(const InvOp* __restrict__ ops,
-                                                           int* status) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// One CTA per matrix: complex Gauss-Jordan inverse (n <= kSmemInvMax), the
+// matrix register-resident across 512 threads (gj_reg.cuh); the permuted
+// result is written back in place.
+template <int TR>
+__global__ void __launch_bounds__(kGjThreads) inverse_reg_kernel(const InvOp* __restrict__ ops,
+                                                                 int* status) {
+  constexpr int TC = (TR + 1) / 2;
+  __shared__ GjShared sh;
   const InvOp op = ops[blockIdx.x];
-  double2* A = reinterpret_cast<double2*>(smem_raw);
-  int* perm = reinterpret_cast<int*>(A + op.n * op.n);
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  for (int idx = threadIdx.x; idx < op.n * op.n; idx += blockDim.x) {
-    const int r = idx % op.n, c = idx / op.n;
-    A[idx] = op.A[(size_t)r + (size_t)c * op.lda];
-  }
-  __syncthreads();
-  const bool ok = gj_inverse_cta(A, op.n, perm, red_v, red_i);
-  for (int idx = threadIdx.x; idx < op.n * op.n; idx += blockDim.x) {
-    const int r = idx % op.n, c = idx / op.n;
-    op.A[(size_t)r + (size_t)c * op.lda] = A[idx];
+  GjReg<TR, TC> g;
+  const bool ok = gj_reg_inverse<TR, TC>(
+      op.n, [&](int i, int j) { return op.A[(size_t)i + (size_t)j * op.lda]; }, g, sh);
+  const int ty = threadIdx.x % kGjY, tx = threadIdx.x / kGjY;
+#pragma unroll
+  for (int a = 0; a < TR; ++a) {
+    const int i = ty + kGjY * a;
+    if (i >= op.n) continue;
+    const int r = sh.step[i];
+#pragma unroll
+    for (int b = 0; b < TC; ++b) {
+      const int j = tx + kGjX * b;
+      if (j < op.n) op.A[(size_t)r + (size_t)sh.piv[j] * op.lda] = g.x[a][b];
+    }
   }
   if (threadIdx.x == 0 && !ok) status[0] = op.tag + 1;
 }
@@ -366,14 +372,18 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
   if (!small.empty()) {
     int nmax = 0;
     for (const auto& o : small) nmax = std::max(nmax, o.n);
-    const size_t smem = sizeof(double2) * nmax * nmax + sizeof(int) * nmax + 16;
-    allow_smem<inverse_smem_kernel>(smem);
     d_small.upload(small, ctx->stream);
     double fl = 0;
     for (const auto& o : small) fl += 8.0 * o.n * double(o.n) * o.n;
     KernelScope ks(ctx, "zinverse_smem", 0.0, fl);
-    inverse_smem_kernel<<<static_cast<int>(small.size()), 256, smem, ctx->stream>>>(d_small.p,
-                                                                                 status_dev);
+    const int grid = static_cast<int>(small.size());
+    switch ((nmax + kGjY - 1) / kGjY) {
+      case 0: case 1: case 2: inverse_reg_kernel<2><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
+      case 3: inverse_reg_kernel<3><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
+      case 4: inverse_reg_kernel<4><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
+      case 5: inverse_reg_kernel<5><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
+      default: inverse_reg_kernel<6><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
+    }
     HPSB_LAUNCHED(ctx);
   }
   if (!large.empty()) {

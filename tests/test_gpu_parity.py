@@ -77,6 +77,26 @@ def test_element_iti_and_source(hps, oracle, ctx, name):
     assert worst_h < TOL_OP, worst_h
 
 
+@pytest.mark.parametrize("config", [0, 1, 2, 3, 4])
+def test_element_cholesky_path_full_configs(hps, oracle, config):
+    """At the BASELINE configs' full sizes the interior block is positive
+    definite: the batched Cholesky path must handle
+    every element with no pivoted-LU fallback launch; sampled elements match
+    the oracle's reference-formula element (element.cpp:127-160)."""
+    prob = hps.problem(2, config, seed=config)
+    fresh = hps.Context(0)
+    fresh.profile(True)
+    el = hps.build_elements(fresh, prob)
+    prof = fresh.profile_entries()
+    assert "element_iti_lu" not in prof, prof
+    ne = prob.n ** 2
+    picks = sorted({0, ne // 2 + 1, ne - 1})
+    for e in picks:
+        T, _ = el.iti(e, 1)
+        To = oracle.element(prob.order, 1.0 / prob.n, prob.eta, prob.coeff[e])[0]
+        assert relf(T[0], To) < TOL_OP, (config, e)
+
+
 @pytest.mark.parametrize("name", ALL)
 def test_skeleton_rhs_and_matvec(hps, oracle, ctx, name):
     c = case(hps, oracle, ctx, name)
