@@ -373,6 +373,9 @@ void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* fi
 Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg);
 void destroy_precond(Precond* p);
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev);
+// precond_apply is a fixed launch sequence (single GPU, gamma == 1 or exact
+// coarse): it can be captured into a CUDA graph
+bool precond_graph_safe(const Precond* p);
 void precond_apply_host(Precond* p, const double2* v_host, double2* z_host);
 int64_t precond_bytes(const Precond* p);
 // Pinned SURVEY §8(d) work: element flops, merge flops (all merges of the

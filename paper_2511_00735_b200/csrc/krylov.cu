@@ -91,10 +91,15 @@ __global__ void __launch_bounds__(kThreads) dots_fused_kernel(
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int i = threadIdx.x; i < ncols; i += kThreads) {
-    double2 s = make_double2(0.0, 0.0);
-    for (unsigned b = 0; b < gridDim.x; ++b) s = cadd(s, __ldcg(partial + b * ncols + i));
-    out[i] = s;
+  {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = warp; i < ncols; i += kThreads / 32) {  // one warp per column (fixed order)
+      double2 s = make_double2(0.0, 0.0);
+      for (unsigned b = lane; b < gridDim.x; b += 32) s = cadd(s, __ldcg(partial + b * ncols + i));
+      s.x = warp_sum(s.x);
+      s.y = warp_sum(s.y);
+      if (lane == 0) out[i] = s;
+    }
   }
   if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
 }
@@ -118,12 +123,17 @@ template <bool kUpdate>
 __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd,
     int nupd, double2* w, int64_t n, int R, double2* partial, double2* out, unsigned* ticket,
-    int fused, OrthStride bs) {
+    int fused, OrthStride bs, const int* jdev) {
   __shared__ double2 sh[kOrthThreads / 32][104];
   __shared__ double2 hs[104];
   __shared__ bool last;
   pdl_trigger();
   pdl_wait();
+  if (jdev) {  // device-driven cycle: nonzero counts mean "j + 1" (j from the device state)
+    const int j1 = *jdev + 1;
+    ncols = ncols ? j1 : 0;
+    nupd = nupd ? j1 : 0;
+  }
   {
     const int b = blockIdx.y;
     V += b * bs.v, w += b * bs.w, partial += b * bs.p, ticket += b;
@@ -206,10 +216,14 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int i = threadIdx.x; i < nout; i += kOrthThreads) {
+  // one warp per column: lanes stride over the blocks (loads in flight in
+  // parallel), then a butterfly -- a fixed order, so still deterministic
+  for (int i = warp; i < nout; i += kOrthThreads / 32) {
     double2 s = make_double2(0.0, 0.0);
-    for (unsigned b = 0; b < gridDim.x; ++b) s = cadd(s, __ldcg(partial + b * nout + i));
-    out[i] = s;
+    for (unsigned b = lane; b < gridDim.x; b += 32) s = cadd(s, __ldcg(partial + b * nout + i));
+    s.x = warp_sum(s.x);
+    s.y = warp_sum(s.y);
+    if (lane == 0) out[i] = s;
   }
   if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
 }
@@ -249,11 +263,13 @@ __global__ void __launch_bounds__(kThreads) axpy_batch_kernel(const double2* __r
 
 // out[i] = sum_b partial[b * ncols + i]  (fixed order: deterministic)
 __global__ void reduce_kernel(const double2* __restrict__ partial, int nblocks, int ncols,
-                              double2* out) {
+                              double2* out, const int* jdev = nullptr) {
   pdl_trigger();
   pdl_wait();
   __shared__ double2 sh[256];
+  if (jdev) ncols = ncols ? *jdev + 1 : 1;  // device-driven cycle (see orth_kernel)
   const int i = blockIdx.x;
+  if (i >= ncols) return;
   double2 s = make_double2(0.0, 0.0);
   for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
     s = cadd(s, partial[static_cast<int64_t>(b) * ncols + i]);
@@ -301,6 +317,115 @@ __global__ void sub_kernel(const double2* __restrict__ b, const double2* __restr
     r[k] = csub(b[k], y[k]);
 }
 
+// ---------------------------------------------------------------- device-driven Arnoldi cycle
+// One restart cycle of fgmres as a CUDA graph: a WHILE conditional node whose
+// body is one Arnoldi step (preconditioner on a fixed input buffer, Z_j copy,
+// interface matvec, the three CGS2 passes with the column count read from the
+// device state, the Givens update, V_{j+1}).  The Givens update runs on the
+// device and ends the loop exactly where the host loop would (krylov.cpp:
+// 92-123: converged estimate, breakdown, restart length, max_iters), so a
+// cycle needs no host round trip per iteration.
+struct CycleState {
+  int j, total, stop, pad;  // stop: 0 running, 1 converged estimate, 2 breakdown, 3 cycle end
+  double bnorm, tol, inv_h, pad2;
+};
+
+__device__ void dev_make_givens(double2 a, double2 b, double& c, double2& s) {  // krylov.cpp:17-31
+  c = 1.0;
+  s = make_double2(0.0, 0.0);
+  const double na = hypot(a.x, a.y), nb = hypot(b.x, b.y);
+  if (nb == 0.0) return;
+  const double r = hypot(na, nb);
+  if (na == 0.0) {
+    c = 0.0;
+    s = make_double2(b.x / nb, -b.y / nb);
+  } else {
+    c = na / r;
+    const double2 t = cmul(make_double2(a.x / na, a.y / na), make_double2(b.x, -b.y));
+    s = make_double2(t.x / r, t.y / r);
+  }
+}
+__device__ void dev_apply_givens(double c, double2 s, double2& a, double2& b) {  // krylov.cpp:33-37
+  const double2 t = cadd(cscale(a, c), cmul(s, b));
+  b = cadd(cmul(make_double2(-s.x, s.y), a), cscale(b, c));
+  a = t;
+}
+
+__global__ void arn_init_kernel(CycleState* st, double2* gv, int restart, int total, double beta,
+                                double bnorm, double tol) {
+  pdl_trigger();
+  pdl_wait();
+  for (int i = threadIdx.x; i <= restart; i += blockDim.x) gv[i] = make_double2(i == 0 ? beta : 0.0, 0.0);
+  if (threadIdx.x == 0) {
+    st->j = 0, st->total = total, st->stop = 0;
+    st->bnorm = bnorm, st->tol = tol, st->inv_h = 0.0;
+  }
+}
+
+// dst_base[j] = src (j from the device state)
+__global__ void arn_copy_col_kernel(const double2* __restrict__ src, double2* dst_base, int64_t n,
+                                    const CycleState* st) {
+  pdl_trigger();
+  pdl_wait();
+  double2* dst = dst_base + static_cast<int64_t>(st->j) * n;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = src[k];
+}
+
+// Hessenberg column j from the CGS2 coefficients (h = h1 + h2, h_{j+1,j} =
+// ||w||), previous rotations, the new rotation, the residual estimate and the
+// loop decision -- the host loop body of fgmres (krylov.cpp:102-123).
+__global__ void arn_givens_kernel(CycleState* st, const double2* __restrict__ hd, int R1, double2* H,
+                                  double* rc, double2* rs, double2* gv, double* hist, int restart,
+                                  int max_iters, cudaGraphConditionalHandle cond) {
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x != 0) return;
+  const int j = st->j;
+  double2* Hj = H + static_cast<size_t>(j) * R1;
+  for (int i = 0; i <= j; ++i) Hj[i] = cadd(hd[i], hd[R1 + i]);
+  const double hnext = sqrt(fmax(hd[2 * R1].x, 0.0));
+  Hj[j + 1] = make_double2(hnext, 0.0);
+  for (int i = 0; i < j; ++i) dev_apply_givens(rc[i], rs[i], Hj[i], Hj[i + 1]);
+  double c;
+  double2 sg;
+  dev_make_givens(Hj[j], Hj[j + 1], c, sg);
+  rc[j] = c, rs[j] = sg;
+  dev_apply_givens(c, sg, Hj[j], Hj[j + 1]);
+  dev_apply_givens(c, sg, gv[j], gv[j + 1]);
+  const double rel = hypot(gv[j + 1].x, gv[j + 1].y) / st->bnorm;
+  if (hist) hist[st->total] = rel;
+  int stop = 0;
+  if (hnext <= 1e-14 * st->bnorm) {
+    stop = 2;
+  } else {
+    st->inv_h = 1.0 / hnext;
+    if (rel <= st->tol) stop = 1;
+  }
+  const int jn = j + 1, tn = st->total + 1;
+  if (!stop && (jn >= restart || tn >= max_iters)) stop = 3;
+  st->j = jn, st->total = tn, st->stop = stop;
+  cudaGraphSetConditional(cond, stop ? 0u : 1u);
+}
+
+// V_{j+1} = w / h_{j+1,j}, also into the preconditioner's fixed input buffer
+__global__ void arn_scale_kernel(const double2* __restrict__ w, double2* Vbase, double2* vin, int64_t n,
+                                 const CycleState* st) {
+  pdl_trigger();
+  pdl_wait();
+  if (st->stop == 2) return;  // breakdown: no next basis vector (krylov.cpp:111-114)
+  const double f = st->inv_h;
+  double2* dst = Vbase + static_cast<int64_t>(st->j) * n;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 v = w[k];
+    const double2 o = make_double2(v.x * f, v.y * f);
+    dst[k] = o;
+    vin[k] = o;
+  }
+}
+
 using cd = std::complex<double>;
 
 struct Givens {
@@ -343,28 +468,40 @@ struct Work {
     HPSB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
   }
   int grid() const { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * ctx->num_sms)); }
-  // One CGS2 pass (orth_kernel): optionally w -= V h_upd, then out = V^H w
-  // (ncols > 0) or out[0] = ||w||^2 (ncols == 0).
-  void orth(const double2* V, int ncols, const double2* h_upd, int nupd, double2* w, double2* out) {
-    // rows per thread: enough blocks for ~2 per SM, at most kOrthMaxR
-    int R = 1;
+  // rows per thread: enough blocks for ~2 per SM, at most kOrthMaxR
+  void orth_grid(int& R, int& nb) const {
+    R = 1;
     while (R < kOrthMaxR && (n + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
       R *= 2;
-    const int nb = static_cast<int>((n + kOrthThreads * R - 1) / (kOrthThreads * R));
-    const int nout = ncols > 0 ? ncols : 1;
+    nb = static_cast<int>((n + kOrthThreads * R - 1) / (kOrthThreads * R));
+  }
+  void reserve(int maxcols) {  // partial sums for maxcols columns (before a graph capture)
+    int R, nb;
+    orth_grid(R, nb);
+    if (static_cast<size_t>(nb) * maxcols > partial.n) partial.alloc(static_cast<size_t>(nb) * maxcols);
+  }
+  // One CGS2 pass (orth_kernel): optionally w -= V h_upd, then out = V^H w
+  // (ncols > 0) or out[0] = ||w||^2 (ncols == 0).
+  void orth(const double2* V, int ncols, const double2* h_upd, int nupd, double2* w, double2* out,
+            const int* jdev = nullptr, int maxcols = 0) {
+    int R, nb;
+    orth_grid(R, nb);
+    // (device-driven: ncols / nupd are flags, the counts come from *jdev; the
+    // launch is sized for maxcols columns)
+    const int nout = jdev ? maxcols : (ncols > 0 ? ncols : 1);
     const bool fused = nb <= 4 * ctx->num_sms;
     if (static_cast<size_t>(nb) * nout > partial.n) partial.alloc(static_cast<size_t>(nb) * nout);
     KernelScope ks(ctx, "gmres_orth", 16.0 * n * (nout + nupd + (h_upd ? 2 : 1)),
                    8.0 * n * (ncols + nupd));
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{});
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev);
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{});
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev);
     if (!fused)
       launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1,
-               static_cast<const double2*>(partial.p), nb, nout, out);
+               static_cast<const double2*>(partial.p), nb, jdev ? ncols : nout, out, jdev);
   }
   // out[0..ncols) = V^H w.  Short vectors: one launch (last-block reduction);
   // long vectors: many row blocks + a column-parallel reduce launch.
@@ -377,7 +514,7 @@ struct Work {
     } else {
       dots_kernel<<<blocks, kThreads, 0, ctx->stream>>>(V, n, ncols, w, n, partial.p);
       HPSB_LAUNCHED(ctx);
-      reduce_kernel<<<ncols, 256, 0, ctx->stream>>>(partial.p, blocks, ncols, out);
+      reduce_kernel<<<ncols, 256, 0, ctx->stream>>>(partial.p, blocks, ncols, out, nullptr);
       HPSB_LAUNCHED(ctx);
     }
   }
@@ -402,6 +539,96 @@ struct Work {
   }
 };
 }  // namespace
+
+// The device-driven restart cycle (see arn_givens_kernel): buffers, the
+// captured graph and the host copies of its outcome.
+struct CycleGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  DevBuf<double2> vin, zout, Hd, rsd, gvd;
+  DevBuf<double> rcd, histd;
+  DevBuf<CycleState> st;
+  CycleState hs{};
+  std::vector<double2> Hh, gh;
+  std::vector<double> hist_h;
+  int R1 = 0;
+  ~CycleGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+  void build(Context* ctx, Skeleton* sk, Precond* pc, Work& wk, double2* V, double2* Z, double2* w,
+             int64_t n, int restart, int max_iters, bool record) {
+    R1 = restart + 1;
+    vin.alloc(n), zout.alloc(pc ? n : 0), Hd.alloc(static_cast<size_t>(R1) * restart);
+    rsd.alloc(restart), gvd.alloc(R1), rcd.alloc(restart), st.alloc(1);
+    histd.alloc(record ? max_iters : 0);
+    Hh.resize(static_cast<size_t>(R1) * restart), gh.resize(R1), hist_h.resize(record ? max_iters : 0);
+    wk.reserve(R1);
+    HPSB_CUDA(cudaMemsetAsync(Hd.p, 0, Hd.bytes(), ctx->stream));
+    HPSB_CUDA(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    HPSB_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = cond;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    HPSB_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+    cudaGraph_t body = np.conditional.phGraph_out[0];
+    HPSB_CUDA(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal));
+    bool ok = true;
+    try {
+      const int* jdev = reinterpret_cast<const int*>(st.p);
+      const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * ctx->num_sms));
+      if (pc) {
+        precond_apply(pc, vin.p, zout.p);
+        launch_k(ctx, arn_copy_col_kernel, dim3(blocks), dim3(256), 0, 1,
+                 static_cast<const double2*>(zout.p), Z, n, static_cast<const CycleState*>(st.p));
+        skeleton_apply(sk, zout.p, w);
+      } else {
+        skeleton_apply(sk, vin.p, w);
+      }
+      double2* h1 = wk.hdev.p;
+      double2* h2 = wk.hdev.p + R1;
+      double2* nn = wk.hdev.p + 2 * R1;
+      wk.orth(V, 1, nullptr, 0, w, h1, jdev, R1);  // h1 = V^H w
+      wk.orth(V, 1, h1, 1, w, h2, jdev, R1);       // w -= V h1; h2 = V^H w
+      wk.orth(V, 0, h2, 1, w, nn, jdev, R1);       // w -= V h2; nn = ||w||^2
+      launch_k(ctx, arn_givens_kernel, dim3(1), dim3(32), 0, 1, st.p,
+               static_cast<const double2*>(wk.hdev.p), R1, Hd.p, rcd.p, rsd.p, gvd.p,
+               record ? histd.p : static_cast<double*>(nullptr), restart, max_iters, cond);
+      launch_k(ctx, arn_scale_kernel, dim3(blocks), dim3(256), 0, 1, static_cast<const double2*>(w), V,
+               vin.p, n, static_cast<const CycleState*>(st.p));
+    } catch (...) {
+      ok = false;
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(ctx->stream, &captured);
+    const cudaError_t ei = (ok && ec == cudaSuccess) ? cudaGraphInstantiate(&exec, graph, 0) : cudaErrorUnknown;
+    if (std::getenv("HPSB_TRACE"))
+      std::fprintf(stderr, "[hpsb cycle graph] capture %s (%s), instantiate %s\n", ok ? "ok" : "threw",
+                   cudaGetErrorString(ec), cudaGetErrorString(ei));
+    if (ei != cudaSuccess) {
+      cudaGetLastError();  // clear; fall back to the host-driven loop
+      if (exec) cudaGraphExecDestroy(exec);
+      exec = nullptr;
+    }
+  }
+  void run(Context* ctx, const double2* V0, int64_t n, int restart, int total, double beta, double bnorm,
+           double tol) {
+    zcopy(ctx, vin.p, V0, n);
+    launch_k(ctx, arn_init_kernel, dim3(1), dim3(128), 0, 1, st.p, gvd.p, restart, total, beta, bnorm, tol);
+    HPSB_CUDA(cudaGraphLaunch(exec, ctx->stream));
+    HPSB_CUDA(cudaMemcpyAsync(&hs, st.p, sizeof(hs), cudaMemcpyDeviceToHost, ctx->stream));
+    HPSB_CUDA(cudaMemcpyAsync(Hh.data(), Hd.p, Hd.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    HPSB_CUDA(cudaMemcpyAsync(gh.data(), gvd.p, gvd.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    if (histd.n)
+      HPSB_CUDA(cudaMemcpyAsync(hist_h.data(), histd.p, histd.bytes(), cudaMemcpyDeviceToHost, ctx->stream));
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+};
 
 hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
                    const hpsb_krylov_config& cfg, hpsb_solve_report* rep) {
@@ -444,6 +671,14 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   auto Hm = [&](int i, int j) -> cd& { return H[i + static_cast<size_t>(j) * (restart + 1)]; };
   int total = 0;
   bool converged = false;
+  CycleGraph cg;
+  // Opt-in (HPSB_CYCLE_GRAPH=1): measured equal to the host-driven loop at
+  // cfg1 / cfg2 (191 vs 193 us per iteration at cfg1: the device, not the
+  // per-iteration host round trip, is the bound) and the first graph in a
+  // process costs ~60 ms of one-time setup.
+  if (!ctx->profile && ctx->world() == 1 && (!pc || precond_graph_safe(pc)) &&
+      std::getenv("HPSB_CYCLE_GRAPH"))
+    cg.build(ctx, sk, pc, wk, V.p, Z.p, w.p, n, restart, cfg.max_iters, cfg.record_history != 0);
   while (total < cfg.max_iters && !converged) {
     double beta;
     if (total == 0) {
@@ -461,7 +696,21 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
     gv[0] = beta;
     int j = 0;
     bool breakdown = false;
-    for (; j < restart && total < cfg.max_iters; ++j, ++total) {
+    if (cg.exec) {
+      // the whole cycle on the device (CycleGraph); read back its outcome
+      const int t0 = total;
+      cg.run(ctx, V.p, n, restart, total, beta, bnorm, cfg.tol);
+      j = cg.hs.j, total = cg.hs.total, breakdown = cg.hs.stop == 2;
+      for (int c = 0; c < j; ++c)
+        for (int i = 0; i <= c + 1; ++i) {
+          const double2 v = cg.Hh[i + static_cast<size_t>(c) * (restart + 1)];
+          Hm(i, c) = cd(v.x, v.y);
+        }
+      for (int i = 0; i <= j; ++i) gv[i] = cd(cg.gh[i].x, cg.gh[i].y);
+      if (cfg.record_history)
+        for (int t = t0; t < total; ++t) ctx->history.push_back(cg.hist_h[t]);
+    }
+    for (; !cg.exec && j < restart && total < cfg.max_iters; ++j, ++total) {
       double2* Vj = V.p + static_cast<size_t>(j) * n;
       if (pc) {
         double2* Zj = Z.p + static_cast<size_t>(j) * n;
@@ -625,11 +874,11 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
                static_cast<const double2*>(V.p), static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
-               RR, partial.p, out, tickets.p, 1, st);
+               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr));
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
                static_cast<const double2*>(V.p), static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
-               RR, partial.p, out, tickets.p, 1, st);
+               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr));
   };
   const int vblocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 2 * ctx->num_sms));
   auto scale = [&](const double2* src, int64_t ls, const std::vector<double>& f, double2* dst, int64_t ld) {

@@ -1449,6 +1449,10 @@ void apply_level_gamma(Precond* p, int l, double2* z) {
 }
 }  // namespace
 
+bool precond_graph_safe(const Precond* p) {
+  return p->ctx->world() == 1 && (p->cfg.exact_coarse || p->cfg.gamma <= 1);
+}
+
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   Context* ctx = p->ctx;
   const int vblocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));

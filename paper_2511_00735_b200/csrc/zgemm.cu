@@ -46,7 +46,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(THREADS) zgemm_grouped_kernel(const GemmDesc* __restrict__ descs,
+__global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDesc* __restrict__ descs,
                                                                 int ndesc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
@@ -116,17 +116,25 @@ __global__ void __launch_bounds__(THREADS) zgemm_grouped_kernel(const GemmDesc* 
       for (int i = 0; i < 4; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
 #pragma unroll
       for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
+      // four passes over the 4 x 2 fragment grid: the two DMMAs into the
+      // same accumulator are 2 4 issues apart instead of back to back (the
+      // asm statements are volatile, so the compiler keeps this order)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const double nai = -a[i].y;
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
-          dmma(cr[i][j][0], cr[i][j][1], nai, b[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
-        }
-      }
+        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
     }
   }
   cp_async_wait<0>();

@@ -123,17 +123,25 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
       for (int i = 0; i < I; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
 #pragma unroll
       for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
+      // four passes over the I x 2 fragment grid: the two DMMAs into the
+      // same accumulator are 2 I issues apart instead of back to back (the
+      // asm statements are volatile, so the compiler keeps this order)
 #pragma unroll
-      for (int i = 0; i < I; ++i) {
-        const double nai = -a[i].y;
+      for (int i = 0; i < I; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
-          dmma(cr[i][j][0], cr[i][j][1], nai, b[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
-          dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
-        }
-      }
+        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
+#pragma unroll
+      for (int i = 0; i < I; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
     }
   }
   asm volatile("cp.async.wait_group 0;\n" ::);

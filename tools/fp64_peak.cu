@@ -46,6 +46,34 @@ __global__ void dmma_m16n8k16_loop(double* out, int iters) {
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
+// Mixed: even warps run DMMA chains, odd warps DFMA chains (do the DMMA and
+// DFMA pipes overlap?).  Reports the combined rate; fl counts both.
+__global__ void mixed_loop(double* out, int iters, int dfma_per_dmma) {
+  const bool mm = ((threadIdx.x >> 5) & 1) == 0;
+  double s = 0;
+  if (mm) {
+    double acc[4][2];
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+    double a = 1.0 + threadIdx.x * 1e-6, b = 1.0 - threadIdx.x * 1e-6;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[i][0]), "+d"(acc[i][1]) : "d"(a), "d"(b));
+    }
+    for (int i = 0; i < 4; ++i) s += acc[i][0] + acc[i][1];
+  } else {
+    double a[8], b = 1.0000001, c = 0.9999999;
+    for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters * dfma_per_dmma; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+    }
+    for (int i = 0; i < 8; ++i) s += a[i];
+  }
+  if (s == 12345.0) out[threadIdx.x] = s;
+}
+
 int main() {
   double* d; cudaMalloc(&d, 4096 * 8);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -71,6 +99,16 @@ int main() {
       fl = 2.0 * 16 * 8 * 16 * 4 * (iters / 4) * (double)grid * (threads / 32);
       printf("dmma m16n8k16 bps=%d  %.2f TFLOP/s\n", blocks_per_sm, fl / ms / 1e9);
     }
+  }
+  for (int ratio : {1, 2, 4}) {
+    int grid = sms * 4, threads = 256;
+    float ms;
+    mixed_loop<<<grid, threads>>>(d, iters, ratio);
+    cudaEventRecord(e0); mixed_loop<<<grid, threads>>>(d, iters, ratio); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    const double half_warps = (double)grid * (threads / 32) / 2;
+    const double fl = 2.0 * 256 * 4 * iters * half_warps + 2.0 * 8 * iters * ratio * half_warps * 32;
+    printf("mixed dmma+dfma ratio=%d  %.2f TFLOP/s combined\n", ratio, fl / ms / 1e9);
   }
   printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

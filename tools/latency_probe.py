@@ -66,5 +66,35 @@ def main():
               f"wall {1e6 * (t1 - t0) / rep.iterations:.1f} us/it")
 
 
+
+
+def coarse_slope():
+    """Preconditioner apply device time vs coarse_iters (the coarse solve's per-step cost)."""
+    cfgno = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    prob = hps.problem(2, cfgno, seed=1)
+    ctx = hps.Context(0)
+    el = hps.build_elements(ctx, prob)
+    sk = hps.assemble_skeleton(el, prob)
+    hier = hps.build_hierarchy(sk, factor_coarse=False)
+    n = sk.dim
+    v = torch.randn(2 * n, dtype=torch.float64, device="cuda")
+    z = torch.empty_like(v)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    for ci in (1, 2, 4, 8):
+        pc = hps.build_preconditioner(hier, coarse_iters=ci)
+        for _ in range(10):
+            hps._check(hps._lib.hpsb_precond_apply_dev(pc._h, P(v), P(z)))
+        ctx.synchronize()
+        ctx.timer_start()
+        for _ in range(200):
+            hps._check(hps._lib.hpsb_precond_apply_dev(pc._h, P(v), P(z)))
+        dev = ctx.timer_stop()
+        print(f"coarse_iters={ci}: precond apply device {1e6 * dev / 200:.1f} us")
+        del pc
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "coarse":
+        coarse_slope()
+    else:
+        main()
