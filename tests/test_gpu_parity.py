@@ -186,6 +186,35 @@ def test_fgmres_solution_and_iterations(hps, oracle, ctx, name):
     assert relf(x, xo) < TOL_SOL
 
 
+@pytest.mark.parametrize("name", ["cfg0", "cfg1", "bump_n4_N4"])
+def test_fgmres_device_cycle_graph(hps, oracle, ctx, name, monkeypatch):
+    """The device-driven restart cycle (HPSB_CYCLE_GRAPH=1: Arnoldi steps and
+    Givens updates in a CUDA graph WHILE node) ends where the host loop does
+    (krylov.cpp:92-123) and matches the oracle; unpreconditioned too, and
+    with small restarts (several cycles) and the residual history."""
+    c = case(hps, oracle, ctx, name)
+    h = hps.build_hierarchy(c.sk)
+    pc = hps.build_preconditioner(h, coarse_iters=4)
+    rhs = c.sk.rhs()
+    x0, rep0 = hps.fgmres(c.sk, rhs, pc, restart=c.prob.restart, tol=c.prob.tol)
+    xs, reps = hps.fgmres(c.sk, rhs, pc, restart=5, tol=c.prob.tol, record_history=True)
+    xu, repu = hps.fgmres(c.sk, rhs, None, restart=30, tol=1e-8, max_iters=60)
+    monkeypatch.setenv("HPSB_CYCLE_GRAPH", "1")
+    x1, rep1 = hps.fgmres(c.sk, rhs, pc, restart=c.prob.restart, tol=c.prob.tol)
+    xs1, reps1 = hps.fgmres(c.sk, rhs, pc, restart=5, tol=c.prob.tol, record_history=True)
+    xu1, repu1 = hps.fgmres(c.sk, rhs, None, restart=30, tol=1e-8, max_iters=60)
+    assert rep1["converged"] and reps1["converged"]
+    assert repu1["iterations"] == repu["iterations"] and relf(xu1, xu) < 1e-12
+    h0, h1 = np.asarray(reps["residual_history"]), np.asarray(reps1["residual_history"])
+    assert h0.shape == h1.shape and np.allclose(h0, h1, rtol=1e-5, atol=0)  # estimates near 1e-10: rounding
+    assert rep1["iterations"] == rep0["iterations"] and reps1["iterations"] == reps["iterations"]
+    assert relf(x1, x0) < 1e-12 and relf(xs1, xs) < 1e-12
+    c.S.build_hierarchy(0, False)
+    c.S.precond(depth=h.depth, gamma=1, coarse_iters=4)
+    xo, repo = c.S.solve(c.S.rhs(), True, restart=c.prob.restart, tol=c.prob.tol)
+    assert abs(rep1["iterations"] - repo["iterations"]) <= 1 and relf(x1, xo) < TOL_SOL
+
+
 @pytest.mark.parametrize("name", ["cfg3_n4", "cfg2_n8", "cfg4_n8"])
 def test_fgmres_underresolved_meshes(hps, oracle, ctx, name):
     # The configs' wavenumbers on 4x4 / 8x8 meshes (kappa h up to 100) give
