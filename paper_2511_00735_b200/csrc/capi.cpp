@@ -28,7 +28,15 @@ struct hpsb_hierarchy_s {
   // factor_coarse: the exact (dense-inverse) coarse solve at the built depth,
   // used by direct_solve (dissection.cpp:225, :240-292).
   hpsb::Precond* direct = nullptr;
-  ~hpsb_hierarchy_s() { hpsb::destroy_precond(direct); }
+  // The reference driver's default preconditioner (MgConfig defaults:
+  // depth = L, gamma = 1, coarse_iters = 4; multigrid.hpp:12-18,
+  // driver.hpp:30-32), planned on the host while the device finishes the
+  // merges; handed out by precond_create for that configuration.
+  hpsb::Precond* pending = nullptr;
+  ~hpsb_hierarchy_s() {
+    hpsb::destroy_precond(direct);
+    hpsb::destroy_precond(pending);
+  }
 };
 struct hpsb_precond_s {
   hpsb::Precond* p = nullptr;
@@ -532,7 +540,17 @@ hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
   return guarded([&] {
     REQUIRE(sk && out, "hierarchy_build: null argument");
     auto h = std::make_unique<hpsb_hierarchy_s>();
-    h->h = hpsb::build_hierarchy(sk->s.get(), depth);
+    auto* hs = h.get();
+    h->h = hpsb::build_hierarchy(sk->s.get(), depth, [hs](hpsb::Hierarchy* hh) {
+      if (hh->depth < 2 || hh->ctx->profile || std::getenv("HPSB_NO_PENDING_PRECOND")) return;
+      hpsb_mg_config c{};
+      c.depth = hh->depth, c.gamma = 1, c.coarse_iters = 4, c.exact_coarse = 0;
+      try {
+        hs->pending = hpsb::create_precond(hh, c);
+      } catch (...) {
+        hs->pending = nullptr;  // built on demand by precond_create instead
+      }
+    });
     if (factor_coarse && h->h->depth >= 2) {
       hpsb_mg_config c{};
       c.depth = h->h->depth, c.gamma = 1, c.coarse_iters = 0, c.exact_coarse = 1;
@@ -588,7 +606,13 @@ hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_preco
   return guarded([&] {
     REQUIRE(h && out, "precond_create: null argument");
     auto p = std::make_unique<hpsb_precond_s>();
-    p->p = hpsb::create_precond(h->h.get(), cfg);
+    if (h->pending && cfg.depth == h->h->depth && cfg.gamma == 1 && cfg.coarse_iters == 4 &&
+        cfg.exact_coarse == 0) {
+      p->p = h->pending;  // planned during hierarchy_build (same configuration)
+      h->pending = nullptr;
+    } else {
+      p->p = hpsb::create_precond(h->h.get(), cfg);
+    }
     *out = p.release();
     return HPSB_OK;
   });

@@ -112,7 +112,8 @@ struct GroupPlan {
 };
 }  // namespace
 
-std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
+std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
+                                           const std::function<void(Hierarchy*)>& before_wait) {
   Context* ctx = sk->ctx;
   const FaceGraph& g = sk->graph;
   const int total = g.num_levels();
@@ -410,10 +411,24 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth) {
     h->levels.push_back(std::move(L));
   }
   HPSB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
-  int st = 0;
-  HPSB_CUDA(cudaMemcpyAsync(&st, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  // status into pinned memory: a copy to pageable memory would block the host
+  // until the stream drains (before the hook could overlap it)
+  thread_local int* st_pinned = [] {
+    int* q = nullptr;
+    HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&q), sizeof(int)));
+    return q;
+  }();
+  *st_pinned = 0;
+  HPSB_CUDA(cudaMemcpyAsync(st_pinned, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  if (before_wait) {
+    // the hook's own device work is stream-ordered after the merges: record
+    // the build's end event first (above), so build_seconds stays the merges'
+    before_wait(h.get());
+    tr.mark("before_wait_hook");
+  }
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   tr.mark("final_wait");
+  const int st = *st_pinned;
   if (st) {  // first singular group pivot (inverse status tag = level << 20 | group) + 1
     const int tag = st - 1, level = tag >> 20, gi = tag & ((1 << 20) - 1);
     throw std::runtime_error("eliminate_level: singular merge block at face " +

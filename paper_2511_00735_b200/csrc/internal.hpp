@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <functional>
 #include <utility>
 #include <cstdint>
 #include <memory>
@@ -367,7 +368,11 @@ void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int 
 hpsb_status fgmres_batch(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
                          const hpsb_krylov_config& cfg, hpsb_solve_report* reports);
 void recover_field(const Skeleton* sk, const double2* x_dev, int rhs_index, double2* field_dev);
-std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth);
+// before_wait runs on the host once every device operation of the build is
+// enqueued, before the final synchronisation (host work that only needs the
+// host-side structure overlaps the device's merge tail).
+std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
+                                           const std::function<void(Hierarchy*)>& before_wait = {});
 void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,
                             int* keys, double* data);
 Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg);

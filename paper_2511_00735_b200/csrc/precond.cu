@@ -1,3 +1,4 @@
+#include <chrono>
 // K4/K5: the HPS-multigrid preconditioner apply on the stored box maps.
 //
 // MgPreconditioner::apply_level (proj/src/multigrid.cpp:30-100) with gamma = 1
@@ -728,6 +729,17 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     throw InvalidArgument("MgPreconditioner: depth must equal the built hierarchy depth on the B200 path");
   if (!cfg.exact_coarse && cfg.coarse_iters > 60) throw InvalidArgument("MgPreconditioner: coarse_iters must be <= 60");
   Context* ctx = h->ctx;
+  // HPSB_TRACE=1: host wall time per creation phase (stderr)
+  const bool trace = std::getenv("HPSB_TRACE") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  std::string trace_line;
+  auto mark = [&](const char* name) {
+    if (!trace) return;
+    const auto now = std::chrono::steady_clock::now();
+    trace_line += std::string(" ") + name + "=" +
+                  std::to_string(std::chrono::duration<double, std::milli>(now - t_last).count()).substr(0, 6) + "ms";
+    t_last = now;
+  };
   auto p = std::make_unique<Precond>();
   p->h = h, p->cfg = cfg, p->ctx = ctx;
   const Skeleton* sk = h->sk;
@@ -851,6 +863,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       }
     }
   };
+  mark("items");
   // Per level: the fused small-merge kernel when every merge's operators fit
   // in shared memory, else the work-list plan phases.
   auto small_level = [&](int l) -> int {
@@ -1029,6 +1042,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     if (small_of[l] < 0) cluster_of[l] = cluster_level(l);
   }
   p->small_level_of = small_of;
+  mark("levels");
   auto add_step = [&](int l, bool downward) {
     Precond::Step st;
     st.level = l;
@@ -1126,6 +1140,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       fuse(p->up_steps, false);
     }
   }
+  mark("steps");
   p->down.name = "vcycle_down";
   p->up.name = "vcycle_up";
   p->down_g.name = "vcycle_down";
@@ -1156,6 +1171,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     }
   }
 
+  mark("plans");
   // ---- coarse level: M_depth = I + sum_boxes scatter(T_box) on the tail
   const LevelOps& C = *h->levels[cfg.depth - 1];
   p->off_d = static_cast<int64_t>(C.first_face) * sk->bs;
@@ -1345,6 +1361,12 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
                        static_cast<int64_t>(ci) * p->coarse_mv.bytes_per_run +
                        p->exact_mv.bytes_per_run;
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  mark("coarse");
+  if (trace) {
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    mark("device_drain");
+    std::fprintf(stderr, "[hpsb trace precond]%s\n", trace_line.c_str());
+  }
   return p.release();
 }
 

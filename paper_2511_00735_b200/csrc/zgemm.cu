@@ -13,6 +13,9 @@
 // prefix sum of tile counts, so levels with thousands of tiny merges and
 // levels with two huge ones use the same kernel.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cooperative_groups.h>
 
 #include "device.cuh"
 #include "internal.hpp"
@@ -216,6 +219,118 @@ __global__ void __launch_bounds__(kGjThreads) inverse_reg_kernel(const InvOp* __
   if (threadIdx.x == 0 && !ok) status[0] = op.tag + 1;
 }
 
+// ---- pivot selection for one panel, one thread-block CLUSTER per matrix.
+// The panel rows k0..n-1 (x kw columns) are split across the C CTAs of the
+// cluster and kept in shared memory; per column j: local argmax of |a_ij|
+// over the unused rows, candidates pushed to every peer (DSMEM), the same
+// fixed-order reduction in every CTA, the owner pushes the pivot row to every
+// peer, every CTA eliminates column j from its unused rows.  Pivoting is
+// implicit (used flags, no row swaps); the pivot order is converted to the
+// LAPACK swap sequence ipiv[k0+j] = k0 + p at the end.  The same pivots as a
+// swap-based partial-pivoting LU of the panel (ties aside); only ipiv is
+// produced (the elimination proper is the GEMM sweep below).
+// (Replaces a one-CTA panel LU whose rank-1 updates went through L2: up to
+// 77 MB of traffic per 32-column panel of a 2432-row matrix.)
+constexpr int kPivThreads = 512;
+constexpr int kPivMaxCluster = 16;
+constexpr int kPivMaxKb = 64;
+__global__ void __launch_bounds__(kPivThreads) panel_pivot_cluster_kernel(
+    const InvOp* __restrict__ ops, int k0, int kb, int chunk_max, int* ipiv_ws, int* status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), crank = static_cast<int>(cl.block_rank());
+  const InvOp op = ops[blockIdx.x / C];
+  if (k0 >= op.n) return;  // the whole cluster (same matrix) leaves together
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = op.n, kw = min(kb, n - k0), rows = n - k0;
+  const int chunk = (rows + C - 1) / C, r0 = min(rows, crank * chunk), nr = min(rows, r0 + chunk) - r0;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* Ps = reinterpret_cast<double2*>(smem_raw);                  // [kw][chunk_max]
+  int* used = reinterpret_cast<int*>(Ps + static_cast<size_t>(kb) * chunk_max);  // [chunk_max]
+  int* posof = used + chunk_max;                                        // [rows] (CTA 0)
+  int* rowat = posof + n;                                               // [rows] (CTA 0)
+  __shared__ double2 prow[kPivMaxKb];
+  __shared__ double cand_v[kPivMaxCluster];
+  __shared__ int cand_i[kPivMaxCluster];
+  __shared__ double red_v[kPivThreads / 32];
+  __shared__ int red_i[kPivThreads / 32];
+  __shared__ int order[kPivMaxKb];
+  for (int idx = tid; idx < nr * kw; idx += kPivThreads) {
+    const int r = idx % nr, c = idx / nr;
+    Ps[r + static_cast<size_t>(c) * chunk_max] = op.A[(size_t)(k0 + r0 + r) + (size_t)(k0 + c) * op.lda];
+  }
+  for (int r = tid; r < nr; r += kPivThreads) used[r] = 0;
+  __syncthreads();
+  for (int j = 0; j < kw; ++j) {
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int r = tid; r < nr; r += kPivThreads)
+      if (!used[r]) {
+        const double v = cabs2(Ps[r + static_cast<size_t>(j) * chunk_max]);
+        if (v > best) best = v, bi = r0 + r;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
+    }
+    if (lane == 0) red_v[warp] = best, red_i[warp] = bi;
+    __syncthreads();
+    if (tid < C) {
+      double b = -1.0;
+      int p = 0x7fffffff;
+      for (int w = 0; w < kPivThreads / 32; ++w)
+        if (red_v[w] > b || (red_v[w] == b && red_i[w] < p)) b = red_v[w], p = red_i[w];
+      *cl.map_shared_rank(&cand_v[crank], tid) = b;
+      *cl.map_shared_rank(&cand_i[crank], tid) = p;
+    }
+    cl.sync();  // candidates of every CTA delivered
+    double pv = -1.0;
+    int p = 0x7fffffff;
+    for (int q = 0; q < C; ++q)
+      if (cand_v[q] > pv || (cand_v[q] == pv && cand_i[q] < p)) pv = cand_v[q], p = cand_i[q];
+    if (!(pv > 0.0)) {
+      if (tid == 0 && crank == 0) status[0] = op.tag + 1;
+      p = j < rows ? p : 0;
+    }
+    if (p >= r0 && p < r0 + nr) {  // owner: pivot row (columns j..kw-1) to every peer
+      const int lr = p - r0;
+      for (int t = tid; t < C * (kw - j); t += kPivThreads) {
+        const int q = t / (kw - j), c = j + t % (kw - j);
+        *cl.map_shared_rank(&prow[c], q) = Ps[lr + static_cast<size_t>(c) * chunk_max];
+      }
+      __syncthreads();
+      if (tid == 0) used[lr] = 1;
+    }
+    if (tid == 0) order[j] = p;
+    cl.sync();  // pivot row delivered
+    const double2 inv = cinv(prow[j]);
+    const int cw = kw - j - 1;
+    for (int idx = tid; idx < nr * cw; idx += kPivThreads) {
+      const int r = idx % nr, c = j + 1 + idx / nr;
+      if (used[r]) continue;
+      const double2 l = cmul(Ps[r + static_cast<size_t>(j) * chunk_max], inv);
+      double2& a = Ps[r + static_cast<size_t>(c) * chunk_max];
+      a = csub(a, cmul(l, prow[c]));
+    }
+    __syncthreads();
+  }
+  if (crank == 0) {  // pivot order -> swap sequence over positions k0..n-1
+    for (int r = tid; r < rows; r += kPivThreads) posof[r] = r, rowat[r] = r;
+    __syncthreads();
+    if (tid == 0)
+      for (int j = 0; j < kw; ++j) {
+        const int q = order[j], pos = posof[q];
+        ipiv_ws[op.perm_off + k0 + j] = k0 + pos;
+        const int a = rowat[j];
+        rowat[j] = q, rowat[pos] = a;
+        posof[a] = pos, posof[q] = j;
+      }
+  }
+  cl.sync();  // no CTA leaves while a peer may still write its shared memory
+}
+
 // ---- blocked Gauss-Jordan (large matrices), one panel of kb columns per step
 // Pivot rows for columns [k0, k0+kb): partial-pivoting LU of a copy of the
 // panel rows k0..n-1 (one CTA per matrix).  ipiv[k0+j] = row swapped with k0+j.
@@ -341,6 +456,14 @@ void GemmBatch::run(Context* ctx) {
     return true;
   }();
   (void)attr;
+  if (std::getenv("HPSB_TRACE_GEMM")) {  // executed (tile-padded) vs useful flops per launch
+    double padded = 0;
+    for (const auto& d : descs) padded += 8.0 * d.tiles_m * BM * d.tiles_n * BN * (((d.K + BK - 1) / BK) * BK);
+    static double tu = 0, tp = 0;
+    tu += flops, tp += padded;
+    std::fprintf(stderr, "[gemm] descs %zu tiles %d useful %.3g padded %.3g (cum useful %.4g padded %.4g)\n",
+                 descs.size(), total_tiles, flops, padded, tu, tp);
+  }
   KernelScope ks(ctx, "zgemm_dmma", 0.0, flops);
   zgemm_grouped_kernel<<<total_tiles, THREADS, GEMM_SMEM, ctx->stream>>>(
       d_descs.p, static_cast<int>(descs.size()));
@@ -399,20 +522,52 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     // columns, choose pivot rows by a panel LU, swap them in, invert the
     // pivot block P = A_KK^{-1} and sweep the rest of the matrix with grouped
     // DMMA GEMMs:  U = P A_KR,  A_RR -= A_RK U,  A_RK = -A_RK P,  A_KR = U.
-    constexpr int kb = 32;
+    const int kb = std::getenv("HPSB_GJ_KB32") ? 32 : kPivMaxKb;
     d_large.upload(large, ctx->stream);
     perm_ws.alloc(perm_total);
     int nmax = 0;
     for (const auto& o : large) nmax = std::max(nmax, o.n);
+    // pivot-selection cluster: rows split so a CTA's panel slice fits in ~150 KB
+    const int csize = std::min(kPivMaxCluster,
+                               std::max(1, static_cast<int>((static_cast<size_t>(nmax) * kb * 16 + 150 * 1024 - 1) /
+                                                            (150 * 1024))));
+    const int chunk_max = (nmax + csize - 1) / csize;
+    const size_t piv_smem = sizeof(double2) * static_cast<size_t>(kb) * chunk_max +
+                            sizeof(int) * (chunk_max + 2 * static_cast<size_t>(nmax));
+    static const bool piv_attr = [] {
+      HPSB_CUDA(cudaFuncSetAttribute(panel_pivot_cluster_kernel,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      return true;
+    }();
+    (void)piv_attr;
+    allow_smem<panel_pivot_cluster_kernel>(piv_smem);
     DevBuf<double2> panel(static_cast<size_t>(perm_total) * kb), U(static_cast<size_t>(perm_total) * kb),
         Q(static_cast<size_t>(perm_total) * kb);
     std::vector<InvOp> pivops(large.size());
     for (int k0 = 0; k0 < nmax; k0 += kb) {
       {
         KernelScope ks(ctx, "zinverse_panel", 0.0, 0.0);
-        panel_pivot_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(
-            d_large.p, k0, kb, panel.p, perm_ws.p, status_dev);
-        HPSB_LAUNCHED(ctx);
+        if (std::getenv("HPSB_GJ_PANEL_V1")) {
+          panel_pivot_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(
+              d_large.p, k0, kb, panel.p, perm_ws.p, status_dev);
+          HPSB_LAUNCHED(ctx);
+        } else {
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3(static_cast<unsigned>(large.size() * csize));
+          cfg.blockDim = dim3(kPivThreads);
+          cfg.dynamicSmemBytes = piv_smem;
+          cfg.stream = ctx->stream;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = static_cast<unsigned>(csize);
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          HPSB_CUDA(cudaLaunchKernelEx(&cfg, panel_pivot_cluster_kernel, static_cast<const InvOp*>(d_large.p),
+                                       k0, kb, chunk_max, perm_ws.p, status_dev));
+          HPSB_LAUNCHED(ctx);
+        }
       }
       {
         KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);
