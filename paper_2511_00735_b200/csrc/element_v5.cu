@@ -42,8 +42,13 @@ constexpr int V5K = 16;                 // k depth of one pipeline stage
 constexpr int V5S = 3;                  // pipeline stages
 constexpr int LDM = V5B + 4;            // [k][m] staging stride (m contiguous)
 constexpr int LDK = V5K + 4;            // [m][k] staging stride (k contiguous)
-constexpr int V5STAGE = V5B * LDK;      // doubles per operand per stage (>= V5K * LDM)
-constexpr int V5_TILE_SMEM = 2 * V5S * V5STAGE;  // doubles
+constexpr int V5STAGE = V5B * LDK;      // doubles of the A operand per stage (>= V5K * LDM)
+// B operand stage for a tile of 16 NJ columns (NJ fragments of 8 per warp column)
+__host__ __device__ constexpr int v5_bstage(int NJ) {
+  return 16 * NJ * LDK > V5K * LDM ? 16 * NJ * LDK : V5K * LDM;
+}
+__host__ __device__ constexpr int v5_tile_smem(int NJ) { return V5S * (V5STAGE + v5_bstage(NJ)); }  // doubles
+constexpr int V5_TILE_SMEM = v5_tile_smem(4);
 constexpr int LDD = V5B + 1;            // diagonal block stride in the panel kernel
 static_assert(V5STAGE >= V5K * LDM, "stage size");
 
@@ -83,23 +88,25 @@ __device__ __forceinline__ void dmma5(double& c0, double& c1, double a, double b
 // DMMA fragments; acc[i][j][h] = C[32 wm + 8 i + g][32 wn + 8 j + 2 t4 + h].
 // Every pointer and leading dimension must keep 16-byte alignment of
 // 2-element runs.  Ends with a CTA barrier (the staging buffers are free).
-template <bool A_KC, bool B_KC>
+template <bool A_KC, bool B_KC, int NJ = 4>
 __device__ __forceinline__ void tile_mma(const double* __restrict__ op1, int ld1,
                                          const double* __restrict__ op2, int ld2, int M, int N,
-                                         int K, double (&acc)[4][4][2], double* smem) {
+                                         int K, double (&acc)[4][NJ][2], double* smem) {
+  static_assert(B_KC || NJ == 4, "transposed B tiles are 64 wide");
+  constexpr int BN = 16 * NJ, BST = v5_bstage(NJ);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   double* As = smem;
   double* Bs = smem + V5S * V5STAGE;
   const int ksteps = K / V5K;
   auto load = [&](int ks, int st) {
     const int k0 = ks * V5K;
     double* as = As + st * V5STAGE;
-    double* bs = Bs + st * V5STAGE;
+    double* bs = Bs + st * BST;
 #pragma unroll
     for (int r = 0; r < (V5B * V5K / 2) / V5T; ++r) {
       const int idx = tid + r * V5T;
@@ -112,8 +119,12 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ op1, int ld1
         const bool ok = m < M;
         cp_async16_zfill(as + m * LDK + 2 * c2, ok ? op1 + k0 + 2 * c2 + static_cast<size_t>(m) * ld1 : op1, ok);
       }
+    }
+#pragma unroll
+    for (int r = 0; r < (BN * V5K / 2) / V5T; ++r) {
+      const int idx = tid + r * V5T;
       if (!B_KC) {
-        const int n2 = idx % (V5B / 2), kk = idx / (V5B / 2);
+        const int n2 = idx % (BN / 2), kk = idx / (BN / 2);
         const bool ok = 2 * n2 < N;
         cp_async16_zfill(bs + kk * LDM + 2 * n2, ok ? op2 + 2 * n2 + static_cast<size_t>(k0 + kk) * ld2 : op2, ok);
       } else {
@@ -134,24 +145,24 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ op1, int ld1
     if (ks + V5S - 1 < ksteps) load(ks + V5S - 1, (ks + V5S - 1) % V5S);
     cp_async_commit();
     const double* as = As + (ks % V5S) * V5STAGE;
-    const double* bs = Bs + (ks % V5S) * V5STAGE;
+    const double* bs = Bs + (ks % V5S) * BST;
 #pragma unroll
     for (int kk = 0; kk < V5K; kk += 4) {
-      double af[4], bf[4];
+      double af[4], bf[NJ];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int row = 32 * wm + 8 * i + g;
         af[i] = A_KC ? as[row * LDK + kk + t4] : as[(kk + t4) * LDM + row];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int col = 32 * wn + 8 * j + g;
+      for (int j = 0; j < NJ; ++j) {
+        const int col = 8 * NJ * wn + 8 * j + g;
         bf[j] = B_KC ? bs[col * LDK + kk + t4] : bs[(kk + t4) * LDM + col];
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma5(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma5(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_async_wait_all();
@@ -159,7 +170,8 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ op1, int ld1
 }
 
 // C (column-major, ldc) = beta * C + alpha * acc over the tile's M x N part.
-__device__ __forceinline__ void tile_store(double* C, int ldc, int M, int N, const double (&acc)[4][4][2],
+template <int NJ>
+__device__ __forceinline__ void tile_store(double* C, int ldc, int M, int N, const double (&acc)[4][NJ][2],
                                            double alpha, bool accumulate) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
   const int wm = warp & 1, wn = warp >> 1;
@@ -168,10 +180,10 @@ __device__ __forceinline__ void tile_store(double* C, int ldc, int M, int N, con
     const int row = 32 * wm + 8 * i + g;
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int col = 32 * wn + 8 * j + 2 * t4 + h;
+        const int col = 8 * NJ * wn + 8 * j + 2 * t4 + h;
         if (col >= N) continue;
         double* c = C + row + static_cast<size_t>(col) * ldc;
         *c = accumulate ? *c + alpha * acc[i][j][h] : alpha * acc[i][j][h];
@@ -243,171 +255,160 @@ __global__ void __launch_bounds__(256) v5_assemble_kernel(V5Args v) {
 }
 
 // ---- update (left-looking): tiles of block column k and of block row k of B
+// (B tiles are 16 NJB columns wide: one tile covers nb + 2 <= 80 columns)
+template <int NJB>
 __global__ void __launch_bounds__(V5T, 3) v5_update_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
-  const int P = v.P, k = v.k, nA = v.nblk - k, nBt = (v.nbc + V5B - 1) / V5B;
+  constexpr int BW = 16 * NJB;
+  const int P = v.P, k = v.k, nA = v.nblk - k, nBt = (v.nbc + BW - 1) / BW;
   const int c = blockIdx.x / (nA + nBt), t = blockIdx.x % (nA + nBt);
   const int e = v5_elem(v, c);
   if (v.a.status[e] & 4) return;
   double* A = v.A + c * v.sA;
   double* B = v.B + c * v.sB;
   const int bk = min(V5B, P - V5B * k), K = V5B * k;
-  double acc[4][4][2];
   if (t < nA) {
+    double acc[4][4][2];
     const int r0 = V5B * (k + t), M = min(V5B, P - r0);
     tile_mma<false, false>(A + r0, P, A + V5B * k, P, M, bk, K, acc, smem5);
-    tile_store(A + r0 + static_cast<size_t>(V5B * k) * P, P, M, bk, acc, -1.0, true);
+    tile_store<4>(A + r0 + static_cast<size_t>(V5B * k) * P, P, M, bk, acc, -1.0, true);
   } else {
-    const int c0 = V5B * (t - nA), N = min(V5B, v.nbc - c0);
-    tile_mma<false, true>(A + V5B * k, P, B + static_cast<size_t>(c0) * P, P, bk, N, K, acc, smem5);
-    tile_store(B + V5B * k + static_cast<size_t>(c0) * P, P, bk, N, acc, -1.0, true);
+    double acc[4][NJB][2];
+    const int c0 = BW * (t - nA), N = min(BW, v.nbc - c0);
+    tile_mma<false, true, NJB>(A + V5B * k, P, B + static_cast<size_t>(c0) * P, P, bk, N, K, acc, smem5);
+    tile_store<NJB>(B + V5B * k + static_cast<size_t>(c0) * P, P, bk, N, acc, -1.0, true);
   }
 }
 
-// ---- diag: L[k,k] = chol(A[k,k]) and Linv_k = L[k,k]^{-1}, one warp per
-// element (the 64-step chains are latency bound: no CTA barriers, six
-// elements resident per SM)
-__global__ void __launch_bounds__(32) v5_diag_kernel(V5Args v) {
+// ---- diag: L[k,k] = chol(A[k,k]) and Linv_k = L[k,k]^{-1}, one 64-thread CTA
+// per element (the 64-step chains are latency bound: six elements resident
+// per SM, no cross-warp dependency except one barrier per Cholesky column)
+constexpr int V5DT = 64;
+// L[r][t] x_tt (the q = t term of column t's sums; x_tt = 1 / l_tt)
+__device__ __forceinline__ double L_X(const double* D, int r, int t, const double* rdiag) {
+  return D[r + t * (V5B + 2)] * rdiag[t];
+}
+__global__ void __launch_bounds__(V5DT) v5_diag_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
-  const int P = v.P, k = v.k, c = blockIdx.x, e = v5_elem(v, c), lane = threadIdx.x;
+  const int P = v.P, k = v.k, c = blockIdx.x, e = v5_elem(v, c), t = threadIdx.x;
   if (v.a.status[e] & 4) return;
   const double* A = v.A + c * v.sA;
   double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;  // ld 64
   const int k0 = V5B * k, bk = min(V5B, P - k0);
-  double* D = smem5;  // [bk][LDD] column-major, factored and inverted in place
-  double* rdiag = smem5 + V5B * LDD;
-  // load the lower triangle: 8 independent global loads in flight per lane
-  // (__ldg: the global-space loads may pass the shared stores)
-  for (int col0 = 0; col0 < bk; col0 += 4) {
-    double t[4][2];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = col0 + u, r = lane + 32 * h;
-        t[u][h] = (col < bk && r < bk && r >= col) ? __ldg(A + k0 + r + static_cast<size_t>(k0 + col) * P) : 0.0;
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = col0 + u, r = lane + 32 * h;
-        if (col < bk && r < bk && r >= col) D[r + col * LDD] = t[u][h];
-      }
+  double* D = smem5;  // [bk][LDK2] column-major, factored and inverted in place
+  constexpr int LDK2 = V5B + 2;  // even: 16-byte cp.async rows; (r + q * 66) spreads banks
+  double* rdiag = smem5 + V5B * LDK2;
+  __shared__ double s_d;
+  // the whole block (both triangles; bk x bk) with every copy in flight at once
+  for (int idx = t; idx < bk * (bk / 2); idx += V5DT) {
+    const int r2 = idx % (bk / 2), col = idx / (bk / 2);
+    cp_async16(D + 2 * r2 + col * LDK2, A + k0 + 2 * r2 + static_cast<size_t>(k0 + col) * P);
   }
-  __syncwarp();
-  // left-looking Cholesky: column j = A[:, j] - L[:, :j] L[j, :j]^T, lanes
-  // over rows (no read-modify-write chains in shared memory: the dot
-  // products' loads are independent and pipeline)
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+  // left-looking Cholesky, thread t owns row t: l_tj = (a_tj - L[t,:j] L[j,:j]^T) / l_jj
   for (int j = 0; j < bk; ++j) {
-    const int r0 = j + lane, r1 = r0 + 32;
-    double s0 = r0 < bk ? D[r0 + j * LDD] : 0.0, s1 = r1 < bk ? D[r1 + j * LDD] : 0.0;
-    double u0 = 0.0, u1 = 0.0;
-    int q = 0;
-    for (; q + 1 < j; q += 2) {
-      const double a0 = D[j + q * LDD], a1 = D[j + (q + 1) * LDD];
-      if (r0 < bk) s0 -= D[r0 + q * LDD] * a0, u0 -= D[r0 + (q + 1) * LDD] * a1;
-      if (r1 < bk) s1 -= D[r1 + q * LDD] * a0, u1 -= D[r1 + (q + 1) * LDD] * a1;
+    double s0 = 0.0, s1 = 0.0;
+    const bool act = t >= j && t < bk;
+    if (act) {
+      s0 = D[t + j * LDK2];
+      int q = 0;
+      for (; q + 1 < j; q += 2) {
+        s0 -= D[t + q * LDK2] * D[j + q * LDK2];
+        s1 -= D[t + (q + 1) * LDK2] * D[j + (q + 1) * LDK2];
+      }
+      if (q < j) s0 -= D[t + q * LDK2] * D[j + q * LDK2];
+      s0 += s1;
     }
-    if (q < j) {
-      const double a0 = D[j + q * LDD];
-      if (r0 < bk) s0 -= D[r0 + q * LDD] * a0;
-      if (r1 < bk) s1 -= D[r1 + q * LDD] * a0;
-    }
-    s0 += u0, s1 += u1;
-    const double d = __shfl_sync(0xffffffffu, s0, 0);  // row j is lane 0's r0
+    if (t == j) s_d = s0;
+    __syncthreads();
+    const double d = s_d;
     if (!(d > 0.0)) {
-      if (lane == 0) atomicOr(v.a.status + e, 4);  // indefinite: pivoted-LU fallback (v1)
+      if (t == 0) atomicOr(v.a.status + e, 4);  // indefinite: pivoted-LU fallback (v1)
       return;
     }
-    const double sq = sqrt(d), rs = 1.0 / sq;
-    __syncwarp();
-    if (r0 < bk) D[r0 + j * LDD] = (lane == 0) ? sq : s0 * rs;
-    if (r1 < bk) D[r1 + j * LDD] = s1 * rs;
-    if (lane == 0) rdiag[j] = rs;
-    __syncwarp();
+    const double sq = sqrt(d);
+    if (act) D[t + j * LDK2] = (t == j) ? sq : s0 / sq;
+    if (t == j) rdiag[j] = 1.0 / sq;
+    __syncthreads();
   }
-  // in-place inverse, row by row: X[i][j] = -X[i][i] sum_{q=j}^{i-1} L[i][q] X[q][j]
-  // (the diagonal becomes X's first; rows of L below i are still intact)
-  for (int r = lane; r < bk; r += 32) D[r + r * LDD] = rdiag[r];
-  __syncwarp();
-  for (int i = 1; i < bk; ++i) {
-    const int j0 = lane, j1 = lane + 32;
-    double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
-    if (j0 < i) {
-      int q = j0;
-      for (; q + 1 < i; q += 2) {
-        s0 += D[i + q * LDD] * D[q + j0 * LDD];
-        t0 += D[i + (q + 1) * LDD] * D[q + 1 + j0 * LDD];
+  // inverse, thread t owns column t of X = L^{-1}:
+  //   x_rt = -x_rr sum_{q=t}^{r-1} L[r][q] x_qt,
+  // stored transposed in the (dead) upper triangle, X[q][t] at D[t + q ld]:
+  // a thread reads only its own X entries and the strict lower L -- no barrier.
+  if (t < bk) {
+    for (int r = t + 1; r < bk; ++r) {
+      double s0 = L_X(D, r, t, rdiag), s1 = 0.0;  // q = t term
+      int q = t + 1;
+      for (; q + 1 < r; q += 2) {
+        s0 += D[r + q * LDK2] * D[t + q * LDK2];
+        s1 += D[r + (q + 1) * LDK2] * D[t + (q + 1) * LDK2];
       }
-      if (q < i) s0 += D[i + q * LDD] * D[q + j0 * LDD];
+      if (q < r) s0 += D[r + q * LDK2] * D[t + q * LDK2];
+      D[t + r * LDK2] = -rdiag[r] * (s0 + s1);
     }
-    if (j1 < i) {
-      int q = j1;
-      for (; q + 1 < i; q += 2) {
-        s1 += D[i + q * LDD] * D[q + j1 * LDD];
-        t1 += D[i + (q + 1) * LDD] * D[q + 1 + j1 * LDD];
-      }
-      if (q < i) s1 += D[i + q * LDD] * D[q + j1 * LDD];
-    }
-    __syncwarp();
-    const double ri = rdiag[i];
-    if (j0 < i) D[i + j0 * LDD] = -ri * (s0 + t0);
-    if (j1 < i) D[i + j1 * LDD] = -ri * (s1 + t1);
-    __syncwarp();
   }
-  // diagonal of the inverse and write-out (full 64 x 64 block, zero upper part)
-  for (int col = 0; col < bk; ++col)
-    for (int r = lane; r < bk; r += 32)
-      Lg[r + col * V5B] = r >= col ? D[r + col * LDD] : 0.0;
+  __syncthreads();
+  for (int idx = t; idx < V5B * V5B; idx += V5DT) {
+    const int r = idx % V5B, col = idx / V5B;
+    double x = 0.0;
+    if (r < bk && col < bk) x = r > col ? D[col + r * LDK2] : (r == col ? rdiag[r] : 0.0);
+    Lg[idx] = x;
+  }
 }
 
 // ---- trsm: L[i,k] = A[i,k] Linv_k^T (i > k) and Y[k,:] = Linv_k B[k,:], one tile per CTA
+template <int NJB>
 __global__ void __launch_bounds__(V5T, 3) v5_trsm_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
+  constexpr int BW = 16 * NJB;
   const int P = v.P, k = v.k, k0 = V5B * k, bk = min(V5B, P - k0);
-  const int nA = v.nblk - k - 1, nBt = (v.nbc + V5B - 1) / V5B;
+  const int nA = v.nblk - k - 1, nBt = (v.nbc + BW - 1) / BW;
   const int c = blockIdx.x / (nA + nBt), t = blockIdx.x % (nA + nBt);
   const int e = v5_elem(v, c);
   if (v.a.status[e] & 4) return;
   double* A = v.A + c * v.sA;
   double* B = v.B + c * v.sB;
   const double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;
-  double acc[4][4][2];
   if (t < nA) {
+    double acc[4][4][2];
     const int r0 = k0 + bk + V5B * t, M = min(V5B, P - r0);
     double* Ci = A + r0 + static_cast<size_t>(k0) * P;
     tile_mma<false, false>(Ci, P, Lg, V5B, M, bk, bk, acc, smem5);
-    tile_store(Ci, P, M, bk, acc, 1.0, false);
+    tile_store<4>(Ci, P, M, bk, acc, 1.0, false);
   } else {
-    const int c0 = V5B * (t - nA), N = min(V5B, v.nbc - c0);
+    double acc[4][NJB][2];
+    const int c0 = BW * (t - nA), N = min(BW, v.nbc - c0);
     double* Ck = B + k0 + static_cast<size_t>(c0) * P;
-    tile_mma<false, true>(Lg, V5B, Ck, P, bk, N, bk, acc, smem5);
-    tile_store(Ck, P, bk, N, acc, 1.0, false);
+    tile_mma<false, true, NJB>(Lg, V5B, Ck, P, bk, N, bk, acc, smem5);
+    tile_store<NJB>(Ck, P, bk, N, acc, 1.0, false);
   }
 }
 
 // ---- backward: X[k,:] = Linv_k^T (Y[k,:] - sum_{j>k} L[j,k]^T X[j,:]), one column tile per CTA
+template <int NJB>
 __global__ void __launch_bounds__(V5T, 3) v5_back_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
-  const int P = v.P, k = v.k, nBt = (v.nbc + V5B - 1) / V5B;
-  const int c = blockIdx.x / nBt, c0 = V5B * (blockIdx.x % nBt), e = v5_elem(v, c);
+  constexpr int BW = 16 * NJB;
+  const int P = v.P, k = v.k, nBt = (v.nbc + BW - 1) / BW;
+  const int c = blockIdx.x / nBt, c0 = BW * (blockIdx.x % nBt), e = v5_elem(v, c);
   if (v.a.status[e] & 4) return;
   double* A = v.A + c * v.sA;
   double* B = v.B + c * v.sB;
   const double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;
-  const int k0 = V5B * k, bk = min(V5B, P - k0), N = min(V5B, v.nbc - c0), kb = k0 + bk;
+  const int k0 = V5B * k, bk = min(V5B, P - k0), N = min(BW, v.nbc - c0), kb = k0 + bk;
   double* Ck = B + k0 + static_cast<size_t>(c0) * P;
-  double acc[4][4][2];
+  double acc[4][NJB][2];
   if (kb < P) {
-    tile_mma<true, true>(A + kb + static_cast<size_t>(k0) * P, P, B + kb + static_cast<size_t>(c0) * P, P,
-                         bk, N, P - kb, acc, smem5);
-    tile_store(Ck, P, bk, N, acc, -1.0, true);
+    tile_mma<true, true, NJB>(A + kb + static_cast<size_t>(k0) * P, P, B + kb + static_cast<size_t>(c0) * P, P,
+                              bk, N, P - kb, acc, smem5);
+    tile_store<NJB>(Ck, P, bk, N, acc, -1.0, true);
     __threadfence_block();
     __syncthreads();
   }
-  tile_mma<true, true>(Lg, V5B, Ck, P, bk, N, bk, acc, smem5);
-  tile_store(Ck, P, bk, N, acc, 1.0, false);
+  tile_mma<true, true, NJB>(Lg, V5B, Ck, P, bk, N, bk, acc, smem5);
+  tile_store<NJB>(Ck, P, bk, N, acc, 1.0, false);
 }
 
 // ---- schur: S = L_GG - L_Gi X (+ i eta I), f = L_Gi x_b, and the recovery
@@ -542,21 +543,26 @@ bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
   DevBuf<double> wA(sA * chunk), wB(sB * chunk), wL(sL * chunk);
   DevBuf<double2> wS(sS * chunk), wf(static_cast<size_t>(nb) * chunk);
 
-  const size_t tile_smem = sizeof(double) * V5_TILE_SMEM;
-  const size_t diag_smem = sizeof(double) * (V5B * LDD + V5B);
+  // B tiles: one tile over the nb + 2 right-hand sides when they fit 80 columns
+  const int njb = nbc <= 80 ? std::max(2, (nbc + 15) / 16) : 4;
+  const size_t tile_smem = sizeof(double) * v5_tile_smem(std::max(njb, 4));
+  const size_t diag_smem = sizeof(double) * (V5B * (V5B + 2) + V5B);
   const size_t schur_smem = sizeof(double) * (V5ST / 32) * P;
   const size_t asm_smem = sizeof(double) * ((a0.order + 1) * (a0.order + 2) + a0.ni);
+  auto update_k = njb == 2 ? v5_update_kernel<2> : njb == 3 ? v5_update_kernel<3> : njb == 5 ? v5_update_kernel<5> : v5_update_kernel<4>;
+  auto trsm_k = njb == 2 ? v5_trsm_kernel<2> : njb == 3 ? v5_trsm_kernel<3> : njb == 5 ? v5_trsm_kernel<5> : v5_trsm_kernel<4>;
+  auto back_k = njb == 2 ? v5_back_kernel<2> : njb == 3 ? v5_back_kernel<3> : njb == 5 ? v5_back_kernel<5> : v5_back_kernel<4>;
   allow_smem<v5_assemble_kernel>(asm_smem);
-  allow_smem<v5_update_kernel>(tile_smem);
-  allow_smem<v5_trsm_kernel>(tile_smem);
-  allow_smem<v5_back_kernel>(tile_smem);
+  HPSB_CUDA(cudaFuncSetAttribute(update_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tile_smem)));
+  HPSB_CUDA(cudaFuncSetAttribute(trsm_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tile_smem)));
+  HPSB_CUDA(cudaFuncSetAttribute(back_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tile_smem)));
   allow_smem<v5_diag_kernel>(diag_smem);
   allow_smem<v5_schur_kernel>(schur_smem);
 
   const int ni = a0.ni;
   const double fe = ni * double(ni) * ni / 3.0 + 2.0 * ni * double(ni) * nb + 8.0 * nb * double(nb) * nb;
   const double bytes_e = 8.0 * ((a0.order + 1) * (a0.order + 1) + 2 * ni + 2 * nb * nb + 2 * nb);
-  const int nBt = (nbc + V5B - 1) / V5B;
+  const int nBt = (nbc + 16 * njb - 1) / (16 * njb);
   for (int base = 0; base < nwork; base += chunk) {
     V5Args v{};
     v.a = a0;
@@ -574,22 +580,22 @@ bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
       v.k = k;
       if (k > 0) {
         KernelScope ks(ctx, "element_iti", 0.0, 0.0);
-        v5_update_kernel<<<cn * (nblk - k + nBt), V5T, tile_smem, ctx->stream>>>(v);
+        update_k<<<cn * (nblk - k + nBt), V5T, tile_smem, ctx->stream>>>(v);
         HPSB_LAUNCHED(ctx);
       }
       {
         KernelScope ks(ctx, "element_iti", 0.0, 0.0);
-        v5_diag_kernel<<<cn, 32, diag_smem, ctx->stream>>>(v);
+        v5_diag_kernel<<<cn, V5DT, diag_smem, ctx->stream>>>(v);
         HPSB_LAUNCHED(ctx);
       }
       KernelScope ks(ctx, "element_iti", 0.0, 0.0);
-      v5_trsm_kernel<<<cn * (nblk - k - 1 + nBt), V5T, tile_smem, ctx->stream>>>(v);
+      trsm_k<<<cn * (nblk - k - 1 + nBt), V5T, tile_smem, ctx->stream>>>(v);
       HPSB_LAUNCHED(ctx);
     }
     for (int k = nblk - 1; k >= 0; --k) {
       v.k = k;
       KernelScope ks(ctx, "element_iti", 0.0, 0.0);
-      v5_back_kernel<<<cn * nBt, V5T, tile_smem, ctx->stream>>>(v);
+      back_k<<<cn * nBt, V5T, tile_smem, ctx->stream>>>(v);
       HPSB_LAUNCHED(ctx);
     }
     {
