@@ -118,6 +118,7 @@ constexpr size_t kClusterMergeSmemMax = 200 * 1024;
 
 namespace {
 constexpr int kCoarseThreads = 1024;
+constexpr int kCoarseRowsReg = 8;  // coarse_step_kernel keeps <= 8 rows of w per thread in registers
 
 // Dense M_depth = I + sum_boxes scatter(T_box): box b writes rows out_b (its
 // outgoing slots, owned by b alone) and columns in_b; the identity was
@@ -609,29 +610,79 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_step_kernel(
   __shared__ double sh[33];
   if (state[1] != 0.0) return;
   const int ldh = ci + 1;
-  for (int i = 0; i <= j; ++i) {
-    const double2* Vi = V + i * n;
-    double sr = 0.0, si = 0.0;
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-      const double2 a = Vi[k], b = cw[k];
-      sr += a.x * b.x + a.y * b.y;
-      si += a.x * b.y - a.y * b.x;
+  double hnext;
+  if (n <= static_cast<int64_t>(kCoarseRowsReg) * kCoarseThreads && j < kMaxCoarseIters) {
+    // Classical Gram-Schmidt with w's rows in registers: the j+1 projections
+    // reduce together (one block reduction instead of j+1; equal to the
+    // modified form of krylov.cpp:98-101 in exact arithmetic, as in the
+    // cluster coarse kernel), then w -= V h and ||w|| in one pass.
+    __shared__ double2 wpart[kCoarseThreads / 32][kMaxCoarseIters + 1];
+    __shared__ double2 hsum[kMaxCoarseIters + 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double2 wr[kCoarseRowsReg];
+#pragma unroll
+    for (int q = 0; q < kCoarseRowsReg; ++q) {
+      const int64_t k = threadIdx.x + static_cast<int64_t>(q) * kCoarseThreads;
+      wr[q] = k < n ? cw[k] : make_double2(0.0, 0.0);
     }
-    const double hr = block_sum(sr, sh);
-    const double hi = block_sum(si, sh);
-    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
-      const double2 a = Vi[k];
-      double2 w = cw[k];
-      w.x -= hr * a.x - hi * a.y;
-      w.y -= hr * a.y + hi * a.x;
-      cw[k] = w;
+    for (int i = 0; i <= j; ++i) {
+      const double2* Vi = V + i * n;
+      double2 d = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kCoarseRowsReg; ++q) {
+        const int64_t k = threadIdx.x + static_cast<int64_t>(q) * kCoarseThreads;
+        if (k < n) d = cfma_conj(Vi[k], wr[q], d);
+      }
+      d.x = warp_sum(d.x);
+      d.y = warp_sum(d.y);
+      if (lane == 0) wpart[warp][i] = d;
     }
-    if (threadIdx.x == 0) Hm[i + j * ldh] = make_double2(hr, hi);
     __syncthreads();
+    if (threadIdx.x <= j) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int w = 0; w < kCoarseThreads / 32; ++w) t = cadd(t, wpart[w][threadIdx.x]);
+      hsum[threadIdx.x] = t;
+      Hm[threadIdx.x + j * ldh] = t;
+    }
+    __syncthreads();
+    double s2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kCoarseRowsReg; ++q) {
+      const int64_t k = threadIdx.x + static_cast<int64_t>(q) * kCoarseThreads;
+      if (k < n) {
+        double2 w = wr[q];
+        for (int i = 0; i <= j; ++i) w = csub(w, cmul(hsum[i], V[i * n + k]));
+        wr[q] = w;
+        cw[k] = w;
+        s2 += cabs2(w);
+      }
+    }
+    hnext = sqrt(block_sum(s2, sh));
+  } else {
+    for (int i = 0; i <= j; ++i) {
+      const double2* Vi = V + i * n;
+      double sr = 0.0, si = 0.0;
+      for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const double2 a = Vi[k], b = cw[k];
+        sr += a.x * b.x + a.y * b.y;
+        si += a.x * b.y - a.y * b.x;
+      }
+      const double hr = block_sum(sr, sh);
+      const double hi = block_sum(si, sh);
+      for (int64_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const double2 a = Vi[k];
+        double2 w = cw[k];
+        w.x -= hr * a.x - hi * a.y;
+        w.y -= hr * a.y + hi * a.x;
+        cw[k] = w;
+      }
+      if (threadIdx.x == 0) Hm[i + j * ldh] = make_double2(hr, hi);
+      __syncthreads();
+    }
+    double s2 = 0.0;
+    for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s2 += cabs2(cw[k]);
+    hnext = sqrt(block_sum(s2, sh));
   }
-  double s2 = 0.0;
-  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s2 += cabs2(cw[k]);
-  const double hnext = sqrt(block_sum(s2, sh));
   if (threadIdx.x == 0) {
     Hm[j + 1 + j * ldh] = make_double2(hnext, 0.0);
     for (int i = 0; i < j; ++i)
@@ -696,9 +747,18 @@ int split_rows(int total_rows, int sms) {
   // ~8 units per SM: small units balance the SMs (no tail wave) at the cost
   // of re-gathering x per unit (a few % of the matrix bytes at these sizes).
   const int want = (total_rows + 8 * sms - 1) / (8 * sms);
-  if (want <= 8) return 8;
-  if (want <= 16) return 16;
-  return std::min(256, (want + 31) & ~31);
+  int rb = want <= 8 ? 8 : want <= 16 ? 16 : std::min(256, (want + 31) & ~31);
+  // Avoid a sparse second wave: the plan kernel holds 4 CTAs per SM, and
+  // e.g. 4864 rows in 8-row units (608 units for 592 slots) ran as a full
+  // wave plus 16 lone CTAs (ncu, cfg3 coarse matvec: 2.8 TB/s).  Take the
+  // next row block when it fits one wave.
+  static const bool off = std::getenv("HPSB_NO_WAVE_FIT") != nullptr;
+  const int slots = 4 * sms, units = (total_rows + rb - 1) / rb;
+  if (!off && units > slots && units < 2 * slots) {
+    const int rb2 = rb < 16 ? 16 : std::min(256, (2 * rb + 31) & ~31);
+    if ((total_rows + rb2 - 1) / rb2 <= slots) rb = rb2;
+  }
+  return rb;
 }
 
 VItem item(const double2* A, int lda, int rows, int cols, const double2* x, const int* xi,
