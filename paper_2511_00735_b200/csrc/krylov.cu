@@ -469,10 +469,18 @@ struct Work {
   }
   int grid() const { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * ctx->num_sms)); }
   // rows per thread: enough blocks for ~2 per SM, at most kOrthMaxR
+  // At most 2 rows per thread: the update-and-project pass reads each V row
+  // twice, and with short row blocks the second read still hits L2 (cfg3:
+  // R = 8 / 4 / 2 / 1 -> 27.9 / 25.6 / 23.1 / 28.7 ms of orthogonalisation).
   void orth_grid(int& R, int& nb) const {
     R = 1;
-    while (R < kOrthMaxR && (n + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
+    while (R < 2 && (n + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
       R *= 2;
+    static const int force_r = [] {
+      const char* e = std::getenv("HPSB_ORTH_R");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (force_r >= 1 && force_r <= kOrthMaxR) R = force_r;
     nb = static_cast<int>((n + kOrthThreads * R - 1) / (kOrthThreads * R));
   }
   void reserve(int maxcols) {  // partial sums for maxcols columns (before a graph capture)
