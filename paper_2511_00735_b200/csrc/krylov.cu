@@ -373,6 +373,17 @@ __global__ void arn_copy_col_kernel(const double2* __restrict__ src, double2* ds
     dst[k] = src[k];
 }
 
+// Rows per thread cap of the multi-RHS CGS2 passes (HPSB_ORTH_RR overrides;
+// cfg4: 8 and 2 measured equal, 5.2-5.3 TB/s).
+int orth_rr_cap() {
+  static const int c = [] {
+    const char* e = std::getenv("HPSB_ORTH_RR");
+    const int v = e ? std::atoi(e) : kOrthMaxR;
+    return v >= 1 && v <= kOrthMaxR ? v : kOrthMaxR;
+  }();
+  return c;
+}
+
 // Hessenberg column j from the CGS2 coefficients (h = h1 + h2, h_{j+1,j} =
 // ||w||), previous rotations, the new rotation, the residual estimate and the
 // loop decision -- the host loop body of fgmres (krylov.cpp:102-123).
@@ -867,7 +878,7 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   DevBuf<unsigned> tickets(R);
   HPSB_CUDA(cudaMemsetAsync(tickets.p, 0, sizeof(unsigned) * R, ctx->stream));
   int RR = 1;  // rows per thread of the orth kernel
-  while (RR < kOrthMaxR && (n + kOrthThreads * 2 * RR - 1) / (kOrthThreads * 2 * RR) >= 2 * ctx->num_sms)
+  while (RR < orth_rr_cap() && (n + kOrthThreads * 2 * RR - 1) / (kOrthThreads * 2 * RR) >= 2 * ctx->num_sms)
     RR *= 2;
   const int nb = static_cast<int>((n + kOrthThreads * RR - 1) / (kOrthThreads * RR));
   const int64_t pstride = static_cast<int64_t>(nb) * (restart + 2);
