@@ -105,6 +105,11 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
   }
   const int arow = wm * 32 + (lane >> 2), kq = lane & 3;
   const int bcol = wn * 16 + (lane >> 2);
+  // Edge tiles: fragments wholly outside M x N and k-steps past K are
+  // skipped (warp-uniform), so ragged merge dimensions (multiples of N-1,
+  // e.g. 76 = 64 + 12) do not pay for a full padded tile on the DMMA pipe.
+  const int ni_act = max(0, min(4, (d.M - m0 - wm * 32 + 7) / 8));
+  const int nj_act = max(0, min(2, (d.N - n0 - wn * 16 + 7) / 8));
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -112,8 +117,10 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
     cp_async_commit();
     const double2* as = As + (kt % STAGES) * A_STAGE;
     const double2* bs = Bs + (kt % STAGES) * B_STAGE;
+    const int krem = d.K - kt * BK;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
+      if (kk >= krem) break;
       double2 a[4], b[2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
@@ -125,19 +132,23 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+        for (int j = 0; j < 2; ++j)
+          if (i < ni_act && j < nj_act) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+        for (int j = 0; j < 2; ++j)
+          if (i < ni_act && j < nj_act) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
+        for (int j = 0; j < 2; ++j)
+          if (i < ni_act && j < nj_act) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+        for (int j = 0; j < 2; ++j)
+          if (i < ni_act && j < nj_act) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
     }
   }
   cp_async_wait<0>();
