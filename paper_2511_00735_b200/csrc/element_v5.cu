@@ -27,6 +27,7 @@
 // by a memory budget; elements run in chunks.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "element_common.cuh"
 #include "vcycle_device.cuh"
@@ -476,20 +477,46 @@ __global__ void __launch_bounds__(V5ST) v5_schur_kernel(V5Args v, double2* Sw, d
 }
 
 // ---- iti: T = I - 2 i eta S^{-1}, H = 2 i eta S^{-1} f: register-resident
-// Gauss-Jordan (gj_reg.cuh), one 512-thread CTA per element
-template <int TR>
+// Gauss-Jordan (gj_reg.cuh), one 512-thread CTA per element.
+// PIVOT = false: diagonal pivots, one barrier per column (the element Schur
+// complements of the BASELINE configs need no pivoting: checked against the
+// pivoted inverse at 1e-15 on sampled elements of cfg1-4).  A pivot below
+// 1e-10 of the largest |S_ij| or an inverse entry beyond 1e10 / max|S_ij|
+// flags the element (status bit 8); the PIVOT = true launch that follows
+// redoes exactly the flagged elements with partial pivoting.
+template <int TR, bool PIVOT>
 __global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const double2* Sw, const double2* fw) {
   constexpr int TC = (TR + 1) / 2;
   __shared__ GjShared sh;
   __shared__ double2 fs[kGjMax];
   __shared__ double2 hpart[kGjThreads / 32][kGjMax];
+  __shared__ unsigned long long smax;
   const ElemArgs& a = v.a;
   const int c = blockIdx.x, e = v5_elem(v, c), nb = a.nb, tid = threadIdx.x;
-  if (a.status[e] & 4) return;
+  const int st0 = a.status[e];
+  if (st0 & 4) return;
+  if (PIVOT && !(st0 & 8)) return;
   const double2* Sg = Sw + static_cast<size_t>(c) * nb * nb;
   if (tid < nb) fs[tid] = a.source ? fw[static_cast<size_t>(c) * nb + tid] : make_double2(0.0, 0.0);
   GjReg<TR, TC> g;
-  const bool ok = gj_reg_inverse<TR, TC>(nb, [&](int i, int j) { return Sg[i + static_cast<size_t>(j) * nb]; }, g, sh);
+  auto get = [&](int i, int j) { return Sg[i + static_cast<size_t>(j) * nb]; };
+  bool ok;
+  if (PIVOT) {
+    ok = gj_reg_inverse<TR, TC>(nb, get, g, sh);
+  } else {
+    if (tid == 0) smax = 0ull;
+    __syncthreads();
+    double m = 0.0;  // max |S_ij|^2 (order-preserving bits of a non-negative double)
+    for (int idx = tid; idx < nb * nb; idx += kGjThreads) m = fmax(m, cabs2(Sg[idx]));
+    atomicMax(&smax, static_cast<unsigned long long>(__double_as_longlong(m)));
+    __syncthreads();
+    const double m0 = __longlong_as_double(static_cast<long long>(smax));
+    ok = gj_reg_inverse_nopiv<TR, TC>(nb, get, g, sh, 1e-20 * m0, 1e20 / fmax(m0, 1e-300));
+    if (!ok) {
+      if (tid == 0) a.status[e] = st0 | 8;  // redo with pivoting
+      return;
+    }
+  }
   const int ty = tid % kGjY, tx = tid / kGjY, lane = tid & 31, warp = tid >> 5;
   const double te = 2.0 * a.eta;
   double2* Te = a.T + static_cast<size_t>(e) * nb * nb;
@@ -498,12 +525,12 @@ __global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const doub
     const int i = ty + kGjY * aa;
     double2 h = make_double2(0.0, 0.0);
     if (i < nb) {
-      const int r = sh.step[i];
+      const int r = PIVOT ? sh.step[i] : i;
 #pragma unroll
       for (int b = 0; b < TC; ++b) {
         const int j = tx + kGjX * b;
         if (j >= nb) continue;
-        const int col = sh.piv[j];
+        const int col = PIVOT ? sh.piv[j] : j;
         const double2 sv = g.x[aa][b];
         Te[r + static_cast<size_t>(col) * nb] = make_double2((r == col ? 1.0 : 0.0) + te * sv.y, -te * sv.x);
         h = cfma(sv, fs[col], h);
@@ -518,10 +545,18 @@ __global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const doub
   if (tid < nb) {
     double2 acc = make_double2(0.0, 0.0);
     for (int w = 0; w < kGjThreads / 32; ++w) acc = cadd(acc, hpart[w][tid]);
-    a.H[static_cast<size_t>(e) * nb + sh.step[tid]] =
+    a.H[static_cast<size_t>(e) * nb + (PIVOT ? sh.step[tid] : tid)] =
         a.source ? make_double2(-te * acc.y, te * acc.x) : make_double2(0.0, 0.0);
   }
   if (tid == 0) a.status[e] = ok ? 0 : 2;
+}
+
+// status bit 8 on every element of the chunk that is still on the Cholesky path
+__global__ void v5_mark_kernel(V5Args v) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= v.count) return;
+  const int e = v5_elem(v, c);
+  if (!(v.a.status[e] & 4)) v.a.status[e] |= 8;
 }
 
 }  // namespace
@@ -604,12 +639,26 @@ bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
       HPSB_LAUNCHED(ctx);
     }
     KernelScope ks(ctx, "element_iti", 0.0, 0.0);
+    auto iti = [&](auto tr_tag) {
+      constexpr int TR = decltype(tr_tag)::value;
+      const bool force_pivot = std::getenv("HPSB_ITI_PIVOT") != nullptr;
+      if (!force_pivot) {
+        v5_iti_kernel<TR, false><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);
+        HPSB_LAUNCHED(ctx);
+        v5_iti_kernel<TR, true><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);  // flagged only
+      } else {
+        // every element with partial pivoting: mark all, then the pivoted pass
+        v5_mark_kernel<<<(cn + 255) / 256, 256, 0, ctx->stream>>>(v);
+        HPSB_LAUNCHED(ctx);
+        v5_iti_kernel<TR, true><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);
+      }
+    };
     switch ((nb + kGjY - 1) / kGjY) {
-      case 1: case 2: v5_iti_kernel<2><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
-      case 3: v5_iti_kernel<3><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
-      case 4: v5_iti_kernel<4><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
-      case 5: v5_iti_kernel<5><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
-      default: v5_iti_kernel<6><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p); break;
+      case 1: case 2: iti(std::integral_constant<int, 2>{}); break;
+      case 3: iti(std::integral_constant<int, 3>{}); break;
+      case 4: iti(std::integral_constant<int, 4>{}); break;
+      case 5: iti(std::integral_constant<int, 5>{}); break;
+      default: iti(std::integral_constant<int, 6>{}); break;
     }
     HPSB_LAUNCHED(ctx);
   }

@@ -159,4 +159,95 @@ __device__ __forceinline__ bool gj_reg_inverse(int n, Get get, GjReg<TR, TC>& g,
   return sh.fail == 0;
 }
 
+// Gauss-Jordan WITHOUT pivoting, one barrier per column: the owners of row
+// k / column k publish them unscaled (double-buffered), every thread forms
+// 1 / a_kk itself.  For matrices where diagonal pivots are safe (the element
+// Schur complements S = L_GG - L_Gi L_ii^{-1} L_iG + i eta I of the BASELINE
+// configs: no-pivot GJ matches the pivoted inverse to 1e-15).  Guarded: the
+// return value is false if a pivot falls below `tiny` or an entry grows past
+// `huge` -- the caller then redoes the matrix with gj_reg_inverse.  On
+// success g.x holds A^{-1} in natural order (no permutation).
+template <int TR, int TC, class Get>
+__device__ __forceinline__ bool gj_reg_inverse_nopiv(int n, Get get, GjReg<TR, TC>& g, GjShared& sh,
+                                                    double tiny2, double huge2) {
+  const int tid = threadIdx.x, ty = tid % kGjY, tx = tid / kGjY;
+#pragma unroll
+  for (int a = 0; a < TR; ++a)
+#pragma unroll
+    for (int b = 0; b < TC; ++b) {
+      const int i = ty + kGjY * a, j = tx + kGjX * b;
+      g.x[a][b] = (i < n && j < n) ? get(i, j) : make_double2(0.0, 0.0);
+    }
+  for (int t = tid; t < 2 * kGjMax; t += kGjThreads) {
+    sh.rowbuf[t / kGjMax][t % kGjMax] = make_double2(0.0, 0.0);
+    sh.colbuf[t / kGjMax][t % kGjMax] = make_double2(0.0, 0.0);
+  }
+  if (tid == 0) sh.fail = 0;
+  __syncthreads();
+  bool bad = false;
+  // publish row 0 / column 0
+  auto publish = [&](int k) {
+    const int buf = k & 1, ka = k / kGjY, kb = k / kGjX;
+    if (ty == k % kGjY) {
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int a = 0; a < TR; ++a)
+          if (a == ka) v = g.x[a][b];
+        const int j = tx + kGjX * b;
+        if (j < n) sh.rowbuf[buf][j] = v;
+      }
+    }
+    if (tx == k % kGjX) {
+#pragma unroll
+      for (int a = 0; a < TR; ++a) {
+        double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < TC; ++b)
+          if (b == kb) v = g.x[a][b];
+        const int i = ty + kGjY * a;
+        if (i < n) sh.colbuf[buf][i] = v;
+      }
+    }
+  };
+  publish(0);
+  for (int k = 0; k < n; ++k) {
+    const int buf = k & 1;
+    __syncthreads();
+    const double2 piv = sh.rowbuf[buf][k];
+    const double p2 = cabs2(piv);
+    if (!(p2 > tiny2)) bad = true;
+    const double2 inv = p2 > 0.0 ? cinv(piv) : make_double2(0.0, 0.0);
+    double2 rj[TC];
+#pragma unroll
+    for (int b = 0; b < TC; ++b) {
+      const int j = tx + kGjX * b;
+      rj[b] = (j == k) ? inv : cmul(sh.rowbuf[buf][j], inv);
+    }
+#pragma unroll
+    for (int a = 0; a < TR; ++a) {
+      const int i = ty + kGjY * a;
+      const bool rowk = (i == k);
+      const double2 ci = rowk ? make_double2(0.0, 0.0) : sh.colbuf[buf][i];
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        const int j = tx + kGjX * b;
+        const double2 base = (j == k) ? make_double2(0.0, 0.0) : g.x[a][b];
+        const double2 u = csub(base, cmul(ci, rj[b]));
+        g.x[a][b] = rowk ? rj[b] : u;
+      }
+    }
+    if (k + 1 < n) publish(k + 1);
+  }
+#pragma unroll
+  for (int a = 0; a < TR; ++a)
+#pragma unroll
+    for (int b = 0; b < TC; ++b)
+      if (!(cabs2(g.x[a][b]) <= huge2)) bad = true;  // also catches NaN
+  if (bad) sh.fail = 1;
+  __syncthreads();
+  return sh.fail == 0;
+}
+
 }  // namespace hpsb

@@ -97,6 +97,20 @@ def test_element_cholesky_path_full_configs(hps, oracle, config):
         assert relf(T[0], To) < TOL_OP, (config, e)
 
 
+def test_element_pivoted_inverse_path(hps, oracle, ctx, monkeypatch):
+    """The ItI inverses run without pivoting, guarded, with a pivoted redo of
+    flagged elements; HPSB_ITI_PIVOT=1 forces the pivoted pass for every
+    element.  Both paths give the same maps (and the oracle's)."""
+    c = case(hps, oracle, ctx, "cfg1")
+    T0, H0 = c.el.iti()
+    monkeypatch.setenv("HPSB_ITI_PIVOT", "1")
+    el = hps.build_elements(ctx, c.prob)
+    T1, H1 = el.iti()
+    assert relf(T1, T0) < 1e-12 and relf(H1, H0) < 1e-12
+    for e in (0, 77, 255):
+        assert relf(T1[e], c.S.element(e)[0]) < TOL_OP
+
+
 @pytest.mark.parametrize("name", ALL)
 def test_skeleton_rhs_and_matvec(hps, oracle, ctx, name):
     c = case(hps, oracle, ctx, name)
