@@ -128,6 +128,14 @@ hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, do
  * hpsb_problem_sample (nrhs right-hand sides).                              */
 hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs,
                                  hpsb_skeleton* out);
+/* Same, with t given on the physical boundary only, as boundary_side_data
+ * produces it (proj/src/mesh.cpp:111-139): tbnd[nrhs][4][n][N-1] complex,
+ * domain sides x=0, x=1, y=0, y=1, each with its n elements in ascending
+ * order (y for the vertical sides, x for the horizontal ones) and the N-1
+ * side nodes ascending.  Moves 4n(N-1) values per right-hand side instead of
+ * n^2 4(N-1).                                                               */
+hpsb_status hpsb_skeleton_create_boundary(hpsb_elements el, const double* tbnd, int nrhs,
+                                          hpsb_skeleton* out);
 hpsb_status hpsb_skeleton_destroy(hpsb_skeleton sk);
 int64_t hpsb_skeleton_dim(hpsb_skeleton sk);
 hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs);

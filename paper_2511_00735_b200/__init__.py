@@ -94,6 +94,7 @@ _sig("hpsb_elements_build_dev", _st, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_d
 _sig("hpsb_elements_destroy", _st, _VP)
 _sig("hpsb_elements_get", _st, _VP, ctypes.c_int, ctypes.c_int, _D, _D)
 _sig("hpsb_skeleton_create", _st, _VP, _D, ctypes.c_int, ctypes.POINTER(_VP))
+_sig("hpsb_skeleton_create_boundary", _st, _VP, _D, ctypes.c_int, ctypes.POINTER(_VP))
 _sig("hpsb_skeleton_destroy", _st, _VP)
 _sig("hpsb_skeleton_dim", ctypes.c_int64, _VP)
 _sig("hpsb_skeleton_rhs", _st, _VP, ctypes.c_int, _D)
@@ -401,11 +402,29 @@ class SkeletonSystem(_Handle):
         return field
 
 
-def assemble_skeleton(elements: ElementRecords, prob: Problem) -> SkeletonSystem:
+def boundary_trace(tside: np.ndarray, n: int) -> np.ndarray:
+    """[nrhs, n^2, 4, N-1] element-side data -> [nrhs, 4, n, N-1] physical-side
+    data (boundary_side_data order, proj/src/mesh.cpp:111-139): x=0, x=1, y=0,
+    y=1, each side's n elements ascending."""
+    t = tside.reshape(tside.shape[0], n, n, 4, -1)  # [r, ey, ex, side, k]
+    return np.ascontiguousarray(np.stack(
+        [t[:, :, 0, 0], t[:, :, n - 1, 1], t[:, 0, :, 2], t[:, n - 1, :, 3]], axis=1))
+
+
+def assemble_skeleton(elements: ElementRecords, prob: Problem,
+                      boundary_only: bool = True) -> SkeletonSystem:
+    """assemble_skeleton (proj/src/skeleton.cpp:88-137).  By default only the
+    physical-boundary data crosses to the device (hpsb_skeleton_create_boundary);
+    boundary_only=False passes the full element-side layout."""
     t = _cplx(prob.tside)
     h = _VP()
-    _check(_lib.hpsb_skeleton_create(elements._h, _dp(t.view(np.float64)), t.shape[0],
-                                     ctypes.byref(h)))
+    if boundary_only:
+        tb = boundary_trace(t, prob.n)
+        _check(_lib.hpsb_skeleton_create_boundary(elements._h, _dp(tb.view(np.float64)),
+                                                  t.shape[0], ctypes.byref(h)))
+    else:
+        _check(_lib.hpsb_skeleton_create(elements._h, _dp(t.view(np.float64)), t.shape[0],
+                                         ctypes.byref(h)))
     return SkeletonSystem(elements, h, t.shape[0])
 
 

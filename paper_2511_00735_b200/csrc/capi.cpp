@@ -467,6 +467,17 @@ hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs
   });
 }
 
+hpsb_status hpsb_skeleton_create_boundary(hpsb_elements el, const double* tbnd, int nrhs,
+                                          hpsb_skeleton* out) {
+  return guarded([&] {
+    REQUIRE(el && out && tbnd && nrhs >= 1, "skeleton_create_boundary: bad argument");
+    auto h = std::make_unique<hpsb_skeleton_s>();
+    h->s = hpsb::build_skeleton(el->e.get(), reinterpret_cast<const double2*>(tbnd), nrhs, true);
+    *out = h.release();
+    return HPSB_OK;
+  });
+}
+
 hpsb_status hpsb_skeleton_destroy(hpsb_skeleton sk) {
   delete sk;
   return HPSB_OK;

@@ -360,7 +360,10 @@ struct Precond;
 // ---------------------------------------------------------------- entry points
 std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double eta,
                                          const double* coeff_dev, const double2* source_dev);
-std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs);
+// tside_host: [nrhs][e][4][N-1] (boundary_only false) or the physical sides
+// only, [nrhs][4][n][N-1] (boundary_only true).
+std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs,
+                                         bool boundary_only = false);
 void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev);
 // Multi-RHS: R <= 32 vectors stored column-wise with leading dimension dim.
 void precond_apply_batch(Precond* p, const double2* v, double2* z, int R);

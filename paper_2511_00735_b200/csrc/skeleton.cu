@@ -40,9 +40,30 @@ __global__ void skeleton_rhs_kernel(const double2* __restrict__ T, const double2
     }
   }
 }
+
+// Expand the physical-boundary data tb[r][side][j][m] (boundary_side_data,
+// proj/src/mesh.cpp:111-139: per physical side, its n elements in ascending
+// order, N-1 nodes each) into the zeroed element layout t[r][e][nb]: side 0
+// (x=0) is element side 0 of e = j*n, side 1 (x=1) side 1 of e = j*n+n-1,
+// side 2 (y=0) side 2 of e = j, side 3 (y=1) side 3 of e = (n-1)*n+j.
+__global__ void tside_expand_kernel(const double2* __restrict__ tb, double2* __restrict__ t, int n,
+                                    int m, int nrhs) {
+  const int64_t total = static_cast<int64_t>(nrhs) * 4 * n * m;
+  const int nb = 4 * m;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % m);
+    const int j = static_cast<int>((i / m) % n);
+    const int side = static_cast<int>((i / (static_cast<int64_t>(m) * n)) % 4);
+    const int64_t r = i / (4LL * n * m);
+    const int e = side == 0 ? j * n : side == 1 ? j * n + n - 1 : side == 2 ? j : (n - 1) * n + j;
+    t[(r * n * n + e) * nb + side * m + k] = tb[i];
+  }
+}
 }  // namespace
 
-std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs) {
+std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs,
+                                         bool boundary_only) {
   Context* ctx = el->ctx;
   auto sk = std::make_unique<Skeleton>();
   sk->ctx = ctx;
@@ -76,7 +97,23 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
   HPSB_CUDA(cudaMemsetAsync(sk->rhs.p, 0, sk->rhs.bytes(), ctx->stream));
   DevBuf<double2>& d_t = sk->tside;  // kept for the solution recovery
   d_t.alloc(static_cast<size_t>(nrhs) * ne * nb);
-  HPSB_CUDA(cudaMemcpyAsync(d_t.p, tside_host, d_t.bytes(), cudaMemcpyHostToDevice, ctx->stream));
+  if (boundary_only) {
+    // Only the 4n physical sides carry data: copy those (cfg4: 5.8 MB instead
+    // of the 1.5 GB element layout) and expand on the device.
+    DevBuf<double2> d_tb;
+    d_tb.alloc(static_cast<size_t>(nrhs) * 4 * el->n * m);
+    HPSB_CUDA(cudaMemcpyAsync(d_tb.p, tside_host, d_tb.bytes(), cudaMemcpyHostToDevice,
+                              ctx->stream));
+    HPSB_CUDA(cudaMemsetAsync(d_t.p, 0, d_t.bytes(), ctx->stream));
+    KernelScope ks(ctx, "skeleton_tside", 32.0 * d_tb.n, 0.0);
+    tside_expand_kernel<<<std::min<int64_t>((d_tb.n + 255) / 256, 148 * 8), 256, 0,
+                          ctx->stream>>>(d_tb.p, d_t.p, el->n, m, nrhs);
+    HPSB_LAUNCHED(ctx);
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));  // d_tb is freed on return
+  } else {
+    HPSB_CUDA(cudaMemcpyAsync(d_t.p, tside_host, d_t.bytes(), cudaMemcpyHostToDevice,
+                              ctx->stream));
+  }
   DevBuf<int> d_own;
   if (sharded) d_own.upload(own, ctx->stream);
   const int nwork = sharded ? static_cast<int>(own.size()) : ne;

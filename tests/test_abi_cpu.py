@@ -100,3 +100,23 @@ def test_no_gpu_fails_loudly(hps):
     with pytest.raises(hps.HpsError) as e:
         hps.Context(0)
     assert e.value.status == hps.INTERNAL
+
+
+@pytest.mark.parametrize("config", [0, 4])
+def test_boundary_trace_holds_every_physical_value(hps, config):
+    """hpsb_skeleton_create_boundary's layout: the element-side array is zero
+    off the physical boundary, and boundary_trace picks each physical side's
+    data in boundary_side_data order (proj/src/mesh.cpp:111-139)."""
+    p = hps.problem(2, config, n=8 if config == 4 else 0)
+    n = p.n
+    tb = hps.boundary_trace(p.tside, n)
+    assert tb.shape == (p.tside.shape[0], 4, n, p.order - 1)
+    t = p.tside.reshape(p.tside.shape[0], n, n, 4, -1)
+    for j in range(n):
+        assert np.array_equal(tb[:, 0, j], t[:, j, 0, 0])
+        assert np.array_equal(tb[:, 1, j], t[:, j, n - 1, 1])
+        assert np.array_equal(tb[:, 2, j], t[:, 0, j, 2])
+        assert np.array_equal(tb[:, 3, j], t[:, n - 1, j, 3])
+    # nothing but the physical sides is nonzero
+    assert np.isclose(np.abs(tb).sum(), np.abs(p.tside).sum(), rtol=0, atol=0)
+    assert np.count_nonzero(tb) == np.count_nonzero(p.tside) > 0

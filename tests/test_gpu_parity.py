@@ -126,6 +126,21 @@ def test_skeleton_rhs_and_matvec(hps, oracle, ctx, name):
     assert relf(c.sk.apply(x), c.S.apply_M(x)) < TOL_OP
 
 
+@pytest.mark.parametrize("name", ["cfg0", "pw_n4_N16", "cfg4_n8"])
+def test_skeleton_boundary_layout_matches_element_layout(hps, oracle, ctx, name):
+    """hpsb_skeleton_create_boundary (physical sides only) and
+    hpsb_skeleton_create (element-side layout) give bit-identical right-hand
+    sides and recovered fields for every right-hand side."""
+    c = case(hps, oracle, ctx, name)
+    sk_full = hps.assemble_skeleton(c.el, c.prob, boundary_only=False)
+    assert sk_full.nrhs == c.sk.nrhs == c.prob.tside.shape[0]
+    for r in range(c.sk.nrhs):
+        assert np.array_equal(c.sk.rhs(r), sk_full.rhs(r))
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal(c.sk.dim) + 1j * rng.standard_normal(c.sk.dim)
+    assert np.array_equal(c.sk.recover(g, c.sk.nrhs - 1), sk_full.recover(g, c.sk.nrhs - 1))
+
+
 @pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg3_n4", "cfg2_n8"])
 def test_hierarchy_level_systems(hps, oracle, ctx, name):
     c = case(hps, oracle, ctx, name)
