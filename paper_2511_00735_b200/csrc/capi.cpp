@@ -556,6 +556,8 @@ hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
       if (hh->depth < 2 || hh->ctx->profile || std::getenv("HPSB_NO_PENDING_PRECOND")) return;
       hpsb_mg_config c{};
       c.depth = hh->depth, c.gamma = 1, c.coarse_iters = 4, c.exact_coarse = 0;
+      hpsb::destroy_precond(hs->pending);  // a discarded first pass (pivot redo)
+      hs->pending = nullptr;
       try {
         hs->pending = hpsb::create_precond(hh, c);
       } catch (...) {

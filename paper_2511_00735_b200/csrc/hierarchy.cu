@@ -112,8 +112,12 @@ struct GroupPlan {
 };
 }  // namespace
 
-std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
-                                           const std::function<void(Hierarchy*)>& before_wait) {
+// pivot = false: the merge inverses use diagonal pivots (InverseBatch
+// diag_pivots); *guard_tripped reports a blocked inverse whose diagonal block
+// failed the guard, and build_hierarchy then redoes the build with pivoting.
+std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
+                                                const std::function<void(Hierarchy*)>& before_wait,
+                                                bool pivot, bool* guard_tripped) {
   Context* ctx = sk->ctx;
   const FaceGraph& g = sk->graph;
   const int total = g.num_levels();
@@ -149,8 +153,8 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
   std::vector<int> pos_of(sk->dim, -1);
   std::vector<int> prev_merge_of;  // previous level: group (= box of this level) -> merge index
   DevBuf<double2> tnew_prev;  // previous level's merged maps (children of this level)
-  DevBuf<int> d_status(1);
-  HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, sizeof(int), ctx->stream));
+  DevBuf<int> d_status(2);  // [0] singular pivot tag + 1, [1] diagonal-pivot guard
+  HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, 2 * sizeof(int), ctx->stream));
 
   HPSB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
   Trace tr;
@@ -361,6 +365,8 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
       }
       pre.run(ctx);
       g1.run(ctx);
+      inv.diag_pivots = !pivot;
+      inv.guard_dev = d_status.p + 1;
       inv.run(ctx, d_status.p);
       g2.run(ctx);
       g3.run(ctx);
@@ -415,11 +421,12 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
   // until the stream drains (before the hook could overlap it)
   thread_local int* st_pinned = [] {
     int* q = nullptr;
-    HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&q), sizeof(int)));
+    HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&q), 2 * sizeof(int)));
     return q;
   }();
-  *st_pinned = 0;
-  HPSB_CUDA(cudaMemcpyAsync(st_pinned, d_status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  st_pinned[0] = st_pinned[1] = 0;
+  HPSB_CUDA(cudaMemcpyAsync(st_pinned, d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                            ctx->stream));
   if (before_wait) {
     // the hook's own device work is stream-ordered after the merges: record
     // the build's end event first (above), so build_seconds stays the merges'
@@ -428,7 +435,9 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
   }
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   tr.mark("final_wait");
-  const int st = *st_pinned;
+  const int st = st_pinned[0];
+  *guard_tripped = st_pinned[1] != 0 || (!pivot && std::getenv("HPSB_TEST_GUARD_TRIP"));
+  if (*guard_tripped) return h;  // results unused: the caller redoes the build
   if (st) {  // first singular group pivot (inverse status tag = level << 20 | group) + 1
     const int tag = st - 1, level = tag >> 20, gi = tag & ((1 << 20) - 1);
     throw std::runtime_error("eliminate_level: singular merge block at face " +
@@ -437,6 +446,18 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
   float ms = 0;
   HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
   h->build_seconds = ms * 1e-3;
+  return h;
+}
+
+std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
+                                           const std::function<void(Hierarchy*)>& before_wait) {
+  const bool pivot = std::getenv("HPSB_MERGE_PIVOT") != nullptr;
+  bool tripped = false;
+  auto h = build_hierarchy_pass(sk, depth, before_wait, pivot, &tripped);
+  if (!tripped) return h;
+  h.reset();
+  h = build_hierarchy_pass(sk, depth, before_wait, true, &tripped);
+  h->pivot_redone = true;
   return h;
 }
 

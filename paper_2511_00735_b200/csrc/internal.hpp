@@ -352,6 +352,7 @@ struct Hierarchy {
   std::vector<std::unique_ptr<LevelOps>> levels;  // levels[l-1], l = 1..depth
   double build_seconds = 0;
   int64_t device_bytes = 0;
+  bool pivot_redone = false;  // diagonal-pivot guard tripped: rebuilt with partial pivoting
   ~Hierarchy();
 };
 

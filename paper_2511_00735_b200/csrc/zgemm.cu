@@ -204,18 +204,56 @@ __global__ void copy_ops_kernel(const CopyOp* __restrict__ ops, int nops) {
 }
 
 // One CTA per matrix: complex Gauss-Jordan inverse (n <= kSmemInvMax), the
-// matrix register-resident across 512 threads (gj_reg.cuh); the permuted
-// result is written back in place.
-template <int TR>
+// matrix register-resident across 512 threads (gj_reg.cuh); the result is
+// written back in place.  MODE 0: partial pivoting.  MODE 1: diagonal
+// pivots, guarded -- written only if the guard holds, else flags[op] = 1
+// (flags != null: the MODE 2 launch that follows redoes it) or guard[0] = 1.
+// MODE 2: partial pivoting of the flagged matrices only.
+// Diagonal pivots are safe for the merge blocks W = I - T2_ss T1_ss: ItI maps
+// of passive media are contractions (unitary when lossless), so W has a
+// positive definite Hermitian part, and so do its leading blocks and Schur
+// complements.
+template <int TR, int MODE>
 __global__ void __launch_bounds__(kGjThreads) inverse_reg_kernel(const InvOp* __restrict__ ops,
-                                                                 int* status) {
+                                                                 int* status, int* flags,
+                                                                 int* guard) {
   constexpr int TC = (TR + 1) / 2;
   __shared__ GjShared sh;
   const InvOp op = ops[blockIdx.x];
+  if (MODE == 2 && !flags[blockIdx.x]) return;
   GjReg<TR, TC> g;
-  const bool ok = gj_reg_inverse<TR, TC>(
-      op.n, [&](int i, int j) { return op.A[(size_t)i + (size_t)j * op.lda]; }, g, sh);
+  auto get = [&](int i, int j) { return op.A[(size_t)i + (size_t)j * op.lda]; };
   const int ty = threadIdx.x % kGjY, tx = threadIdx.x / kGjY;
+  if (MODE == 1) {
+    __shared__ unsigned long long smax;
+    if (threadIdx.x == 0) smax = 0ull;
+    __syncthreads();
+    double m = 0.0;  // max |a_ij|^2 (order-preserving bits of a non-negative double)
+    for (int idx = threadIdx.x; idx < op.n * op.n; idx += kGjThreads)
+      m = fmax(m, cabs2(get(idx % op.n, idx / op.n)));
+    atomicMax(&smax, static_cast<unsigned long long>(__double_as_longlong(m)));
+    __syncthreads();
+    const double m0 = __longlong_as_double(static_cast<long long>(smax));
+    if (!gj_reg_inverse_nopiv<TR, TC>(op.n, get, g, sh, 1e-20 * m0, 1e20 / fmax(m0, 1e-300))) {
+      if (threadIdx.x == 0) {
+        if (flags) flags[blockIdx.x] = 1;
+        else *guard = 1;
+      }
+      return;
+    }
+#pragma unroll
+    for (int a = 0; a < TR; ++a) {
+      const int i = ty + kGjY * a;
+      if (i >= op.n) continue;
+#pragma unroll
+      for (int b = 0; b < TC; ++b) {
+        const int j = tx + kGjX * b;
+        if (j < op.n) op.A[(size_t)i + (size_t)j * op.lda] = g.x[a][b];
+      }
+    }
+    return;
+  }
+  const bool ok = gj_reg_inverse<TR, TC>(op.n, get, g, sh);
 #pragma unroll
   for (int a = 0; a < TR; ++a) {
     const int i = ty + kGjY * a;
@@ -228,6 +266,18 @@ __global__ void __launch_bounds__(kGjThreads) inverse_reg_kernel(const InvOp* __
     }
   }
   if (threadIdx.x == 0 && !ok) status[0] = op.tag + 1;
+}
+
+template <int MODE>
+void launch_inverse_reg(int nmax, int grid, cudaStream_t st, const InvOp* ops, int* status,
+                        int* flags, int* guard) {
+  switch ((nmax + kGjY - 1) / kGjY) {
+    case 0: case 1: case 2: inverse_reg_kernel<2, MODE><<<grid, kGjThreads, 0, st>>>(ops, status, flags, guard); break;
+    case 3: inverse_reg_kernel<3, MODE><<<grid, kGjThreads, 0, st>>>(ops, status, flags, guard); break;
+    case 4: inverse_reg_kernel<4, MODE><<<grid, kGjThreads, 0, st>>>(ops, status, flags, guard); break;
+    case 5: inverse_reg_kernel<5, MODE><<<grid, kGjThreads, 0, st>>>(ops, status, flags, guard); break;
+    default: inverse_reg_kernel<6, MODE><<<grid, kGjThreads, 0, st>>>(ops, status, flags, guard); break;
+  }
 }
 
 // ---- pivot selection for one panel, one thread-block CLUSTER per matrix.
@@ -519,14 +569,25 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     for (const auto& o : small) fl += 8.0 * o.n * double(o.n) * o.n;
     KernelScope ks(ctx, "zinverse_smem", 0.0, fl);
     const int grid = static_cast<int>(small.size());
-    switch ((nmax + kGjY - 1) / kGjY) {
-      case 0: case 1: case 2: inverse_reg_kernel<2><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
-      case 3: inverse_reg_kernel<3><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
-      case 4: inverse_reg_kernel<4><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
-      case 5: inverse_reg_kernel<5><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
-      default: inverse_reg_kernel<6><<<grid, kGjThreads, 0, ctx->stream>>>(d_small.p, status_dev); break;
+    if (diag_pivots) {
+      // per-matrix redo of guard failures, unless the caller takes them
+      // (blocked diagonal blocks: guard_dev)
+      int* flags = nullptr;
+      if (!guard_dev) {
+        d_flags.alloc(small.size());
+        HPSB_CUDA(cudaMemsetAsync(d_flags.p, 0, d_flags.bytes(), ctx->stream));
+        flags = d_flags.p;
+      }
+      launch_inverse_reg<1>(nmax, grid, ctx->stream, d_small.p, status_dev, flags, guard_dev);
+      HPSB_LAUNCHED(ctx);
+      if (flags) {
+        launch_inverse_reg<2>(nmax, grid, ctx->stream, d_small.p, status_dev, flags, guard_dev);
+        HPSB_LAUNCHED(ctx);
+      }
+    } else {
+      launch_inverse_reg<0>(nmax, grid, ctx->stream, d_small.p, status_dev, nullptr, nullptr);
+      HPSB_LAUNCHED(ctx);
     }
-    HPSB_LAUNCHED(ctx);
   }
   if (!large.empty()) {
     // Blocked Gauss-Jordan with partial pivoting: for each panel K of kb
@@ -555,8 +616,10 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     DevBuf<double2> panel(static_cast<size_t>(perm_total) * kb), U(static_cast<size_t>(perm_total) * kb),
         Q(static_cast<size_t>(perm_total) * kb);
     std::vector<InvOp> pivops(large.size());
+    // diag_pivots needs a guard word for the diagonal blocks (no redo)
+    const bool diag = diag_pivots && guard_dev;
     for (int k0 = 0; k0 < nmax; k0 += kb) {
-      {
+      if (!diag) {
         KernelScope ks(ctx, "zinverse_panel", 0.0, 0.0);
         if (std::getenv("HPSB_GJ_PANEL_V1")) {
           panel_pivot_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(
@@ -580,7 +643,7 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
           HPSB_LAUNCHED(ctx);
         }
       }
-      {
+      if (!diag) {
         KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);
         dim3 grid((nmax + 255) / 256, static_cast<unsigned>(large.size()));
         swap_rows_kernel<<<grid, 256, 0, ctx->stream>>>(d_large.p, k0, kb, perm_ws.p);
@@ -617,12 +680,14 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
         back.copy(Ub, kw, A + k0, o.lda, kw, k0, 1.0);
         back.copy(Ub + static_cast<size_t>(k1) * kw, kw, A + k0 + k1 * ld, o.lda, kw, tail, 1.0);
       }
+      piv.diag_pivots = diag, piv.guard_dev = diag ? guard_dev : nullptr;
       piv.run(ctx, status_dev);  // in place: A_KK <- P (kw <= 32 uses the smem kernel)
       gu.run(ctx);
       gr.run(ctx);
       gq.run(ctx);
       back.run(ctx);
     }
+    if (diag) return;  // no pivots: nothing to unscramble
     KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);
     dim3 grid((nmax + 255) / 256, static_cast<unsigned>(large.size()));
     unscramble_kernel<<<grid, 256, 0, ctx->stream>>>(d_large.p, perm_ws.p);

@@ -74,10 +74,20 @@ struct InvOp {
 };
 constexpr int kSmemInvMax = 96;
 
+// In-place complex inverses.  Default: partial pivoting.  diag_pivots:
+// Gauss-Jordan on the diagonal (no pivot search, one barrier per column;
+// blocked panels without pivot selection or row swaps), guarded: a pivot
+// below 1e-10 max|a_ij| or an inverse entry beyond 1e10 / max|a_ij| marks
+// the matrix.  Marked matrices of <= kSmemInvMax are redone with partial
+// pivoting in the same call; a marked diagonal block of a blocked inverse
+// sets guard_dev[0] = 1 instead (its caller redoes the whole build with
+// pivoting, see build_hierarchy).
 struct InverseBatch {
   std::vector<InvOp> ops;
+  bool diag_pivots = false;
+  int* guard_dev = nullptr;
   DevBuf<InvOp> d_small, d_large;
-  DevBuf<int> perm_ws;
+  DevBuf<int> perm_ws, d_flags;
   void run(Context* ctx, int* status_dev);
 };
 

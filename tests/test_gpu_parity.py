@@ -141,8 +141,22 @@ def test_skeleton_boundary_layout_matches_element_layout(hps, oracle, ctx, name)
     assert np.array_equal(c.sk.recover(g, c.sk.nrhs - 1), sk_full.recover(g, c.sk.nrhs - 1))
 
 
-@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg3_n4", "cfg2_n8"])
-def test_hierarchy_level_systems(hps, oracle, ctx, name):
+MERGE_MODES = {
+    "diag": {},                                  # default: diagonal pivots, guarded
+    "pivot": {"HPSB_MERGE_PIVOT": "1"},          # partial pivoting throughout
+    "redo": {"HPSB_TEST_GUARD_TRIP": "1"},       # guard tripped: pivoted rebuild
+}
+
+
+@pytest.mark.parametrize("mode", list(MERGE_MODES))
+@pytest.mark.parametrize("name", ["cfg0", "bump_n4_N4", "cfg3_n4", "cfg2_n8", "cfg1"])
+def test_hierarchy_level_systems(hps, oracle, ctx, name, mode, monkeypatch):
+    """Every level system M_l within 1e-10 of the oracle's, for the merge
+    inverses on diagonal pivots (default; cfg1 / cfg2_n8 reach the blocked
+    path with s = 120), with partial pivoting, and through the pivoted
+    rebuild that a tripped guard takes."""
+    for k, v in MERGE_MODES[mode].items():
+        monkeypatch.setenv(k, v)
     c = case(hps, oracle, ctx, name)
     h = hps.build_hierarchy(c.sk)
     c.S.build_hierarchy(0, True)
