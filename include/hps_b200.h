@@ -112,13 +112,22 @@ hpsb_status hpsb_problem_sample(int kind, int config, uint64_t seed, int n, int 
  * elements (proj/src/element.cpp:127-174, proj/src/mesh.cpp:36-109).
  * coeff = c = kappa^2 (1 - b) at every tensor node (real, as mesh.cpp:62),
  * source = s at the interior nodes (unweighted; the kernel applies the
- * tensor quadrature weights as mesh.cpp:89-103), or NULL for s = 0.         */
+ * tensor quadrature weights as mesh.cpp:89-103), or NULL for s = 0.
+ * The call returns once the stage is enqueued on the context's stream (the
+ * caller goes on to hpsb_skeleton_create / hpsb_hierarchy_build while the
+ * device works).  A singular element -- the reference's exception from
+ * build_elements (mesh.cpp:82-84) -- is reported with its element id by the
+ * first call that waits for the stage: hpsb_elements_get, hpsb_hierarchy_build
+ * or any skeleton call other than hpsb_skeleton_create*.                   */
 hpsb_status hpsb_elements_build(hpsb_context ctx, int n, int order, double eta,
                                 const double* coeff, const double* source, hpsb_elements* out);
 hpsb_status hpsb_elements_build_dev(hpsb_context ctx, int n, int order, double eta,
                                     const double* coeff_dev, const double* source_dev,
                                     hpsb_elements* out);
 hpsb_status hpsb_elements_destroy(hpsb_elements el);
+/* Waits for the element stage; *count = elements whose interior block was
+ * not positive definite and went through the pivoted-LU fallback.          */
+hpsb_status hpsb_elements_fallbacks(hpsb_elements el, int* count);
 /* T[e] (4(N-1))^2 complex col-major and H[e] 4(N-1) complex, for e in [e0, e0+count). */
 hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, double* H);
 

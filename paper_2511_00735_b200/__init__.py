@@ -94,6 +94,7 @@ _sig("hpsb_elements_build_dev", _st, _VP, ctypes.c_int, ctypes.c_int, ctypes.c_d
 _sig("hpsb_elements_destroy", _st, _VP)
 _sig("hpsb_elements_get", _st, _VP, ctypes.c_int, ctypes.c_int, _D, _D)
 _sig("hpsb_skeleton_create", _st, _VP, _D, ctypes.c_int, ctypes.POINTER(_VP))
+_sig("hpsb_elements_fallbacks", _st, _VP, ctypes.POINTER(ctypes.c_int))
 _sig("hpsb_skeleton_create_boundary", _st, _VP, _D, ctypes.c_int, ctypes.POINTER(_VP))
 _sig("hpsb_skeleton_destroy", _st, _VP)
 _sig("hpsb_skeleton_dim", ctypes.c_int64, _VP)
@@ -349,6 +350,12 @@ class ElementRecords(_Handle):
         self.ctx, self._h, self.n, self.order, self.eta = ctx, h, n, order, eta
         self.m = order - 1
         self.nb = 4 * self.m
+
+    def fallbacks(self) -> int:
+        """Elements redone by the pivoted-LU fallback (indefinite L_ii)."""
+        c = ctypes.c_int()
+        _check(_lib.hpsb_elements_fallbacks(self._h, ctypes.byref(c)))
+        return c.value
 
     def iti(self, e0: int = 0, count: int | None = None):
         count = self.n * self.n - e0 if count is None else count

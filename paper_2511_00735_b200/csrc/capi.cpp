@@ -441,8 +441,18 @@ hpsb_status hpsb_elements_destroy(hpsb_elements el) {
   return HPSB_OK;
 }
 
+hpsb_status hpsb_elements_fallbacks(hpsb_elements el, int* count) {
+  return guarded([&] {
+    REQUIRE(el && count, "elements_fallbacks: null argument");
+    hpsb::elements_wait(el->e.get());
+    *count = el->e->fallbacks;
+    return HPSB_OK;
+  });
+}
+
 hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, double* H) {
   return guarded([&] {
+    hpsb::elements_wait(el ? el->e.get() : nullptr);
     const auto& E = *el->e;
     const int ne = E.n * E.n;
     REQUIRE(e0 >= 0 && count >= 0 && e0 + count <= ne, "elements_get: range out of bounds");
@@ -493,6 +503,10 @@ const double* hpsb_skeleton_rhs_dev(hpsb_skeleton sk, int r) {
 hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs) {
   return guarded([&] {
     REQUIRE(sk && rhs && r >= 0 && r < sk->s->nrhs, "skeleton_rhs: bad argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
+    // the skeleton build returns without synchronising; cudaMemcpy runs on
+    // the legacy stream, which does not wait for the context's stream
+    HPSB_CUDA(cudaStreamSynchronize(sk->s->ctx->stream));
     HPSB_CUDA(cudaMemcpy(rhs, sk->s->rhs.p + static_cast<size_t>(r) * sk->s->dim,
                          sk->s->dim * sizeof(double2), cudaMemcpyDeviceToHost));
     return HPSB_OK;
@@ -502,6 +516,7 @@ hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs) {
 hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x, double* y) {
   return guarded([&] {
     REQUIRE(sk && x && y, "skeleton_apply: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     hpsb::skeleton_apply(sk->s.get(), reinterpret_cast<const double2*>(x),
                          reinterpret_cast<double2*>(y));
     return HPSB_OK;
@@ -511,6 +526,7 @@ hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x, double* y
 hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y) {
   return guarded([&] {
     REQUIRE(sk && x && y, "skeleton_apply: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     auto* S = sk->s.get();
     cudaStream_t st = S->ctx->stream;
     HPSB_CUDA(cudaMemcpyAsync(S->x_buf.p, x, S->dim * sizeof(double2), cudaMemcpyHostToDevice, st));
@@ -524,6 +540,7 @@ hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y) {
 hpsb_status hpsb_recover_dev(hpsb_skeleton sk, const double* x, int r, double* field) {
   return guarded([&] {
     REQUIRE(sk && x && field, "recover: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     hpsb::recover_field(sk->s.get(), reinterpret_cast<const double2*>(x), r,
                         reinterpret_cast<double2*>(field));
     return HPSB_OK;
@@ -533,6 +550,7 @@ hpsb_status hpsb_recover_dev(hpsb_skeleton sk, const double* x, int r, double* f
 hpsb_status hpsb_recover(hpsb_skeleton sk, const double* x, int r, double* field) {
   return guarded([&] {
     REQUIRE(sk && x && field, "recover: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     auto* S = sk->s.get();
     cudaStream_t st = S->ctx->stream;
     const auto* el = S->el;
@@ -678,6 +696,7 @@ hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double
                             hpsb_krylov_config cfg, hpsb_solve_report* report) {
   return guarded([&] {
     REQUIRE(sk && rhs && x && report, "fgmres: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     return hpsb::fgmres(sk->s.get(), precond ? precond->p : nullptr,
                         reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x), cfg,
                         report);
@@ -688,6 +707,7 @@ hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rh
                         hpsb_krylov_config cfg, hpsb_solve_report* report) {
   return guarded([&] {
     REQUIRE(sk && rhs && x && report, "fgmres: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     auto* S = sk->s.get();
     cudaStream_t st = S->ctx->stream;
     hpsb::DevBuf<double2> b(S->dim), xd(S->dim);
@@ -703,6 +723,7 @@ hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rh
 hpsb_status hpsb_skeleton_apply_batch_dev(hpsb_skeleton sk, const double* x, double* y, int nrhs) {
   return guarded([&] {
     REQUIRE(sk && x && y, "skeleton_apply: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     hpsb::skeleton_apply_batch(sk->s.get(), reinterpret_cast<const double2*>(x),
                                reinterpret_cast<double2*>(y), nrhs);
     return HPSB_OK;
@@ -723,6 +744,7 @@ hpsb_status hpsb_fgmres_batch_dev(hpsb_skeleton sk, hpsb_precond precond, const 
                                   hpsb_solve_report* reports) {
   return guarded([&] {
     REQUIRE(sk && rhs && x && reports, "fgmres: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     return hpsb::fgmres_batch(sk->s.get(), precond ? precond->p : nullptr,
                               reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x),
                               nrhs, cfg, reports);
@@ -733,6 +755,7 @@ hpsb_status hpsb_fgmres_batch(hpsb_skeleton sk, hpsb_precond precond, const doub
                               int nrhs, hpsb_krylov_config cfg, hpsb_solve_report* reports) {
   return guarded([&] {
     REQUIRE(sk && rhs && x && reports, "fgmres: null argument");
+    hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     REQUIRE(nrhs >= 1 && nrhs <= 32, "fgmres: 1 <= nrhs <= 32");
     auto* S = sk->s.get();
     cudaStream_t st = S->ctx->stream;

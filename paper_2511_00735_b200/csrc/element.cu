@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kThreads) element_kernel(ElemArgs a) {
 
   for (int i = tid; i < np; i += blockDim.x) mass[i] = a.mass[i];
   auto K = [&](int r, int c) { return __ldg(a.stiff + r + c * np); };
-  const int count = a.elist ? a.nlist : a.ne;
+  const int count = a.elist ? (a.nlist_dev ? *a.nlist_dev : a.nlist) : a.ne;
 
   for (int ii = blockIdx.x; ii < count; ii += gridDim.x) {
     const int e = a.elist ? a.elist[ii] : ii;
@@ -993,6 +993,14 @@ __global__ void __launch_bounds__(kV3Threads, 1) element_v3_kernel(ElemArgs a) {
 
 }  // namespace
 
+namespace {
+// status bit 4 (indefinite interior block: redo with the pivoted LU) -> list
+__global__ void collect_redo_kernel(const int* __restrict__ status, int ne, int* list, int* count) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x)
+    if (status[e] & 4) list[atomicAdd(count, 1)] = e;
+}
+}  // namespace
+
 std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double eta,
                                          const double* coeff_dev, const double2* source_dev) {
   if (n < 2 || (n & (n - 1)) != 0)
@@ -1114,44 +1122,58 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
     HPSB_LAUNCHED(ctx);
   }
   }
-  std::vector<int> st(ne);
-  HPSB_CUDA(cudaMemcpyAsync(st.data(), el->status.p, ne * sizeof(int), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
-  // pivoted-LU fallback (v1) for elements whose interior block is indefinite
-  std::vector<int> redo;
-  for (int e = 0; e < ne; ++e)
-    if (st[e] & 4) redo.push_back(e);
-  if (!redo.empty()) {
-    DevBuf<int> d_redo;
-    d_redo.upload(redo, ctx->stream);
-    const int slots = std::min(static_cast<int>(redo.size()), 2 * ctx->num_sms);
+  // Pivoted-LU fallback (v1) for elements whose interior block is
+  // indefinite (status bit 4), without a host round trip: the flagged
+  // elements are listed on the device and the v1 launch reads the count.
+  {
+    DevBuf<int> d_redo(ne + 1);
+    HPSB_CUDA(cudaMemsetAsync(d_redo.p + ne, 0, sizeof(int), ctx->stream));
+    collect_redo_kernel<<<std::max(1, std::min((ne + 255) / 256, 4 * ctx->num_sms)), 256, 0,
+                          ctx->stream>>>(el->status.p, ne, d_redo.p, d_redo.p + ne);
+    HPSB_LAUNCHED(ctx);
+    const int slots = std::min(ne, ctx->num_sms);
     const size_t stride = static_cast<size_t>(ni) * ni + static_cast<size_t>(ni) * (nb + 2);
     ws.alloc(stride * slots);
     a.ws = ws.p, a.ws_stride = stride;
-    a.elist = d_redo.p, a.nlist = static_cast<int>(redo.size());
+    a.elist = d_redo.p, a.nlist = ne, a.nlist_dev = d_redo.p + ne;
     const size_t smem = sizeof(double2) * (nb * nb + nb) + sizeof(double) * (ni + np) +
                         sizeof(int) * nb + 16;
     allow_smem<element_kernel>(smem);
     KernelScope ks(ctx, "element_iti_lu", 0.0, 0.0);
     element_kernel<<<slots, kThreads, smem, ctx->stream>>>(a);
     HPSB_LAUNCHED(ctx);
-    HPSB_CUDA(cudaMemcpyAsync(st.data(), el->status.p, ne * sizeof(int), cudaMemcpyDeviceToHost,
-                              ctx->stream));
+    // h_status[ne] = number of elements the fallback redid
+    HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&el->h_status), (ne + 1) * sizeof(int)));
+    HPSB_CUDA(cudaMemcpyAsync(el->h_status, el->status.p, ne * sizeof(int),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    HPSB_CUDA(cudaMemcpyAsync(el->h_status + ne, d_redo.p + ne, sizeof(int),
+                              cudaMemcpyDeviceToHost, ctx->stream));
   }
-  HPSB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
-  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
-  float ms = 0;
-  HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
-  el->build_seconds = ms * 1e-3;
+  HPSB_CUDA(cudaEventCreateWithFlags(&el->done, cudaEventDisableTiming));
+  HPSB_CUDA(cudaEventRecord(el->done, ctx->stream));
+  el->pending = true;
+  if (std::getenv("HPSB_ELEMENTS_SYNC")) elements_wait(el.get());
+  return el;
+}
+
+Elements::~Elements() {
+  if (done) cudaEventDestroy(done);
+  if (h_status) cudaFreeHost(h_status);
+}
+
+void elements_wait(Elements* el) {
+  if (!el || !el->pending) return;
+  HPSB_CUDA(cudaEventSynchronize(el->done));
+  el->pending = false;
+  const int ne = el->n * el->n;
+  el->fallbacks = el->h_status[ne];
   for (int e = 0; e < ne; ++e)
-    if (st[e]) {
+    if (el->h_status[e]) {
       // mesh.cpp:82-84 annotates element failures with the element id.
       throw std::runtime_error("element " + std::to_string(e) + ": " +
-                               ((st[e] & 1) ? "singular interior block"
-                                            : "singular local operator"));
+                               ((el->h_status[e] & 1) ? "singular interior block"
+                                                      : "singular local operator"));
     }
-  return el;
 }
 
 }  // namespace hpsb

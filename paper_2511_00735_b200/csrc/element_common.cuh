@@ -25,6 +25,7 @@ struct ElemArgs {
   size_t ws_stride;  // doubles per slot
   const int* elist;  // optional element list (fallback re-run)
   int nlist;
+  const int* nlist_dev;  // list length on the device (overrides nlist)
   int npad, nbc;     // v2: padded interior size (multiple of 16), padded rhs count
   double* Y;         // [e][nb+2][ni]: L_ii^{-1} [L_iG | re b~ | im b~] kept for recovery
 };

@@ -435,6 +435,7 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
   }
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   tr.mark("final_wait");
+  elements_wait(sk->el);  // long finished: the merges consumed the element maps
   const int st = st_pinned[0];
   *guard_tripped = st_pinned[1] != 0 || (!pivot && std::getenv("HPSB_TEST_GUARD_TRIP"));
   if (*guard_tripped) return h;  // results unused: the caller redoes the build

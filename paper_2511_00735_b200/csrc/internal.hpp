@@ -325,7 +325,18 @@ struct Elements {
   DevBuf<double> Y;   // [e][nb+2][ni] L_ii^{-1}[L_iG | re b~ | im b~] (solution recovery)
   double build_seconds = 0;
   Partition part;     // sharding of the elements over the context's ranks
+  // The element stage returns without waiting for the device: the status
+  // copy lands in h_status (pinned) behind `done`, and elements_wait checks
+  // it at the first call that needs the stage finished (the host builds the
+  // skeleton and the merge plans meanwhile).
+  int* h_status = nullptr;
+  cudaEvent_t done = nullptr;
+  bool pending = false;
+  int fallbacks = 0;  // elements redone by the pivoted-LU fallback (v1)
+  ~Elements();
 };
+// Wait for the element stage and raise its per-element errors (mesh.cpp:82-84).
+void elements_wait(Elements* el);
 
 struct Skeleton {
   Context* ctx = nullptr;

@@ -102,17 +102,19 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
     // of the 1.5 GB element layout) and expand on the device.
     DevBuf<double2> d_tb;
     d_tb.alloc(static_cast<size_t>(nrhs) * 4 * el->n * m);
-    HPSB_CUDA(cudaMemcpyAsync(d_tb.p, tside_host, d_tb.bytes(), cudaMemcpyHostToDevice,
-                              ctx->stream));
+    // through the pinned staging ring: a pageable cudaMemcpyAsync on a busy
+    // stream (the element stage may still run) can return before it has
+    // consumed the caller's buffer
+    staged_upload(d_tb.p, tside_host, d_tb.bytes(), ctx->stream);
     HPSB_CUDA(cudaMemsetAsync(d_t.p, 0, d_t.bytes(), ctx->stream));
     KernelScope ks(ctx, "skeleton_tside", 32.0 * d_tb.n, 0.0);
     tside_expand_kernel<<<std::min<int64_t>((d_tb.n + 255) / 256, 148 * 8), 256, 0,
                           ctx->stream>>>(d_tb.p, d_t.p, el->n, m, nrhs);
     HPSB_LAUNCHED(ctx);
-    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));  // d_tb is freed on return
   } else {
     HPSB_CUDA(cudaMemcpyAsync(d_t.p, tside_host, d_t.bytes(), cudaMemcpyHostToDevice,
                               ctx->stream));
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));  // see above; this layout is large
   }
   DevBuf<int> d_own;
   if (sharded) d_own.upload(own, ctx->stream);
@@ -143,7 +145,8 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
   }
   sk->apply_plan.name = "skeleton_matvec";
   sk->apply_plan.finalize(ctx->stream);
-  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+  // no synchronisation: buffers are freed stream-ordered, host uploads are
+  // staged, and the element stage may still be running (Elements::pending)
   return sk;
 }
 

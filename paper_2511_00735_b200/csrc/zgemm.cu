@@ -50,19 +50,15 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDesc* __restrict__ descs,
-                                                                int ndesc) {
+                                                                const int* __restrict__ tile_map) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + STAGES * A_STAGE;
   const int tile = blockIdx.x;
-  // locate the problem owning this tile
-  int lo = 0, hi = ndesc - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (descs[mid].tile_begin <= tile) lo = mid;
-    else hi = mid - 1;
-  }
-  const GemmDesc d = descs[lo];
+  // the problem owning this tile: one load (a binary search over the
+  // thousands of problems of a low level was a chain of ~14 dependent L2
+  // loads per CTA, as long as a K = 19 tile's whole main loop)
+  const GemmDesc d = descs[tile_map[tile]];
   const int local = tile - d.tile_begin;
   const int tm = local % d.tiles_m, tn = local / d.tiles_m;
   const int m0 = tm * BM, n0 = tn * BN;
@@ -152,38 +148,52 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
     }
   }
   cp_async_wait<0>();
-  // epilogue: C = alpha * acc + beta * C
+  // epilogue: C = alpha * acc + beta * C.  All C reads are issued before
+  // the first store: interleaved, every read waited for the previous store
+  // (possible aliasing), 16 serial L2/HBM round trips per thread -- longer
+  // than the whole main loop of the K = 19..76 merges of the low levels.
   const double2 alpha = make_double2(d.alpha_re, d.alpha_im);
   const double2 beta = make_double2(d.beta_re, d.beta_im);
   const bool use_beta = (d.beta_re != 0.0 || d.beta_im != 0.0);
+  const int row0 = m0 + wm * 32 + (lane >> 2), col0 = n0 + wn * 16 + 2 * (lane & 3);
+  // two halves of the fragment rows: 8 reads in flight, no spills
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + (lane >> 2);
-    if (row >= d.M) continue;
+  for (int half = 0; half < 2; ++half) {
+    double2 cold[2][2][2];
+    if (use_beta) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int col = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + h;
-        if (col >= d.N) continue;
-        double2* c = d.C + (size_t)row + (size_t)col * d.ldc;
-        double2 v = cmul(alpha, make_double2(cr[i][j][h], ci[i][j][h]));
-        if (use_beta) v = cadd(v, cmul(beta, *c));
-        *c = v;
-      }
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int row = row0 + (2 * half + i) * 8, col = col0 + j * 8 + h;
+            cold[i][j][h] = (row < d.M && col < d.N) ? d.C[(size_t)row + (size_t)col * d.ldc]
+                                                     : make_double2(0.0, 0.0);
+          }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int ii = 2 * half + i, row = row0 + ii * 8;
+      if (row >= d.M) continue;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = col0 + j * 8 + h;
+          if (col >= d.N) continue;
+          double2 v = cmul(alpha, make_double2(cr[ii][j][h], ci[ii][j][h]));
+          if (use_beta) v = cadd(v, cmul(beta, cold[i][j][h]));
+          d.C[(size_t)row + (size_t)col * d.ldc] = v;
+        }
+    }
   }
 }
 
 // Sub-matrix copy / gather ops, tiled 8 columns per CTA.
-__global__ void copy_ops_kernel(const CopyOp* __restrict__ ops, int nops) {
+__global__ void copy_ops_kernel(const CopyOp* __restrict__ ops, const int* __restrict__ tile_map) {
   const int tile = blockIdx.x;
-  int lo = 0, hi = nops - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (ops[mid].tile_begin <= tile) lo = mid;
-    else hi = mid - 1;
-  }
-  const CopyOp op = ops[lo];
+  const CopyOp op = ops[tile_map[tile]];
   const int c0 = (tile - op.tile_begin) * 8;
   const int c1 = min(c0 + 8, op.cols);
   for (int c = c0; c < c1; ++c) {
@@ -510,6 +520,14 @@ void GemmBatch::run(Context* ctx) {
   if (descs.empty()) return;
   // K == 0 problems still apply the epilogue (C = beta C): keep them valid.
   d_descs.upload(descs, ctx->stream);
+  {
+    std::vector<int> map(total_tiles);
+    for (size_t i = 0; i < descs.size(); ++i) {
+      const int end = i + 1 < descs.size() ? descs[i + 1].tile_begin : total_tiles;
+      std::fill(map.begin() + descs[i].tile_begin, map.begin() + end, static_cast<int>(i));
+    }
+    d_map.upload(map, ctx->stream);
+  }
   static const bool attr = [] {  // thread-safe one-time init
     HPSB_CUDA(cudaFuncSetAttribute(zgemm_grouped_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -526,8 +544,7 @@ void GemmBatch::run(Context* ctx) {
                  descs.size(), total_tiles, flops, padded, tu, tp);
   }
   KernelScope ks(ctx, "zgemm_dmma", 0.0, flops);
-  zgemm_grouped_kernel<<<total_tiles, THREADS, GEMM_SMEM, ctx->stream>>>(
-      d_descs.p, static_cast<int>(descs.size()));
+  zgemm_grouped_kernel<<<total_tiles, THREADS, GEMM_SMEM, ctx->stream>>>(d_descs.p, d_map.p);
   HPSB_LAUNCHED(ctx);
 }
 
@@ -542,10 +559,18 @@ void CopyBatch::add(const CopyOp& o0) {
 void CopyBatch::run(Context* ctx) {
   if (ops.empty()) return;
   d_ops.upload(ops, ctx->stream);
+  {
+    std::vector<int> map(total_tiles);
+    for (size_t i = 0; i < ops.size(); ++i) {
+      const int end = i + 1 < ops.size() ? ops[i + 1].tile_begin : total_tiles;
+      std::fill(map.begin() + ops[i].tile_begin, map.begin() + end, static_cast<int>(i));
+    }
+    d_map.upload(map, ctx->stream);
+  }
   double elems = 0;
   for (const auto& o : ops) elems += double(o.rows) * o.cols;
   KernelScope ks(ctx, "merge_copy", 32.0 * elems, 0.0);
-  copy_ops_kernel<<<total_tiles, 128, 0, ctx->stream>>>(d_ops.p, static_cast<int>(ops.size()));
+  copy_ops_kernel<<<total_tiles, 128, 0, ctx->stream>>>(d_ops.p, d_map.p);
   HPSB_LAUNCHED(ctx);
 }
 

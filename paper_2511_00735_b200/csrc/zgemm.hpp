@@ -23,6 +23,7 @@ struct GemmBatch {
   int total_tiles = 0;
   double flops = 0;
   DevBuf<GemmDesc> d_descs;
+  DevBuf<int> d_map;  // tile -> problem (one load per CTA instead of a binary search)
   int add(const GemmDesc& d);
   int add(const double2* A, int lda, const double2* B, int ldb, double2* C, int ldc, int M, int N,
           int K, double alpha, double beta) {
@@ -50,6 +51,7 @@ struct CopyBatch {
   std::vector<CopyOp> ops;
   int total_tiles = 0;
   DevBuf<CopyOp> d_ops;
+  DevBuf<int> d_map;  // tile -> op
   void add(const CopyOp& o);
   void copy(const double2* src, int lds, double2* dst, int ldd, int rows, int cols, double scale) {
     add(CopyOp{src, dst, nullptr, nullptr, lds, ldd, rows, cols, scale, CopyOp::kCopy, 0});

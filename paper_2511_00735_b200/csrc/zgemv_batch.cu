@@ -7,6 +7,8 @@
 // scatters C rows through theirs.  A complex product is four real DMMAs
 // (mma.sync.m8n8k4.f64) on de-interleaved fragments, as in zgemm.cu.
 #include "device.cuh"
+#include <algorithm>
+
 #include "zgemv_batch.hpp"
 
 namespace hpsb {
@@ -39,7 +41,8 @@ __device__ __forceinline__ const double2* bind_ptr(const double2* p, const BBind
 // BN = 32 (R > 16): 4 x 2 warps of 16 x 16 outputs; BN = 16: 8 x 1 warps of 8 x 16.
 template <int BN>
 __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __restrict__ descs,
-                                                              int ndesc, int R, BBind bind) {
+                                                              const int* __restrict__ tile_map,
+                                                              int R, BBind bind) {
   constexpr int WN = BN / 16, WM = 8 / WN, I = BM / (8 * WM);
   constexpr int B_STAGE = BN * SB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -47,13 +50,7 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
   double2* Bs = As + STAGES * A_STAGE;
   pdl_trigger();
   const int tile = blockIdx.x;
-  int lo = 0, hi = ndesc - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (descs[mid].tile_begin <= tile) lo = mid;
-    else hi = mid - 1;
-  }
-  BDesc d = descs[lo];
+  BDesc d = descs[tile_map[tile]];
   d.B = bind_ptr(d.B, bind);
   d.C = const_cast<double2*>(bind_ptr(d.C, bind));
   d.Z = bind_ptr(d.Z, bind);
@@ -182,6 +179,16 @@ void BPhase::add(const BDesc& x0) {
   descs.push_back(x);
 }
 
+void BPhase::finalize(cudaStream_t s) {
+  d.upload(descs, s);
+  std::vector<int> map(total_tiles);
+  for (size_t i = 0; i < descs.size(); ++i) {
+    const int end = i + 1 < descs.size() ? descs[i + 1].tile_begin : total_tiles;
+    std::fill(map.begin() + descs[i].tile_begin, map.begin() + end, static_cast<int>(i));
+  }
+  d_map.upload(map, s);
+}
+
 void BPhase::run(Context* ctx, int R, const char* label, BBind bind) const {
   if (descs.empty()) return;
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("batch: 1 <= nrhs <= 32");
@@ -189,11 +196,11 @@ void BPhase::run(Context* ctx, int R, const char* label, BBind bind) const {
   if (R <= 16) {
     allow_smem<zgemv_batch_kernel<16>>(bsmem<16>());
     launch_k(ctx, zgemv_batch_kernel<16>, dim3(total_tiles), dim3(THREADS), bsmem<16>(), 1,
-             static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R, bind);
+             static_cast<const BDesc*>(d.p), static_cast<const int*>(d_map.p), R, bind);
   } else {
     allow_smem<zgemv_batch_kernel<32>>(bsmem<32>());
     launch_k(ctx, zgemv_batch_kernel<32>, dim3(total_tiles), dim3(THREADS), bsmem<32>(), 1,
-             static_cast<const BDesc*>(d.p), static_cast<int>(descs.size()), R, bind);
+             static_cast<const BDesc*>(d.p), static_cast<const int*>(d_map.p), R, bind);
   }
 }
 

@@ -42,8 +42,9 @@ struct BPhase {
   double flops = 0, bytes = 0;
   std::string label;  // profiling name (overrides run()'s)
   DevBuf<BDesc> d;
+  DevBuf<int> d_map;  // tile -> desc
   void add(const BDesc& x);
-  void finalize(cudaStream_t s) { d.upload(descs, s); }
+  void finalize(cudaStream_t s);
   void run(Context* ctx, int R, const char* label, BBind bind = {}) const;
 };
 

@@ -87,14 +87,27 @@ def test_element_cholesky_path_full_configs(hps, oracle, config):
     fresh = hps.Context(0)
     fresh.profile(True)
     el = hps.build_elements(fresh, prob)
-    prof = fresh.profile_entries()
-    assert "element_iti_lu" not in prof, prof
+    assert el.fallbacks() == 0
     ne = prob.n ** 2
     picks = sorted({0, ne // 2 + 1, ne - 1})
     for e in picks:
         T, _ = el.iti(e, 1)
         To = oracle.element(prob.order, 1.0 / prob.n, prob.eta, prob.coeff[e])[0]
         assert relf(T[0], To) < TOL_OP, (config, e)
+
+
+def test_element_indefinite_fallback(hps, oracle, ctx):
+    """kappa^2 above the smallest interior eigenvalue (n = 8, N = 8,
+    kappa = 41.9): L_ii is indefinite, the device-listed elements take the
+    pivoted-LU fallback inside the same (non-blocking) element stage, and the
+    maps still match the oracle."""
+    prob = hps.problem(1, 0, n=8, order=8, kappa=41.88790204786391)
+    el = hps.build_elements(ctx, prob)
+    assert el.fallbacks() > 0
+    T, _ = el.iti()
+    for e in (0, 27, 63):
+        To = oracle.element(prob.order, 1.0 / prob.n, prob.eta, prob.coeff[e])[0]
+        assert relf(T[e], To) < TOL_OP, e
 
 
 def test_element_pivoted_inverse_path(hps, oracle, ctx, monkeypatch):
