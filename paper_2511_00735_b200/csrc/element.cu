@@ -1,3 +1,4 @@
+#include <mutex>
 // K1 element_iti: batched local impedance-to-impedance build.
 //
 // Replaces ElementOperators (proj/src/element.cpp:127-160) + source_to_outgoing
@@ -1143,7 +1144,7 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
     element_kernel<<<slots, kThreads, smem, ctx->stream>>>(a);
     HPSB_LAUNCHED(ctx);
     // h_status[ne] = number of elements the fallback redid
-    HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&el->h_status), (ne + 1) * sizeof(int)));
+    el->h_status = pinned_ints_acquire(ne + 1, &el->h_status_cap);
     HPSB_CUDA(cudaMemcpyAsync(el->h_status, el->status.p, ne * sizeof(int),
                               cudaMemcpyDeviceToHost, ctx->stream));
     HPSB_CUDA(cudaMemcpyAsync(el->h_status + ne, d_redo.p + ne, sizeof(int),
@@ -1156,9 +1157,37 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
   return el;
 }
 
+// Pinned status buffers are recycled, never freed: cudaFreeHost (and often
+// cudaMallocHost) synchronises the whole device, which would stall the next
+// setup's overlapped pipeline when the previous Elements is released.
+namespace {
+std::mutex g_pinned_mu;
+std::vector<std::pair<int*, size_t>> g_pinned_free;
+}  // namespace
+
+int* pinned_ints_acquire(size_t n, size_t* cap) {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    for (size_t i = 0; i < g_pinned_free.size(); ++i)
+      if (g_pinned_free[i].second >= n) {
+        auto pr = g_pinned_free[i];
+        g_pinned_free.erase(g_pinned_free.begin() + i);
+        *cap = pr.second;
+        return pr.first;
+      }
+  }
+  int* p = nullptr;
+  HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&p), n * sizeof(int)));
+  *cap = n;
+  return p;
+}
+
 Elements::~Elements() {
   if (done) cudaEventDestroy(done);
-  if (h_status) cudaFreeHost(h_status);
+  if (h_status) {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.emplace_back(h_status, h_status_cap);
+  }
 }
 
 void elements_wait(Elements* el) {

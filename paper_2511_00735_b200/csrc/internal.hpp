@@ -330,11 +330,13 @@ struct Elements {
   // it at the first call that needs the stage finished (the host builds the
   // skeleton and the merge plans meanwhile).
   int* h_status = nullptr;
+  size_t h_status_cap = 0;
   cudaEvent_t done = nullptr;
   bool pending = false;
   int fallbacks = 0;  // elements redone by the pivoted-LU fallback (v1)
   ~Elements();
 };
+int* pinned_ints_acquire(size_t n, size_t* cap);  // recycled pinned host ints
 // Wait for the element stage and raise its per-element errors (mesh.cpp:82-84).
 void elements_wait(Elements* el);
 
