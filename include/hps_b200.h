@@ -25,8 +25,10 @@
  * Pointers are HOST pointers unless the function name ends in _dev.
  * Objects are immutable after build and owned by the library behind opaque
  * handles with create/destroy pairs; calls on one context are serialised on
- * that context's CUDA stream.  There is no CPU fallback: without a usable
- * sm_100 device every compute call returns HPSB_INTERNAL.
+ * that context's CUDA stream (several contexts may live on one host thread).
+ * Destroy every object before the context it was built on.  There is no CPU
+ * fallback: without a usable sm_100 device every compute call returns
+ * HPSB_INTERNAL.
  */
 #ifndef HPS_B200_H
 #define HPS_B200_H
@@ -52,21 +54,27 @@ typedef struct hpsb_skeleton_s* hpsb_skeleton;
 typedef struct hpsb_hierarchy_s* hpsb_hierarchy;
 typedef struct hpsb_precond_s* hpsb_precond;
 
-/* MgConfig (proj/include/hps/multigrid.hpp:12-18). */
+/* MgConfig (proj/include/hps/multigrid.hpp:12-18; reference defaults
+ * depth 2, gamma 1, coarse_iters 4, exact_coarse 0). */
 typedef struct hpsb_mg_config {
-  int depth;        /* number of hierarchy levels used (>= 2) */
-  int gamma;        /* coarse calls per intermediate level (1 = V-cycle, <= 16; > 1 single GPU) */
-  int coarse_iters; /* unpreconditioned GMRES steps at the deepest level */
-  int exact_coarse; /* dense inverse of M_depth instead of coarse GMRES (gamma = 1) */
+  int depth;        /* number of hierarchy levels used (2 <= depth <= built depth) */
+  int gamma;        /* coarse calls per intermediate level (1 = V-cycle; > 1 single GPU) */
+  int coarse_iters; /* unpreconditioned GMRES steps at the deepest level (<= 512) */
+  int exact_coarse; /* dense inverse of M_depth instead of coarse GMRES; gamma and
+                       coarse_iters are then ignored */
 } hpsb_mg_config;
 
-/* KrylovConfig (proj/include/hps/krylov.hpp:15-21). */
+/* KrylovConfig (proj/include/hps/krylov.hpp:15-21; reference defaults
+ * restart 60, tol 1e-8, max_iters 2000, record_history 1, reorthogonalize 0). */
 typedef struct hpsb_krylov_config {
   int restart;
   double tol;
   int max_iters;
-  int record_history;
-  int reorthogonalize; /* the B200 path always runs two Gram-Schmidt passes */
+  int record_history;  /* residual history (hpsb_context_residual_history) and
+                          basis_orthogonality, single right-hand side */
+  int reorthogonalize; /* 0: one modified Gram-Schmidt pass per Arnoldi step
+                          (krylov.cpp:98-102); != 0: two passes, run as two
+                          classical passes (CGS2, one kernel each) */
 } hpsb_krylov_config;
 
 /* SolveReport (proj/include/hps/krylov.hpp:23-34), device-timed. */
@@ -74,9 +82,13 @@ typedef struct hpsb_solve_report {
   int iterations;
   int converged;
   double final_residual;
-  double seconds;           /* CUDA-event time of the solve */
-  double precond_seconds;   /* part of `seconds` spent in preconditioner applies */
-  double matvec_seconds;    /* part of `seconds` spent in skeleton matvecs */
+  double seconds;             /* CUDA-event time of the solve */
+  double precond_seconds;     /* reserved (0) */
+  double matvec_seconds;      /* reserved (0) */
+  double wall_build;          /* device build time of the preconditioner's hierarchy (s), 0 without */
+  double wall_solve;          /* = seconds */
+  int64_t precond_memory;     /* device bytes of the preconditioner (MgPreconditioner::memory_bytes) */
+  double basis_orthogonality; /* max ||<V_a,V_b>| - delta_ab| per cycle (with record_history) */
 } hpsb_solve_report;
 
 /* ---------------------------------------------------------------- library */
@@ -100,7 +112,8 @@ hpsb_status hpsb_face_graph(int n, int* faces, int* level_range, int* face_of_el
 
 /* Seeded BASELINE.json problem samples (shared conventions).
  * kind: 0 reference bump, 1 reference plane wave, 2 BASELINE config `config`.
- * n / order override the config's mesh when > 0.  coeff[n^2][(N+1)^2] real,
+ * n / order (and kappa for kind 2) override the config's mesh / wavenumber
+ * when > 0 (hpsb_problem_dims reports the config's own wavenumber).  coeff[n^2][(N+1)^2] real,
  * source[n^2][(N-1)^2] complex, tside[nrhs][n^2][4][N-1] complex.          */
 hpsb_status hpsb_problem_dims(int kind, int config, int n, int order, int* n_out, int* order_out,
                               int* nrhs_out, double* kappa_out, int* restart_out, double* tol_out);
@@ -115,7 +128,10 @@ hpsb_status hpsb_problem_sample(int kind, int config, uint64_t seed, int n, int 
  * tensor quadrature weights as mesh.cpp:89-103), or NULL for s = 0.
  * The call returns once the stage is enqueued on the context's stream (the
  * caller goes on to hpsb_skeleton_create / hpsb_hierarchy_build while the
- * device works).  A singular element -- the reference's exception from
+ * device works): device inputs of hpsb_elements_build_dev must stay valid
+ * until the stage completes (hpsb_elements_fallbacks or
+ * hpsb_context_synchronize waits for it; host inputs are copied before the
+ * call returns).  A singular element -- the reference's exception from
  * build_elements (mesh.cpp:82-84) -- is reported with its element id by the
  * first call that waits for the stage: hpsb_elements_get, hpsb_hierarchy_build
  * or any skeleton call other than hpsb_skeleton_create*.                   */
@@ -173,6 +189,11 @@ hpsb_status hpsb_hierarchy_info(hpsb_hierarchy h, int* depth, int* total_levels,
  * with keys == NULL to get the number of structurally non-zero blocks.     */
 hpsb_status hpsb_hierarchy_level_blocks(hpsb_hierarchy h, int level, int* nblocks, int* first_face,
                                         int* keys, double* data);
+/* y = M_l x for level l's system (HierarchyLevel::M.apply on the level
+ * system over faces [first_face(l), total), proj/src/block_matrix.cpp:23-31,
+ * proj/include/hps/dissection.hpp:35-41): x, y of length
+ * (faces - first_face(l)) * 2 (N - 1), host pointers.  Single-GPU hierarchies. */
+hpsb_status hpsb_hierarchy_level_apply(hpsb_hierarchy h, int level, const double* x, double* y);
 /* Two-element merge (merge_pair, proj/src/dissection.cpp:23-82). */
 hpsb_status hpsb_merge_pair(hpsb_context ctx, int side_len, const double* T1, const double* H1,
                             const double* T2, const double* H2, int alpha, int beta, double* T,
@@ -198,6 +219,12 @@ hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rh
                         hpsb_krylov_config cfg, hpsb_solve_report* report);
 hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs_dev,
                             double* x_dev, hpsb_krylov_config cfg, hpsb_solve_report* report);
+/* gmres(op, rhs, cfg, right_precond) (proj/src/krylov.cpp:180-186): restarted
+ * GMRES with an optional FIXED right preconditioner (NULL: unpreconditioned).  */
+hpsb_status hpsb_gmres(hpsb_skeleton sk, hpsb_precond right_precond, const double* rhs, double* x,
+                       hpsb_krylov_config cfg, hpsb_solve_report* report);
+hpsb_status hpsb_gmres_dev(hpsb_skeleton sk, hpsb_precond right_precond, const double* rhs_dev,
+                           double* x_dev, hpsb_krylov_config cfg, hpsb_solve_report* report);
 
 /* Multi-RHS (nrhs <= 32, single GPU): the R vectors are stored column-wise
  * (vector b at offset b * dim).  The operators are applied to all R at once

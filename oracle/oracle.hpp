@@ -62,6 +62,10 @@ struct CMat {
 
 using CVec = std::vector<cplx>;
 
+// Host threads used by the per-iteration operators (BlockMatrix::apply, the
+// multigrid group solves); every result is bit-identical for any count.
+void set_threads(int threads);
+
 CMat matmul(const CMat& A, const CMat& B);           // A * B
 void gemv_acc(const CMat& A, const cplx* x, cplx* y, cplx alpha);  // y += alpha A x
 double norm2(const CVec& x);

@@ -1,6 +1,7 @@
 // CPU ORACLE — TEST INFRASTRUCTURE ONLY.  C entry points for ctypes (tests,
 // smoke(), bench.py's cpu_baseline).  Complex arrays are interleaved
 // (re, im) doubles; matrices column-major, as in the reference.
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <memory>
@@ -47,6 +48,7 @@ struct Session {
   std::unique_ptr<MgPreconditioner> mg;
   int threads = 1;
   double t_elements = 0, t_skeleton = 0, t_hierarchy = 0;
+  std::vector<double> history;  // residual history of the last solve (record_history)
 };
 
 struct MOp : LinOp {
@@ -142,7 +144,7 @@ int oracle_sample(int kind, int config, unsigned long long seed, int n, int orde
     hpsb::problem::Spec spec;
     if (kind == 0) spec = hpsb::problem::reference_bump(n, order, kappa);
     else if (kind == 1) spec = hpsb::problem::reference_planewave(n, order, kappa);
-    else spec = hpsb::problem::baseline_config(config, seed, n, order);
+    else spec = hpsb::problem::baseline_config(config, seed, n, order, kappa);
     const Gll r = gll_rule(spec.order);
     const auto s = hpsb::problem::sample(spec, r.nodes.data());
     std::memcpy(coeff, s.coeff.data(), s.coeff.size() * 8);
@@ -157,6 +159,7 @@ void* oracle_session_create(int n, int order, double kappa, double eta, const do
   auto* S = new Session;
   const int rc = guarded([&] {
     S->threads = threads;
+    set_threads(threads);
     Mesh& m = S->mesh;
     if (n < 2 || (n & (n - 1))) throw std::invalid_argument("Mesh: n must be a power of two >= 2");
     m.n = n, m.order = order, m.kappa = kappa, m.eta = eta;
@@ -194,6 +197,36 @@ int oracle_get_element(void* s, int e, double* T, double* H) {
 
 int oracle_get_rhs(void* s, double* rhs) {
   return guarded([&] { put(static_cast<Session*>(s)->sys.rhs, rhs); });
+}
+
+// The skeleton right-hand side of another impedance datum t on the same
+// elements (the rhs part of assemble_skeleton, skeleton.cpp:121-132):
+// rhs slot = -H_alpha - sum_{gamma physical} T_{alpha gamma} t_gamma.
+int oracle_rhs_for_tside(void* s, const double* tside, double* out) {
+  return guarded([&] {
+    auto* S = static_cast<Session*>(s);
+    const Mesh& mesh = S->mesh;
+    const FaceGraph& graph = S->sys.graph;
+    const int sl = mesh.order - 1, bs = 2 * sl;
+    const std::size_t ne = static_cast<std::size_t>(mesh.n) * mesh.n;
+    const CVec t = get(tside, ne * 4 * sl);
+    CVec rhs(S->sys.M.dim());
+    for (int f = 0; f < graph.num_faces(); ++f) {
+      const Face& face = graph.faces[f];
+      for (int slot = 0; slot < 2; ++slot) {
+        const int eid = slot == 0 ? face.e1 : face.e2;
+        const int alpha = slot == 0 ? face.s1 : face.s2;
+        const ElementRecord& rec = S->elements[eid];
+        cplx* r = rhs.data() + static_cast<std::size_t>(f) * bs + slot * sl;
+        for (int k = 0; k < sl; ++k) r[k] = -rec.outgoing_source[alpha * sl + k];
+        for (int gamma = 0; gamma < 4; ++gamma)
+          if (graph.face_of_element[eid][gamma] < 0)
+            gemv_acc(rec.ops->iti_block(alpha, gamma),
+                     t.data() + (static_cast<std::size_t>(eid) * 4 + gamma) * sl, r, -1.0);
+      }
+    }
+    put(rhs, out);
+  });
 }
 
 int oracle_apply_M(void* s, const double* x, double* y) {
@@ -242,6 +275,17 @@ int oracle_level_blocks(void* s, int level, int* keys, double* data) {
   });
 }
 
+// y = M_l x for level l's system (faces [first_face, total), the level's
+// HierarchyLevel::M, BlockMatrix::apply of block_matrix.cpp:23-31).
+int oracle_level_apply(void* s, int level, const double* x, double* y) {
+  return guarded([&] {
+    auto* S = static_cast<Session*>(s);
+    if (!S->hier) throw std::logic_error("no hierarchy");
+    const auto& M = S->hier->levels.at(level - 1).M;
+    put(M.apply(get(x, M.dim())), y);
+  });
+}
+
 int oracle_precond_create(void* s, int depth, int gamma, int coarse_iters, int exact) {
   return guarded([&] {
     auto* S = static_cast<Session*>(s);
@@ -269,7 +313,8 @@ long long oracle_hierarchy_storage(void* s) {
   return S->hier ? static_cast<long long>(S->hier->storage_bytes()) : -1;
 }
 
-// mode 0: gmres (no preconditioner), 1: fgmres with the session preconditioner.
+// mode 0: gmres (no preconditioner), 1: fgmres with the session preconditioner,
+// 2: gmres with the session preconditioner on the right (krylov.cpp:180-186).
 // stats[0]=iterations, stats[1]=converged, stats[2]=final residual, stats[3]=seconds,
 // stats[4]=basis orthogonality
 int oracle_solve(void* s, int mode, const double* rhs, double* x, int restart, double tol,
@@ -286,6 +331,10 @@ int oracle_solve(void* s, int mode, const double* rhs, double* x, int restart, d
     if (mode == 1) {
       if (!S->mg) throw std::logic_error("no preconditioner");
       res = fgmres(op, b, POp(*S->mg), k);
+    } else if (mode == 2) {
+      if (!S->mg) throw std::logic_error("no preconditioner");
+      const POp pc(*S->mg);
+      res = gmres(op, b, k, &pc);
     } else {
       res = gmres(op, b, k, nullptr);
     }
@@ -295,7 +344,17 @@ int oracle_solve(void* s, int mode, const double* rhs, double* x, int restart, d
     stats[1] = res.second.converged ? 1.0 : 0.0;
     stats[2] = res.second.final_residual;
     stats[4] = res.second.basis_orthogonality;
+    S->history = res.second.residual_history;
   });
+}
+
+// Residual history of the last oracle_solve with record_history (length returned).
+long long oracle_history(void* s, double* out, long long cap) {
+  auto* S = static_cast<Session*>(s);
+  const long long n = static_cast<long long>(S->history.size());
+  if (out)
+    for (long long i = 0; i < std::min(n, cap); ++i) out[i] = S->history[i];
+  return n;
 }
 
 int oracle_direct_solve(void* s, const double* rhs, double* x) {

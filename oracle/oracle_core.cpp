@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <limits>
 #include <set>
 #include <thread>
 
@@ -482,12 +483,38 @@ const CMat* BlockMatrix::find(int r, int c) const {
   return it == blocks.end() ? nullptr : &it->second;
 }
 
+namespace {
+int g_threads = 1;  // host threads for the per-iteration operators (set_threads)
+
+// fn(key, block) for every stored block with block row in [r0, r1), block
+// rows split into contiguous chunks over the threads.  Each block row is
+// visited by one thread in the map's (column-ascending) order, so the
+// accumulation order per row -- and every result bit -- equals the serial
+// loop's.
+template <class F>
+void for_block_rows(const BlockMatrix& M, int r0, int r1, F&& fn) {
+  const int rows = r1 - r0;
+  const int chunks = (g_threads <= 1 || M.blocks.size() < 2048) ? 1 : 8 * g_threads;
+  const int per = std::max(1, (rows + chunks - 1) / chunks);
+  const int nchunk = (rows + per - 1) / per;
+  parallel_for(nchunk, g_threads, [&](int k) {
+    const int a = r0 + k * per, b = std::min(r1, a + per);
+    auto it = M.blocks.lower_bound({a, std::numeric_limits<int>::min()});
+    const auto end = M.blocks.lower_bound({b, std::numeric_limits<int>::min()});
+    for (; it != end; ++it) fn(it->first, it->second);
+  });
+}
+}  // namespace
+
+void set_threads(int threads) { g_threads = std::max(1, threads); }
+
 CVec BlockMatrix::apply(const CVec& v) const {  // block_matrix.cpp:23-31
   if (v.size() != dim()) throw std::invalid_argument("BlockMatrix::apply: size mismatch");
   CVec y(dim());
-  for (const auto& [key, blk] : blocks)
+  for_block_rows(*this, 0, nblocks, [&](const std::pair<int, int>& key, const CMat& blk) {
     gemv_acc(blk, v.data() + static_cast<std::size_t>(key.second) * bs,
              y.data() + static_cast<std::size_t>(key.first) * bs, 1.0);
+  });
   return y;
 }
 
@@ -687,31 +714,34 @@ BlockMatrix eliminate_level(const BlockMatrix& parent, const LevelPartition& par
     else if (r >= na && c < na)
       crows[gidx.group_of[c]].insert(r);
   }
-  // Per-group updates; groups touch disjoint (r, c) sets only through
-  // next.block(), so the per-group contributions are gathered then merged.
-  std::vector<std::vector<std::pair<std::pair<int, int>, CMat>>> upd(ng);
-  parallel_for(ng, threads, [&](int g) {
+  // Per-(group, column) updates, computed in parallel into private lists and
+  // merged afterwards in the serial loop's order (group, then column, then
+  // row), so every next(r, c) accumulates its terms in the same order.
+  std::vector<std::pair<int, int>> work;  // (group, column)
+  for (int g = 0; g < ng; ++g)
+    for (int c : bcols[g]) work.push_back({g, c});
+  std::vector<std::vector<std::pair<std::pair<int, int>, CMat>>> upd(work.size());
+  parallel_for(static_cast<int>(work.size()), threads, [&](int w) {
+    const auto [g, c] = work[w];
     const auto& grp = part.groups[g];
     const int gsz = static_cast<int>(grp.size());
-    for (int c : bcols[g]) {
-      CMat Bg(gsz * bs, bs);
+    CMat Bg(gsz * bs, bs);
+    for (int i = 0; i < gsz; ++i)
+      if (const CMat* b = parent.find(grp[i], c)) Bg.set_block(i * bs, 0, *b);
+    const CMat X = group_lu[g].solve(Bg);
+    for (int r : crows[g]) {
+      CMat u(bs, bs);
+      bool touched = false;
       for (int i = 0; i < gsz; ++i)
-        if (const CMat* b = parent.find(grp[i], c)) Bg.set_block(i * bs, 0, *b);
-      const CMat X = group_lu[g].solve(Bg);
-      for (int r : crows[g]) {
-        CMat u(bs, bs);
-        bool touched = false;
-        for (int i = 0; i < gsz; ++i)
-          if (const CMat* b = parent.find(r, grp[i])) {
-            u.add_block(0, 0, matmul(*b, X.block(i * bs, 0, bs, bs)));
-            touched = true;
-          }
-        if (touched) upd[g].push_back({{r - na, c - na}, std::move(u)});
-      }
+        if (const CMat* b = parent.find(r, grp[i])) {
+          u.add_block(0, 0, matmul(*b, X.block(i * bs, 0, bs, bs)));
+          touched = true;
+        }
+      if (touched) upd[w].push_back({{r - na, c - na}, std::move(u)});
     }
   });
-  for (int g = 0; g < ng; ++g)
-    for (auto& [key, u] : upd[g]) next.block(key.first, key.second).add_block(0, 0, u, -1.0);
+  for (auto& lst : upd)
+    for (auto& [key, u] : lst) next.block(key.first, key.second).add_block(0, 0, u, -1.0);
   return next;
 }
 
@@ -1006,7 +1036,8 @@ CVec MgPreconditioner::apply_level(const CVec& v, int level) const {  // multigr
   const int bs = h->block_size(), na = hl.partition.a_faces;
   const std::size_t lead = static_cast<std::size_t>(na) * bs;
   CVec w(v.size());
-  for (std::size_t g = 0; g < hl.partition.groups.size(); ++g) {  // F
+  const int ng = static_cast<int>(hl.partition.groups.size());
+  parallel_for(ng, ng >= 64 ? g_threads : 1, [&](int g) {  // F (groups are independent)
     const auto& grp = hl.partition.groups[g];
     CVec hg(grp.size() * bs);
     for (std::size_t i = 0; i < grp.size(); ++i)
@@ -1014,7 +1045,7 @@ CVec MgPreconditioner::apply_level(const CVec& v, int level) const {  // multigr
     const CVec xg = hl.group_lu[g].solve(hg);
     for (std::size_t i = 0; i < grp.size(); ++i)
       std::copy_n(xg.begin() + i * bs, bs, w.begin() + static_cast<std::size_t>(grp[i]) * bs);
-  }
+  });
   const CVec mw = hl.M.apply(w);  // R (v - M F v)
   CVec rc(v.size() - lead);
   for (std::size_t k = 0; k < rc.size(); ++k) rc[k] = v[lead + k] - mw[lead + k];
@@ -1031,14 +1062,14 @@ CVec MgPreconditioner::apply_level(const CVec& v, int level) const {  // multigr
     for (std::size_t k = 0; k < z.size(); ++k) z[k] += dz[k];
   }
   CVec bz(lead);  // P z = [-A^{-1} B z; z]
-  for (const auto& [key, blk] : hl.M.blocks) {
+  for_block_rows(hl.M, 0, na, [&](const std::pair<int, int>& key, const CMat& blk) {
     const auto [r, c] = key;
-    if (r < na && c >= na)
+    if (c >= na)
       gemv_acc(blk, z.data() + static_cast<std::size_t>(c - na) * bs,
                bz.data() + static_cast<std::size_t>(r) * bs, 1.0);
-  }
+  });
   CVec out = w;
-  for (std::size_t g = 0; g < hl.partition.groups.size(); ++g) {
+  parallel_for(ng, ng >= 64 ? g_threads : 1, [&](int g) {
     const auto& grp = hl.partition.groups[g];
     CVec hg(grp.size() * bs);
     for (std::size_t i = 0; i < grp.size(); ++i)
@@ -1046,7 +1077,7 @@ CVec MgPreconditioner::apply_level(const CVec& v, int level) const {  // multigr
     const CVec xg = hl.group_lu[g].solve(hg);
     for (std::size_t i = 0; i < grp.size(); ++i)
       for (int k = 0; k < bs; ++k) out[static_cast<std::size_t>(grp[i]) * bs + k] -= xg[i * bs + k];
-  }
+  });
   for (std::size_t k = 0; k < z.size(); ++k) out[lead + k] += z[k];
   return out;
 }

@@ -44,6 +44,8 @@ def lib():
         L.oracle_precond_memory.argtypes = [ctypes.c_void_p]
         L.oracle_hierarchy_storage.restype = ctypes.c_longlong
         L.oracle_hierarchy_storage.argtypes = [ctypes.c_void_p]
+        L.oracle_history.restype = ctypes.c_longlong
+        L.oracle_history.argtypes = [ctypes.c_void_p, _D, ctypes.c_longlong]
         L.oracle_sample.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_int,
                                     ctypes.c_int, ctypes.c_double, _D, _D, _D, _I]
         L.oracle_element.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double, _D, _D,
@@ -53,7 +55,8 @@ def lib():
         for name in ("oracle_get_element", "oracle_get_rhs", "oracle_apply_M",
                      "oracle_build_hierarchy", "oracle_level_info", "oracle_level_blocks",
                      "oracle_precond_create", "oracle_precond_apply", "oracle_direct_solve",
-                     "oracle_recover", "oracle_dense_M", "oracle_timings"):
+                     "oracle_recover", "oracle_dense_M", "oracle_timings",
+                     "oracle_level_apply", "oracle_rhs_for_tside"):
             getattr(L, name).argtypes = None  # set per call via explicit casts
         _lib = L
     return _lib
@@ -213,6 +216,13 @@ class Session:
         _check(lib().oracle_get_rhs(self.h, _p(r.view(np.float64))))
         return r
 
+    def rhs_for(self, tside):
+        """Skeleton rhs of another impedance datum tside[n^2, 4, N-1] on the same elements."""
+        t = np.ascontiguousarray(tside, dtype=np.complex128).ravel()
+        r = np.zeros(self.dim, dtype=np.complex128)
+        _check(lib().oracle_rhs_for_tside(self.h, _p(t.view(np.float64)), _p(r.view(np.float64))))
+        return r
+
     def apply_M(self, x):
         x = np.ascontiguousarray(x, dtype=np.complex128)
         y = np.zeros(self.dim, dtype=np.complex128)
@@ -243,6 +253,20 @@ class Session:
                 data[k * bs * bs:(k + 1) * bs * bs].reshape(bs, bs, order="F")
         return first.value, blocks
 
+    def level_apply(self, level: int, x) -> np.ndarray:
+        """y = M_l x on level l's system (faces [first_face, total))."""
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        y = np.zeros_like(x)
+        _check(lib().oracle_level_apply(self.h, ctypes.c_int(level), _p(x.view(np.float64)),
+                                        _p(y.view(np.float64))))
+        return y
+
+    def level_dim(self, level: int) -> int:
+        nst, first, nf = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().oracle_level_info(self.h, ctypes.c_int(level), ctypes.byref(nst),
+                                       ctypes.byref(first), ctypes.byref(nf)))
+        return nf.value * 2 * self.m
+
     def precond(self, depth: int, gamma: int = 1, coarse_iters: int = 4, exact: bool = False):
         _check(lib().oracle_precond_create(self.h, ctypes.c_int(depth), ctypes.c_int(gamma),
                                            ctypes.c_int(coarse_iters), ctypes.c_int(int(exact))))
@@ -259,17 +283,27 @@ class Session:
     def hierarchy_storage(self) -> int:
         return int(lib().oracle_hierarchy_storage(self.h))
 
-    def solve(self, rhs, preconditioned: bool = True, restart: int = 60, tol: float = 1e-8,
+    def solve(self, rhs, preconditioned=True, restart: int = 60, tol: float = 1e-8,
               max_iters: int = 2000, reorth: bool = True, record_history: bool = False):
+        """preconditioned: False/0 gmres, True/1 fgmres (flexible, the session
+        preconditioner), 2 or "right": gmres with the preconditioner on the right."""
+        mode = 2 if preconditioned == "right" else int(preconditioned)
         rhs = np.ascontiguousarray(rhs, dtype=np.complex128)
         x = np.zeros(self.dim, dtype=np.complex128)
         stats = np.zeros(5)
-        _check(lib().oracle_solve(self.h, int(preconditioned), _p(rhs.view(np.float64)),
+        _check(lib().oracle_solve(self.h, mode, _p(rhs.view(np.float64)),
                                   _p(x.view(np.float64)), restart, tol, max_iters, int(reorth),
                                   int(record_history), _p(stats)))
-        return x, {"iterations": int(stats[0]), "converged": bool(stats[1]),
-                   "final_residual": float(stats[2]), "seconds": float(stats[3]),
-                   "basis_orthogonality": float(stats[4])}
+        rep = {"iterations": int(stats[0]), "converged": bool(stats[1]),
+               "final_residual": float(stats[2]), "seconds": float(stats[3]),
+               "basis_orthogonality": float(stats[4])}
+        if record_history:
+            n = int(lib().oracle_history(self.h, None, 0))
+            hist = np.zeros(n)
+            if n:
+                lib().oracle_history(self.h, _p(hist), n)
+            rep["residual_history"] = hist.tolist()
+        return x, rep
 
     def direct_solve(self, rhs):
         rhs = np.ascontiguousarray(rhs, dtype=np.complex128)

@@ -59,7 +59,9 @@ class SolveReport(ctypes.Structure):
     """SolveReport (proj/include/hps/krylov.hpp:23-34), device-timed."""
     _fields_ = [("iterations", ctypes.c_int), ("converged", ctypes.c_int),
                 ("final_residual", ctypes.c_double), ("seconds", ctypes.c_double),
-                ("precond_seconds", ctypes.c_double), ("matvec_seconds", ctypes.c_double)]
+                ("precond_seconds", ctypes.c_double), ("matvec_seconds", ctypes.c_double),
+                ("wall_build", ctypes.c_double), ("wall_solve", ctypes.c_double),
+                ("precond_memory", ctypes.c_int64), ("basis_orthogonality", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -108,6 +110,7 @@ _sig("hpsb_hierarchy_build", _st, _VP, ctypes.c_int, ctypes.c_int, ctypes.POINTE
 _sig("hpsb_hierarchy_destroy", _st, _VP)
 _sig("hpsb_hierarchy_info", _st, _VP, _I, _I, ctypes.POINTER(ctypes.c_int64), _D)
 _sig("hpsb_hierarchy_level_blocks", _st, _VP, ctypes.c_int, _I, _I, _I, _D)
+_sig("hpsb_hierarchy_level_apply", _st, _VP, ctypes.c_int, _D, _D)
 _sig("hpsb_merge_pair", _st, _VP, ctypes.c_int, _D, _D, _D, _D, ctypes.c_int, ctypes.c_int, _D, _D)
 _sig("hpsb_precond_create", _st, _VP, MgConfig, ctypes.POINTER(_VP))
 _sig("hpsb_precond_destroy", _st, _VP)
@@ -119,6 +122,8 @@ _sig("hpsb_direct_solve_dev", _st, _VP, _VP, _VP)
 _sig("hpsb_precond_apply_dev", _st, _VP, _VP, _VP)
 _sig("hpsb_fgmres", _st, _VP, _VP, _D, _D, KrylovConfig, ctypes.POINTER(SolveReport))
 _sig("hpsb_fgmres_dev", _st, _VP, _VP, _VP, _VP, KrylovConfig, ctypes.POINTER(SolveReport))
+_sig("hpsb_gmres", _st, _VP, _VP, _D, _D, KrylovConfig, ctypes.POINTER(SolveReport))
+_sig("hpsb_gmres_dev", _st, _VP, _VP, _VP, _VP, KrylovConfig, ctypes.POINTER(SolveReport))
 _sig("hpsb_fgmres_batch", _st, _VP, _VP, _D, _D, ctypes.c_int, KrylovConfig,
      ctypes.POINTER(SolveReport))
 _sig("hpsb_fgmres_batch_dev", _st, _VP, _VP, _VP, _VP, ctypes.c_int, KrylovConfig,
@@ -222,8 +227,8 @@ def problem(kind: int = 2, config: int = 0, seed: int | None = None, n: int = 0,
                                   ctypes.byref(nr), ctypes.byref(kk), ctypes.byref(rs),
                                   ctypes.byref(tl)))
     n, order, nrhs = no.value, oo.value, nr.value
-    if kind == 2:
-        kappa = kk.value
+    if kind == 2 and not kappa:
+        kappa = kk.value  # the config's own wavenumber (else an override)
     ne, np1, m = n * n, order + 1, order - 1
     coeff = np.zeros((ne, np1 * np1))
     source = np.zeros((ne, m * m), dtype=np.complex128)
@@ -460,6 +465,14 @@ class MergeHierarchy(_Handle):
         _check(_lib.hpsb_hierarchy_pinned_flops(self._h, ctypes.byref(fe), ctypes.byref(fm)))
         return fe.value, fm.value
 
+    def level_apply(self, level: int, x) -> np.ndarray:
+        """y = M_l x on level l's system (faces [first_face(l), total))."""
+        x = _cplx(x)
+        y = np.zeros_like(x)
+        _check(_lib.hpsb_hierarchy_level_apply(self._h, level, _dp(x.view(np.float64)),
+                                               _dp(y.view(np.float64))))
+        return y
+
     def level_blocks(self, level: int):
         """(first_face, {(r, c): bs x bs block}) of the level system M_l."""
         nb, ff = ctypes.c_int(), ctypes.c_int()
@@ -516,15 +529,20 @@ def build_preconditioner(hier: MergeHierarchy, depth: int = 0, gamma: int = 1,
 
 
 def fgmres(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: int = 60,
-           tol: float = 1e-8, max_iters: int = 2000, record_history: bool = False):
+           tol: float = 1e-8, max_iters: int = 2000, record_history: bool = False,
+           reorthogonalize: bool = True, right: bool = False):
     """Flexible GMRES (fgmres, proj/src/krylov.cpp:188-192); precond None = gmres.
+    right=True: gmres with `precond` as a fixed right preconditioner
+    (krylov.cpp:180-186).  reorthogonalize as KrylovConfig (the reference
+    driver sets it, driver.cpp:132); False runs one modified Gram-Schmidt pass.
     record_history adds the per-iteration |g_{j+1}| / ||b|| (krylov.cpp:118)."""
     rhs = _cplx(rhs)
     x = np.zeros_like(rhs)
     rep = SolveReport()
-    cfg = KrylovConfig(restart, tol, max_iters, int(record_history), 1)
-    _check(_lib.hpsb_fgmres(sk._h, precond._h if precond else None, _dp(rhs.view(np.float64)),
-                            _dp(x.view(np.float64)), cfg, ctypes.byref(rep)),
+    cfg = KrylovConfig(restart, tol, max_iters, int(record_history), int(reorthogonalize))
+    fn = _lib.hpsb_gmres if right else _lib.hpsb_fgmres
+    _check(fn(sk._h, precond._h if precond else None, _dp(rhs.view(np.float64)),
+              _dp(x.view(np.float64)), cfg, ctypes.byref(rep)),
            allow=(OK, NO_CONVERGENCE))
     out = rep.as_dict()
     if record_history:
@@ -538,22 +556,26 @@ def fgmres(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: i
 
 
 def fgmres_batch(sk: SkeletonSystem, rhs, precond: MgPreconditioner | None, restart: int = 60,
-                 tol: float = 1e-8, max_iters: int = 2000):
+                 tol: float = 1e-8, max_iters: int = 2000, reorthogonalize: bool = True):
     """R <= 32 right-hand sides (rows of `rhs`) solved in lockstep with
     multi-RHS operator applications; one report per right-hand side."""
     rhs = np.ascontiguousarray(np.atleast_2d(rhs), dtype=np.complex128)
     R = rhs.shape[0]
     x = np.zeros_like(rhs)
     reps = (SolveReport * R)()
-    cfg = KrylovConfig(restart, tol, max_iters, 0, 1)
+    cfg = KrylovConfig(restart, tol, max_iters, 0, int(reorthogonalize))
     _check(_lib.hpsb_fgmres_batch(sk._h, precond._h if precond else None,
                                   _dp(rhs.view(np.float64)), _dp(x.view(np.float64)), R, cfg, reps),
            allow=(OK, NO_CONVERGENCE))
     return x, [r.as_dict() for r in reps]
 
 
-def gmres(sk: SkeletonSystem, rhs, restart: int = 60, tol: float = 1e-8, max_iters: int = 2000):
-    return fgmres(sk, rhs, None, restart, tol, max_iters)
+def gmres(sk: SkeletonSystem, rhs, restart: int = 60, tol: float = 1e-8, max_iters: int = 2000,
+          right_precond: MgPreconditioner | None = None, record_history: bool = False,
+          reorthogonalize: bool = True):
+    """gmres(op, rhs, cfg, right_precond) (proj/src/krylov.cpp:180-186)."""
+    return fgmres(sk, rhs, right_precond, restart, tol, max_iters, record_history,
+                  reorthogonalize, right=True)
 
 
 def merge_pair(ctx: Context, T1, H1, T2, H2, alpha: int, beta: int, side_len: int):

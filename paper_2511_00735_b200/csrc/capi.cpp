@@ -76,6 +76,15 @@ hpsb_status guarded(F&& f) {
   }
 }
 
+hpsb::Context* ctx_of(hpsb_context c) { return c ? &c->c : nullptr; }
+hpsb::Context* ctx_of(hpsb_elements e) { return e && e->e ? e->e->ctx : nullptr; }
+hpsb::Context* ctx_of(hpsb_skeleton s) { return s && s->s ? s->s->ctx : nullptr; }
+hpsb::Context* ctx_of(hpsb_hierarchy h) { return h && h->h ? h->h->ctx : nullptr; }
+hpsb::Context* ctx_of(hpsb_precond p) { return p ? hpsb::precond_context(p->p) : nullptr; }
+// Device allocations and staged uploads of the call go to the stream of the
+// handle's own context (internal.hpp, ContextBind).
+#define BIND(h) hpsb::ContextBind bind_ctx_(ctx_of(h))
+
 #define REQUIRE(cond, msg) \
   do {                     \
     if (!(cond)) throw hpsb::InvalidArgument(msg); \
@@ -84,7 +93,7 @@ hpsb_status guarded(F&& f) {
 hpsb::problem::Spec make_spec(int kind, int config, uint64_t seed, int n, int order, double kappa) {
   if (kind == 0) return hpsb::problem::reference_bump(n, order, kappa);
   if (kind == 1) return hpsb::problem::reference_planewave(n, order, kappa);
-  if (kind == 2) return hpsb::problem::baseline_config(config, seed, n, order);
+  if (kind == 2) return hpsb::problem::baseline_config(config, seed, n, order, kappa);
   throw hpsb::InvalidArgument("problem kind must be 0, 1 or 2");
 }
 }  // namespace
@@ -115,7 +124,6 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     HPSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
     uint64_t threshold = UINT64_MAX;
     HPSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
-    hpsb::alloc_stream() = ctx->c.stream;
     // Map pool memory once, here, instead of inside the first setups: growing
     // a stream-ordered pool maps physical pages (~60 ms/GB measured), which
     // would otherwise land inside build_hierarchy.  HPSB_POOL_RESERVE_GB
@@ -137,15 +145,6 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
         HPSB_CUDA(cudaStreamSynchronize(ctx->c.stream));
       }
     }
-    auto& st = hpsb::staging();
-    if (!st.base) {
-      // Large enough that one setup's descriptor uploads never wrap (a wrap
-      // synchronises the stream and stalls host/device overlap).
-      st.size = size_t(512) << 20;
-      HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.base), st.size));
-    }
-    st.stream = ctx->c.stream;
-    st.head = 0;
     *out = ctx.release();
     return HPSB_OK;
   });
@@ -153,10 +152,9 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
 
 hpsb_status hpsb_context_destroy(hpsb_context ctx) {
   return guarded([&] {
+    BIND(ctx);
     if (!ctx) return HPSB_OK;
     cudaStreamSynchronize(ctx->c.stream);
-    if (hpsb::alloc_stream() == ctx->c.stream) hpsb::alloc_stream() = nullptr;
-    if (hpsb::staging().stream == ctx->c.stream) hpsb::staging().stream = nullptr;
     for (auto& e : ctx->c.ev) cudaEventDestroy(e);
     for (auto& e : ctx->c.timer)
       if (e) cudaEventDestroy(e);
@@ -170,6 +168,7 @@ hpsb_status hpsb_context_destroy(hpsb_context ctx) {
 
 hpsb_status hpsb_context_synchronize(hpsb_context ctx) {
   return guarded([&] {
+    BIND(ctx);
     HPSB_CUDA(cudaStreamSynchronize(ctx->c.stream));
     return HPSB_OK;
   });
@@ -188,6 +187,7 @@ int64_t hpsb_context_residual_history(hpsb_context ctx, double* out, int64_t cap
 
 hpsb_status hpsb_context_timer_start(hpsb_context ctx) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx, "timer: null context");
     for (auto& e : ctx->c.timer)
       if (!e) HPSB_CUDA(cudaEventCreate(&e));
@@ -198,6 +198,7 @@ hpsb_status hpsb_context_timer_start(hpsb_context ctx) {
 
 hpsb_status hpsb_context_timer_stop(hpsb_context ctx, double* seconds) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx && seconds && ctx->c.timer[0], "timer: not started");
     HPSB_CUDA(cudaEventRecord(ctx->c.timer[1], ctx->c.stream));
     HPSB_CUDA(cudaEventSynchronize(ctx->c.timer[1]));
@@ -210,6 +211,7 @@ hpsb_status hpsb_context_timer_stop(hpsb_context ctx, double* seconds) {
 
 hpsb_status hpsb_context_profile(hpsb_context ctx, int enable) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx, "profile: null context");
     ctx->c.collect();
     ctx->c.profile = enable != 0;
@@ -231,6 +233,7 @@ hpsb_status hpsb_context_profile_entry(hpsb_context ctx, int i, char* name, int 
                                        int64_t* launches, double* ms, double* bytes,
                                        double* flops) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx, "profile: null context");
     ctx->c.collect();
     REQUIRE(i >= 0 && i < static_cast<int>(ctx->c.agg.size()), "profile: index out of range");
@@ -249,6 +252,7 @@ hpsb_status hpsb_context_profile_entry(hpsb_context ctx, int i, char* name, int 
 
 hpsb_status hpsb_context_profile_reset(hpsb_context ctx) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx, "profile: null context");
     ctx->c.collect();
     ctx->c.agg.clear();
@@ -261,6 +265,7 @@ int64_t hpsb_precond_bytes(hpsb_precond p) { return p ? hpsb::precond_bytes(p->p
 hpsb_status hpsb_hierarchy_pinned_flops(hpsb_hierarchy h, double* element_flops,
                                         double* merge_flops) {
   return guarded([&] {
+    BIND(h);
     REQUIRE(h, "hierarchy_pinned_flops: null handle");
     double fe = 0, fm = 0;
     hpsb::hierarchy_pinned(h->h.get(), &fe, &fm, nullptr);
@@ -290,6 +295,7 @@ hpsb_status hpsb_nccl_unique_id(unsigned char id[128]) {
 hpsb_status hpsb_context_attach_nccl(hpsb_context ctx, const unsigned char id[128], int rank,
                                      int world) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx && id && world >= 1 && rank >= 0 && rank < world, "attach_nccl: bad argument");
     ctx->c.comm = hpsb::make_nccl_comm(id, rank, world, ctx->c.device);
     return HPSB_OK;
@@ -311,6 +317,7 @@ hpsb_status hpsb_local_group_destroy(hpsb_local_group g) {
 
 hpsb_status hpsb_context_attach_local(hpsb_context ctx, hpsb_local_group g, int rank) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx && g, "attach_local: null argument");
     ctx->c.comm = hpsb::make_thread_comm(g->g, rank);
     return HPSB_OK;
@@ -319,6 +326,7 @@ hpsb_status hpsb_context_attach_local(hpsb_context ctx, hpsb_local_group g, int 
 
 hpsb_status hpsb_context_comm_info(hpsb_context ctx, int* rank, int* world) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx, "comm_info: null context");
     if (rank) *rank = ctx->c.rank();
     if (world) *world = ctx->c.world();
@@ -382,7 +390,7 @@ hpsb_status hpsb_problem_dims(int kind, int config, int n, int order, int* n_out
                               int* nrhs_out, double* kappa_out, int* restart_out,
                               double* tol_out) {
   return guarded([&] {
-    const auto spec = make_spec(kind, config, 0, n, order, 1.0);
+    const auto spec = make_spec(kind, config, 0, n, order, kind == 2 ? 0.0 : 1.0);
     *n_out = spec.n, *order_out = spec.order, *nrhs_out = static_cast<int>(spec.angles.size());
     if (kappa_out) *kappa_out = spec.kappa;
     if (restart_out) *restart_out = spec.restart;
@@ -409,6 +417,7 @@ hpsb_status hpsb_elements_build_dev(hpsb_context ctx, int n, int order, double e
                                     const double* coeff_dev, const double* source_dev,
                                     hpsb_elements* out) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx && out && coeff_dev, "elements_build: null argument");
     auto h = std::make_unique<hpsb_elements_s>();
     h->e = hpsb::build_elements(&ctx->c, n, order, eta, coeff_dev,
@@ -421,6 +430,7 @@ hpsb_status hpsb_elements_build_dev(hpsb_context ctx, int n, int order, double e
 hpsb_status hpsb_elements_build(hpsb_context ctx, int n, int order, double eta, const double* coeff,
                                 const double* source, hpsb_elements* out) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx && out && coeff, "elements_build: null argument");
     REQUIRE(n >= 2 && order >= 2, "elements_build: bad mesh");
     const size_t ne = static_cast<size_t>(n) * n, np = order + 1, m = order - 1;
@@ -437,12 +447,14 @@ hpsb_status hpsb_elements_build(hpsb_context ctx, int n, int order, double eta, 
 }
 
 hpsb_status hpsb_elements_destroy(hpsb_elements el) {
+  BIND(el);
   delete el;
   return HPSB_OK;
 }
 
 hpsb_status hpsb_elements_fallbacks(hpsb_elements el, int* count) {
   return guarded([&] {
+    BIND(el);
     REQUIRE(el && count, "elements_fallbacks: null argument");
     hpsb::elements_wait(el->e.get());
     *count = el->e->fallbacks;
@@ -452,6 +464,7 @@ hpsb_status hpsb_elements_fallbacks(hpsb_elements el, int* count) {
 
 hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, double* H) {
   return guarded([&] {
+    BIND(el);
     hpsb::elements_wait(el ? el->e.get() : nullptr);
     const auto& E = *el->e;
     const int ne = E.n * E.n;
@@ -469,6 +482,7 @@ hpsb_status hpsb_elements_get(hpsb_elements el, int e0, int count, double* T, do
 hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs,
                                  hpsb_skeleton* out) {
   return guarded([&] {
+    BIND(el);
     REQUIRE(el && out && tside && nrhs >= 1, "skeleton_create: bad argument");
     auto h = std::make_unique<hpsb_skeleton_s>();
     h->s = hpsb::build_skeleton(el->e.get(), reinterpret_cast<const double2*>(tside), nrhs);
@@ -480,6 +494,7 @@ hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs
 hpsb_status hpsb_skeleton_create_boundary(hpsb_elements el, const double* tbnd, int nrhs,
                                           hpsb_skeleton* out) {
   return guarded([&] {
+    BIND(el);
     REQUIRE(el && out && tbnd && nrhs >= 1, "skeleton_create_boundary: bad argument");
     auto h = std::make_unique<hpsb_skeleton_s>();
     h->s = hpsb::build_skeleton(el->e.get(), reinterpret_cast<const double2*>(tbnd), nrhs, true);
@@ -489,6 +504,7 @@ hpsb_status hpsb_skeleton_create_boundary(hpsb_elements el, const double* tbnd, 
 }
 
 hpsb_status hpsb_skeleton_destroy(hpsb_skeleton sk) {
+  BIND(sk);
   delete sk;
   return HPSB_OK;
 }
@@ -502,6 +518,7 @@ const double* hpsb_skeleton_rhs_dev(hpsb_skeleton sk, int r) {
 
 hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && rhs && r >= 0 && r < sk->s->nrhs, "skeleton_rhs: bad argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     // the skeleton build returns without synchronising; cudaMemcpy runs on
@@ -515,6 +532,7 @@ hpsb_status hpsb_skeleton_rhs(hpsb_skeleton sk, int r, double* rhs) {
 
 hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x, double* y) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && x && y, "skeleton_apply: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     hpsb::skeleton_apply(sk->s.get(), reinterpret_cast<const double2*>(x),
@@ -525,6 +543,7 @@ hpsb_status hpsb_skeleton_apply_dev(hpsb_skeleton sk, const double* x, double* y
 
 hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && x && y, "skeleton_apply: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     auto* S = sk->s.get();
@@ -539,6 +558,7 @@ hpsb_status hpsb_skeleton_apply(hpsb_skeleton sk, const double* x, double* y) {
 
 hpsb_status hpsb_recover_dev(hpsb_skeleton sk, const double* x, int r, double* field) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && x && field, "recover: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     hpsb::recover_field(sk->s.get(), reinterpret_cast<const double2*>(x), r,
@@ -549,6 +569,7 @@ hpsb_status hpsb_recover_dev(hpsb_skeleton sk, const double* x, int r, double* f
 
 hpsb_status hpsb_recover(hpsb_skeleton sk, const double* x, int r, double* field) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && x && field, "recover: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     auto* S = sk->s.get();
@@ -567,6 +588,7 @@ hpsb_status hpsb_recover(hpsb_skeleton sk, const double* x, int r, double* field
 hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
                                  hpsb_hierarchy* out) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && out, "hierarchy_build: null argument");
     auto h = std::make_unique<hpsb_hierarchy_s>();
     auto* hs = h.get();
@@ -593,6 +615,7 @@ hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
 }
 
 hpsb_status hpsb_hierarchy_destroy(hpsb_hierarchy h) {
+  BIND(h);
   delete h;
   return HPSB_OK;
 }
@@ -600,6 +623,7 @@ hpsb_status hpsb_hierarchy_destroy(hpsb_hierarchy h) {
 hpsb_status hpsb_hierarchy_info(hpsb_hierarchy h, int* depth, int* total_levels,
                                 int64_t* device_bytes, double* build_seconds) {
   return guarded([&] {
+    BIND(h);
     REQUIRE(h, "hierarchy_info: null handle");
     if (depth) *depth = h->h->depth;
     if (total_levels) *total_levels = h->h->total_levels;
@@ -612,8 +636,27 @@ hpsb_status hpsb_hierarchy_info(hpsb_hierarchy h, int* depth, int* total_levels,
 hpsb_status hpsb_hierarchy_level_blocks(hpsb_hierarchy h, int level, int* nblocks, int* first_face,
                                         int* keys, double* data) {
   return guarded([&] {
+    BIND(h);
     REQUIRE(h && nblocks && first_face, "hierarchy_level_blocks: null argument");
     hpsb::hierarchy_level_blocks(h->h.get(), level, nblocks, first_face, keys, data);
+    return HPSB_OK;
+  });
+}
+
+hpsb_status hpsb_hierarchy_level_apply(hpsb_hierarchy h, int level, const double* x, double* y) {
+  return guarded([&] {
+    BIND(h);
+    REQUIRE(h && x && y, "hierarchy_level_apply: null argument");
+    auto* H = h->h.get();
+    REQUIRE(level >= 1 && level <= H->depth, "hierarchy_level_apply: level out of range");
+    const auto& g = H->sk->graph;
+    const size_t n = static_cast<size_t>(g.num_faces() - g.level_range[level - 1].first) * H->sk->bs;
+    cudaStream_t st = H->ctx->stream;
+    hpsb::DevBuf<double2> xd(n), yd(n);
+    HPSB_CUDA(cudaMemcpyAsync(xd.p, x, xd.bytes(), cudaMemcpyHostToDevice, st));
+    hpsb::hierarchy_level_apply(H, level, xd.p, yd.p);
+    HPSB_CUDA(cudaMemcpyAsync(y, yd.p, yd.bytes(), cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
     return HPSB_OK;
   });
 }
@@ -622,6 +665,7 @@ hpsb_status hpsb_merge_pair(hpsb_context ctx, int side_len, const double* T1, co
                             const double* T2, const double* H2, int alpha, int beta, double* T,
                             double* H) {
   return guarded([&] {
+    BIND(ctx);
     REQUIRE(ctx && T1 && H1 && T2 && H2 && T && H, "merge_pair: null argument");
     REQUIRE(side_len >= 1 && alpha >= 0 && alpha < 4 && beta >= 0 && beta < 4,
             "merge_pair: bad sides");
@@ -635,6 +679,7 @@ hpsb_status hpsb_merge_pair(hpsb_context ctx, int side_len, const double* T1, co
 
 hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_precond* out) {
   return guarded([&] {
+    BIND(h);
     REQUIRE(h && out, "precond_create: null argument");
     auto p = std::make_unique<hpsb_precond_s>();
     if (h->pending && cfg.depth == h->h->depth && cfg.gamma == 1 && cfg.coarse_iters == 4 &&
@@ -651,6 +696,7 @@ hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_preco
 
 hpsb_status hpsb_direct_solve_dev(hpsb_hierarchy h, const double* rhs, double* x) {
   return guarded([&] {
+    BIND(h);
     REQUIRE(h && rhs && x, "direct_solve: null argument");
     REQUIRE(h->direct && h->h->depth == h->h->total_levels,
             "direct_solve: hierarchy not built to full depth");
@@ -661,6 +707,7 @@ hpsb_status hpsb_direct_solve_dev(hpsb_hierarchy h, const double* rhs, double* x
 
 hpsb_status hpsb_direct_solve(hpsb_hierarchy h, const double* rhs, double* x) {
   return guarded([&] {
+    BIND(h);
     REQUIRE(h && rhs && x, "direct_solve: null argument");
     REQUIRE(h->direct && h->h->depth == h->h->total_levels,
             "direct_solve: hierarchy not built to full depth");
@@ -671,12 +718,14 @@ hpsb_status hpsb_direct_solve(hpsb_hierarchy h, const double* rhs, double* x) {
 }
 
 hpsb_status hpsb_precond_destroy(hpsb_precond p) {
+  BIND(p);
   delete p;
   return HPSB_OK;
 }
 
 hpsb_status hpsb_precond_apply_dev(hpsb_precond p, const double* v, double* z) {
   return guarded([&] {
+    BIND(p);
     REQUIRE(p && v && z, "precond_apply: null argument");
     hpsb::precond_apply(p->p, reinterpret_cast<const double2*>(v), reinterpret_cast<double2*>(z));
     return HPSB_OK;
@@ -685,6 +734,7 @@ hpsb_status hpsb_precond_apply_dev(hpsb_precond p, const double* v, double* z) {
 
 hpsb_status hpsb_precond_apply(hpsb_precond p, const double* v, double* z) {
   return guarded([&] {
+    BIND(p);
     REQUIRE(p && v && z, "precond_apply: null argument");
     hpsb::precond_apply_host(p->p, reinterpret_cast<const double2*>(v),
                              reinterpret_cast<double2*>(z));
@@ -695,6 +745,7 @@ hpsb_status hpsb_precond_apply(hpsb_precond p, const double* v, double* z) {
 hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
                             hpsb_krylov_config cfg, hpsb_solve_report* report) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && rhs && x && report, "fgmres: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     return hpsb::fgmres(sk->s.get(), precond ? precond->p : nullptr,
@@ -706,6 +757,7 @@ hpsb_status hpsb_fgmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double
 hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
                         hpsb_krylov_config cfg, hpsb_solve_report* report) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && rhs && x && report, "fgmres: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     auto* S = sk->s.get();
@@ -720,8 +772,39 @@ hpsb_status hpsb_fgmres(hpsb_skeleton sk, hpsb_precond precond, const double* rh
   });
 }
 
+hpsb_status hpsb_gmres_dev(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                           hpsb_krylov_config cfg, hpsb_solve_report* report) {
+  return guarded([&] {
+    BIND(sk);
+    REQUIRE(sk && rhs && x && report, "gmres: null argument");
+    hpsb::elements_wait(sk->s->el);
+    return hpsb::fgmres(sk->s.get(), precond ? precond->p : nullptr,
+                        reinterpret_cast<const double2*>(rhs), reinterpret_cast<double2*>(x), cfg,
+                        report, /*right=*/true);
+  });
+}
+
+hpsb_status hpsb_gmres(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
+                       hpsb_krylov_config cfg, hpsb_solve_report* report) {
+  return guarded([&] {
+    BIND(sk);
+    REQUIRE(sk && rhs && x && report, "gmres: null argument");
+    hpsb::elements_wait(sk->s->el);
+    auto* S = sk->s.get();
+    cudaStream_t st = S->ctx->stream;
+    hpsb::DevBuf<double2> b(S->dim), xd(S->dim);
+    HPSB_CUDA(cudaMemcpyAsync(b.p, rhs, b.bytes(), cudaMemcpyHostToDevice, st));
+    const hpsb_status rc =
+        hpsb::fgmres(S, precond ? precond->p : nullptr, b.p, xd.p, cfg, report, /*right=*/true);
+    HPSB_CUDA(cudaMemcpyAsync(x, xd.p, xd.bytes(), cudaMemcpyDeviceToHost, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    return rc;
+  });
+}
+
 hpsb_status hpsb_skeleton_apply_batch_dev(hpsb_skeleton sk, const double* x, double* y, int nrhs) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && x && y, "skeleton_apply: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     hpsb::skeleton_apply_batch(sk->s.get(), reinterpret_cast<const double2*>(x),
@@ -732,6 +815,7 @@ hpsb_status hpsb_skeleton_apply_batch_dev(hpsb_skeleton sk, const double* x, dou
 
 hpsb_status hpsb_precond_apply_batch_dev(hpsb_precond p, const double* v, double* z, int nrhs) {
   return guarded([&] {
+    BIND(p);
     REQUIRE(p && v && z, "precond_apply: null argument");
     hpsb::precond_apply_batch(p->p, reinterpret_cast<const double2*>(v),
                               reinterpret_cast<double2*>(z), nrhs);
@@ -743,6 +827,7 @@ hpsb_status hpsb_fgmres_batch_dev(hpsb_skeleton sk, hpsb_precond precond, const 
                                   double* x, int nrhs, hpsb_krylov_config cfg,
                                   hpsb_solve_report* reports) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && rhs && x && reports, "fgmres: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     return hpsb::fgmres_batch(sk->s.get(), precond ? precond->p : nullptr,
@@ -754,6 +839,7 @@ hpsb_status hpsb_fgmres_batch_dev(hpsb_skeleton sk, hpsb_precond precond, const 
 hpsb_status hpsb_fgmres_batch(hpsb_skeleton sk, hpsb_precond precond, const double* rhs, double* x,
                               int nrhs, hpsb_krylov_config cfg, hpsb_solve_report* reports) {
   return guarded([&] {
+    BIND(sk);
     REQUIRE(sk && rhs && x && reports, "fgmres: null argument");
     hpsb::elements_wait(sk->s->el);  // element-stage errors surface here at the latest
     REQUIRE(nrhs >= 1 && nrhs <= 32, "fgmres: 1 <= nrhs <= 32");

@@ -562,7 +562,6 @@ __global__ void v5_mark_kernel(V5Args v) {
 }  // namespace
 
 bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
-  if (std::getenv("HPSB_ELEMENT_V4")) return false;
   const int P = a0.npad, nbc = a0.nbc, nb = a0.nb;
   if (a0.order + 1 > 64 || nb > kGjMax || nwork <= 0) return false;
   const int nblk = (P + V5B - 1) / V5B;

@@ -282,16 +282,39 @@ void Context::collect() {
   pending.clear();
 }
 
+Context*& bound_context() {
+  thread_local Context* c = nullptr;
+  return c;
+}
+cudaStream_t alloc_stream() {
+  const Context* c = bound_context();
+  return c ? c->stream : nullptr;
+}
+
+Staging::~Staging() {
+  if (base) cudaFreeHost(base);
+}
+
 void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-  Staging& st = staging();
-  if (!st.base || st.stream != s || bytes > st.size / 2) {
+  Context* c = bound_context();
+  if (!c || c->stream != s || bytes > kStagingMax / 2) {
     HPSB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
     return;
   }
+  Staging& st = c->staging;
   const size_t need = (bytes + 255) & ~size_t(255);
   if (st.head + need > st.size) {
     HPSB_CUDA(cudaStreamSynchronize(s));  // all earlier staged copies have completed
     st.head = 0;
+    if (st.size < kStagingMax || need > st.size) {
+      size_t grow = std::max<size_t>(size_t(16) << 20, 2 * st.size);
+      while (grow < need) grow *= 2;
+      grow = std::min(grow, kStagingMax);
+      if (st.base) HPSB_CUDA(cudaFreeHost(st.base));
+      st.base = nullptr;
+      HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.base), grow));
+      st.size = grow;
+    }
   }
   std::memcpy(st.base + st.head, src, bytes);
   HPSB_CUDA(cudaMemcpyAsync(dst, st.base + st.head, bytes, cudaMemcpyHostToDevice, s));

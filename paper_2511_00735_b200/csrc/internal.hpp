@@ -58,30 +58,38 @@ void allow_smem(size_t bytes) {
   } while (0)
 
 // ---------------------------------------------------------------- device memory
-// Device buffers come from the stream-ordered pool of the active context's
-// stream (cudaMallocAsync with an unbounded release threshold): the merge
-// stage allocates and frees per level, and pooled allocations keep that off
-// the critical path (no implicit device synchronisation as in cudaFree).
-// Per host thread (one context per thread, e.g. the emulated ranks).
-inline cudaStream_t& alloc_stream() {
-  thread_local cudaStream_t s = nullptr;
-  return s;
-}
+// Device buffers come from the stream-ordered pool (cudaMallocAsync with an
+// unbounded release threshold): the merge stage allocates and frees per
+// level, and pooled allocations keep that off the critical path (no implicit
+// device synchronisation as in cudaFree).  Allocations are ordered on the
+// stream of the context BOUND to the calling host thread (every ABI entry
+// point binds the context of the handle it works on, ContextBind); a buffer
+// remembers that stream and is freed on it, so its release is ordered after
+// every kernel of its own context whatever context is bound at that point.
+struct Context;
+Context*& bound_context();
+cudaStream_t alloc_stream();  // the bound context's stream, or null (plain cudaMalloc)
+struct ContextBind {
+  Context* prev;
+  explicit ContextBind(Context* c) : prev(bound_context()) { bound_context() = c; }
+  ~ContextBind() { bound_context() = prev; }
+  ContextBind(const ContextBind&) = delete;
+  ContextBind& operator=(const ContextBind&) = delete;
+};
 
-// Pinned staging ring for host->device descriptor uploads: a cudaMemcpyAsync
-// from pageable memory waits for the stream to drain, which would serialise
-// every batched launch of the merge stage with the host.  Uploads are copied
-// into this ring and issued from pinned memory; the ring is recycled after a
-// stream synchronisation when it wraps.
+// Pinned staging ring for host->device descriptor uploads, one per context:
+// a cudaMemcpyAsync from pageable memory waits for the stream to drain, which
+// would serialise every batched launch of the merge stage with the host.
+// Uploads are copied into the ring and issued from pinned memory on the
+// context's stream; when the ring wraps, the stream is synchronised (every
+// earlier staged copy has landed) and the ring grows, up to kStagingMax, so
+// that one setup's uploads stop wrapping after the first.
 struct Staging {
   unsigned char* base = nullptr;
   size_t size = 0, head = 0;
-  cudaStream_t stream = nullptr;
+  ~Staging();
 };
-inline Staging& staging() {
-  thread_local Staging s;
-  return s;
-}
+constexpr size_t kStagingMax = size_t(512) << 20;
 void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
 template <class T>
@@ -92,12 +100,13 @@ struct DevBuf {
   explicit DevBuf(std::size_t count) { alloc(count); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  cudaStream_t s = nullptr;  // stream the buffer was allocated on (null: cudaMalloc)
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr, o.n = 0, o.s = nullptr; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     if (this != &o) {
       release();
-      p = o.p, n = o.n;
-      o.p = nullptr, o.n = 0;
+      p = o.p, n = o.n, s = o.s;
+      o.p = nullptr, o.n = 0, o.s = nullptr;
     }
     return *this;
   }
@@ -105,8 +114,9 @@ struct DevBuf {
   void alloc(std::size_t count) {
     release();
     if (count) {
-      if (alloc_stream())
-        HPSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), alloc_stream()));
+      s = alloc_stream();
+      if (s)
+        HPSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
       else
         HPSB_CUDA(cudaMalloc(reinterpret_cast<void**>(&p), count * sizeof(T)));
     }
@@ -114,10 +124,10 @@ struct DevBuf {
   }
   void release() {
     if (p) {
-      if (alloc_stream()) cudaFreeAsync(p, alloc_stream());
+      if (s) cudaFreeAsync(p, s);
       else cudaFree(p);
     }
-    p = nullptr, n = 0;
+    p = nullptr, n = 0, s = nullptr;
   }
   std::size_t bytes() const { return n * sizeof(T); }
   void upload(const std::vector<T>& v, cudaStream_t s) {
@@ -178,6 +188,7 @@ struct Context {
   // residual history of the last single-RHS (F)GMRES with record_history
   // (gmres_driver's report.residual_history, krylov.cpp:118)
   std::vector<double> history;
+  Staging staging;  // pinned upload ring of this context's stream
 };
 
 // Brackets one kernel launch with CUDA events when profiling is enabled and
@@ -392,8 +403,11 @@ std::unique_ptr<Hierarchy> build_hierarchy(Skeleton* sk, int depth,
                                            const std::function<void(Hierarchy*)>& before_wait = {});
 void hierarchy_level_blocks(const Hierarchy* h, int level, int* nblocks, int* first_face,
                             int* keys, double* data);
+// y = M_l x on level l's system (device vectors of the level's length).
+void hierarchy_level_apply(Hierarchy* h, int level, const double2* x_dev, double2* y_dev);
 Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg);
 void destroy_precond(Precond* p);
+Context* precond_context(const Precond* p);
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev);
 // precond_apply is a fixed launch sequence (single GPU, gamma == 1 or exact
 // coarse): it can be captured into a CUDA graph
@@ -408,7 +422,12 @@ double precond_pinned_bytes(const Precond* p);
 void merge_pair(Context* ctx, int m, const double2* T1, const double2* H1, const double2* T2,
                 const double2* H2, int alpha, int beta, double2* T, double2* H);
 hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs_dev, double2* x_dev,
-                   const hpsb_krylov_config& cfg, hpsb_solve_report* rep);
+                   const hpsb_krylov_config& cfg, hpsb_solve_report* rep, bool right = false);
+// MgPreconditioner::memory_bytes (multigrid.cpp:102-113) on the device layout
+// (box maps of levels 2..depth, merge factors of levels < depth, dense coarse
+// inverse), and the device build time of the hierarchy behind it.
+int64_t precond_memory(const Precond* p);
+double precond_build_seconds(const Precond* p);
 
 // Small device kernels shared between modules (csrc/blas.cu).
 void zfill(Context* ctx, double2* p, std::size_t n, double2 v);

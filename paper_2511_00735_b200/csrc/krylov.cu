@@ -107,8 +107,10 @@ __global__ void __launch_bounds__(kThreads) dots_fused_kernel(
 // One pass of CGS2 over the rows of a block (kOrthThreads x R rows per block,
 // w's rows kept in registers):
 //   kUpdate: w -= V h_upd (the previous pass's projection), written back;
-//   then partial[b, i] = sum_rows conj(V[k, i]) w[k] for i < ncols, or, with
-//   ncols == 0, partial[b, 0] = sum_rows |w[k]|^2.
+//   then partial[b, i] = sum_rows conj(V[k, vdot + i]) w[k] for i < ncols,
+//   or, with ncols == 0, partial[b, 0] = sum_rows |w[k]|^2.
+// A modified Gram-Schmidt step is the same pass with one update column and
+// one dot column (vdot = 1): w -= h_{i-1} V_{i-1}, then h_i = V_i^H w.
 // With `fused`, the last block to finish (atomic ticket) sums the partials in
 // fixed block order into out (deterministic); else reduce_kernel does.
 constexpr int kOrthThreads = 128;
@@ -123,7 +125,7 @@ template <bool kUpdate>
 __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd,
     int nupd, double2* w, int64_t n, int R, double2* partial, double2* out, unsigned* ticket,
-    int fused, OrthStride bs, const int* jdev) {
+    int fused, OrthStride bs, const int* jdev, int vdot) {
   __shared__ double2 sh[kOrthThreads / 32][104];
   __shared__ double2 hs[104];
   __shared__ bool last;
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
           double2 v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            v[q] = i0 + q < ncols ? ldg2(V + (i0 + q) * ld + k) : make_double2(0.0, 0.0);
+            v[q] = i0 + q < ncols ? ldg2(V + (vdot + i0 + q) * ld + k) : make_double2(0.0, 0.0);
 #pragma unroll
           for (int q = 0; q < 8; ++q) acc[q] = cfma_conj(v[q], wv[r], acc[q]);
         }
@@ -463,6 +465,31 @@ void apply_givens(const Givens& g, cd& a, cd& b) {  // krylov.cpp:33-37
   a = t;
 }
 
+// The orthogonalisation kernels keep their coefficients in shared memory
+// (<= 104 columns per launch).  orth_any issues one logical pass over any
+// number of columns as launches of at most kOrthChunk columns:
+//   w -= V[0..nupd) h_upd, then out = V[vdot..vdot+ncols)^H w (ncols > 0) or
+//   out[0] = ||w||^2 (ncols == 0).
+// launch(Vbase, ncols, h_upd, nupd, out, vdot) is one kernel launch of that
+// form; `scratch` receives the discarded norms of intermediate update chunks.
+constexpr int kOrthChunk = 96;
+template <class L>
+void orth_any(L&& launch, const double2* V, int64_t ld, int ncols, const double2* h_upd, int nupd,
+              double2* out, int vdot, double2* scratch) {
+  if (ncols <= kOrthChunk && nupd <= kOrthChunk) {
+    launch(V, ncols, h_upd, nupd, out, vdot);
+    return;
+  }
+  for (int u0 = 0; u0 < nupd; u0 += kOrthChunk) {
+    const int cu = std::min(kOrthChunk, nupd - u0);
+    const bool last = u0 + cu >= nupd;
+    launch(V + u0 * ld, 0, h_upd + u0, cu, (last && ncols == 0) ? out : scratch, 0);
+  }
+  if (ncols == 0 && nupd > 0) return;
+  for (int d0 = 0; d0 < ncols; d0 += kOrthChunk)
+    launch(V, std::min(kOrthChunk, ncols - d0), nullptr, 0, out + d0, vdot + d0);
+}
+
 struct Work {
   Context* ctx;
   int64_t n;
@@ -474,7 +501,7 @@ struct Work {
     blocks = static_cast<int>((dim + kRowsPerBlock - 1) / kRowsPerBlock);
     chunk = kRowsPerBlock;
     partial.alloc(static_cast<size_t>((dim + kOrthThreads - 1) / kOrthThreads + blocks) * maxcols);
-    hdev.alloc(3 * static_cast<size_t>(maxcols) + 4);
+    hdev.alloc(3 * static_cast<size_t>(maxcols) + 4);  // h1 | h2 | norm ... | scratch (last)
     ticket.alloc(1);
     HPSB_CUDA(cudaMemsetAsync(ticket.p, 0, sizeof(unsigned), c->stream));
   }
@@ -501,8 +528,17 @@ struct Work {
   }
   // One CGS2 pass (orth_kernel): optionally w -= V h_upd, then out = V^H w
   // (ncols > 0) or out[0] = ||w||^2 (ncols == 0).
+  // any column count (orth_any); jdev (device-driven cycle) needs <= kOrthChunk
   void orth(const double2* V, int ncols, const double2* h_upd, int nupd, double2* w, double2* out,
-            const int* jdev = nullptr, int maxcols = 0) {
+            const int* jdev = nullptr, int maxcols = 0, int vdot = 0) {
+    if (jdev) return orth1(V, ncols, h_upd, nupd, w, out, jdev, maxcols, vdot);
+    orth_any([&](const double2* Vb, int nc, const double2* hu, int nu, double2* o, int vd) {
+               orth1(Vb, nc, hu, nu, w, o, nullptr, 0, vd);
+             },
+             V, n, ncols, h_upd, nupd, out, vdot, hdev.p + hdev.n - 1);
+  }
+  void orth1(const double2* V, int ncols, const double2* h_upd, int nupd, double2* w, double2* out,
+             const int* jdev, int maxcols, int vdot) {
     int R, nb;
     orth_grid(R, nb);
     // (device-driven: ncols / nupd are flags, the counts come from *jdev; the
@@ -514,10 +550,10 @@ struct Work {
                    8.0 * n * (ncols + nupd));
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev);
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot);
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev);
+               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot);
     if (!fused)
       launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1,
                static_cast<const double2*>(partial.p), nb, jdev ? ncols : nout, out, jdev);
@@ -539,7 +575,9 @@ struct Work {
   }
   void axpy(const double2* V, int ncols, const double2* h, double sign, double2* w) {
     KernelScope ks(ctx, "gmres_axpy", 16.0 * n * (ncols + 2), 8.0 * n * ncols);
-    launch_k(ctx, axpy_kernel, dim3(grid()), dim3(kThreads), 0, 1, V, n, ncols, h, sign, w, n);
+    for (int c0 = 0; c0 < ncols; c0 += kOrthChunk)
+      launch_k(ctx, axpy_kernel, dim3(grid()), dim3(kThreads), 0, 1, V + c0 * n, n,
+               std::min(kOrthChunk, ncols - c0), h + c0, sign, w, n);
   }
   double norm(const double2* w) {
     dots(w, 1, w, hdev.p);
@@ -649,10 +687,12 @@ struct CycleGraph {
   }
 };
 
+// right = true: gmres with a fixed right preconditioner (krylov.cpp:180-186):
+// w = M P(V_j), and at the end of a cycle x += P(V y); else flexible GMRES
+// (fgmres, krylov.cpp:188-192) storing Z_j = P(V_j) and x += Z y.
 hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
-                   const hpsb_krylov_config& cfg, hpsb_solve_report* rep) {
+                   const hpsb_krylov_config& cfg, hpsb_solve_report* rep, bool right) {
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
-  if (cfg.restart > 100) throw InvalidArgument("gmres: restart must be <= 100 on the B200 path");
   if (!(cfg.tol > 0.0 && cfg.tol < 1.0)) throw InvalidArgument("gmres: tol must lie in (0, 1)");
   if (cfg.max_iters < 1) throw InvalidArgument("gmres: max_iters must be >= 1");
   Context* ctx = sk->ctx;
@@ -662,8 +702,13 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   Work wk(ctx, n, restart + 2);
   ctx->history.clear();
   DevBuf<double2> V(static_cast<size_t>(n) * (restart + 1));
-  DevBuf<double2> Z(pc ? static_cast<size_t>(n) * restart : 0);
-  DevBuf<double2> w(n), tmp(n);
+  if (!pc) right = false;
+  DevBuf<double2> Z(pc && !right ? static_cast<size_t>(n) * restart : 0);
+  DevBuf<double2> w(n), tmp(n), pz(right ? n : 0), pu(right ? n : 0);
+  if (pc) {
+    rep->precond_memory = precond_memory(pc);
+    rep->wall_build = precond_build_seconds(pc);
+  }
   HPSB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   HPSB_CUDA(cudaMemsetAsync(x, 0, sizeof(double2) * n, ctx->stream));
   const double bnorm = wk.norm(rhs);
@@ -673,6 +718,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
     float ms = 0;
     HPSB_CUDA(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
     rep->seconds = ms * 1e-3;
+    rep->wall_solve = rep->seconds;
   };
   if (bnorm == 0.0) {
     rep->converged = 1;
@@ -695,8 +741,11 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   // cfg1 / cfg2 (191 vs 193 us per iteration at cfg1: the device, not the
   // per-iteration host round trip, is the bound) and the first graph in a
   // process costs ~60 ms of one-time setup.
-  if (!ctx->profile && ctx->world() == 1 && (!pc || precond_graph_safe(pc)) &&
-      std::getenv("HPSB_CYCLE_GRAPH"))
+  // reorthogonalize (KrylovConfig, krylov.hpp:19): two classical passes
+  // (CGS2); off: the reference's single modified Gram-Schmidt pass.
+  const bool reorth = cfg.reorthogonalize != 0;
+  if (!ctx->profile && ctx->world() == 1 && (!pc || precond_graph_safe(pc)) && reorth && !right &&
+      restart + 1 <= kOrthChunk && std::getenv("HPSB_CYCLE_GRAPH"))
     cg.build(ctx, sk, pc, wk, V.p, Z.p, w.p, n, restart, cfg.max_iters, cfg.record_history != 0);
   while (total < cfg.max_iters && !converged) {
     double beta;
@@ -731,20 +780,33 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
     }
     for (; !cg.exec && j < restart && total < cfg.max_iters; ++j, ++total) {
       double2* Vj = V.p + static_cast<size_t>(j) * n;
-      if (pc) {
+      if (right) {
+        precond_apply(pc, Vj, pz.p);
+        skeleton_apply(sk, pz.p, w.p);
+      } else if (pc) {
         double2* Zj = Z.p + static_cast<size_t>(j) * n;
         precond_apply(pc, Vj, Zj);
         skeleton_apply(sk, Zj, w.p);
       } else {
         skeleton_apply(sk, Vj, w.p);
       }
-      // CGS2: two passes of h = V^H w, w -= V h
       double2* h1 = wk.hdev.p;
       double2* h2 = wk.hdev.p + (j + 1);
       double2* nn = wk.hdev.p + 2 * (j + 1);
-      wk.orth(V.p, j + 1, nullptr, 0, w.p, h1);  // h1 = V^H w
-      wk.orth(V.p, j + 1, h1, j + 1, w.p, h2);   // w -= V h1; h2 = V^H w
-      wk.orth(V.p, 0, h2, j + 1, w.p, nn);       // w -= V h2; nn = ||w||^2
+      if (reorth) {
+        // CGS2: two passes of h = V^H w, w -= V h
+        wk.orth(V.p, j + 1, nullptr, 0, w.p, h1);  // h1 = V^H w
+        wk.orth(V.p, j + 1, h1, j + 1, w.p, h2);   // w -= V h1; h2 = V^H w
+        wk.orth(V.p, 0, h2, j + 1, w.p, nn);       // w -= V h2; nn = ||w||^2
+      } else {
+        // single-pass modified Gram-Schmidt (krylov.cpp:98-102): h_i = V_i^H w,
+        // w -= h_i V_i for i = 0..j in order, each step one pass over w
+        HPSB_CUDA(cudaMemsetAsync(h2, 0, sizeof(double2) * (j + 1), ctx->stream));
+        wk.orth(V.p, 1, nullptr, 0, w.p, h1);
+        for (int i = 1; i <= j; ++i)
+          wk.orth(V.p + static_cast<size_t>(i - 1) * n, 1, h1 + i - 1, 1, w.p, h1 + i, nullptr, 0, 1);
+        wk.orth(V.p + static_cast<size_t>(j) * n, 0, h1 + j, 1, w.p, nn);
+      }
       HPSB_CUDA(cudaMemcpyAsync(hh.data(), wk.hdev.p, sizeof(double2) * (2 * (j + 1) + 1),
                                 cudaMemcpyDeviceToHost, ctx->stream));
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -778,12 +840,36 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
         for (int k = i + 1; k < j; ++k) s -= Hm(i, k) * y[k];
         y[i] = s / Hm(i, i);
       }
-      std::vector<double2> yd(j);
+      std::vector<double2> yd(j + 1);
       for (int i = 0; i < j; ++i) yd[i] = make_double2(y[i].real(), y[i].imag());
-      HPSB_CUDA(cudaMemcpyAsync(wk.hdev.p, yd.data(), sizeof(double2) * j, cudaMemcpyHostToDevice,
-                                ctx->stream));
-      wk.axpy(pc ? Z.p : V.p, j, wk.hdev.p, 1.0, x);
+      yd[j] = make_double2(1.0, 0.0);
+      HPSB_CUDA(cudaMemcpyAsync(wk.hdev.p, yd.data(), sizeof(double2) * (j + 1),
+                                cudaMemcpyHostToDevice, ctx->stream));
+      if (right) {  // x += P(V y)
+        zfill(ctx, pu.p, n, make_double2(0.0, 0.0));
+        wk.axpy(V.p, j, wk.hdev.p, 1.0, pu.p);
+        precond_apply(pc, pu.p, pz.p);
+        wk.axpy(pz.p, 1, wk.hdev.p + j, 1.0, x);
+      } else {
+        wk.axpy(pc ? Z.p : V.p, j, wk.hdev.p, 1.0, x);
+      }
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    if (cfg.record_history && j > 0) {
+      // basis orthogonality over the cycle's first j basis vectors
+      // (krylov.cpp:149-160): max | |<V_a, V_b>| - delta_ab |, b <= a
+      std::vector<double2> g(j);
+      for (int a = 0; a < j; ++a) {
+        double2* Va = V.p + static_cast<size_t>(a) * n;
+        wk.orth(V.p, a + 1, nullptr, 0, Va, wk.hdev.p);
+        HPSB_CUDA(cudaMemcpyAsync(g.data(), wk.hdev.p, sizeof(double2) * (a + 1),
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+        HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int b = 0; b <= a; ++b)
+          rep->basis_orthogonality =
+              std::max(rep->basis_orthogonality,
+                       std::abs(std::hypot(g[b].x, g[b].y) - (a == b ? 1.0 : 0.0)));
+      }
     }
     const double true_rel = true_residual();
     rep->final_residual = true_rel;
@@ -860,7 +946,6 @@ namespace {
 hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
                          const hpsb_krylov_config& cfg, hpsb_solve_report* reps) {
   if (cfg.restart < 1) throw InvalidArgument("gmres: restart must be >= 1");
-  if (cfg.restart > 100) throw InvalidArgument("gmres: restart must be <= 100 on the B200 path");
   if (!(cfg.tol > 0.0 && cfg.tol < 1.0)) throw InvalidArgument("gmres: tol must lie in (0, 1)");
   if (cfg.max_iters < 1) throw InvalidArgument("gmres: max_iters must be >= 1");
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("gmres: 1 <= nrhs <= 32");
@@ -869,6 +954,7 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   const int64_t n = sk->dim;
   const int restart = cfg.restart;
   const int hs = 2 * (restart + 2) + 1;  // per-RHS slots: h1 | h2 | nn (and y)
+  const bool reorth = cfg.reorthogonalize != 0;  // CGS2, else single-pass MGS
   for (int b = 0; b < R; ++b) reps[b] = hpsb_solve_report{};
   DevBuf<double2> V(static_cast<size_t>(restart + 1) * R * n);
   DevBuf<double2> Z(pc ? static_cast<size_t>(restart) * R * n : 0);
@@ -884,7 +970,8 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   const int64_t pstride = static_cast<int64_t>(nb) * (restart + 2);
   DevBuf<double2> partial(static_cast<size_t>(R) * pstride);
   // one CGS2 pass for all R: optional w -= V h_upd, then V^H w / ||w||^2
-  auto orth = [&](int ncols, const double2* h_upd, int nupd, double2* wv, double2* out) {
+  auto orth1 = [&](int ncols, const double2* h_upd, int nupd, double2* wv, double2* out,
+                   const double2* Vb, int vdot) {
     OrthStride st;
     st.v = n, st.w = n, st.p = pstride, st.h = hs;
     const int nout = ncols > 0 ? ncols : 1;
@@ -892,12 +979,19 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
                    8.0 * n * R * (ncols + nupd));
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
-               static_cast<const double2*>(V.p), static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
-               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr));
+               Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
+               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr), vdot);
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
-               static_cast<const double2*>(V.p), static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
-               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr));
+               Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
+               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr), vdot);
+  };
+  auto orth = [&](int ncols, const double2* h_upd, int nupd, double2* wv, double2* out,
+                  const double2* Vb, int vdot) {
+    orth_any([&](const double2* V0, int nc, const double2* hu, int nu, double2* o, int vd) {
+               orth1(nc, hu, nu, wv, o, V0, vd);
+             },
+             Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, out, vdot, hdev.p + hs - 1);
   };
   const int vblocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 2 * ctx->num_sms));
   auto scale = [&](const double2* src, int64_t ls, const std::vector<double>& f, double2* dst, int64_t ld) {
@@ -908,7 +1002,7 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   };
   std::vector<double2> hh(static_cast<size_t>(R) * hs);
   auto norms = [&](double2* vecs, std::vector<double>& out) {  // ||vecs[b]|| for all b
-    orth(0, nullptr, 0, vecs, hdev.p);
+    orth(0, nullptr, 0, vecs, hdev.p, V.p, 0);
     HPSB_CUDA(cudaMemcpyAsync(hh.data(), hdev.p, sizeof(double2) * R * hs, cudaMemcpyDeviceToHost,
                               ctx->stream));
     HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -974,9 +1068,17 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
         precond_apply_batch(pc, Vj, src, R);
       }
       skeleton_apply_batch(sk, src, w.p, R);
-      orth(j + 1, nullptr, 0, w.p, hdev.p);                      // h1 = V^H w
-      orth(j + 1, hdev.p, j + 1, w.p, hdev.p + (j + 1));         // w -= V h1; h2 = V^H w
-      orth(0, hdev.p + (j + 1), j + 1, w.p, hdev.p + 2 * (j + 1));  // w -= V h2; ||w||^2
+      if (reorth) {
+        orth(j + 1, nullptr, 0, w.p, hdev.p, V.p, 0);                       // h1 = V^H w
+        orth(j + 1, hdev.p, j + 1, w.p, hdev.p + (j + 1), V.p, 0);          // w -= V h1; h2 = V^H w
+        orth(0, hdev.p + (j + 1), j + 1, w.p, hdev.p + 2 * (j + 1), V.p, 0);  // w -= V h2; ||w||^2
+      } else {  // single-pass MGS, as the single-RHS driver
+        HPSB_CUDA(cudaMemsetAsync(hdev.p, 0, hdev.bytes(), ctx->stream));
+        orth(1, nullptr, 0, w.p, hdev.p, V.p, 0);
+        for (int i = 1; i <= j; ++i)
+          orth(1, hdev.p + i - 1, 1, w.p, hdev.p + i, V.p + static_cast<size_t>(i - 1) * R * n, 1);
+        orth(0, hdev.p + j, 1, w.p, hdev.p + 2 * (j + 1), V.p + static_cast<size_t>(j) * R * n, 0);
+      }
       HPSB_CUDA(cudaMemcpyAsync(hh.data(), hdev.p, sizeof(double2) * R * hs, cudaMemcpyDeviceToHost,
                                 ctx->stream));
       HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1023,9 +1125,11 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
       HPSB_CUDA(cudaMemcpyAsync(hdev.p, yd.data(), sizeof(double2) * R * hs, cudaMemcpyHostToDevice,
                                 ctx->stream));
       KernelScope ks(ctx, "gmres_axpy", 16.0 * n * R * (jmax + 2), 8.0 * n * R * jmax);
-      launch_k(ctx, axpy_batch_kernel, dim3(vblocks, R), dim3(kThreads), 0, 1,
-               static_cast<const double2*>(pc ? Z.p : V.p), static_cast<int64_t>(R) * n, jmax,
-               static_cast<const double2*>(hdev.p), hs, x, n);
+      for (int c0 = 0; c0 < jmax; c0 += kOrthChunk)
+        launch_k(ctx, axpy_batch_kernel, dim3(vblocks, R), dim3(kThreads), 0, 1,
+                 static_cast<const double2*>(pc ? Z.p : V.p) + static_cast<size_t>(c0) * R * n,
+                 static_cast<int64_t>(R) * n, std::min(kOrthChunk, jmax - c0),
+                 static_cast<const double2*>(hdev.p) + c0, hs, x, n);
     }
     true_residual(res);
     for (int b = 0; b < R; ++b) {

@@ -111,7 +111,8 @@ struct Precond {
   }
 };
 
-constexpr int kMaxCoarseIters = 30;
+constexpr int kMaxCoarseIters = 30;    // fused / on-chip coarse kernels
+constexpr int kCoarseItersMax = 512;   // MgConfig.coarse_iters (coarse_finish_kernel's y)
 constexpr int64_t kExactCoarseMax = 24576;  // dense coarse inverse: <= 9.7 GB
 constexpr size_t kSmallMergeSmemMax = 160 * 1024;
 constexpr size_t kClusterMergeSmemMax = 200 * 1024;
@@ -721,7 +722,7 @@ __global__ void __launch_bounds__(kCoarseThreads) coarse_finish_kernel(int64_t n
     V += static_cast<int64_t>(b) * (ci + 1) * n, Hm += static_cast<int64_t>(b) * (ci + 1) * ci;
     gv += b * (ci + 1), state += b * 4, outd += b * ldr;
   }
-  __shared__ double2 y[64];
+  __shared__ double2 y[kCoarseItersMax];
   const int ju = static_cast<int>(state[2]);
   const int ldh = ci + 1;
   if (threadIdx.x == 0) {
@@ -772,6 +773,57 @@ VItem item(const double2* A, int lda, int rows, int cols, const double2* x, cons
 }
 }  // namespace
 
+Context* precond_context(const Precond* p) { return p ? p->ctx : nullptr; }
+
+int64_t precond_memory(const Precond* p) {
+  int64_t b = 0;
+  for (int l = 1; l <= p->cfg.depth; ++l) {
+    const LevelOps& L = *p->h->levels[l - 1];
+    if (l > 1) b += static_cast<int64_t>(L.tperm.bytes());  // M_l as box maps
+    if (l < p->cfg.depth) b += static_cast<int64_t>(L.w.bytes());  // merge factors
+  }
+  return b + static_cast<int64_t>(p->cinv.bytes());
+}
+
+double precond_build_seconds(const Precond* p) { return p->h->build_seconds; }
+
+// y = M_l x on level l's system (HierarchyLevel::M.apply, block_matrix.cpp:23-31;
+// the level system over faces [first_face, total), dissection.hpp:35-41):
+// M_l = I + sum_{boxes b entering level l} scatter_out(T_b gather_in(x)).  Every
+// slot of the level is the outgoing row of exactly one box, so the items
+// write disjoint rows (y = x there, plus the box's contribution).
+void hierarchy_level_apply(Hierarchy* h, int level, const double2* x, double2* y) {
+  if (level < 1 || level > h->depth) throw InvalidArgument("level_apply: level out of range");
+  if (h->ctx->world() > 1) throw InvalidArgument("level_apply: single-GPU hierarchies only");
+  Context* ctx = h->ctx;
+  const LevelOps& Lv = *h->levels[level - 1];
+  const int off = Lv.first_face * h->sk->bs;
+  std::vector<int> gidx;
+  std::vector<size_t> in_at, out_at;
+  int rows = 0;
+  for (const ChildBox& c : Lv.children) {
+    in_at.push_back(gidx.size());
+    for (const auto& q : c.pos) gidx.push_back(q.in - off);
+    out_at.push_back(gidx.size());
+    for (const auto& q : c.pos) gidx.push_back(q.out - off);
+    rows += c.P;
+  }
+  VPlan mv;
+  mv.idx_store.upload(gidx, ctx->stream);
+  const int rb = split_rows(std::max(rows, 1), ctx->num_sms);
+  mv.begin_phase();
+  for (size_t k = 0; k < Lv.children.size(); ++k) {
+    const ChildBox& c = Lv.children[k];
+    const int* gi = mv.idx_store.p + in_at[k];
+    const int* go = mv.idx_store.p + out_at[k];
+    mv.add_split(item(Lv.tperm.p + c.t_off, c.P, c.P, c.P, x, gi, x, go, y, go, 1.0, 0.0, 1.0), rb);
+  }
+  mv.name = "level_matvec";
+  mv.finalize(ctx->stream);
+  mv.run(ctx);
+  HPSB_CUDA(cudaStreamSynchronize(ctx->stream));  // the plan's buffers die here
+}
+
 Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   // multigrid.cpp:9-28
   if (cfg.depth < 2) throw InvalidArgument("MgPreconditioner: depth must be >= 2");
@@ -783,11 +835,14 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   // (W- / gamma-cycles) runs host-recursively on one GPU.
   if (!cfg.exact_coarse && cfg.gamma > 1 && h->ctx->world() > 1)
     throw InvalidArgument("MgPreconditioner: gamma > 1 is single-GPU");
-  if (!cfg.exact_coarse && cfg.gamma > 16)
-    throw InvalidArgument("MgPreconditioner: gamma must be <= 16");
-  if (cfg.depth != h->depth)
-    throw InvalidArgument("MgPreconditioner: depth must equal the built hierarchy depth on the B200 path");
-  if (!cfg.exact_coarse && cfg.coarse_iters > 60) throw InvalidArgument("MgPreconditioner: coarse_iters must be <= 60");
+  // A preconditioner shallower than the hierarchy uses levels 1..depth of it
+  // (multigrid.cpp:13-16,24-26).  Sharded, the coarse level must be a global
+  // one: the local levels hold this rank's boxes only.
+  if (h->ctx->world() > 1 && cfg.depth <= h->sk->el->part.last_local)
+    throw InvalidArgument("MgPreconditioner: a sharded preconditioner's depth must exceed the last "
+                          "subtree level " + std::to_string(h->sk->el->part.last_local));
+  if (!cfg.exact_coarse && cfg.coarse_iters > kCoarseItersMax)
+    throw InvalidArgument("MgPreconditioner: coarse_iters must be <= " + std::to_string(kCoarseItersMax));
   Context* ctx = h->ctx;
   // HPSB_TRACE=1: host wall time per creation phase (stderr)
   const bool trace = std::getenv("HPSB_TRACE") != nullptr;

@@ -174,8 +174,10 @@ inline std::vector<FourierMode> fourier_modes(std::mt19937_64& rng, int count) {
 // BASELINE.json configs[0..4] with the seed (default: the config index).
 // `n_override` / `order_override` > 0 shrink the mesh for parity tests while
 // keeping the config's fields.
+// n / order / kappa overrides (> 0) shrink or reshape a config (the seeded
+// draws are unchanged); the BASELINE configs themselves use none.
 inline Spec baseline_config(int config, std::uint64_t seed, int n_override = 0,
-                            int order_override = 0) {
+                            int order_override = 0, double kappa_override = 0.0) {
   static const int kN[5] = {4, 16, 64, 128, 256};
   static const int kOrder[5] = {8, 16, 16, 20, 12};
   static const double kKappa[5] = {10.0, 40.0, 160.0, 400.0, 600.0};
@@ -189,7 +191,7 @@ inline Spec baseline_config(int config, std::uint64_t seed, int n_override = 0,
   s.seed = seed;
   s.n = n_override > 0 ? n_override : kN[config];
   s.order = order_override > 0 ? order_override : kOrder[config];
-  s.kappa = s.eta = kKappa[config];
+  s.kappa = s.eta = kappa_override > 0.0 ? kappa_override : kKappa[config];
   s.restart = kRestart[config];
   s.tol = kTol[config];
   std::mt19937_64 rng(seed);

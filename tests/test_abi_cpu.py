@@ -120,3 +120,35 @@ def test_boundary_trace_holds_every_physical_value(hps, config):
     # nothing but the physical sides is nonzero
     assert np.isclose(np.abs(tb).sum(), np.abs(p.tside).sum(), rtol=0, atol=0)
     assert np.count_nonzero(tb) == np.count_nonzero(p.tside) > 0
+
+
+def _build_c_client(hps, tmp_path):
+    """Compile tests/c/capi_client.c as strict C99 against include/hps_b200.h
+    and link it to the library, like the reference's C99 smoke client
+    (proj/tests/CMakeLists.txt:21-24, capi_smoke.c:12-44)."""
+    exe = os.path.join(str(tmp_path), "capi_client")
+    libdir = os.path.dirname(hps.LIB_PATH)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-Werror", "-pedantic",
+                    "-I", os.path.join(ROOT, "include"), os.path.join(ROOT, "tests", "c", "capi_client.c"),
+                    "-o", exe, "-L", libdir, "-l:libhps_b200.so", f"-Wl,-rpath,{libdir}", "-lm"],
+                   check=True, capture_output=True, text=True)
+    return exe
+
+
+def test_c_client_compiles_and_fails_loudly_without_gpu(hps, tmp_path):
+    exe = _build_c_client(hps, tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    import torch
+    if torch.cuda.is_available():
+        assert r.returncode == 0, r.stderr
+    else:
+        # no sm_100 device: the client's first device call returns a status
+        assert r.returncode == 77 and "no device" in r.stderr, (r.returncode, r.stderr)
+
+
+@pytest.mark.gpu
+def test_c_client_runs_on_gpu(hps, tmp_path):
+    exe = _build_c_client(hps, tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "c client ok" in r.stdout
