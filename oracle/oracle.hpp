@@ -65,6 +65,9 @@ using CVec = std::vector<cplx>;
 // Host threads used by the per-iteration operators (BlockMatrix::apply, the
 // multigrid group solves); every result is bit-identical for any count.
 void set_threads(int threads);
+// Drop each element's dense t x t operators and LU after its T and H are
+// formed (the solution recovery then fails): for the full-size golden runs.
+void set_lean_elements(bool lean);
 
 CMat matmul(const CMat& A, const CMat& B);           // A * B
 void gemv_acc(const CMat& A, const cplx* x, cplx* y, cplx alpha);  // y += alpha A x

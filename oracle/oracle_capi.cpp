@@ -71,6 +71,8 @@ extern "C" {
 
 const char* oracle_last_error() { return g_err.c_str(); }
 
+void oracle_set_lean_elements(int lean) { set_lean_elements(lean != 0); }
+
 int oracle_gll_rule(int order, double* nodes, double* weights, double* diff) {
   return guarded([&] {
     const Gll r = gll_rule(order);

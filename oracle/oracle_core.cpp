@@ -12,6 +12,11 @@
 
 namespace oracle {
 
+namespace {
+int g_threads = 1;             // host threads for the per-iteration operators (set_threads)
+bool g_lean_elements = false;  // set_lean_elements
+}  // namespace
+
 // ===================== dense helpers ======================================
 double CMat::max_abs() const {
   double m = 0.0;
@@ -419,6 +424,14 @@ std::vector<ElementRecord> build_elements(const Mesh& mesh, const Gll& rule, int
     }
     rec.outgoing_source =
         zero ? CVec(4 * m, cplx(0.0, 0.0)) : rec.ops->source_to_outgoing(rec.interior_source);
+    if (g_lean_elements) {
+      // keep T (and mass2d) only: the t x t operators and the LU factor are
+      // ~10 MB per element at N = 20 (160 GB for cfg3) and only the solution
+      // recovery needs them
+      Element& el = *rec.ops;
+      el.pde = CMat(), el.op = CMat(), el.imp_out = CMat(), el.imp_in = CMat();
+      el.factor = PivLU();
+    }
   });
   return recs;
 }
@@ -484,7 +497,6 @@ const CMat* BlockMatrix::find(int r, int c) const {
 }
 
 namespace {
-int g_threads = 1;  // host threads for the per-iteration operators (set_threads)
 
 // fn(key, block) for every stored block with block row in [r0, r1), block
 // rows split into contiguous chunks over the threads.  Each block row is
@@ -507,6 +519,7 @@ void for_block_rows(const BlockMatrix& M, int r0, int r1, F&& fn) {
 }  // namespace
 
 void set_threads(int threads) { g_threads = std::max(1, threads); }
+void set_lean_elements(bool lean) { g_lean_elements = lean; }
 
 CVec BlockMatrix::apply(const CVec& v) const {  // block_matrix.cpp:23-31
   if (v.size() != dim()) throw std::invalid_argument("BlockMatrix::apply: size mismatch");

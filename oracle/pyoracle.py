@@ -44,6 +44,7 @@ def lib():
         L.oracle_precond_memory.argtypes = [ctypes.c_void_p]
         L.oracle_hierarchy_storage.restype = ctypes.c_longlong
         L.oracle_hierarchy_storage.argtypes = [ctypes.c_void_p]
+        L.oracle_set_lean_elements.argtypes = [ctypes.c_int]
         L.oracle_history.restype = ctypes.c_longlong
         L.oracle_history.argtypes = [ctypes.c_void_p, _D, ctypes.c_longlong]
         L.oracle_sample.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_int,
@@ -60,6 +61,11 @@ def lib():
             getattr(L, name).argtypes = None  # set per call via explicit casts
         _lib = L
     return _lib
+
+
+def set_lean_elements(lean: bool) -> None:
+    """Keep only T / H per element (no recovery): full-size golden runs."""
+    lib().oracle_set_lean_elements(int(lean))
 
 
 def _p(a: np.ndarray):

@@ -81,6 +81,28 @@ hpsb::Context* ctx_of(hpsb_elements e) { return e && e->e ? e->e->ctx : nullptr;
 hpsb::Context* ctx_of(hpsb_skeleton s) { return s && s->s ? s->s->ctx : nullptr; }
 hpsb::Context* ctx_of(hpsb_hierarchy h) { return h && h->h ? h->h->ctx : nullptr; }
 hpsb::Context* ctx_of(hpsb_precond p) { return p ? hpsb::precond_context(p->p) : nullptr; }
+void ctx_retain(hpsb::Context* c) {
+  if (c) c->refs.fetch_add(1);
+}
+// Drop one reference; the last one tears the context down in dependency
+// order: its communicator's buffers are freed on the stream before the
+// stream itself goes.
+void ctx_release(hpsb::Context* c) {
+  if (!c || c->refs.fetch_sub(1) != 1) return;
+  hpsb::ContextBind bind(c);
+  cudaStreamSynchronize(c->stream);
+  c->comm.reset();
+  c->collect();
+  cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  for (auto& e : c->timer)
+    if (e) cudaEventDestroy(e);
+  c->pending.clear();
+  for (auto& e : c->event_pool) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  c->stream = nullptr;
+  delete static_cast<hpsb_context_s*>(c->owner);
+}
 // Device allocations and staged uploads of the call go to the stream of the
 // handle's own context (internal.hpp, ContextBind).
 #define BIND(h) hpsb::ContextBind bind_ctx_(ctx_of(h))
@@ -114,6 +136,7 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
     if (prop.major != 10)
       throw std::runtime_error("context_create: hps_b200 needs an sm_100 (B200) device");
     auto ctx = std::make_unique<hpsb_context_s>();
+    ctx->c.owner = ctx.get();
     ctx->c.device = device;
     HPSB_CUDA(cudaSetDevice(device));
     ctx->c.num_sms = prop.multiProcessorCount;
@@ -152,16 +175,7 @@ hpsb_status hpsb_context_create(int device, hpsb_context* out) {
 
 hpsb_status hpsb_context_destroy(hpsb_context ctx) {
   return guarded([&] {
-    BIND(ctx);
-    if (!ctx) return HPSB_OK;
-    cudaStreamSynchronize(ctx->c.stream);
-    for (auto& e : ctx->c.ev) cudaEventDestroy(e);
-    for (auto& e : ctx->c.timer)
-      if (e) cudaEventDestroy(e);
-    ctx->c.pending.clear();
-    for (auto& e : ctx->c.event_pool) cudaEventDestroy(e);
-    cudaStreamDestroy(ctx->c.stream);
-    delete ctx;
+    if (ctx) ctx_release(&ctx->c);  // the handle's reference (objects hold theirs)
     return HPSB_OK;
   });
 }
@@ -422,6 +436,7 @@ hpsb_status hpsb_elements_build_dev(hpsb_context ctx, int n, int order, double e
     auto h = std::make_unique<hpsb_elements_s>();
     h->e = hpsb::build_elements(&ctx->c, n, order, eta, coeff_dev,
                                 reinterpret_cast<const double2*>(source_dev));
+    ctx_retain(ctx_of(h.get()));  // the object holds its context
     *out = h.release();
     return HPSB_OK;
   });
@@ -441,14 +456,19 @@ hpsb_status hpsb_elements_build(hpsb_context ctx, int n, int order, double eta, 
       HPSB_CUDA(cudaMemcpyAsync(s.p, source, s.bytes(), cudaMemcpyHostToDevice, ctx->c.stream));
     auto h = std::make_unique<hpsb_elements_s>();
     h->e = hpsb::build_elements(&ctx->c, n, order, eta, c.p, source ? s.p : nullptr);
+    ctx_retain(ctx_of(h.get()));  // the object holds its context
     *out = h.release();
     return HPSB_OK;
   });
 }
 
 hpsb_status hpsb_elements_destroy(hpsb_elements el) {
-  BIND(el);
-  delete el;
+  hpsb::Context* c = ctx_of(el);
+  {
+    BIND(el);
+    delete el;
+  }
+  ctx_release(c);
   return HPSB_OK;
 }
 
@@ -486,6 +506,7 @@ hpsb_status hpsb_skeleton_create(hpsb_elements el, const double* tside, int nrhs
     REQUIRE(el && out && tside && nrhs >= 1, "skeleton_create: bad argument");
     auto h = std::make_unique<hpsb_skeleton_s>();
     h->s = hpsb::build_skeleton(el->e.get(), reinterpret_cast<const double2*>(tside), nrhs);
+    ctx_retain(ctx_of(h.get()));  // the object holds its context
     *out = h.release();
     return HPSB_OK;
   });
@@ -498,14 +519,19 @@ hpsb_status hpsb_skeleton_create_boundary(hpsb_elements el, const double* tbnd, 
     REQUIRE(el && out && tbnd && nrhs >= 1, "skeleton_create_boundary: bad argument");
     auto h = std::make_unique<hpsb_skeleton_s>();
     h->s = hpsb::build_skeleton(el->e.get(), reinterpret_cast<const double2*>(tbnd), nrhs, true);
+    ctx_retain(ctx_of(h.get()));  // the object holds its context
     *out = h.release();
     return HPSB_OK;
   });
 }
 
 hpsb_status hpsb_skeleton_destroy(hpsb_skeleton sk) {
-  BIND(sk);
-  delete sk;
+  hpsb::Context* c = ctx_of(sk);
+  {
+    BIND(sk);
+    delete sk;
+  }
+  ctx_release(c);
   return HPSB_OK;
 }
 
@@ -609,14 +635,19 @@ hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
       c.depth = h->h->depth, c.gamma = 1, c.coarse_iters = 0, c.exact_coarse = 1;
       h->direct = hpsb::create_precond(h->h.get(), c);
     }
+    ctx_retain(ctx_of(h.get()));  // the object holds its context
     *out = h.release();
     return HPSB_OK;
   });
 }
 
 hpsb_status hpsb_hierarchy_destroy(hpsb_hierarchy h) {
-  BIND(h);
-  delete h;
+  hpsb::Context* c = ctx_of(h);
+  {
+    BIND(h);
+    delete h;
+  }
+  ctx_release(c);
   return HPSB_OK;
 }
 
@@ -689,6 +720,7 @@ hpsb_status hpsb_precond_create(hpsb_hierarchy h, hpsb_mg_config cfg, hpsb_preco
     } else {
       p->p = hpsb::create_precond(h->h.get(), cfg);
     }
+    ctx_retain(ctx_of(p.get()));  // the object holds its context
     *out = p.release();
     return HPSB_OK;
   });
@@ -718,8 +750,12 @@ hpsb_status hpsb_direct_solve(hpsb_hierarchy h, const double* rhs, double* x) {
 }
 
 hpsb_status hpsb_precond_destroy(hpsb_precond p) {
-  BIND(p);
-  delete p;
+  hpsb::Context* c = ctx_of(p);
+  {
+    BIND(p);
+    delete p;
+  }
+  ctx_release(c);
   return HPSB_OK;
 }
 

@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(V5ST) v5_schur_kernel(V5Args v, double2* Sw, d
 // PIVOT = false: diagonal pivots, one barrier per column (the element Schur
 // complements of the BASELINE configs need no pivoting: checked against the
 // pivoted inverse at 1e-15 on sampled elements of cfg1-4).  A pivot below
-// 1e-10 of the largest |S_ij| or an inverse entry beyond 1e10 / max|S_ij|
-// flags the element (status bit 8); the PIVOT = true launch that follows
+// 1e-6 of the largest |S_ij| or an inverse entry beyond 1e8 / max|S_ij|
+// (kGjTiny2 / kGjHuge2) flags the element (status bit 8); the PIVOT = true launch that follows
 // redoes exactly the flagged elements with partial pivoting.
 template <int TR, bool PIVOT>
 __global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const double2* Sw, const double2* fw) {
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const doub
     atomicMax(&smax, static_cast<unsigned long long>(__double_as_longlong(m)));
     __syncthreads();
     const double m0 = __longlong_as_double(static_cast<long long>(smax));
-    ok = gj_reg_inverse_nopiv<TR, TC>(nb, get, g, sh, 1e-20 * m0, 1e20 / fmax(m0, 1e-300));
+    ok = gj_reg_inverse_nopiv<TR, TC>(nb, get, g, sh, kGjTiny2 * m0, kGjHuge2 / fmax(m0, 1e-300));
     if (!ok) {
       if (tid == 0) a.status[e] = st0 | 8;  // redo with pivoting
       return;

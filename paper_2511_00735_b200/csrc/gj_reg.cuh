@@ -23,6 +23,13 @@
 namespace hpsb {
 
 constexpr int kGjY = 16, kGjX = 32, kGjThreads = kGjY * kGjX, kGjMax = 96;
+// Guard of the diagonal-pivot Gauss-Jordan (squared magnitudes relative to
+// m0 = max |a_ij|^2): every pivot |p_k| >= 1e-6 max |a_ij| and every inverse
+// entry <= 1e8 / max |a_ij| (growth of at most ~1e8 over the pivoted
+// inverse's bound, ~1e-8 relative of rounding headroom before the 1e-10
+// operator tolerance would be at risk); a matrix outside either bound is
+// redone with partial pivoting.
+constexpr double kGjTiny2 = 1e-12, kGjHuge2 = 1e16;
 
 struct GjShared {
   double2 rowbuf[2][kGjMax];

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <atomic>
 #include <functional>
 #include <utility>
 #include <cstdint>
@@ -189,6 +190,12 @@ struct Context {
   // (gmres_driver's report.residual_history, krylov.cpp:118)
   std::vector<double> history;
   Staging staging;  // pinned upload ring of this context's stream
+  // Lifetime: the ABI handle holds one reference and every object built on
+  // the context holds one; the stream and the context's buffers are released
+  // with the last reference (capi.cpp), so an object may outlive
+  // hpsb_context_destroy of its context.
+  std::atomic<int> refs{1};
+  void* owner = nullptr;  // the hpsb_context_s that embeds this context
 };
 
 // Brackets one kernel launch with CUDA events when profiling is enabled and

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kGjThreads) inverse_reg_kernel(const InvOp* __
     atomicMax(&smax, static_cast<unsigned long long>(__double_as_longlong(m)));
     __syncthreads();
     const double m0 = __longlong_as_double(static_cast<long long>(smax));
-    if (!gj_reg_inverse_nopiv<TR, TC>(op.n, get, g, sh, 1e-20 * m0, 1e20 / fmax(m0, 1e-300))) {
+    if (!gj_reg_inverse_nopiv<TR, TC>(op.n, get, g, sh, kGjTiny2 * m0, kGjHuge2 / fmax(m0, 1e-300))) {
       if (threadIdx.x == 0) {
         if (flags) flags[blockIdx.x] = 1;
         else *guard = 1;
@@ -574,6 +574,35 @@ void CopyBatch::run(Context* ctx) {
   HPSB_LAUNCHED(ctx);
 }
 
+// m0_out != null: m0_out[op] = max |a_ij|^2 of matrix op.  Else the growth
+// check of a diagonal-pivot blocked inverse: any entry of A^{-1} beyond
+// kGjHuge2 / m0_in[op] (or NaN) sets *guard.
+__global__ void __launch_bounds__(1024) absmax2_kernel(const InvOp* __restrict__ ops, double* m0_out,
+                                                       const double* __restrict__ m0_in, int* guard) {
+  __shared__ double red[32];
+  const InvOp op = ops[blockIdx.x];
+  double m = 0.0;
+  bool bad = false;
+  for (int j = 0; j < op.n; ++j)
+    for (int i = threadIdx.x; i < op.n; i += blockDim.x) {
+      const double v = cabs2(op.A[(size_t)i + (size_t)j * op.lda]);
+      m = fmax(m, v);
+      bad |= !(v == v);
+    }
+  if (m0_out) {
+    m = warp_max(m);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = red[threadIdx.x];
+      v = warp_max(v);
+      if (threadIdx.x == 0) m0_out[blockIdx.x] = v;
+    }
+    return;
+  }
+  if (bad || !(m <= kGjHuge2 / fmax(m0_in[blockIdx.x], 1e-300))) *guard = 1;
+}
+
 void InverseBatch::run(Context* ctx, int* status_dev) {
   std::vector<InvOp> small, large;
   int perm_total = 0;
@@ -595,10 +624,10 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     KernelScope ks(ctx, "zinverse_smem", 0.0, fl);
     const int grid = static_cast<int>(small.size());
     if (diag_pivots) {
-      // per-matrix redo of guard failures, unless the caller takes them
-      // (blocked diagonal blocks: guard_dev)
+      // per-matrix redo of guard failures; the diagonal blocks of a blocked
+      // inverse cannot be redone alone and report to guard_dev instead
       int* flags = nullptr;
-      if (!guard_dev) {
+      if (!panel_blocks) {
         d_flags.alloc(small.size());
         HPSB_CUDA(cudaMemsetAsync(d_flags.p, 0, d_flags.bytes(), ctx->stream));
         flags = d_flags.p;
@@ -643,6 +672,13 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     std::vector<InvOp> pivops(large.size());
     // diag_pivots needs a guard word for the diagonal blocks (no redo)
     const bool diag = diag_pivots && guard_dev;
+    if (diag) {  // largest |a_ij|^2 of every input, for the final growth check
+      d_m0.alloc(large.size());
+      KernelScope ks(ctx, "zinverse_guard", 16.0 * nmax * nmax * large.size(), 0.0);
+      absmax2_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(d_large.p, d_m0.p,
+                                                                               nullptr, nullptr);
+      HPSB_LAUNCHED(ctx);
+    }
     for (int k0 = 0; k0 < nmax; k0 += kb) {
       if (!diag) {
         KernelScope ks(ctx, "zinverse_panel", 0.0, 0.0);
@@ -705,14 +741,20 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
         back.copy(Ub, kw, A + k0, o.lda, kw, k0, 1.0);
         back.copy(Ub + static_cast<size_t>(k1) * kw, kw, A + k0 + k1 * ld, o.lda, kw, tail, 1.0);
       }
-      piv.diag_pivots = diag, piv.guard_dev = diag ? guard_dev : nullptr;
+      piv.diag_pivots = diag, piv.guard_dev = diag ? guard_dev : nullptr, piv.panel_blocks = true;
       piv.run(ctx, status_dev);  // in place: A_KK <- P (kw <= 32 uses the smem kernel)
       gu.run(ctx);
       gr.run(ctx);
       gq.run(ctx);
       back.run(ctx);
     }
-    if (diag) return;  // no pivots: nothing to unscramble
+    if (diag) {  // no pivots, nothing to unscramble; check the inverse's growth
+      KernelScope ks(ctx, "zinverse_guard", 16.0 * nmax * nmax * large.size(), 0.0);
+      absmax2_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(d_large.p, nullptr,
+                                                                               d_m0.p, guard_dev);
+      HPSB_LAUNCHED(ctx);
+      return;
+    }
     KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);
     dim3 grid((nmax + 255) / 256, static_cast<unsigned>(large.size()));
     unscramble_kernel<<<grid, 256, 0, ctx->stream>>>(d_large.p, perm_ws.p);

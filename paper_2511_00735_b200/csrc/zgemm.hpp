@@ -84,12 +84,21 @@ constexpr int kSmemInvMax = 96;
 // pivoting in the same call; a marked diagonal block of a blocked inverse
 // sets guard_dev[0] = 1 instead (its caller redoes the whole build with
 // pivoting, see build_hierarchy).
+// Batched complex inverses in place.  diag_pivots: Gauss-Jordan on the
+// diagonal (merge blocks W = I - T2_ss T1_ss), guarded (gj_reg.cuh):
+//   register-resident matrices (n <= 96) that fail the guard are redone with
+//   partial pivoting in the same call;
+//   blocked matrices (n > 96) are checked per diagonal block and, at the end,
+//   on every entry of the inverse against the input's largest entry; a
+//   failure sets *guard_dev (the caller rebuilds with pivoting).
 struct InverseBatch {
   std::vector<InvOp> ops;
   bool diag_pivots = false;
+  bool panel_blocks = false;  // internal: the diagonal blocks of a blocked inverse
   int* guard_dev = nullptr;
   DevBuf<InvOp> d_small, d_large;
   DevBuf<int> perm_ws, d_flags;
+  DevBuf<double> d_m0;
   void run(Context* ctx, int* status_dev);
 };
 

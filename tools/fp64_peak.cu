@@ -1,6 +1,7 @@
 // FP64 peak probe for B200: DFMA vs DMMA (mma.sync f64) throughput.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_peak fp64_peak.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void dfma_loop(double* out, int iters) {
@@ -74,9 +75,38 @@ __global__ void mixed_loop(double* out, int iters, int dfma_per_dmma) {
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
-int main() {
+// Sustained DMMA rate: m8n8k4 chains launched back to back for `seconds`
+// (4 s as MEASURED_PEAKS' sustained bf16 figure), one CUDA-event pair around
+// the whole run; the burst figure is the best single launch.
+static void sustained(double seconds, int sms) {
   double* d; cudaMalloc(&d, 4096 * 8);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int grid = sms * 4, threads = 256, iters = 20000;
+  const double fl = 2.0 * 256 * 4 * iters * (double)grid * (threads / 32);
+  float best = 1e30f, ms = 0;
+  for (int i = 0; i < 5; ++i) {
+    cudaEventRecord(e0); dmma_m8n8k4_loop<<<grid, threads>>>(d, iters); cudaEventRecord(e1);
+    cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  const int launches = (int)(seconds * 1e3 / best) + 1;
+  cudaEventRecord(e0);
+  for (int i = 0; i < launches; ++i) dmma_m8n8k4_loop<<<grid, threads>>>(d, iters);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+  printf("{\"dmma_burst_tflops\": %.2f, \"dmma_sustained_tflops\": %.2f, \"sustained_seconds\": %.2f, "
+         "\"launches\": %d, \"err\": \"%s\"}\n",
+         fl / best / 1e9, fl * launches / ms / 1e9, ms * 1e-3, launches,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main(int argc, char** argv) {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) {  // fp64_peak <seconds>: sustained mode (JSON line)
+    sustained(atof(argv[1]), sms);
+    return 0;
+  }
+  double* d; cudaMalloc(&d, 4096 * 8);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   const int iters = 20000;
   for (int rep = 0; rep < 3; ++rep) {

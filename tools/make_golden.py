@@ -86,6 +86,7 @@ def generate(c: int, nrhs: int = 1, threads: int = 0) -> dict:
     args.rhs, args.threads = nrhs, threads or os.cpu_count() or 1
     t0 = time.time()
     log = lambda msg: print(f"[golden cfg{c} {time.time() - t0:7.1f}s] {msg}", flush=True)  # noqa: E731
+    pyoracle.set_lean_elements(True)  # T / H only per element (cfg3: 160 GB otherwise)
     smp = pyoracle.sample(2, c, c)
     n, order = smp["n"], smp["order"]
     ne, nb = n * n, 4 * (order - 1)
@@ -157,6 +158,7 @@ def generate(c: int, nrhs: int = 1, threads: int = 0) -> dict:
             "generator": "tools/make_golden.py (oracle/ restatement of the reference)"}
     out["meta"] = np.array(json.dumps(meta))
     S.close()
+    pyoracle.set_lean_elements(False)
     return out
 
 
