@@ -436,8 +436,27 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
   HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
   tr.mark("final_wait");
   elements_wait(sk->el);  // long finished: the merges consumed the element maps
-  const int st = st_pinned[0];
-  *guard_tripped = st_pinned[1] != 0 || (!pivot && std::getenv("HPSB_TEST_GUARD_TRIP"));
+  int st = st_pinned[0];
+  bool trip = st_pinned[1] != 0 || (!pivot && std::getenv("HPSB_TEST_GUARD_TRIP"));
+  if (sharded) {
+    // test hook: trip the guard on one rank only
+    if (const char* r = std::getenv("HPSB_TEST_GUARD_TRIP_RANK"))
+      trip |= !pivot && std::atoi(r) == ctx->rank();
+    // The guard and the singular-block status are per rank (each rank merged
+    // its own subtree): agree on them, so that every rank redoes the build
+    // (and its collectives) together, or every rank throws.
+    DevBuf<double2> flag(1);
+    const double2 mine = make_double2(trip ? 1.0 : 0.0, st ? 1.0 : 0.0);
+    HPSB_CUDA(cudaMemcpyAsync(flag.p, &mine, sizeof(mine), cudaMemcpyHostToDevice, ctx->stream));
+    ctx->comm->allreduce_sum(flag.p, 1, ctx);
+    double2 all;
+    HPSB_CUDA(cudaMemcpyAsync(&all, flag.p, sizeof(all), cudaMemcpyDeviceToHost, ctx->stream));
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    trip = all.x > 0.0;
+    if (!st && all.y > 0.0)
+      throw std::runtime_error("eliminate_level: singular merge block on another rank");
+  }
+  *guard_tripped = trip;
   if (*guard_tripped) return h;  // results unused: the caller redoes the build
   if (st) {  // first singular group pivot (inverse status tag = level << 20 | group) + 1
     const int tag = st - 1, level = tag >> 20, gi = tag & ((1 << 20) - 1);

@@ -120,14 +120,19 @@ def test_solve_report_fields(hps, oracle, ctx):
 
 @pytest.mark.parametrize("reorth", [True, False])
 def test_restart_above_100(hps, oracle, ctx, reorth):
-    """restart 150 > the 96 columns one orthogonalisation launch holds."""
-    p, S, el, sk, h = setup(hps, oracle, ctx, "cfg0")
-    x, rep = hps.gmres(sk, sk.rhs(), restart=150, tol=1e-10, max_iters=400,
+    """restart 150 > the 96 columns one orthogonalisation launch holds:
+    150 unpreconditioned Arnoldi steps in one cycle on cfg1 (not converged
+    yet), the same iterate as the oracle's."""
+    p, S, el, sk, h = setup(hps, oracle, ctx, "cfg1")
+    x, rep = hps.gmres(sk, sk.rhs(), restart=150, tol=1e-12, max_iters=150,
                        reorthogonalize=reorth, record_history=True)
-    xo, repo = S.solve(S.rhs(), False, restart=150, tol=1e-10, max_iters=400, reorth=reorth)
-    assert rep["converged"] and repo["converged"]
-    assert repo["iterations"] > 100
-    assert abs(rep["iterations"] - repo["iterations"]) <= 1, (rep, repo)
+    xo, repo = S.solve(S.rhs(), False, restart=150, tol=1e-12, max_iters=150, reorth=reorth,
+                       record_history=True)
+    assert rep["iterations"] == repo["iterations"] == 150
+    assert not rep["converged"] and not repo["converged"]
+    assert abs(rep["final_residual"] / repo["final_residual"] - 1) < 1e-6
+    h, ho = np.asarray(rep["residual_history"]), np.asarray(repo["residual_history"])
+    assert np.allclose(h, ho, rtol=1e-6, atol=0)
     assert relf(x, xo) < 1e-8
 
 

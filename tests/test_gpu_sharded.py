@@ -102,3 +102,22 @@ def test_sharded_matches_single_gpu(config, world):
     # every rank holds the same replicated solution
     for s in shards[1:]:
         assert relf(s["x"], shards[0]["x"]) < 1e-12
+
+
+def test_guard_trip_on_one_rank_rebuilds_on_all(monkeypatch):
+    """The diagonal-pivot guard trips on rank 1 only: the ranks agree on it
+    (allreduce) and all rebuild with partial pivoting together -- no
+    mismatched collectives, same results as the single GPU."""
+    import paper_2511_00735_b200 as hps
+    prob = hps.problem(2, 1)
+    rng = np.random.default_rng(4)
+    dim = 2 * (2 * prob.n * (prob.n - 1)) * (prob.order - 1)
+    x = rng.standard_normal(dim) + 1j * rng.standard_normal(dim)
+    v = rng.standard_normal(dim) + 1j * rng.standard_normal(dim)
+    ref = _single(hps, prob, x, v)
+    monkeypatch.setenv("HPSB_TEST_GUARD_TRIP_RANK", "1")
+    shards = _sharded(hps, prob, 4, x, v)
+    for s in shards:
+        assert relf(s["Pv"], ref["Pv"]) < 1e-10
+        assert abs(s["rep"]["iterations"] - ref["rep"]["iterations"]) <= 1
+        assert relf(s["x"], ref["x"]) < 1e-9
