@@ -17,8 +17,10 @@ BASELINE targets (setup vs FP64 peak, GMRES vs HBM) are defined; cfg4 (32
 right-hand sides) is the second documented line (--config 4).
 
 Multi-GPU (torchrun): the config is sharded by quadtree subtree over the
-ranks (NCCL: subtree-box broadcast at setup, allreduce in the matvec and the
-V-cycle), value = the problem's DOF-iterations / max-over-ranks time,
+ranks (NCCL: owner-computes top merges with send / recv of box maps at
+setup; distributed Krylov vectors with allreduced inner products and
+global-row exchanges in the matvec and the V-cycle; cfg4's 32 right-hand
+sides too), value = the problem's DOF-iterations / max-over-ranks time,
 scaling "strong"; --replicas runs independent copies instead ("weak").
 """
 from __future__ import annotations
@@ -294,7 +296,7 @@ def run_b200(args, rank, world, local):
                   f"hierarchy {1e3 * (w3 - w2):.1f} (device {1e3 * hier.build_seconds:.1f}) "
                   f"precond {1e3 * (w4 - w3):.1f}", file=sys.stderr)
         cfg = hps.KrylovConfig(restart, tol, 2000, 0, 1)
-        nrhs = sk.nrhs if world == 1 else 1
+        nrhs = sk.nrhs
         x = torch.empty(2 * sk.dim * nrhs, dtype=torch.float64, device=f"cuda:{local}")
         if nrhs > 1:
             # cfg4: all right-hand sides in lockstep, one multi-RHS operator

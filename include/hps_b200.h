@@ -284,10 +284,13 @@ double hpsb_precond_pinned_bytes(hpsb_precond p);
  * Quadtree-subtree sharding over G = 2^g ranks, one per GPU.
  * Attach a communicator to a context BEFORE building objects on it; every
  * object built on that context is then sharded: each rank builds the
- * elements and merge levels 1..L-g of its own subtree, the subtree boxes
- * are broadcast, the top g levels run on every rank, and the matvec /
- * preconditioner combine their partial results with an allreduce.  Vectors
- * at the ABI stay full length (replicated) on every rank.                   */
+ * elements and merge levels 1..L-g of its own subtree; each merge of the
+ * top levels runs on one rank (owner-computes, the other child's box map
+ * arrives by NCCL send / recv) and the coarse level is replicated.  The
+ * solvers keep distributed vectors (a rank's subtree rows plus the few
+ * global rows), exchange only the global rows between levels and in the
+ * matvec, and sum the Krylov inner products with an NCCL allreduce.
+ * Vectors at the ABI stay full length (replicated) on every rank.           */
 typedef struct hpsb_local_group_s* hpsb_local_group;
 /* NCCL (one process per GPU): rank 0 makes the id, all ranks attach. */
 hpsb_status hpsb_nccl_unique_id(unsigned char id[128]);
@@ -303,6 +306,11 @@ hpsb_status hpsb_context_comm_info(hpsb_context ctx, int* rank, int* world);
  * face with -1 on the shared top-level faces) and the last local level.    */
 hpsb_status hpsb_partition(int n, int world, int rank, int* elem_owner, int* face_owner,
                            int* last_local_level);
+/* Host-only: owners[g] = the rank that runs merge (group) g of `level`
+ * (owner-computes: the rank holding the merge's first child box; the
+ * elements' owners at level 1).  Levels above the subtrees spread their
+ * merges over the ranks; the coarse (last built) level is replicated.     */
+hpsb_status hpsb_merge_owners(int n, int world, int level, int* owners);
 
 #ifdef __cplusplus
 }

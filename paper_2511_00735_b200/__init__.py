@@ -142,6 +142,7 @@ _sig("hpsb_local_group_create", _st, ctypes.c_int, ctypes.POINTER(_VP))
 _sig("hpsb_local_group_destroy", _st, _VP)
 _sig("hpsb_context_attach_local", _st, _VP, _VP, ctypes.c_int)
 _sig("hpsb_context_comm_info", _st, _VP, _I, _I)
+_sig("hpsb_merge_owners", _st, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I)
 _sig("hpsb_partition", _st, ctypes.c_int, ctypes.c_int, ctypes.c_int, _I, _I, _I)
 _sig("hpsb_hierarchy_pinned_flops", _st, _VP, _D, _D)
 _sig("hpsb_precond_pinned_bytes", ctypes.c_double, _VP)
@@ -323,6 +324,15 @@ def partition(n: int, world: int, rank: int) -> dict:
     _check(_lib.hpsb_partition(n, world, rank, eo.ctypes.data_as(_I), fo.ctypes.data_as(_I),
                                ctypes.byref(ll)))
     return {"elem_owner": eo, "face_owner": fo, "last_local": ll.value}
+
+
+def merge_owners(n: int, world: int, level: int) -> np.ndarray:
+    """Rank that runs each merge (group) of `level` under `world` ranks."""
+    faces = face_graph(n)["faces"]
+    ng = int(np.max(faces[faces[:, 4] == level][:, 5])) + 1
+    out = np.zeros(ng, dtype=np.int32)
+    _check(_lib.hpsb_merge_owners(n, world, level, out.ctypes.data_as(_I)))
+    return out
 
 
 class _Handle:

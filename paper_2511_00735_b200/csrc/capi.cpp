@@ -359,6 +359,17 @@ hpsb_status hpsb_partition(int n, int world, int rank, int* elem_owner, int* fac
   });
 }
 
+hpsb_status hpsb_merge_owners(int n, int world, int level, int* owners) {
+  return guarded([&] {
+    const hpsb::FaceGraph g = hpsb::build_face_graph(n);
+    REQUIRE(level >= 1 && level <= g.num_levels(), "merge_owners: level out of range");
+    const auto all = hpsb::merge_owners(g, hpsb::make_partition(g, world, 0));
+    const auto& o = all[level - 1];
+    if (owners) std::memcpy(owners, o.data(), o.size() * sizeof(int));
+    return HPSB_OK;
+  });
+}
+
 hpsb_status hpsb_gll_rule(int order, double* nodes, double* weights, double* diff) {
   return guarded([&] {
     const hpsb::Gll g = hpsb::gll_rule(order);

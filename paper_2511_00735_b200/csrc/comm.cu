@@ -6,6 +6,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
+#include <algorithm>
 
 #include "device.cuh"
 #include "internal.hpp"
@@ -32,6 +33,19 @@ struct NcclComm : Comm {
     KernelScope ks(ctx, "nccl_broadcast", static_cast<double>(bytes), 0.0);
     nccl_check(ncclBroadcast(buf, buf, bytes, ncclUint8, root, comm, ctx->stream), "ncclBroadcast");
   }
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                Context* ctx) override {
+    if (sends.empty() && recvs.empty()) return;
+    double bytes = 0;
+    for (const auto& x : sends) bytes += static_cast<double>(x.bytes);
+    KernelScope ks(ctx, "nccl_sendrecv", bytes, 0.0);
+    nccl_check(ncclGroupStart(), "ncclGroupStart");
+    for (const auto& x : sends)
+      nccl_check(ncclSend(x.buf, x.bytes, ncclUint8, x.peer, comm, ctx->stream), "ncclSend");
+    for (const auto& x : recvs)
+      nccl_check(ncclRecv(x.buf, x.bytes, ncclUint8, x.peer, comm, ctx->stream), "ncclRecv");
+    nccl_check(ncclGroupEnd(), "ncclGroupEnd");
+  }
 };
 
 // out[i] = sum_q in[q][i] in fixed rank order (identical on every rank)
@@ -43,7 +57,47 @@ __global__ void sum_ranks_kernel(double2* const* in, int nr, double2* out, size_
     out[i] = s;
   }
 }
+__global__ void delta_pack_kernel(double2* pack, const double2* __restrict__ a, int64_t lda,
+                                  const double2* __restrict__ base, int64_t ldb, int64_t n) {
+  const int c = blockIdx.y;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    pack[c * n + k] = base ? csub(a[c * lda + k], base[c * ldb + k]) : a[c * lda + k];
+}
+__global__ void delta_unpack_kernel(double2* a, int64_t lda, const double2* __restrict__ base,
+                                    int64_t ldb, const double2* __restrict__ pack, int64_t n) {
+  const int c = blockIdx.y;
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    a[c * lda + k] = base ? cadd(base[c * ldb + k], pack[c * n + k]) : pack[c * n + k];
+}
 }  // namespace
+
+void exchange_deltas(Context* ctx, DevBuf<double2>& buf, const std::vector<DeltaSeg>& segs) {
+  int64_t tot = 0;
+  for (const DeltaSeg& sg : segs) tot += sg.n * sg.cols;
+  if (!tot) return;
+  if (buf.n < static_cast<size_t>(tot)) buf.alloc(tot);
+  int64_t at = 0;
+  for (const DeltaSeg& sg : segs) {
+    if (!sg.n) continue;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((sg.n + 255) / 256, 2 * ctx->num_sms)),
+                    static_cast<unsigned>(sg.cols));
+    delta_pack_kernel<<<grid, 256, 0, ctx->stream>>>(buf.p + at, sg.a, sg.lda, sg.base, sg.ldb, sg.n);
+    HPSB_LAUNCHED(ctx);
+    at += sg.n * sg.cols;
+  }
+  ctx->comm->allreduce_sum(buf.p, tot, ctx);
+  at = 0;
+  for (const DeltaSeg& sg : segs) {
+    if (!sg.n) continue;
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>((sg.n + 255) / 256, 2 * ctx->num_sms)),
+                    static_cast<unsigned>(sg.cols));
+    delta_unpack_kernel<<<grid, 256, 0, ctx->stream>>>(sg.a, sg.lda, sg.base, sg.ldb, buf.p + at, sg.n);
+    HPSB_LAUNCHED(ctx);
+    at += sg.n * sg.cols;
+  }
+}
 
 struct LocalGroup {
   int size = 1;
@@ -51,6 +105,7 @@ struct LocalGroup {
   std::condition_variable cv;
   int arrived = 0, generation = 0;
   std::vector<void*> slots;
+  std::vector<std::vector<Comm::Xfer>> sends;  // exchange(): published per rank
   bool broken = false;
   // A rank that fails (throws) before a collective would leave the others
   // waiting: the wait is bounded and a timed-out group stays broken so every
@@ -103,6 +158,31 @@ struct ThreadComm : Comm {
     HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
     grp->barrier();
   }
+  // Every rank publishes its sends; each receiver copies the matching send
+  // of its peer (device to device: the emulated ranks share one GPU).  The
+  // k-th receive from peer p pairs with the k-th send from p to this rank.
+  void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                Context* ctx) override {
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    {
+      std::lock_guard<std::mutex> lk(grp->mu);
+      grp->sends[rank] = sends;
+    }
+    grp->barrier();
+    std::vector<int> taken(size, 0);
+    for (const auto& r : recvs) {
+      const auto& ps = grp->sends[r.peer];
+      int k = 0, seen = 0;
+      for (; k < static_cast<int>(ps.size()); ++k)
+        if (ps[k].peer == rank && seen++ == taken[r.peer]) break;
+      if (k == static_cast<int>(ps.size()) || ps[k].bytes != r.bytes)
+        throw std::logic_error("local group: unmatched receive");
+      ++taken[r.peer];
+      HPSB_CUDA(cudaMemcpyAsync(r.buf, ps[k].buf, r.bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
+    grp->barrier();  // every receiver has copied: the senders may reuse their buffers
+  }
 };
 }  // namespace
 
@@ -128,6 +208,7 @@ std::shared_ptr<LocalGroup> make_local_group(int size) {
   auto g = std::make_shared<LocalGroup>();
   g->size = size;
   g->slots.assign(size, nullptr);
+  g->sends.assign(size, {});
   return g;
 }
 

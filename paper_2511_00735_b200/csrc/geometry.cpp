@@ -189,4 +189,30 @@ Partition make_partition(const FaceGraph& g, int G, int rank) {
   return p;
 }
 
+// Owner-computes rule of the sharded merges: a level's group (merge) runs on
+// the rank holding its first child -- the box with the faces' e1 -- and the
+// box it produces stays there.  Level 1's children are elements (their
+// owners); the boxes entering a level are the previous level's groups.
+std::vector<std::vector<int>> merge_owners(const FaceGraph& g, const Partition& part) {
+  const int ne = g.n * g.n;
+  std::vector<int> box(ne), box_owner(ne);
+  for (int e = 0; e < ne; ++e) box[e] = e, box_owner[e] = part.elem_owner[e];
+  std::vector<std::vector<int>> owners(g.num_levels());
+  for (int level = 1; level <= g.num_levels(); ++level) {
+    const auto& groups = g.groups[level - 1];
+    std::vector<int>& own = owners[level - 1];
+    own.resize(groups.size());
+    std::vector<int> merged(ne, -1);
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const Face& f = g.faces[groups[gi][0]];
+      own[gi] = box_owner[box[f.e1]];
+      merged[box[f.e1]] = static_cast<int>(gi);
+      merged[box[f.e2]] = static_cast<int>(gi);
+    }
+    for (int e = 0; e < ne; ++e) box[e] = merged[box[e]];
+    box_owner = own;
+  }
+  return owners;
+}
+
 }  // namespace hpsb

@@ -152,6 +152,14 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
   // write disjoint entries of one shared table.
   std::vector<int> pos_of(sk->dim, -1);
   std::vector<int> prev_merge_of;  // previous level: group (= box of this level) -> merge index
+  // Rank holding each current box's map (sharded; level 1: the element's
+  // owner).  Owner-computes at the global levels: a merge runs on the rank
+  // that holds its first child (the box with the faces' e1) and receives the
+  // second child from its holder; the coarse level is replicated.
+  std::vector<int> box_owner(ne, 0);
+  for (int e = 0; e < ne; ++e) box_owner[e] = sharded ? part.elem_owner[e] : 0;
+  const std::vector<std::vector<int>> owners = merge_owners(g, part);
+  const int me = ctx->rank();
   DevBuf<double2> tnew_prev;  // previous level's merged maps (children of this level)
   DevBuf<int> d_status(2);  // [0] singular pivot tag + 1, [1] diagonal-pivot guard
   HPSB_CUDA(cudaMemsetAsync(d_status.p, 0, 2 * sizeof(int), ctx->stream));
@@ -181,7 +189,7 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
       for (int gi = g0; gi < g1; ++gi) {
         GroupPlan& gp = plan[gi];
         const Face& f0 = g.faces[groups[gi][0]];
-        gp.own = !sharded || level > part.last_local || part.owns_elem(f0.e1);
+        gp.own = !sharded || level == depth || box_owner[elem_box[f0.e1]] == me;
         const HostBox* bx[2] = {&boxes[elem_box[f0.e1]], &boxes[elem_box[f0.e2]]};
         for (int k = 0; k < 2; ++k)
           for (int i = 0; i < static_cast<int>(bx[k]->pos.size()); ++i)
@@ -253,6 +261,41 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
     prev_merge_of = merge_of;
     L->tperm.alloc(toff);
     tr.mark("alloc");
+
+    // ---- sharded global levels: bring the child maps this rank merges
+    // (owner-computes: the second child from its holder, NCCL send / recv),
+    // or every child to every rank at the replicated coarse level
+    std::vector<DevBuf<double2>> remote;
+    if (sharded && level > part.last_local) {
+      std::vector<Comm::Xfer> sends, recvs;
+      for (int gi = 0; gi < ng; ++gi) {
+        const Face& f0 = g.faces[groups[gi][0]];
+        const int b1 = elem_box[f0.e1], b2 = elem_box[f0.e2];
+        for (const int b : {b1, b2}) {
+          HostBox& hb = boxes[b];
+          const size_t bytes = sizeof(double2) * static_cast<size_t>(hb.ld) * hb.ld;
+          const int holder = box_owner[b];
+          if (level == depth) {  // coarse: every box to every rank (broadcast)
+            if (holder != me) {
+              remote.emplace_back(static_cast<size_t>(hb.ld) * hb.ld);
+              hb.T = remote.back().p;
+            }
+            ctx->comm->broadcast(const_cast<double2*>(hb.T), bytes, holder, ctx);
+          } else {
+            const int owner = box_owner[b1];
+            if (holder == owner) continue;
+            if (holder == me) sends.push_back({owner, const_cast<double2*>(hb.T), bytes});
+            if (owner == me) {
+              remote.emplace_back(static_cast<size_t>(hb.ld) * hb.ld);
+              hb.T = remote.back().p;
+              recvs.push_back({holder, remote.back().p, bytes});
+            }
+          }
+        }
+      }
+      if (level < depth) ctx->comm->exchange(sends, recvs, ctx);
+      tr.mark("box_exchange");
+    }
 
     // ---- gather children into the permuted layout
     {
@@ -382,25 +425,7 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
         nbx.ld = static_cast<int>(nbx.pos.size());
         nbx.T = merge_of[gi] >= 0 ? tnew.p + n_at[merge_of[gi]] : nullptr;
       }
-      if (sharded && level == part.last_local) {
-        // Subtree boxes -> every rank (NCCL broadcast per owner): the top
-        // merges and the coarse system are then built on all ranks.
-        size_t tot = 0;
-        std::vector<size_t> at(ng);
-        for (int gi = 0; gi < ng; ++gi) {
-          at[gi] = tot;
-          tot += static_cast<size_t>(next[gi].ld) * next[gi].ld;
-        }
-        DevBuf<double2> all(tot);
-        const int me = ctx->rank();
-        if (merge_of[me] < 0) throw std::logic_error("build_hierarchy: rank owns no subtree box");
-        zcopy(ctx, all.p + at[me], next[me].T, static_cast<size_t>(next[me].ld) * next[me].ld);
-        for (int r = 0; r < ng; ++r)
-          ctx->comm->broadcast(all.p + at[r],
-                               sizeof(double2) * static_cast<size_t>(next[r].ld) * next[r].ld, r, ctx);
-        for (int gi = 0; gi < ng; ++gi) next[gi].T = all.p + at[gi];
-        tnew = std::move(all);
-      }
+      box_owner = sharded ? owners[level - 1] : std::vector<int>(ng, 0);
       // element -> new box: the merge owning the element's old box
       std::vector<int> box_to_group(boxes.size(), -1);
       for (int gi = 0; gi < ng; ++gi) {

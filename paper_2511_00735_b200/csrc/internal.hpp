@@ -149,7 +149,29 @@ struct Comm {
   // In-place sum over ranks of n complex values on the context stream.
   virtual void allreduce_sum(double2* buf, size_t n, Context* ctx) = 0;
   virtual void broadcast(void* buf, size_t bytes, int root, Context* ctx) = 0;
+  // Point-to-point transfers of one step (every rank calls it; the sends and
+  // receives of all ranks must match pairwise): ncclSend / ncclRecv in one
+  // NCCL group.
+  struct Xfer {
+    int peer;
+    void* buf;
+    size_t bytes;
+  };
+  virtual void exchange(const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs,
+                        Context* ctx) = 0;
 };
+// One segment of a sharded exchange: rows [0, n) of `cols` columns of a
+// (column stride lda), against the baseline `base` (stride ldb; null = 0).
+struct DeltaSeg {
+  double2* a;
+  const double2* base;
+  int64_t n;
+  int cols = 1;
+  int64_t lda = 0, ldb = 0;
+};
+// Every row of the segments changed on at most one rank: one allreduce
+// makes a = base + sum_ranks (a_rank - base) on every rank (buf: workspace).
+void exchange_deltas(Context* ctx, DevBuf<double2>& buf, const std::vector<DeltaSeg>& segs);
 std::unique_ptr<Comm> make_nccl_comm(const unsigned char id[128], int rank, int size, int device);
 struct LocalGroup;
 std::shared_ptr<LocalGroup> make_local_group(int size);
@@ -281,6 +303,9 @@ struct Partition {
   bool owns_elem(int e) const { return elem_owner[e] == rank; }
 };
 Partition make_partition(const FaceGraph& g, int G, int rank);
+// owners[l - 1][group]: the rank that runs merge `group` of level l
+// (owner-computes: the holder of its first child, geometry.cpp).
+std::vector<std::vector<int>> merge_owners(const FaceGraph& g, const Partition& part);
 
 // ---------------------------------------------------------------- GEMV work lists
 // y[yi] = beta * y[yi] + gamma * z[zi] + alpha * A x[xi]   (complex, A col-major)
@@ -373,7 +398,21 @@ struct Skeleton {
   VPlan apply_plan;      // y = x + sum_e scatter(T_e gather(x))
   DevBuf<double2> x_buf, y_buf;  // plan endpoints
   std::shared_ptr<void> batch;   // multi-RHS matvec phase (skeleton.cu), built on first use
+  // Sharded layout of the solver's vectors: every rank keeps full-length
+  // buffers but owns only its subtree's local-face rows; the global rows
+  // (faces of the levels above the subtrees: the tail [tail_off, dim)) are
+  // replicated.  dist_rows lists the owned rows, then the tail rows encoded
+  // as -(row + 1) on ranks other than 0 (updated everywhere, counted in the
+  // dot products once).
+  int64_t tail_off = 0;
+  DevBuf<int> dist_rows;
+  int64_t n_dist_rows = 0;
+  DevBuf<int> keep_face;  // faces whose rows this rank contributes to a gathered vector
+  DevBuf<double2> gather_buf;
 };
+// Full vector on every rank from a distributed one (owned rows from their
+// owner, global rows from rank 0): one allreduce.
+void gather_distributed(const Skeleton* sk, double2* v, int R = 1);
 
 struct LevelOps;
 struct Hierarchy {
@@ -396,10 +435,15 @@ std::unique_ptr<Elements> build_elements(Context* ctx, int n, int order, double 
 // only, [nrhs][4][n][N-1] (boundary_only true).
 std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host, int nrhs,
                                          bool boundary_only = false);
-void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev);
+// distributed (sharded): y valid on the owned and global rows only (one
+// allreduce of the global rows) -- the sharded FGMRES's layout; else full.
+void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev,
+                    bool distributed = false);
 // Multi-RHS: R <= 32 vectors stored column-wise with leading dimension dim.
-void precond_apply_batch(Precond* p, const double2* v, double2* z, int R);
-void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int R);
+void precond_apply_batch(Precond* p, const double2* v, double2* z, int R,
+                         bool distributed = false);
+void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int R,
+                          bool distributed = false);
 hpsb_status fgmres_batch(Skeleton* sk, Precond* pc, const double2* rhs, double2* x, int R,
                          const hpsb_krylov_config& cfg, hpsb_solve_report* reports);
 void recover_field(const Skeleton* sk, const double2* x_dev, int rhs_index, double2* field_dev);
@@ -415,7 +459,10 @@ void hierarchy_level_apply(Hierarchy* h, int level, const double2* x_dev, double
 Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg);
 void destroy_precond(Precond* p);
 Context* precond_context(const Precond* p);
-void precond_apply(Precond* p, const double2* v_dev, double2* z_dev);
+// Sharded contexts: distributed = true leaves z valid on this rank's own
+// (subtree-local) rows and the global rows only, as the sharded FGMRES keeps
+// its vectors; false returns the full vector on every rank.
+void precond_apply(Precond* p, const double2* v_dev, double2* z_dev, bool distributed = false);
 // precond_apply is a fixed launch sequence (single GPU, gamma == 1 or exact
 // coarse): it can be captured into a CUDA graph
 bool precond_graph_safe(const Precond* p);

@@ -125,7 +125,7 @@ template <bool kUpdate>
 __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd,
     int nupd, double2* w, int64_t n, int R, double2* partial, double2* out, unsigned* ticket,
-    int fused, OrthStride bs, const int* jdev, int vdot) {
+    int fused, OrthStride bs, const int* jdev, int vdot, const int* __restrict__ rows) {
   __shared__ double2 sh[kOrthThreads / 32][104];
   __shared__ double2 hs[104];
   __shared__ bool last;
@@ -148,12 +148,23 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     for (int i = threadIdx.x; i < nupd; i += kOrthThreads) hs[i] = h_upd[i];
     __syncthreads();
   }
+  // rows (sharded): compact row k is vector row rows[k], or -(rows[k] + 1)
+  // for a row that is updated but left out of the dot products
   double2 wv[kOrthMaxR];
+  int64_t kx[kOrthMaxR];
+  bool cnt[kOrthMaxR];
 #pragma unroll
   for (int r = 0; r < kOrthMaxR; ++r) {
-    const int64_t k = base + threadIdx.x + r * kOrthThreads;
-    wv[r] = (r < R && k < n) ? __ldcg(w + k) : make_double2(0.0, 0.0);
-    if (kUpdate && r < R && k < n) {
+    const int64_t kc = base + threadIdx.x + r * kOrthThreads;
+    kx[r] = -1, cnt[r] = false;
+    if (r < R && kc < n) {
+      const int64_t rr = rows ? rows[kc] : kc;
+      kx[r] = rr >= 0 ? rr : -rr - 1;
+      cnt[r] = rr >= 0;
+    }
+    const int64_t k = kx[r];
+    wv[r] = k >= 0 ? __ldcg(w + k) : make_double2(0.0, 0.0);
+    if (kUpdate && k >= 0) {
       double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
       int i = 0;
       for (; i + 8 <= nupd; i += 8) {  // 8 independent loads in flight
@@ -176,7 +187,7 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     double a = 0.0;
 #pragma unroll
     for (int r = 0; r < kOrthMaxR; ++r)
-      if (r < R) a += cabs2(wv[r]);
+      if (cnt[r]) a += cabs2(wv[r]);
     a = warp_sum(a);
     if (lane == 0) sh[warp][0] = make_double2(a, 0.0);
   } else {
@@ -187,8 +198,8 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
       for (int q = 0; q < 8; ++q) acc[q] = make_double2(0.0, 0.0);
 #pragma unroll
       for (int r = 0; r < kOrthMaxR; ++r) {
-        const int64_t k = base + threadIdx.x + r * kOrthThreads;
-        if (r < R && k < n) {
+        const int64_t k = kx[r];
+        if (cnt[r]) {
           double2 v[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
@@ -497,7 +508,13 @@ struct Work {
   int64_t chunk;
   DevBuf<double2> partial, hdev;
   DevBuf<unsigned> ticket;
-  explicit Work(Context* c, int64_t dim, int maxcols) : ctx(c), n(dim) {
+  // Sharded: the dot products run over this rank's rows (rows / on, see
+  // Skeleton::dist_rows) and are summed over the ranks (one allreduce of the
+  // few coefficients per pass); elementwise updates stay full length.
+  const int* rows = nullptr;
+  int64_t on = 0;
+  bool sharded() const { return ctx->world() > 1; }
+  explicit Work(Context* c, int64_t dim, int maxcols) : ctx(c), n(dim), on(dim) {
     blocks = static_cast<int>((dim + kRowsPerBlock - 1) / kRowsPerBlock);
     chunk = kRowsPerBlock;
     partial.alloc(static_cast<size_t>((dim + kOrthThreads - 1) / kOrthThreads + blocks) * maxcols);
@@ -512,14 +529,14 @@ struct Work {
   // R = 8 / 4 / 2 / 1 -> 27.9 / 25.6 / 23.1 / 28.7 ms of orthogonalisation).
   void orth_grid(int& R, int& nb) const {
     R = 1;
-    while (R < 2 && (n + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
+    while (R < 2 && (on + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
       R *= 2;
     static const int force_r = [] {
       const char* e = std::getenv("HPSB_ORTH_R");
       return e ? std::atoi(e) : 0;
     }();
     if (force_r >= 1 && force_r <= kOrthMaxR) R = force_r;
-    nb = static_cast<int>((n + kOrthThreads * R - 1) / (kOrthThreads * R));
+    nb = static_cast<int>((on + kOrthThreads * R - 1) / (kOrthThreads * R));
   }
   void reserve(int maxcols) {  // partial sums for maxcols columns (before a graph capture)
     int R, nb;
@@ -550,13 +567,14 @@ struct Work {
                    8.0 * n * (ncols + nupd));
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot);
+               w, on, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot, rows);
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
-               w, n, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot);
+               w, on, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot, rows);
     if (!fused)
       launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1,
                static_cast<const double2*>(partial.p), nb, jdev ? ncols : nout, out, jdev);
+    if (sharded()) ctx->comm->allreduce_sum(out, nout, ctx);  // GMRES inner products (NCCL)
   }
   // out[0..ncols) = V^H w.  Short vectors: one launch (last-block reduction);
   // long vectors: many row blocks + a column-parallel reduce launch.
@@ -580,7 +598,10 @@ struct Work {
                std::min(kOrthChunk, ncols - c0), h + c0, sign, w, n);
   }
   double norm(const double2* w) {
-    dots(w, 1, w, hdev.p);
+    if (sharded())
+      orth1(w, 0, nullptr, 0, const_cast<double2*>(w), hdev.p, nullptr, 0, 0);
+    else
+      dots(w, 1, w, hdev.p);
     double2 v;
     HPSB_CUDA(cudaMemcpyAsync(&v, hdev.p, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream));
     HPSB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -700,6 +721,8 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   const int restart = cfg.restart;
   *rep = hpsb_solve_report{};
   Work wk(ctx, n, restart + 2);
+  const bool dist = ctx->world() > 1;  // sharded: distributed vectors (Skeleton::dist_rows)
+  if (dist) wk.rows = sk->dist_rows.p, wk.on = sk->n_dist_rows;
   ctx->history.clear();
   DevBuf<double2> V(static_cast<size_t>(n) * (restart + 1));
   if (!pc) right = false;
@@ -726,7 +749,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
     return HPSB_OK;
   }
   auto true_residual = [&]() {
-    skeleton_apply(sk, x, tmp.p);
+    skeleton_apply(sk, x, tmp.p, dist);
     wk.sub(rhs, tmp.p, tmp.p);
     return wk.norm(tmp.p) / bnorm;
   };
@@ -781,14 +804,14 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
     for (; !cg.exec && j < restart && total < cfg.max_iters; ++j, ++total) {
       double2* Vj = V.p + static_cast<size_t>(j) * n;
       if (right) {
-        precond_apply(pc, Vj, pz.p);
-        skeleton_apply(sk, pz.p, w.p);
+        precond_apply(pc, Vj, pz.p, dist);
+        skeleton_apply(sk, pz.p, w.p, dist);
       } else if (pc) {
         double2* Zj = Z.p + static_cast<size_t>(j) * n;
-        precond_apply(pc, Vj, Zj);
-        skeleton_apply(sk, Zj, w.p);
+        precond_apply(pc, Vj, Zj, dist);
+        skeleton_apply(sk, Zj, w.p, dist);
       } else {
-        skeleton_apply(sk, Vj, w.p);
+        skeleton_apply(sk, Vj, w.p, dist);
       }
       double2* h1 = wk.hdev.p;
       double2* h2 = wk.hdev.p + (j + 1);
@@ -848,7 +871,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
       if (right) {  // x += P(V y)
         zfill(ctx, pu.p, n, make_double2(0.0, 0.0));
         wk.axpy(V.p, j, wk.hdev.p, 1.0, pu.p);
-        precond_apply(pc, pu.p, pz.p);
+        precond_apply(pc, pu.p, pz.p, dist);
         wk.axpy(pz.p, 1, wk.hdev.p + j, 1.0, x);
       } else {
         wk.axpy(pc ? Z.p : V.p, j, wk.hdev.p, 1.0, x);
@@ -883,6 +906,7 @@ hpsb_status fgmres(Skeleton* sk, Precond* pc, const double2* rhs, double2* x,
   rep->iterations = total;
   rep->final_residual = true_residual();
   rep->converged = rep->final_residual <= cfg.tol;
+  if (dist) gather_distributed(sk, x);  // the ABI's x is the full vector on every rank
   finish_time();
   return rep->converged ? HPSB_OK : HPSB_NO_CONVERGENCE;
 }
@@ -950,8 +974,12 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   if (cfg.max_iters < 1) throw InvalidArgument("gmres: max_iters must be >= 1");
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("gmres: 1 <= nrhs <= 32");
   Context* ctx = sk->ctx;
-  if (ctx->world() > 1) throw InvalidArgument("gmres: multi-RHS is single-GPU");
-  const int64_t n = sk->dim;
+  // Sharded: distributed vectors as the single-RHS driver (Skeleton::dist_rows;
+  // the R columns' coefficients are summed over the ranks in one allreduce).
+  const bool dist = ctx->world() > 1;
+  const int* rows = dist ? sk->dist_rows.p : nullptr;
+  const int64_t n = sk->dim, on = dist ? sk->n_dist_rows : sk->dim;
+  DevBuf<double2> xch;
   const int restart = cfg.restart;
   const int hs = 2 * (restart + 2) + 1;  // per-RHS slots: h1 | h2 | nn (and y)
   const bool reorth = cfg.reorthogonalize != 0;  // CGS2, else single-pass MGS
@@ -964,9 +992,9 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   DevBuf<unsigned> tickets(R);
   HPSB_CUDA(cudaMemsetAsync(tickets.p, 0, sizeof(unsigned) * R, ctx->stream));
   int RR = 1;  // rows per thread of the orth kernel
-  while (RR < orth_rr_cap() && (n + kOrthThreads * 2 * RR - 1) / (kOrthThreads * 2 * RR) >= 2 * ctx->num_sms)
+  while (RR < orth_rr_cap() && (on + kOrthThreads * 2 * RR - 1) / (kOrthThreads * 2 * RR) >= 2 * ctx->num_sms)
     RR *= 2;
-  const int nb = static_cast<int>((n + kOrthThreads * RR - 1) / (kOrthThreads * RR));
+  const int nb = static_cast<int>((on + kOrthThreads * RR - 1) / (kOrthThreads * RR));
   const int64_t pstride = static_cast<int64_t>(nb) * (restart + 2);
   DevBuf<double2> partial(static_cast<size_t>(R) * pstride);
   // one CGS2 pass for all R: optional w -= V h_upd, then V^H w / ||w||^2
@@ -979,12 +1007,13 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
                    8.0 * n * R * (ncols + nupd));
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
-               Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
-               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr), vdot);
+               Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, on,
+               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr), vdot, rows);
     else
       launch_k(ctx, orth_kernel<false>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
-               Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n,
-               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr), vdot);
+               Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, on,
+               RR, partial.p, out, tickets.p, 1, st, static_cast<const int*>(nullptr), vdot, rows);
+    if (dist) exchange_deltas(ctx, xch, {{out, nullptr, nout, R, hs, 0}});  // NCCL allreduce
   };
   auto orth = [&](int ncols, const double2* h_upd, int nupd, double2* wv, double2* out,
                   const double2* Vb, int vdot) {
@@ -1015,7 +1044,7 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   HPSB_CUDA(cudaMemcpyAsync(tmp.p, rhs, sizeof(double2) * R * n, cudaMemcpyDeviceToDevice, ctx->stream));
   norms(tmp.p, bnorm);
   auto true_residual = [&](std::vector<double>& out) {  // ||rhs - M x|| / ||rhs||
-    skeleton_apply_batch(sk, x, tmp.p, R);
+    skeleton_apply_batch(sk, x, tmp.p, R, dist);
     {
       KernelScope ks(ctx, "gmres_sub", 48.0 * n * R, 0.0);
       launch_k(ctx, sub_kernel, dim3(vblocks), dim3(256), 0, 1, rhs, static_cast<const double2*>(tmp.p),
@@ -1065,9 +1094,9 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
       double2* src = Vj;
       if (pc) {
         src = Z.p + static_cast<size_t>(j) * R * n;
-        precond_apply_batch(pc, Vj, src, R);
+        precond_apply_batch(pc, Vj, src, R, dist);
       }
-      skeleton_apply_batch(sk, src, w.p, R);
+      skeleton_apply_batch(sk, src, w.p, R, dist);
       if (reorth) {
         orth(j + 1, nullptr, 0, w.p, hdev.p, V.p, 0);                       // h1 = V^H w
         orth(j + 1, hdev.p, j + 1, w.p, hdev.p + (j + 1), V.p, 0);          // w -= V h1; h2 = V^H w
@@ -1145,6 +1174,7 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   }
   std::vector<double> fin;
   true_residual(fin);
+  if (dist) gather_distributed(sk, x, R);  // full solutions on every rank
   HPSB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
   HPSB_CUDA(cudaEventSynchronize(ctx->ev[3]));
   float ms = 0;

@@ -98,17 +98,23 @@ struct Precond {
   std::vector<BPhase> bdown, bup;
   BPhase bcoarse;              // coarse matvec of the batched gmres_fixed_steps
   std::vector<BPhase> bexact;  // exact coarse: one phase per column chunk
+  // sharded: the global rows (faces of the levels above the subtrees) form
+  // the tail [tail_off, dim) of every skeleton vector; exchange buffers
+  int64_t tail_off = 0;
+  DevBuf<double2> xbuf, xsave;
+  void run_step(const Step& st, bool down, double2* z) const {
+    if (st.subtree >= 0) subtrees[st.subtree]->run(ctx, down, r.p, z);
+    else if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
+    else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
+    else
+      for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
+  }
   void run_steps(bool down, bool global, double2* z) const {
     const int last_local = h->sk->el->part.last_local;
-    for (const Step& st : down ? down_steps : up_steps) {
-      if ((st.level > last_local) != global) continue;
-      if (st.subtree >= 0) subtrees[st.subtree]->run(ctx, down, r.p, z);
-      else if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
-      else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
-      else
-        for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
-    }
+    for (const Step& st : down ? down_steps : up_steps)
+      if ((st.level > last_local) == global) run_step(st, down, z);
   }
+  void run_global_sharded(bool down, double2* z);
 };
 
 constexpr int kMaxCoarseIters = 30;    // fused / on-chip coarse kernels
@@ -1270,6 +1276,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     for (size_t f = 0; f < keep.size(); ++f)
       keep[f] = part.face_owner[f] == ctx->rank() || (part.face_owner[f] < 0 && ctx->rank() == 0);
     p->keep_face.upload(keep, ctx->stream);
+    p->tail_off = static_cast<int64_t>(h->sk->graph.level_range[part.last_local].first) * h->sk->bs;
   }
 
   // stage lists for the multi-RHS phases (single GPU)
@@ -1590,7 +1597,38 @@ bool precond_graph_safe(const Precond* p) {
   return p->ctx->world() == 1 && (p->cfg.exact_coarse || p->cfg.gamma <= 1);
 }
 
-void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
+// Sharded global levels (owner-computes: each merge of a level above the
+// subtrees runs on one rank).  Every rank holds the same global rows of r
+// and out before a level; a level's merges change out at their separator
+// rows (assignments, down) or by increments (up) and r at their perimeter
+// rows, each row on exactly one rank, so one allreduce of the changes per
+// level makes every rank consistent again for the next level.
+void Precond::run_global_sharded(bool down, double2* z) {
+  const auto& g = h->sk->graph;
+  const int bs = h->sk->bs, last_local = h->sk->el->part.last_local;
+  auto ff = [&](int l) { return static_cast<int64_t>(g.level_range[l - 1].first) * bs; };
+  const auto& steps = down ? down_steps : up_steps;
+  for (const Step& st : steps) {
+    const int l = st.level;
+    if (l <= last_local) continue;
+    const int64_t s0 = ff(l), s1 = ff(l + 1);  // level-l separator rows; rows above: [s1, dim)
+    if (down) {
+      // baseline of r above the level; out at the level's separators is 0
+      // on every rank (zeroed before the global sweep)
+      if (xsave.n < static_cast<size_t>(dim - s1)) xsave.alloc(dim - s1);
+      zcopy(ctx, xsave.p, r.p + s1, dim - s1);
+      run_step(st, true, z);
+      exchange_deltas(ctx, xbuf, {{z + s0, nullptr, s1 - s0}, {r.p + s1, xsave.p, dim - s1}});
+    } else {
+      if (xsave.n < static_cast<size_t>(s1 - s0)) xsave.alloc(s1 - s0);
+      zcopy(ctx, xsave.p, z + s0, s1 - s0);
+      run_step(st, false, z);
+      exchange_deltas(ctx, xbuf, {{z + s0, xsave.p, s1 - s0}});
+    }
+  }
+}
+
+void precond_apply(Precond* p, const double2* v_dev, double2* z_dev, bool distributed) {
   Context* ctx = p->ctx;
   const int vblocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
   launch_k(ctx, copy_vec_kernel, dim3(vblocks), dim3(256), 0, 1, p->r.p, v_dev, p->dim);
@@ -1602,25 +1640,22 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev) {
   p->run_steps(true, false, z_dev);  // local levels, down
   const bool sharded = ctx->world() > 1;
   if (sharded) {
-    // Each residual entry was updated by at most one rank's subtree:
-    // r = v + sum_ranks (r_rank - v).
-    const int blocks = static_cast<int>(std::min<int64_t>((p->dim + 255) / 256, 8 * ctx->num_sms));
-    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, -1.0, p->dim);
-    ctx->comm->allreduce_sum(p->r.p, p->dim, ctx);
-    launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p, v_dev, 1.0, p->dim);
+    // Only global rows (the tail) were changed by more than one rank's
+    // subtree, each by at most one: r_tail = v_tail + sum_ranks (r_rank - v)_tail.
+    const int64_t t0 = p->tail_off;
+    exchange_deltas(ctx, p->xbuf, {{p->r.p + t0, v_dev + t0, p->dim - t0}});
+    HPSB_CUDA(cudaMemsetAsync(z_dev + t0, 0, sizeof(double2) * (p->dim - t0), ctx->stream));
+    p->run_global_sharded(true, z_dev);  // top (global) levels, down: owner-computes
+  } else {
+    p->run_steps(true, true, z_dev);
   }
-  p->run_steps(true, true, z_dev);  // top (global) levels, down
-  run_coarse(p, z_dev);
-  p->run_steps(false, true, z_dev);
+  run_coarse(p, z_dev);  // replicated on every rank (identical inputs)
+  if (sharded) p->run_global_sharded(false, z_dev);
+  else p->run_steps(false, true, z_dev);
   p->run_steps(false, false, z_dev);
-  if (sharded) {
-    // Local faces come from their owner, global faces from rank 0: sum.
-    const int bs = p->h->sk->bs;
-    const int nf = static_cast<int>(p->dim / bs);
-    launch_k(ctx, mask_faces_kernel, dim3(nf), dim3(64), 0, 1, z_dev,
-             static_cast<const int*>(p->keep_face.p), bs);
-    ctx->comm->allreduce_sum(z_dev, p->dim, ctx);
-  }
+  // distributed: each rank's own (local-face) rows and the global rows are
+  // valid -- what the sharded FGMRES consumes; else the full vector
+  if (sharded && !distributed) gather_distributed(p->h->sk, z_dev);
 }
 
 namespace {
@@ -1695,9 +1730,8 @@ void build_batch(Precond* p) {
 }
 }  // namespace
 
-void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
+void precond_apply_batch(Precond* p, const double2* v, double2* z, int R, bool distributed) {
   Context* ctx = p->ctx;
-  if (ctx->world() > 1) throw InvalidArgument("precond_apply: multi-RHS is single-GPU");
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("precond_apply: 1 <= nrhs <= 32");
   if (!p->cfg.exact_coarse && p->cfg.gamma > 1)
     throw InvalidArgument("precond_apply: multi-RHS runs gamma = 1");
@@ -1715,12 +1749,40 @@ void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
            !std::getenv("HPSB_NO_SMALL_BATCH");
   };
   const int depth = p->cfg.depth;
-  for (int l = 1; l < depth; ++l) {
+  auto level = [&](int l, bool down) {
     if (small_fits(l)) {
-      p->smalls[p->small_level_of[l]]->run_batch(ctx, true, p->rB.p, z, R, dim);
-      continue;
+      p->smalls[p->small_level_of[l]]->run_batch(ctx, down, p->rB.p, z, R, dim);
+      return;
     }
-    for (int k = 0; k < 4; ++k) p->bdown[(l - 1) * 4 + k].run(ctx, R, "vcycle_down_batch", bind);
+    for (int k = 0; k < 4; ++k) {
+      if (down) p->bdown[(l - 1) * 4 + k].run(ctx, R, "vcycle_down_batch", bind);
+      else p->bup[(depth - 1 - l) * 4 + k].run(ctx, R, "vcycle_up_batch", bind);
+    }
+  };
+  // Sharded: the single-RHS exchanges (precond_apply) on R columns at once.
+  const bool sharded = ctx->world() > 1;
+  const int last_local = sharded ? p->h->sk->el->part.last_local : depth;
+  const int bs = p->h->sk->bs;
+  const auto& g = p->h->sk->graph;
+  auto ff = [&](int l) { return static_cast<int64_t>(g.level_range[l - 1].first) * bs; };
+  auto save = [&](const double2* src, int64_t rows) {
+    if (p->xsave.n < static_cast<size_t>(rows) * R) p->xsave.alloc(static_cast<size_t>(rows) * R);
+    HPSB_CUDA(cudaMemcpy2DAsync(p->xsave.p, rows * sizeof(double2), src, dim * sizeof(double2),
+                                rows * sizeof(double2), R, cudaMemcpyDeviceToDevice, ctx->stream));
+  };
+  for (int l = 1; l < depth && l <= last_local; ++l) level(l, true);
+  if (sharded) {
+    const int64_t t0 = p->tail_off;
+    exchange_deltas(ctx, p->xbuf, {{p->rB.p + t0, v + t0, dim - t0, R, dim, dim}});
+    HPSB_CUDA(cudaMemset2DAsync(z + t0, dim * sizeof(double2), 0, (dim - t0) * sizeof(double2), R,
+                                ctx->stream));
+    for (int l = last_local + 1; l < depth; ++l) {
+      const int64_t s0 = ff(l), s1 = ff(l + 1);
+      save(p->rB.p + s1, dim - s1);
+      level(l, true);
+      exchange_deltas(ctx, p->xbuf, {{z + s0, nullptr, s1 - s0, R, dim, 0},
+                                     {p->rB.p + s1, p->xsave.p, dim - s1, R, dim, dim - s1}});
+    }
   }
   if (p->cfg.exact_coarse) {
     for (const BPhase& ph : p->bexact) ph.run(ctx, R, "coarse_exact_batch", bind);
@@ -1739,13 +1801,15 @@ void precond_apply_batch(Precond* p, const double2* v, double2* z, int R) {
              static_cast<const double2*>(p->gvB.p), static_cast<const double*>(p->stateB.p),
              z + p->off_d, dim);
   }
-  for (int l = depth - 1; l >= 1; --l) {
-    if (small_fits(l)) {
-      p->smalls[p->small_level_of[l]]->run_batch(ctx, false, p->rB.p, z, R, dim);
-      continue;
+  if (sharded)
+    for (int l = depth - 1; l > last_local; --l) {
+      const int64_t s0 = ff(l), s1 = ff(l + 1);
+      save(z + s0, s1 - s0);
+      level(l, false);
+      exchange_deltas(ctx, p->xbuf, {{z + s0, p->xsave.p, s1 - s0, R, dim, s1 - s0}});
     }
-    for (int k = 0; k < 4; ++k) p->bup[(depth - 1 - l) * 4 + k].run(ctx, R, "vcycle_up_batch", bind);
-  }
+  for (int l = std::min(depth - 1, last_local); l >= 1; --l) level(l, false);
+  if (sharded && !distributed) gather_distributed(p->h->sk, z, R);
 }
 
 int64_t precond_bytes(const Precond* p) { return p->bytes_per_apply; }

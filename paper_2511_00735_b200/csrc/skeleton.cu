@@ -145,24 +145,64 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
   }
   sk->apply_plan.name = "skeleton_matvec";
   sk->apply_plan.finalize(ctx->stream);
+  if (sharded) {
+    const Partition& part = el->part;
+    sk->tail_off = static_cast<int64_t>(sk->graph.level_range[part.last_local].first) * sk->bs;
+    std::vector<int> rows, keep(sk->graph.num_faces());
+    for (int f = 0; f < sk->graph.num_faces(); ++f) {
+      keep[f] = part.face_owner[f] == ctx->rank() || (part.face_owner[f] < 0 && ctx->rank() == 0);
+      if (part.face_owner[f] == ctx->rank())
+        for (int k = 0; k < sk->bs; ++k) rows.push_back(f * sk->bs + k);
+    }
+    for (int64_t i = sk->tail_off; i < sk->dim; ++i)
+      rows.push_back(ctx->rank() == 0 ? static_cast<int>(i) : -static_cast<int>(i) - 1);
+    sk->n_dist_rows = static_cast<int64_t>(rows.size());
+    sk->dist_rows.upload(rows, ctx->stream);
+    sk->keep_face.upload(keep, ctx->stream);
+  }
   // no synchronisation: buffers are freed stream-ordered, host uploads are
   // staged, and the element stage may still be running (Elements::pending)
   return sk;
 }
 
-void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev) {
+void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev, bool distributed) {
   // The plan was built on x_buf / y_buf; bind the caller's vectors instead.
   Context* ctx = sk->ctx;
   const bool sharded = ctx->world() > 1;
-  if (sharded) HPSB_CUDA(cudaMemsetAsync(y_dev, 0, sk->dim * sizeof(double2), ctx->stream));
+  // Every skeleton row is produced by exactly one rank's element: zero, then
+  // sum -- the whole vector, or (distributed) the global rows only: an
+  // element reads and writes only its own subtree's rows and the global rows
+  // (the subtree boundaries are global-level faces).
+  const int64_t z0 = distributed ? sk->tail_off : 0;
+  if (sharded)
+    HPSB_CUDA(cudaMemsetAsync(y_dev + z0, 0, (sk->dim - z0) * sizeof(double2), ctx->stream));
   sk->apply_plan.run(ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
-  // Every skeleton row is produced by exactly one rank's element: sum.
-  if (sharded) ctx->comm->allreduce_sum(y_dev, sk->dim, ctx);
+  if (sharded) ctx->comm->allreduce_sum(y_dev + z0, sk->dim - z0, ctx);
 }
 
-void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int R) {
+namespace {
+__global__ void keep_faces_kernel(double2* v, const int* __restrict__ keep, int bs) {
+  if (keep[blockIdx.x]) return;
+  for (int k = threadIdx.x; k < bs; k += blockDim.x)
+    v[static_cast<int64_t>(blockIdx.x) * bs + k] = make_double2(0.0, 0.0);
+}
+}  // namespace
+
+void gather_distributed(const Skeleton* sk, double2* v, int R) {
   Context* ctx = sk->ctx;
-  if (ctx->world() > 1) throw InvalidArgument("skeleton_apply: multi-RHS is single-GPU");
+  if (ctx->world() == 1) return;
+  for (int b = 0; b < R; ++b) {
+    keep_faces_kernel<<<sk->graph.num_faces(), 64, 0, ctx->stream>>>(v + b * sk->dim,
+                                                                      sk->keep_face.p, sk->bs);
+    HPSB_LAUNCHED(ctx);
+  }
+  ctx->comm->allreduce_sum(v, static_cast<size_t>(R) * sk->dim, ctx);
+}
+
+void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int R,
+                          bool distributed) {
+  Context* ctx = sk->ctx;
+  const bool sharded = ctx->world() > 1;
   auto* self = const_cast<Skeleton*>(sk);
   if (!self->batch) {
     // Y = X + sum_e scatter(T_e gather(X)): the matvec plan's items as a
@@ -180,10 +220,18 @@ void skeleton_apply_batch(const Skeleton* sk, const double2* x, double2* y, int 
     ph->finalize(ctx->stream);
     self->batch = ph;
   }
+  // sharded: as skeleton_apply, on R columns (own elements' rows; the rows
+  // several ranks produce are zeroed and summed)
+  const int64_t z0 = distributed ? sk->tail_off : 0;
+  if (sharded)
+    HPSB_CUDA(cudaMemset2DAsync(y + z0, sk->dim * sizeof(double2), 0,
+                                (sk->dim - z0) * sizeof(double2), R, ctx->stream));
   BBind bind;
   bind.from[0] = sk->x_buf.p, bind.to[0] = const_cast<double2*>(x);
   bind.from[1] = sk->y_buf.p, bind.to[1] = y;
   static_cast<const BPhase*>(sk->batch.get())->run(ctx, R, "skeleton_matvec_batch", bind);
+  if (sharded)
+    exchange_deltas(ctx, self->gather_buf, {{y + z0, nullptr, sk->dim - z0, R, sk->dim, 0}});
 }
 
 }  // namespace hpsb

@@ -121,3 +121,86 @@ def test_guard_trip_on_one_rank_rebuilds_on_all(monkeypatch):
         assert relf(s["Pv"], ref["Pv"]) < 1e-10
         assert abs(s["rep"]["iterations"] - ref["rep"]["iterations"]) <= 1
         assert relf(s["x"], ref["x"]) < 1e-9
+
+
+def _run_ranks(world, fn):
+    grp_out, errs = [None] * world, [None] * world
+
+    def run(rank):
+        try:
+            grp_out[rank] = fn(rank)
+        except Exception as exc:  # noqa: BLE001
+            errs[rank] = exc
+
+    threads = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not any(t.is_alive() for t in threads), "sharded run hung"
+    failed = [(r, repr(e)) for r, e in enumerate(errs) if e is not None]
+    assert not failed, failed
+    return grp_out
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_multi_rhs(world):
+    """cfg4's setting (plane-wave right-hand sides, s = 0) on a 16 x 16 mesh:
+    the lockstep multi-RHS FGMRES on distributed vectors (owner-computes top
+    merges, batched halo / coefficient allreduces) matches the single GPU."""
+    import paper_2511_00735_b200 as hps
+    prob = hps.problem(2, 4, n=16)
+    R = 4
+    ctx = hps.Context(0)
+    el = hps.build_elements(ctx, prob)
+    sk = hps.assemble_skeleton(el, prob)
+    pc = hps.build_preconditioner(hps.build_hierarchy(sk, factor_coarse=False), coarse_iters=4)
+    rhs = np.stack([sk.rhs(b) for b in range(R)])
+    X0, reps0 = hps.fgmres_batch(sk, rhs, pc, restart=60, tol=1e-8)
+    grp = hps.LocalGroup(world)
+
+    def rank_run(rank):
+        c = hps.Context(0)
+        c.attach_local(grp, rank)
+        e = hps.build_elements(c, prob)
+        s = hps.assemble_skeleton(e, prob)
+        p = hps.build_preconditioner(hps.build_hierarchy(s, factor_coarse=False), coarse_iters=4)
+        r = np.stack([s.rhs(b) for b in range(R)])
+        return hps.fgmres_batch(s, r, p, restart=60, tol=1e-8)
+
+    for X, reps in _run_ranks(world, rank_run):
+        for b in range(R):
+            assert reps[b]["converged"]
+            assert abs(reps[b]["iterations"] - reps0[b]["iterations"]) <= 1
+            assert relf(X[b], X0[b]) < 1e-7
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_krylov_variants(world):
+    """Distributed vectors under single-pass MGS and the right-preconditioned
+    gmres: every rank matches the single GPU."""
+    import paper_2511_00735_b200 as hps
+    prob = hps.problem(2, 1)
+    ctx = hps.Context(0)
+    el = hps.build_elements(ctx, prob)
+    sk = hps.assemble_skeleton(el, prob)
+    pc = hps.build_preconditioner(hps.build_hierarchy(sk, factor_coarse=False), coarse_iters=4)
+    xm, rm = hps.fgmres(sk, sk.rhs(), pc, restart=50, tol=1e-10, reorthogonalize=False)
+    xr, rr = hps.gmres(sk, sk.rhs(), restart=50, tol=1e-10, right_precond=pc)
+    grp = hps.LocalGroup(world)
+
+    def rank_run(rank):
+        c = hps.Context(0)
+        c.attach_local(grp, rank)
+        e = hps.build_elements(c, prob)
+        s = hps.assemble_skeleton(e, prob)
+        p = hps.build_preconditioner(hps.build_hierarchy(s, factor_coarse=False), coarse_iters=4)
+        a = hps.fgmres(s, s.rhs(), p, restart=50, tol=1e-10, reorthogonalize=False,
+                       record_history=True)
+        b = hps.gmres(s, s.rhs(), restart=50, tol=1e-10, right_precond=p)
+        return a, b
+
+    for (x1, r1), (x2, r2) in _run_ranks(world, rank_run):
+        assert abs(r1["iterations"] - rm["iterations"]) <= 1 and relf(x1, xm) < 1e-9
+        assert r1["basis_orthogonality"] < 1e-6
+        assert abs(r2["iterations"] - rr["iterations"]) <= 1 and relf(x2, xr) < 1e-9

@@ -8,7 +8,13 @@ The CUDA path itself cannot run here; these tests pin what it relies on:
     from per-rank element contributions (the oracle's element ItI maps) and
     summed with an allreduce equals the reference interface operator M x;
   - the preconditioner's residual combination r = v + sum_ranks (r_rank - v)
-    and the masked output allreduce reproduce the replicated vectors.
+    and the masked output allreduce reproduce the replicated vectors;
+  - owner-computes: the merges of each global level run on distinct ranks
+    (hpsb_merge_owners), nested level to level;
+  - distributed vectors: an element reads / writes only its rank's rows and
+    the global rows, so the matvec needs one allreduce of the global rows,
+    and inner products over own rows + the global rows once (allreduced)
+    equal the full ones.
 """
 import os
 import socket
@@ -115,6 +121,58 @@ def _worker(rank, world, port, q):
         zm = torch.from_numpy(np.where(keep, z, 0.0))
         dist.all_reduce(zm)
         res["masked_output"] = bool(np.allclose(zm.numpy(), z, rtol=0, atol=0))
+        # ---- owner-computes merges of the global levels (cfg3 mesh):
+        # each global level's merges on distinct ranks, each rank's merge at
+        # level l+1 on a rank that held a merge at level l
+        pg = hps.partition(128, world, rank)
+        prev = None
+        for level in range(pg["last_local"] + 1, 14):
+            own = hps.merge_owners(128, world, level)
+            res[f"owners_distinct_{level}"] = len(set(own.tolist())) == len(own)
+            if prev is not None:
+                res[f"owners_nested_{level}"] = set(own.tolist()) <= set(prev.tolist())
+            prev = own
+        if world > 1:
+            res["owners_subtree"] = bool(np.array_equal(
+                hps.merge_owners(128, world, pg["last_local"]), np.arange(world)))
+        # ---- distributed vectors: an element touches only its rank's rows
+        # and the global rows; the matvec's own rows are exact without any
+        # exchange and one allreduce of the global rows completes the rest
+        fo = np.repeat(p["face_owner"], bs)
+        touched_ok = True
+        yd = np.zeros(S.dim, dtype=complex)
+        for e in range(n * n):
+            if p["elem_owner"][e] != rank:
+                continue
+            ins, outs = _slots(fg, n, m, e)
+            for idx in np.concatenate([ins, outs]):
+                if idx >= 0 and fo[idx] not in (rank, -1):
+                    touched_ok = False
+            T, _ = S.element(e)
+            Tx = T @ np.where(ins >= 0, x[np.maximum(ins, 0)], 0)
+            for b in range(len(outs)):
+                if outs[b] >= 0:
+                    yd[outs[b]] = x[outs[b]] + Tx[b]
+        res["element_rows_own_or_global"] = touched_ok
+        tail = fo < 0
+        tt = torch.from_numpy(np.ascontiguousarray(yd[tail]).view(np.float64).copy())
+        dist.all_reduce(tt)
+        Mx = S.apply_M(x)
+        res["dist_matvec_own_rows"] = bool(np.allclose(yd[fo == rank], Mx[fo == rank], rtol=1e-13,
+                                                       atol=0))
+        res["dist_matvec_global_rows"] = bool(np.allclose(tt.numpy().view(complex), Mx[tail],
+                                                          rtol=1e-13, atol=0))
+        # ---- distributed inner products: own rows + the global rows once
+        a = rng.standard_normal(S.dim) + 1j * rng.standard_normal(S.dim)
+        at = torch.from_numpy(a.view(np.float64).copy())
+        dist.broadcast(at, 0)
+        a = at.numpy().view(complex).copy()
+        wgt = (fo == rank) | (tail & (rank == 0))
+        part = torch.tensor([np.vdot(a[wgt], Mx[wgt]).real, np.vdot(a[wgt], Mx[wgt]).imag],
+                            dtype=torch.float64)
+        dist.all_reduce(part)
+        full = np.vdot(a, Mx)
+        res["dist_dot"] = bool(abs(complex(part[0], part[1]) - full) <= 1e-12 * abs(full))
         q.put((rank, res))
     finally:
         dist.destroy_process_group()
