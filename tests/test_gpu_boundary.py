@@ -102,20 +102,27 @@ def test_right_preconditioned_gmres(hps, oracle, ctx, name, reorth):
 
 def test_solve_report_fields(hps, oracle, ctx):
     """test_driver.cpp:70-117: basis orthogonality <= 1e-8 with
-    record_history, a positive preconditioner memory, build / solve times."""
+    record_history on the driver's reorthogonalised solve, a positive
+    preconditioner memory, build / solve times.  A single MGS pass (the
+    KrylovConfig default) keeps the basis orthogonal only to ~1e-6 here, on
+    the oracle as on the GPU."""
     p, S, el, sk, h = setup(hps, oracle, ctx, "cfg1")
     pc = hps.build_preconditioner(h, depth=3, coarse_iters=4)
+    S.precond(depth=3, gamma=1, coarse_iters=4)
     for reorth in (True, False):
         x, rep = hps.fgmres(sk, sk.rhs(), pc, restart=p.restart, tol=p.tol, record_history=True,
                             reorthogonalize=reorth)
+        _, repo = S.solve(S.rhs(), True, restart=p.restart, tol=p.tol, record_history=True,
+                          reorth=reorth)
         assert rep["converged"]
-        assert 0.0 < rep["basis_orthogonality"] <= 1e-8, rep
+        if reorth:
+            assert 0.0 < rep["basis_orthogonality"] <= 1e-8, rep
+            assert repo["basis_orthogonality"] <= 1e-8
+        else:
+            assert 0.0 < rep["basis_orthogonality"] <= 10 * repo["basis_orthogonality"], (rep, repo)
         assert rep["precond_memory"] > 0 and rep["wall_build"] > 0
         assert rep["wall_solve"] == rep["seconds"] > 0
         assert len(rep["residual_history"]) == rep["iterations"]
-    S.precond(depth=3, gamma=1, coarse_iters=4)
-    _, repo = S.solve(S.rhs(), True, restart=p.restart, tol=p.tol, record_history=True)
-    assert repo["basis_orthogonality"] <= 1e-8
 
 
 @pytest.mark.parametrize("reorth", [True, False])
