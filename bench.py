@@ -169,6 +169,10 @@ def oracle_setup(config: int, seed: int, threads: int, n: int = 0, kappa: float 
     """Full setup as the reference driver times it (driver.cpp:41-51,138-171):
     elements + skeleton + hierarchy + preconditioner."""
     from oracle import pyoracle
+    # T / H only per element: the reference keeps each element's dense t x t
+    # operator and LU for the solution recovery (element.hpp:61-106), 160 GB
+    # at cfg3 -- not timed here, and beyond the host's memory
+    pyoracle.set_lean_elements(True)
     smp = pyoracle.sample(2, config=config, seed=seed, n=n)
     t0 = time.perf_counter()
     S = pyoracle.Session.from_sample(smp, kappa or KAPPA[config], threads=threads)

@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <tuple>
 
 #include "device.cuh"
@@ -291,8 +292,19 @@ cudaStream_t alloc_stream() {
   return c ? c->stream : nullptr;
 }
 
+// Pinned rings are recycled process-wide: cudaMallocHost of a 512 MB ring
+// costs ~0.1-0.5 s (page pinning) and cudaFreeHost synchronises the device,
+// so a context takes a ring from the pool at its first staged upload and
+// returns it when it is destroyed (its stream drained by then).
+namespace {
+std::mutex g_ring_mu;
+std::vector<std::pair<unsigned char*, size_t>> g_rings;
+}  // namespace
+
 Staging::~Staging() {
-  if (base) cudaFreeHost(base);
+  if (!base) return;
+  std::lock_guard<std::mutex> lk(g_ring_mu);
+  g_rings.emplace_back(base, size);
 }
 
 void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
@@ -302,19 +314,24 @@ void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     return;
   }
   Staging& st = c->staging;
+  if (!st.base) {
+    {
+      std::lock_guard<std::mutex> lk(g_ring_mu);
+      if (!g_rings.empty()) {
+        st.base = g_rings.back().first, st.size = g_rings.back().second;
+        g_rings.pop_back();
+      }
+    }
+    if (!st.base) {
+      HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.base), kStagingMax));
+      st.size = kStagingMax;
+    }
+    st.head = 0;
+  }
   const size_t need = (bytes + 255) & ~size_t(255);
   if (st.head + need > st.size) {
     HPSB_CUDA(cudaStreamSynchronize(s));  // all earlier staged copies have completed
     st.head = 0;
-    if (st.size < kStagingMax || need > st.size) {
-      size_t grow = std::max<size_t>(size_t(16) << 20, 2 * st.size);
-      while (grow < need) grow *= 2;
-      grow = std::min(grow, kStagingMax);
-      if (st.base) HPSB_CUDA(cudaFreeHost(st.base));
-      st.base = nullptr;
-      HPSB_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.base), grow));
-      st.size = grow;
-    }
   }
   std::memcpy(st.base + st.head, src, bytes);
   HPSB_CUDA(cudaMemcpyAsync(dst, st.base + st.head, bytes, cudaMemcpyHostToDevice, s));

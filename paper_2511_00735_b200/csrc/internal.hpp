@@ -78,13 +78,12 @@ struct ContextBind {
   ContextBind& operator=(const ContextBind&) = delete;
 };
 
-// Pinned staging ring for host->device descriptor uploads, one per context:
-// a cudaMemcpyAsync from pageable memory waits for the stream to drain, which
-// would serialise every batched launch of the merge stage with the host.
-// Uploads are copied into the ring and issued from pinned memory on the
-// context's stream; when the ring wraps, the stream is synchronised (every
-// earlier staged copy has landed) and the ring grows, up to kStagingMax, so
-// that one setup's uploads stop wrapping after the first.
+// Pinned staging ring for host->device descriptor uploads, one per context
+// (from a process-wide pool, gemv.cu): a cudaMemcpyAsync from pageable memory
+// waits for the stream to drain, which would serialise every batched launch
+// of the merge stage with the host.  Uploads are copied into the ring and
+// issued from pinned memory on the context's stream; when the ring wraps,
+// the stream is synchronised (every earlier staged copy has landed).
 struct Staging {
   unsigned char* base = nullptr;
   size_t size = 0, head = 0;
