@@ -630,7 +630,7 @@ hpsb_status hpsb_hierarchy_build(hpsb_skeleton sk, int depth, int factor_coarse,
     auto h = std::make_unique<hpsb_hierarchy_s>();
     auto* hs = h.get();
     h->h = hpsb::build_hierarchy(sk->s.get(), depth, [hs](hpsb::Hierarchy* hh) {
-      if (hh->depth < 2 || hh->ctx->profile || std::getenv("HPSB_NO_PENDING_PRECOND")) return;
+      if (hh->depth < 2 || hh->ctx->profile) return;
       hpsb_mg_config c{};
       c.depth = hh->depth, c.gamma = 1, c.coarse_iters = 4, c.exact_coarse = 0;
       hpsb::destroy_precond(hs->pending);  // a discarded first pass (pivot redo)

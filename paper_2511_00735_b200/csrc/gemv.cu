@@ -179,10 +179,7 @@ void VPlan::add_split(const VItem& it, int row_block) {
 void VPlan::finalize(cudaStream_t s) {
   // Stage a phase's operators in shared memory when every CTA's share fits
   // (default 96 KB: two CTAs per SM).
-  static const size_t limit = [] {
-    const char* e = std::getenv("HPSB_STAGE_KB");
-    return static_cast<size_t>(e ? std::atoi(e) : 96) * 1024;
-  }();
+  constexpr size_t limit = 96 * 1024;
   for (VPhase& ph : phases) {
     size_t worst = 0;
     for (int ui = ph.unit_begin; ui < ph.unit_begin + ph.unit_count; ++ui) {

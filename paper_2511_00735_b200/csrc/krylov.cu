@@ -386,16 +386,9 @@ __global__ void arn_copy_col_kernel(const double2* __restrict__ src, double2* ds
     dst[k] = src[k];
 }
 
-// Rows per thread cap of the multi-RHS CGS2 passes (HPSB_ORTH_RR overrides;
-// cfg4: 8 and 2 measured equal, 5.2-5.3 TB/s).
-int orth_rr_cap() {
-  static const int c = [] {
-    const char* e = std::getenv("HPSB_ORTH_RR");
-    const int v = e ? std::atoi(e) : kOrthMaxR;
-    return v >= 1 && v <= kOrthMaxR ? v : kOrthMaxR;
-  }();
-  return c;
-}
+// Rows per thread cap of the multi-RHS CGS2 passes (cfg4: 8 and 2 measured
+// equal, 5.2-5.3 TB/s).
+constexpr int orth_rr_cap() { return kOrthMaxR; }
 
 // Hessenberg column j from the CGS2 coefficients (h = h1 + h2, h_{j+1,j} =
 // ||w||), previous rotations, the new rotation, the residual estimate and the
@@ -531,11 +524,6 @@ struct Work {
     R = 1;
     while (R < 2 && (on + kOrthThreads * 2 * R - 1) / (kOrthThreads * 2 * R) >= 2 * ctx->num_sms)
       R *= 2;
-    static const int force_r = [] {
-      const char* e = std::getenv("HPSB_ORTH_R");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (force_r >= 1 && force_r <= kOrthMaxR) R = force_r;
     nb = static_cast<int>((on + kOrthThreads * R - 1) / (kOrthThreads * R));
   }
   void reserve(int maxcols) {  // partial sums for maxcols columns (before a graph capture)
@@ -950,7 +938,6 @@ hpsb_status fgmres_batch(Skeleton* sk, Precond* pc, const double2* rhs, double2*
   const double per_rhs = 16.0 * n * (2.0 * std::max(cfg.restart, 1) + 4.0);
   const double avail = 0.85 * static_cast<double>(available_device_bytes(sk->ctx->device));
   int G = std::max(1, std::min(R, static_cast<int>(avail / per_rhs)));
-  if (const char* e = std::getenv("HPSB_BATCH_GROUP")) G = std::max(1, std::min(R, std::atoi(e)));
   const int ngroups = (R + G - 1) / G;
   G = (R + ngroups - 1) / ngroups;  // balanced groups
   hpsb_status rc = HPSB_OK;

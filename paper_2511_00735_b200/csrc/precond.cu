@@ -66,14 +66,13 @@ struct Precond {
   VPlan exact_mv;
   // per-level execution order of the sweeps
   struct Step {
-    int level = 0, small = -1, cluster = -1, subtree = -1;
+    int level = 0, small = -1, cluster = -1;
     const VPlan* plan = nullptr;
     int p0 = 0, p1 = 0;
   };
   std::vector<Step> down_steps, up_steps;
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
-  std::vector<std::unique_ptr<SubtreeLevels>> subtrees;
   std::vector<int> small_level_of;  // level -> smalls index (-1: none)
   // fused-operator levels: per level, the folded down / up operators of every
   // merge, their index lists and the plan items that apply them
@@ -103,8 +102,7 @@ struct Precond {
   int64_t tail_off = 0;
   DevBuf<double2> xbuf, xsave;
   void run_step(const Step& st, bool down, double2* z) const {
-    if (st.subtree >= 0) subtrees[st.subtree]->run(ctx, down, r.p, z);
-    else if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
+    if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
     else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
     else
       for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
@@ -759,9 +757,8 @@ int split_rows(int total_rows, int sms) {
   // e.g. 4864 rows in 8-row units (608 units for 592 slots) ran as a full
   // wave plus 16 lone CTAs (ncu, cfg3 coarse matvec: 2.8 TB/s).  Take the
   // next row block when it fits one wave.
-  static const bool off = std::getenv("HPSB_NO_WAVE_FIT") != nullptr;
   const int slots = 4 * sms, units = (total_rows + rb - 1) / rb;
-  if (!off && units > slots && units < 2 * slots) {
+  if (units > slots && units < 2 * slots) {
     const int rb2 = rb < 16 ? 16 : std::min(256, (2 * rb + 31) & ~31);
     if ((total_rows + rb2 - 1) / rb2 <= slots) rb = rb2;
   }
@@ -989,7 +986,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   // in shared memory, else the work-list plan phases.
   auto small_level = [&](int l) -> int {
     const LevelOps& L = *h->levels[l - 1];
-    if (L.merges.empty() || std::getenv("HPSB_NO_SMALL_MERGE")) return -1;
+    if (L.merges.empty()) return -1;
     auto sl = std::make_unique<SmallLevel>();
     std::vector<SmallMerge> v;
     const int* ix = L.idx.p;
@@ -1014,7 +1011,6 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     }
     sl->level = l;
     sl->count = static_cast<int>(v.size());
-    sl->host = v;
     if (std::getenv("HPSB_PROFILE_LEVELS")) sl->label = "vcycle_small_L" + std::to_string(l);
     sl->d.upload(v, ctx->stream);
     p->smalls.push_back(std::move(sl));
@@ -1025,7 +1021,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   auto cluster_level = [&](int l) -> int {
     const LevelOps& L = *h->levels[l - 1];
     const int ng = static_cast<int>(L.merges.size());
-    if (!ng || std::getenv("HPSB_NO_CLUSTER_MERGE")) return -1;
+    if (!ng) return -1;
     // Only for latency-bound levels: few merges (>= 4 CTAs each within ~2
     // CTAs per SM) and a few MB of operators.  With many merges, one CTA per
     // SM holding a whole staged slice serialises load and compute, and the
@@ -1074,11 +1070,8 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   // A level step is then ONE launch of independent row blocks -- no chain of
   // dependent GEMVs, no barriers -- for up to ~1.7x the chain's operator
   // bytes.  Used where the level's folded operators are small (latency
-  // bound); HPSB_FUSED_MB sets the threshold (0 disables).
-  static const double fused_max = [] {
-    const char* e = std::getenv("HPSB_FUSED_MB");
-    return (e ? std::atof(e) : 24.0) * 1e6;
-  }();
+  // bound): folded operators of at most 24 MB per level.
+  constexpr double fused_max = 24e6;
   auto fused_level = [&](int l) -> int {
     const LevelOps& L = *h->levels[l - 1];
     if (L.merges.empty() || fused_max <= 0.0) return -1;
@@ -1202,65 +1195,6 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   };
   for (int l = 1; l < cfg.depth; ++l) add_step(l, true);
   for (int l = cfg.depth - 1; l >= 1; --l) add_step(l, false);
-  // Fuse the leading run of small-merge levels 1..k into one launch per
-  // direction (one CTA per level-k subtree), single GPU / V-cycle only.
-  {
-    int k = 0;
-    while (k + 1 < cfg.depth && small_of[k + 1] >= 0) ++k;
-    if (const char* e = std::getenv("HPSB_SUBTREE_LEVELS")) k = std::min(k, std::atoi(e));
-    else k = 0;  // opt-in: measured slower (sequential merges per CTA, see DESIGN)
-    if (k >= 2 && ctx->world() == 1 && cfg.gamma == 1) {
-      auto st = std::make_unique<SubtreeLevels>();
-      std::vector<SmallMerge> all;
-      std::vector<size_t> base(k + 1, 0);
-      for (int l = 1; l <= k; ++l) {
-        base[l] = all.size();
-        const SmallLevel& sl = *p->smalls[small_of[l]];
-        all.insert(all.end(), sl.host.begin(), sl.host.end());
-        st->smem = std::max(st->smem, sl.smem);
-        st->bytes_down += sl.bytes_down;
-        st->bytes_up += sl.bytes_up;
-      }
-      std::vector<int> order, seg{0};
-      const auto& topm = h->levels[k - 1]->merges;
-      for (size_t b = 0; b < topm.size(); ++b) {
-        std::vector<std::vector<int>> per(k + 1);
-        per[k].push_back(static_cast<int>(b));
-        for (int l = k; l >= 2; --l)
-          for (int mi : per[l]) {
-            const MergeRec& mr = h->levels[l - 1]->merges[mi];
-            if (mr.src1 < 0 || mr.src2 < 0) throw std::logic_error("subtree: missing child merge");
-            per[l - 1].push_back(mr.src1);
-            per[l - 1].push_back(mr.src2);
-          }
-        for (int l = 1; l <= k; ++l)
-          for (int mi : per[l]) order.push_back(static_cast<int>(base[l]) + mi);
-        seg.push_back(static_cast<int>(order.size()));
-      }
-      if (order.size() != all.size()) throw std::logic_error("subtree: merges not covered exactly once");
-      st->levels = k;
-      st->count = static_cast<int>(topm.size());
-      if (std::getenv("HPSB_PROFILE_LEVELS")) st->label = "vcycle_subtree_L1-" + std::to_string(k);
-      st->d.upload(all, ctx->stream);
-      st->order.upload(order, ctx->stream);
-      st->seg.upload(seg, ctx->stream);
-      p->subtrees.push_back(std::move(st));
-      const int si = static_cast<int>(p->subtrees.size()) - 1;
-      auto fuse = [&](std::vector<Precond::Step>& steps, bool front) {
-        std::vector<Precond::Step> kept;
-        for (const auto& s2 : steps)
-          if (s2.level > k) kept.push_back(s2);
-        Precond::Step f;
-        f.level = 1;
-        f.subtree = si;
-        if (front) kept.insert(kept.begin(), f);
-        else kept.push_back(f);
-        steps = std::move(kept);
-      };
-      fuse(p->down_steps, true);
-      fuse(p->up_steps, false);
-    }
-  }
   mark("steps");
   p->down.name = "vcycle_down";
   p->up.name = "vcycle_up";
@@ -1357,11 +1291,9 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     // their rows of the coarse maps in shared memory.  The largest cluster
     // wins: each CTA's staging burst is on the critical path when the
     // previous kernel's CTAs still occupy the SMs (cfg1: 16 CTAs 116 us per
-    // apply, 4 CTAs 149 us).  HPSB_COARSE_CSIZE forces a size.
+    // apply, 4 CTAs 149 us). 
     {
-      const char* force = std::getenv("HPSB_COARSE_CSIZE");
       for (int Cc = kCoarseMaxCluster; Cc >= 2 && !p->coarse_cluster; Cc /= 2) {
-        if (force && std::atoi(force) != Cc) continue;
         size_t stage = 0;
         for (const VItem& it : whole)
           stage += static_cast<size_t>(std::min(it.rows, cluster_chunk(it.rows, Cc))) * it.cols;
@@ -1376,7 +1308,6 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
                                                xs_total + stage) +
                             sizeof(int) * nidx;
         if (p->coarse_fused && smem <= (200u << 10) && slice <= kCoarseCThreads &&
-            !std::getenv("HPSB_NO_COARSE_CLUSTER") &&
             whole.size() <= static_cast<size_t>(kCoarseClusterItems) &&
             coarse_cluster_fits(smem, Cc)) {
           p->coarse_cluster = true;
@@ -1745,8 +1676,7 @@ void precond_apply_batch(Precond* p, const double2* v, double2* z, int R, bool d
   // vectors fit in shared memory, else the level's four GEMM phases
   auto small_fits = [&](int l) {
     const int si = p->small_level_of[l];
-    return si >= 0 && p->smalls[si]->batch_smem(R) <= (200u << 10) &&
-           !std::getenv("HPSB_NO_SMALL_BATCH");
+    return si >= 0 && p->smalls[si]->batch_smem(R) <= (200u << 10);
   };
   const int depth = p->cfg.depth;
   auto level = [&](int l, bool down) {

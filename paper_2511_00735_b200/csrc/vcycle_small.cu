@@ -131,25 +131,6 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
   small_step(M, down, r, out, smem_raw, red);
 }
 
-// Subtree-fused levels 1..k: CTA b runs every merge of the subtree under the
-// b-th level-k merge, in level order (down) or reversed (up).  Valid without
-// grid-wide barriers because every residual / correction entry a merge reads
-// is produced by merges of the same subtree or by earlier launches (the
-// slots on a face between two boxes belong to those two boxes only).
-__global__ void __launch_bounds__(kThreads) merge_subtree_kernel(const SmallMerge* __restrict__ ms,
-                                                                 const int* __restrict__ order,
-                                                                 const int* __restrict__ seg, int down,
-                                                                 double2* r, double2* out) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double2 red[kThreads];
-  const int b0 = seg[blockIdx.x], b1 = seg[blockIdx.x + 1];
-  for (int q = 0; q < b1 - b0; ++q) {
-    const int idx = down ? order[b0 + q] : order[b1 - 1 - q];
-    const SmallMerge M = ms[idx];
-    small_step(M, down, r, out, smem_raw, red);
-    __syncthreads();  // this merge's stores are visible to the next (same CTA)
-  }
-}
 
 // Multi-RHS variant: the same fused chain for R right-hand sides (vectors
 // with RHS stride ld); every GEMV becomes a small GEMM on shared memory,
@@ -278,15 +259,6 @@ void SmallLevel::run_batch(Context* ctx, bool down, double2* r, double2* out, in
            static_cast<const SmallMerge*>(d.p), down ? 1 : 0, r, out, R, ld);
 }
 
-void SubtreeLevels::run(Context* ctx, bool down, double2* r, double2* out) const {
-  if (!count) return;
-  allow_smem<merge_subtree_kernel>(smem);
-  KernelScope ks(ctx, label.empty() ? (down ? "vcycle_down" : "vcycle_up") : label.c_str(),
-                 down ? bytes_down : bytes_up, 0.0);
-  launch_k(ctx, merge_subtree_kernel, dim3(count), dim3(kThreads), smem, 1,
-           static_cast<const SmallMerge*>(d.p), static_cast<const int*>(order.p),
-           static_cast<const int*>(seg.p), down ? 1 : 0, r, out);
-}
 
 size_t small_merge_smem(int s, int p1, int p2) {
   const size_t P1 = p1 + s, P2 = p2 + s;

@@ -25,23 +25,9 @@ struct SmallLevel {
   double bytes_down = 0, bytes_up = 0;
   std::string label;
   DevBuf<SmallMerge> d;
-  std::vector<SmallMerge> host;  // the same list on the host (subtree fusion)
   void run(Context* ctx, bool down, double2* r, double2* out) const;
   // R right-hand sides, vectors with RHS stride ld
   void run_batch(Context* ctx, bool down, double2* r, double2* out, int R, int64_t ld) const;
-};
-
-// Levels 1..k of small merges fused: one CTA per level-k merge runs its whole
-// subtree (merge_subtree_kernel); order[seg[b]..seg[b+1]) lists CTA b's merges
-// (indices into d) in level order.
-struct SubtreeLevels {
-  int levels = 0, count = 0;
-  size_t smem = 0;
-  double bytes_down = 0, bytes_up = 0;
-  std::string label;
-  DevBuf<SmallMerge> d;
-  DevBuf<int> order, seg;
-  void run(Context* ctx, bool down, double2* r, double2* out) const;
 };
 
 // One thread-block cluster of `csize` CTAs per merge (csrc/vcycle_cluster.cu).

@@ -402,69 +402,6 @@ __global__ void __launch_bounds__(kPivThreads) panel_pivot_cluster_kernel(
   cl.sync();  // no CTA leaves while a peer may still write its shared memory
 }
 
-// ---- blocked Gauss-Jordan (large matrices), one panel of kb columns per step
-// Pivot rows for columns [k0, k0+kb): partial-pivoting LU of a copy of the
-// panel rows k0..n-1 (one CTA per matrix).  ipiv[k0+j] = row swapped with k0+j.
-__global__ void __launch_bounds__(1024) panel_pivot_kernel(const InvOp* __restrict__ ops, int k0,
-                                                           int kb, double2* panel_ws,
-                                                           int* ipiv_ws, int* status) {
-  const InvOp op = ops[blockIdx.x];
-  if (k0 >= op.n) return;
-  const int n = op.n, kw = min(kb, n - k0), rows = n - k0;
-  double2* P = panel_ws + op.perm_off * (size_t)kb;  // rows x kw, ld rows
-  int* ipiv = ipiv_ws + op.perm_off;
-  __shared__ double red_v[32];
-  __shared__ int red_i[32];
-  __shared__ int s_p;
-  for (int idx = threadIdx.x; idx < rows * kw; idx += blockDim.x) {
-    const int r = idx % rows, c = idx / rows;
-    P[idx] = op.A[(size_t)(k0 + r) + (size_t)(k0 + c) * op.lda];
-  }
-  __syncthreads();
-  for (int j = 0; j < kw; ++j) {
-    double best = -1.0;
-    int bi = j;
-    for (int i = j + threadIdx.x; i < rows; i += blockDim.x) {
-      const double v = cabs2(P[i + j * rows]);
-      if (v > best) best = v, bi = i;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
-    }
-    if ((threadIdx.x & 31) == 0) red_v[threadIdx.x >> 5] = best, red_i[threadIdx.x >> 5] = bi;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = -1.0;
-      int p = j;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
-        if (red_v[w] > b || (red_v[w] == b && red_i[w] < p)) b = red_v[w], p = red_i[w];
-      s_p = p;
-      ipiv[k0 + j] = k0 + p;
-      if (!(b > 0.0)) status[0] = op.tag + 1;
-    }
-    __syncthreads();
-    const int p = s_p;
-    if (p != j)
-      for (int c = threadIdx.x; c < kw; c += blockDim.x) {
-        const double2 t = P[j + c * rows];
-        P[j + c * rows] = P[p + c * rows];
-        P[p + c * rows] = t;
-      }
-    __syncthreads();
-    const double2 inv = cinv(P[j + j * rows]);
-    for (int i = j + 1 + threadIdx.x; i < rows; i += blockDim.x)
-      P[i + j * rows] = cmul(P[i + j * rows], inv);
-    __syncthreads();
-    const int rem = rows - j - 1, cw = kw - j - 1;
-    for (int idx = threadIdx.x; idx < rem * cw; idx += blockDim.x) {
-      const int i = j + 1 + idx % rem, c = j + 1 + idx / rem;
-      P[i + c * rows] = csub(P[i + c * rows], cmul(P[i + j * rows], P[j + c * rows]));
-    }
-    __syncthreads();
-  }
-}
 
 // Apply the panel's row swaps to every column of A (sequential swaps per column).
 __global__ void swap_rows_kernel(const InvOp* __restrict__ ops, int k0, int kb,
@@ -535,7 +472,7 @@ void GemmBatch::run(Context* ctx) {
     return true;
   }();
   (void)attr;
-  if (std::getenv("HPSB_TRACE_GEMM")) {  // executed (tile-padded) vs useful flops per launch
+  if (std::getenv("HPSB_TRACE")) {  // executed (tile-padded) vs useful flops per launch
     double padded = 0;
     for (const auto& d : descs) padded += 8.0 * d.tiles_m * BM * d.tiles_n * BN * (((d.K + BK - 1) / BK) * BK);
     static double tu = 0, tp = 0;
@@ -648,7 +585,7 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     // columns, choose pivot rows by a panel LU, swap them in, invert the
     // pivot block P = A_KK^{-1} and sweep the rest of the matrix with grouped
     // DMMA GEMMs:  U = P A_KR,  A_RR -= A_RK U,  A_RK = -A_RK P,  A_KR = U.
-    const int kb = std::getenv("HPSB_GJ_KB32") ? 32 : kPivMaxKb;
+    const int kb = kPivMaxKb;
     d_large.upload(large, ctx->stream);
     perm_ws.alloc(perm_total);
     int nmax = 0;
@@ -682,11 +619,6 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     for (int k0 = 0; k0 < nmax; k0 += kb) {
       if (!diag) {
         KernelScope ks(ctx, "zinverse_panel", 0.0, 0.0);
-        if (std::getenv("HPSB_GJ_PANEL_V1")) {
-          panel_pivot_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(
-              d_large.p, k0, kb, panel.p, perm_ws.p, status_dev);
-          HPSB_LAUNCHED(ctx);
-        } else {
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(static_cast<unsigned>(large.size() * csize));
           cfg.blockDim = dim3(kPivThreads);
@@ -702,7 +634,6 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
           HPSB_CUDA(cudaLaunchKernelEx(&cfg, panel_pivot_cluster_kernel, static_cast<const InvOp*>(d_large.p),
                                        k0, kb, chunk_max, perm_ws.p, status_dev));
           HPSB_LAUNCHED(ctx);
-        }
       }
       if (!diag) {
         KernelScope ks(ctx, "zinverse_swap", 0.0, 0.0);

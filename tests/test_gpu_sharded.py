@@ -145,11 +145,12 @@ def _run_ranks(world, fn):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_multi_rhs(world):
-    """cfg4's setting (plane-wave right-hand sides, s = 0) on a 16 x 16 mesh:
-    the lockstep multi-RHS FGMRES on distributed vectors (owner-computes top
-    merges, batched halo / coefficient allreduces) matches the single GPU."""
+    """cfg4's setting (plane-wave right-hand sides, s = 0) on a 16 x 16 mesh at
+    cfg4's kappa h (kappa = 600 * 16 / 256): the lockstep multi-RHS FGMRES on
+    distributed vectors (owner-computes top merges, batched global-row and
+    coefficient allreduces) matches the single GPU."""
     import paper_2511_00735_b200 as hps
-    prob = hps.problem(2, 4, n=16)
+    prob = hps.problem(2, 4, n=16, kappa=37.5)
     R = 4
     ctx = hps.Context(0)
     el = hps.build_elements(ctx, prob)
@@ -157,6 +158,7 @@ def test_sharded_multi_rhs(world):
     pc = hps.build_preconditioner(hps.build_hierarchy(sk, factor_coarse=False), coarse_iters=4)
     rhs = np.stack([sk.rhs(b) for b in range(R)])
     X0, reps0 = hps.fgmres_batch(sk, rhs, pc, restart=60, tol=1e-8)
+    assert all(r["converged"] for r in reps0)
     grp = hps.LocalGroup(world)
 
     def rank_run(rank):
