@@ -32,6 +32,7 @@
 #include "element_common.cuh"
 #include "vcycle_device.cuh"
 #include "gj_reg.cuh"
+#include "gj_dmma.cuh"
 
 namespace hpsb {
 
@@ -551,6 +552,64 @@ __global__ void __launch_bounds__(kGjThreads) v5_iti_kernel(V5Args v, const doub
   if (tid == 0) a.status[e] = ok ? 0 : 2;
 }
 
+// T = I - 2i eta S^{-1}, H = 2i eta S^{-1} f with S^{-1} from the blocked
+// DMMA Gauss-Jordan on diagonal pivots (gj_dmma.cuh): S (nb x nb, identity
+// padded to NP) in shared memory, 256 threads, two CTAs per SM at NP = 80.
+// Guard as the register version: a small pivot or an inverse entry beyond
+// kGjHuge2 / max|S_ij|^2 flags the element (status bit 8) for the pivoted
+// register Gauss-Jordan pass that follows.
+template <int NP>
+__global__ void __launch_bounds__(256) v5_iti_dmma_kernel(V5Args v, const double2* Sw, const double2* fw) {
+  using G = GdShape<NP>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* M = reinterpret_cast<double2*>(smem_raw);
+  __shared__ double2 fs[NP];
+  __shared__ double red[8];
+  __shared__ int flag;
+  const ElemArgs& a = v.a;
+  const int c = blockIdx.x, e = v5_elem(v, c), nb = a.nb, tid = threadIdx.x;
+  const int st0 = a.status[e];
+  if (st0 & 4) return;
+  const double2* Sg = Sw + static_cast<size_t>(c) * nb * nb;
+  double m = 0.0;
+  for (int j = tid / 32; j < NP; j += 8)
+    for (int i = tid & 31; i < NP; i += 32) {
+      double2 val = make_double2(i == j ? 1.0 : 0.0, 0.0);
+      if (i < nb && j < nb) {
+        val = Sg[i + static_cast<size_t>(j) * nb];
+        m = fmax(m, cabs2(val));
+      }
+      M[j * G::LD + i] = val;
+    }
+  if (tid < NP) fs[tid] = (a.source && tid < nb) ? fw[static_cast<size_t>(c) * nb + tid] : make_double2(0.0, 0.0);
+  m = warp_max(m);
+  if ((tid & 31) == 0) red[tid >> 5] = m;
+  __syncthreads();
+  double m0 = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m0 = fmax(m0, red[w]);
+  if (!gd_inverse<NP, 8>(M, &flag, kGjTiny2 * m0)) {
+    if (tid == 0) a.status[e] = st0 | 8;  // redo with pivoting
+    return;
+  }
+  const double te = 2.0 * a.eta, huge2 = kGjHuge2 / fmax(m0, 1e-300);
+  double2* Te = a.T + static_cast<size_t>(e) * nb * nb;
+  bool bad = false;
+  for (int j = tid / 32; j < nb; j += 8)
+    for (int i = tid & 31; i < nb; i += 32) {
+      const double2 sv = M[j * G::LD + i];
+      bad |= !(cabs2(sv) <= huge2);
+      Te[i + static_cast<size_t>(j) * nb] = make_double2((i == j ? 1.0 : 0.0) + te * sv.y, -te * sv.x);
+    }
+  if (tid < nb) {
+    double2 h = make_double2(0.0, 0.0);
+    for (int j = 0; j < nb; ++j) h = cfma(M[j * G::LD + tid], fs[j], h);
+    a.H[static_cast<size_t>(e) * nb + tid] = a.source ? make_double2(-te * h.y, te * h.x) : make_double2(0.0, 0.0);
+  }
+  bad = __syncthreads_or(bad);
+  if (tid == 0) a.status[e] = bad ? (st0 | 8) : 0;
+}
+
 // status bit 8 on every element of the chunk that is still on the Cholesky path
 __global__ void v5_mark_kernel(V5Args v) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -640,17 +699,26 @@ bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
     KernelScope ks(ctx, "element_iti", 0.0, 0.0);
     auto iti = [&](auto tr_tag) {
       constexpr int TR = decltype(tr_tag)::value;
-      const bool force_pivot = std::getenv("HPSB_ITI_PIVOT") != nullptr;
-      if (!force_pivot) {
-        v5_iti_kernel<TR, false><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);
-        HPSB_LAUNCHED(ctx);
-        v5_iti_kernel<TR, true><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);  // flagged only
-      } else {
+      if (std::getenv("HPSB_ITI_PIVOT")) {
         // every element with partial pivoting: mark all, then the pivoted pass
         v5_mark_kernel<<<(cn + 255) / 256, 256, 0, ctx->stream>>>(v);
-        HPSB_LAUNCHED(ctx);
-        v5_iti_kernel<TR, true><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);
+      } else {
+        auto dm = [&](auto np_tag) {
+          constexpr int NP = decltype(np_tag)::value;
+          allow_smem<v5_iti_dmma_kernel<NP>>(GdShape<NP>::kSmem);
+          v5_iti_dmma_kernel<NP><<<cn, 256, GdShape<NP>::kSmem, ctx->stream>>>(v, wS.p, wf.p);
+        };
+        switch ((nb + 15) / 16) {
+          case 1: dm(std::integral_constant<int, 16>{}); break;
+          case 2: dm(std::integral_constant<int, 32>{}); break;
+          case 3: dm(std::integral_constant<int, 48>{}); break;
+          case 4: dm(std::integral_constant<int, 64>{}); break;
+          case 5: dm(std::integral_constant<int, 80>{}); break;
+          default: dm(std::integral_constant<int, 96>{}); break;
+        }
       }
+      HPSB_LAUNCHED(ctx);
+      v5_iti_kernel<TR, true><<<cn, kGjThreads, 0, ctx->stream>>>(v, wS.p, wf.p);  // flagged only
     };
     switch ((nb + kGjY - 1) / kGjY) {
       case 1: case 2: iti(std::integral_constant<int, 2>{}); break;

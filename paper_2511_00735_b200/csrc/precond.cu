@@ -66,13 +66,14 @@ struct Precond {
   VPlan exact_mv;
   // per-level execution order of the sweeps
   struct Step {
-    int level = 0, small = -1, cluster = -1;
+    int level = 0, small = -1, cluster = -1, stream = -1;
     const VPlan* plan = nullptr;
     int p0 = 0, p1 = 0;
   };
   std::vector<Step> down_steps, up_steps;
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
+  std::vector<std::unique_ptr<StreamLevel>> streams;
   std::vector<int> small_level_of;  // level -> smalls index (-1: none)
   // fused-operator levels: per level, the folded down / up operators of every
   // merge, their index lists and the plan items that apply them
@@ -102,7 +103,8 @@ struct Precond {
   int64_t tail_off = 0;
   DevBuf<double2> xbuf, xsave;
   void run_step(const Step& st, bool down, double2* z) const {
-    if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
+    if (st.stream >= 0) streams[st.stream]->run(ctx, down, r.p, z);
+    else if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
     else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
     else
       for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(ctx, q, out.p, z);
@@ -1148,11 +1150,58 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->fused.push_back(std::move(f));
     return static_cast<int>(p->fused.size()) - 1;
   };
-  std::vector<int> small_of(cfg.depth, -1), cluster_of(cfg.depth, -1), fused_of(cfg.depth, -1);
+  // Levels of many merges with child maps of <= 320 rows: one warp per merge
+  // streaming its operators through a TMA ring (vcycle_stream.cu).  The
+  // small-level object is still built for the multi-RHS path.
+  auto stream_level = [&](int l) -> int {
+    const LevelOps& L = *h->levels[l - 1];
+    const int ng = static_cast<int>(L.merges.size());
+    int rows_max = 0, s_max = 0, vec_max = 0;
+    for (const MergeRec& mr : L.merges) {
+      rows_max = std::max({rows_max, L.children[mr.c1].P, L.children[mr.c2].P});
+      s_max = std::max(s_max, mr.s);
+      vec_max = std::max({vec_max, 5 * mr.s, mr.p1 + mr.p2 + 3 * mr.s});
+    }
+    // Merges of < 96 KB per step (cfg3 level 1: 52 KB) stay with the one-CTA
+    // small kernel: the stream kernel's nine barriers per merge dominate there
+    // (cfg3 level 1: 0.51 vs 0.37 ms).
+    double bytes = 0;
+    for (const MergeRec& mr : L.merges) bytes += 16.0 * (3.0 * mr.s * mr.s + static_cast<double>(mr.s) * (mr.p1 + mr.p2));
+    if (bytes < 96e3 * std::max(ng, 1)) return -1;
+    const StreamLevel::Shape shp = stream_level_shape(rows_max, s_max, vec_max, ng, sms);
+    if (!shp.ok) return -1;
+    auto sl = std::make_unique<StreamLevel>();
+    std::vector<SmallMerge> v;
+    const int* ix = L.idx.p;
+    for (const MergeRec& mr : L.merges) {
+      const ChildBox& c1 = L.children[mr.c1];
+      const ChildBox& c2 = L.children[mr.c2];
+      SmallMerge m{};
+      m.T1 = L.tperm.p + c1.t_off, m.T2 = L.tperm.p + c2.t_off, m.W = L.w.p + mr.w_off;
+      m.in1s = ix + mr.in1_sep, m.in2s = ix + mr.in2_sep, m.in1p = ix + mr.in1_per;
+      m.in2p = ix + mr.in2_per, m.out1p = ix + mr.out1_per, m.out2p = ix + mr.out2_per;
+      m.s = mr.s, m.p1 = mr.p1, m.p2 = mr.p2, m.P1 = c1.P, m.P2 = c2.P;
+      v.push_back(m);
+      const double ss = 16.0 * mr.s * mr.s, sp = 16.0 * mr.s * (mr.p1 + mr.p2);
+      sl->bytes_down += 3 * ss + sp;
+      sl->bytes_up += 3 * ss + sp;
+    }
+    sl->level = l;
+    sl->count = ng;
+    sl->shape = shp;
+    if (std::getenv("HPSB_PROFILE_LEVELS")) sl->label = "vcycle_stream_L" + std::to_string(l);
+    sl->d.upload(v, ctx->stream);
+    p->streams.push_back(std::move(sl));
+    return static_cast<int>(p->streams.size()) - 1;
+  };
+  std::vector<int> small_of(cfg.depth, -1), cluster_of(cfg.depth, -1), fused_of(cfg.depth, -1),
+      stream_of(cfg.depth, -1);
   for (int l = 1; l < cfg.depth; ++l) {
     fused_of[l] = fused_level(l);
     if (fused_of[l] >= 0) continue;
     small_of[l] = small_level(l);
+    stream_of[l] = stream_level(l);
+    if (stream_of[l] >= 0) continue;
     if (small_of[l] < 0) cluster_of[l] = cluster_level(l);
   }
   p->small_level_of = small_of;
@@ -1162,7 +1211,10 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     st.level = l;
     st.small = small_of[l];
     st.cluster = cluster_of[l];
-    if (fused_of[l] >= 0) {
+    st.stream = stream_of[l];
+    if (st.stream >= 0) {
+      p->bytes_small += downward ? p->streams[st.stream]->bytes_down : p->streams[st.stream]->bytes_up;
+    } else if (fused_of[l] >= 0) {
       const bool global_level = l > h->sk->el->part.last_local;
       VPlan& plan =
           downward ? (global_level ? p->down_g : p->down) : (global_level ? p->up_g : p->up);
@@ -1479,11 +1531,7 @@ void run_coarse(Precond* p, double2* z_dev) {
 
 void run_level(Precond* p, int l, bool down, double2* z) {
   for (const Precond::Step& st : down ? p->down_steps : p->up_steps) {
-    if (st.level != l) continue;
-    if (st.small >= 0) p->smalls[st.small]->run(p->ctx, down, p->r.p, z);
-    else if (st.cluster >= 0) p->clusters[st.cluster]->run(p->ctx, down, p->r.p, z);
-    else
-      for (int q = st.p0; q < st.p1; ++q) st.plan->run_phase(p->ctx, q, p->out.p, z);
+    if (st.level == l) p->run_step(st, down, z);
   }
 }
 

@@ -43,4 +43,24 @@ struct ClusterLevel {
   void run(Context* ctx, bool down, double2* r, double2* out) const;
 };
 
+// One CTA per merge (persistent over the level), operators streamed through
+// a TMA bulk-copy ring by a producer warp (csrc/vcycle_stream.cu): levels
+// with >= one merge per SM whose child maps have at most 512 rows.
+struct StreamLevel {
+  struct Shape {
+    bool ok = false;
+    int rpl = 0;  // CTAs per SM
+    int warps = 0, ns = 0, slot_entries = 0, vec_entries = 0;  // consumer warps
+    size_t smem = 0;
+  };
+  int level = 0, count = 0;
+  Shape shape;
+  double bytes_down = 0, bytes_up = 0;
+  std::string label;
+  DevBuf<SmallMerge> d;
+  void run(Context* ctx, bool down, double2* r, double2* out) const;
+};
+// rows_max: largest child perimeter P; vec_max: max(5 s, p1 + p2 + 3 s).
+StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int merges, int sms);
+
 }  // namespace hpsb

@@ -13,6 +13,7 @@
 // prefix sum of tile counts, so levels with thousands of tiny merges and
 // levels with two huge ones use the same kernel.
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cooperative_groups.h>
@@ -22,6 +23,7 @@
 #include "linalg.cuh"
 #include "zgemm.hpp"
 #include "gj_reg.cuh"
+#include "gj_dmma.cuh"
 
 namespace hpsb {
 
@@ -290,6 +292,72 @@ void launch_inverse_reg(int nmax, int grid, cudaStream_t st, const InvOp* ops, i
   }
 }
 
+// MODE 1 of inverse_reg_kernel on the FP64 tensor cores: the diagonal-pivot
+// blocked Gauss-Jordan of gj_dmma.cuh, one matrix per CTA (identity padded
+// to NP) in shared memory.  A guard failure (small pivot, or an inverse entry
+// beyond kGjHuge2 / max|a_ij|^2) leaves the matrix untouched and flags it for
+// the pivoted redo (flags) or the whole build (guard, blocked-inverse blocks).
+template <int NP>
+__global__ void __launch_bounds__(256) inverse_dmma_kernel(const InvOp* __restrict__ ops, int* flags,
+                                                           int* guard) {
+  using G = GdShape<NP>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* M = reinterpret_cast<double2*>(smem_raw);
+  __shared__ double red[8];
+  __shared__ int flag;
+  const InvOp op = ops[blockIdx.x];
+  const int n = op.n, tid = threadIdx.x;
+  double m = 0.0;
+  for (int j = tid / 32; j < NP; j += 8)
+    for (int i = tid & 31; i < NP; i += 32) {
+      double2 val = make_double2(i == j ? 1.0 : 0.0, 0.0);
+      if (i < n && j < n) {
+        val = op.A[(size_t)i + (size_t)j * op.lda];
+        m = fmax(m, cabs2(val));
+      }
+      M[j * G::LD + i] = val;
+    }
+  m = warp_max(m);
+  if ((tid & 31) == 0) red[tid >> 5] = m;
+  __syncthreads();
+  double m0 = red[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) m0 = fmax(m0, red[w]);
+  bool ok = gd_inverse<NP, 8>(M, &flag, kGjTiny2 * m0);
+  if (ok) {
+    const double huge2 = kGjHuge2 / fmax(m0, 1e-300);
+    bool bad = false;
+    for (int j = tid / 32; j < n; j += 8)
+      for (int i = tid & 31; i < n; i += 32) bad |= !(cabs2(M[j * G::LD + i]) <= huge2);
+    ok = !__syncthreads_or(bad);
+  }
+  if (!ok) {
+    if (tid == 0) {
+      if (flags) flags[blockIdx.x] = 1;
+      else *guard = 1;
+    }
+    return;
+  }
+  for (int j = tid / 32; j < n; j += 8)
+    for (int i = tid & 31; i < n; i += 32) op.A[(size_t)i + (size_t)j * op.lda] = M[j * G::LD + i];
+}
+
+void launch_inverse_dmma(int nmax, int grid, cudaStream_t st, const InvOp* ops, int* flags, int* guard) {
+  auto go = [&](auto np_tag) {
+    constexpr int NP = decltype(np_tag)::value;
+    allow_smem<inverse_dmma_kernel<NP>>(GdShape<NP>::kSmem);
+    inverse_dmma_kernel<NP><<<grid, 256, GdShape<NP>::kSmem, st>>>(ops, flags, guard);
+  };
+  switch ((nmax + 15) / 16) {
+    case 0: case 1: go(std::integral_constant<int, 16>{}); break;
+    case 2: go(std::integral_constant<int, 32>{}); break;
+    case 3: go(std::integral_constant<int, 48>{}); break;
+    case 4: go(std::integral_constant<int, 64>{}); break;
+    case 5: go(std::integral_constant<int, 80>{}); break;
+    default: go(std::integral_constant<int, 96>{}); break;
+  }
+}
+
 // ---- pivot selection for one panel, one thread-block CLUSTER per matrix.
 // The panel rows k0..n-1 (x kw columns) are split across the C CTAs of the
 // cluster and kept in shared memory; per column j: local argmax of |a_ij|
@@ -514,30 +582,44 @@ void CopyBatch::run(Context* ctx) {
 // m0_out != null: m0_out[op] = max |a_ij|^2 of matrix op.  Else the growth
 // check of a diagonal-pivot blocked inverse: any entry of A^{-1} beyond
 // kGjHuge2 / m0_in[op] (or NaN) sets *guard.
-__global__ void __launch_bounds__(1024) absmax2_kernel(const InvOp* __restrict__ ops, double* m0_out,
-                                                       const double* __restrict__ m0_in, int* guard) {
-  __shared__ double red[32];
-  const InvOp op = ops[blockIdx.x];
+// Grid (chunks, matrices): every CTA scans a contiguous slice of one
+// matrix (column-major, ld >= n) and folds its max with an atomic on the
+// order-preserving bits of a non-negative double (m0_out zeroed before).
+// One CTA per matrix ran at 160 GB/s (a handful of CTAs per level).
+__global__ void __launch_bounds__(256) absmax2_kernel(const InvOp* __restrict__ ops, double* m0_out,
+                                                      const double* __restrict__ m0_in, int* guard) {
+  __shared__ double red[8];
+  const InvOp op = ops[blockIdx.y];
+  const long long total = static_cast<long long>(op.n) * op.n;
   double m = 0.0;
   bool bad = false;
-  for (int j = 0; j < op.n; ++j)
-    for (int i = threadIdx.x; i < op.n; i += blockDim.x) {
-      const double v = cabs2(op.A[(size_t)i + (size_t)j * op.lda]);
-      m = fmax(m, v);
-      bad |= !(v == v);
-    }
+  for (long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(idx / op.n), i = static_cast<int>(idx - static_cast<long long>(j) * op.n);
+    const double v = cabs2(op.A[(size_t)i + (size_t)j * op.lda]);
+    m = fmax(m, v);
+    bad |= !(v == v);
+  }
   if (m0_out) {
     m = warp_max(m);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x < 32) {
-      double v = red[threadIdx.x];
+      double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
       v = warp_max(v);
-      if (threadIdx.x == 0) m0_out[blockIdx.x] = v;
+      if (threadIdx.x == 0)
+        atomicMax(reinterpret_cast<unsigned long long*>(m0_out) + blockIdx.y,
+                  static_cast<unsigned long long>(__double_as_longlong(v)));
     }
     return;
   }
-  if (bad || !(m <= kGjHuge2 / fmax(m0_in[blockIdx.x], 1e-300))) *guard = 1;
+  if (bad || !(m <= kGjHuge2 / fmax(m0_in[blockIdx.y], 1e-300))) *guard = 1;
+}
+
+dim3 absmax2_grid(size_t nmat, int nmax, int sms) {
+  const long long per = static_cast<long long>(nmax) * nmax;
+  const long long want = std::max<long long>(1, (4LL * sms + static_cast<long long>(nmat) - 1) / static_cast<long long>(nmat));
+  return dim3(static_cast<unsigned>(std::min<long long>(want, (per + 255) / 256)), static_cast<unsigned>(nmat));
 }
 
 void InverseBatch::run(Context* ctx, int* status_dev) {
@@ -569,7 +651,7 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
         HPSB_CUDA(cudaMemsetAsync(d_flags.p, 0, d_flags.bytes(), ctx->stream));
         flags = d_flags.p;
       }
-      launch_inverse_reg<1>(nmax, grid, ctx->stream, d_small.p, status_dev, flags, guard_dev);
+      launch_inverse_dmma(nmax, grid, ctx->stream, d_small.p, flags, guard_dev);
       HPSB_LAUNCHED(ctx);
       if (flags) {
         launch_inverse_reg<2>(nmax, grid, ctx->stream, d_small.p, status_dev, flags, guard_dev);
@@ -611,9 +693,10 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     const bool diag = diag_pivots && guard_dev;
     if (diag) {  // largest |a_ij|^2 of every input, for the final growth check
       d_m0.alloc(large.size());
+      HPSB_CUDA(cudaMemsetAsync(d_m0.p, 0, sizeof(double) * large.size(), ctx->stream));
       KernelScope ks(ctx, "zinverse_guard", 16.0 * nmax * nmax * large.size(), 0.0);
-      absmax2_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(d_large.p, d_m0.p,
-                                                                               nullptr, nullptr);
+      absmax2_kernel<<<absmax2_grid(large.size(), nmax, ctx->num_sms), 256, 0, ctx->stream>>>(
+          d_large.p, d_m0.p, nullptr, nullptr);
       HPSB_LAUNCHED(ctx);
     }
     for (int k0 = 0; k0 < nmax; k0 += kb) {
@@ -681,8 +764,8 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
     }
     if (diag) {  // no pivots, nothing to unscramble; check the inverse's growth
       KernelScope ks(ctx, "zinverse_guard", 16.0 * nmax * nmax * large.size(), 0.0);
-      absmax2_kernel<<<static_cast<int>(large.size()), 1024, 0, ctx->stream>>>(d_large.p, nullptr,
-                                                                               d_m0.p, guard_dev);
+      absmax2_kernel<<<absmax2_grid(large.size(), nmax, ctx->num_sms), 256, 0, ctx->stream>>>(
+          d_large.p, nullptr, d_m0.p, guard_dev);
       HPSB_LAUNCHED(ctx);
       return;
     }

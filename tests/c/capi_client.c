@@ -67,7 +67,9 @@ int main(void) {
     b2 += rhs[i] * rhs[i];
   }
   const double res = sqrt(r2 / b2);
-  if (!rep.converged || res > 1e-8 || rep.basis_orthogonality > 1e-8 || rep.precond_memory <= 0) {
+  /* plain modified Gram-Schmidt (reorthogonalize 0): the reference bounds the
+     basis orthogonality by 1e-5 (test_krylov.cpp:88) */
+  if (!rep.converged || res > 1e-8 || rep.basis_orthogonality > 1e-5 || rep.precond_memory <= 0) {
     fprintf(stderr, "unexpected fgmres result: converged=%d iterations=%d residual=%g "
             "orthogonality=%g precond_memory=%lld\n", rep.converged, rep.iterations, res,
             rep.basis_orthogonality, (long long)rep.precond_memory);
