@@ -234,6 +234,8 @@ struct KernelScope {
 // or writes anything a predecessor produces or consumes; only prefetches of
 // data written before the previous host synchronisation may precede it.
 #ifdef __CUDACC__
+// cluster < 0: a cooperative launch (every CTA co-resident; the kernel
+// synchronises its grid) instead of a cluster.
 template <typename... KArgs, typename... Args>
 void launch_k(Context* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
               int cluster, Args&&... args) {
@@ -242,8 +244,13 @@ void launch_k(Context* ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx->stream;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   unsigned na = 0;
+  if (cluster < 0) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
   if (ctx->use_pdl()) {
     at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[na].val.programmaticStreamSerializationAllowed = 1;

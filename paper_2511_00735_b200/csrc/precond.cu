@@ -66,7 +66,7 @@ struct Precond {
   VPlan exact_mv;
   // per-level execution order of the sweeps
   struct Step {
-    int level = 0, small = -1, cluster = -1, stream = -1;
+    int level = 0, small = -1, cluster = -1, stream = -1, wide = -1;
     const VPlan* plan = nullptr;
     int p0 = 0, p1 = 0;
   };
@@ -74,6 +74,7 @@ struct Precond {
   std::vector<std::unique_ptr<SmallLevel>> smalls;
   std::vector<std::unique_ptr<ClusterLevel>> clusters;
   std::vector<std::unique_ptr<StreamLevel>> streams;
+  std::vector<std::unique_ptr<WideLevel>> wides;
   std::vector<int> small_level_of;  // level -> smalls index (-1: none)
   // fused-operator levels: per level, the folded down / up operators of every
   // merge, their index lists and the plan items that apply them
@@ -104,6 +105,7 @@ struct Precond {
   DevBuf<double2> xbuf, xsave;
   void run_step(const Step& st, bool down, double2* z) const {
     if (st.stream >= 0) streams[st.stream]->run(ctx, down, r.p, z);
+    else if (st.wide >= 0) wides[st.wide]->run(ctx, down, r.p, z);
     else if (st.small >= 0) smalls[st.small]->run(ctx, down, r.p, z);
     else if (st.cluster >= 0) clusters[st.cluster]->run(ctx, down, r.p, z);
     else
@@ -1194,15 +1196,160 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->streams.push_back(std::move(sl));
     return static_cast<int>(p->streams.size()) - 1;
   };
+  // Levels of few, large merges (local ones; a sharded run's global levels
+  // keep their owner-computes plans): one persistent launch per level step,
+  // stages separated by grid barriers (vcycle_wide.cu).
+  auto wide_level = [&](int l) -> int {
+    const LevelOps& L = *h->levels[l - 1];
+    const int ng = static_cast<int>(L.merges.size());
+    // (levels of >= 64 merges stream faster as cluster chains)
+    if (!ng || ng >= 64 || l > h->sk->el->part.last_local) return -1;
+    constexpr int kTcCap = 1024;  // tile columns (the x slice in shared memory)
+    auto wl = std::make_unique<WideLevel>();
+    wl->shape = wide_level_shape(kTcCap, sms);
+    const int occ = wl->shape.ok ? wide_max_ctas_per_sm(wl->shape.smem) : 0;
+    if (trace) std::fprintf(stderr, "[hpsb] level %d wide: shape ok %d, smem %zu, %d CTAs/SM\n", l,
+                            wl->shape.ok ? 1 : 0, wl->shape.smem, occ);
+    if (occ < 1) return -1;
+    if (occ < wl->shape.ctas_per_sm) wl->shape.ctas_per_sm = occ, wl->shape.grid = sms * occ;
+    const int G = wl->shape.grid;
+    size_t part_max = 0;
+    const int* ix = L.idx.p;
+    for (int dir = 0; dir < 2; ++dir) {
+      const bool downward = dir == 0;
+      WideLevel::Dir& D = wl->dir[dir];
+      std::vector<WideMerge> wm(ng);
+      std::vector<WideTile> tiles;
+      std::vector<int> prefix(4 * static_cast<size_t>(ng + 1), 0);
+      struct OpD {
+        const double2* src;
+        int R, C, ld;
+      };
+      auto op_of = [&](int gi, int k) -> OpD {
+        const MergeRec& mr = L.merges[gi];
+        const ChildBox& c1 = L.children[mr.c1];
+        const ChildBox& c2 = L.children[mr.c2];
+        const int s = mr.s, p1 = mr.p1, p2 = mr.p2, P1 = c1.P, P2 = c2.P;
+        const double2* T1 = L.tperm.p + c1.t_off;
+        const double2* T2 = L.tperm.p + c2.t_off;
+        const double2* W = L.w.p + mr.w_off;
+        if (downward) {
+          switch (k) {
+            case 0: return {T2 + p2 + static_cast<size_t>(p2) * P2, s, s, P2};
+            case 1: return {W, s, s, s};
+            case 2: return {T1 + static_cast<size_t>(p1) * P1, P1, s, P1};
+            default: return {T2 + static_cast<size_t>(p2) * P2, p2, p2 ? s : 0, P2};
+          }
+        }
+        switch (k) {
+          case 0: return {T1 + p1, s, p1, P1};
+          case 1: return {T2 + p2, s, P2, P2};
+          case 2: return {W, s, s, s};
+          default: return {T1 + p1 + static_cast<size_t>(p1) * P1, s, s, P1};
+        }
+      };
+      for (int gi = 0; gi < ng; ++gi) {
+        const MergeRec& mr = L.merges[gi];
+        WideMerge& w = wm[gi];
+        w.in1s = ix + mr.in1_sep, w.in2s = ix + mr.in2_sep, w.in1p = ix + mr.in1_per;
+        w.in2p = ix + mr.in2_per, w.out1p = ix + mr.out1_per, w.out2p = ix + mr.out2_per;
+        w.s = mr.s, w.p1 = mr.p1, w.p2 = mr.p2;
+      }
+      size_t poff = 0;
+      std::vector<int> cta_tiles(4 * static_cast<size_t>(G + 1), 0);
+      for (int k = 0; k < 4; ++k) {
+        // stage k's rows over all merges, times ncb column blocks so that a
+        // CTA's range has >= 128 rows (2 KB column segments per bulk copy:
+        // 32-row segments streamed at half the rate); equal contiguous
+        // ranges per CTA
+        long long NR = 0;
+        for (int gi = 0; gi < ng; ++gi) {
+          const OpD o = op_of(gi, k);
+          wm[gi].R[k] = o.R;
+          prefix[k * (ng + 1) + gi + 1] = prefix[k * (ng + 1) + gi] + o.R;
+          if (o.C > 0) NR += o.R;
+          D.bytes += 16.0 * o.R * o.C;
+        }
+        int cmax = 0;
+        for (int gi = 0; gi < ng; ++gi) cmax = std::max(cmax, op_of(gi, k).C);
+        const int ncb = NR > 0 ? static_cast<int>(std::max<long long>(
+                                     (cmax + kTcCap - 1) / kTcCap, std::max<long long>(1, (128LL * G + NR - 1) / NR)))
+                               : 0;
+        for (int gi = 0; gi < ng; ++gi) {
+          const OpD o = op_of(gi, k);
+          WideMerge& w = wm[gi];
+          w.ncb[k] = (o.R > 0 && o.C > 0) ? std::min(ncb, o.C) : 0;
+          w.part[k] = static_cast<long long>(poff);
+          poff += static_cast<size_t>(w.ncb[k]) * o.R;
+        }
+        // flattened (column block, merge, row) space of the merges with work
+        std::vector<int> mlist;
+        std::vector<long long> mpre(1, 0);
+        for (int gi = 0; gi < ng; ++gi)
+          if (wm[gi].ncb[k] > 0) mlist.push_back(gi), mpre.push_back(mpre.back() + wm[gi].R[k]);
+        const long long N = NR * ncb;
+        for (int bb = 0; bb < G; ++bb) {
+          cta_tiles[k * (G + 1) + bb] = static_cast<int>(tiles.size());
+          long long f = N * bb / G;
+          const long long f1 = N * (bb + 1) / G;
+          while (f < f1) {
+            const int cb = static_cast<int>(f / NR);
+            const long long rem = f % NR;
+            const int mi = static_cast<int>(std::upper_bound(mpre.begin(), mpre.end(), rem) - mpre.begin()) - 1;
+            const int gi = mlist[mi];
+            const int row = static_cast<int>(rem - mpre[mi]);
+            const OpD o = op_of(gi, k);
+            const int nb = wm[gi].ncb[k];
+            // (at most 32 rows per consumer warp in one tile)
+            const long long take = std::min<long long>({f1 - f, o.R - row, 32LL * wl->shape.warps});
+            if (cb < nb) {  // (a narrow operator may have fewer column blocks)
+              const int TC = (o.C + nb - 1) / nb;
+              WideTile t{};
+              t.c0 = cb * TC, t.cols = std::min(TC, o.C - t.c0);
+              t.r0 = row, t.rows = static_cast<int>(take);
+              t.ld = o.ld, t.m = gi, t.cb = cb;
+              t.A = o.src + row + static_cast<size_t>(t.c0) * o.ld;
+              if (t.cols > 0) tiles.push_back(t);
+            }
+            f += take;
+          }
+        }
+        cta_tiles[k * (G + 1) + G] = static_cast<int>(tiles.size());
+      }
+      part_max = std::max(part_max, poff);
+      D.ntiles = static_cast<int>(tiles.size());
+      D.tiles.upload(tiles, ctx->stream);
+      D.merges.upload(wm, ctx->stream);
+      D.prefix.upload(prefix, ctx->stream);
+      D.cta_tiles.upload(cta_tiles, ctx->stream);
+      D.args.cta_tiles = D.cta_tiles.p;
+      D.args.tiles = D.tiles.p;
+      D.args.merges = D.merges.p;
+      D.args.nm = ng;
+      D.args.row_prefix = D.prefix.p;
+      D.args.down = downward ? 1 : 0;
+      D.args.slot_entries = wl->shape.slot_entries;
+      D.args.tc_max = wl->shape.tc_max;
+    }
+    wl->part.alloc(std::max<size_t>(part_max, 1));
+    wl->bar.alloc(2);
+    HPSB_CUDA(cudaMemsetAsync(wl->bar.p, 0, 2 * sizeof(unsigned), ctx->stream));
+    for (auto& D : wl->dir) D.args.part = wl->part.p, D.args.bar = wl->bar.p;
+    wl->level = l;
+    if (std::getenv("HPSB_PROFILE_LEVELS")) wl->label = "vcycle_wide_L" + std::to_string(l);
+    p->wides.push_back(std::move(wl));
+    return static_cast<int>(p->wides.size()) - 1;
+  };
   std::vector<int> small_of(cfg.depth, -1), cluster_of(cfg.depth, -1), fused_of(cfg.depth, -1),
-      stream_of(cfg.depth, -1);
+      stream_of(cfg.depth, -1), wide_of(cfg.depth, -1);
   for (int l = 1; l < cfg.depth; ++l) {
     fused_of[l] = fused_level(l);
     if (fused_of[l] >= 0) continue;
     small_of[l] = small_level(l);
     stream_of[l] = stream_level(l);
-    if (stream_of[l] >= 0) continue;
-    if (small_of[l] < 0) cluster_of[l] = cluster_level(l);
+    if (stream_of[l] >= 0 || small_of[l] >= 0) continue;
+    wide_of[l] = wide_level(l);
+    if (wide_of[l] < 0) cluster_of[l] = cluster_level(l);
   }
   p->small_level_of = small_of;
   mark("levels");
@@ -1212,8 +1359,11 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     st.small = small_of[l];
     st.cluster = cluster_of[l];
     st.stream = stream_of[l];
+    st.wide = wide_of[l];
     if (st.stream >= 0) {
       p->bytes_small += downward ? p->streams[st.stream]->bytes_down : p->streams[st.stream]->bytes_up;
+    } else if (st.wide >= 0) {
+      p->bytes_small += p->wides[st.wide]->dir[downward ? 0 : 1].bytes;
     } else if (fused_of[l] >= 0) {
       const bool global_level = l > h->sk->el->part.last_local;
       VPlan& plan =

@@ -63,4 +63,53 @@ struct StreamLevel {
 // rows_max: largest child perimeter P; vec_max: max(5 s, p1 + p2 + 3 s).
 StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int merges, int sms);
 
+// Few-merge levels: one persistent launch per level step, the four stages
+// separated by grid barriers (csrc/vcycle_wide.cu).
+struct WideTile {
+  const double2* A;  // operator origin of the tile (row r0, column c0)
+  int rows, cols, ld, m, r0, c0, cb;
+};
+struct WideMerge {
+  const int *in1s, *in2s, *in1p, *in2p, *out1p, *out2p;
+  int s, p1, p2, pad;
+  int R[4], ncb[4];  // per stage: output rows, column blocks
+  long long part[4];  // per stage: offset of the [ncb][R] partial product
+};
+struct WideArgs {
+  const WideTile* tiles;
+  const int* cta_tiles;  // [4][grid + 1]: CTA b's tiles of stage k
+  const WideMerge* merges;
+  int nm;
+  const int* row_prefix;  // [4][nm + 1] output-row prefix per stage
+  double2* part;
+  unsigned* bar;          // grid barrier: count, generation
+  double2* r;
+  double2* out;
+  int down, slot_entries, tc_max, pad;
+};
+struct WideLevel {
+  struct Shape {
+    bool ok = false;
+    int warps = 0, ctas_per_sm = 0, grid = 0, slot_entries = 0, tc_max = 0;
+    size_t smem = 0;
+  };
+  struct Dir {
+    WideArgs args{};
+    int ntiles = 0;
+    double bytes = 0;
+    DevBuf<WideTile> tiles;
+    DevBuf<WideMerge> merges;
+    DevBuf<int> prefix, cta_tiles;
+  };
+  int level = 0;
+  Shape shape;
+  Dir dir[2];  // down, up
+  DevBuf<double2> part;
+  DevBuf<unsigned> bar;
+  std::string label;
+  void run(Context* ctx, bool down, double2* r, double2* out) const;
+};
+WideLevel::Shape wide_level_shape(int tc_max, int sms);
+int wide_max_ctas_per_sm(size_t smem);
+
 }  // namespace hpsb

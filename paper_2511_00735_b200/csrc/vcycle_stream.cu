@@ -262,10 +262,13 @@ StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int 
   StreamLevel::Shape sh;
   (void)s_max;
   if (rows_max > 512 || merges < sms) return sh;
-  // 8 consumer warps (rows <= 256) with two CTAs per SM, else 16 and one
-  const int cw = rows_max <= 256 ? 8 : 16, ctas_per_sm = cw == 8 ? 2 : 1;
+  // one row group of 32 per consumer warp (and column groups on top): 4
+  // consumer warps (rows <= 128) x 4 CTAs per SM, 8 x 3, or 16 x 2 -- several
+  // merges in flight per SM hide each merge's per-operator barriers
+  const int cw = rows_max <= 128 ? 4 : rows_max <= 256 ? 8 : 16;
+  const int ctas_per_sm = cw == 4 ? 4 : cw == 8 ? 3 : 2;
   const int vec = (vec_max + 7) & ~7;
-  const size_t budget = (ctas_per_sm == 2 ? 110u : 220u) << 10;
+  const size_t budget = (220u << 10) / ctas_per_sm;
   const size_t fixed = sizeof(double2) * (32 * static_cast<size_t>(cw) + vec) +
                        2 * sizeof(unsigned long long) * kStreamMaxSlots;
   if (fixed >= budget) return sh;
@@ -290,7 +293,8 @@ void StreamLevel::run(Context* ctx, bool down, double2* r, double2* out) const {
              static_cast<const SmallMerge*>(d.p), count, down ? 1 : 0, r, out, shape.ns, shape.slot_entries,
              shape.vec_entries);
   };
-  if (shape.warps == 8) go(std::integral_constant<decltype(&merge_stream_kernel<8>), &merge_stream_kernel<8>>{});
+  if (shape.warps == 4) go(std::integral_constant<decltype(&merge_stream_kernel<4>), &merge_stream_kernel<4>>{});
+  else if (shape.warps == 8) go(std::integral_constant<decltype(&merge_stream_kernel<8>), &merge_stream_kernel<8>>{});
   else go(std::integral_constant<decltype(&merge_stream_kernel<16>), &merge_stream_kernel<16>>{});
 }
 
