@@ -1164,12 +1164,6 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       s_max = std::max(s_max, mr.s);
       vec_max = std::max({vec_max, 5 * mr.s, mr.p1 + mr.p2 + 3 * mr.s});
     }
-    // Merges of < 96 KB per step (cfg3 level 1: 52 KB) stay with the one-CTA
-    // small kernel: the stream kernel's nine barriers per merge dominate there
-    // (cfg3 level 1: 0.51 vs 0.37 ms).
-    double bytes = 0;
-    for (const MergeRec& mr : L.merges) bytes += 16.0 * (3.0 * mr.s * mr.s + static_cast<double>(mr.s) * (mr.p1 + mr.p2));
-    if (bytes < 96e3 * std::max(ng, 1)) return -1;
     const StreamLevel::Shape shp = stream_level_shape(rows_max, s_max, vec_max, ng, sms);
     if (!shp.ok) return -1;
     auto sl = std::make_unique<StreamLevel>();
