@@ -389,11 +389,15 @@ def run_b200(args, rank, world, local):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     roof["launches"] = d["launches"]
     # DRAM traffic per launch of the same kernel label from a committed ncu
-    # capture of this config (profiles/r01_traffic.json), when there is one
+    # capture of this config (profiles/r02_traffic.json, else r01), when there is one
     try:
-        tr = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)),
-                                         "profiles", "r01_traffic.json")))
-        ent = tr.get(f"cfg{args.config}", {})
+        ent = {}
+        for fn in ("r02_traffic.json", "r01_traffic.json"):
+            pth = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", fn)
+            if os.path.exists(pth):
+                ent = json.load(open(pth)).get(f"cfg{args.config}", {})
+                if name in ent:
+                    break
         if name in ent:
             roof["traffic"] = ent[name]
             roof["traffic_unit"] = "bytes per launch (DRAM read + write, ncu)"
