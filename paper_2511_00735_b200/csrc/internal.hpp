@@ -389,6 +389,7 @@ int* pinned_ints_acquire(size_t n, size_t* cap);  // recycled pinned host ints
 // Wait for the element stage and raise its per-element errors (mesh.cpp:82-84).
 void elements_wait(Elements* el);
 
+struct GemvStream;
 struct Skeleton {
   Context* ctx = nullptr;
   Elements* el = nullptr;
@@ -403,6 +404,7 @@ struct Skeleton {
   DevBuf<double2> tside;  // [nrhs][e][nb] physical-side impedance data
   VPlan apply_plan;      // y = x + sum_e scatter(T_e gather(x))
   DevBuf<double2> x_buf, y_buf;  // plan endpoints
+  std::shared_ptr<GemvStream> apply_stream;  // the same matvec, TMA-streamed (vcycle_stream.cu)
   std::shared_ptr<void> batch;   // multi-RHS matvec phase (skeleton.cu), built on first use
   // Sharded layout of the solver's vectors: every rank keeps full-length
   // buffers but owns only its subtree's local-face rows; the global rows

@@ -12,6 +12,7 @@
 
 #include "device.cuh"
 #include "internal.hpp"
+#include "vcycle_small.hpp"
 #include "zgemv_batch.hpp"
 
 namespace hpsb {
@@ -145,6 +146,25 @@ std::unique_ptr<Skeleton> build_skeleton(Elements* el, const double2* tside_host
   }
   sk->apply_plan.name = "skeleton_matvec";
   sk->apply_plan.finalize(ctx->stream);
+  {
+    // the same element GEMVs through the TMA-streamed kernel (the plan above
+    // stays for the multi-RHS path)
+    const GemvStream::Shape shp = gemv_stream_shape(nb, nb);
+    if (shp.ok) {
+      auto gs = std::make_shared<GemvStream>();
+      std::vector<GemvItem> items;
+      for (int e = 0; e < ne; ++e) {
+        if (sharded && !el->part.owns_elem(e)) continue;
+        items.push_back({el->T.p + static_cast<size_t>(e) * nb * nb, sk->d_in.p + static_cast<size_t>(e) * nb,
+                         sk->d_out.p + static_cast<size_t>(e) * nb, nb, nb});
+      }
+      gs->shape = shp;
+      gs->count = static_cast<int>(items.size());
+      gs->bytes = 16.0 * nb * nb * items.size();
+      gs->d.upload(items, ctx->stream);
+      sk->apply_stream = gs;
+    }
+  }
   if (sharded) {
     const Partition& part = el->part;
     sk->tail_off = static_cast<int64_t>(sk->graph.level_range[part.last_local].first) * sk->bs;
@@ -176,7 +196,8 @@ void skeleton_apply(const Skeleton* sk, const double2* x_dev, double2* y_dev, bo
   const int64_t z0 = distributed ? sk->tail_off : 0;
   if (sharded)
     HPSB_CUDA(cudaMemsetAsync(y_dev + z0, 0, (sk->dim - z0) * sizeof(double2), ctx->stream));
-  sk->apply_plan.run(ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
+  if (sk->apply_stream) sk->apply_stream->run(ctx, x_dev, y_dev);
+  else sk->apply_plan.run(ctx, sk->x_buf.p, const_cast<double2*>(x_dev), sk->y_buf.p, y_dev);
   if (sharded) ctx->comm->allreduce_sum(y_dev + z0, sk->dim - z0, ctx);
 }
 

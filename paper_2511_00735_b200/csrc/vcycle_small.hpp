@@ -63,6 +63,29 @@ struct StreamLevel {
 // rows_max: largest child perimeter P; vec_max: max(5 s, p1 + p2 + 3 s).
 StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int merges, int sms);
 
+// Independent streamed GEMVs y[yi] = x[yi] + A x[xi] (csrc/vcycle_stream.cu):
+// the interface matvec over the element maps.
+struct GemvItem {
+  const double2* A;  // rows x cols, contiguous column-major
+  const int* xi;     // [cols] (< 0: zero)
+  const int* yi;     // [rows] (< 0: no output)
+  int rows, cols;
+};
+struct GemvStream {
+  struct Shape {
+    bool ok = false;
+    int warps = 0, ctas_per_sm = 0, ns = 0, slot_entries = 0, xs_entries = 0;
+    size_t smem = 0;
+  };
+  Shape shape;
+  int count = 0;
+  double bytes = 0;
+  std::string label = "skeleton_matvec";
+  DevBuf<GemvItem> d;
+  void run(Context* ctx, const double2* x, double2* y) const;
+};
+GemvStream::Shape gemv_stream_shape(int rows_max, int cols_max);
+
 // Few-merge levels: one persistent launch per level step, the four stages
 // separated by grid barriers (csrc/vcycle_wide.cu).
 struct WideTile {

@@ -33,6 +33,7 @@
 
 #include "device.cuh"
 #include "hierarchy.hpp"
+#include "vcycle_device.cuh"
 #include "vcycle_small.hpp"
 
 namespace hpsb {
@@ -114,8 +115,8 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
   const int slot_stride = slot_entries + 32;
   double2* ring = reinterpret_cast<double2*>(smem_raw);
   double2* red = ring + static_cast<size_t>(ns) * slot_stride;  // [CW * 32]
-  double2* v = red + 32 * CW;                                    // vector scratch
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(v + vec_entries);
+  double2* vbuf = red + 32 * CW;  // two vector scratch areas (this merge / the next)
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(vbuf + 2 * vec_entries);
   unsigned long long* empty = full + kStreamMaxSlots;
   // No early launch_dependents: the dependents are scheduled when this grid
   // exits (an early trigger let them occupy the SMs while this persistent
@@ -157,26 +158,54 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
   }
 
   // ---- consumer warps
+  // A merge's input vector (down r1 | r2, up u1 | u2) is gathered during the
+  // previous merge: its indices are loaded at that merge's start and the
+  // gathers issued as cp.async after its first operator, so neither L2
+  // round trip sits on the chain.  (Same-level merges touch disjoint rows.)
   constexpr int NT = 32 * CW;
   pdl_wait();
+  const double2* src = down ? r : out;
+  auto in_ptrs = [&](const SmallMerge& X, const int*& i1, const int*& i2, int& n1, int& n2) {
+    if (down) i1 = X.in1s, i2 = X.in2s, n1 = X.s, n2 = X.s;
+    else i1 = X.in1p, i2 = X.in2p, n1 = X.p1, n2 = X.p2;
+  };
+  auto zero_b2 = [&](const SmallMerge& X, double2* vv) {  // up without T1_sp: b2 = 0
+    if (!down && X.p1 == 0)
+      for (int i = tid; i < X.s; i += NT) vv[X.p1 + X.p2 + i] = make_double2(0.0, 0.0);
+  };
+  if (blockIdx.x < count) {  // the first merge's inputs
+    const SmallMerge& X = ms[blockIdx.x];
+    const int *i1, *i2;
+    int n1, n2;
+    in_ptrs(X, i1, i2, n1, n2);
+    for (int i = tid; i < n1 + n2; i += NT) cp_async16(vbuf + i, src + (i < n1 ? i1[i] : i2[i - n1]));
+    cp_async_commit();
+    zero_b2(X, vbuf);
+  }
   unsigned q = 0;
-  for (int m = blockIdx.x; m < count; m += gridDim.x) {
+  int it = 0;
+  for (int m = blockIdx.x; m < count; m += gridDim.x, ++it) {
     const SmallMerge& M = ms[m];
     const int s = M.s, p1 = M.p1, p2 = M.p2;
-    if (down) {
-      const int *i1 = M.in1s, *i2 = M.in2s;
-      for (int i = tid; i < s; i += NT) {
-        v[i] = __ldcg(r + i1[i]);
-        v[s + i] = __ldcg(r + i2[i]);
-      }
-    } else {
-      const int *i1 = M.in1p, *i2 = M.in2p;
-      for (int i = tid; i < p1; i += NT) v[i] = __ldcg(out + i1[i]);
-      for (int i = tid; i < p2; i += NT) v[p1 + i] = __ldcg(out + i2[i]);
-      if (p1 == 0)  // no T1_sp: b2 = 0
-        for (int i = tid; i < s; i += NT) v[p1 + p2 + i] = make_double2(0.0, 0.0);
-    }
+    double2* v = vbuf + (it & 1) * vec_entries;
+    double2* vn = vbuf + ((it + 1) & 1) * vec_entries;
+    cp_async_wait_all();
     bar_consumers(NT);
+    // next merge: indices now (their loads overlap operator 0), gathers after it
+    const int mn = m + gridDim.x;
+    int pidx[2] = {-1, -1};
+    if (mn < count) {
+      const int *i1, *i2;
+      int n1, n2;
+      in_ptrs(ms[mn], i1, i2, n1, n2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = tid + e * NT;
+        if (i < n1 + n2) pidx[e] = i < n1 ? i1[i] : i2[i - n1];
+      }
+      for (int i = tid + 2 * NT; i < n1 + n2; i += NT)  // (beyond two per thread: issued now)
+        cp_async16(vn + i, src + (i < n1 ? i1[i] : i2[i - n1]));
+    }
     for (int k = 0; k < 4; ++k) {
       const Op op = merge_op(M, down, k);
       if (op.cols == 0) continue;
@@ -251,7 +280,122 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
           }
         }
       }
+      if (k == 0 || (k == 1 && pidx[0] != -2)) {  // after the first operator that ran
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (pidx[e] >= 0) cp_async16(vn + tid + e * NT, src + pidx[e]);
+        cp_async_commit();
+        if (mn < count) zero_b2(ms[mn], vn);
+        pidx[0] = pidx[1] = -2;
+      }
       bar_consumers(NT);
+    }
+    if (pidx[0] != -2) {  // (no operator ran)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (pidx[e] >= 0) cp_async16(vn + tid + e * NT, src + pidx[e]);
+      cp_async_commit();
+      if (mn < count) zero_b2(ms[mn], vn);
+    }
+  }
+}
+
+// Independent GEMVs y[yi] = x[yi] + A x[xi] (A contiguous rows x cols; an
+// index < 0 reads zero / skips the row) -- the interface matvec over the
+// element maps (block_matrix.cpp:23-31).  Persistent CTAs over the items, the
+// producer warp streams each A through the TMA ring (contiguous bulk copies),
+// the next item's gathered x is prefetched with cp.async while this item runs.
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(valid ? 16 : 0));
+}
+
+template <int CW>
+__global__ void __launch_bounds__(32 * (CW + 1)) gemv_stream_kernel(const GemvItem* __restrict__ items, int count,
+                                                                    const double2* x, double2* y, int ns,
+                                                                    int slot_entries, int xs_entries) {
+  constexpr int U = 2, NT = 32 * CW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int slot_stride = slot_entries + 32;
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  double2* red = ring + static_cast<size_t>(ns) * slot_stride;  // [CW * 32]
+  double2* xbuf = red + 32 * CW;                                 // [2][xs_entries]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(xbuf + 2 * xs_entries);
+  unsigned long long* empty = full + kStreamMaxSlots;
+  if (tid == 0) {
+    for (int q = 0; q < ns; ++q) mbar_init(full + q, 1), mbar_init(empty + q, CW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == CW) {  // producer: the operators are static (no PDL wait)
+    unsigned q = 0;
+    for (int t = blockIdx.x; t < count; t += gridDim.x) {
+      const GemvItem T = items[t];
+      const int ncp = max(1, slot_entries / T.rows);
+      for (int c0 = 0; c0 < T.cols; c0 += ncp, ++q) {
+        const int nc = min(ncp, T.cols - c0), slot = static_cast<int>(q % ns);
+        if (q >= static_cast<unsigned>(ns)) mbar_wait(empty + slot, (q / ns - 1) & 1u);
+        const unsigned bytes = static_cast<unsigned>(sizeof(double2) * T.rows * nc);
+        if (lane == 0) {
+          mbar_expect_tx(full + slot, bytes);
+          bulk_g2s(ring + static_cast<size_t>(slot) * slot_stride, T.A + static_cast<size_t>(c0) * T.rows, bytes,
+                   full + slot);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  pdl_wait();
+  auto prefetch = [&](int t, double2* xb) {
+    const GemvItem T = items[t];
+    for (int c = tid; c < T.cols; c += NT) {
+      const int i = T.xi[c];
+      cp_async16z(xb + c, x + (i >= 0 ? i : 0), i >= 0);
+    }
+    cp_async_commit();
+  };
+  if (blockIdx.x < count) prefetch(blockIdx.x, xbuf);
+  unsigned q = 0;
+  int it = 0;
+  for (int t = blockIdx.x; t < count; t += gridDim.x, ++it) {
+    const GemvItem T = items[t];
+    const double2* xs = xbuf + (it & 1) * xs_entries;
+    cp_async_wait_all();
+    bar_consumers(NT);
+    if (t + static_cast<int>(gridDim.x) < count) prefetch(t + gridDim.x, xbuf + ((it + 1) & 1) * xs_entries);
+    const int rows = T.rows, ncp = max(1, slot_entries / rows);
+    const int RG = (rows + 31) >> 5, CG = CW / RG;
+    const int rg = warp % RG, cg = warp / RG;
+    const bool active = cg < CG;
+    double2 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = make_double2(0.0, 0.0);
+    for (int c0 = 0; c0 < T.cols; c0 += ncp, ++q) {
+      const int nc = min(ncp, T.cols - c0), slot = static_cast<int>(q % ns);
+      mbar_wait(full + slot, (q / ns) & 1u);
+      if (active) {
+        const double2* A = ring + static_cast<size_t>(slot) * slot_stride + rg * 32 + lane;
+        const double2* xp = xs + c0;
+        int c = cg;
+        for (; c + (U - 1) * CG < nc; c += U * CG) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) acc[u] = cfma(A[(c + u * CG) * rows], xp[c + u * CG], acc[u]);
+        }
+        for (; c < nc; c += CG) acc[0] = cfma(A[c * rows], xp[c], acc[0]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
+    }
+    if (active) red[cg * (RG * 32) + rg * 32 + lane] = cadd(acc[0], acc[1]);
+    bar_consumers(NT);
+    for (int i = tid; i < rows; i += NT) {
+      const int o = T.yi[i];
+      if (o < 0) continue;
+      double2 v = red[i];
+      for (int g = 1; g < CG; ++g) v = cadd(v, red[g * (RG * 32) + i]);
+      __stcg(y + o, cadd(__ldcg(x + o), v));
     }
   }
 }
@@ -269,7 +413,7 @@ StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int 
   const int ctas_per_sm = cw == 4 ? 4 : cw == 8 ? 3 : 2;
   const int vec = (vec_max + 7) & ~7;
   const size_t budget = (220u << 10) / ctas_per_sm;
-  const size_t fixed = sizeof(double2) * (32 * static_cast<size_t>(cw) + vec) +
+  const size_t fixed = sizeof(double2) * (32 * static_cast<size_t>(cw) + 2 * static_cast<size_t>(vec)) +
                        2 * sizeof(unsigned long long) * kStreamMaxSlots;
   if (fixed >= budget) return sh;
   // ns slots of whole columns: 4 slots, each as large as the budget allows
@@ -296,6 +440,38 @@ void StreamLevel::run(Context* ctx, bool down, double2* r, double2* out) const {
   if (shape.warps == 4) go(std::integral_constant<decltype(&merge_stream_kernel<4>), &merge_stream_kernel<4>>{});
   else if (shape.warps == 8) go(std::integral_constant<decltype(&merge_stream_kernel<8>), &merge_stream_kernel<8>>{});
   else go(std::integral_constant<decltype(&merge_stream_kernel<16>), &merge_stream_kernel<16>>{});
+}
+
+}  // namespace hpsb
+
+namespace hpsb {
+
+GemvStream::Shape gemv_stream_shape(int rows_max, int cols_max) {
+  GemvStream::Shape sh;
+  if (rows_max > 256 || rows_max < 1) return sh;
+  sh.warps = 8;
+  sh.ctas_per_sm = 3;
+  const size_t budget = (220u << 10) / sh.ctas_per_sm;
+  const int xs = (cols_max + 7) & ~7;
+  const size_t fixed = sizeof(double2) * (32 * static_cast<size_t>(sh.warps) + 2 * static_cast<size_t>(xs)) +
+                       2 * sizeof(unsigned long long) * kStreamMaxSlots;
+  if (fixed >= budget) return sh;
+  sh.ns = 4;
+  sh.slot_entries = static_cast<int>((budget - fixed) / (sizeof(double2) * sh.ns)) - 32;
+  if (sh.slot_entries < rows_max) return sh;
+  sh.xs_entries = xs;
+  sh.smem = fixed + sizeof(double2) * sh.ns * (static_cast<size_t>(sh.slot_entries) + 32);
+  sh.ok = true;
+  return sh;
+}
+
+void GemvStream::run(Context* ctx, const double2* x, double2* y) const {
+  if (!count) return;
+  KernelScope ks(ctx, label.c_str(), bytes, 0.0);
+  const int ctas = std::max(1, std::min(ctx->num_sms * shape.ctas_per_sm, count));
+  allow_smem<gemv_stream_kernel<8>>(shape.smem);
+  launch_k(ctx, gemv_stream_kernel<8>, dim3(ctas), dim3(32 * (shape.warps + 1)), shape.smem, 1,
+           static_cast<const GemvItem*>(d.p), count, x, y, shape.ns, shape.slot_entries, shape.xs_entries);
 }
 
 }  // namespace hpsb
