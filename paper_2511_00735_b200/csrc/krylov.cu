@@ -17,6 +17,7 @@
 #include <complex>
 
 #include "device.cuh"
+#include "tma.cuh"
 #include "internal.hpp"
 #include "zgemv_batch.hpp"
 
@@ -239,6 +240,116 @@ __global__ void __launch_bounds__(kOrthThreads) orth_kernel(
     if (lane == 0) out[i] = s;
   }
   if (threadIdx.x == 0) *ticket = 0;  // ready for the next launch (stream-ordered)
+}
+
+// One CGS2 pass as orth_kernel (single right-hand side, full-length rows),
+// with V streamed by TMA bulk copies: a CTA owns kOsRows rows; a producer
+// warp copies each needed column's row segment (8 KB) into a ring of
+// shared-memory slots.  The update runs row-parallel (2 rows per thread, w in
+// registers); the dot products column-parallel (a warp per column, lanes
+// over the rows of w' kept in shared memory), so each column costs one warp
+// reduction instead of one per warp.  The dots re-stream the columns, which
+// the update just pulled through L2.  out: per-block partials (reduce_kernel).
+// (orth_kernel at cfg3: 148 registers, 19% occupancy, 32-40% of DRAM
+// bandwidth, long-scoreboard bound.)
+constexpr int kOsRows = 512, kOsWarps = 8, kOsSlots = 8;
+constexpr size_t kOsSmem = sizeof(double2) * (static_cast<size_t>(kOsSlots) * kOsRows + kOsRows) +
+                           2 * kOsSlots * sizeof(unsigned long long);
+template <bool kUpdate>
+__global__ void __launch_bounds__(32 * (kOsWarps + 1)) orth_stream_kernel(
+    const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd, int nupd, double2* w,
+    int64_t n, double2* partial, int vdot) {
+  constexpr int NT = 32 * kOsWarps;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  double2* wsm = ring + static_cast<size_t>(kOsSlots) * kOsRows;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(wsm + kOsRows);
+  unsigned long long* empty = full + kOsSlots;
+  __shared__ double2 hs[104];
+  __shared__ double nsum[kOsWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.x) * kOsRows;
+  const int rows = static_cast<int>(n - r0 < kOsRows ? n - r0 : kOsRows);
+  const int nu = kUpdate ? nupd : 0;
+  if (tid == 0) {
+    for (int q = 0; q < kOsSlots; ++q) tma_mbar_init(full + q, 1), tma_mbar_init(empty + q, kOsWarps);
+    tma_mbar_init_fence();
+  }
+  __syncthreads();
+  pdl_trigger();
+  if (warp == kOsWarps) {  // producer: update columns, then dot columns (V is static here)
+    if (lane == 0) {
+      const unsigned bytes = static_cast<unsigned>(sizeof(double2) * rows);
+      for (int q = 0; q < nu + ncols; ++q) {
+        const int slot = q % kOsSlots;
+        if (q >= kOsSlots) tma_wait(empty + slot, (q / kOsSlots - 1) & 1u);
+        const int col = q < nu ? q : vdot + (q - nu);
+        tma_expect_tx(full + slot, bytes);
+        tma_load(ring + static_cast<size_t>(slot) * kOsRows, V + static_cast<int64_t>(col) * ld + r0, bytes, full + slot);
+      }
+    }
+    return;
+  }
+  pdl_wait();
+  if (kUpdate)
+    for (int i = tid; i < nu; i += NT) hs[i] = h_upd[i];
+  double2 wr[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int rr = tid + e * NT;
+    wr[e] = rr < rows ? __ldcg(w + r0 + rr) : make_double2(0.0, 0.0);
+  }
+  named_bar(1, NT);  // hs
+  int q = 0;
+  if (kUpdate) {
+    for (; q < nu; ++q) {
+      const int slot = q % kOsSlots;
+      tma_wait(full + slot, (q / kOsSlots) & 1u);
+      const double2* col = ring + static_cast<size_t>(slot) * kOsRows;
+      const double2 h = hs[q];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) wr[e] = csub(wr[e], cmul(h, col[tid + e * NT]));
+      tma_release(empty + slot, lane);
+    }
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {  // (rows past the vector: stale slot entries, drop them)
+      const int rr = tid + e * NT;
+      if (rr < rows) __stcg(w + r0 + rr, wr[e]);
+      else wr[e] = make_double2(0.0, 0.0);
+    }
+  }
+  if (ncols == 0) {  // ||w||^2 partial
+    double a = cabs2(wr[0]) + cabs2(wr[1]);
+    a = warp_sum(a);
+    if (lane == 0) nsum[warp] = a;
+    named_bar(1, NT);
+    if (tid == 0) {
+      double t = 0.0;
+      for (int k = 0; k < kOsWarps; ++k) t += nsum[k];
+      partial[blockIdx.x] = make_double2(t, 0.0);
+    }
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < 2; ++e) wsm[tid + e * NT] = wr[e];  // rows >= rows hold zeros
+  named_bar(1, NT);
+  for (int i = 0; i < ncols; ++i, ++q) {
+    const int slot = q % kOsSlots;
+    tma_wait(full + slot, (q / kOsSlots) & 1u);
+    if ((i % kOsWarps) == warp) {
+      const double2* col = ring + static_cast<size_t>(slot) * kOsRows;
+      double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+      for (int rr = lane; rr < rows; rr += 64) {
+        acc = cfma_conj(col[rr], wsm[rr], acc);
+        if (rr + 32 < rows) acc2 = cfma_conj(col[rr + 32], wsm[rr + 32], acc2);
+      }
+      acc = cadd(acc, acc2);
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+      if (lane == 0) partial[static_cast<int64_t>(blockIdx.x) * ncols + i] = acc;
+    }
+    tma_release(empty + slot, lane);
+  }
 }
 
 // dst[b] = s[b] * src[b] for the R vectors of a block (strides ls / ld)
@@ -553,6 +664,21 @@ struct Work {
     if (static_cast<size_t>(nb) * nout > partial.n) partial.alloc(static_cast<size_t>(nb) * nout);
     KernelScope ks(ctx, "gmres_orth", 16.0 * n * (nout + nupd + (h_upd ? 2 : 1)),
                    8.0 * n * (ncols + nupd));
+    if (!jdev && !rows && !sharded() && n >= 64LL * kOsRows) {
+      const int nbs = static_cast<int>((n + kOsRows - 1) / kOsRows);
+      if (static_cast<size_t>(nbs) * nout > partial.n) partial.alloc(static_cast<size_t>(nbs) * nout);
+      allow_smem<orth_stream_kernel<true>>(kOsSmem);
+      allow_smem<orth_stream_kernel<false>>(kOsSmem);
+      if (h_upd)
+        launch_k(ctx, orth_stream_kernel<true>, dim3(nbs), dim3(32 * (kOsWarps + 1)), kOsSmem, 1, V, n, ncols,
+                 h_upd, nupd, w, n, partial.p, vdot);
+      else
+        launch_k(ctx, orth_stream_kernel<false>, dim3(nbs), dim3(32 * (kOsWarps + 1)), kOsSmem, 1, V, n, ncols,
+                 h_upd, nupd, w, n, partial.p, vdot);
+      launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1, static_cast<const double2*>(partial.p), nbs, nout,
+               out, static_cast<const int*>(nullptr));
+      return;
+    }
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb), dim3(kOrthThreads), 0, 1, V, n, ncols, h_upd, nupd,
                w, on, R, partial.p, out, ticket.p, fused ? 1 : 0, OrthStride{}, jdev, vdot, rows);

@@ -55,6 +55,7 @@ struct Precond {
   // fused coarse solve (one cluster launch)
   bool coarse_fused = false;
   bool coarse_cluster = false;  // on-chip variant (coarse_cluster_kernel)
+  std::unique_ptr<CoarseWide> coarse_wide;  // persistent grid variant (large coarse systems)
   int coarse_slice = 0;
   size_t coarse_smem = 0, coarse_stage = 0;
   int coarse_xs = 0;
@@ -1604,6 +1605,86 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->exact_mv.finalize(ctx->stream);
     p->coarse_fused = false;
   }
+  // Large coarse systems (the split-launch path): the whole gmres_fixed_steps
+  // as one persistent cooperative grid (vcycle_wide.cu).
+  if (!cfg.exact_coarse && !p->coarse_fused && !p->coarse_cluster && ci >= 1 && ci <= kCoarseWideMax &&
+      !C.children.empty()) {
+    auto cw = std::make_unique<CoarseWide>();
+    cw->shape = wide_level_shape(1024, sms);
+    const int occ = cw->shape.ok ? coarse_wide_max_ctas_per_sm(cw->shape.smem) : 0;
+    if (occ >= 1) {
+      if (occ < cw->shape.ctas_per_sm) cw->shape.ctas_per_sm = occ, cw->shape.grid = sms * occ;
+      const int G = cw->shape.grid, nb = static_cast<int>(C.children.size());
+      long long NR = 0;
+      int cmax = 0;
+      for (const ChildBox& c : C.children) NR += c.P, cmax = std::max(cmax, c.P);
+      const int ncb = static_cast<int>(std::max<long long>((cmax + 1023) / 1024, std::max<long long>(1, (128LL * G + NR - 1) / NR)));
+      std::vector<WideMerge> boxes(nb);
+      std::vector<long long> mpre(1, 0);
+      size_t poff = 0;
+      std::vector<int> inv_box(p->dim_d, -1), inv_row(p->dim_d, -1);
+      for (int k = 0; k < nb; ++k) {
+        const ChildBox& c = C.children[k];
+        WideMerge& w = boxes[k];
+        w.in1s = p->coarse_idx.p + in_at[k];
+        w.R[0] = c.P, w.ncb[0] = std::min(ncb, c.P), w.part[0] = static_cast<long long>(poff);
+        poff += static_cast<size_t>(w.ncb[0]) * c.P;
+        mpre.push_back(mpre.back() + c.P);
+        for (int r0 = 0; r0 < c.P; ++r0) {
+          const int o = lidx[out_at[k] + r0];
+          if (o < 0 || o >= p->dim_d || inv_box[o] >= 0) throw std::runtime_error("coarse map: bad output slot");
+          inv_box[o] = k, inv_row[o] = r0;
+        }
+      }
+      for (int64_t i = 0; i < p->dim_d; ++i)
+        if (inv_box[i] < 0) throw std::runtime_error("coarse map: slot without a box row");
+      std::vector<WideTile> tiles;
+      std::vector<int> cta(G + 1, 0);
+      const long long N = NR * ncb;
+      for (int bb = 0; bb < G; ++bb) {
+        cta[bb] = static_cast<int>(tiles.size());
+        long long f = N * bb / G;
+        const long long f1 = N * (bb + 1) / G;
+        while (f < f1) {
+          const int cb = static_cast<int>(f / NR);
+          const long long rem = f % NR;
+          const int k = static_cast<int>(std::upper_bound(mpre.begin(), mpre.end(), rem) - mpre.begin()) - 1;
+          const ChildBox& c = C.children[k];
+          const int row = static_cast<int>(rem - mpre[k]);
+          const long long take = std::min<long long>({f1 - f, c.P - row, 32LL * cw->shape.warps});
+          const int nbk = boxes[k].ncb[0];
+          if (cb < nbk) {
+            const int TC = (c.P + nbk - 1) / nbk;
+            WideTile t{};
+            t.c0 = cb * TC, t.cols = std::min(TC, c.P - t.c0);
+            t.r0 = row, t.rows = static_cast<int>(take);
+            t.ld = c.P, t.m = k, t.cb = cb;
+            t.A = C.tperm.p + c.t_off + row + static_cast<size_t>(t.c0) * c.P;
+            if (t.cols > 0) tiles.push_back(t);
+          }
+          f += take;
+        }
+      }
+      cta[G] = static_cast<int>(tiles.size());
+      cw->tiles.upload(tiles, ctx->stream);
+      cw->boxes.upload(boxes, ctx->stream);
+      cw->cta_tiles.upload(cta, ctx->stream);
+      cw->inv_box.upload(inv_box, ctx->stream);
+      cw->inv_row.upload(inv_row, ctx->stream);
+      cw->part.alloc(std::max<size_t>(poff, 1));
+      cw->pd.alloc(static_cast<size_t>(G) * (kCoarseWideMax + 1));
+      cw->pn.alloc(G);
+      cw->bar.alloc(2);
+      HPSB_CUDA(cudaMemsetAsync(cw->bar.p, 0, 2 * sizeof(unsigned), ctx->stream));
+      CoarseArgs& A = cw->args;
+      A.tiles = cw->tiles.p, A.cta_tiles = cw->cta_tiles.p, A.boxes = cw->boxes.p;
+      A.inv_box = cw->inv_box.p, A.inv_row = cw->inv_row.p, A.part = cw->part.p;
+      A.V = p->V.p, A.W = p->cw.p, A.pd = cw->pd.p, A.pn = cw->pn.p, A.bar = cw->bar.p;
+      A.n = p->dim_d, A.ci = ci, A.slot_entries = cw->shape.slot_entries, A.tc_max = cw->shape.tc_max;
+      cw->bytes = static_cast<double>(ci) * p->coarse_mv.bytes_per_run;
+      p->coarse_wide = std::move(cw);
+    }
+  }
   p->bytes_per_apply = static_cast<int64_t>(p->bytes_small) + p->down.bytes_per_run +
                        p->up.bytes_per_run + p->down_g.bytes_per_run +
                        p->up_g.bytes_per_run +
@@ -1629,6 +1710,8 @@ void run_coarse(Precond* p, double2* z_dev) {
   const int ci = p->cfg.coarse_iters;
   if (p->cfg.exact_coarse) {
     p->exact_mv.run(ctx, p->out.p, z_dev);
+  } else if (p->coarse_wide) {
+    p->coarse_wide->run(ctx, p->r.p + p->off_d, z_dev + p->off_d);
   } else if (p->coarse_cluster) {
     KernelScope ks(ctx, "coarse_fused", static_cast<double>(p->coarse_mv.bytes_per_run), 0.0);
     launch_k(ctx, coarse_cluster_kernel, dim3(p->coarse_csize), dim3(kCoarseCThreads),

@@ -133,6 +133,40 @@ struct WideLevel {
   void run(Context* ctx, bool down, double2* r, double2* out) const;
 };
 WideLevel::Shape wide_level_shape(int tc_max, int sms);
+
+// The coarse gmres_fixed_steps as one persistent cooperative launch
+// (csrc/vcycle_wide.cu); coarse_iters <= kCoarseWideMax.
+constexpr int kCoarseWideMax = 8;
+struct CoarseArgs {
+  const WideTile* tiles;  // matvec tiles of the coarse box maps (m = box)
+  const int* cta_tiles;   // [grid + 1]
+  const WideMerge* boxes; // in1s = box input indices, R[0] / ncb[0] / part[0]
+  const int* inv_box;     // coarse index -> (box, row of its map)
+  const int* inv_row;
+  double2* part;
+  double2* V;             // (ci + 1) x n; V_0 is the right-hand side
+  double2* W;             // n
+  double2* pd;            // [grid][kCoarseWideMax + 1] partial dots
+  double* pn;             // [grid] partial squared norms
+  unsigned* bar;
+  const double2* rhs;
+  double2* z;
+  int64_t n;
+  int ci, slot_entries, tc_max, pad;
+};
+struct CoarseWide {
+  WideLevel::Shape shape;
+  CoarseArgs args{};
+  double bytes = 0;
+  DevBuf<WideTile> tiles;
+  DevBuf<WideMerge> boxes;
+  DevBuf<int> cta_tiles, inv_box, inv_row;
+  DevBuf<double2> part, pd;
+  DevBuf<double> pn;
+  DevBuf<unsigned> bar;
+  void run(Context* ctx, const double2* rhs, double2* z) const;
+};
+int coarse_wide_max_ctas_per_sm(size_t smem);
 int wide_max_ctas_per_sm(size_t smem);
 
 }  // namespace hpsb

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
           for (; c < nc; c += CG) acc[0] = cfma(A[c * rows], xp[c], acc[0]);
         }
         __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the next TMA write
         if (lane == 0) mbar_arrive(empty + slot);
       }
       if (active) {
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) gemv_stream_kernel(const GemvIt
         for (; c < nc; c += CG) acc[0] = cfma(A[c * rows], xp[c], acc[0]);
       }
       __syncwarp();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the next TMA write
       if (lane == 0) mbar_arrive(empty + slot);
     }
     if (active) red[cg * (RG * 32) + rg * 32 + lane] = cadd(acc[0], acc[1]);

@@ -74,6 +74,28 @@ __device__ __forceinline__ void wbar_consumers(int nthreads) {
 
 constexpr int kWideSlots = 4;
 
+__device__ void make_givens_w(double2 a, double2 b, double& c, double2& s) {  // krylov.cpp:17-31
+  c = 1.0;
+  s = make_double2(0.0, 0.0);
+  const double na = hypot(a.x, a.y), nb = hypot(b.x, b.y);
+  if (nb == 0.0) return;
+  const double r = hypot(na, nb);
+  const double2 cb = make_double2(b.x, -b.y);
+  if (na == 0.0) {
+    c = 0.0;
+    s = make_double2(cb.x / nb, cb.y / nb);
+  } else {
+    c = na / r;
+    const double2 an = make_double2(a.x / na, a.y / na);
+    s = cmul(an, make_double2(cb.x / r, cb.y / r));
+  }
+}
+__device__ void apply_givens_w(double c, double2 s, double2& a, double2& b) {  // krylov.cpp:33-37
+  const double2 t = cadd(cscale(a, c), cmul(s, b));
+  b = cadd(cmul(make_double2(-s.x, s.y), a), cscale(b, c));
+  a = t;
+}
+
 // CTA b's tiles of stage k: [cta_tiles[k][b], cta_tiles[k][b + 1])
 __device__ __forceinline__ void stage_range(const WideArgs& a, int k, int b, int G, int& t0, int& t1) {
   const int* o = a.cta_tiles + k * (G + 1);
@@ -261,6 +283,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_wide_kernel(const __grid_
           for (; c < nc; c += CG) acc[0] = cfma(A[c * rows], xp[c], acc[0]);
         }
         __syncwarp();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the next TMA write
         if (lane == 0) wmbar_arrive(empty + slot);
       }
       if (active) {
@@ -280,6 +303,243 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_wide_kernel(const __grid_
   }
   grid_sync(a.bar, G, NT);
   stage_writes(a, 3, b, G, tid, NT);
+}
+
+// gmres_fixed_steps (krylov.cpp:194-201) on the coarse system
+// M_L = I + sum_boxes scatter(T_box) as ONE persistent cooperative launch:
+// per Arnoldi step the matvec tiles (the box maps, streamed by the producer
+// warp through the TMA ring -- ahead of the grid barriers, the maps are
+// static), a grid barrier, the projections (classical Gram-Schmidt, as the
+// other coarse kernels: the j + 1 dot products of a step reduce together),
+// a grid barrier, the update and partial norm, a grid barrier.  Every CTA
+// keeps the identical Hessenberg / Givens state (sums in a fixed order), so
+// no broadcast is needed.  V_0 is the right-hand side itself; V_k (k >= 1)
+// are stored unnormalised with their scale factors.
+__device__ __forceinline__ double grid_sum_fixed(const double* v, int n, double* sh) {
+  // every CTA sums the same n values in the same order (warp 0, then lane 0)
+  if (threadIdx.x < 32) {
+    double a = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) a += __ldcg(v + i);
+    a = warp_sum(a);
+    if (threadIdx.x == 0) *sh = a;
+  }
+  return 0.0;
+}
+
+template <int CW>
+__global__ void __launch_bounds__(32 * (CW + 1)) coarse_wide_kernel(const __grid_constant__ CoarseArgs a) {
+  constexpr int U = 2, NT = 32 * CW;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, b = blockIdx.x, ci = a.ci;
+  const int ns = kWideSlots, slot_stride = a.slot_entries + 32;
+  double2* ring = reinterpret_cast<double2*>(smem_raw);
+  double2* red = ring + static_cast<size_t>(ns) * slot_stride;  // [CW * 32]
+  double2* xs = red + 32 * CW;                                   // [tc_max]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(xs + a.tc_max);
+  unsigned long long* empty = full + kWideSlots;
+  __shared__ double2 Hs[kCoarseWideMax + 1][kCoarseWideMax];  // Hessenberg (rotated), column j
+  __shared__ double2 gs[kCoarseWideMax + 1], rs[kCoarseWideMax], hsum[kCoarseWideMax + 1];
+  __shared__ double rcs[kCoarseWideMax], sc[kCoarseWideMax + 1], dsh[2];
+  __shared__ double2 dpart[CW][kCoarseWideMax + 1];
+  if (tid == 0) {
+    for (int q = 0; q < ns; ++q) wmbar_init(full + q, 1), wmbar_init(empty + q, CW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int t0, t1;
+  t0 = a.cta_tiles[b], t1 = a.cta_tiles[b + 1];
+  if (warp == CW) {  // producer: the same tiles every step
+    unsigned q = 0;
+    for (int j = 0; j < ci; ++j)
+      for (int t = t0; t < t1; ++t) {
+        const WideTile T = a.tiles[t];
+        const int ncp = max(1, a.slot_entries / T.rows);
+        for (int c0 = 0; c0 < T.cols; c0 += ncp, ++q) {
+          const int nc = min(ncp, T.cols - c0), slot = static_cast<int>(q % ns);
+          if (q >= static_cast<unsigned>(ns)) wmbar_wait(empty + slot, (q / ns - 1) & 1u);
+          const unsigned cb = static_cast<unsigned>(sizeof(double2) * T.rows);
+          if (lane == 0) wmbar_expect_tx(full + slot, cb * nc);
+          __syncwarp();
+          double2* dst = ring + static_cast<size_t>(slot) * slot_stride;
+          const double2* src = T.A + static_cast<size_t>(c0) * T.ld;
+          for (int jj = lane; jj < nc; jj += 32)
+            wbulk_g2s(dst + static_cast<size_t>(jj) * T.rows, src + static_cast<size_t>(jj) * T.ld, cb, full + slot);
+        }
+      }
+    return;
+  }
+  pdl_wait();
+  const int64_t n = a.n;
+  const int64_t i0 = n * b / G, i1 = n * (b + 1) / G;  // this CTA's slice of the coarse vector
+  auto Vk = [&](int k) -> const double2* { return k == 0 ? a.rhs : a.V + static_cast<int64_t>(k) * n; };
+  auto block_red = [&](double v) -> double {  // consumer-block sum (fixed order)
+    v = warp_sum(v);
+    __shared__ double wsum[CW];
+    if (lane == 0) wsum[warp] = v;
+    wbar_consumers(NT);
+    double t = 0.0;
+    for (int w = 0; w < CW; ++w) t += wsum[w];
+    wbar_consumers(NT);
+    return t;
+  };
+  // ---- ||b||
+  {
+    double s2 = 0.0;
+    for (int64_t i = i0 + tid; i < i1; i += NT) s2 += cabs2(__ldcg(a.rhs + i));
+    s2 = block_red(s2);
+    if (tid == 0) a.pn[b] = s2;
+  }
+  grid_sync(a.bar, G, NT);
+  grid_sum_fixed(a.pn, G, dsh);
+  wbar_consumers(NT);
+  const double beta = sqrt(dsh[0]);
+  if (tid <= ci) gs[tid] = make_double2(tid == 0 ? beta : 0.0, 0.0);
+  if (tid == 0) sc[0] = beta > 0.0 ? 1.0 / beta : 0.0;
+  wbar_consumers(NT);
+  int ju = 0;
+  unsigned q = 0;
+  if (beta > 0.0) {
+    for (int j = 0; j < ci; ++j) {
+      const double2* Vj = Vk(j);
+      const double sj = sc[j];
+      // ---- matvec tiles: partial products of the box maps with x = s_j V_j
+      for (int t = t0; t < t1; ++t) {
+        const WideTile T = a.tiles[t];
+        const WideMerge& B = a.boxes[T.m];
+        for (int c = tid; c < T.cols; c += NT) {
+          const double2 v = __ldcg(Vj + B.in1s[T.c0 + c]);
+          xs[c] = make_double2(sj * v.x, sj * v.y);
+        }
+        wbar_consumers(NT);
+        const int rows = T.rows, ncp = max(1, a.slot_entries / rows);
+        const int RG = (rows + 31) >> 5, CG = CW / RG;
+        const int rg = warp % RG, cg = warp / RG;
+        const bool active = cg < CG;
+        double2 acc[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc[u] = make_double2(0.0, 0.0);
+        for (int c0 = 0; c0 < T.cols; c0 += ncp, ++q) {
+          const int nc = min(ncp, T.cols - c0), slot = static_cast<int>(q % ns);
+          wmbar_wait(full + slot, (q / ns) & 1u);
+          if (active) {
+            const double2* A = ring + static_cast<size_t>(slot) * slot_stride + rg * 32 + lane;
+            const double2* xp = xs + c0;
+            int c = cg;
+            for (; c + (U - 1) * CG < nc; c += U * CG) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) acc[u] = cfma(A[(c + u * CG) * rows], xp[c + u * CG], acc[u]);
+            }
+            for (; c < nc; c += CG) acc[0] = cfma(A[c * rows], xp[c], acc[0]);
+          }
+          __syncwarp();
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // reads before the next TMA write
+          if (lane == 0) wmbar_arrive(empty + slot);
+        }
+        if (active) red[cg * (RG * 32) + rg * 32 + lane] = cadd(acc[0], acc[1]);
+        wbar_consumers(NT);
+        double2* dst = a.part + B.part[0] + static_cast<size_t>(T.cb) * B.R[0] + T.r0;
+        for (int i = tid; i < rows; i += NT) {
+          double2 y = red[i];
+          for (int g = 1; g < CG; ++g) y = cadd(y, red[g * (RG * 32) + i]);
+          __stcg(dst + i, y);
+        }
+        wbar_consumers(NT);
+      }
+      grid_sync(a.bar, G, NT);
+      // ---- w = s_j V_j + sum of the partials (this CTA's slice), dots with V_0..V_j
+      double2 dk[kCoarseWideMax + 1];
+#pragma unroll
+      for (int k = 0; k <= kCoarseWideMax; ++k) dk[k] = make_double2(0.0, 0.0);
+      for (int64_t i = i0 + tid; i < i1; i += NT) {
+        const int bx = a.inv_box[i], row = a.inv_row[i];
+        const WideMerge& B = a.boxes[bx];
+        const double2* pp = a.part + B.part[0] + row;
+        double2 w = __ldcg(Vj + i);
+        w = make_double2(sj * w.x, sj * w.y);
+        for (int cb = 0; cb < B.ncb[0]; ++cb) w = cadd(w, __ldcg(pp + static_cast<size_t>(cb) * B.R[0]));
+        __stcg(a.W + i, w);
+#pragma unroll
+        for (int k = 0; k <= kCoarseWideMax; ++k)
+          if (k <= j) {
+            const double2 v = __ldcg(Vk(k) + i);
+            dk[k] = cfma_conj(make_double2(sc[k] * v.x, sc[k] * v.y), w, dk[k]);
+          }
+      }
+#pragma unroll
+      for (int k = 0; k <= kCoarseWideMax; ++k)
+        if (k <= j) {
+          double2 d = dk[k];
+          d.x = warp_sum(d.x), d.y = warp_sum(d.y);
+          if (lane == 0) dpart[warp][k] = d;
+        }
+      wbar_consumers(NT);
+      if (tid <= j) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int w = 0; w < CW; ++w) t = cadd(t, dpart[w][tid]);
+        a.pd[static_cast<int64_t>(b) * (kCoarseWideMax + 1) + tid] = t;
+      }
+      grid_sync(a.bar, G, NT);
+      // ---- h = sum of the dots (fixed order), w' = w - sum_k h_k v_k, ||w'||
+      if (warp <= j) {
+        double2 t = make_double2(0.0, 0.0);
+        for (int c = lane; c < G; c += 32) t = cadd(t, __ldcg(a.pd + static_cast<int64_t>(c) * (kCoarseWideMax + 1) + warp));
+        t.x = warp_sum(t.x), t.y = warp_sum(t.y);
+        if (lane == 0) hsum[warp] = t;
+      }
+      wbar_consumers(NT);
+      double s2 = 0.0;
+      double2* Vn = a.V + static_cast<int64_t>(j + 1) * n;
+      for (int64_t i = i0 + tid; i < i1; i += NT) {
+        double2 w = __ldcg(a.W + i);
+        for (int k = 0; k <= j; ++k) {
+          const double2 v = __ldcg(Vk(k) + i);
+          w = csub(w, cmul(hsum[k], make_double2(sc[k] * v.x, sc[k] * v.y)));
+        }
+        __stcg(Vn + i, w);
+        s2 += cabs2(w);
+      }
+      s2 = block_red(s2);
+      if (tid == 0) a.pn[b] = s2;
+      grid_sync(a.bar, G, NT);
+      grid_sum_fixed(a.pn, G, dsh);
+      wbar_consumers(NT);
+      const double hn = sqrt(dsh[0]);
+      if (tid == 0) {  // Hessenberg column j, previous rotations, new rotation (krylov.cpp:110-131)
+        for (int i = 0; i <= j; ++i) Hs[i][j] = hsum[i];
+        Hs[j + 1][j] = make_double2(hn, 0.0);
+        for (int i = 0; i < j; ++i) apply_givens_w(rcs[i], rs[i], Hs[i][j], Hs[i + 1][j]);
+        double cc;
+        double2 ss;
+        make_givens_w(Hs[j][j], Hs[j + 1][j], cc, ss);
+        rcs[j] = cc, rs[j] = ss;
+        apply_givens_w(cc, ss, Hs[j][j], Hs[j + 1][j]);
+        apply_givens_w(cc, ss, gs[j], gs[j + 1]);
+        sc[j + 1] = hn > 0.0 ? 1.0 / hn : 0.0;
+      }
+      wbar_consumers(NT);
+      ju = j + 1;
+      if (hn <= 1e-14 * beta) break;  // happy breakdown (identical in every CTA)
+    }
+  }
+  // ---- y = H^{-1} g, z = sum_k y_k v_k on this CTA's slice
+  __shared__ double2 ys[kCoarseWideMax];
+  if (tid == 0) {
+    for (int i = ju - 1; i >= 0; --i) {
+      double2 t = gs[i];
+      for (int k = i + 1; k < ju; ++k) t = csub(t, cmul(Hs[i][k], ys[k]));
+      ys[i] = cdiv(t, Hs[i][i]);
+    }
+  }
+  wbar_consumers(NT);
+  for (int64_t i = i0 + tid; i < i1; i += NT) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < ju; ++k) {
+      const double2 v = __ldcg(Vk(k) + i);
+      acc = cfma(ys[k], make_double2(sc[k] * v.x, sc[k] * v.y), acc);
+    }
+    a.z[i] = acc;
+  }
 }
 
 }  // namespace
@@ -318,6 +578,25 @@ int wide_max_ctas_per_sm(size_t smem) {
   int n = 0;
   allow_smem<merge_wide_kernel<8>>(smem);
   HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, merge_wide_kernel<8>, 32 * 9, smem));
+  return n;
+}
+
+}  // namespace hpsb
+
+namespace hpsb {
+
+void CoarseWide::run(Context* ctx, const double2* rhs, double2* z) const {
+  KernelScope ks(ctx, "coarse_wide", bytes, 0.0);
+  CoarseArgs a = args;
+  a.rhs = rhs, a.z = z;
+  allow_smem<coarse_wide_kernel<8>>(shape.smem);
+  launch_k(ctx, coarse_wide_kernel<8>, dim3(shape.grid), dim3(32 * (shape.warps + 1)), shape.smem, -1, a);
+}
+
+int coarse_wide_max_ctas_per_sm(size_t smem) {
+  int n = 0;
+  allow_smem<coarse_wide_kernel<8>>(smem);
+  HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, coarse_wide_kernel<8>, 32 * 9, smem));
   return n;
 }
 
