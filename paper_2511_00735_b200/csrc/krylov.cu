@@ -258,8 +258,13 @@ constexpr size_t kOsSmem = sizeof(double2) * (static_cast<size_t>(kOsSlots) * kO
 template <bool kUpdate>
 __global__ void __launch_bounds__(32 * (kOsWarps + 1)) orth_stream_kernel(
     const double2* __restrict__ V, int64_t ld, int ncols, const double2* __restrict__ h_upd, int nupd, double2* w,
-    int64_t n, double2* partial, int vdot) {
+    int64_t n, double2* partial, int vdot, OrthStride bs) {
   constexpr int NT = 32 * kOsWarps;
+  {  // multi-RHS: blockIdx.y selects the right-hand side
+    const int b = blockIdx.y;
+    V += b * bs.v, w += b * bs.w, partial += b * bs.p;
+    if (h_upd) h_upd += b * bs.h;
+  }
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* ring = reinterpret_cast<double2*>(smem_raw);
   double2* wsm = ring + static_cast<size_t>(kOsSlots) * kOsRows;
@@ -404,6 +409,26 @@ __global__ void reduce_kernel(const double2* __restrict__ partial, int nblocks, 
     __syncthreads();
   }
   if (threadIdx.x == 0) out[i] = sh[0];
+}
+
+// out[b * hstride + i] = sum_blk partial[b * pstride + blk * ncols + i]
+// (multi-RHS partials of orth_stream_kernel; fixed order: deterministic)
+__global__ void reduce_batch_kernel(const double2* __restrict__ partial, int64_t pstride, int nblocks, int ncols,
+                                    double2* out, int hstride) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double2 sh[256];
+  const int i = blockIdx.x, b = blockIdx.y;
+  partial += b * pstride;
+  double2 s = make_double2(0.0, 0.0);
+  for (int k = threadIdx.x; k < nblocks; k += blockDim.x) s = cadd(s, partial[static_cast<int64_t>(k) * ncols + i]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] = cadd(sh[threadIdx.x], sh[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[b * hstride + i] = sh[0];
 }
 
 // w[k] += sign * sum_i h[i] V[k, i]
@@ -671,10 +696,10 @@ struct Work {
       allow_smem<orth_stream_kernel<false>>(kOsSmem);
       if (h_upd)
         launch_k(ctx, orth_stream_kernel<true>, dim3(nbs), dim3(32 * (kOsWarps + 1)), kOsSmem, 1, V, n, ncols,
-                 h_upd, nupd, w, n, partial.p, vdot);
+                 h_upd, nupd, w, n, partial.p, vdot, OrthStride{});
       else
         launch_k(ctx, orth_stream_kernel<false>, dim3(nbs), dim3(32 * (kOsWarps + 1)), kOsSmem, 1, V, n, ncols,
-                 h_upd, nupd, w, n, partial.p, vdot);
+                 h_upd, nupd, w, n, partial.p, vdot, OrthStride{});
       launch_k(ctx, reduce_kernel, dim3(nout), dim3(256), 0, 1, static_cast<const double2*>(partial.p), nbs, nout,
                out, static_cast<const int*>(nullptr));
       return;
@@ -1118,6 +1143,22 @@ hpsb_status fgmres_group(Skeleton* sk, Precond* pc, const double2* rhs, double2*
     const int nout = ncols > 0 ? ncols : 1;
     KernelScope ks(ctx, "gmres_orth", 16.0 * n * R * (nout + nupd + (h_upd ? 2 : 1)),
                    8.0 * n * R * (ncols + nupd));
+    const int nbs = static_cast<int>((n + kOsRows - 1) / kOsRows);
+    if (!dist && n >= 64LL * kOsRows && static_cast<int64_t>(nbs) * nout <= pstride) {
+      // TMA-streamed pass (as the single-RHS driver), a batched reduction
+      allow_smem<orth_stream_kernel<true>>(kOsSmem);
+      allow_smem<orth_stream_kernel<false>>(kOsSmem);
+      st.p = pstride;
+      if (h_upd)
+        launch_k(ctx, orth_stream_kernel<true>, dim3(nbs, R), dim3(32 * (kOsWarps + 1)), kOsSmem, 1, Vb,
+                 static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n, partial.p, vdot, st);
+      else
+        launch_k(ctx, orth_stream_kernel<false>, dim3(nbs, R), dim3(32 * (kOsWarps + 1)), kOsSmem, 1, Vb,
+                 static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, n, partial.p, vdot, st);
+      launch_k(ctx, reduce_batch_kernel, dim3(nout, R), dim3(256), 0, 1, static_cast<const double2*>(partial.p),
+               pstride, nbs, nout, out, hs);
+      return;
+    }
     if (h_upd)
       launch_k(ctx, orth_kernel<true>, dim3(nb, R), dim3(kOrthThreads), 0, 1,
                Vb, static_cast<int64_t>(R) * n, ncols, h_upd, nupd, wv, on,
