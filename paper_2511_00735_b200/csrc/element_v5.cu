@@ -50,8 +50,6 @@ __host__ __device__ constexpr int v5_bstage(int NJ) {
   return 16 * NJ * LDK > V5K * LDM ? 16 * NJ * LDK : V5K * LDM;
 }
 __host__ __device__ constexpr int v5_tile_smem(int NJ) { return V5S * (V5STAGE + v5_bstage(NJ)); }  // doubles
-constexpr int V5_TILE_SMEM = v5_tile_smem(4);
-constexpr int LDD = V5B + 1;            // diagonal block stride in the panel kernel
 static_assert(V5STAGE >= V5K * LDM, "stage size");
 
 struct V5Args {

@@ -1165,6 +1165,13 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       s_max = std::max(s_max, mr.s);
       vec_max = std::max({vec_max, 5 * mr.s, mr.p1 + mr.p2 + 3 * mr.s});
     }
+    {
+      // merges of < 48 KB per step: the one-CTA small kernel (cfg2 level 1,
+      // 32 KB merges: solve 39.2 -> 38.7 ms)
+      double mb = 0;
+      for (const MergeRec& mr : L.merges) mb += 16.0 * (3.0 * mr.s * mr.s + static_cast<double>(mr.s) * (mr.p1 + mr.p2));
+      if (mb < 48e3 * ng) return -1;
+    }
     const StreamLevel::Shape shp = stream_level_shape(rows_max, s_max, vec_max, ng, sms);
     if (!shp.ok) return -1;
     auto sl = std::make_unique<StreamLevel>();
@@ -1197,8 +1204,15 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   auto wide_level = [&](int l) -> int {
     const LevelOps& L = *h->levels[l - 1];
     const int ng = static_cast<int>(L.merges.size());
-    // (levels of >= 64 merges stream faster as cluster chains)
+    // (levels of >= 64 merges stream faster as cluster chains; levels of
+    // < 150 MB per step are bound by the grid barriers: cfg2 levels 7-11,
+    // 37-88 MB, ran at 0.6-1.6 TB/s as wide levels)
     if (!ng || ng >= 64 || l > h->sk->el->part.last_local) return -1;
+    {
+      double lb = 0;
+      for (const MergeRec& mr : L.merges) lb += 16.0 * (3.0 * mr.s * mr.s + static_cast<double>(mr.s) * (mr.p1 + mr.p2));
+      if (lb < 150e6) return -1;
+    }
     constexpr int kTcCap = 1024;  // tile columns (the x slice in shared memory)
     auto wl = std::make_unique<WideLevel>();
     wl->shape = wide_level_shape(kTcCap, sms);
@@ -1605,9 +1619,11 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
     p->exact_mv.finalize(ctx->stream);
     p->coarse_fused = false;
   }
-  // Large coarse systems (the split-launch path): the whole gmres_fixed_steps
-  // as one persistent cooperative grid (vcycle_wide.cu).
-  if (!cfg.exact_coarse && !p->coarse_fused && !p->coarse_cluster && ci >= 1 && ci <= kCoarseWideMax &&
+  // Large coarse systems (>= 100 MB of box maps per matvec; the split-launch
+  // path otherwise): the whole gmres_fixed_steps as one persistent
+  // cooperative grid (vcycle_wide.cu).  (cfg3, 189 MB: solve -1%; cfg2,
+  // 30 MB: +5% -- the grid barriers dominate small coarse systems.)
+  if (!cfg.exact_coarse && !p->coarse_fused && !p->coarse_cluster && p->coarse_mv.bytes_per_run >= (100ll << 20) && ci >= 1 && ci <= kCoarseWideMax &&
       !C.children.empty()) {
     auto cw = std::make_unique<CoarseWide>();
     cw->shape = wide_level_shape(1024, sms);
