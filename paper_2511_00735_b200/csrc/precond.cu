@@ -118,6 +118,7 @@ struct Precond {
       if ((st.level > last_local) == global) run_step(st, down, z);
   }
   void run_global_sharded(bool down, double2* z);
+  void run_global_level(const Step& st, bool down, double2* z);
 };
 
 constexpr int kMaxCoarseIters = 30;    // fused / on-chip coarse kernels
@@ -840,9 +841,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   if (!cfg.exact_coarse && cfg.coarse_iters < 1)
     throw InvalidArgument("MgPreconditioner: coarse_iters must be >= 1");
   // multigrid.cpp:71: the exact coarse mode runs gamma = 1.  gamma > 1
-  // (W- / gamma-cycles) runs host-recursively on one GPU.
-  if (!cfg.exact_coarse && cfg.gamma > 1 && h->ctx->world() > 1)
-    throw InvalidArgument("MgPreconditioner: gamma > 1 is single-GPU");
+  // (W- / gamma-cycles) runs host-recursively (apply_level_gamma), sharded too.
   // A preconditioner shallower than the hierarchy uses levels 1..depth of it
   // (multigrid.cpp:13-16,24-26).  Sharded, the coarse level must be a global
   // one: the local levels hold this rank's boxes only.
@@ -1778,17 +1777,57 @@ void run_level(Precond* p, int l, bool down, double2* z) {
   }
 }
 
+// One level step of the gamma-cycle.  Sharded: a local level runs the rank's
+// own merges and, going down, sums the residual changes on the global rows
+// (each changed by at most one rank); a global level runs owner-computes with
+// the exchanges of run_global_sharded (its separator rows of z zeroed first:
+// the exchange sums them over the ranks and only the owner assigns them).
+void level_step(Precond* p, int l, bool down, double2* z) {
+  Context* ctx = p->ctx;
+  if (ctx->world() == 1) {
+    run_level(p, l, down, z);
+    return;
+  }
+  const int last_local = p->h->sk->el->part.last_local;
+  if (l > last_local) {
+    for (const Precond::Step& st : down ? p->down_steps : p->up_steps) {
+      if (st.level != l) continue;
+      if (down) {
+        const auto& g = p->h->sk->graph;
+        const int64_t s0 = static_cast<int64_t>(g.level_range[l - 1].first) * p->h->sk->bs;
+        const int64_t s1 = static_cast<int64_t>(g.level_range[l].first) * p->h->sk->bs;
+        HPSB_CUDA(cudaMemsetAsync(z + s0, 0, sizeof(double2) * (s1 - s0), ctx->stream));
+      }
+      p->run_global_level(st, down, z);
+    }
+    return;
+  }
+  if (!down) {
+    run_level(p, l, false, z);
+    return;
+  }
+  const int64_t t0 = p->tail_off, n = p->dim - t0;
+  if (p->xsave.n < static_cast<size_t>(n)) p->xsave.alloc(n);
+  zcopy(ctx, p->xsave.p, p->r.p + t0, n);
+  run_level(p, l, true, z);
+  exchange_deltas(ctx, p->xbuf, {{p->r.p + t0, p->xsave.p, n}});
+}
+
 // apply_level (multigrid.cpp:30-100) with gamma > 1: F and restriction at
 // level l (down step), gamma recursive coarse corrections with the level
 // system residual rc - M_{l+1} z in between, prolongation (up step).
+// Sharded: vectors valid on the rank's own rows and the (replicated) global
+// rows; M_{l+1} z below the coarse level sums the ranks' box rows on the
+// global rows (each produced by one box, i.e. one rank).
 void apply_level_gamma(Precond* p, int l, double2* z) {
   Context* ctx = p->ctx;
   if (l == p->cfg.depth) {
     run_coarse(p, z);
     return;
   }
-  run_level(p, l, true, z);
+  level_step(p, l, true, z);
   const Hierarchy* h = p->h;
+  const bool sharded = ctx->world() > 1;
   const int64_t off = static_cast<int64_t>(h->levels[l]->first_face) * h->sk->bs;  // level l+1 tail
   const int64_t len = p->dim - off;
   double2* rc = p->gam_rc.p + static_cast<size_t>(l) * p->dim;
@@ -1799,7 +1838,11 @@ void apply_level_gamma(Precond* p, int l, double2* z) {
   for (int step = 0; step < p->cfg.gamma; ++step) {
     if (step > 0) {
       // r = rc - M_{l+1} z on the tail
+      const bool split = sharded && l + 1 < p->cfg.depth;  // (the coarse boxes are on every rank)
+      const int64_t t0 = p->tail_off;
+      if (split) HPSB_CUDA(cudaMemsetAsync(p->gam_t.p + t0, 0, sizeof(double2) * (p->dim - t0), ctx->stream));
       p->level_mv[l + 1].run(ctx, p->gam_t.p, zacc, p->r.p, p->gam_t.p);
+      if (split) ctx->comm->allreduce_sum(p->gam_t.p + t0, p->dim - t0, ctx);
       launch_k(ctx, copy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p + off,
                static_cast<const double2*>(rc + off), len);
       launch_k(ctx, axpy_vec_kernel, dim3(blocks), dim3(256), 0, 1, p->r.p + off,
@@ -1811,7 +1854,7 @@ void apply_level_gamma(Precond* p, int l, double2* z) {
   }
   launch_k(ctx, copy_vec_kernel, dim3(blocks), dim3(256), 0, 1, z + off,
            static_cast<const double2*>(zacc + off), len);
-  run_level(p, l, false, z);
+  level_step(p, l, false, z);
 }
 }  // namespace
 
@@ -1825,29 +1868,31 @@ bool precond_graph_safe(const Precond* p) {
 // rows (assignments, down) or by increments (up) and r at their perimeter
 // rows, each row on exactly one rank, so one allreduce of the changes per
 // level makes every rank consistent again for the next level.
-void Precond::run_global_sharded(bool down, double2* z) {
+void Precond::run_global_level(const Step& st, bool down, double2* z) {
   const auto& g = h->sk->graph;
-  const int bs = h->sk->bs, last_local = h->sk->el->part.last_local;
+  const int bs = h->sk->bs;
   auto ff = [&](int l) { return static_cast<int64_t>(g.level_range[l - 1].first) * bs; };
-  const auto& steps = down ? down_steps : up_steps;
-  for (const Step& st : steps) {
-    const int l = st.level;
-    if (l <= last_local) continue;
-    const int64_t s0 = ff(l), s1 = ff(l + 1);  // level-l separator rows; rows above: [s1, dim)
-    if (down) {
-      // baseline of r above the level; out at the level's separators is 0
-      // on every rank (zeroed before the global sweep)
-      if (xsave.n < static_cast<size_t>(dim - s1)) xsave.alloc(dim - s1);
-      zcopy(ctx, xsave.p, r.p + s1, dim - s1);
-      run_step(st, true, z);
-      exchange_deltas(ctx, xbuf, {{z + s0, nullptr, s1 - s0}, {r.p + s1, xsave.p, dim - s1}});
-    } else {
-      if (xsave.n < static_cast<size_t>(s1 - s0)) xsave.alloc(s1 - s0);
-      zcopy(ctx, xsave.p, z + s0, s1 - s0);
-      run_step(st, false, z);
-      exchange_deltas(ctx, xbuf, {{z + s0, xsave.p, s1 - s0}});
-    }
+  const int l = st.level;
+  const int64_t s0 = ff(l), s1 = ff(l + 1);  // level-l separator rows; rows above: [s1, dim)
+  if (down) {
+    // baseline of r above the level; out at the level's separators is 0
+    // on every rank (zeroed before the global sweep)
+    if (xsave.n < static_cast<size_t>(dim - s1)) xsave.alloc(dim - s1);
+    zcopy(ctx, xsave.p, r.p + s1, dim - s1);
+    run_step(st, true, z);
+    exchange_deltas(ctx, xbuf, {{z + s0, nullptr, s1 - s0}, {r.p + s1, xsave.p, dim - s1}});
+  } else {
+    if (xsave.n < static_cast<size_t>(s1 - s0)) xsave.alloc(s1 - s0);
+    zcopy(ctx, xsave.p, z + s0, s1 - s0);
+    run_step(st, false, z);
+    exchange_deltas(ctx, xbuf, {{z + s0, xsave.p, s1 - s0}});
   }
+}
+
+void Precond::run_global_sharded(bool down, double2* z) {
+  const int last_local = h->sk->el->part.last_local;
+  for (const Step& st : down ? down_steps : up_steps)
+    if (st.level > last_local) run_global_level(st, down, z);
 }
 
 void precond_apply(Precond* p, const double2* v_dev, double2* z_dev, bool distributed) {
@@ -1856,6 +1901,7 @@ void precond_apply(Precond* p, const double2* v_dev, double2* z_dev, bool distri
   launch_k(ctx, copy_vec_kernel, dim3(vblocks), dim3(256), 0, 1, p->r.p, v_dev, p->dim);
   if (!p->cfg.exact_coarse && p->cfg.gamma > 1) {
     apply_level_gamma(p, 1, z_dev);
+    if (ctx->world() > 1 && !distributed) gather_distributed(p->h->sk, z_dev);
     return;
   }
   // `out` of the plans is bound to the caller's z: no copy-out.

@@ -206,3 +206,37 @@ def test_sharded_krylov_variants(world):
         assert abs(r1["iterations"] - rm["iterations"]) <= 1 and relf(x1, xm) < 1e-9
         assert r1["basis_orthogonality"] < 1e-5  # single MGS pass (oracle: ~1e-6 on cfg1)
         assert abs(r2["iterations"] - rr["iterations"]) <= 1 and relf(x2, xr) < 1e-9
+
+
+@pytest.mark.parametrize("world,gamma", [(2, 2), (4, 2), (4, 3)])
+def test_sharded_gamma_cycle(world, gamma):
+    """gamma-cycles (multigrid.cpp:66-80) on distributed vectors: the level
+    residuals rc - M_{l+1} z sum the ranks' box rows on the global rows, the
+    global levels run owner-computes; MG(v) and the FGMRES solve match the
+    single GPU."""
+    import paper_2511_00735_b200 as hps
+    prob = hps.problem(2, 1)
+    rng = np.random.default_rng(7)
+    dim = 2 * (2 * prob.n * (prob.n - 1)) * (prob.order - 1)
+    v = rng.standard_normal(dim) + 1j * rng.standard_normal(dim)
+    ctx = hps.Context(0)
+    el = hps.build_elements(ctx, prob)
+    sk = hps.assemble_skeleton(el, prob)
+    pc = hps.build_preconditioner(hps.build_hierarchy(sk, factor_coarse=False), gamma=gamma, coarse_iters=2)
+    z0 = pc.apply(v)
+    x0, r0 = hps.fgmres(sk, sk.rhs(), pc, restart=50, tol=1e-10)
+    assert r0["converged"]
+    grp = hps.LocalGroup(world)
+
+    def rank_run(rank):
+        c = hps.Context(0)
+        c.attach_local(grp, rank)
+        e = hps.build_elements(c, prob)
+        s = hps.assemble_skeleton(e, prob)
+        p = hps.build_preconditioner(hps.build_hierarchy(s, factor_coarse=False), gamma=gamma, coarse_iters=2)
+        return p.apply(v), hps.fgmres(s, s.rhs(), p, restart=50, tol=1e-10)
+
+    for z, (x, r) in _run_ranks(world, rank_run):
+        assert relf(z, z0) < 1e-10
+        assert r["converged"] and abs(r["iterations"] - r0["iterations"]) <= 1
+        assert relf(x, x0) < 1e-9
