@@ -537,15 +537,6 @@ __global__ void copy_vec_kernel(double2* y, const double2* __restrict__ x, int64
     y[k] = x[k];
 }
 
-// zero the face blocks this rank does not contribute
-__global__ void mask_faces_kernel(double2* z, const int* __restrict__ keep, int bs) {
-  pdl_trigger();
-  pdl_wait();
-  if (keep[blockIdx.x]) return;
-  for (int k = threadIdx.x; k < bs; k += blockDim.x)
-    z[static_cast<int64_t>(blockIdx.x) * bs + k] = make_double2(0.0, 0.0);
-}
-
 // state: [0] bnorm, [1] done, [2] jused, [3] zero-rhs
 // Multi-RHS: CTA b works on right-hand side b (rd / outd stride ldr, the
 // Krylov state of each RHS packed behind the previous one's).
