@@ -1149,11 +1149,11 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
   auto stream_level = [&](int l) -> int {
     const LevelOps& L = *h->levels[l - 1];
     const int ng = static_cast<int>(L.merges.size());
-    int rows_max = 0, s_max = 0, vec_max = 0;
+    int rows_max = 0, vec_in = 0, vec_all = 0;
     for (const MergeRec& mr : L.merges) {
       rows_max = std::max({rows_max, L.children[mr.c1].P, L.children[mr.c2].P});
-      s_max = std::max(s_max, mr.s);
-      vec_max = std::max({vec_max, 5 * mr.s, mr.p1 + mr.p2 + 3 * mr.s});
+      vec_in = std::max({vec_in, 5 * mr.s, mr.p1 + mr.p2 + 3 * mr.s});
+      vec_all = std::max(vec_all, 5 * mr.s + mr.p1 + mr.p2);  // with the output bases
     }
     {
       // merges of < 48 KB per step: the one-CTA small kernel (cfg2 level 1,
@@ -1162,7 +1162,7 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       for (const MergeRec& mr : L.merges) mb += 16.0 * (3.0 * mr.s * mr.s + static_cast<double>(mr.s) * (mr.p1 + mr.p2));
       if (mb < 48e3 * ng) return -1;
     }
-    const StreamLevel::Shape shp = stream_level_shape(rows_max, s_max, vec_max, ng, sms);
+    const StreamLevel::Shape shp = stream_level_shape(rows_max, vec_in, vec_all, ng, sms);
     if (!shp.ok) return -1;
     auto sl = std::make_unique<StreamLevel>();
     std::vector<SmallMerge> v;

@@ -50,6 +50,7 @@ struct StreamLevel {
   struct Shape {
     bool ok = false;
     int rpl = 0;  // CTAs per SM
+    bool pre_out = false;  // prefetch the epilogue's output bases with the inputs
     int warps = 0, ns = 0, slot_entries = 0, vec_entries = 0;  // consumer warps
     size_t smem = 0;
   };
@@ -60,8 +61,9 @@ struct StreamLevel {
   DevBuf<SmallMerge> d;
   void run(Context* ctx, bool down, double2* r, double2* out) const;
 };
-// rows_max: largest child perimeter P; vec_max: max(5 s, p1 + p2 + 3 s).
-StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int merges, int sms);
+// rows_max: largest child perimeter P; vec_in: max(5 s, p1 + p2 + 3 s) (the vector
+// scratch), vec_all: 5 s + p1 + p2 (with the epilogue's output bases).
+StreamLevel::Shape stream_level_shape(int rows_max, int vec_in, int vec_all, int merges, int sms);
 
 // Independent streamed GEMVs y[yi] = x[yi] + A x[xi] (csrc/vcycle_stream.cu):
 // the interface matvec over the element maps.

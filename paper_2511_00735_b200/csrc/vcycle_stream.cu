@@ -108,7 +108,7 @@ constexpr int kStreamMaxSlots = 8;
 template <int CW>
 __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const SmallMerge* __restrict__ ms, int count,
                                                                      int down, double2* r, double2* out, int ns,
-                                                                     int slot_entries, int vec_entries) {
+                                                                     int slot_entries, int vec_entries, int pre_out) {
   constexpr int U = 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -165,20 +165,37 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
   constexpr int NT = 32 * CW;
   pdl_wait();
   const double2* src = down ? r : out;
-  auto in_ptrs = [&](const SmallMerge& X, const int*& i1, const int*& i2, int& n1, int& n2) {
-    if (down) i1 = X.in1s, i2 = X.in2s, n1 = X.s, n2 = X.s;
-    else i1 = X.in1p, i2 = X.in2p, n1 = X.p1, n2 = X.p2;
+  // A merge's gathered rows, in scratch order: its inputs (down r1 | r2 at 0,
+  // up u1 | u2 at 0) and the bases of its read-modify-write outputs (down
+  // r[out1p] | r[out2p] at 5s, up out[in1s] | out[in2s] at p1 + p2 + 3s).
+  auto gather_row = [&](const SmallMerge& X, int i, int& dst) -> int {
+    const int s2 = X.s, q1 = X.p1, q2 = X.p2;
+    if (down) {
+      if (i < s2) return dst = i, X.in1s[i];
+      if (i < 2 * s2) return dst = i, X.in2s[i - s2];
+      if (i < 2 * s2 + q1) return dst = 5 * s2 + (i - 2 * s2), X.out1p[i - 2 * s2];
+      return dst = 5 * s2 + q1 + (i - 2 * s2 - q1), X.out2p[i - 2 * s2 - q1];
+    }
+    if (i < q1) return dst = i, X.in1p[i];
+    if (i < q1 + q2) return dst = i, X.in2p[i - q1];
+    if (i < q1 + q2 + s2) return dst = q1 + q2 + 3 * s2 + (i - q1 - q2), X.in1s[i - q1 - q2];
+    return dst = q1 + q2 + 4 * s2 + (i - q1 - q2 - s2), X.in2s[i - q1 - q2 - s2];
   };
+  // (pre_out: the output bases too -- levels of small merges, where the extra
+  // scratch does not shrink the ring; cfg3 levels 1-2 -8% / -4%, levels 4-6 +5%)
+  auto n_gather = [&](const SmallMerge& X) { return pre_out ? 2 * X.s + X.p1 + X.p2 : (down ? 2 * X.s : X.p1 + X.p2); };
   auto zero_b2 = [&](const SmallMerge& X, double2* vv) {  // up without T1_sp: b2 = 0
     if (!down && X.p1 == 0)
       for (int i = tid; i < X.s; i += NT) vv[X.p1 + X.p2 + i] = make_double2(0.0, 0.0);
   };
-  if (blockIdx.x < count) {  // the first merge's inputs
+  if (blockIdx.x < count) {  // the first merge's rows
     const SmallMerge& X = ms[blockIdx.x];
-    const int *i1, *i2;
-    int n1, n2;
-    in_ptrs(X, i1, i2, n1, n2);
-    for (int i = tid; i < n1 + n2; i += NT) cp_async16(vbuf + i, src + (i < n1 ? i1[i] : i2[i - n1]));
+    const int ng = n_gather(X);
+    for (int i = tid; i < ng; i += NT) {
+      int dst;
+      const int row = gather_row(X, i, dst);
+      cp_async16(vbuf + dst, src + row);
+    }
     cp_async_commit();
     zero_b2(X, vbuf);
   }
@@ -191,20 +208,22 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
     double2* vn = vbuf + ((it + 1) & 1) * vec_entries;
     cp_async_wait_all();
     bar_consumers(NT);
-    // next merge: indices now (their loads overlap operator 0), gathers after it
+    // next merge: row indices now (their loads overlap operator 0), gathers after it
     const int mn = m + gridDim.x;
-    int pidx[2] = {-1, -1};
+    int pidx[2] = {-1, -1}, pdst[2] = {0, 0};
     if (mn < count) {
-      const int *i1, *i2;
-      int n1, n2;
-      in_ptrs(ms[mn], i1, i2, n1, n2);
+      const SmallMerge& X = ms[mn];
+      const int ng = n_gather(X);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int i = tid + e * NT;
-        if (i < n1 + n2) pidx[e] = i < n1 ? i1[i] : i2[i - n1];
+        if (i < ng) pidx[e] = gather_row(X, i, pdst[e]);
       }
-      for (int i = tid + 2 * NT; i < n1 + n2; i += NT)  // (beyond two per thread: issued now)
-        cp_async16(vn + i, src + (i < n1 ? i1[i] : i2[i - n1]));
+      for (int i = tid + 2 * NT; i < ng; i += NT) {  // (beyond two per thread: issued now)
+        int dst;
+        const int row = gather_row(X, i, dst);
+        cp_async16(vn + dst, src + row);
+      }
     }
     for (int k = 0; k < 4; ++k) {
       const Op op = merge_op(M, down, k);
@@ -254,16 +273,16 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
             __stcg(out + M.in1s[i], y);
           } else if (k == 2) {
             if (i < p1) {
-              const int o = M.out1p[i];
-              __stcg(r + o, csub(__ldcg(r + o), y));
+              double2* qp = r + M.out1p[i];
+              __stcg(qp, csub(pre_out ? v[5 * s + i] : __ldcg(qp), y));
             } else {
               const double2 xv = csub(r2[i - p1], y);
               x2[i - p1] = xv;
               __stcg(out + M.in2s[i - p1], xv);
             }
           } else {
-            const int o = M.out2p[i];
-            __stcg(r + o, csub(__ldcg(r + o), y));
+            double2* qp = r + M.out2p[i];
+            __stcg(qp, csub(pre_out ? v[5 * s + p1 + i] : __ldcg(qp), y));
           }
         } else {
           double2 *nb2 = v + p1 + p2, *t = nb2 + s, *y1 = t + s;
@@ -274,17 +293,17 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
           } else if (k == 2) {
             y1[i] = y;
             double2* qp = out + M.in1s[i];
-            __stcg(qp, csub(__ldcg(qp), y));
+            __stcg(qp, csub(pre_out ? y1[s + i] : __ldcg(qp), y));  // base out[in1s] at p1 + p2 + 3s
           } else {
             double2* qp = out + M.in2s[i];
-            __stcg(qp, cadd(__ldcg(qp), cadd(y, nb2[i])));
+            __stcg(qp, cadd(pre_out ? y1[2 * s + i] : __ldcg(qp), cadd(y, nb2[i])));  // base at p1 + p2 + 4s
           }
         }
       }
       if (k == 0 || (k == 1 && pidx[0] != -2)) {  // after the first operator that ran
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          if (pidx[e] >= 0) cp_async16(vn + tid + e * NT, src + pidx[e]);
+          if (pidx[e] >= 0) cp_async16(vn + pdst[e], src + pidx[e]);
         cp_async_commit();
         if (mn < count) zero_b2(ms[mn], vn);
         pidx[0] = pidx[1] = -2;
@@ -294,7 +313,7 @@ __global__ void __launch_bounds__(32 * (CW + 1)) merge_stream_kernel(const Small
     if (pidx[0] != -2) {  // (no operator ran)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        if (pidx[e] >= 0) cp_async16(vn + tid + e * NT, src + pidx[e]);
+        if (pidx[e] >= 0) cp_async16(vn + pdst[e], src + pidx[e]);
       cp_async_commit();
       if (mn < count) zero_b2(ms[mn], vn);
     }
@@ -404,16 +423,16 @@ __global__ void __launch_bounds__(32 * (CW + 1)) gemv_stream_kernel(const GemvIt
 
 }  // namespace
 
-StreamLevel::Shape stream_level_shape(int rows_max, int s_max, int vec_max, int merges, int sms) {
+StreamLevel::Shape stream_level_shape(int rows_max, int vec_in, int vec_all, int merges, int sms) {
   StreamLevel::Shape sh;
-  (void)s_max;
   if (rows_max > 512 || merges < sms) return sh;
   // one row group of 32 per consumer warp (and column groups on top): 4
   // consumer warps (rows <= 128) x 4 CTAs per SM, 8 x 3, or 16 x 2 -- several
   // merges in flight per SM hide each merge's per-operator barriers
   const int cw = rows_max <= 128 ? 4 : rows_max <= 256 ? 8 : 16;
   const int ctas_per_sm = cw == 4 ? 4 : cw == 8 ? 3 : 2;
-  const int vec = (vec_max + 7) & ~7;
+  sh.pre_out = cw == 4;
+  const int vec = ((sh.pre_out ? vec_all : vec_in) + 7) & ~7;
   const size_t budget = (220u << 10) / ctas_per_sm;
   const size_t fixed = sizeof(double2) * (32 * static_cast<size_t>(cw) + 2 * static_cast<size_t>(vec)) +
                        2 * sizeof(unsigned long long) * kStreamMaxSlots;
@@ -437,7 +456,7 @@ void StreamLevel::run(Context* ctx, bool down, double2* r, double2* out) const {
     allow_smem<decltype(kern)::value>(shape.smem);
     launch_k(ctx, decltype(kern)::value, dim3(ctas), dim3(32 * (shape.warps + 1)), shape.smem, 1,
              static_cast<const SmallMerge*>(d.p), count, down ? 1 : 0, r, out, shape.ns, shape.slot_entries,
-             shape.vec_entries);
+             shape.vec_entries, shape.pre_out ? 1 : 0);
   };
   if (shape.warps == 4) go(std::integral_constant<decltype(&merge_stream_kernel<4>), &merge_stream_kernel<4>>{});
   else if (shape.warps == 8) go(std::integral_constant<decltype(&merge_stream_kernel<8>), &merge_stream_kernel<8>>{});
