@@ -41,7 +41,7 @@ namespace {
 constexpr int V5B = 64;                 // block size of the factorisation
 constexpr int V5T = 128;                // threads of the tile / panel kernels (4 warps, 2 x 2)
 constexpr int V5K = 16;                 // k depth of one pipeline stage
-constexpr int V5S = 3;                  // pipeline stages
+constexpr int V5S = 2;                  // pipeline stages (2 x 4 CTAs per SM: cfg3 elements 62.6 -> 57.9 ms vs 3 x 3)
 constexpr int LDM = V5B + 4;            // [k][m] staging stride (m contiguous)
 constexpr int LDK = V5K + 4;            // [m][k] staging stride (k contiguous)
 constexpr int V5STAGE = V5B * LDK;      // doubles of the A operand per stage (>= V5K * LDM)
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) v5_assemble_kernel(V5Args v) {
 // ---- update (left-looking): tiles of block column k and of block row k of B
 // (B tiles are 16 NJB columns wide: one tile covers nb + 2 <= 80 columns)
 template <int NJB>
-__global__ void __launch_bounds__(V5T, 3) v5_update_kernel(V5Args v) {
+__global__ void __launch_bounds__(V5T, 4) v5_update_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
   constexpr int BW = 16 * NJB;
   const int P = v.P, k = v.k, nA = v.nblk - k, nBt = (v.nbc + BW - 1) / BW;
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(V5DT) v5_diag_kernel(V5Args v) {
 
 // ---- trsm: L[i,k] = A[i,k] Linv_k^T (i > k) and Y[k,:] = Linv_k B[k,:], one tile per CTA
 template <int NJB>
-__global__ void __launch_bounds__(V5T, 3) v5_trsm_kernel(V5Args v) {
+__global__ void __launch_bounds__(V5T, 4) v5_trsm_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
   constexpr int BW = 16 * NJB;
   const int P = v.P, k = v.k, k0 = V5B * k, bk = min(V5B, P - k0);
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(V5T, 3) v5_trsm_kernel(V5Args v) {
 
 // ---- backward: X[k,:] = Linv_k^T (Y[k,:] - sum_{j>k} L[j,k]^T X[j,:]), one column tile per CTA
 template <int NJB>
-__global__ void __launch_bounds__(V5T, 3) v5_back_kernel(V5Args v) {
+__global__ void __launch_bounds__(V5T, 4) v5_back_kernel(V5Args v) {
   extern __shared__ __align__(16) double smem5[];
   constexpr int BW = 16 * NJB;
   const int P = v.P, k = v.k, nBt = (v.nbc + BW - 1) / BW;
