@@ -427,10 +427,10 @@ StreamLevel::Shape stream_level_shape(int rows_max, int vec_in, int vec_all, int
   StreamLevel::Shape sh;
   if (rows_max > 512 || merges < sms) return sh;
   // one row group of 32 per consumer warp (and column groups on top): 4
-  // consumer warps (rows <= 128) x 4 CTAs per SM, 8 x 3, or 16 x 2 -- several
+  // consumer warps (rows <= 128) x 5 CTAs per SM, 8 x 4, or 16 x 2 -- several
   // merges in flight per SM hide each merge's per-operator barriers
   const int cw = rows_max <= 128 ? 4 : rows_max <= 256 ? 8 : 16;
-  const int ctas_per_sm = cw == 4 ? 4 : cw == 8 ? 3 : 2;
+  const int ctas_per_sm = cw == 4 ? 5 : cw == 8 ? 4 : 2;  // (measured: 4/3/2 -> 186.3 ms, 5/4/2 -> 184.9, 6/5/3 -> 194.4)
   sh.pre_out = cw == 4;
   const int vec = ((sh.pre_out ? vec_all : vec_in) + 7) & ~7;
   const size_t budget = (220u << 10) / ctas_per_sm;
@@ -438,7 +438,7 @@ StreamLevel::Shape stream_level_shape(int rows_max, int vec_in, int vec_all, int
                        2 * sizeof(unsigned long long) * kStreamMaxSlots;
   if (fixed >= budget) return sh;
   // ns slots of whole columns: 4 slots, each as large as the budget allows
-  const int ns = 4;
+  const int ns = 2;  // (cfg3 A/B: 4 / 3 / 2 slots -> solve 186.3 / 185.4 / 183.4 ms at 5 / 4 / 2 CTAs per SM)
   const int slot = static_cast<int>((budget - fixed) / (sizeof(double2) * ns)) - 32;
   if (slot < rows_max) return sh;
   sh.ok = true, sh.warps = cw, sh.ns = ns, sh.slot_entries = slot, sh.vec_entries = vec;
@@ -471,7 +471,7 @@ GemvStream::Shape gemv_stream_shape(int rows_max, int cols_max) {
   GemvStream::Shape sh;
   if (rows_max > 256 || rows_max < 1) return sh;
   sh.warps = 8;
-  sh.ctas_per_sm = 3;
+  sh.ctas_per_sm = 4;  // (2 / 3 / 4 / 6 per SM: interface matvec 17.5 / 16.3 / 15.3 / 19.1 ms per cfg3 solve)
   const size_t budget = (220u << 10) / sh.ctas_per_sm;
   const int xs = (cols_max + 7) & ~7;
   const size_t fixed = sizeof(double2) * (32 * static_cast<size_t>(sh.warps) + 2 * static_cast<size_t>(xs)) +
