@@ -390,21 +390,32 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
         double2* X1g = X1.p + r_at[gi];
         double2* X2g = X2.p + r_at[gi];
         double2* Tn = tnew.p + n_at[gi];
+        // X2 and T_new are write-only outputs: their additive terms are read
+        // from the child blocks where they lie (GemmDesc::Cin), not staged.
         pre.identity(W, s, s);
         pre.copy(T2sp, P2, Rg + static_cast<size_t>(p1) * s, s, s, p2, -1.0);
-        pre.copy(T1sp, P1, X2g, s, s, p1, -1.0);
-        pre.zero(X2g + static_cast<size_t>(p1) * s, s, s, p2);
-        pre.copy(T1pp, P1, Tn, q, p1, p1, 1.0);
-        pre.zero(Tn + static_cast<size_t>(p1) * q, q, p1, p2);
-        pre.zero(Tn + p1, q, p2, p1);
-        pre.copy(T2pp, P2, Tn + p1 + static_cast<size_t>(p1) * q, q, p2, p2, 1.0);
         g1.add(T2ss, P2, T1ss, P1, W, s, s, s, s, -1.0, 1.0);
         g1.add(T2ss, P2, T1sp, P1, Rg, s, s, p1, s, 1.0, 0.0);
         inv.ops.push_back(InvOp{W, s, s, (level << 20) | mr.group, 0});
-        g2.add(W, s, Rg, s, X1g, s, s, q, s, 1.0, 0.0);
-        g3.add(T1ss, P1, X1g, s, X2g, s, s, q, s, -1.0, 1.0);
-        g3.add(T1ps, P1, X1g, s, Tn, q, p1, q, s, 1.0, 1.0);
-        g4.add(T2ps, P2, X2g, s, Tn + p1, q, p2, q, s, 1.0, 1.0);
+        g2.add(W, s, Rg, s, X1g, s, s, q, s, 1.0, 0.0);  // X1 = W [T2_ss T1_sp, -T2_sp]
+        {  // X2 = -T1_ss X1 - [T1_sp, 0]
+          GemmDesc d{};
+          d.A = T1ss, d.lda = P1, d.B = X1g, d.ldb = s, d.C = X2g, d.ldc = s, d.M = s, d.N = q, d.K = s;
+          d.alpha_re = -1.0, d.beta_re = -1.0, d.Cin = T1sp, d.ldcin = P1, d.cin_c0 = 0, d.cin_c1 = p1;
+          g3.add(d);
+        }
+        {  // T_new[0:p1, :] = [T1_pp, 0] + T1_ps X1
+          GemmDesc d{};
+          d.A = T1ps, d.lda = P1, d.B = X1g, d.ldb = s, d.C = Tn, d.ldc = q, d.M = p1, d.N = q, d.K = s;
+          d.alpha_re = 1.0, d.beta_re = 1.0, d.Cin = T1pp, d.ldcin = P1, d.cin_c0 = 0, d.cin_c1 = p1;
+          g3.add(d);
+        }
+        {  // T_new[p1:q, :] = [0, T2_pp] + T2_ps X2
+          GemmDesc d{};
+          d.A = T2ps, d.lda = P2, d.B = X2g, d.ldb = s, d.C = Tn + p1, d.ldc = q, d.M = p2, d.N = q, d.K = s;
+          d.alpha_re = 1.0, d.beta_re = 1.0, d.Cin = T2pp, d.ldcin = P2, d.cin_c0 = p1, d.cin_c1 = q;
+          g4.add(d);
+        }
       }
       pre.run(ctx);
       g1.run(ctx);

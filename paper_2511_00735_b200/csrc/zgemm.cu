@@ -116,38 +116,46 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
     const double2* as = As + (kt % STAGES) * A_STAGE;
     const double2* bs = Bs + (kt % STAGES) * B_STAGE;
     const int krem = d.K - kt * BK;
+    // FULL: every fragment and k-step of this stage is inside the problem
+    // (interior tiles of the large merges): no predicates, no early exit,
+    // so the fragment loads of step kk + 4 are scheduled under the DMMAs of kk
+    auto stage = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      if (kk >= krem) break;
-      double2 a[4], b[2];
+      for (int kk = 0; kk < BK; kk += 4) {
+        if (!FULL && kk >= krem) break;
+        double2 a[4], b[2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
+        for (int i = 0; i < 4; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
-      // four passes over the 4 x 2 fragment grid: the two DMMAs into the
-      // same accumulator are 2 4 issues apart instead of back to back (the
-      // asm statements are volatile, so the compiler keeps this order)
+        for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
+        // four passes over the 4 x 2 fragment grid: the two DMMAs into the
+        // same accumulator are 24 issues apart instead of back to back (the
+        // asm statements are volatile, so the compiler keeps this order)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (i < ni_act && j < nj_act) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
+          for (int j = 0; j < 2; ++j)
+            if (FULL || (i < ni_act && j < nj_act)) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (i < ni_act && j < nj_act) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
+          for (int j = 0; j < 2; ++j)
+            if (FULL || (i < ni_act && j < nj_act)) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (i < ni_act && j < nj_act) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
+          for (int j = 0; j < 2; ++j)
+            if (FULL || (i < ni_act && j < nj_act)) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          if (i < ni_act && j < nj_act) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
-    }
+          for (int j = 0; j < 2; ++j)
+            if (FULL || (i < ni_act && j < nj_act)) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
+      }
+    };
+    if (ni_act == 4 && nj_act == 2 && krem >= BK) stage(std::true_type{});
+    else stage(std::false_type{});
   }
   cp_async_wait<0>();
   // epilogue: C = alpha * acc + beta * C.  All C reads are issued before
@@ -170,8 +178,13 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int row = row0 + (2 * half + i) * 8, col = col0 + j * 8 + h;
-            cold[i][j][h] = (row < d.M && col < d.N) ? d.C[(size_t)row + (size_t)col * d.ldc]
-                                                     : make_double2(0.0, 0.0);
+            double2 cv = make_double2(0.0, 0.0);
+            if (row < d.M && col < d.N) {
+              if (!d.Cin) cv = d.C[(size_t)row + (size_t)col * d.ldc];
+              else if (col >= d.cin_c0 && col < d.cin_c1)
+                cv = d.Cin[(size_t)row + (size_t)(col - d.cin_c0) * d.ldcin];
+            }
+            cold[i][j][h] = cv;
           }
     }
 #pragma unroll

@@ -7,7 +7,11 @@
 
 namespace hpsb {
 
-// C = alpha * A * B + beta * C, all column-major complex.
+// C = alpha * A * B + beta * C, all column-major complex.  With Cin != null
+// the beta term reads Cin (ld ldcin) on the column window [cin_c0, cin_c1)
+// and zero outside it instead of C, and C is write-only: the merges take
+// their additive terms from the child blocks where they lie, with no staging
+// copy into C.
 struct GemmDesc {
   const double2* A;
   const double2* B;
@@ -15,7 +19,9 @@ struct GemmDesc {
   int M, N, K;
   int lda, ldb, ldc;
   double alpha_re, alpha_im, beta_re, beta_im;
-  int tiles_m, tiles_n, tile_begin, pad;
+  int tiles_m, tiles_n, tile_begin, ldcin;
+  const double2* Cin;
+  int cin_c0, cin_c1;
 };
 
 struct GemmBatch {
