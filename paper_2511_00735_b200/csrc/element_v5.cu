@@ -170,6 +170,9 @@ __device__ __forceinline__ void tile_mma(const double* __restrict__ op1, int ld1
 }
 
 // C (column-major, ldc) = beta * C + alpha * acc over the tile's M x N part.
+// Accumulating stores read a whole fragment row (2 NJ values) before the
+// first store: interleaved, every read waited for the previous store
+// (possible aliasing) -- 8 NJ serial L2 round trips per thread.
 template <int NJ>
 __device__ __forceinline__ void tile_store(double* C, int ldc, int M, int N, const double (&acc)[4][NJ][2],
                                            double alpha, bool accumulate) {
@@ -179,14 +182,20 @@ __device__ __forceinline__ void tile_store(double* C, int ldc, int M, int N, con
   for (int i = 0; i < 4; ++i) {
     const int row = 32 * wm + 8 * i + g;
     if (row >= M) continue;
+    double old[NJ][2];
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = 8 * NJ * wn + 8 * j + 2 * t4 + h;
-        if (col >= N) continue;
-        double* c = C + row + static_cast<size_t>(col) * ldc;
-        *c = accumulate ? *c + alpha * acc[i][j][h] : alpha * acc[i][j][h];
+        old[j][h] = (accumulate && col < N) ? C[row + static_cast<size_t>(col) * ldc] : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = 8 * NJ * wn + 8 * j + 2 * t4 + h;
+        if (col < N) C[row + static_cast<size_t>(col) * ldc] = old[j][h] + alpha * acc[i][j][h];
       }
   }
 }
@@ -212,45 +221,58 @@ __global__ void __launch_bounds__(256) v5_assemble_kernel(V5Args v) {
   __syncthreads();
   double* A = v.A + c * v.sA;
   double* B = v.B + c * v.sB;
-  // column col: rows from the top of its diagonal block (the diagonal tile is read whole)
-  for (int col = threadIdx.x >> 5; col < P; col += blockDim.x >> 5) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  // One warp per column: zero fill with 16-byte stores (rows from the top of
+  // the column's diagonal block: the diagonal tile is read whole), then the
+  // 2m - 1 entries of the column (its grid line in x and in y) are patched.
+  // (Per-entry index arithmetic over the whole column made this kernel
+  // instruction bound: 2.7 TB/s of stores.)
+  for (int col = warp; col < P; col += nwarps) {
     const int r0 = col / V5B * V5B;
-    const int k = col / m + 1, l = col % m + 1;
     double* Ac = A + static_cast<size_t>(col) * P;
-    for (int r = r0 + (threadIdx.x & 31); r < P; r += 32) {
-      double val;
-      if (r >= ni || col >= ni) {
-        val = (r == col) ? 1.0 : 0.0;
-      } else {
-        const int i = r / m + 1, j = r - (i - 1) * m + 1;
-        val = 0.0;
-        if (j == l) val += Ks[i + k * np] * mass[j];
-        if (i == k) val += mass[i] * Ks[j + l * np];
-        if (r == col) val -= cm[r];
-      }
+    for (int r = r0 + 2 * lane; r < P; r += 64) {
+      double2 z = make_double2(0.0, 0.0);
+      if (col >= ni) z = make_double2(r == col ? 1.0 : 0.0, r + 1 == col ? 1.0 : 0.0);
+      *reinterpret_cast<double2*>(Ac + r) = z;
+    }
+    if (col >= ni) continue;
+    __syncwarp();
+    const int k = col / m + 1, l = col % m + 1;
+    for (int i = 1 + lane; i <= m; i += 32) {  // nodes (i, l), i != k
+      const int r = (i - 1) * m + (l - 1);
+      if (r >= r0 && i != k) Ac[r] = Ks[i + k * np] * mass[l];
+    }
+    for (int j = 1 + lane; j <= m; j += 32) {  // nodes (k, j)
+      const int r = (k - 1) * m + (j - 1);
+      if (r < r0) continue;
+      double val = mass[k] * Ks[j + l * np];
+      if (j == l) val = (Ks[k + k * np] * mass[l] + val) - cm[r];
       Ac[r] = val;
     }
   }
-  for (int idx = threadIdx.x; idx < P * nbc; idx += blockDim.x) {
-    const int q = idx % P, b = idx / P;
-    double val = 0.0;
-    if (q < ni && b < nb + 2) {
-      const int i = q / m + 1, j = q % m + 1;
-      if (b < nb) {
-        const int side = b / m, t = b % m + 1;
-        switch (side) {
-          case 0: val = (j == t) ? Ks[i + 0 * np] * mass[j] : 0.0; break;
-          case 1: val = (j == t) ? Ks[i + N * np] * mass[j] : 0.0; break;
-          case 2: val = (i == t) ? mass[i] * Ks[j + 0 * np] : 0.0; break;
-          default: val = (i == t) ? mass[i] * Ks[j + N * np] : 0.0; break;
+  for (int bc = warp; bc < nbc; bc += nwarps) {
+    double* Bc = B + static_cast<size_t>(bc) * P;
+    if (bc >= nb && bc < nb + 2 && a.source) {
+      for (int q = lane; q < P; q += 32) {
+        double val = 0.0;
+        if (q < ni) {
+          const int i = q / m + 1, j = q % m + 1;
+          const double2 sv = a.source[static_cast<size_t>(e) * ni + q];
+          const double w = mass[i] * mass[j];
+          val = (bc == nb) ? sv.x * w : sv.y * w;
         }
-      } else if (a.source) {
-        const double2 sv = a.source[static_cast<size_t>(e) * ni + q];
-        const double w = mass[i] * mass[j];
-        val = (b == nb) ? sv.x * w : sv.y * w;
+        Bc[q] = val;
       }
+      continue;
     }
-    B[idx] = val;
+    for (int r = 2 * lane; r < P; r += 64) *reinterpret_cast<double2*>(Bc + r) = make_double2(0.0, 0.0);
+    if (bc >= nb) continue;
+    __syncwarp();
+    const int side = bc / m, t = bc % m + 1, edge = (side & 1) ? N : 0;
+    for (int kk = 1 + lane; kk <= m; kk += 32) {
+      if (side < 2) Bc[(kk - 1) * m + (t - 1)] = Ks[kk + edge * np] * mass[t];  // nodes (kk, t)
+      else Bc[(t - 1) * m + (kk - 1)] = mass[t] * Ks[kk + edge * np];           // nodes (t, kk)
+    }
   }
 }
 
