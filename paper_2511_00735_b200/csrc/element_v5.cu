@@ -313,11 +313,13 @@ __global__ void __launch_bounds__(V5T, 4) v5_update_kernel(V5Args v) {
 //   memory with uniform (broadcast) addresses, x stays in registers, and the
 //   result rows are stored coalesced.
 // Rows / columns past bk (the ragged last block) are identity.
+// Two launches (Cholesky, then inverse): the unrolled phases are ~85 KB of
+// code each; as one 170 KB kernel the warps of an SM, at different points of
+// it, missed the instruction cache (26% no_instructions stalls).  L passes
+// through the Linv block (1 / l_jj on its diagonal).
 constexpr int V5DT = 64;
 __global__ void __launch_bounds__(V5DT, 6) v5_diag_kernel(V5Args v) {
-  __shared__ __align__(16) double Lc[V5B * V5B];  // L column-major (strict lower part used)
   __shared__ __align__(16) double colbuf[2][V5B];
-  __shared__ double rdiag[V5B];                   // 1 / l_jj
   const int P = v.P, k = v.k, c = blockIdx.x, e = v5_elem(v, c), t = threadIdx.x;
   if (v.a.status[e] & 4) return;
   const double* A = v.A + c * v.sA;
@@ -337,15 +339,28 @@ __global__ void __launch_bounds__(V5DT, 6) v5_diag_kernel(V5Args v) {
       if (t == 0) atomicOr(v.a.status + e, 4);  // indefinite: pivoted-LU fallback (v1)
       return;
     }
+    // 1 / d as rs^2: a double division takes its slow path (a subroutine
+    // call) whenever the quotient is zero, i.e. for most entries of the
+    // sparse first columns -- 29% of this kernel's stall samples
     const double rs = rsqrt(d);
-    const double f = a[j] / d;
-    if (t == j) rdiag[j] = rs;
-    Lc[j * V5B + t] = a[j] * rs;
+    const double f = a[j] * (rs * rs);
+    Lg[j * V5B + t] = (t == j) ? rs : a[j] * rs;  // column j of L (upper part: don't care)
 #pragma unroll
     for (int q = j + 1; q < V5B; ++q) a[q] -= f * cb[q];
   }
+}
+
+__global__ void __launch_bounds__(V5DT, 6) v5_dinv_kernel(V5Args v) {
+  __shared__ __align__(16) double Lc[V5B * V5B];  // L column-major (lower part used; 1 / l_jj on the diagonal)
+  const int P = v.P, k = v.k, c = blockIdx.x, e = v5_elem(v, c), t = threadIdx.x;
+  if (v.a.status[e] & 4) return;
+  double* Lg = v.Linv + c * v.sL + static_cast<size_t>(k) * V5B * V5B;  // ld 64
+  const int bk = min(V5B, P - V5B * k);
+  for (int idx = t; idx < V5B * V5B / 2; idx += V5DT) cp_async16(Lc + 2 * idx, Lg + 2 * idx);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
-  // a[] is dead: a[c] = X[t][c] from here on
+  double a[V5B];  // a[c] = X[t][c]
 #pragma unroll
   for (int cc = V5B - 1; cc >= 0; --cc) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -360,7 +375,7 @@ __global__ void __launch_bounds__(V5DT, 6) v5_diag_kernel(V5Args v) {
         default: s3 += term; break;
       }
     }
-    const double rd = rdiag[cc];
+    const double rd = lc[cc];
     a[cc] = cc > t ? 0.0 : (cc == t ? rd : -rd * ((s0 + s1) + (s2 + s3)));
   }
 #pragma unroll
@@ -684,6 +699,8 @@ bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
       {
         KernelScope ks(ctx, "element_iti", 0.0, 0.0);
         v5_diag_kernel<<<cn, V5DT, 0, ctx->stream>>>(v);
+        HPSB_LAUNCHED(ctx);
+        v5_dinv_kernel<<<cn, V5DT, 0, ctx->stream>>>(v);
         HPSB_LAUNCHED(ctx);
       }
       KernelScope ks(ctx, "element_iti", 0.0, 0.0);

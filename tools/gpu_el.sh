@@ -1,6 +1,6 @@
 #!/bin/bash
-# Element stage: parity tests, then the cfg3 element probe (device time per build from the per-label profile).
+# Element-stage launch list: cfg3 element probe under ncu (time + DRAM bytes per launch), summarised by kernel.
 cd "$GRAFT_REPO_ROOT"
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -m gpu -q -p no:cacheprovider -k "element or iti or golden" 2>&1 | tail -2
-for c in 3 4; do timeout 300 python tools/element_probe.py $c 4 prof 2>&1 | tail -1 | python -c "
-import sys,ast; d=ast.literal_eval(sys.stdin.read()); print('cfg$c element_iti ms/build', round(d['element_iti']['ms']/4,2))"; done
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
+  --log-file gpurun_out/el_launches.csv python tools/element_probe.py 3 2 > gpurun_out/el_ncu.log 2>&1
+python tools/ncu_summary.py gpurun_out/el_launches.csv "element probe cfg3 (2 builds)" | tee gpurun_out/el_launches.txt
