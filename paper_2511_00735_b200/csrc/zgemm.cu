@@ -119,11 +119,13 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
     // FULL: every fragment and k-step of this stage is inside the problem
     // (interior tiles of the large merges): no predicates, no early exit,
     // so the fragment loads of step kk + 4 are scheduled under the DMMAs of kk
-    auto stage = [&](auto full_tag) {
-      constexpr bool FULL = decltype(full_tag)::value;
+    // KFULL: all BK k-values are inside K (fragment predicates only, no
+    // early exit: the loads still pipeline under the DMMAs)
+    auto stage = [&](auto full_tag, auto kfull_tag) {
+      constexpr bool FULL = decltype(full_tag)::value, KFULL = decltype(kfull_tag)::value;
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
-        if (!FULL && kk >= krem) break;
+        if (!KFULL && kk >= krem) break;
         double2 a[4], b[2];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
@@ -154,8 +156,12 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
             if (FULL || (i < ni_act && j < nj_act)) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
       }
     };
-    if (ni_act == 4 && nj_act == 2 && krem >= BK) stage(std::true_type{});
-    else stage(std::false_type{});
+    if (krem >= BK) {
+      if (ni_act == 4 && nj_act == 2) stage(std::true_type{}, std::true_type{});
+      else stage(std::false_type{}, std::true_type{});
+    } else {
+      stage(std::false_type{}, std::false_type{});
+    }
   }
   cp_async_wait<0>();
   // epilogue: C = alpha * acc + beta * C.  All C reads are issued before
