@@ -28,11 +28,22 @@
 namespace hpsb {
 
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
-constexpr int SA = BM + 2;  // complex stride of an A k-row in smem
+constexpr int BK = 16, STAGES = 3, THREADS = 256;
 constexpr int SB = BK + 4;  // complex stride of a B column in smem
-constexpr int A_STAGE = BK * SA, B_STAGE = BN * SB;
-constexpr size_t GEMM_SMEM = sizeof(double2) * STAGES * (A_STAGE + B_STAGE);
+// Tile shapes: IM = 4 / 3 / 2 row fragments per warp (64 / 48 / 32 rows over
+// 2 warp rows), JN = 2 / 1 column fragments per warp (64 / 32 columns over 4
+// warp columns).  A tile's time is its busiest warp's: with 64 x 64 tiles
+// only, a ragged dimension (merge sizes are multiples of N - 1: 76 = 64 + 12)
+// cost a full tile and the launch times followed the tile-padded flops.
+// Shapes are compile time (a run-time shape spilled registers in the main
+// loop: 116.6 -> 131 ms at cfg3); GemmBatch::run launches once per shape.
+template <int IM, int JN>
+struct GemmTile {
+  static constexpr int BM = 16 * IM, BN = 32 * JN;
+  static constexpr int SA = BM + 2;  // complex stride of an A k-row in smem
+  static constexpr int A_STAGE = BK * SA, B_STAGE = BN * SB;
+  static constexpr size_t kSmem = sizeof(double2) * STAGES * (A_STAGE + B_STAGE);
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -51,8 +62,11 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+template <int IM, int JN>
 __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDesc* __restrict__ descs,
                                                                 const int* __restrict__ tile_map) {
+  using TS = GemmTile<IM, JN>;
+  constexpr int BM = TS::BM, BN = TS::BN, SA = TS::SA, A_STAGE = TS::A_STAGE, B_STAGE = TS::B_STAGE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + STAGES * A_STAGE;
@@ -65,7 +79,7 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
   const int tm = local % d.tiles_m, tn = local / d.tiles_m;
   const int m0 = tm * BM, n0 = tn * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps
+  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps of (8 IM) x (8 JN)
   const int ktiles = (d.K + BK - 1) / BK;
 
   auto load_stage = [&](int kt, int st) {
@@ -90,24 +104,24 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
     }
   };
 
-  double cr[4][2][2], ci[4][2][2];
+  double cr[IM][JN][2], ci[IM][JN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < IM; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
+    for (int j = 0; j < JN; ++j) cr[i][j][0] = cr[i][j][1] = ci[i][j][0] = ci[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) load_stage(s, s);
     cp_async_commit();
   }
-  const int arow = wm * 32 + (lane >> 2), kq = lane & 3;
-  const int bcol = wn * 16 + (lane >> 2);
+  const int arow = wm * (8 * IM) + (lane >> 2), kq = lane & 3;
+  const int bcol = wn * (8 * JN) + (lane >> 2);
   // Edge tiles: fragments wholly outside M x N and k-steps past K are
   // skipped (warp-uniform), so ragged merge dimensions (multiples of N-1,
   // e.g. 76 = 64 + 12) do not pay for a full padded tile on the DMMA pipe.
-  const int ni_act = max(0, min(4, (d.M - m0 - wm * 32 + 7) / 8));
-  const int nj_act = max(0, min(2, (d.N - n0 - wn * 16 + 7) / 8));
+  const int ni_act = max(0, min(IM, (d.M - m0 - wm * (8 * IM) + 7) / 8));
+  const int nj_act = max(0, min(JN, (d.N - n0 - wn * (8 * JN) + 7) / 8));
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -126,38 +140,38 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
 #pragma unroll
       for (int kk = 0; kk < BK; kk += 4) {
         if (!KFULL && kk >= krem) break;
-        double2 a[4], b[2];
+        double2 a[IM], b[JN];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
+        for (int i = 0; i < IM; ++i) a[i] = as[(kk + kq) * SA + arow + i * 8];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
+        for (int j = 0; j < JN; ++j) b[j] = bs[(bcol + j * 8) * SB + kk + kq];
         // four passes over the 4 x 2 fragment grid: the two DMMAs into the
         // same accumulator are 24 issues apart instead of back to back (the
         // asm statements are volatile, so the compiler keeps this order)
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < IM; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
+          for (int j = 0; j < JN; ++j)
             if (FULL || (i < ni_act && j < nj_act)) dmma(cr[i][j][0], cr[i][j][1], a[i].x, b[j].x);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < IM; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
+          for (int j = 0; j < JN; ++j)
             if (FULL || (i < ni_act && j < nj_act)) dmma(ci[i][j][0], ci[i][j][1], a[i].x, b[j].y);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < IM; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
+          for (int j = 0; j < JN; ++j)
             if (FULL || (i < ni_act && j < nj_act)) dmma(cr[i][j][0], cr[i][j][1], -a[i].y, b[j].y);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < IM; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
+          for (int j = 0; j < JN; ++j)
             if (FULL || (i < ni_act && j < nj_act)) dmma(ci[i][j][0], ci[i][j][1], a[i].y, b[j].x);
       }
     };
     if (krem >= BK) {
-      if (ni_act == 4 && nj_act == 2) stage(std::true_type{}, std::true_type{});
+      if (ni_act == IM && nj_act == JN) stage(std::true_type{}, std::true_type{});
       else stage(std::false_type{}, std::true_type{});
     } else {
       stage(std::false_type{}, std::false_type{});
@@ -171,21 +185,21 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
   const double2 alpha = make_double2(d.alpha_re, d.alpha_im);
   const double2 beta = make_double2(d.beta_re, d.beta_im);
   const bool use_beta = (d.beta_re != 0.0 || d.beta_im != 0.0);
-  const int row0 = m0 + wm * 32 + (lane >> 2), col0 = n0 + wn * 16 + 2 * (lane & 3);
-  // two halves of the fragment rows: 8 reads in flight, no spills
+  const int row0 = m0 + wm * (8 * IM) + (lane >> 2), col0 = n0 + wn * (8 * JN) + 2 * (lane & 3);
+  // fragment rows two at a time: 4 JN reads in flight, no spills
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    double2 cold[2][2][2];
+  for (int half = 0; half < (IM + 1) / 2; ++half) {
+    double2 cold[2][JN][2];
     if (use_beta) {
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < JN; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int row = row0 + (2 * half + i) * 8, col = col0 + j * 8 + h;
             double2 cv = make_double2(0.0, 0.0);
-            if (row < d.M && col < d.N) {
+            if (2 * half + i < IM && row < d.M && col < d.N) {
               if (!d.Cin) cv = d.C[(size_t)row + (size_t)col * d.ldc];
               else if (col >= d.cin_c0 && col < d.cin_c1)
                 cv = d.Cin[(size_t)row + (size_t)(col - d.cin_c0) * d.ldcin];
@@ -196,14 +210,14 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int ii = 2 * half + i, row = row0 + ii * 8;
-      if (row >= d.M) continue;
+      if (ii >= IM || row >= d.M) continue;
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < JN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int col = col0 + j * 8 + h;
           if (col >= d.N) continue;
-          double2 v = cmul(alpha, make_double2(cr[ii][j][h], ci[ii][j][h]));
+          double2 v = cmul(alpha, make_double2(cr[ii < IM ? ii : 0][j][h], ci[ii < IM ? ii : 0][j][h]));
           if (use_beta) v = cadd(v, cmul(beta, cold[i][j][h]));
           d.C[(size_t)row + (size_t)col * d.ldc] = v;
         }
@@ -530,46 +544,97 @@ __global__ void unscramble_kernel(const InvOp* __restrict__ ops, const int* __re
 
 int GemmBatch::add(const GemmDesc& d0) {
   if (d0.M <= 0 || d0.N <= 0) return -1;
-  GemmDesc d = d0;
-  d.tiles_m = (d.M + BM - 1) / BM;
-  d.tiles_n = (d.N + BN - 1) / BN;
-  d.tile_begin = total_tiles;
-  total_tiles += d.tiles_m * d.tiles_n;
-  flops += 8.0 * d.M * d.N * std::max(d.K, 0);
-  descs.push_back(d);
+  flops += 8.0 * d0.M * d0.N * std::max(d0.K, 0);
+  descs.push_back(d0);
   return static_cast<int>(descs.size()) - 1;
 }
+
+namespace {
+// the largest tile, unless a smaller one cuts the padded size by more than 8%
+int pick_tile(int n, std::initializer_list<int> sizes) {
+  int best = *sizes.begin();
+  for (int b : sizes) {
+    const int pb = (n + best - 1) / best * best, pn = (n + b - 1) / b * b;
+    if (pn * 100 < pb * 92) best = b;
+  }
+  return best;
+}
+template <int IM, int JN>
+void launch_gemm(Context* ctx, int tiles, const GemmDesc* descs, const int* map) {
+  static const bool attr = [] {  // thread-safe one-time init
+    HPSB_CUDA(cudaFuncSetAttribute(zgemm_grouped_kernel<IM, JN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(GemmTile<IM, JN>::kSmem)));
+    return true;
+  }();
+  (void)attr;
+  zgemm_grouped_kernel<IM, JN><<<tiles, THREADS, GemmTile<IM, JN>::kSmem, ctx->stream>>>(descs, map);
+  HPSB_LAUNCHED(ctx);
+}
+}  // namespace
 
 void GemmBatch::run(Context* ctx) {
   if (descs.empty()) return;
   // K == 0 problems still apply the epilogue (C = beta C): keep them valid.
-  d_descs.upload(descs, ctx->stream);
+  // Problems are grouped by tile shape, one launch per shape present.
+  constexpr int kShapes = 6;  // (bm, bn): 64/48/32 x 64/32
+  auto shape_of = [](const GemmDesc& d) {
+    return (d.bm == 64 ? 0 : d.bm == 48 ? 1 : 2) * 2 + (d.bn == 64 ? 0 : 1);
+  };
+  std::vector<GemmDesc> sorted;
+  sorted.reserve(descs.size());
+  int first[kShapes + 1] = {0}, tiles[kShapes] = {0}, map_off[kShapes + 1] = {0};
+  for (auto& d : descs) {
+    d.bm = pick_tile(d.M, {64, 48, 32});
+    d.bn = pick_tile(d.N, {64, 32});
+    d.tiles_m = (d.M + d.bm - 1) / d.bm;
+    d.tiles_n = (d.N + d.bn - 1) / d.bn;
+  }
+  double padded = 0;
+  for (int sh = 0; sh < kShapes; ++sh) {
+    first[sh] = static_cast<int>(sorted.size());
+    for (const auto& d0 : descs) {
+      if (shape_of(d0) != sh) continue;
+      GemmDesc d = d0;
+      d.tile_begin = tiles[sh];
+      tiles[sh] += d.tiles_m * d.tiles_n;
+      padded += 8.0 * d.tiles_m * d.bm * d.tiles_n * d.bn * (((d.K + BK - 1) / BK) * BK);
+      sorted.push_back(d);
+    }
+    map_off[sh + 1] = map_off[sh] + tiles[sh];
+  }
+  first[kShapes] = static_cast<int>(sorted.size());
+  total_tiles = map_off[kShapes];
+  d_descs.upload(sorted, ctx->stream);
   {
     std::vector<int> map(total_tiles);
-    for (size_t i = 0; i < descs.size(); ++i) {
-      const int end = i + 1 < descs.size() ? descs[i + 1].tile_begin : total_tiles;
-      std::fill(map.begin() + descs[i].tile_begin, map.begin() + end, static_cast<int>(i));
-    }
+    for (int sh = 0; sh < kShapes; ++sh)
+      for (int i = first[sh]; i < first[sh + 1]; ++i) {
+        const GemmDesc& d = sorted[i];
+        std::fill(map.begin() + map_off[sh] + d.tile_begin,
+                  map.begin() + map_off[sh] + d.tile_begin + d.tiles_m * d.tiles_n, i - first[sh]);
+      }
     d_map.upload(map, ctx->stream);
   }
-  static const bool attr = [] {  // thread-safe one-time init
-    HPSB_CUDA(cudaFuncSetAttribute(zgemm_grouped_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(GEMM_SMEM)));
-    return true;
-  }();
-  (void)attr;
-  if (std::getenv("HPSB_TRACE")) {  // executed (tile-padded) vs useful flops per launch
-    double padded = 0;
-    for (const auto& d : descs) padded += 8.0 * d.tiles_m * BM * d.tiles_n * BN * (((d.K + BK - 1) / BK) * BK);
+  if (std::getenv("HPSB_TRACE")) {  // executed (tile-padded) vs useful flops per batch
     static double tu = 0, tp = 0;
     tu += flops, tp += padded;
     std::fprintf(stderr, "[gemm] descs %zu tiles %d useful %.3g padded %.3g (cum useful %.4g padded %.4g)\n",
                  descs.size(), total_tiles, flops, padded, tu, tp);
   }
   KernelScope ks(ctx, "zgemm_dmma", 0.0, flops);
-  zgemm_grouped_kernel<<<total_tiles, THREADS, GEMM_SMEM, ctx->stream>>>(d_descs.p, d_map.p);
-  HPSB_LAUNCHED(ctx);
+  for (int sh = 0; sh < kShapes; ++sh) {
+    if (!tiles[sh]) continue;
+    const GemmDesc* dp = d_descs.p + first[sh];
+    const int* mp = d_map.p + map_off[sh];
+    switch (sh) {
+      case 0: launch_gemm<4, 2>(ctx, tiles[sh], dp, mp); break;
+      case 1: launch_gemm<4, 1>(ctx, tiles[sh], dp, mp); break;
+      case 2: launch_gemm<3, 2>(ctx, tiles[sh], dp, mp); break;
+      case 3: launch_gemm<3, 1>(ctx, tiles[sh], dp, mp); break;
+      case 4: launch_gemm<2, 2>(ctx, tiles[sh], dp, mp); break;
+      default: launch_gemm<2, 1>(ctx, tiles[sh], dp, mp); break;
+    }
+  }
 }
 
 void CopyBatch::add(const CopyOp& o0) {

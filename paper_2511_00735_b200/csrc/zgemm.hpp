@@ -22,6 +22,7 @@ struct GemmDesc {
   int tiles_m, tiles_n, tile_begin, ldcin;
   const double2* Cin;
   int cin_c0, cin_c1;
+  int bm, bn;  // tile shape, chosen per problem by GemmBatch::run (64 / 48 / 32 rows, 64 / 32 columns)
 };
 
 struct GemmBatch {

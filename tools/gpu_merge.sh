@@ -1,6 +1,7 @@
 #!/bin/bash
-# Merge-stage check: the cfg3 bench kernel table (setup kernels), twice.
+# Merge-stage check: hierarchy / golden / sharded parity tests, then the cfg3 bench kernel table.
 cd "$GRAFT_REPO_ROOT"
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_golden.py -m gpu -q -p no:cacheprovider -x 2>&1 | tail -2
 for i in 1 2; do
 timeout 900 python bench.py --steps 4 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']
