@@ -58,7 +58,7 @@ typedef struct hpsb_precond_s* hpsb_precond;
  * depth 2, gamma 1, coarse_iters 4, exact_coarse 0). */
 typedef struct hpsb_mg_config {
   int depth;        /* number of hierarchy levels used (2 <= depth <= built depth) */
-  int gamma;        /* coarse calls per intermediate level (1 = V-cycle; > 1 single GPU) */
+  int gamma;        /* coarse calls per intermediate level (1 = V-cycle; > 1: host-recursive cycle, single-RHS applies) */
   int coarse_iters; /* unpreconditioned GMRES steps at the deepest level (<= 512) */
   int exact_coarse; /* dense inverse of M_depth instead of coarse GMRES; gamma and
                        coarse_iters are then ignored */

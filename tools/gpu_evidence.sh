@@ -22,8 +22,7 @@ cap() {  # $1 kernel regex, $2 launches to skip, $3 name, $4.. command
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $s -c 1 -o $O/$n "$@" > $O/ncu_$n.log 2>&1
   python tools/ncu_full_summary.py $O/$n.ncu-rep "ncu --set full --clock-control none -k regex:$k -s $s -c 1 $*" > $O/$n.txt; tail -n +3 $O/$n.txt | head -24
 }
-cap zgemm_grouped 271 ncu_zgemm_L13 python tools/setup_probe.py 3 1
-cap zgemm_grouped 60 ncu_zgemm_L6 python tools/setup_probe.py 3 1
+# large and mid-level merge GEMM launches: tools/gpu_recap.sh (kernel filter on the demangled template name)
 cap v5_update 3 ncu_element_update python tools/element_probe.py 3 1
 cap v5_diag 3 ncu_element_diag python tools/element_probe.py 3 1
 cap v5_dinv 3 ncu_element_dinv python tools/element_probe.py 3 1
