@@ -417,11 +417,14 @@ std::unique_ptr<Hierarchy> build_hierarchy_pass(Skeleton* sk, int depth,
           g4.add(d);
         }
       }
+      tr.mark("merge_lists");
       pre.run(ctx);
       g1.run(ctx);
+      tr.mark("merge_run_g1");
       inv.diag_pivots = !pivot;
       inv.guard_dev = d_status.p + 1;
       inv.run(ctx, d_status.p);
+      tr.mark("merge_run_inv");
       g2.run(ctx);
       g3.run(ctx);
       g4.run(ctx);

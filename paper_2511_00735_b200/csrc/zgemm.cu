@@ -580,29 +580,31 @@ void GemmBatch::run(Context* ctx) {
   auto shape_of = [](const GemmDesc& d) {
     return (d.bm == 64 ? 0 : d.bm == 48 ? 1 : 2) * 2 + (d.bn == 64 ? 0 : 1);
   };
-  std::vector<GemmDesc> sorted;
-  sorted.reserve(descs.size());
+  // counting sort by shape (stable: problems keep their order within a shape)
   int first[kShapes + 1] = {0}, tiles[kShapes] = {0}, map_off[kShapes + 1] = {0};
+  double padded = 0;
   for (auto& d : descs) {
     d.bm = pick_tile(d.M, {64, 48, 32});
     d.bn = pick_tile(d.N, {64, 32});
     d.tiles_m = (d.M + d.bm - 1) / d.bm;
     d.tiles_n = (d.N + d.bn - 1) / d.bn;
+    ++first[shape_of(d) + 1];
+    padded += 8.0 * d.tiles_m * d.bm * d.tiles_n * d.bn * (((d.K + BK - 1) / BK) * BK);
   }
-  double padded = 0;
-  for (int sh = 0; sh < kShapes; ++sh) {
-    first[sh] = static_cast<int>(sorted.size());
+  for (int sh = 0; sh < kShapes; ++sh) first[sh + 1] += first[sh];
+  std::vector<GemmDesc> sorted(descs.size());
+  {
+    int at[kShapes];
+    for (int sh = 0; sh < kShapes; ++sh) at[sh] = first[sh];
     for (const auto& d0 : descs) {
-      if (shape_of(d0) != sh) continue;
-      GemmDesc d = d0;
+      const int sh = shape_of(d0);
+      GemmDesc& d = sorted[at[sh]++];
+      d = d0;
       d.tile_begin = tiles[sh];
       tiles[sh] += d.tiles_m * d.tiles_n;
-      padded += 8.0 * d.tiles_m * d.bm * d.tiles_n * d.bn * (((d.K + BK - 1) / BK) * BK);
-      sorted.push_back(d);
     }
-    map_off[sh + 1] = map_off[sh] + tiles[sh];
   }
-  first[kShapes] = static_cast<int>(sorted.size());
+  for (int sh = 0; sh < kShapes; ++sh) map_off[sh + 1] = map_off[sh] + tiles[sh];
   total_tiles = map_off[kShapes];
   d_descs.upload(sorted, ctx->stream);
   {
@@ -639,14 +641,16 @@ void GemmBatch::run(Context* ctx) {
 
 void CopyBatch::add(const CopyOp& o0) {
   if (o0.rows <= 0 || o0.cols <= 0) return;
-  CopyOp o = o0;
-  o.tile_begin = total_tiles;
-  total_tiles += (o.cols + 7) / 8;
-  ops.push_back(o);
+  ops.push_back(o0);
 }
 
 void CopyBatch::run(Context* ctx) {
   if (ops.empty()) return;
+  total_tiles = 0;
+  for (auto& o : ops) {
+    o.tile_begin = total_tiles;
+    total_tiles += (o.cols + 7) / 8;
+  }
   d_ops.upload(ops, ctx->stream);
   {
     std::vector<int> map(total_tiles);
