@@ -651,7 +651,7 @@ bool element_v5_build(Context* ctx, const ElemArgs& a0, int nwork) {
   const size_t per = sizeof(double) * (sA + sB + sL) + sizeof(double2) * (sS + nb);
   size_t free_b = 0, total_b = 0;
   HPSB_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const size_t budget = std::min<size_t>(size_t(6) << 30, free_b / 4);
+  const size_t budget = std::min<size_t>(size_t(24) << 30, free_b / 4);
   const int cap = static_cast<int>(std::max<size_t>(1, std::min<size_t>(nwork, budget / per)));
   const int nchunks = (nwork + cap - 1) / cap;
   const int chunk = (nwork + nchunks - 1) / nchunks;  // even chunks

@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of sed-made source variants on the cfg3 bench (setup kernels): usage in-file.
+# A/B of sed-made source variants on the cfg3 bench (setup kernels); edit the variant lines per experiment.
 cd "$GRAFT_REPO_ROOT"
 b() { timeout 900 python bench.py --steps 4 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); k=d['kernels']
@@ -9,6 +9,6 @@ variant() {  # $1 name, $2 file, $3 sed
     sed -i "$3" csrc/$2 && make -s -j 2>&1 | grep -i " error"; cd /tmp/vb; b $1; cd "$GRAFT_REPO_ROOT"
 }
 b base
-variant thr97 zgemm.cu 's/pn \* 100 < pb \* 92/pn * 100 < pb * 97/'
-variant thr85 zgemm.cu 's/pn \* 100 < pb \* 92/pn * 100 < pb * 85/'
-variant thr100 zgemm.cu 's/pn \* 100 < pb \* 92/pn * 100 < pb * 100/'
+
+
+variant njb3 element_v5.cu 's/nbc <= 80 ? std::max(2, (nbc + 15) \/ 16) : 4/nbc <= 80 ? 3 : 4/'
