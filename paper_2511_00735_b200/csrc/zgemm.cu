@@ -813,7 +813,7 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
         HPSB_LAUNCHED(ctx);
       }
       InverseBatch piv;
-      GemmBatch gu, gr, gq;
+      GemmBatch gu, gr;
       CopyBatch back;
       for (const auto& o : large) {
         if (k0 >= o.n) continue;
@@ -836,8 +836,8 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
             gr.add(A + r0 + k0 * ld, o.lda, Ub + static_cast<size_t>(c0) * kw, kw,
                    A + r0 + c0 * ld, o.lda, rn, cn, kw, -1.0, 1.0);
           }
-          // Q = -A_RK P
-          gq.add(A + r0 + k0 * ld, o.lda, AKK, o.lda, Qb + r0, n, rn, kw, kw, -1.0, 0.0);
+          // Q = -A_RK P (needs only P: same launch as U; both are a few dozen tiles)
+          gu.add(A + r0 + k0 * ld, o.lda, AKK, o.lda, Qb + r0, n, rn, kw, kw, -1.0, 0.0);
           back.copy(Qb + r0, n, A + r0 + k0 * ld, o.lda, rn, kw, 1.0);
         }
         back.copy(Ub, kw, A + k0, o.lda, kw, k0, 1.0);
@@ -847,7 +847,6 @@ void InverseBatch::run(Context* ctx, int* status_dev) {
       piv.run(ctx, status_dev);  // in place: A_KK <- P (kw <= 32 uses the smem kernel)
       gu.run(ctx);
       gr.run(ctx);
-      gq.run(ctx);
       back.run(ctx);
     }
     if (diag) {  // no pivots, nothing to unscramble; check the inverse's growth

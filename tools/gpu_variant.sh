@@ -11,4 +11,4 @@ variant() {  # $1 name, $2 file, $3 sed
 b base
 
 
-variant njb3 element_v5.cu 's/nbc <= 80 ? std::max(2, (nbc + 15) \/ 16) : 4/nbc <= 80 ? 3 : 4/'
+
