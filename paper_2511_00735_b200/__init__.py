@@ -301,7 +301,8 @@ class Context:
         return out
 
     def close(self):
-        if getattr(self, "_h", None):
+        # at interpreter shutdown the module globals may already be cleared
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.hpsb_context_destroy(self._h)
             self._h = None
 
