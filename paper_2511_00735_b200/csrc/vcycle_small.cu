@@ -134,10 +134,24 @@ __global__ void __launch_bounds__(kThreads) merge_small_kernel(const SmallMerge*
 
 // Multi-RHS variant: the same fused chain for R right-hand sides (vectors
 // with RHS stride ld); every GEMV becomes a small GEMM on shared memory,
-// one (row, rhs) output per thread pass.  Block-wide.
+// Y (rows x R) = A (rows x K, ld lda) X (K x R, ld ldx), on the FP64 tensor
+// cores: a warp owns 8-row x 16-column output tiles (two 8 x 8 fragments,
+// complex = four real DMMAs each), k in steps of 4 straight from shared
+// memory; rows, K and R are masked to the problem (merge sizes are multiples
+// of N - 1).  The scalar version (one output per thread pass, two 16-byte
+// shared-memory loads per complex FMA) stays for separators below 16 nodes,
+// where the 8 x 16 tiles are mostly padding (cfg4 level 1, s = 11: 1.79 ms
+// scalar, 2.24 ms DMMA; levels 2-3, s = 22: 5.06 -> 4.43 ms).  These levels
+// remain bound by the per-merge latency chain at one or two CTAs per SM, not
+// by the arithmetic.
+__device__ __forceinline__ void sdmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 template <class F>
-__device__ __forceinline__ void smem_gemm_r(const double2* A, int lda, int rows, int K,
-                                            const double2* X, int ldx, int R, F&& emit) {
+__device__ __forceinline__ void smem_gemm_scalar(const double2* A, int lda, int rows, int K,
+                                                 const double2* X, int ldx, int R, F&& emit) {
   for (int idx = threadIdx.x; idx < rows * R; idx += kThreads) {
     const int r = idx % rows, b = idx / rows;
     double2 acc = make_double2(0.0, 0.0);
@@ -145,7 +159,52 @@ __device__ __forceinline__ void smem_gemm_r(const double2* A, int lda, int rows,
     emit(r, b, acc);
   }
 }
+template <class F>
+__device__ __forceinline__ void smem_gemm_dmma(const double2* A, int lda, int rows, int K,
+                                               const double2* X, int ldx, int R, F&& emit) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  const int nrt = (rows + 7) >> 3, nct = (R + 15) >> 4;
+  const double2 zero = make_double2(0.0, 0.0);
+  for (int unit = warp; unit < nrt * nct; unit += kThreads / 32) {
+    const int rt = unit % nrt, ct = unit / nrt;
+    const int row = 8 * rt + g, col0 = 16 * ct + g;
+    double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int k = k0 + t4;
+      const bool kin = k < K;
+      const double2 a = (kin && row < rows) ? A[row + k * lda] : zero;
+      double2 b[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) b[j] = (kin && col0 + 8 * j < R) ? X[k + (col0 + 8 * j) * ldx] : zero;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        sdmma(cr[j][0], cr[j][1], a.x, b[j].x);
+        sdmma(ci[j][0], ci[j][1], a.x, b[j].y);
+        sdmma(cr[j][0], cr[j][1], -a.y, b[j].y);
+        sdmma(ci[j][0], ci[j][1], a.y, b[j].x);
+      }
+    }
+    // fragment (g, t4) holds C[8 rt + g][16 ct + 8 j + 2 t4 + h]
+    if (row < rows) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 16 * ct + 8 * j + 2 * t4 + h;
+          if (col < R) emit(row, col, make_double2(cr[j][h], ci[j][h]));
+        }
+    }
+  }
+}
 
+template <bool DMMA, class F>
+__device__ __forceinline__ void smem_gemm_r(const double2* A, int lda, int rows, int K,
+                                            const double2* X, int ldx, int R, F&& emit) {
+  if (DMMA) smem_gemm_dmma(A, lda, rows, K, X, ldx, R, emit);
+  else smem_gemm_scalar(A, lda, rows, K, X, ldx, R, emit);
+}
+
+template <bool DMMA>
 __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
     const SmallMerge* __restrict__ ms, int down, double2* r, double2* out, int R, int64_t ld) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -192,29 +251,29 @@ __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
   if (down) {
     const double2 *T1ps = A1, *T1ss = A1 + p1, *T2ps = A2, *T2ss = A2 + p2;
     // t = v1 - T2_ss v2
-    smem_gemm_r(T2ss, P2, s, s, v2, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(T2ss, P2, s, s, v2, s, R, [&](int i, int b, double2 y) {
       t[i + b * s] = csub(v1[i + b * s], y);
     });
     __syncthreads();
     // x1 = W t
-    smem_gemm_r(Ws, s, s, s, t, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(Ws, s, s, s, t, s, R, [&](int i, int b, double2 y) {
       w1[i + b * s] = y;
       __stcg(out + b * ld + M.in1s[i], y);
     });
     __syncthreads();
     // x2 = v2 - T1_ss x1  (into t)
-    smem_gemm_r(T1ss, P1, s, s, w1, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(T1ss, P1, s, s, w1, s, R, [&](int i, int b, double2 y) {
       const double2 x2 = csub(v2[i + b * s], y);
       t[i + b * s] = x2;
       __stcg(out + b * ld + M.in2s[i], x2);
     });
     // r[out1_p] -= T1_ps x1 (independent of the x2 rows above)
-    smem_gemm_r(T1ps, P1, p1, s, w1, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(T1ps, P1, p1, s, w1, s, R, [&](int i, int b, double2 y) {
       double2* q = r + b * ld + M.out1p[i];
       __stcg(q, csub(__ldcg(q), y));
     });
     __syncthreads();
-    smem_gemm_r(T2ps, P2, p2, s, t, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(T2ps, P2, p2, s, t, s, R, [&](int i, int b, double2 y) {
       double2* q = r + b * ld + M.out2p[i];
       __stcg(q, csub(__ldcg(q), y));
     });
@@ -222,19 +281,19 @@ __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
     const double2 *T1sp = A1, *T1ss = A1 + static_cast<size_t>(p1) * s, *T2sp = A2,
                   *T2ss = A2 + static_cast<size_t>(p2) * s;
     // b1 = T2_sp u2 (v1), b2 = T1_sp u1 (v2)
-    smem_gemm_r(T2sp, s, s, p2, u2, p2, R, [&](int i, int b, double2 y) { v1[i + b * s] = y; });
-    smem_gemm_r(T1sp, s, s, p1, u1, p1, R, [&](int i, int b, double2 y) { v2[i + b * s] = y; });
+    smem_gemm_r<DMMA>(T2sp, s, s, p2, u2, p2, R, [&](int i, int b, double2 y) { v1[i + b * s] = y; });
+    smem_gemm_r<DMMA>(T1sp, s, s, p1, u1, p1, R, [&](int i, int b, double2 y) { v2[i + b * s] = y; });
     __syncthreads();
     // t = b1 - T2_ss b2
-    smem_gemm_r(T2ss, s, s, s, v2, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(T2ss, s, s, s, v2, s, R, [&](int i, int b, double2 y) {
       t[i + b * s] = csub(v1[i + b * s], y);
     });
     __syncthreads();
     // y1 = W t
-    smem_gemm_r(Ws, s, s, s, t, s, R, [&](int i, int b, double2 y) { w1[i + b * s] = y; });
+    smem_gemm_r<DMMA>(Ws, s, s, s, t, s, R, [&](int i, int b, double2 y) { w1[i + b * s] = y; });
     __syncthreads();
     // out[s2] += T1_ss y1 - b2,  out[s1] -= y1
-    smem_gemm_r(T1ss, s, s, s, w1, s, R, [&](int i, int b, double2 y) {
+    smem_gemm_r<DMMA>(T1ss, s, s, s, w1, s, R, [&](int i, int b, double2 y) {
       double2* q2 = out + b * ld + M.in2s[i];
       __stcg(q2, cadd(__ldcg(q2), csub(y, v2[i + b * s])));
       double2* q1 = out + b * ld + M.in1s[i];
@@ -252,11 +311,16 @@ size_t small_merge_batch_smem(int s, int p1, int p2, int R) {
 void SmallLevel::run_batch(Context* ctx, bool down, double2* r, double2* out, int R, int64_t ld) const {
   if (!count) return;
   const size_t smem = batch_smem(R);
-  allow_smem<merge_small_batch_kernel>(smem);
+  allow_smem<merge_small_batch_kernel<false>>(smem);
+  allow_smem<merge_small_batch_kernel<true>>(smem);
   KernelScope ks(ctx, label.empty() ? (down ? "vcycle_down_batch" : "vcycle_up_batch") : label.c_str(),
                  down ? bytes_down : bytes_up, 0.0);
-  launch_k(ctx, merge_small_batch_kernel, dim3(count), dim3(kThreads), smem, 1,
-           static_cast<const SmallMerge*>(d.p), down ? 1 : 0, r, out, R, ld);
+  if (max_s >= 16)
+    launch_k(ctx, merge_small_batch_kernel<true>, dim3(count), dim3(kThreads), smem, 1,
+             static_cast<const SmallMerge*>(d.p), down ? 1 : 0, r, out, R, ld);
+  else
+    launch_k(ctx, merge_small_batch_kernel<false>, dim3(count), dim3(kThreads), smem, 1,
+             static_cast<const SmallMerge*>(d.p), down ? 1 : 0, r, out, R, ld);
 }
 
 

@@ -19,6 +19,7 @@ size_t small_merge_smem(int s, int p1, int p2);
 size_t small_merge_batch_smem(int s, int p1, int p2, int R);
 struct SmallLevel {
   int level = 0, count = 0;
+  int max_s = 0;  // largest separator of the level (multi-RHS: DMMA tiles from 16 nodes up)
   size_t smem = 0;
   size_t batch_ops = 0, batch_vec = 0;  // multi-RHS smem: operators + per-RHS vectors
   size_t batch_smem(int R) const { return batch_ops + static_cast<size_t>(R) * batch_vec; }
