@@ -992,6 +992,8 @@ Precond* create_precond(Hierarchy* h, const hpsb_mg_config& cfg) {
       if (need > kSmallMergeSmemMax) return -1;
       sl->smem = std::max(sl->smem, need);
       sl->max_s = std::max(sl->max_s, mr.s);
+      sl->batch_vec_down = std::max(sl->batch_vec_down, small_merge_batch_vec(mr.s, mr.p1, mr.p2, true));
+      sl->batch_vec_up = std::max(sl->batch_vec_up, small_merge_batch_vec(mr.s, mr.p1, mr.p2, false));
       sl->batch_ops = std::max(sl->batch_ops, small_merge_batch_smem(mr.s, mr.p1, mr.p2, 0));
       sl->batch_vec = std::max(sl->batch_vec, small_merge_batch_smem(mr.s, mr.p1, mr.p2, 1) -
                                                   small_merge_batch_smem(mr.s, mr.p1, mr.p2, 0));

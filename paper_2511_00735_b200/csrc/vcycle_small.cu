@@ -213,12 +213,15 @@ __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
   double2* A1 = reinterpret_cast<double2*>(smem_raw);
   double2* A2 = A1 + static_cast<size_t>(P1) * s;
   double2* Ws = A2 + static_cast<size_t>(P2) * s;
-  double2* v1 = Ws + static_cast<size_t>(s) * s;  // s x R each
+  // Vectors (s x R each): down v1 v2 t w1; up v1 v2 and ONE perimeter buffer
+  // ub (max(p1, p2, 2 s) x R) that holds u2, then u1, then t and w1 (u1 is
+  // dead once b2 is formed).  Sized per direction, so the level fits two CTAs
+  // per SM where the single layout fitted one (cfg4 level 3: 126 -> 92 / 98 KB).
+  double2* v1 = Ws + static_cast<size_t>(s) * s;
   double2* v2 = v1 + static_cast<size_t>(s) * R;
-  double2* t = v2 + static_cast<size_t>(s) * R;
+  double2* ub = v2 + static_cast<size_t>(s) * R;
+  double2* t = ub;
   double2* w1 = t + static_cast<size_t>(s) * R;
-  double2* u1 = w1 + static_cast<size_t>(s) * R;  // p1 x R
-  double2* u2 = u1 + static_cast<size_t>(p1) * R;  // p2 x R
   pdl_trigger();
   if (down) {
     const double2* g1 = M.T1 + static_cast<size_t>(p1) * P1;
@@ -241,10 +244,8 @@ __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
       v2[k] = __ldcg(r + b * ld + M.in2s[i]);
     }
   } else {
-    for (int k = tid; k < p1 * R; k += kThreads)
-      u1[k] = __ldcg(out + (k / p1) * ld + M.in1p[k % p1]);
     for (int k = tid; k < p2 * R; k += kThreads)
-      u2[k] = __ldcg(out + (k / p2) * ld + M.in2p[k % p2]);
+      ub[k] = __ldcg(out + (k / p2) * ld + M.in2p[k % p2]);
   }
   cp_async_wait_all();
   __syncthreads();
@@ -280,9 +281,13 @@ __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
   } else {
     const double2 *T1sp = A1, *T1ss = A1 + static_cast<size_t>(p1) * s, *T2sp = A2,
                   *T2ss = A2 + static_cast<size_t>(p2) * s;
-    // b1 = T2_sp u2 (v1), b2 = T1_sp u1 (v2)
-    smem_gemm_r<DMMA>(T2sp, s, s, p2, u2, p2, R, [&](int i, int b, double2 y) { v1[i + b * s] = y; });
-    smem_gemm_r<DMMA>(T1sp, s, s, p1, u1, p1, R, [&](int i, int b, double2 y) { v2[i + b * s] = y; });
+    // b1 = T2_sp u2 (v1), then b2 = T1_sp u1 (v2), through the one buffer
+    smem_gemm_r<DMMA>(T2sp, s, s, p2, ub, p2, R, [&](int i, int b, double2 y) { v1[i + b * s] = y; });
+    __syncthreads();
+    for (int k = tid; k < p1 * R; k += kThreads)
+      ub[k] = __ldcg(out + (k / p1) * ld + M.in1p[k % p1]);
+    __syncthreads();
+    smem_gemm_r<DMMA>(T1sp, s, s, p1, ub, p1, R, [&](int i, int b, double2 y) { v2[i + b * s] = y; });
     __syncthreads();
     // t = b1 - T2_ss b2
     smem_gemm_r<DMMA>(T2ss, s, s, s, v2, s, R, [&](int i, int b, double2 y) {
@@ -303,14 +308,21 @@ __global__ void __launch_bounds__(kThreads) merge_small_batch_kernel(
 }
 }  // namespace
 
-size_t small_merge_batch_smem(int s, int p1, int p2, int R) {
+// vector entries per right-hand side of one direction (see the kernel's layout)
+size_t small_merge_batch_vec(int s, int p1, int p2, bool down) {
+  return down ? 4 * static_cast<size_t>(s)
+              : 2 * static_cast<size_t>(s) + std::max<size_t>(std::max(p1, p2), 2 * static_cast<size_t>(s));
+}
+size_t small_merge_batch_smem(int s, int p1, int p2, int R) {  // the larger direction
   const size_t P1 = p1 + s, P2 = p2 + s;
-  return sizeof(double2) * ((P1 + P2 + s) * s + static_cast<size_t>(R) * (4 * s + p1 + p2));
+  return sizeof(double2) * ((P1 + P2 + s) * s +
+                            static_cast<size_t>(R) * std::max(small_merge_batch_vec(s, p1, p2, true),
+                                                              small_merge_batch_vec(s, p1, p2, false)));
 }
 
 void SmallLevel::run_batch(Context* ctx, bool down, double2* r, double2* out, int R, int64_t ld) const {
   if (!count) return;
-  const size_t smem = batch_smem(R);
+  const size_t smem = batch_ops + sizeof(double2) * R * (down ? batch_vec_down : batch_vec_up);
   allow_smem<merge_small_batch_kernel<false>>(smem);
   allow_smem<merge_small_batch_kernel<true>>(smem);
   KernelScope ks(ctx, label.empty() ? (down ? "vcycle_down_batch" : "vcycle_up_batch") : label.c_str(),

@@ -17,11 +17,13 @@ struct SmallMerge {
 size_t small_merge_smem(int s, int p1, int p2);
 
 size_t small_merge_batch_smem(int s, int p1, int p2, int R);
+size_t small_merge_batch_vec(int s, int p1, int p2, bool down);  // vector entries per RHS and direction
 struct SmallLevel {
   int level = 0, count = 0;
   int max_s = 0;  // largest separator of the level (multi-RHS: DMMA tiles from 16 nodes up)
   size_t smem = 0;
-  size_t batch_ops = 0, batch_vec = 0;  // multi-RHS smem: operators + per-RHS vectors
+  size_t batch_ops = 0, batch_vec = 0;  // multi-RHS smem: operators + per-RHS vectors (larger direction)
+  size_t batch_vec_down = 0, batch_vec_up = 0;  // vector entries per RHS of each direction
   size_t batch_smem(int R) const { return batch_ops + static_cast<size_t>(R) * batch_vec; }
   double bytes_down = 0, bytes_up = 0;
   std::string label;
