@@ -374,9 +374,16 @@ def run_b200(args, rank, world, local):
     ctx.profile(False)
     prof = ctx.profile_entries()
     peaks = measured_peaks()
-    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    # dominant kernel: the multi-RHS V-cycle runs the same kernels under two
+    # direction labels (vcycle_up_batch / vcycle_down_batch): one entry
+    fam = dict(prof)
+    ub, db = fam.pop("vcycle_up_batch", None), fam.pop("vcycle_down_batch", None)
+    if ub or db:
+        parts = [x for x in (ub, db) if x]
+        fam["vcycle_batch"] = {k: sum(x[k] for x in parts) for k in ("launches", "ms", "bytes", "flops")}
+    dom = max(fam.items(), key=lambda kv: kv[1]["ms"])
     name, d = dom
-    if d["flops"] > 0 and d["bytes"] == 0 or name in ("element_iti", "zgemm_dmma"):
+    if d["flops"] > 0 and d["bytes"] == 0 or name in ("element_iti", "zgemm_dmma", "vcycle_batch"):  # multi-RHS apply: FP64 bound
         achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12
         roof = {"kernel": name, "bound": "tensor", "achieved": achieved,
                 "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s (fp64)",
