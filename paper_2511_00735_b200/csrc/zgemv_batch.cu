@@ -1,8 +1,11 @@
 // Multi-RHS GEMM for the per-iteration operators (see zgemv_batch.hpp).
 //
 // Tile: 64 rows x 32 right-hand sides per 256-thread CTA (8 warps as 4 x 2,
-// 16 x 16 complex outputs per warp), K-steps of 16 through a 3-stage cp.async
-// pipeline.  The B tile gathers its K rows through the item's index map
+// 16 x 16 complex outputs per warp), or 64 x 16 (8 x 1 warps of 8 x 16);
+// phases with too few 64-row tiles to fill the SMs (the top levels and the
+// coarse matvec: cfg4's coarse matvec ran 88 CTAs) use 32-row tiles on 128
+// threads.  K-steps of 16 through a 2-stage cp.async pipeline (3 stages
+// measured slower: 15.8 vs 15.5 ms per cfg4 apply; more CTAs per SM win).  The B tile gathers its K rows through the item's index map
 // (cp.async with zero-fill for -1 / out-of-range entries), the epilogue
 // scatters C rows through theirs.  A complex product is four real DMMAs
 // (mma.sync.m8n8k4.f64) on de-interleaved fragments, as in zgemm.cu.
@@ -14,14 +17,17 @@
 namespace hpsb {
 
 namespace {
-constexpr int BM = 64, BK = 16, STAGES = 3, THREADS = 256;
-constexpr int SA = BM + 2;  // complex stride of an A k-row in smem
+constexpr int BK = 16, STAGES = 2;
 constexpr int SB = BK + 4;  // complex stride of a B column in smem
-constexpr int A_STAGE = BK * SA;
-template <int BN>
-constexpr size_t bsmem() {
-  return sizeof(double2) * STAGES * (A_STAGE + BN * SB);
-}
+template <int BN, int BM>
+struct BTile {
+  static constexpr int WN = BN / 16, I = BN / 16;       // warp columns; 8-row fragments per warp
+  static constexpr int WM = BM / (8 * I);               // warp rows
+  static constexpr int THREADS = 32 * WM * WN;          // 256 (BM = 64) or 128 (BM = 32)
+  static constexpr int SA = BM + 2;                     // complex stride of an A k-row in smem
+  static constexpr int A_STAGE = BK * SA, B_STAGE = BN * SB;
+  static constexpr size_t kSmem = sizeof(double2) * STAGES * (A_STAGE + B_STAGE);
+};
 
 __device__ __forceinline__ void cpa16(void* smem, const void* gmem, bool valid) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -38,13 +44,14 @@ __device__ __forceinline__ const double2* bind_ptr(const double2* p, const BBind
   return !p ? p : p == b.from[0] ? b.to[0] : p == b.from[1] ? b.to[1] : p;
 }
 
-// BN = 32 (R > 16): 4 x 2 warps of 16 x 16 outputs; BN = 16: 8 x 1 warps of 8 x 16.
-template <int BN>
-__global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __restrict__ descs,
-                                                              const int* __restrict__ tile_map,
-                                                              int R, BBind bind) {
-  constexpr int WN = BN / 16, WM = 8 / WN, I = BM / (8 * WM);
-  constexpr int B_STAGE = BN * SB;
+// BN = 32 (R > 16): WM x 2 warps of 16 x 16 outputs; BN = 16: WM x 1 warps of 8 x 16.
+template <int BN, int BM>
+__global__ void __launch_bounds__(BTile<BN, BM>::THREADS) zgemv_batch_kernel(const BDesc* __restrict__ descs,
+                                                                              const int* __restrict__ tile_map,
+                                                                              int R, BBind bind) {
+  using TS = BTile<BN, BM>;
+  constexpr int WM = TS::WM, I = TS::I, THREADS = TS::THREADS, SA = TS::SA;
+  constexpr int A_STAGE = TS::A_STAGE, B_STAGE = TS::B_STAGE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
   double2* Bs = As + STAGES * A_STAGE;
@@ -168,18 +175,24 @@ __global__ void __launch_bounds__(THREADS) zgemv_batch_kernel(const BDesc* __res
 
 void BPhase::add(const BDesc& x0) {
   if (x0.M <= 0) return;
-  BDesc x = x0;
-  x.tiles_m = (x.M + BM - 1) / BM;
-  x.tile_begin = total_tiles;
-  total_tiles += x.tiles_m;
-  if (x.A) {
-    flops += 8.0 * x.M * x.K;  // per right-hand side
-    bytes += 16.0 * x.M * x.K;
+  if (x0.A) {
+    flops += 8.0 * x0.M * x0.K;  // per right-hand side
+    bytes += 16.0 * x0.M * x0.K;
   }
-  descs.push_back(x);
+  descs.push_back(x0);
 }
 
 void BPhase::finalize(cudaStream_t s) {
+  // 32-row tiles when 64-row tiles would leave SMs without a CTA
+  int tiles64 = 0;
+  for (const BDesc& x : descs) tiles64 += (x.M + 63) / 64;
+  bm = tiles64 < 2 * 148 ? 32 : 64;
+  total_tiles = 0;
+  for (BDesc& x : descs) {
+    x.tiles_m = (x.M + bm - 1) / bm;
+    x.tile_begin = total_tiles;
+    total_tiles += x.tiles_m;
+  }
   d.upload(descs, s);
   std::vector<int> map(total_tiles);
   for (size_t i = 0; i < descs.size(); ++i) {
@@ -189,18 +202,27 @@ void BPhase::finalize(cudaStream_t s) {
   d_map.upload(map, s);
 }
 
+namespace {
+template <int BN, int BM>
+void launch_batch(Context* ctx, int tiles, const BDesc* descs, const int* map, int R, const BBind& bind) {
+  using TS = BTile<BN, BM>;
+  allow_smem<zgemv_batch_kernel<BN, BM>>(TS::kSmem);
+  launch_k(ctx, zgemv_batch_kernel<BN, BM>, dim3(tiles), dim3(TS::THREADS), TS::kSmem, 1, descs, map, R, bind);
+}
+}  // namespace
+
 void BPhase::run(Context* ctx, int R, const char* label, BBind bind) const {
   if (descs.empty()) return;
   if (R < 1 || R > kBatchMaxRhs) throw InvalidArgument("batch: 1 <= nrhs <= 32");
   KernelScope ks(ctx, this->label.empty() ? label : this->label.c_str(), bytes, flops * R);
+  const BDesc* dp = d.p;
+  const int* mp = d_map.p;
   if (R <= 16) {
-    allow_smem<zgemv_batch_kernel<16>>(bsmem<16>());
-    launch_k(ctx, zgemv_batch_kernel<16>, dim3(total_tiles), dim3(THREADS), bsmem<16>(), 1,
-             static_cast<const BDesc*>(d.p), static_cast<const int*>(d_map.p), R, bind);
+    if (bm == 32) launch_batch<16, 32>(ctx, total_tiles, dp, mp, R, bind);
+    else launch_batch<16, 64>(ctx, total_tiles, dp, mp, R, bind);
   } else {
-    allow_smem<zgemv_batch_kernel<32>>(bsmem<32>());
-    launch_k(ctx, zgemv_batch_kernel<32>, dim3(total_tiles), dim3(THREADS), bsmem<32>(), 1,
-             static_cast<const BDesc*>(d.p), static_cast<const int*>(d_map.p), R, bind);
+    if (bm == 32) launch_batch<32, 32>(ctx, total_tiles, dp, mp, R, bind);
+    else launch_batch<32, 64>(ctx, total_tiles, dp, mp, R, bind);
   }
 }
 

@@ -39,6 +39,7 @@ struct BBind {
 struct BPhase {
   std::vector<BDesc> descs;
   int total_tiles = 0;
+  int bm = 64;  // tile rows, chosen in finalize(): 32 when 64-row tiles would not fill the SMs
   double flops = 0, bytes = 0;
   std::string label;  // profiling name (overrides run()'s)
   DevBuf<BDesc> d;
