@@ -17,13 +17,16 @@
 namespace hpsb {
 
 namespace {
-constexpr int BK = 16, STAGES = 2;
+constexpr int BK = 16;
 constexpr int SB = BK + 4;  // complex stride of a B column in smem
 template <int BN, int BM>
 struct BTile {
   static constexpr int WN = BN / 16, I = BN / 16;       // warp columns; 8-row fragments per warp
   static constexpr int WM = BM / (8 * I);               // warp rows
   static constexpr int THREADS = 32 * WM * WN;          // 256 (BM = 64) or 128 (BM = 32)
+  // 64-row tiles: 2 stages (occupancy); 32-row tiles run the phases with few,
+  // long tiles (K up to 2816 at one CTA per SM): 4 stages keep more bytes in flight
+  static constexpr int STAGES = BM == 32 ? 4 : 2;
   static constexpr int SA = BM + 2;                     // complex stride of an A k-row in smem
   static constexpr int A_STAGE = BK * SA, B_STAGE = BN * SB;
   static constexpr size_t kSmem = sizeof(double2) * STAGES * (A_STAGE + B_STAGE);
@@ -50,7 +53,7 @@ __global__ void __launch_bounds__(BTile<BN, BM>::THREADS) zgemv_batch_kernel(con
                                                                               const int* __restrict__ tile_map,
                                                                               int R, BBind bind) {
   using TS = BTile<BN, BM>;
-  constexpr int WM = TS::WM, I = TS::I, THREADS = TS::THREADS, SA = TS::SA;
+  constexpr int WM = TS::WM, I = TS::I, THREADS = TS::THREADS, SA = TS::SA, STAGES = TS::STAGES;
   constexpr int A_STAGE = TS::A_STAGE, B_STAGE = TS::B_STAGE;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* As = reinterpret_cast<double2*>(smem_raw);
@@ -78,16 +81,27 @@ __global__ void __launch_bounds__(BTile<BN, BM>::THREADS) zgemv_batch_kernel(con
       cpa16(as + k * SA + m, src, ok);
     }
   };
-  auto load_b = [&](int kt, int st) {
+  // B rows are gathered through bidx.  The index of a stage is loaded one
+  // k-step ahead (rows_of) and kept in registers: loaded inside load_b, every
+  // k-step stalled on an L2 round trip before its copies could be issued
+  // (2 us per step at one CTA per SM: cfg4's coarse matvec ran at 0.7 TB/s).
+  constexpr int NB = (BN * BK) / THREADS;
+  auto rows_of = [&](int kt, int (&rows)[NB]) {
     const int k0 = kt * BK;
+#pragma unroll
+    for (int r = 0; r < NB; ++r) {
+      const int k = (tid + r * THREADS) % BK;
+      rows[r] = k0 + k < d.K ? (d.bidx ? __ldg(d.bidx + k0 + k) : k0 + k) : -1;
+    }
+  };
+  auto load_b = [&](int st, const int (&rows)[NB]) {
     double2* bs = Bs + st * B_STAGE;
 #pragma unroll
-    for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+    for (int r = 0; r < NB; ++r) {
       const int idx = tid + r * THREADS;
       const int k = idx % BK, n = idx / BK;
-      int row = k0 + k < d.K ? (d.bidx ? __ldg(d.bidx + k0 + k) : k0 + k) : -1;
-      const bool ok = n < R && row >= 0;
-      const double2* src = ok ? d.B + (size_t)row + (size_t)n * d.ldb : d.B;
+      const bool ok = n < R && rows[r] >= 0;
+      const double2* src = ok ? d.B + (size_t)rows[r] + (size_t)n * d.ldb : d.B;
       cpa16(bs + n * SB + k, src, ok);
     }
   };
@@ -102,12 +116,17 @@ __global__ void __launch_bounds__(BTile<BN, BM>::THREADS) zgemv_batch_kernel(con
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s)
     if (s < ktiles) load_a(s, s);
+  int brow[NB];
   pdl_wait();
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_b(s, s);
+    if (s < ktiles) {
+      rows_of(s, brow);
+      load_b(s, brow);
+    }
     asm volatile("cp.async.commit_group;\n" ::);
   }
+  if (STAGES - 1 < ktiles) rows_of(STAGES - 1, brow);
   const int arow = wm * (8 * I) + (lane >> 2), kq = lane & 3;
   const int bcol = wn * 16 + (lane >> 2);
   for (int kt = 0; kt < ktiles; ++kt) {
@@ -115,9 +134,10 @@ __global__ void __launch_bounds__(BTile<BN, BM>::THREADS) zgemv_batch_kernel(con
     __syncthreads();
     if (kt + STAGES - 1 < ktiles) {
       load_a(kt + STAGES - 1, (kt + STAGES - 1) % STAGES);
-      load_b(kt + STAGES - 1, (kt + STAGES - 1) % STAGES);
+      load_b((kt + STAGES - 1) % STAGES, brow);
     }
     asm volatile("cp.async.commit_group;\n" ::);
+    if (kt + STAGES < ktiles) rows_of(kt + STAGES, brow);  // next step's rows: the load overlaps the DMMAs below
     const double2* as = As + (kt % STAGES) * A_STAGE;
     const double2* bs = Bs + (kt % STAGES) * B_STAGE;
 #pragma unroll
