@@ -225,26 +225,36 @@ __global__ void __launch_bounds__(THREADS, 2) zgemm_grouped_kernel(const GemmDes
   }
 }
 
-// Sub-matrix copy / gather ops, tiled 8 columns per CTA.
+// Sub-matrix copy / gather ops, tiled 8 columns per CTA.  A thread owns rows
+// and walks the tile's 8 columns with all 8 loads in flight before the first
+// store (row index loaded once): per-column loops with one dependent load per
+// iteration ran the gathers at 4.3 TB/s.
 __global__ void copy_ops_kernel(const CopyOp* __restrict__ ops, const int* __restrict__ tile_map) {
   const int tile = blockIdx.x;
   const CopyOp op = ops[tile_map[tile]];
   const int c0 = (tile - op.tile_begin) * 8;
-  const int c1 = min(c0 + 8, op.cols);
-  for (int c = c0; c < c1; ++c) {
-    const int sc = op.cidx ? op.cidx[c] : c;
-    for (int r = threadIdx.x; r < op.rows; r += blockDim.x) {
-      double2 v;
-      if (op.mode == CopyOp::kIdentity) {
-        v = make_double2(r == c ? 1.0 : 0.0, 0.0);
-      } else if (op.mode == CopyOp::kZero) {
-        v = make_double2(0.0, 0.0);
-      } else {
-        const int sr = op.ridx ? op.ridx[r] : r;
-        v = cscale(op.src[(size_t)sr + (size_t)sc * op.lds], op.scale);
-      }
-      op.dst[(size_t)r + (size_t)c * op.ldd] = v;
-    }
+  const int nc = min(8, op.cols - c0);
+  if (op.mode != CopyOp::kCopy) {
+    for (int c = c0; c < c0 + nc; ++c)
+      for (int r = threadIdx.x; r < op.rows; r += blockDim.x)
+        op.dst[(size_t)r + (size_t)c * op.ldd] =
+            make_double2(op.mode == CopyOp::kIdentity && r == c ? 1.0 : 0.0, 0.0);
+    return;
+  }
+  size_t scol[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = c0 + min(j, nc - 1);
+    scol[j] = (size_t)(op.cidx ? op.cidx[c] : c) * op.lds;
+  }
+  for (int r = threadIdx.x; r < op.rows; r += blockDim.x) {
+    const double2* s = op.src + (op.ridx ? op.ridx[r] : r);
+    double2 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = s[scol[j]];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nc) op.dst[(size_t)r + (size_t)(c0 + j) * op.ldd] = cscale(v[j], op.scale);
   }
 }
 
